@@ -1,0 +1,164 @@
+/*
+ * gdwd_b200 -- C ABI of the B200-native sGS-ADMM hot path for generalized
+ * Distance Weighted Discrimination (arXiv 2305.12019).
+ *
+ * The reference (pkg/src/gdwd, pure Python on numpy/scipy) has no FFI; the
+ * entry points below are the seams a maintainer binds (ctypes stub in
+ * INTEGRATION.md) to replace its hot path.  Each declaration cites the
+ * reference interface it stands in for.
+ *
+ * Conventions
+ *   - plain pointers + sizes; host pointers are borrowed for the call only;
+ *     device memory is owned by the context.
+ *   - all arithmetic is fp64; Z~ is the scaled d x n data matrix of
+ *     ProblemData (reference solver.py:60-71), samples as columns.
+ *   - return value: GDWD_OK (0) or one of the GDWD_ERR_* codes; codes map 1:1
+ *     onto the reference's exceptions; gdwd_last_error() has the message.
+ *   - one context per host thread; a context is not re-entrant.
+ */
+#ifndef GDWD_B200_H
+#define GDWD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  GDWD_OK = 0,
+  GDWD_ERR_CUDA = 1,         /* RuntimeError (device / launch failure)                  */
+  GDWD_ERR_VALUE = 2,        /* ValueError (solver.py:73-87,118-124)                   */
+  GDWD_ERR_INDEFINITE = 3,   /* IndefiniteMatrixError (linalg/cholesky.py:12,47-48)     */
+  GDWD_ERR_SCHUR = 4,        /* DegenerateSchurError (subsolvers.py:38,249-252)        */
+  GDWD_ERR_LANCZOS = 5,      /* LanczosConvergenceError (linalg/lanczos.py:25-30)      */
+  GDWD_ERR_ASSERT = 6,       /* AssertionError: r left the positive orthant (solver.py:319-320) */
+  GDWD_ERR_UNSUPPORTED = 7,  /* feature not available on this path                     */
+  GDWD_ERR_ABORTED = 8       /* the per-iteration callback asked to stop               */
+};
+
+enum { GDWD_BACKEND_AUTO = 0, GDWD_BACKEND_DIRECT = 1, GDWD_BACKEND_SMW2 = 2, GDWD_BACKEND_ITERATIVE = 3 };
+
+typedef struct gdwd_ctx gdwd_ctx;
+
+/* SolverConfig (reference solver.py:101-124).  NaN in sigma0 / epsilon_c
+ * means "reference default" (solver.py:440-445). */
+typedef struct {
+  int32_t max_iter;
+  int32_t backend;            /* GDWD_BACKEND_* (Backend enum, solver.py:48-57) */
+  int32_t use_sgs;
+  int32_t psqmr_switch_steps;
+  int32_t ell;
+  int32_t seed;
+  int32_t use_graph;          /* capture the iteration body in a CUDA graph (DIRECT/SMW2) */
+  int32_t poll_every;         /* host polls the device stop flag every k iterations      */
+  double steplength;
+  double tol_feas;
+  double tol_cgap;
+  double tol_cap;
+  double sigma0;
+  double epsilon_c;
+  double mu;
+} gdwd_config;
+
+/* SolveResult scalars (reference solver.py:170-183). */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  int32_t backend;            /* resolved backend */
+  int32_t psqmr_total;
+  int32_t double_count;
+  int32_t status;
+  double beta;
+  double sigma;
+  double eps_c;
+  double setup_ms;            /* factorisation / preconditioner build, device time */
+  double loop_ms;             /* iteration loop, device time                        */
+  double resid[11];           /* KKTResiduals fields, reference order (solver.py:143-155) */
+} gdwd_result;
+
+/* callback(state, residuals) of sgs_admm_solve (solver.py:546-547): called on
+ * the host after each iteration with the 11 KKT values; the iterates can be
+ * fetched with gdwd_get_state from inside the callback.  Nonzero return
+ * aborts the solve (GDWD_ERR_ABORTED). */
+typedef int (*gdwd_iter_cb)(void* user, int32_t iter, const double* resid11, double sigma, double beta);
+
+/* context ------------------------------------------------------------------*/
+int gdwd_ctx_create(int32_t device, gdwd_ctx** out);
+void gdwd_ctx_destroy(gdwd_ctx* ctx);
+const char* gdwd_last_error(const gdwd_ctx* ctx);
+int gdwd_version(void);
+
+/* data ----------------------------------------------------------------------
+ * Dense Z~: the CSC values array of a fully stored d x n matrix, i.e. the
+ * row-major [n][d] sample matrix (SparseMatrixCSC, linalg/sparse.py:20-57). */
+int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n);
+/* Sparse Z~ in the reference's CSC layout (int64 colptr/rowidx). */
+int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx, const double* values,
+                    int64_t d, int64_t n);
+/* ProblemData vectors and scalars (solver.py:60-71); all length n. */
+int gdwd_set_problem(gdwd_ctx* ctx, const double* y, const double* e, const double* weights, double C,
+                     double q, double z_scale);
+
+/* operator seams ------------------------------------------------------------
+ * Z~ v  (scipy csc_matvec at solver.py:496,508,517,300; subsolvers.py:146) */
+int gdwd_matvec(gdwd_ctx* ctx, const double* v_n, double* out_d);
+/* Z~^T v (scipy csr_matvec at solver.py:501,530,322; subsolvers.py:140)   */
+int gdwd_matvec_t(gdwd_ctx* ctx, const double* v_d, double* out_n);
+
+/* the solver ----------------------------------------------------------------
+ * sgs_admm_solve (solver.py:392-602).  sigma_schedule (nullable, test hook):
+ * sigma of iteration k for 1 <= k < sched_len replaces update_sigma. */
+int gdwd_solve(gdwd_ctx* ctx, const gdwd_config* cfg, const double* sigma_schedule, int64_t sched_len,
+               gdwd_iter_cb cb, void* user, gdwd_result* out);
+/* The same solve in three calls, so a caller (the benchmark) can time an
+ * exact number of iterations on device-resident state: _begin does the setup
+ * (factorisation / preconditioner, initial iterates, CUDA-graph capture),
+ * _iterate runs up to `count` more iterations (fewer if the stopping rule
+ * fires), _end evaluates the last iteration's stop test and fills `out`. */
+int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const double* sigma_schedule, int64_t sched_len);
+int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb, void* user, int32_t* iters_done,
+                       int32_t* stopped);
+int gdwd_solve_end(gdwd_ctx* ctx, gdwd_result* out);
+/* Device time (ms, CUDA events on the solve's stream, synchronised on both
+ * sides) of `count` further iterations of the current solve. */
+int gdwd_time_iterations(gdwd_ctx* ctx, int32_t count, double* ms, int32_t* iters_done);
+/* Per-kernel profiling: with profiling on, iterations run without the CUDA
+ * graph and every launch is bracketed by events; gdwd_get_profile writes
+ * "tag launches total_ms" lines and the launch counter. */
+int gdwd_set_profile(gdwd_ctx* ctx, int32_t enable);
+int gdwd_get_profile(gdwd_ctx* ctx, char* buf, int64_t buflen, int64_t* launches);
+int gdwd_reset_counters(gdwd_ctx* ctx);
+/* End-of-iteration iterates (SolverState, solver.py:127-140); any pointer may
+ * be NULL.  n-vectors: r, xi, alpha, ztw; d-vectors: w, u, rho. */
+int gdwd_get_state(gdwd_ctx* ctx, double* r, double* xi, double* alpha, double* w, double* u, double* rho,
+                   double* ztw, double* beta);
+/* Per-iteration history rows of 16 doubles: the 11 KKT fields, sigma, beta,
+ * reused (0/1), psqmr steps, eps_k.  Returns rows written in *rows. */
+int gdwd_get_history(gdwd_ctx* ctx, double* hist, int64_t max_rows, int64_t* rows);
+
+/* standalone kernels (unit-test seams) -------------------------------------*/
+/* newton_r_sweep (subsolvers.py:321-364); scalar_form=1 gives newton_r
+ * (subsolvers.py:283-318) per coordinate, iters (nullable) its counts. */
+int gdwd_newton_sweep(int32_t device, int64_t n, const double* a, double sigma, double q, const double* weights,
+                      const double* r_init, double tol, int32_t max_newton, int32_t scalar_form, double* out,
+                      int32_t* iters);
+/* cholesky_factorize + explicit inverse (linalg/cholesky.py:25-66): S (m x m
+ * SPD, row-major) -> S^{-1}.  GDWD_ERR_INDEFINITE on a non-positive pivot. */
+int gdwd_chol_inverse(int32_t device, const double* S, int64_t m, double* inv_out);
+/* Gram of a row-major [rows][cols] matrix X on the FP64 tensor cores:
+ * sum_over_rows=1: X^T X (cols x cols, "Z Z^T" of subsolvers.py:76)
+ * sum_over_rows=0: X X^T (rows x rows, "Z^T Z" of subsolvers.py:109)
+ * result = gram / div + shift * I. */
+int gdwd_gram(int32_t device, const double* X, int64_t rows, int64_t cols, int32_t sum_over_rows, double div,
+              double shift, double* out);
+/* psqmr (linalg/psqmr.py:27-95) with a dense symmetric operator A (m x m,
+ * row-major) and diagonal preconditioner M (nullable = identity); x0 nullable.
+ * info[4] = {iterations, converged, breakdown, 0}; *resnorm = final |res|. */
+int gdwd_psqmr_dense(int32_t device, const double* A, int64_t m, const double* b, const double* M, double tol,
+                     int32_t max_iter, const double* x0, double* x_out, int32_t* info, double* resnorm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GDWD_B200_H */

@@ -1,0 +1,44 @@
+"""B200-native generalized DWD solver (inexact sGS-ADMM, arXiv 2305.12019).
+
+Drop-in for the reference package ``gdwd`` on its hot path: the same
+``sgs_admm_solve(data, config, meta=None, callback=None)`` entry point and
+records, with every iteration running in ``libgdwd_b200.so`` (hand-written
+sm_100a CUDA behind the C ABI in include/gdwd_b200.h).  There is no CPU
+fallback.
+"""
+
+from .model import FeatureMeta, ModelFile, identity_meta
+from .solver import (
+    Backend,
+    DegenerateSchurError,
+    DeviceProblem,
+    IndefiniteMatrixError,
+    KKTResiduals,
+    LanczosConvergenceError,
+    ProblemData,
+    SingleClassError,
+    SolveResult,
+    SolverConfig,
+    SolverKind,
+    SolverState,
+    compute_weights,
+    device_problem,
+    matvec,
+    newton_r,
+    newton_r_sweep,
+    scale_problem,
+    select_solver,
+    sgs_admm_solve,
+    update_sigma,
+)
+from .sparse import SparseFormatError, SparseMatrixCSC, csc_from_dense, csc_from_triplets
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Backend", "DegenerateSchurError", "DeviceProblem", "FeatureMeta", "IndefiniteMatrixError", "KKTResiduals",
+    "LanczosConvergenceError", "ModelFile", "ProblemData", "SingleClassError", "SolveResult", "SolverConfig",
+    "SolverKind", "SolverState", "SparseFormatError", "SparseMatrixCSC", "compute_weights", "csc_from_dense",
+    "csc_from_triplets", "device_problem", "identity_meta", "matvec", "newton_r", "newton_r_sweep",
+    "scale_problem", "select_solver", "sgs_admm_solve", "update_sigma",
+]

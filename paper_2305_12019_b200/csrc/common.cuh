@@ -1,0 +1,109 @@
+// Common device helpers for the gdwd B200 kernels.
+//
+// Everything here is fp64.  Reductions are deterministic: a fixed
+// warp-shuffle tree, then a fixed-order sum over warps, then (across CTAs) a
+// fixed-order sum over per-CTA partials performed by whichever CTA arrives
+// last at a ticket (the order of the final sum never depends on which CTA
+// that is).  SPEC.md:103,109 requires reproducible reductions.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define GDWD_DEV __device__ __forceinline__
+
+namespace gdwd {
+
+constexpr int WARP = 32;
+
+// ---------------------------------------------------------------------------
+// numpy-compatible elementwise helpers.  numpy's ``power`` with a scalar
+// exponent takes exact fast paths for 2, 0.5, -1 and 1 (square, sqrt,
+// reciprocal, copy); everything else is a libm-class pow.  Mirroring the fast
+// paths keeps q = 1 (the common case) bitwise identical to the reference.
+// ---------------------------------------------------------------------------
+GDWD_DEV double np_pow(double x, double e) {
+  if (e == 2.0) return __dmul_rn(x, x);
+  if (e == 0.5) return __dsqrt_rn(x);
+  if (e == 1.0) return x;
+  if (e == -1.0) return __ddiv_rn(1.0, x);
+  if (e == 0.0) return 1.0;
+  return pow(x, e);
+}
+
+// ---------------------------------------------------------------------------
+// Reductions
+// ---------------------------------------------------------------------------
+template <int K>
+GDWD_DEV void warp_sum(double (&v)[K]) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+  }
+}
+
+// Block-wide sum of K values; result valid in thread 0 (returned in v).
+// ``scratch`` must hold (blockDim.x/32)*K doubles.
+template <int K>
+GDWD_DEV void block_sum(double (&v)[K], double* scratch) {
+  warp_sum<K>(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) scratch[wid * K + k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += scratch[w * K + k];
+      v[k] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Ticket: returns true in exactly one CTA (the last of ``count`` arrivals),
+// after a fence that makes every earlier CTA's global writes visible.  The
+// counter is reset so the same slot can be reused (CUDA-graph replay).
+GDWD_DEV bool last_arrival(unsigned int* ticket, unsigned int count) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned int t = atomicAdd(ticket, 1u);
+    s_last = (t == count - 1);
+    if (s_last) *ticket = 0u;
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
+// load that bypasses L1 (data written by other CTAs of the same grid)
+GDWD_DEV double ld_cg(const double* p) { return __ldcg(p); }
+
+// Fixed-order sum of partials[p*stride + k], p in [0, np), for k < K, done by
+// thread 0.  Used by the ticket winner.
+template <int K>
+GDWD_DEV void sum_partials(const double* partials, int np, double (&out)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = 0.0;
+  for (int p = 0; p < np; ++p) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] += ld_cg(partials + (size_t)p * K + k);
+  }
+}
+
+// 128-bit streaming load (no L1 allocation): X is read once per pass.
+GDWD_DEV double2 ld_stream2(const double* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p));
+  return r;
+}
+
+}  // namespace gdwd

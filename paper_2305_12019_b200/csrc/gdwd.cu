@@ -1,0 +1,1095 @@
+// gdwd_b200: context, one-time setup, the device-resident sGS-ADMM loop
+// and the C ABI (include/gdwd_b200.h).
+//
+// The loop is the reference's sgs_admm_solve (solver.py:392-602) with every
+// vector resident in HBM; the host only launches work and, every
+// `poll_every` iterations, reads the device stop flag.  DIRECT and SMW2
+// iteration bodies are captured once into a CUDA graph and replayed; the
+// ITERATIVE body is host-driven because PSQMR's step count is data
+// dependent (one 4-byte flag read per PSQMR step).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/gdwd_b200.h"
+#include "common.cuh"
+#include "gram.cuh"
+#include "solver_ops.cuh"
+#include "zops.cuh"
+
+using namespace gdwd;
+
+namespace {
+
+constexpr int NUM_SMS = 148;
+
+struct DevBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t cnt) {
+    if (cnt <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(cnt, 1) * sizeof(double));
+    if (e == cudaSuccess) n = cnt;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+ZmvGeom zmv_geom(int64_t rows, int64_t cols) {
+  ZmvGeom g;
+  g.tiles = (int)((cols + ZMV_TILE - 1) / ZMV_TILE);
+  const int64_t target = NUM_SMS * 8;
+  int64_t segs = (target + g.tiles - 1) / g.tiles;
+  int64_t maxsegs = std::max<int64_t>(1, rows / 16);
+  segs = std::max<int64_t>(1, std::min(segs, maxsegs));
+  g.seg_len = (rows + segs - 1) / segs;
+  if (g.seg_len < 1) g.seg_len = 1;
+  g.segs = (int)((rows + g.seg_len - 1) / g.seg_len);
+  if (g.segs < 1) g.segs = 1;
+  g.ldp = (cols + 1) / 2 * 2;
+  return g;
+}
+
+ZtGeom zt_geom(int64_t rows, int64_t ld) {
+  ZtGeom g;
+  int64_t cw = std::min<int64_t>((ld + 63) / 64 * 64, ZT_CW);
+  g.cw = (int)cw;
+  g.chunks = (int)((ld + cw - 1) / cw);
+  int sb = 8;
+  while (sb < 256 && rows * g.chunks / (sb * 2) >= NUM_SMS * 8) sb *= 2;
+  g.sb = sb;
+  g.sblocks = (int)((rows + sb - 1) / sb);
+  if (g.sblocks < 1) g.sblocks = 1;
+  return g;
+}
+
+int vm_grid(int64_t len) {
+  int64_t b = (len + VM_THREADS - 1) / VM_THREADS;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, NUM_SMS * 4));
+}
+
+}  // namespace
+
+struct gdwd_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  // data
+  int64_t n = 0, d = 0, ldz = 0;
+  bool has_dense = false;
+  double* Zs = nullptr;
+  bool has_problem = false;
+  double C = 0, q = 0, zscale = 0, yty = 0;
+  DevBuf y, e, wl;
+  // scratch
+  DevBuf part, npart, tpart;
+  unsigned* tickets = nullptr;
+  size_t ntickets = 0;
+  Scratch scr{};
+  // solver buffers
+  DevBuf nvec, mvec, tabs, histb, fac, facw, colsq;
+  int64_t ldm = 0, fac_rows = 0;
+  int fac_kind = 0;
+  double fac_mu2 = -1;
+  uint64_t data_gen = 0, fac_gen = (uint64_t)-1;
+  int* dinfo = nullptr;
+  Scal* S = nullptr;
+  Scal* Sh = nullptr;  // pinned mirror
+  Dev D{};
+  int64_t hist_rows = 0;
+  std::vector<double> ps_per_iter;
+  int last_kind = 0;
+  // solve session (gdwd_solve_begin / _iterate / _end)
+  bool in_solve = false;
+  int kind = 0, poll = 16, max_iter = 0, max_steps = 50, k_host = 0, psqmr_total = 0;
+  bool use_sgs = true, stopped = false;
+  cudaGraphExec_t gexec = nullptr;
+  int64_t body_nodes = 0;
+  cudaEvent_t ev_begin = nullptr, ev_loop = nullptr, ev_end = nullptr;
+  cudaEvent_t poll_ev[2] = {nullptr, nullptr};
+  int* poll_flag = nullptr;  // pinned [2]
+  int poll_slot = 0, poll_pending = 0;
+  double eps_c = 0, setup_ms = 0;
+  // counters and per-kernel profile
+  int64_t launches = 0;
+  bool prof = false;
+  struct ProfRec { const char* tag; cudaEvent_t a, b; };
+  std::vector<ProfRec> prof_pending;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::map<std::string, std::pair<int64_t, double>> prof_acc;
+  cudaEvent_t take_event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+};
+
+static void end_session(gdwd_ctx* ctx);
+
+static int set_err(gdwd_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define RC(call)                           \
+  do {                                     \
+    int rc_ = (call);                      \
+    if (rc_ != GDWD_OK) return rc_;        \
+  } while (0)
+
+#define CK(call)                                                                 \
+  do {                                                                           \
+    cudaError_t e_ = (call);                                                     \
+    if (e_ != cudaSuccess)                                                       \
+      return set_err(ctx, GDWD_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+struct Launch {  // counts launches; with profiling on, brackets the launch with events
+  gdwd_ctx* c;
+  const char* tag;
+  cudaEvent_t a = nullptr;
+  Launch(gdwd_ctx* c_, const char* t) : c(c_), tag(t) {
+    c->launches++;
+    if (c->prof) {
+      a = c->take_event();
+      cudaEventRecord(a, c->st);
+    }
+  }
+  ~Launch() {
+    if (c->prof) {
+      cudaEvent_t b = c->take_event();
+      cudaEventRecord(b, c->st);
+      c->prof_pending.push_back({tag, a, b});
+    }
+  }
+};
+
+template <class Op>
+static void run_zmv(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "zmv") {
+  Launch L(ctx, tag);
+  ZmvGeom g = zmv_geom(X.rows, X.cols);
+  zmv_kernel<Op><<<dim3(g.tiles, g.segs), ZMV_THREADS, 0, ctx->st>>>(op, X, g, ctx->scr);
+}
+template <class Op>
+static void run_zt(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "ztmv") {
+  Launch L(ctx, tag);
+  ZtGeom g = zt_geom(X.rows, X.ld);
+  size_t sm = (size_t)(g.cw + g.sb) * sizeof(double);
+  ztmv_kernel<Op><<<dim3(g.chunks, g.sblocks), ZT_THREADS, sm, ctx->st>>>(op, X, g, ctx->scr);
+}
+template <class Op>
+static void run_vm(gdwd_ctx* ctx, const Op& op, int64_t len, const char* tag = "vmap") {
+  Launch L(ctx, tag);
+  vmap_kernel<Op><<<vm_grid(len), VM_THREADS, 0, ctx->st>>>(op, len, ctx->scr);
+}
+
+static void prof_flush(gdwd_ctx* ctx) {
+  if (ctx->prof_pending.empty()) return;
+  cudaStreamSynchronize(ctx->st);
+  for (auto& r : ctx->prof_pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto& acc = ctx->prof_acc[r.tag];
+    acc.first += 1;
+    acc.second += ms;
+  }
+  ctx->prof_pending.clear();
+  ctx->ev_used = 0;
+}
+
+// scratch sized for matrices with (rows, cols)
+static int ensure_scratch(gdwd_ctx* ctx, int64_t rows, int64_t cols) {
+  ZmvGeom zg = zmv_geom(rows, cols);
+  ZtGeom tg = zt_geom(rows, (cols + 1) / 2 * 2);
+  size_t part = std::max<size_t>((size_t)zg.segs * 2 * zg.ldp, tg.chunks > 1 ? (size_t)tg.chunks * rows : 0);
+  size_t npart = (size_t)std::max<int64_t>({(int64_t)zg.segs, (int64_t)tg.sblocks, (int64_t)NUM_SMS * 4}) * 16;
+  size_t tpart = (size_t)zg.tiles * 16 + 16;
+  size_t nt = (size_t)std::max<int64_t>(zg.tiles, tg.sblocks) + 4;
+  CK(ctx->part.ensure(std::max(part, ctx->part.n)));
+  CK(ctx->npart.ensure(std::max(npart, ctx->npart.n)));
+  CK(ctx->tpart.ensure(std::max(tpart, ctx->tpart.n)));
+  if (nt > ctx->ntickets) {
+    if (ctx->tickets) cudaFree(ctx->tickets);
+    CK(cudaMalloc(&ctx->tickets, nt * sizeof(unsigned)));
+    CK(cudaMemset(ctx->tickets, 0, nt * sizeof(unsigned)));
+    ctx->ntickets = nt;
+  }
+  ctx->scr = Scratch{ctx->part.p, ctx->npart.p, ctx->tpart.p, ctx->tickets};
+  return GDWD_OK;
+}
+
+// column sums of squares (row_sq_sums, sparse.py:66-70) via zmv with t = x
+struct OpColSqPrep {};
+template <class Op>
+__global__ void colsq_kernel(MatView X, double* out) {
+  // one thread per column, fixed sample order (matches bincount's order)
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= X.cols) return;
+  double s = 0.0;
+  for (int64_t i = 0; i < X.rows; ++i) {
+    const double v = X.a[i * X.ld + j];
+    s += v * v;
+  }
+  out[j] = s;
+}
+
+__global__ void jacobi_kernel(const double* colsq, int64_t d, double mu2, double yty, double* jac) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < d) {
+    const double v = colsq[j] + mu2;
+    jac[j] = v > 1e-12 ? v : 1e-12;
+  } else if (j == d) {
+    const double v = yty > mu2 ? yty : mu2;
+    jac[j] = v > 1e-12 ? v : 1e-12;
+  }
+}
+
+__global__ void assemble_direct_kernel(double* A, int64_t ld, int64_t d, const double* zy, double yty) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < d) {
+    A[j * ld + d] = zy[j];
+    A[d * ld + j] = zy[j];
+  } else if (j == d) {
+    A[d * ld + d] = yty;
+  }
+}
+
+__global__ void fill_kernel(double* p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+static void fill(gdwd_ctx* ctx, double* p, int64_t n, double v) {
+  fill_kernel<<<vm_grid(n), 256, 0, ctx->st>>>(p, n, v);
+}
+
+extern "C" {
+
+int gdwd_version(void) { return 1; }
+
+const char* gdwd_last_error(const gdwd_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int gdwd_ctx_create(int32_t device, gdwd_ctx** out) {
+  if (!out) return GDWD_ERR_VALUE;
+  *out = nullptr;
+  gdwd_ctx* ctx = new gdwd_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->S, sizeof(Scal));
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->Sh, sizeof(Scal));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->dinfo, sizeof(int));
+  if (e != cudaSuccess) {
+    fprintf(stderr, "gdwd_ctx_create: %s\n", cudaGetErrorString(e));
+    delete ctx;
+    return GDWD_ERR_CUDA;
+  }
+  *out = ctx;
+  return GDWD_OK;
+}
+
+void gdwd_ctx_destroy(gdwd_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->st) cudaStreamSynchronize(ctx->st);
+  if (ctx->Zs) cudaFree(ctx->Zs);
+  for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq})
+    b->release();
+  end_session(ctx);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : {ctx->ev_begin, ctx->ev_loop, ctx->ev_end, ctx->poll_ev[0], ctx->poll_ev[1]})
+    if (e) cudaEventDestroy(e);
+  if (ctx->poll_flag) cudaFreeHost(ctx->poll_flag);
+  if (ctx->tickets) cudaFree(ctx->tickets);
+  if (ctx->S) cudaFree(ctx->S);
+  if (ctx->Sh) cudaFreeHost(ctx->Sh);
+  if (ctx->dinfo) cudaFree(ctx->dinfo);
+  if (ctx->st) cudaStreamDestroy(ctx->st);
+  delete ctx;
+}
+
+int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n) {
+  if (!ctx || !samples || d < 1 || n < 1) return set_err(ctx, GDWD_ERR_VALUE, "bad dense upload arguments");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t ld = (d + 1) / 2 * 2;
+  if (ctx->Zs) cudaFree(ctx->Zs);
+  ctx->Zs = nullptr;
+  CK(cudaMalloc(&ctx->Zs, (size_t)n * ld * sizeof(double)));
+  if (ld != d) CK(cudaMemsetAsync(ctx->Zs, 0, (size_t)n * ld * sizeof(double), ctx->st));
+  CK(cudaMemcpy2DAsync(ctx->Zs, ld * sizeof(double), samples, d * sizeof(double), d * sizeof(double), n,
+                       cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  ctx->n = n;
+  ctx->d = d;
+  ctx->ldz = ld;
+  ctx->has_dense = true;
+  ctx->has_problem = false;
+  ctx->data_gen++;
+  return ensure_scratch(ctx, n, d);
+}
+
+int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t*, const int64_t*, const double*, int64_t, int64_t) {
+  return set_err(ctx, GDWD_ERR_UNSUPPORTED, "sparse CSC upload is not built in this version");
+}
+
+int gdwd_set_problem(gdwd_ctx* ctx, const double* y, const double* e, const double* weights, double C, double q,
+                     double z_scale) {
+  if (!ctx || !ctx->has_dense) return set_err(ctx, GDWD_ERR_VALUE, "upload Z~ before set_problem");
+  if (!y || !e || !weights) return set_err(ctx, GDWD_ERR_VALUE, "null problem vector");
+  if (!(C > 0 && q > 0 && z_scale > 0)) return set_err(ctx, GDWD_ERR_VALUE, "C, q and z_scale must be positive");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t n = ctx->n;
+  double yty = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(y[i] == 1.0 || y[i] == -1.0)) return set_err(ctx, GDWD_ERR_VALUE, "labels must be a length-n vector over {-1,+1}");
+    if (!(e[i] > 0)) return set_err(ctx, GDWD_ERR_VALUE, "e must be positive of length n");
+    if (!(weights[i] > 0)) return set_err(ctx, GDWD_ERR_VALUE, "weights must be positive of length n");
+    yty += y[i] * y[i];
+  }
+  CK(ctx->y.ensure(n));
+  CK(ctx->e.ensure(n));
+  CK(ctx->wl.ensure(n));
+  CK(cudaMemcpyAsync(ctx->y.p, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(ctx->e.p, e, n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(ctx->wl.p, weights, n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  ctx->C = C;
+  ctx->q = q;
+  ctx->zscale = z_scale;
+  ctx->yty = yty;
+  ctx->has_problem = true;
+  ctx->data_gen++;
+  return GDWD_OK;
+}
+
+int gdwd_matvec(gdwd_ctx* ctx, const double* v_n, double* out_d) {
+  if (!ctx || !ctx->has_dense || !v_n || !out_d) return set_err(ctx, GDWD_ERR_VALUE, "matvec: no data or null pointer");
+  CK(cudaSetDevice(ctx->device));
+  double *dv = nullptr, *dout = nullptr;
+  CK(cudaMalloc(&dv, ctx->n * sizeof(double)));
+  CK(cudaMalloc(&dout, ctx->d * sizeof(double)));
+  CK(cudaMemcpyAsync(dv, v_n, ctx->n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  OpPlainZ op{dv, nullptr, dout, nullptr};
+  run_zmv(ctx, op, MatView{ctx->Zs, ctx->n, ctx->d, ctx->ldz});
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out_d, dout, ctx->d * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  cudaFree(dv);
+  cudaFree(dout);
+  return GDWD_OK;
+}
+
+int gdwd_matvec_t(gdwd_ctx* ctx, const double* v_d, double* out_n) {
+  if (!ctx || !ctx->has_dense || !v_d || !out_n) return set_err(ctx, GDWD_ERR_VALUE, "matvec_t: no data or null pointer");
+  CK(cudaSetDevice(ctx->device));
+  double *dv = nullptr, *dout = nullptr;
+  CK(cudaMalloc(&dv, ctx->d * sizeof(double)));
+  CK(cudaMalloc(&dout, ctx->n * sizeof(double)));
+  CK(cudaMemcpyAsync(dv, v_d, ctx->d * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  OpPlainZt op{dv, dout};
+  run_zt(ctx, op, MatView{ctx->Zs, ctx->n, ctx->d, ctx->ldz});
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out_n, dout, ctx->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  cudaFree(dv);
+  cudaFree(dout);
+  return GDWD_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// solver internals
+// ---------------------------------------------------------------------------
+static int select_kind(int64_t n, int64_t d) {  // subsolvers.py:42-55
+  if (d > 5000 && 5 * n < d && n <= 2500) return GDWD_BACKEND_SMW2;
+  if (d > 5000) return GDWD_BACKEND_ITERATIVE;
+  return GDWD_BACKEND_DIRECT;
+}
+
+// One-time factorisation (cached per data generation / kind / mu^2).
+static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
+  if (ctx->fac_gen == ctx->data_gen && ctx->fac_kind == kind && ctx->fac_mu2 == mu2) return GDWD_OK;
+  Dev& D = ctx->D;
+  const int64_t n = ctx->n, d = ctx->d;
+  MatView Z{ctx->Zs, n, d, ctx->ldz};
+  if (kind == GDWD_BACKEND_DIRECT || kind == GDWD_BACKEND_SMW2) {
+    const int64_t m = (kind == GDWD_BACKEND_DIRECT) ? d + 1 : n;
+    const int64_t ld = (m + 1) / 2 * 2;
+    CK(ctx->fac.ensure((size_t)m * ld));
+    CK(cudaMemsetAsync(ctx->fac.p, 0, (size_t)m * ld * sizeof(double), ctx->st));
+    const int64_t K = (kind == GDWD_BACKEND_DIRECT) ? n : d;
+    const int64_t M = (kind == GDWD_BACKEND_DIRECT) ? d : n;
+    size_t ws = std::max<size_t>((size_t)gram_workspace_doubles(M, K), (size_t)2 * m * ld);
+    CK(ctx->facw.ensure(ws));
+    if (kind == GDWD_BACKEND_DIRECT) {
+      CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, true, 1.0, mu2, ctx->fac.p, ld, ctx->facw.p, ctx->st));
+      assemble_direct_kernel<<<(unsigned)((d + 256) / 256), 256, 0, ctx->st>>>(ctx->fac.p, ld, d, D.zy, ctx->yty);
+    } else {
+      CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, false, mu2, 1.0, ctx->fac.p, ld, ctx->facw.p, ctx->st));
+    }
+    CK(cudaMemsetAsync(ctx->dinfo, 0, sizeof(int), ctx->st));
+    CK(chol_inverse(ctx->fac.p, ctx->facw.p, ctx->facw.p + (size_t)m * ld, ld, m, ctx->dinfo, ctx->st));
+    int info = 0;
+    CK(cudaMemcpyAsync(&info, ctx->dinfo, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    if (info != 0) return set_err(ctx, GDWD_ERR_INDEFINITE, "non-positive pivot in Cholesky factorisation");
+    ctx->ldm = ld;
+    ctx->fac_rows = m;
+    if (kind == GDWD_BACKEND_SMW2) {
+      OpJyG op{ctx->y.p, D.ynorm, const_cast<double*>(D.jy), ctx->S};
+      RC(ensure_scratch(ctx, m, m));
+      run_zt(ctx, op, MatView{ctx->fac.p, m, m, ld});
+      CK(cudaGetLastError());
+      RC(ensure_scratch(ctx, n, d));
+    }
+  } else {
+    CK(ctx->colsq.ensure(d));
+    colsq_kernel<OpColSqPrep><<<(unsigned)((d + 255) / 256), 256, 0, ctx->st>>>(Z, ctx->colsq.p);
+    jacobi_kernel<<<(unsigned)((d + 256) / 256), 256, 0, ctx->st>>>(ctx->colsq.p, d, mu2, ctx->yty,
+                                                                     const_cast<double*>(D.jac));
+    CK(cudaGetLastError());
+  }
+  CK(cudaStreamSynchronize(ctx->st));
+  ctx->fac_gen = ctx->data_gen;
+  ctx->fac_kind = kind;
+  ctx->fac_mu2 = mu2;
+  return GDWD_OK;
+}
+
+// enqueue one normal-system solve: out = A^{-1} hv (DIRECT / SMW2)
+static void enqueue_solve(gdwd_ctx* ctx, int kind, const double* hv, double* out, int pred) {
+  const Dev& D = ctx->D;
+  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  MatView F{ctx->fac.p, ctx->fac_rows, ctx->fac_rows, ctx->ldm};
+  if (kind == GDWD_BACKEND_DIRECT) {
+    run_zt(ctx, OpGemvSolve{D, hv, out, pred}, F, pred ? "gemv_Ainv_2" : "gemv_Ainv");
+  } else {
+    run_zt(ctx, OpSmwS1{D, hv, pred}, Z, pred ? "ztmv_smw_s1_2" : "ztmv_smw_s1");
+    run_zt(ctx, OpSmwG{D, hv, pred}, F, pred ? "gemv_Ginv_2" : "gemv_Ginv");
+    run_zmv(ctx, OpSmwP{D, hv, out, pred}, Z, pred ? "zmv_smw_p_2" : "zmv_smw_p");
+  }
+}
+
+// host-driven PSQMR solve (ITERATIVE): out ~ A^{-1} b from x0
+static int psqmr_solve(gdwd_ctx* ctx, const double* b, const double* x0, double* out, int pred, double tolmul,
+                       int max_steps, int* steps, int* conv, int* active_run) {
+  const Dev& D = ctx->D;
+  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  run_zt(ctx, OpApplyZt{D, x0, pred, 0}, Z, "ztmv_psqmr_init");
+  run_zmv(ctx, OpInitResidual{D, x0, b, pred}, Z, "zmv_psqmr_init");
+  run_vm(ctx, OpPsInit{D, x0, out, pred, tolmul}, D.m, "vmap_psqmr_init");
+  CK(cudaGetLastError());
+  *steps = 0;
+  *conv = 1;
+  *active_run = 0;
+  for (int it = 0; it <= max_steps; ++it) {
+    CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    const Scal& s = *ctx->Sh;
+    if (s.stopped) return GDWD_OK;
+    if (it == 0) {
+      if (pred && s.reuse) return GDWD_OK;  // skipped by the Step-1c predicate
+      *active_run = 1;
+    }
+    if (!s.ps_active) {
+      *steps = s.ps_iters;
+      *conv = s.ps_conv;
+      return GDWD_OK;
+    }
+    if (it == max_steps) break;
+    run_zt(ctx, OpApplyZt{D, D.pq, 0, 1}, Z, "ztmv_psqmr_apply");
+    run_zmv(ctx, OpPsApply{D}, Z, "zmv_psqmr_apply");
+    run_vm(ctx, OpPsV1{D}, D.m, "vmap_psqmr_v1");
+    run_vm(ctx, OpPsV2{D, out, tolmul, max_steps}, D.m, "vmap_psqmr_v2");
+    CK(cudaGetLastError());
+  }
+  *steps = ctx->Sh->ps_iters;
+  *conv = ctx->Sh->ps_conv;
+  return GDWD_OK;
+}
+
+// the tail shared by every backend: w/ztw commit, Steps 2-3, KKT sample terms
+static void enqueue_tail(gdwd_ctx* ctx) {
+  const Dev& D = ctx->D;
+  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  run_vm(ctx, OpCopyIfReuse{D, D.xb, D.x}, D.m, "vmap_copy_x");
+  run_zt(ctx, OpZtStore{D, D.x, D.ztw, 1}, Z, "ztmv_ztw_2");
+  run_vm(ctx, OpCopyIfReuse{D, D.ztwb, D.ztw}, D.n, "vmap_copy_ztw");
+  run_vm(ctx, OpStep2a{D}, D.d, "vmap_step2a");
+  run_vm(ctx, OpStep2b{D}, D.d, "vmap_step2b");
+  run_vm(ctx, OpStep3{D}, D.n, "vmap_step3_kkt");
+}
+
+static void enqueue_body_fixed(gdwd_ctx* ctx, int kind, bool use_sgs) {
+  const Dev& D = ctx->D;
+  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
+  enqueue_solve(ctx, kind, D.h, D.xb, 0);
+  run_zt(ctx, OpZtNewton{D}, Z, "ztmv_newton");
+  if (use_sgs) run_zmv(ctx, OpDrZtwb{D}, Z, "zmv_dr_ztwb");
+  else run_vm(ctx, OpSetReuse{D}, 1, "vmap_set_reuse");
+  enqueue_solve(ctx, kind, D.h2, D.x, 1);
+  enqueue_tail(ctx);
+}
+
+static int body_iterative(gdwd_ctx* ctx, bool use_sgs, int max_steps, int* psqmr_steps) {
+  const Dev& D = ctx->D;
+  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
+  int steps = 0, conv = 1, ran = 0, rc;
+  *psqmr_steps = 0;
+  rc = psqmr_solve(ctx, D.h, D.x, D.xb, 0, 1.0, max_steps, &steps, &conv, &ran);
+  if (rc) return rc;
+  if (ctx->Sh->stopped) return GDWD_OK;
+  *psqmr_steps += steps;
+  if (ran && !conv)
+    return set_err(ctx, GDWD_ERR_UNSUPPORTED,
+                   "PSQMR exceeded psqmr_switch_steps: proximal backend switch not built in this version");
+  run_zt(ctx, OpZtNewton{D}, Z, "ztmv_newton");
+  if (use_sgs) run_zmv(ctx, OpDrZtwb{D}, Z, "zmv_dr_ztwb");
+  else run_vm(ctx, OpSetReuse{D}, 1, "vmap_set_reuse");
+  rc = psqmr_solve(ctx, D.h2, D.xb, D.x, 1, 5.0, max_steps, &steps, &conv, &ran);
+  if (rc) return rc;
+  *psqmr_steps += ran ? steps : 0;
+  if (ran && !conv)
+    return set_err(ctx, GDWD_ERR_UNSUPPORTED,
+                   "PSQMR exceeded psqmr_switch_steps: proximal backend switch not built in this version");
+  enqueue_tail(ctx);
+  CK(cudaGetLastError());
+  return GDWD_OK;
+}
+
+static void end_session(gdwd_ctx* ctx) {
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  ctx->gexec = nullptr;
+  ctx->in_solve = false;
+}
+
+extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const double* sched, int64_t sched_len) {
+  if (!ctx || !cfg) return set_err(ctx, GDWD_ERR_VALUE, "null argument");
+  if (!ctx->has_dense || !ctx->has_problem) return set_err(ctx, GDWD_ERR_VALUE, "no problem uploaded");
+  if (!(cfg->steplength > 0.0 && cfg->steplength <= 1.618034))
+    return set_err(ctx, GDWD_ERR_VALUE, "steplength must lie in (0, 1.618034)");
+  if (std::min({cfg->tol_feas, cfg->tol_cgap, cfg->tol_cap}) <= 0)
+    return set_err(ctx, GDWD_ERR_VALUE, "tolerances must be positive");
+  if (cfg->mu <= 0 || cfg->ell < 1 || cfg->max_iter < 1)
+    return set_err(ctx, GDWD_ERR_VALUE, "q, mu must be positive; ell, max_iter at least 1");
+  CK(cudaSetDevice(ctx->device));
+  end_session(ctx);
+  const int64_t n = ctx->n, d = ctx->d, m = d + 1;
+  int kind = cfg->backend == GDWD_BACKEND_AUTO ? select_kind(n, d) : cfg->backend;
+  if (kind < 1 || kind > 3) return set_err(ctx, GDWD_ERR_VALUE, "bad backend");
+  const double mu = cfg->mu, mu2 = mu * mu, q = ctx->q, C = ctx->C;
+  const int max_iter = cfg->max_iter;
+
+  // ---- buffers ------------------------------------------------------------
+  const int NV = 10, MV = 13;
+  CK(ctx->nvec.ensure((size_t)NV * n));
+  CK(ctx->mvec.ensure((size_t)MV * (m + 1)));
+  CK(ctx->tabs.ensure((size_t)2 * (max_iter + 2) + (size_t)std::max<int64_t>(sched_len, 1)));
+  CK(ctx->histb.ensure((size_t)(max_iter + 1) * HIST_W));
+  if (!ctx->poll_flag) CK(cudaMallocHost(&ctx->poll_flag, 2 * sizeof(int)));
+  for (int i = 0; i < 2; ++i)
+    if (!ctx->poll_ev[i]) CK(cudaEventCreateWithFlags(&ctx->poll_ev[i], cudaEventDisableTiming));
+  for (cudaEvent_t* e : {&ctx->ev_begin, &ctx->ev_loop, &ctx->ev_end})
+    if (!*e) CK(cudaEventCreate(e));
+  Dev& D = ctx->D;
+  D = Dev{};
+  D.n = n; D.d = d; D.m = m;
+  D.C = C; D.q = q; D.mu = mu; D.mu2 = mu2; D.zscale = ctx->zscale; D.tau = cfg->steplength;
+  D.yty = ctx->yty; D.ynorm = sqrt(ctx->yty);
+  D.kappa = (q + 1.0) / q * pow(q, 1.0 / (q + 1.0));
+  D.e1 = 1.0 / (q + 1.0); D.e2 = q / (q + 1.0); D.qp1 = q + 1.0; D.one_c = 1.0 + C;
+  D.tol_feas = cfg->tol_feas; D.tol_cgap = cfg->tol_cgap; D.tol_cap = cfg->tol_cap;
+  D.max_iter = max_iter;
+  D.y = ctx->y.p; D.e = ctx->e.p; D.wl = ctx->wl.p;
+  double* nv = ctx->nvec.p;
+  D.r = nv; D.xi = nv + n; D.al = nv + 2 * n; D.ztw = nv + 3 * n; D.rnew = nv + 4 * n; D.dr = nv + 5 * n;
+  D.ztwb = nv + 6 * n; D.s1 = nv + 7 * n; D.g = nv + 8 * n; D.tq = nv + 9 * n;
+  double* mv = ctx->mvec.p;
+  const int64_t ms = m + 1;
+  D.u = mv; D.rho = mv + ms; D.h = mv + 2 * ms; D.h2 = mv + 3 * ms; D.xb = mv + 4 * ms; D.x = mv + 5 * ms;
+  D.pr = mv + 6 * ms; D.pres = mv + 7 * ms; D.pq = mv + 8 * ms; D.pu = mv + 9 * ms; D.pd = mv + 10 * ms;
+  D.pAd = mv + 11 * ms; D.pAq = mv + 12 * ms;
+  // persistent per-problem vectors: [colsq (d) | zy (d) | jac (m) | jy (n)]
+  CK(ctx->colsq.ensure((size_t)d + (size_t)d + m + n + 8));
+  D.zy = ctx->colsq.p + d;
+  D.jac = ctx->colsq.p + 2 * d;
+  D.jy = ctx->colsq.p + 2 * d + m;
+  D.S = ctx->S;
+  D.hist = ctx->histb.p;
+
+  // ---- tables (host pow == Python's float pow) -------------------------------
+  const double eps_c = cfg->epsilon_c;
+  if (isnan(eps_c)) return set_err(ctx, GDWD_ERR_VALUE, "epsilon_c must be supplied by the host layer");
+  std::vector<double> tab(2 * (size_t)(max_iter + 2) + (size_t)std::max<int64_t>(sched_len, 1), 0.0);
+  const double sqrt_n = sqrt((double)n);
+  for (int k = 0; k < max_iter + 2; ++k) {
+    tab[k] = eps_c / pow(k + 1.0, 1.5);
+    tab[(max_iter + 2) + k] = tab[k] / sqrt_n;
+  }
+  if (sched && sched_len > 0) std::copy(sched, sched + sched_len, tab.begin() + 2 * (max_iter + 2));
+  CK(cudaMemcpyAsync(ctx->tabs.p, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  D.eps_tab = ctx->tabs.p;
+  D.tol_tab = ctx->tabs.p + (max_iter + 2);
+  D.sched = (sched && sched_len > 0) ? ctx->tabs.p + 2 * (max_iter + 2) : nullptr;
+  D.sched_len = (int)sched_len;
+
+  double sigma0 = cfg->sigma0;
+  if (isnan(sigma0)) sigma0 = pow(std::min(10.0 * C, (double)n), q);
+
+  // ---- setup: zy, factor / preconditioner ------------------------------------
+  CK(cudaEventRecord(ctx->ev_begin, ctx->st));
+  RC(ensure_scratch(ctx, n, d));
+  MatView Z{ctx->Zs, n, d, ctx->ldz};
+  run_zmv(ctx, OpPlainZ{ctx->y.p, nullptr, const_cast<double*>(D.zy), nullptr}, Z, "zmv_zy");
+  CK(cudaGetLastError());
+  RC(build_factor(ctx, kind, mu2));
+  if (kind != GDWD_BACKEND_ITERATIVE) RC(ensure_scratch(ctx, ctx->fac_rows, ctx->fac_rows));
+  RC(ensure_scratch(ctx, n, d));
+  // initial iterates (solver.py:447-454)
+  fill(ctx, D.r, n, 1.0);
+  fill(ctx, D.xi, n, 1.0);
+  fill(ctx, D.al, n, 0.0);
+  fill(ctx, D.ztw, n, 0.0);
+  CK(cudaMemsetAsync(ctx->mvec.p, 0, (size_t)MV * ms * sizeof(double), ctx->st));
+  CK(cudaMemsetAsync(ctx->histb.p, 0, (size_t)(max_iter + 1) * HIST_W * sizeof(double), ctx->st));
+  {
+    CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    const double ys = ctx->Sh->ys;  // computed by build_factor (SMW2)
+    Scal s0;
+    memset(&s0, 0, sizeof(s0));
+    s0.sigma = sigma0;
+    s0.sigma_next = sigma0;
+    s0.ys = ys;
+    *ctx->Sh = s0;
+    CK(cudaMemcpyAsync(ctx->S, ctx->Sh, sizeof(Scal), cudaMemcpyHostToDevice, ctx->st));
+  }
+  CK(cudaEventRecord(ctx->ev_loop, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  float setup = 0.f;
+  cudaEventElapsedTime(&setup, ctx->ev_begin, ctx->ev_loop);
+
+  ctx->ps_per_iter.assign(max_iter + 1, 0.0);
+  ctx->kind = kind;
+  ctx->use_sgs = cfg->use_sgs != 0;
+  ctx->poll = std::max(1, cfg->poll_every);
+  ctx->max_iter = max_iter;
+  ctx->max_steps = cfg->psqmr_switch_steps;
+  ctx->k_host = 0;
+  ctx->psqmr_total = 0;
+  ctx->stopped = false;
+  ctx->eps_c = eps_c;
+  ctx->setup_ms = setup;
+  ctx->poll_pending = 0;
+  if (kind != GDWD_BACKEND_ITERATIVE && cfg->use_graph && !ctx->prof) {
+    cudaGraph_t graph;
+    const int64_t before = ctx->launches;
+    CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+    enqueue_body_fixed(ctx, kind, ctx->use_sgs);
+    CK(cudaStreamEndCapture(ctx->st, &graph));
+    ctx->body_nodes = ctx->launches - before;
+    ctx->launches = before;
+    CK(cudaGraphInstantiate(&ctx->gexec, graph, 0));
+    cudaGraphDestroy(graph);
+  }
+  ctx->in_solve = true;
+  return GDWD_OK;
+}
+
+// Run up to `count` more iterations (fewer if the stopping rule fires).
+extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb, void* user, int32_t* iters_done,
+                                  int32_t* stopped_out) {
+  if (!ctx || !ctx->in_solve) return set_err(ctx, GDWD_ERR_VALUE, "no solve in progress");
+  CK(cudaSetDevice(ctx->device));
+  const Dev& D = ctx->D;
+  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  int status = GDWD_OK;
+  const int kend = std::min(ctx->max_iter, ctx->k_host + std::max(0, count));
+  while (ctx->k_host < kend && !ctx->stopped) {
+    const int k = ctx->k_host;
+    if (ctx->kind == GDWD_BACKEND_ITERATIVE) {
+      int steps = 0;
+      status = body_iterative(ctx, ctx->use_sgs, ctx->max_steps, &steps);
+      if (status) break;
+      ctx->psqmr_total += steps;
+      ctx->ps_per_iter[k] = steps;
+    } else if (ctx->gexec) {
+      CK(cudaGraphLaunch(ctx->gexec, ctx->st));
+      ctx->launches += ctx->body_nodes;
+    } else {
+      enqueue_body_fixed(ctx, ctx->kind, ctx->use_sgs);
+    }
+    CK(cudaGetLastError());
+    ctx->k_host = k + 1;
+    if (ctx->prof) prof_flush(ctx);
+    if (cb) {
+      run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");  // completes KKT (dual objective, gap) + stop test
+      CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
+      CK(cudaStreamSynchronize(ctx->st));
+      const Scal& s = *ctx->Sh;
+      if (s.error) {
+        ctx->stopped = true;
+        break;
+      }
+      if (s.iters_done == k + 1) {
+        double hrow[HIST_W];
+        CK(cudaMemcpy(hrow, D.hist + (int64_t)k * HIST_W, sizeof(hrow), cudaMemcpyDeviceToHost));
+        double res11[11];
+        for (int f = 0; f < 11; ++f)
+          res11[f] = (f < 8) ? hrow[f] : (f == 8 ? hrow[H_GAP] : (f == 9 ? hrow[H_OBJP] : hrow[H_OBJD]));
+        if (cb(user, k + 1, res11, hrow[H_SIGMA], hrow[H_BETA]) != 0) {
+          status = set_err(ctx, GDWD_ERR_ABORTED, "callback requested abort");
+          break;
+        }
+      }
+      ctx->stopped = s.stopped != 0;
+    } else if (ctx->kind == GDWD_BACKEND_ITERATIVE) {
+      ctx->stopped = ctx->Sh->stopped != 0;  // synced inside the PSQMR loop
+    } else if ((k + 1) % ctx->poll == 0) {
+      // lagged poll: read the flag copied one poll interval ago (the GPU
+      // still has this interval queued, so it never idles on the host)
+      const int sl = ctx->poll_slot;
+      CK(cudaMemcpyAsync(ctx->poll_flag + sl, &ctx->S->stopped, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+      CK(cudaEventRecord(ctx->poll_ev[sl], ctx->st));
+      if (ctx->poll_pending) {
+        CK(cudaEventSynchronize(ctx->poll_ev[sl ^ 1]));
+        if (ctx->poll_flag[sl ^ 1]) ctx->stopped = true;
+      }
+      ctx->poll_pending = 1;
+      ctx->poll_slot = sl ^ 1;
+    }
+  }
+  if (ctx->prof) prof_flush(ctx);
+  if (iters_done) *iters_done = ctx->k_host;
+  if (stopped_out) *stopped_out = ctx->stopped ? 1 : 0;
+  if (status) end_session(ctx);
+  return status;
+}
+
+extern "C" int gdwd_solve_end(gdwd_ctx* ctx, gdwd_result* out) {
+  if (!ctx || !ctx->in_solve || !out) return set_err(ctx, GDWD_ERR_VALUE, "no solve in progress");
+  CK(cudaSetDevice(ctx->device));
+  memset(out, 0, sizeof(*out));
+  const Dev& D = ctx->D;
+  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  // final pass: dual objective / gap / stop test of the last iteration
+  run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev_end, ctx->st));
+  CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  if (ctx->prof) prof_flush(ctx);
+  const Scal s = *ctx->Sh;
+  float ms_loop = 0;
+  cudaEventElapsedTime(&ms_loop, ctx->ev_loop, ctx->ev_end);
+  end_session(ctx);
+  if (s.error == 6) return set_err(ctx, GDWD_ERR_ASSERT, "margin iterate left the positive orthant");
+  ctx->hist_rows = s.iters_done;
+  ctx->last_kind = ctx->kind;
+  out->iterations = s.iters_done;
+  out->converged = s.converged;
+  out->backend = ctx->kind;
+  out->psqmr_total = ctx->psqmr_total;
+  out->double_count = s.double_count;
+  out->status = 0;
+  out->sigma = s.sigma;
+  out->eps_c = ctx->eps_c;
+  out->setup_ms = ctx->setup_ms;
+  out->loop_ms = ms_loop;
+  double bet = 0.0;
+  CK(cudaMemcpy(&bet, D.x + ctx->d, sizeof(double), cudaMemcpyDeviceToHost));
+  out->beta = bet;
+  for (int f = 0; f < 11; ++f) out->resid[f] = s.eta[f];
+  return GDWD_OK;
+}
+
+extern "C" int gdwd_solve(gdwd_ctx* ctx, const gdwd_config* cfg, const double* sched, int64_t sched_len,
+                          gdwd_iter_cb cb, void* user, gdwd_result* out) {
+  if (!out) return set_err(ctx, GDWD_ERR_VALUE, "null result");
+  RC(gdwd_solve_begin(ctx, cfg, sched, sched_len));
+  RC(gdwd_solve_iterate(ctx, cfg->max_iter, cb, user, nullptr, nullptr));
+  return gdwd_solve_end(ctx, out);
+}
+
+extern "C" int gdwd_set_profile(gdwd_ctx* ctx, int32_t enable) {
+  if (!ctx) return GDWD_ERR_VALUE;
+  ctx->prof = enable != 0;
+  if (!ctx->prof) ctx->prof_acc.clear();
+  return GDWD_OK;
+}
+
+extern "C" int gdwd_get_profile(gdwd_ctx* ctx, char* buf, int64_t buflen, int64_t* launches) {
+  if (!ctx) return GDWD_ERR_VALUE;
+  if (launches) *launches = ctx->launches;
+  if (buf && buflen > 0) {
+    std::string txt;
+    char line[256];
+    for (auto& kv : ctx->prof_acc) {
+      snprintf(line, sizeof(line), "%s %lld %.6f\n", kv.first.c_str(), (long long)kv.second.first, kv.second.second);
+      txt += line;
+    }
+    strncpy(buf, txt.c_str(), (size_t)buflen - 1);
+    buf[buflen - 1] = 0;
+  }
+  return GDWD_OK;
+}
+
+extern "C" int gdwd_reset_counters(gdwd_ctx* ctx) {
+  if (!ctx) return GDWD_ERR_VALUE;
+  ctx->launches = 0;
+  ctx->prof_acc.clear();
+  return GDWD_OK;
+}
+
+// Device time (ms) of `count` iterations of the current solve, CUDA events on
+// the solve's stream, with a synchronize on both sides.
+extern "C" int gdwd_time_iterations(gdwd_ctx* ctx, int32_t count, double* ms, int32_t* iters_done) {
+  if (!ctx || !ctx->in_solve || !ms) return set_err(ctx, GDWD_ERR_VALUE, "no solve in progress");
+  CK(cudaStreamSynchronize(ctx->st));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaEventRecord(a, ctx->st));
+  int32_t st = 0;
+  RC(gdwd_solve_iterate(ctx, count, nullptr, nullptr, iters_done, &st));
+  CK(cudaEventRecord(b, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  float f = 0.f;
+  cudaEventElapsedTime(&f, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *ms = f;
+  return GDWD_OK;
+}
+
+extern "C" int gdwd_get_state(gdwd_ctx* ctx, double* r, double* xi, double* alpha, double* w, double* u,
+                              double* rho, double* ztw, double* beta) {
+  if (!ctx || !ctx->nvec.p) return set_err(ctx, GDWD_ERR_VALUE, "no solve state");
+  CK(cudaSetDevice(ctx->device));
+  const Dev& D = ctx->D;
+  const int64_t n = ctx->n, d = ctx->d;
+  struct P { double* h; const double* dp; int64_t len; } items[] = {
+      {r, D.r, n}, {xi, D.xi, n}, {alpha, D.al, n}, {ztw, D.ztw, n}, {w, D.x, d}, {u, D.u, d}, {rho, D.rho, d}, {beta, D.x + d, 1}};
+  for (auto& it : items)
+    if (it.h) CK(cudaMemcpyAsync(it.h, it.dp, it.len * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return GDWD_OK;
+}
+
+extern "C" int gdwd_get_history(gdwd_ctx* ctx, double* hist, int64_t max_rows, int64_t* rows) {
+  if (!ctx || !hist || !rows) return set_err(ctx, GDWD_ERR_VALUE, "null argument");
+  int64_t nr = std::min(max_rows, ctx->hist_rows);
+  if (nr > 0) {
+    CK(cudaMemcpy(hist, ctx->histb.p, nr * HIST_W * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < nr && k < (int64_t)ctx->ps_per_iter.size(); ++k) hist[k * HIST_W + H_PSQMR] = ctx->ps_per_iter[k];
+  }
+  *rows = nr;
+  return GDWD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// standalone seams
+// ---------------------------------------------------------------------------
+namespace {
+struct Tmp {
+  std::vector<void*> ptrs;
+  ~Tmp() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+};
+
+// Dense symmetric operator for standalone PSQMR: Aq = A q, fused q.Aq
+struct OpDenseApply {
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return !D.S->ps_active; }
+  GDWD_DEV double wval(int64_t j) const { return D.pq[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&na)[NN]) const {
+    D.pAq[i] = dot;
+    na[0] += D.pq[i] * dot;
+  }
+  GDWD_DEV void fin(const double (&ns)[NN]) const {
+    Scal* S = D.S;
+    if (fabs(ns[0]) < TINY) {
+      S->ps_brk = 1;
+      S->ps_active = 0;
+      return;
+    }
+    S->ps_alpha = S->ps_rho / ns[0];
+  }
+};
+struct OpDenseInitRes {
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = false;
+  const double* x0;
+  const double* b;
+  double* r;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV double wval(int64_t j) const { return x0[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&)[NN]) const { r[i] = b[i] - dot; }
+  GDWD_DEV void fin(const double (&)[NN]) const {}
+};
+}  // namespace
+
+extern "C" int gdwd_newton_sweep(int32_t device, int64_t n, const double* a, double sigma, double q,
+                                 const double* w, const double* r0, double tol, int32_t max_newton,
+                                 int32_t scalar_form, double* out, int32_t* iters) {
+  gdwd_ctx* ctx = nullptr;
+  if (n < 0 || !a || !w || !r0 || !out) return GDWD_ERR_VALUE;
+  if (!(sigma > 0 && q > 0)) return GDWD_ERR_VALUE;
+  if (n == 0) return GDWD_OK;
+  if (cudaSetDevice(device) != cudaSuccess) return GDWD_ERR_CUDA;
+  Tmp t;
+  double *da = t.alloc<double>(n), *dw = t.alloc<double>(n), *dr = t.alloc<double>(n), *dout = t.alloc<double>(n);
+  int* dit = t.alloc<int>(n);
+  if (!da || !dw || !dr || !dout || !dit) return GDWD_ERR_CUDA;
+  CK(cudaMemcpy(da, a, n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dw, w, n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dr, r0, n * 8, cudaMemcpyHostToDevice));
+  OpNewtonSweep op{da, dw, dr, dout, dit, sigma, q, tol, max_newton, scalar_form};
+  vmap_kernel<OpNewtonSweep><<<vm_grid(n), VM_THREADS>>>(op, n, Scratch{});
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out, dout, n * 8, cudaMemcpyDeviceToHost));
+  if (iters) CK(cudaMemcpy(iters, dit, n * 4, cudaMemcpyDeviceToHost));
+  return GDWD_OK;
+}
+
+extern "C" int gdwd_chol_inverse(int32_t device, const double* Sm, int64_t m, double* inv_out) {
+  gdwd_ctx* ctx = nullptr;
+  if (m < 1 || !Sm || !inv_out) return GDWD_ERR_VALUE;
+  if (cudaSetDevice(device) != cudaSuccess) return GDWD_ERR_CUDA;
+  Tmp t;
+  const int64_t ld = (m + 1) / 2 * 2;
+  double* A = t.alloc<double>((size_t)m * ld);
+  double* W = t.alloc<double>((size_t)2 * m * ld);
+  int* info = t.alloc<int>(1);
+  if (!A || !W || !info) return GDWD_ERR_CUDA;
+  CK(cudaMemcpy2D(A, ld * 8, Sm, m * 8, m * 8, m, cudaMemcpyHostToDevice));
+  CK(cudaMemset(info, 0, sizeof(int)));
+  CK(chol_inverse(A, W, W + (size_t)m * ld, ld, m, info, 0));
+  int h = 0;
+  CK(cudaMemcpy(&h, info, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h) return GDWD_ERR_INDEFINITE;
+  CK(cudaMemcpy2D(inv_out, m * 8, A, ld * 8, m * 8, m, cudaMemcpyDeviceToHost));
+  return GDWD_OK;
+}
+
+extern "C" int gdwd_gram(int32_t device, const double* X, int64_t rows, int64_t cols, int32_t sum_over_rows,
+                         double div, double shift, double* outp) {
+  gdwd_ctx* ctx = nullptr;
+  if (rows < 1 || cols < 1 || !X || !outp) return GDWD_ERR_VALUE;
+  if (cudaSetDevice(device) != cudaSuccess) return GDWD_ERR_CUDA;
+  Tmp t;
+  const int64_t ld = (cols + 1) / 2 * 2;
+  const int64_t M = sum_over_rows ? cols : rows, K = sum_over_rows ? rows : cols;
+  double* dX = t.alloc<double>((size_t)rows * ld);
+  double* C = t.alloc<double>((size_t)M * M);
+  double* W = t.alloc<double>((size_t)gram_workspace_doubles(M, K));
+  if (!dX || !C || !W) return GDWD_ERR_CUDA;
+  CK(cudaMemset(dX, 0, (size_t)rows * ld * 8));
+  CK(cudaMemcpy2D(dX, ld * 8, X, cols * 8, cols * 8, rows, cudaMemcpyHostToDevice));
+  CK(gram_syrk(dX, rows, cols, ld, sum_over_rows != 0, div, shift, C, M, W, 0));
+  CK(cudaMemcpy(outp, C, (size_t)M * M * 8, cudaMemcpyDeviceToHost));
+  return GDWD_OK;
+}
+
+extern "C" int gdwd_psqmr_dense(int32_t device, const double* A, int64_t m, const double* b, const double* M,
+                                double tol, int32_t max_iter, const double* x0, double* x_out, int32_t* info,
+                                double* resnorm) {
+  if (m < 1 || !A || !b || !x_out || !info) return GDWD_ERR_VALUE;
+  if (cudaSetDevice(device) != cudaSuccess) return GDWD_ERR_CUDA;
+  gdwd_ctx* ctx = nullptr;
+  Tmp t;
+  const int64_t ld = (m + 1) / 2 * 2;
+  double* dA = t.alloc<double>((size_t)m * ld);
+  double* vec = t.alloc<double>((size_t)12 * (m + 1));
+  Scal* S = t.alloc<Scal>(1);
+  size_t npn = (size_t)NUM_SMS * 4 * 16 + 64;
+  double* npart = t.alloc<double>(npn);
+  double* part = t.alloc<double>((size_t)8 * (m + 1));
+  unsigned* tk = t.alloc<unsigned>(((m + 7) / 8) + 8);
+  if (!dA || !vec || !S || !npart || !part || !tk) return GDWD_ERR_CUDA;
+  CK(cudaMemset(dA, 0, (size_t)m * ld * 8));
+  CK(cudaMemcpy2D(dA, ld * 8, A, m * 8, m * 8, m, cudaMemcpyHostToDevice));
+  CK(cudaMemset(vec, 0, (size_t)12 * (m + 1) * 8));
+  CK(cudaMemset(tk, 0, (((m + 7) / 8) + 8) * sizeof(unsigned)));
+  const int64_t s = m + 1;
+  Dev D{};
+  D.m = m;
+  double* bb = vec;
+  double* x0d = vec + s;
+  double* jac = vec + 2 * s;
+  D.pr = vec + 3 * s; D.pres = vec + 4 * s; D.pq = vec + 5 * s; D.pu = vec + 6 * s; D.pd = vec + 7 * s;
+  D.pAd = vec + 8 * s; D.pAq = vec + 9 * s;
+  double* xo = vec + 10 * s;
+  double* epsd = vec + 11 * s;
+  D.jac = jac;
+  D.S = S;
+  D.eps_tab = epsd;
+  CK(cudaMemcpy(bb, b, m * 8, cudaMemcpyHostToDevice));
+  if (x0) CK(cudaMemcpy(x0d, x0, m * 8, cudaMemcpyHostToDevice));
+  std::vector<double> jh(m, 1.0);
+  if (M) std::copy(M, M + m, jh.begin());
+  CK(cudaMemcpy(jac, jh.data(), m * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(epsd, &tol, 8, cudaMemcpyHostToDevice));
+  Scal s0;
+  memset(&s0, 0, sizeof(s0));
+  CK(cudaMemcpy(S, &s0, sizeof(Scal), cudaMemcpyHostToDevice));
+  Scratch scr{part, npart, npart + (npn - 32), tk};
+  MatView Av{dA, m, m, ld};
+  ZtGeom g = zt_geom(m, ld);
+  size_t sm = (size_t)(g.cw + g.sb) * 8;
+  ztmv_kernel<OpDenseInitRes><<<dim3(g.chunks, g.sblocks), ZT_THREADS, sm>>>(OpDenseInitRes{x0d, bb, D.pr}, Av, g, scr);
+  vmap_kernel<OpPsInit><<<vm_grid(m), VM_THREADS>>>(OpPsInit{D, x0d, xo, 0, 1.0}, m, scr);
+  CK(cudaGetLastError());
+  Scal h;
+  for (int it = 0; it <= max_iter; ++it) {
+    CK(cudaMemcpy(&h, S, sizeof(Scal), cudaMemcpyDeviceToHost));
+    if (!h.ps_active || it == max_iter) break;
+    ztmv_kernel<OpDenseApply><<<dim3(g.chunks, g.sblocks), ZT_THREADS, sm>>>(OpDenseApply{D}, Av, g, scr);
+    vmap_kernel<OpPsV1><<<vm_grid(m), VM_THREADS>>>(OpPsV1{D}, m, scr);
+    vmap_kernel<OpPsV2><<<vm_grid(m), VM_THREADS>>>(OpPsV2{D, xo, 1.0, max_iter}, m, scr);
+    CK(cudaGetLastError());
+  }
+  CK(cudaMemcpy(x_out, xo, m * 8, cudaMemcpyDeviceToHost));
+  info[0] = h.ps_iters;
+  info[1] = h.ps_conv;
+  info[2] = h.ps_brk;
+  info[3] = 0;
+  if (resnorm) *resnorm = h.ps_resn;
+  return GDWD_OK;
+}

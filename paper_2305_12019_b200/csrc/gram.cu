@@ -1,0 +1,348 @@
+// FP64 tensor-core (DMMA) GEMM, Gram (SYRK) and the one-time dense
+// Cholesky + explicit inverse used by the DIRECT and SMW regimes.
+//
+// Reference call sites replaced:
+//   subsolvers.py:76   (Z Z^T).toarray()        -> gram_syrk(TN)  [DIRECT]
+//   subsolvers.py:109  (Z^T Z).toarray()/mu^2   -> gram_syrk(NT)  [SMW]
+//   cholesky.py:46     scipy.linalg.cholesky    -> chol_inverse (recursive
+//                      blocked potrf+trtri on DMMA GEMMs)
+//   cholesky.py:60-61  two solve_triangular     -> replaced per iteration by
+//                      one GEMV with the explicit inverse (solver kernels).
+//
+// tcgen05 has no f64 kind; the FP64 tensor path on sm_100a is the legacy
+// warp-level mma.sync m8n8k4 (SASS: DMMA.8x8x4).  Tiles: CTA 64x64, BK=16,
+// 8 warps as 2(m) x 4(n), each warp 32x16 = 4x2 DMMA tiles; register-staged
+// double buffering of the next K-slab; split-K over grid.z writes
+// deterministic per-slice partials that a fixed-order reduction sums.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "common.cuh"
+#include "gram.cuh"
+
+namespace gdwd {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, GT = 256;
+constexpr int APAD = 8;
+
+// operand element (row r in [0,R), k) with strides (sr, sk)
+struct Opnd {
+  const double* p;
+  int64_t sr, sk;
+};
+
+GDWD_DEV void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Load a BK x 64 slab of operand op (rows r0.., k0..) into registers.
+// kfast: the k index varies fastest across threads (for operands whose k
+// stride is 1) so that the warp's loads coalesce; otherwise r is fastest.
+template <bool KFAST>
+GDWD_DEV void load_slab(const Opnd& op, int64_t R, int64_t K, int64_t r0, int64_t k0, double (&reg)[4]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    int idx = threadIdx.x + e * GT;  // 0..1023
+    int kk, rr;
+    if (KFAST) { kk = idx & (BK - 1); rr = idx >> 4; }
+    else       { rr = idx & 63;       kk = idx >> 6; }
+    int64_t r = r0 + rr, k = k0 + kk;
+    reg[e] = (r < R && k < K) ? op.p[r * op.sr + k * op.sk] : 0.0;
+  }
+}
+
+template <bool KFAST>
+GDWD_DEV void store_slab(double (*s)[BM + APAD], const double (&reg)[4]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    int idx = threadIdx.x + e * GT;
+    int kk, rr;
+    if (KFAST) { kk = idx & (BK - 1); rr = idx >> 4; }
+    else       { rr = idx & 63;       kk = idx >> 6; }
+    s[kk][rr] = reg[e];
+  }
+}
+
+// C-tile partial: Cw[m][n] = sum_{k in slice} A(m,k) B(n,k)
+template <bool AK, bool BKF>
+__global__ void __launch_bounds__(GT) gemm_dmma_kernel(Opnd A, Opnd B, int64_t M, int64_t N, int64_t K,
+                                                       int64_t kslice, double* W, int64_t ldw,
+                                                       int64_t wslice, bool upper_only, double alpha,
+                                                       double beta, double* C, int64_t ldc) {
+  const int bm = blockIdx.y, bn = blockIdx.x;
+  if (upper_only && bn < bm) return;
+  __shared__ double As[2][BK][BM + APAD];
+  __shared__ double Bs[2][BK][BN + APAD];
+  const int64_t m0 = (int64_t)bm * BM, n0 = (int64_t)bn * BN;
+  const int64_t kb = (int64_t)blockIdx.z * kslice;
+  const int64_t ke = (kb + kslice < K) ? kb + kslice : K;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int g = lane >> 2, t4 = lane & 3;
+
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  double ra[4], rb[4];
+  int buf = 0;
+  if (kb < ke) {
+    load_slab<AK>(A, M, ke, m0, kb, ra);
+    load_slab<BKF>(B, N, ke, n0, kb, rb);
+    store_slab<AK>(As[0], ra);
+    store_slab<BKF>(Bs[0], rb);
+  }
+  __syncthreads();
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+    const bool more = k0 + BK < ke;
+    if (more) {
+      load_slab<AK>(A, M, ke, m0, k0 + BK, ra);
+      load_slab<BKF>(B, N, ke, n0, k0 + BK, rb);
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[buf][kk + t4][wm * 32 + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = Bs[buf][kk + t4][wn * 16 + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+    if (more) {
+      store_slab<AK>(As[buf ^ 1], ra);
+      store_slab<BKF>(Bs[buf ^ 1], rb);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + wm * 32 + i * 8 + g;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t nn = n0 + wn * 16 + j * 8 + t4 * 2 + h;
+        if (nn >= N) continue;
+        if (W) {
+          W[(int64_t)blockIdx.z * wslice + m * ldw + nn] = acc[i][j][h];
+        } else {
+          double* cp = C + m * ldc + nn;
+          *cp = (beta == 0.0) ? alpha * acc[i][j][h] : beta * *cp + alpha * acc[i][j][h];
+        }
+      }
+    }
+  }
+}
+
+// Sum split-K partials in slice order, symmetric fill from the upper
+// triangle, C[i][j] = S[min][max] / div + (i==j ? shift : 0).
+__global__ void syrk_finish_kernel(const double* W, int64_t ldw, int64_t wslice, int nslice, int64_t M,
+                                   double div, double shift, double* C, int64_t ldc) {
+  const int64_t tot = M * M;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = idx / M, j = idx % M;
+    int64_t a = i < j ? i : j, b = i < j ? j : i;
+    double s = 0.0;
+    for (int z = 0; z < nslice; ++z) s += W[z * wslice + a * ldw + b];
+    double v = (div == 1.0) ? s : s / div;
+    if (i == j) v += shift;
+    C[i * ldc + j] = v;
+  }
+}
+
+// Dense factor + inverse of one diagonal block (m <= 64) in shared memory:
+// A = L L^T (L lower), Linv = L^{-1}.  Upper parts are written as zeros.
+__global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t ldl, int m, int* info,
+                                  int64_t offset) {
+  __shared__ double L[64][65];
+  __shared__ int bad;
+  const int t = threadIdx.x;
+  if (t == 0) bad = 0;
+  for (int idx = t; idx < 64 * 64; idx += blockDim.x) {
+    int i = idx >> 6, j = idx & 63;
+    L[i][j] = (i < m && j < m && j <= i) ? A[i * lda + j] : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    if (t == 0) {
+      double dj = L[j][j];
+      if (!(dj > 0.0)) { bad = 1; dj = 1.0; }
+      L[j][j] = sqrt(dj);
+    }
+    __syncthreads();
+    for (int i = j + 1 + t; i < m; i += blockDim.x) L[i][j] = L[i][j] / L[j][j];
+    __syncthreads();
+    for (int idx = t; idx < 64 * 64; idx += blockDim.x) {
+      int i = idx >> 6, k = idx & 63;
+      if (k > j && i >= k && i < m) L[i][k] -= L[i][j] * L[k][j];
+    }
+    __syncthreads();
+  }
+  // Linv by forward substitution, one column per thread, written straight
+  // to global memory (each thread re-reads only its own column)
+  if (t < 64) {
+    const int c = t;
+    for (int i = 0; i < m; ++i) {
+      if (c >= m) break;
+      if (i < c) { Linv[i * ldl + c] = 0.0; continue; }
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) s -= L[i][k] * Linv[k * ldl + c];
+      Linv[i * ldl + c] = s / L[i][i];
+    }
+  }
+  __syncthreads();
+  for (int idx = t; idx < m * m; idx += blockDim.x) {
+    int i = idx / m, j = idx % m;
+    A[i * lda + j] = (j <= i) ? L[i][j] : 0.0;
+  }
+  if (t == 0 && bad && info) atomicCAS(info, 0, (int)offset + 1);
+}
+
+__global__ void zero_kernel(double* p, int64_t rows, int64_t cols, int64_t ld) {
+  const int64_t tot = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    p[(idx / cols) * ld + idx % cols] = 0.0;
+}
+
+__global__ void copy2d_kernel(const double* s, int64_t lds, double* d, int64_t ldd, int64_t rows,
+                              int64_t cols) {
+  const int64_t tot = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    d[(idx / cols) * ldd + idx % cols] = s[(idx / cols) * lds + idx % cols];
+}
+
+int grid_for(int64_t tot) {
+  int64_t b = (tot + 255) / 256;
+  return (int)(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+}  // namespace
+
+// C (M x N) = alpha * sum_k A(m,k) B(n,k) + beta * C.
+// A(m,k) = a[m*sam + k*sak]; B(n,k) = b[n*sbn + k*sbk].
+cudaError_t gemm_f64(const double* a, int64_t sam, int64_t sak, const double* b, int64_t sbn,
+                     int64_t sbk, int64_t M, int64_t N, int64_t K, double alpha, double beta, double* C,
+                     int64_t ldc, cudaStream_t st) {
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), 1);
+  Opnd A{a, sam, sak}, B{b, sbn, sbk};
+  const bool ak = (sak == 1), bk = (sbk == 1);
+  if (ak && bk)
+    gemm_dmma_kernel<true, true><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc);
+  else if (ak)
+    gemm_dmma_kernel<true, false><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc);
+  else if (bk)
+    gemm_dmma_kernel<false, true><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc);
+  else
+    gemm_dmma_kernel<false, false><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc);
+  return cudaGetLastError();
+}
+
+int64_t gram_workspace_doubles(int64_t M, int64_t K) {
+  int nslice = gram_slices(M, K);
+  return (int64_t)nslice * M * M;
+}
+
+int gram_slices(int64_t M, int64_t K) {
+  const int64_t tiles = ((M + BM - 1) / BM) * ((M + BM - 1) / BM + 1) / 2;
+  int64_t s = (148 * 3 + tiles - 1) / tiles;  // aim for >= 3 CTAs per SM
+  int64_t kmax = (K + 255) / 256;             // keep >= 256 K per slice
+  if (s > kmax) s = kmax;
+  if (s > 64) s = 64;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+
+// Symmetric Gram of the rows/columns of a row-major [R x L] matrix Zs:
+//   trans_k = true : C (L x L) = Zs^T Zs   (sum over rows,   "DIRECT": Z Z^T)
+//   trans_k = false: C (R x R) = Zs Zs^T   (sum over columns, "SMW":   Z^T Z)
+// then C = C / div + shift * I.  W: workspace of gram_workspace_doubles.
+cudaError_t gram_syrk(const double* Zs, int64_t R, int64_t Lc, int64_t ldz, bool sum_over_rows, double div,
+                      double shift, double* C, int64_t ldc, double* W, cudaStream_t st) {
+  const int64_t M = sum_over_rows ? Lc : R;
+  const int64_t K = sum_over_rows ? R : Lc;
+  const int ns = gram_slices(M, K);
+  int64_t kslice = (K + ns - 1) / ns;
+  kslice = (kslice + BK - 1) / BK * BK;
+  dim3 grid((unsigned)((M + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)ns);
+  if (sum_over_rows) {
+    // A(m,k) = Zs[k][m]: m stride 1, k stride ldz (r fastest)
+    Opnd A{Zs, 1, ldz};
+    gemm_dmma_kernel<false, false><<<grid, GT, 0, st>>>(A, A, M, M, K, kslice, W, M, M * M, true, 1.0, 0.0,
+                                                        nullptr, 0);
+  } else {
+    Opnd A{Zs, ldz, 1};
+    gemm_dmma_kernel<true, true><<<grid, GT, 0, st>>>(A, A, M, M, K, kslice, W, M, M * M, true, 1.0, 0.0,
+                                                      nullptr, 0);
+  }
+  syrk_finish_kernel<<<grid_for(M * M), 256, 0, st>>>(W, M, M * M, ns, M, div, shift, C, ldc);
+  return cudaGetLastError();
+}
+
+namespace {
+
+// Recursive blocked Cholesky + triangular inverse (lower):
+//   A (m x m, ld) is overwritten by L; Li (ld) receives L^{-1}; T scratch.
+cudaError_t chol_rec(double* A, double* Li, double* T, int64_t ld, int64_t m, int64_t off, int* info,
+                     cudaStream_t st) {
+  if (m <= 64) {
+    potrf_trtri_small<<<1, 256, 0, st>>>(A, ld, Li, ld, (int)m, info, off);
+    return cudaGetLastError();
+  }
+  int64_t m1 = ((m / 2) + 63) / 64 * 64;
+  if (m1 >= m) m1 = m - 64;
+  const int64_t m2 = m - m1;
+  double* A11 = A;
+  double* A21 = A + m1 * ld;
+  double* A22 = A + m1 * ld + m1;
+  double* L11i = Li;
+  double* L21i = Li + m1 * ld;
+  double* L22i = Li + m1 * ld + m1;
+  cudaError_t e = chol_rec(A11, L11i, T, ld, m1, off, info, st);
+  if (e != cudaSuccess) return e;
+  // T = A21 * L11i^T   (m2 x m1): A(i,k)=A21[i][k], B(j,k)=L11i[j][k]
+  e = gemm_f64(A21, ld, 1, L11i, ld, 1, m2, m1, m1, 1.0, 0.0, T, ld, st);
+  if (e != cudaSuccess) return e;
+  copy2d_kernel<<<grid_for(m2 * m1), 256, 0, st>>>(T, ld, A21, ld, m2, m1);  // L21
+  // A22 -= L21 L21^T
+  e = gemm_f64(A21, ld, 1, A21, ld, 1, m2, m2, m1, -1.0, 1.0, A22, ld, st);
+  if (e != cudaSuccess) return e;
+  e = chol_rec(A22, L22i, T, ld, m2, off + m1, info, st);
+  if (e != cudaSuccess) return e;
+  // T = L21 * L11i  (m2 x m1): A(i,k)=L21[i][k], B(j,k)=L11i[k][j]
+  e = gemm_f64(A21, ld, 1, L11i, 1, ld, m2, m1, m1, 1.0, 0.0, T, ld, st);
+  if (e != cudaSuccess) return e;
+  // L21i = -L22i * T : A(i,k)=L22i[i][k], B(j,k)=T[k][j]
+  e = gemm_f64(L22i, ld, 1, T, 1, ld, m2, m1, m2, -1.0, 0.0, L21i, ld, st);
+  return e;
+}
+
+}  // namespace
+
+// In place: A (m x m SPD, row-major ld) -> A^{-1}.  Li, T: m x m scratch
+// (ld).  *info (device int) receives 1 + index of the first non-positive
+// pivot block, 0 on success.  Returns launch errors only.
+cudaError_t chol_inverse(double* A, double* Li, double* T, int64_t ld, int64_t m, int* info, cudaStream_t st) {
+  zero_kernel<<<grid_for(m * m), 256, 0, st>>>(Li, m, m, ld);
+  cudaError_t e = chol_rec(A, Li, T, ld, m, 0, info, st);
+  if (e != cudaSuccess) return e;
+  // A^{-1} = Li^T Li : C(i,j) = sum_k Li[k][i] Li[k][j]
+  return gemm_f64(Li, 1, ld, Li, 1, ld, m, m, m, 1.0, 0.0, A, ld, st);
+}
+
+}  // namespace gdwd

@@ -1,0 +1,676 @@
+// Fused per-iteration operators of the inexact sGS-ADMM loop
+// (reference pkg/src/gdwd/solver.py:493-555 and subsolvers.py).  Each Op
+// plugs into zmv / ztmv / vmap (zops.cuh).  Expression order follows the
+// reference's numpy expressions so elementwise results round identically
+// (the library is compiled with -fmad=false; numpy never contracts).
+#pragma once
+#include "common.cuh"
+#include "zops.cuh"
+
+namespace gdwd {
+
+constexpr double TINY = 1e-300;  // psqmr.py:14
+constexpr int HIST_W = 16;       // history row: 11 KKT fields + sigma beta reused psqmr eps
+enum HistCol { H_GAP = 8, H_OBJP = 9, H_OBJD = 10, H_SIGMA = 11, H_BETA = 12, H_REUSE = 13, H_PSQMR = 14, H_EPS = 15 };
+
+// Device-resident scalars of one solve.
+struct Scal {
+  int k;          // index of the iteration (body) being executed
+  int stopped;    // 1 => all later kernels of the solve are no-ops
+  int iters_done; // completed iterations
+  int converged;
+  int reuse;      // Step-1c reuse decision of the current iteration
+  int double_count;
+  int error;      // 6: r <= 0 (AssertionError), 7: psqmr needs proximal switch
+  int ps_iters, ps_active, ps_conv, ps_brk, ps_total, need_prox, pad0;
+  double sigma, sigma_next;
+  double sdual;       // sum w^(1/(q+1)) a+^(q/(q+1)) of the last KKT pass
+  double eta[11];     // last KKT residuals (KKT_FIELDS order)
+  double gnorm, wu2, w2;
+  double smw_coef, smw_s2;
+  double ps_tau, ps_rho, ps_theta, ps_alpha, ps_thnew, ps_cA, ps_cB, ps_rhonew, ps_resn;
+  double ys;          // SMW: 1 + ybar^T J^{-1} ybar - 1
+};
+
+struct Dev {
+  int64_t n, d, m;  // m = d + 1
+  double C, q, mu, mu2, zscale, tau, yty, ynorm, kappa, e1, e2, qp1, one_c;
+  double tol_feas, tol_cgap, tol_cap;
+  int max_iter, sched_len;
+  const double *y, *e, *wl, *zy, *jac, *jy;
+  double *r, *xi, *al, *ztw, *rnew, *dr, *ztwb, *s1, *g, *tq;
+  double *u, *rho, *h, *h2, *xb, *x;
+  double *pr, *pres, *pq, *pu, *pd, *pAd, *pAq;
+  const double *eps_tab, *tol_tab, *sched;
+  double* hist;
+  Scal* S;
+};
+
+// ---------------------------------------------------------------------------
+// scalar rules
+// ---------------------------------------------------------------------------
+GDWD_DEV double sigma_rule(double sigma, double ep, double ed) {  // solver.py:343-362
+  if (ep == 0.0 && ed == 0.0) return sigma;
+  const double chi = (ed == 0.0) ? INFINITY : ep / ed;
+  const double ichi = (ep == 0.0) ? INFINITY : ed / ep;
+  const double worst = chi > ichi ? chi : ichi;
+  const double zeta = worst > 500.0 ? 2.2 : (worst > 50.0 ? 1.65 : 1.1);
+  if (chi > 5.0) return sigma * zeta;
+  if (ichi > 5.0) return sigma / zeta;
+  return sigma;
+}
+
+GDWD_DEV double bisect_margin(double a, double sigma, double q, double wt, double tol) {  // subsolvers.py:264-280
+  double lo = 1e-12;
+  double hi = (a > 0.0 ? a : 0.0) + pow((q * wt) / sigma, 1.0 / (q + 2.0)) + 1.0;
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    const double gg = sigma * (mid - a) - (q * wt) / np_pow(mid, q + 1.0);
+    if (fabs(gg) <= tol) return mid;
+    if (gg < 0.0) lo = mid; else hi = mid;
+    if (hi - lo <= 1e-17 * (1.0 > hi ? 1.0 : hi)) break;
+  }
+  return 0.5 * (lo + hi);
+}
+
+// One coordinate of newton_r_sweep (subsolvers.py:321-364): same update and
+// the sweep's two activity-test forms (``/ s**(q+1)`` first, then
+// ``* s**(-(q+1))``).  scalar_form=1 reproduces the scalar newton_r
+// (subsolvers.py:283-318), which uses the first form throughout; *iters
+// receives its iteration count.
+GDWD_DEV double newton_margin(double a, double sigma, double q, double wt, double r0, double tol,
+                              int max_newton = 50, int scalar_form = 0, int* iters = nullptr) {
+  const double mq = -q, qp1 = q + 1.0;
+  const double c = (q * wt) / sigma;
+  double s = r0;
+  double foc = (mq * wt) / np_pow(s, qp1) + sigma * (s - a);
+  int it = 0;
+  if (!(fabs(foc) > tol)) {
+    if (iters) *iters = 0;
+    return s;
+  }
+  for (it = 0; it < max_newton; ++it) {
+    const double sp = np_pow(s, qp1);
+    const double nxt = (s * ((q + 2.0) * c + a * sp)) / ((q + 1.0) * c + sp * s);
+    if (!isfinite(nxt) || nxt <= 0.0) {
+      if (iters) *iters = it;
+      return bisect_margin(a, sigma, q, wt, tol);
+    }
+    s = nxt;
+    foc = scalar_form ? (mq * wt) / np_pow(s, qp1) + sigma * (s - a)
+                      : (mq * wt) * np_pow(s, -qp1) + sigma * (s - a);
+    if (!(fabs(foc) > tol)) {
+      if (iters) *iters = it + 1;
+      return s;
+    }
+  }
+  if (iters) *iters = max_newton;
+  return bisect_margin(a, sigma, q, wt, tol);
+}
+
+GDWD_DEV double np_max0(double x) { return isnan(x) ? x : (x > 0.0 ? x : 0.0); }   // np.maximum(x, 0)
+GDWD_DEV double np_min0(double x) { return isnan(x) ? x : (x < 0.0 ? x : 0.0); }   // np.minimum(x, 0)
+
+// ---------------------------------------------------------------------------
+// KA: h = [-Z(xi - r - a/sigma) + mu^2 u + (mu/sigma) rho ; -y.rhs], fused
+// with Z alpha of the previous iteration (its dual objective, gap and the
+// stopping test, solver.py:293-304,334,548-554) -- one X pass, 2 RHS.
+// ---------------------------------------------------------------------------
+struct OpRhsAlpha {
+  static constexpr int R = 2, NN = 1, ND = 1;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void input(int64_t i, double (&t)[R], double (&na)[NN]) const {
+    const double sig = D.S->sigma_next;
+    t[0] = (D.xi[i] - D.r[i]) - D.al[i] / sig;
+    t[1] = D.al[i];
+    na[0] += D.y[i] * t[0];
+  }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&da)[ND]) const {
+    const double sig = D.S->sigma_next;
+    D.h[j] = (-v[0] + D.mu2 * D.u[j]) + (D.mu / sig) * D.rho[j];
+    da[0] += v[1] * v[1];
+  }
+  GDWD_DEV void fin(const double (&ns)[NN], const double (&ds)[ND]) const {
+    Scal* S = D.S;
+    D.h[D.d] = -ns[0];
+    const int k = S->k;
+    if (k > 0) {
+      const double od = D.kappa * S->sdual - D.zscale * sqrt(ds[0]);
+      const double op = S->eta[9];
+      const double gap = fabs(op - od) / (1.0 + fabs(op) + fabs(od));
+      S->eta[10] = od;
+      S->eta[8] = gap;
+      double* hr = D.hist + (int64_t)(k - 1) * HIST_W;
+      hr[H_OBJD] = od;
+      hr[H_GAP] = gap;
+      const double* e = S->eta;
+      const double ep = fmax(fmax(e[3], e[4]), e[5]);
+      const double ed = fmax(e[6], e[7]);
+      const double ec = fmax(fmax(e[0], e[1]), e[2]);
+      if (fmax(ep, ed) < D.tol_feas && fmin(ec, gap) < D.tol_cgap && fmax(ec, gap) < D.tol_cap) {
+        S->stopped = 1;
+        S->converged = 1;
+        return;
+      }
+    }
+    if (k >= D.max_iter) {
+      S->stopped = 1;
+      return;
+    }
+    S->sigma = S->sigma_next;
+    double* hr = D.hist + (int64_t)k * HIST_W;
+    hr[H_SIGMA] = S->sigma;
+    hr[H_EPS] = D.eps_tab[k];
+    hr[H_REUSE] = 1.0;
+    hr[H_PSQMR] = 0.0;
+  }
+};
+
+// Dense GEMV with the explicit inverse (DIRECT: A^{-1}; replaces the two
+// triangular solves of cholesky.py:60-61).  out = M hv.
+struct OpGemvSolve {
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = false;
+  Dev D;
+  const double* hv;
+  double* out;
+  int pred;  // 1: run only when the Step-1c reuse test failed
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV double wval(int64_t j) const { return hv[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&)[NN]) const { out[i] = dot; }
+  GDWD_DEV void fin(const double (&)[NN]) const {}
+};
+
+// copy src -> dst when the reuse test passed (solver.py:521-522)
+struct OpCopyIfReuse {
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = false;
+  Dev D;
+  const double* src;
+  double* dst;
+  GDWD_DEV bool skip() const { return D.S->stopped || !D.S->reuse; }
+  GDWD_DEV void elem(int64_t i, double (&)[NR]) const { dst[i] = src[i]; }
+  GDWD_DEV void fin(const double (&)[NR]) const {}
+};
+
+// KT: ztw_bar = Z^T w_bar, then c = ztw_bar + y beta_bar + xi - alpha/sigma,
+// r+ = Newton (solver.py:501-504), dr = r+ - r, y.dr (solver.py:507-509).
+struct OpZtNewton {
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV double wval(int64_t j) const { return D.xb[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&na)[NN]) const {
+    const Scal* S = D.S;
+    const double sig = S->sigma, bb = D.xb[D.d];
+    D.ztwb[i] = dot;
+    const double a = ((dot + D.y[i] * bb) + D.xi[i]) - D.al[i] / sig;
+    const double rn = newton_margin(a, sig, D.q, D.wl[i], D.r[i], D.tol_tab[S->k]);
+    D.rnew[i] = rn;
+    const double dri = rn - D.r[i];
+    D.dr[i] = dri;
+    na[0] += D.y[i] * dri;
+  }
+  GDWD_DEV void fin(const double (&ns)[NN]) const { D.h2[D.d] = D.h[D.d] + ns[0]; }
+};
+
+// KC: h2 = h + [Z dr; y.dr], reuse residual ||h2 - A [w_bar; beta_bar]||
+// with A x via Z ztw_bar (solver.py:506-524); one X pass, 2 RHS.
+struct OpDrZtwb {
+  static constexpr int R = 2, NN = 1, ND = 2;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void input(int64_t i, double (&t)[R], double (&)[NN]) const {
+    t[0] = D.dr[i];
+    t[1] = D.ztwb[i];
+  }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&da)[ND]) const {
+    const double bb = D.xb[D.d];
+    const double h2j = D.h[j] + v[0];
+    D.h2[j] = h2j;
+    const double ax = (v[1] + D.mu2 * D.xb[j]) + D.zy[j] * bb;
+    const double rj = h2j - ax;
+    da[0] += rj * rj;
+    da[1] += D.zy[j] * D.xb[j];
+  }
+  GDWD_DEV void fin(const double (&)[NN], const double (&ds)[ND]) const {
+    Scal* S = D.S;
+    const double bb = D.xb[D.d];
+    const double rb = D.h2[D.d] - (ds[1] + D.yty * bb);
+    const double rr = hypot(sqrt(ds[0]), rb);
+    const int reuse = rr <= 5.0 * D.eps_tab[S->k];
+    S->reuse = reuse;
+    if (!reuse) S->double_count += 1;
+    D.hist[(int64_t)S->k * HIST_W + H_REUSE] = reuse ? 1.0 : 0.0;
+  }
+};
+
+struct OpSetReuse {  // use_sgs = False
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void elem(int64_t, double (&)[NR]) const {}
+  GDWD_DEV void fin(const double (&)[NR]) const { D.S->reuse = 1; }
+};
+
+// ztw = Z^T w after a re-solve (solver.py:530)
+struct OpZtStore {
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = false;
+  Dev D;
+  const double* wv;
+  double* out;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV double wval(int64_t j) const { return wv[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&)[NN]) const { out[i] = dot; }
+  GDWD_DEV void fin(const double (&)[NN]) const {}
+};
+
+// Step 2a: g = w - rho/(sigma mu), ||g|| (solver.py:535-536)
+struct OpStep2a {
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void elem(int64_t j, double (&a)[NR]) const {
+    const double gj = D.x[j] - D.rho[j] / (D.S->sigma * D.mu);
+    a[0] += gj * gj;
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const { D.S->gnorm = sqrt(s[0]); }
+};
+
+// Step 2b: ball projection u, rho update (solver.py:537,542), ||w-u||, ||w||
+struct OpStep2b {
+  static constexpr int NR = 2;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void elem(int64_t j, double (&a)[NR]) const {
+    const double sig = D.S->sigma, gn = D.S->gnorm;
+    const double wj = D.x[j];
+    const double gj = wj - D.rho[j] / (sig * D.mu);
+    const double uj = (gn <= D.zscale) ? gj : (D.zscale / gn) * gj;
+    D.u[j] = uj;
+    D.rho[j] = D.rho[j] - ((D.tau * sig) * D.mu) * (wj - uj);
+    const double dw = wj - uj;
+    a[0] += dw * dw;
+    a[1] += wj * wj;
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const {
+    D.S->wu2 = s[0];
+    D.S->w2 = s[1];
+  }
+};
+
+// Step 3 + KKT sample terms (solver.py:533,538-541,311-333) and the
+// per-iteration scalar logic: residuals, sigma update (or replay).
+struct OpStep3 {
+  static constexpr int NR = 10;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void elem(int64_t i, double (&a)[NR]) const {
+    const double sig = D.S->sigma, bet = D.x[D.d];
+    const double C = D.C;
+    const double rr = D.rnew[i];
+    D.r[i] = rr;
+    const double yi = D.y[i], ei = D.e[i], zt = D.ztw[i], ali = D.al[i];
+    const double xv = np_max0((((rr - zt) - yi * bet) + ali / sig) - (C / sig) * ei);
+    D.xi[i] = xv;
+    const double pg = ((zt + yi * bet) + xv) - rr;
+    const double an = ali - (D.tau * sig) * pg;
+    D.al[i] = an;
+    const double wl = D.wl[i];
+    const double s = (D.q * wl) / np_pow(rr, D.qp1);
+    const double d2 = an - s;
+    const double mn = np_min0(an);
+    const double mx = np_max0(an - C * ei);
+    a[0] += yi * an;
+    a[1] += xv * (C * ei - an);
+    a[2] += d2 * d2;
+    a[3] += pg * pg;
+    a[4] += mn * mn;
+    a[5] += mx * mx;
+    a[6] += wl / np_pow(rr, D.q);
+    a[7] += ei * xv;
+    a[8] += np_pow(wl, D.e1) * np_pow(np_max0(an), D.e2);
+    a[9] += (rr <= 0.0) ? 1.0 : 0.0;
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const {
+    Scal* S = D.S;
+    const int k = S->k;
+    const double oc = D.one_c;
+    if (s[9] > 0.0) {
+      S->error = 6;
+      S->stopped = 1;
+      return;
+    }
+    double* e = S->eta;
+    e[0] = fabs(s[0]) / oc;
+    e[1] = fabs(s[1]) / oc;
+    e[2] = s[2] / oc;
+    e[3] = sqrt(s[3]) / oc;
+    e[4] = (D.mu * sqrt(S->wu2)) / oc;
+    e[5] = fmax(sqrt(S->w2) - D.zscale, 0.0) / oc;
+    e[6] = sqrt(s[4]) / oc;
+    e[7] = sqrt(s[5]) / oc;
+    e[9] = s[6] + D.C * s[7];
+    S->sdual = s[8];
+    double* hr = D.hist + (int64_t)k * HIST_W;
+    for (int f = 0; f < 8; ++f) hr[f] = e[f];
+    hr[H_OBJP] = e[9];
+    hr[H_BETA] = D.x[D.d];
+    const double ep = fmax(fmax(e[3], e[4]), e[5]);
+    const double ed = fmax(e[6], e[7]);
+    if (D.sched && k + 1 < D.sched_len) S->sigma_next = D.sched[k + 1];
+    else S->sigma_next = sigma_rule(S->sigma, ep, ed);
+    S->iters_done = k + 1;
+    S->k = k + 1;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// SMW solve (subsolvers.py:127-151) with the explicit G^{-1}
+// ---------------------------------------------------------------------------
+struct OpSmwS1 {  // s1 = Z^T (h/mu^2) + y t2
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = false;
+  Dev D;
+  const double* hv;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV double wval(int64_t j) const { return hv[j] / D.mu2; }
+  GDWD_DEV void row(int64_t i, double dot, double (&)[NN]) const {
+    const double t2 = hv[D.d] / D.yty;
+    D.s1[i] = dot + D.y[i] * t2;
+  }
+  GDWD_DEV void fin(const double (&)[NN]) const {}
+};
+
+struct OpSmwG {  // g = G^{-1} s1 ; ybar.J^{-1}s
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  const double* hv;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV double wval(int64_t j) const { return D.s1[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&na)[NN]) const {
+    D.g[i] = dot;
+    na[0] += (D.y[i] / D.ynorm) * dot;
+  }
+  GDWD_DEV void fin(const double (&ns)[NN]) const {
+    const double t2 = hv[D.d] / D.yty;
+    const double s2 = D.ynorm * t2;
+    const double bd = ns[0] + (-s2);
+    D.S->smw_coef = bd / D.S->ys;
+    D.S->smw_s2 = s2;
+  }
+};
+
+struct OpSmwP {  // p1 = Z v[:n]; x = [t1 - p1/mu^2 ; t2 - p2/|y|^2]
+  static constexpr int R = 1, NN = 1, ND = 1;
+  Dev D;
+  const double* hv;
+  double* out;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void input(int64_t i, double (&t)[R], double (&na)[NN]) const {
+    const double v = D.g[i] - D.S->smw_coef * D.jy[i];
+    t[0] = v;
+    na[0] += D.y[i] * v;
+  }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&)[ND]) const {
+    out[j] = hv[j] / D.mu2 - v[0] / D.mu2;
+  }
+  GDWD_DEV void fin(const double (&ns)[NN], const double (&)[ND]) const {
+    const double vn = (-D.S->smw_s2) - D.S->smw_coef * (-1.0);
+    const double p2 = ns[0] + D.ynorm * vn;
+    out[D.d] = hv[D.d] / D.yty - p2 / D.yty;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// PSQMR (linalg/psqmr.py:27-95) on A = [Z Z^T + mu^2 I, zy; zy^T, y^Ty]
+// with the Jacobi preconditioner (solver.py:428-438).
+// ---------------------------------------------------------------------------
+struct OpApplyZt {  // tq = Z^T v_top
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = false;
+  Dev D;
+  const double* v;
+  int pred;
+  int mode;  // 0: initial residual (predicated on reuse), 1: PSQMR step (needs ps_active)
+  GDWD_DEV bool skip() const {
+    if (D.S->stopped) return true;
+    return mode == 0 ? (pred && D.S->reuse) : !D.S->ps_active;
+  }
+  GDWD_DEV double wval(int64_t j) const { return v[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&)[NN]) const { D.tq[i] = dot; }
+  GDWD_DEV void fin(const double (&)[NN]) const {}
+};
+
+// r = b - A x0 (init, psqmr.py:49) -- pred >= 0 flags; active test skipped
+struct OpInitResidual {
+  static constexpr int R = 1, NN = 1, ND = 1;
+  Dev D;
+  const double* x0;
+  const double* b;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void input(int64_t i, double (&t)[R], double (&)[NN]) const { t[0] = D.tq[i]; }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&da)[ND]) const {
+    const double ax = (v[0] + D.mu2 * x0[j]) + D.zy[j] * x0[D.d];
+    D.pr[j] = b[j] - ax;
+    da[0] += D.zy[j] * x0[j];
+  }
+  GDWD_DEV void fin(const double (&)[NN], const double (&ds)[ND]) const {
+    const double ax = ds[0] + D.yty * x0[D.d];
+    D.pr[D.d] = b[D.d] - ax;
+  }
+};
+
+struct OpPsInit {
+  static constexpr int NR = 3;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  const double* x0;
+  double* xo;
+  int pred;
+  double tolmul;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void elem(int64_t j, double (&a)[NR]) const {
+    xo[j] = x0[j];
+    const double rj = D.pr[j];
+    D.pres[j] = rj;
+    const double qj = rj / D.jac[j];
+    D.pq[j] = qj;
+    D.pd[j] = 0.0;
+    D.pAd[j] = 0.0;
+    a[0] += rj * rj;
+    a[1] += qj * qj;
+    a[2] += rj * qj;
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const {
+    Scal* S = D.S;
+    const double tol = tolmul * D.eps_tab[S->k];
+    S->ps_resn = sqrt(s[0]);
+    S->ps_iters = 0;
+    S->ps_conv = 0;
+    S->ps_brk = 0;
+    if (S->ps_resn <= tol) {
+      S->ps_conv = 1;
+      S->ps_active = 0;
+      return;
+    }
+    S->ps_tau = sqrt(s[1]);
+    S->ps_rho = s[2];
+    S->ps_theta = 0.0;
+    S->ps_active = 1;
+  }
+};
+
+// Aq = A q  (second half of the operator) fused with sigma = q.Aq, alpha
+struct OpPsApply {
+  static constexpr int R = 1, NN = 1, ND = 2;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped || !D.S->ps_active; }
+  GDWD_DEV void input(int64_t i, double (&t)[R], double (&)[NN]) const { t[0] = D.tq[i]; }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&da)[ND]) const {
+    const double qj = D.pq[j];
+    const double aq = (v[0] + D.mu2 * qj) + D.zy[j] * D.pq[D.d];
+    D.pAq[j] = aq;
+    da[0] += D.zy[j] * qj;
+    da[1] += qj * aq;
+  }
+  GDWD_DEV void fin(const double (&)[NN], const double (&ds)[ND]) const {
+    Scal* S = D.S;
+    const double qd = D.pq[D.d];
+    const double aqd = ds[0] + D.yty * qd;
+    D.pAq[D.d] = aqd;
+    const double sg = ds[1] + qd * aqd;
+    if (fabs(sg) < TINY) {
+      S->ps_brk = 1;
+      S->ps_active = 0;
+      return;
+    }
+    S->ps_alpha = S->ps_rho / sg;
+  }
+};
+
+struct OpPsV1 {  // r -= alpha Aq ; u = M^{-1} r ; ||u||, r.u
+  static constexpr int NR = 2;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped || !D.S->ps_active; }
+  GDWD_DEV void elem(int64_t j, double (&a)[NR]) const {
+    const double rj = D.pr[j] - D.S->ps_alpha * D.pAq[j];
+    D.pr[j] = rj;
+    const double uj = rj / D.jac[j];
+    D.pu[j] = uj;
+    a[0] += uj * uj;
+    a[1] += rj * uj;
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const {
+    Scal* S = D.S;
+    const double th = (S->ps_tau > TINY) ? sqrt(s[0]) / S->ps_tau : 0.0;
+    const double c2 = 1.0 / (1.0 + th * th);
+    S->ps_tau = (S->ps_tau * th) * sqrt(c2);
+    S->ps_cA = (c2 * S->ps_theta) * S->ps_theta;
+    S->ps_cB = c2 * S->ps_alpha;
+    S->ps_thnew = th;
+    S->ps_rhonew = s[1];
+  }
+};
+
+struct OpPsV2 {  // d, x, Ad, res updates; ||res||; q = u + beta q
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  double* xo;
+  double tolmul;
+  int max_steps;
+  GDWD_DEV bool skip() const { return D.S->stopped || !D.S->ps_active; }
+  GDWD_DEV void elem(int64_t j, double (&a)[NR]) const {
+    const Scal* S = D.S;
+    const double cA = S->ps_cA, cB = S->ps_cB;
+    const double qj = D.pq[j];
+    const double dj = cA * D.pd[j] + cB * qj;
+    D.pd[j] = dj;
+    xo[j] = xo[j] + dj;
+    const double adj = cA * D.pAd[j] + cB * D.pAq[j];
+    D.pAd[j] = adj;
+    const double rs = D.pres[j] - adj;
+    D.pres[j] = rs;
+    a[0] += rs * rs;
+    D.pq[j] = D.pu[j] + (S->ps_rhonew / S->ps_rho) * qj;
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const {
+    Scal* S = D.S;
+    S->ps_iters += 1;
+    S->ps_resn = sqrt(s[0]);
+    if (S->ps_resn <= tolmul * D.eps_tab[S->k]) {
+      S->ps_conv = 1;
+      S->ps_active = 0;
+      return;
+    }
+    if (fabs(S->ps_rho) < TINY) {
+      S->ps_brk = 1;
+      S->ps_active = 0;
+      return;
+    }
+    S->ps_rho = S->ps_rhonew;
+    S->ps_theta = S->ps_thnew;
+    if (S->ps_iters >= max_steps) S->ps_active = 0;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// setup / seam ops
+// ---------------------------------------------------------------------------
+struct OpPlainZ {  // out = Z t (+ n-dot y.t into *dot)
+  static constexpr int R = 1, NN = 1, ND = 1;
+  const double* t;
+  const double* y;
+  double* out;
+  double* dot;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV void input(int64_t i, double (&tv)[R], double (&na)[NN]) const {
+    tv[0] = t[i];
+    if (y) na[0] += y[i] * t[i];
+  }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&)[ND]) const { out[j] = v[0]; }
+  GDWD_DEV void fin(const double (&ns)[NN], const double (&)[ND]) const {
+    if (dot) *dot = ns[0];
+  }
+};
+
+struct OpPlainZt {  // out = Z^T w
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = false;
+  const double* w;
+  double* out;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV double wval(int64_t j) const { return w[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&)[NN]) const { out[i] = dot; }
+  GDWD_DEV void fin(const double (&)[NN]) const {}
+};
+
+struct OpJyG {  // jy = G^{-1} (y/|y|) ; ys = 1 + (y/|y|).jy - 1  (subsolvers.py:114-117)
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = true;
+  const double* y;
+  double ynorm;
+  double* jy;
+  Scal* S;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV double wval(int64_t j) const { return y[j] / ynorm; }
+  GDWD_DEV void row(int64_t i, double dot, double (&na)[NN]) const {
+    jy[i] = dot;
+    na[0] += (y[i] / ynorm) * dot;
+  }
+  GDWD_DEV void fin(const double (&ns)[NN]) const { S->ys = 1.0 + ns[0] - 1.0; }
+};
+
+struct OpNewtonSweep {  // standalone newton_r_sweep / newton_r (subsolvers.py:283-364)
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = false;
+  const double *a, *w, *r0;
+  double* out;
+  int* iters;
+  double sigma, q, tol;
+  int max_newton, scalar_form;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV void elem(int64_t i, double (&)[NR]) const {
+    int it = 0;
+    out[i] = newton_margin(a[i], sigma, q, w[i], r0[i], tol, max_newton, scalar_form, &it);
+    if (iters) iters[i] = it;
+  }
+  GDWD_DEV void fin(const double (&)[NR]) const {}
+};
+
+}  // namespace gdwd

@@ -1,0 +1,276 @@
+// Streaming fp64 matvec kernels over a row-major [rows x cols] matrix X
+// whose rows are samples (X = Z~^T stored sample-major, i.e. the CSC values
+// array of a fully dense Z~), plus a generic fused map-reduce.
+//
+//   zmv  : v = X^T t   (n -> d, "Z~ t";   reference scipy csc_matvec)
+//   ztmv : v = X w     (d -> n, "Z~^T w"; reference scipy csr_matvec)
+//   vmap : elementwise update + K fused sums
+//
+// Each kernel is a template over an Op functor that supplies the input
+// vector on the fly (no materialised temporaries), consumes the result in an
+// epilogue (the per-feature or per-sample update the reference does next),
+// and contributes to fused reductions.  Reductions are deterministic
+// (common.cuh); the final scalar logic runs in the last-arriving CTA.
+//
+// HBM layout: rows are padded to ld (multiple of 2 doubles, zero-filled) so
+// every thread streams 16-byte double2 loads with L1::no_allocate.
+#pragma once
+#include "common.cuh"
+
+namespace gdwd {
+
+struct MatView {
+  const double* a;
+  int64_t rows, cols, ld;
+};
+
+struct Scratch {
+  double* part;       // per-segment vector partials
+  double* npart;      // per-CTA n-sum partials
+  double* tpart;      // per-tile d-sum partials
+  unsigned* tickets;  // zero-initialised ticket counters
+};
+
+// ---------------------------------------------------------------------------
+// zmv: grid (tiles, segs); CTA of 256 threads covers 512 columns (2 per
+// thread) and a contiguous segment of rows.  Input t is staged in shared
+// memory STAGE rows at a time.
+// ---------------------------------------------------------------------------
+constexpr int ZMV_THREADS = 256;
+constexpr int ZMV_TILE = 2 * ZMV_THREADS;
+constexpr int ZMV_STAGE = 512;
+
+struct ZmvGeom {
+  int tiles, segs;
+  int64_t seg_len;
+  int64_t ldp;  // leading dim of partial rows (>= cols, even)
+};
+
+template <class Op>
+__global__ void __launch_bounds__(ZMV_THREADS) zmv_kernel(Op op, MatView X, ZmvGeom g, Scratch s) {
+  constexpr int R = Op::R, NN = Op::NN, ND = Op::ND;
+  if (op.skip()) return;
+  __shared__ double ts[R][ZMV_STAGE];
+  __shared__ double red[(ZMV_THREADS / 32) * (NN > ND ? NN : ND)];
+  const int tile = blockIdx.x, seg = blockIdx.y;
+  const int64_t s0 = (int64_t)seg * g.seg_len;
+  const int64_t s1 = (s0 + g.seg_len < X.rows) ? s0 + g.seg_len : X.rows;
+  const int64_t j0 = (int64_t)tile * ZMV_TILE + 2 * threadIdx.x;
+  const bool colok = j0 < X.cols;
+
+  double acc[R][2];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = 0.0;
+  double nacc[NN];
+#pragma unroll
+  for (int k = 0; k < NN; ++k) nacc[k] = 0.0;
+
+  for (int64_t c0 = s0; c0 < s1; c0 += ZMV_STAGE) {
+    const int cn = (int)((c0 + ZMV_STAGE < s1) ? ZMV_STAGE : s1 - c0);
+    __syncthreads();
+    for (int ii = threadIdx.x; ii < cn; ii += ZMV_THREADS) {
+      double tv[R];
+      double na[NN];
+#pragma unroll
+      for (int k = 0; k < NN; ++k) na[k] = 0.0;
+      op.input(c0 + ii, tv, na);
+#pragma unroll
+      for (int r = 0; r < R; ++r) ts[r][ii] = tv[r];
+#pragma unroll
+      for (int k = 0; k < NN; ++k) nacc[k] += na[k];
+    }
+    __syncthreads();
+    if (colok) {
+      const double* p = X.a + c0 * X.ld + j0;
+      int ii = 0;
+      for (; ii + 4 <= cn; ii += 4) {
+        double2 z[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) z[u] = ld_stream2(p + (int64_t)(ii + u) * X.ld);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const double t = ts[r][ii + u];
+            acc[r][0] += z[u].x * t;
+            acc[r][1] += z[u].y * t;
+          }
+        }
+      }
+      for (; ii < cn; ++ii) {
+        const double2 z = ld_stream2(p + (int64_t)ii * X.ld);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double t = ts[r][ii];
+          acc[r][0] += z.x * t;
+          acc[r][1] += z.y * t;
+        }
+      }
+    }
+  }
+  if (colok) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      *reinterpret_cast<double2*>(s.part + ((int64_t)seg * R + r) * g.ldp + j0) = make_double2(acc[r][0], acc[r][1]);
+  }
+  if (tile == 0) {
+    block_sum<NN>(nacc, red);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < NN; ++k) s.npart[(int64_t)seg * NN + k] = nacc[k];
+    }
+  }
+  if (!last_arrival(&s.tickets[tile], gridDim.y)) return;
+
+  double dacc[ND];
+#pragma unroll
+  for (int k = 0; k < ND; ++k) dacc[k] = 0.0;
+  if (colok) {
+    double v0[R], v1[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v0[r] = v1[r] = 0.0;
+    for (int sg = 0; sg < (int)gridDim.y; ++sg) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double2 pv = __ldcg(reinterpret_cast<const double2*>(s.part + ((int64_t)sg * R + r) * g.ldp + j0));
+        v0[r] += pv.x;
+        v1[r] += pv.y;
+      }
+    }
+    op.epi(j0, v0, dacc);
+    if (j0 + 1 < X.cols) op.epi(j0 + 1, v1, dacc);
+  }
+  block_sum<ND>(dacc, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < ND; ++k) s.tpart[(int64_t)tile * ND + k] = dacc[k];
+  }
+  if (!last_arrival(&s.tickets[gridDim.x], gridDim.x)) return;
+  if (threadIdx.x == 0) {
+    double nsum[NN], dsum[ND];
+    sum_partials<NN>(s.npart, gridDim.y, nsum);
+    sum_partials<ND>(s.tpart, gridDim.x, dsum);
+    op.fin(nsum, dsum);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ztmv: grid (chunks, sblocks); CTA of 256 threads (8 warps).  The chunk of
+// w (<= ZT_CW columns) is staged in shared memory; each warp computes full
+// row dots over the chunk for its samples; with several chunks the last CTA
+// of a sample block sums the chunk partials in fixed order.  The per-sample
+// epilogue then runs one sample per thread.
+// ---------------------------------------------------------------------------
+constexpr int ZT_THREADS = 256;
+constexpr int ZT_CW = 4096;
+
+struct ZtGeom {
+  int chunks, sblocks;
+  int cw;   // chunk width (even)
+  int sb;   // samples per block (multiple of 8, <= 256)
+};
+
+template <class Op>
+__global__ void __launch_bounds__(ZT_THREADS) ztmv_kernel(Op op, MatView X, ZtGeom g, Scratch s) {
+  constexpr int NN = Op::NN;
+  if (op.skip()) return;
+  extern __shared__ double zsm[];
+  double* ws = zsm;          // cw
+  double* sdot = zsm + g.cw;  // sb
+  __shared__ double red[(ZT_THREADS / 32) * NN];
+  const int c = blockIdx.x, sbk = blockIdx.y;
+  const int64_t c0 = (int64_t)c * g.cw;
+  const int64_t clen = (c0 + g.cw < X.ld) ? g.cw : X.ld - c0;
+  for (int jj = threadIdx.x; jj < clen; jj += ZT_THREADS) {
+    const int64_t j = c0 + jj;
+    ws[jj] = (j < X.cols) ? op.wval(j) : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i0 = (int64_t)sbk * g.sb;
+  const int nsb = (int)((i0 + g.sb < X.rows) ? g.sb : X.rows - i0);
+  for (int li = warp; li < nsb; li += ZT_THREADS / 32) {
+    const double* p = X.a + (i0 + li) * X.ld + c0;
+    double acc = 0.0;
+    int64_t jj = 2 * lane;
+    for (; jj + 3 * 64 < clen; jj += 4 * 64) {
+      double2 z[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) z[u] = ld_stream2(p + jj + u * 64);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc += z[u].x * ws[jj + u * 64];
+        acc += z[u].y * ws[jj + u * 64 + 1];
+      }
+    }
+    for (; jj < clen; jj += 64) {
+      const double2 z = ld_stream2(p + jj);
+      acc += z.x * ws[jj];
+      acc += z.y * ws[jj + 1];
+    }
+    double a1[1] = {acc};
+    warp_sum<1>(a1);
+    if (lane == 0) {
+      if (gridDim.x == 1) sdot[li] = a1[0];
+      else s.part[(int64_t)c * X.rows + i0 + li] = a1[0];
+    }
+  }
+  double dot = 0.0;
+  if (gridDim.x > 1) {
+    if (!last_arrival(&s.tickets[sbk], gridDim.x)) return;
+    if (threadIdx.x < nsb) {
+      for (int cc = 0; cc < (int)gridDim.x; ++cc) dot += ld_cg(s.part + (int64_t)cc * X.rows + i0 + threadIdx.x);
+    }
+  } else {
+    __syncthreads();
+    if (threadIdx.x < nsb) dot = sdot[threadIdx.x];
+  }
+  double nacc[NN];
+#pragma unroll
+  for (int k = 0; k < NN; ++k) nacc[k] = 0.0;
+  if (threadIdx.x < nsb) op.row(i0 + threadIdx.x, dot, nacc);
+  if (!Op::HAS_FIN) return;
+  block_sum<NN>(nacc, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NN; ++k) s.npart[(int64_t)sbk * NN + k] = nacc[k];
+  }
+  // global ticket lives after the per-sblock slots
+  if (!last_arrival(&s.tickets[(gridDim.x > 1 ? gridDim.y : 0)], gridDim.y)) return;
+  if (threadIdx.x == 0) {
+    double nsum[NN];
+    sum_partials<NN>(s.npart, gridDim.y, nsum);
+    op.fin(nsum);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// vmap: grid-stride elementwise pass with NR fused sums.
+// ---------------------------------------------------------------------------
+constexpr int VM_THREADS = 256;
+
+template <class Op>
+__global__ void __launch_bounds__(VM_THREADS) vmap_kernel(Op op, int64_t len, Scratch s) {
+  constexpr int NR = Op::NR;
+  if (op.skip()) return;
+  __shared__ double red[(VM_THREADS / 32) * NR];
+  double acc[NR];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) acc[k] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)VM_THREADS + threadIdx.x; i < len; i += (int64_t)gridDim.x * VM_THREADS)
+    op.elem(i, acc);
+  if (!Op::HAS_FIN) return;
+  block_sum<NR>(acc, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) s.npart[(int64_t)blockIdx.x * NR + k] = acc[k];
+  }
+  if (!last_arrival(&s.tickets[0], gridDim.x)) return;
+  if (threadIdx.x == 0) {
+    double sum[NR];
+    sum_partials<NR>(s.npart, gridDim.x, sum);
+    op.fin(sum);
+  }
+}
+
+}  // namespace gdwd

@@ -1,0 +1,181 @@
+"""Generate the golden fixtures by running the REFERENCE package itself.
+
+Run in the build container (the reference is importable from
+/root/reference/pkg/src; it does not exist on the GPU box):
+
+    python tests/golden/make_golden.py            # everything
+    python tests/golden/make_golden.py --quick    # skip the 2000-iteration c1 run
+
+Outputs (committed, small):
+  kat.json           SPEC.md known-answer tests evaluated by the reference
+  traj_<case>.npz    per-iteration trajectories of sgs_admm_solve on seeded
+                     problems (all three backends; full vectors for tiny
+                     cases, scalars + sampled coordinates for larger ones)
+  c1_full.npz        BASELINE config 1 (d=2000, n=1000), 2000 iterations:
+                     scalar history (incl. the sigma trace), first 20 iterates
+                     of w and alpha, final state
+
+Inputs are regenerated from paper_2305_12019_b200.synth (pure function of the
+seed); each fixture stores a checksum of Z~ so a generator change is caught.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import math
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import gdwd  # noqa: E402  (the reference)
+from gdwd.linalg import SparseMatrixCSC as RefCSC  # noqa: E402
+from gdwd.linalg import cholesky_factorize, cholesky_solve, lanczos_topk, psqmr  # noqa: E402
+
+from paper_2305_12019_b200 import synth  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+# (name, synth config, d, n, backend, max_iter, full vectors?)
+CASES = [
+    ("tiny_direct", "c1", 60, 40, "direct", 80, True),
+    ("tiny_smw2", "c2", 90, 16, "smw2", 80, True),
+    ("tiny_iter", "c1", 70, 50, "iterative", 80, True),
+    ("tiny_iter_c4gen", "c2", 64, 40, "iterative", 60, True),
+    ("tiny_direct_q2", "c3", 40, 120, "direct", 80, True),
+    ("smw2_natural", "c2", 6000, 200, "auto", 40, False),
+    ("iter_natural", "c1", 6000, 1500, "auto", 25, False),
+    ("direct_q4", "c5", 300, 900, "auto", 60, False),
+]
+SAMPLE = 64  # sampled coordinates per vector for the non-full cases
+
+
+def z_checksum(values: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(values).tobytes()).hexdigest()[:16]
+
+
+def to_ref(prob):
+    z = prob.z_tilde
+    rz = RefCSC(nrows=z.nrows, ncols=z.ncols, colptr=z.colptr, rowidx=z.rowidx, values=z.values)
+    return gdwd.ProblemData(z_tilde=rz, y=prob.y, e=prob.e, weights=prob.weights, C=prob.C, q=prob.q,
+                            z_scale=prob.z_scale)
+
+
+def run_case(name, cfgname, d, n, backend, max_iter, full, seed=0):
+    cfg = synth.CONFIGS[cfgname].scaled(d=d, n=n)
+    prob = synth.make_problem(cfg, seed)
+    rp = to_ref(prob)
+    conf = gdwd.SolverConfig(q=prob.q, max_iter=max_iter, backend=gdwd.Backend(backend))
+    rows, vecs = [], {k: [] for k in ("w", "u", "rho", "r", "xi", "alpha")}
+    rng = np.random.default_rng(1234)
+    idx_d = np.sort(rng.choice(d, min(SAMPLE, d), replace=False))
+    idx_n = np.sort(rng.choice(n, min(SAMPLE, n), replace=False))
+
+    def cb(st, res):
+        rows.append([res.eta_c1, res.eta_c2, res.eta_c3, res.eta_p1, res.eta_p2, res.eta_p3, res.eta_d1,
+                     res.eta_d2, res.eta_gap, res.obj_primal, res.obj_dual, st.sigma, st.beta, st.iter,
+                     float(np.linalg.norm(st.w)), float(np.linalg.norm(st.alpha))])
+        for k in vecs:
+            v = np.array(getattr(st, k), copy=True)
+            if not full:
+                v = v[idx_d] if k in ("w", "u", "rho") else v[idx_n]
+            vecs[k].append(v)
+
+    t0 = time.perf_counter()
+    res = gdwd.sgs_admm_solve(rp, conf, callback=cb)
+    dt = time.perf_counter() - t0
+    out = dict(hist=np.array(rows), idx_d=idx_d, idx_n=idx_n, iterations=res.iterations,
+               converged=int(res.converged), double_count=res.double_count, psqmr_total=res.psqmr_total,
+               backend=res.backend_used.value, final_w=res.final_state.w, final_beta=res.final_state.beta,
+               z_sha=z_checksum(prob.z_tilde.values), d=d, n=n, seed=seed, cfg=cfgname, max_iter=max_iter,
+               full=int(full), train_error=res.train_error_pct)
+    for k, v in vecs.items():
+        out["it_" + k] = np.array(v)
+    np.savez_compressed(OUT / f"traj_{name}.npz", **out)
+    print(f"{name}: backend={res.backend_used.value} iters={res.iterations} doubles={res.double_count} "
+          f"psqmr={res.psqmr_total} conv={res.converged} {dt:.1f}s", flush=True)
+
+
+def run_c1_full():
+    prob = synth.make_problem(synth.CONFIGS["c1"], 0)
+    rp = to_ref(prob)
+    conf = gdwd.SolverConfig(q=1.0, max_iter=2000)
+    rows, w20, a20 = [], [], []
+
+    def cb(st, res):
+        rows.append([res.eta_c1, res.eta_c2, res.eta_c3, res.eta_p1, res.eta_p2, res.eta_p3, res.eta_d1,
+                     res.eta_d2, res.eta_gap, res.obj_primal, res.obj_dual, st.sigma, st.beta, st.iter,
+                     float(np.linalg.norm(st.w)), float(np.linalg.norm(st.alpha))])
+        if st.iter <= 20:
+            w20.append(np.array(st.w, copy=True))
+            a20.append(np.array(st.alpha, copy=True))
+
+    t0 = time.perf_counter()
+    res = gdwd.sgs_admm_solve(rp, conf, callback=cb)
+    dt = time.perf_counter() - t0
+    fs = res.final_state
+    np.savez_compressed(OUT / "c1_full.npz", hist=np.array(rows), w20=np.array(w20), alpha20=np.array(a20),
+                        final_w=fs.w, final_beta=fs.beta, final_r=fs.r, final_xi=fs.xi, final_alpha=fs.alpha,
+                        iterations=res.iterations, converged=int(res.converged), double_count=res.double_count,
+                        z_sha=z_checksum(prob.z_tilde.values), solve_time=dt,
+                        obj_primal=res.final_residuals.obj_primal)
+    print(f"c1_full: iters={res.iterations} conv={res.converged} doubles={res.double_count} {dt:.1f}s", flush=True)
+
+
+def kats():
+    """SPEC.md KATs evaluated by the reference."""
+    k = {}
+    k["newton_r"] = [[a, s, q, w, r0] + list(gdwd.newton_r(a, s, q, w, r0))
+                     for (a, s, q, w, r0) in [(0.0, 1.0, 1.0, 1.0, 1.0), (0.0, 2.0, 1.0, 1.0, 1.0),
+                                              (10.0, 1.0, 1.0, 1.0, 1.0), (-3.0, 5.0, 2.0, 0.5, 1.0),
+                                              (2.0, 100.0, 4.0, 0.3, 0.5), (0.5, 1e6, 1.0, 1.0, 1.0)]]
+    k["select_solver"] = [[n, d, gdwd.select_solver(n, d).value] for (n, d) in
+                          [(100, 100), (1000, 10000), (30000, 300000), (1000, 5000), (1000, 5001), (1000, 5000 + 1),
+                           (2500, 12501), (2501, 20000), (1000, 5005), (1001, 5005), (1, 1)]]
+    k["update_sigma"] = [[s, p, dd, gdwd.update_sigma(s, p, dd)] for (s, p, dd) in
+                         [(1.0, 10.0, 1.0), (1.0, 1.0, 1.0), (1.0, 600.0, 1.0), (1.0, 1.0, 10.0), (2.0, 0.0, 0.0),
+                          (3.0, 1e-9, 0.0), (3.0, 0.0, 1e-9), (1.0, 60.0, 1.0), (1.0, 1.0, 60.0)]]
+    y = np.array([1.0] * 90 + [-1.0] * 10)
+    k["compute_weights"] = {"q1": gdwd.compute_weights(y, 1.0).tolist()[:1] + gdwd.compute_weights(y, 1.0).tolist()[-1:],
+                            "q2": gdwd.compute_weights(y, 2.0).tolist()[:1] + gdwd.compute_weights(y, 2.0).tolist()[-1:]}
+    f = cholesky_factorize(np.array([[4.0, 2.0], [2.0, 3.0]]))
+    k["cholesky"] = {"R": f.r_factor.tolist(), "solve": cholesky_solve(f, np.array([6.0, 5.0])).tolist()}
+    pr = psqmr(lambda v: np.array([1.0, 2.0, 3.0]) * v, np.array([1.0, 2.0, 3.0]), tol=1e-12)
+    k["psqmr_diag"] = {"x": pr.x.tolist(), "iterations": pr.iterations, "converged": pr.converged}
+    rng = np.random.default_rng(7)
+    B = rng.standard_normal((50, 50))
+    S = B @ B.T + 50 * np.eye(50)
+    b = rng.standard_normal(50)
+    M = np.diag(S).copy()
+    pr2 = psqmr(lambda v: S @ v, b, precond=lambda v: v / M, tol=1e-10, max_iter=200)
+    k["psqmr_spd50"] = {"seed": 7, "x": pr2.x.tolist(), "iterations": pr2.iterations,
+                        "converged": pr2.converged, "residual_norm": pr2.residual_norm}
+    pe = lanczos_topk(lambda v: np.array([5.0, 4.0, 3.0, 2.0, 1.0]) * v, 5, 2)
+    k["lanczos_diag"] = {"eigenvalues": pe.eigenvalues.tolist()}
+    (OUT / "kat.json").write_text(json.dumps(k, indent=1))
+    print("kat.json written")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default=None)
+    a = ap.parse_args()
+    if a.only in (None, "kat"):
+        kats()
+    for c in CASES:
+        if a.only in (None, c[0]):
+            run_case(*c)
+    if not a.quick and a.only in (None, "c1"):
+        run_c1_full()
+
+
+if __name__ == "__main__":
+    main()

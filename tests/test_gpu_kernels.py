@@ -1,0 +1,93 @@
+"""GPU kernel parity through the C ABI (run on a B200: pytest -m gpu)."""
+
+import numpy as np
+import pytest
+
+import paper_2305_12019_b200 as G
+from conftest import load_kat, relerr
+from oracle import gdwd_oracle as O
+from paper_2305_12019_b200 import linalg as L
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("d,n", [(2000, 1000), (1001, 37), (9000, 300), (17, 5000), (64, 1)])
+def test_matvec_both_directions(d, n):
+    rng = np.random.default_rng(d * 7 + n)
+    S = rng.standard_normal((n, d))  # sample-major [n, d] = CSC values of Z (d x n)
+    z = G.SparseMatrixCSC.from_dense_samples(S)
+    t = rng.standard_normal(n)
+    w = rng.standard_normal(d)
+    ones = np.ones(n)
+    dp = G.DeviceProblem(G.ProblemData(z, ones, ones, ones, 1.0, 1.0, 1.0))
+    try:
+        assert relerr(dp.matvec(t), S.T @ t) < 1e-13
+        assert relerr(dp.rmatvec(w), S @ w) < 1e-13
+        # deterministic: same bits twice
+        assert np.array_equal(dp.matvec(t), dp.matvec(t))
+        assert np.array_equal(dp.rmatvec(w), dp.rmatvec(w))
+    finally:
+        dp.close()
+
+
+@pytest.mark.parametrize("rows,cols", [(1000, 300), (130, 2001), (5, 70)])
+def test_gram_dmma(rows, cols):
+    rng = np.random.default_rng(rows + cols)
+    X = rng.standard_normal((rows, cols))
+    g1 = L.gram(X, True, div=1.0, shift=0.5)
+    assert relerr(g1, X.T @ X + 0.5 * np.eye(cols)) < 1e-13
+    g2 = L.gram(X, False, div=4.0, shift=1.0)
+    assert relerr(g2, X @ X.T / 4.0 + np.eye(rows)) < 1e-13
+    assert np.array_equal(g1, g1.T)
+
+
+@pytest.mark.parametrize("m", [2, 63, 64, 65, 300, 2001])
+def test_cholesky_inverse(m):
+    rng = np.random.default_rng(m)
+    B = rng.standard_normal((m, m))
+    S = B @ B.T + m * np.eye(m)
+    inv = L.cholesky_inverse(S)
+    assert relerr(inv, np.linalg.inv(S)) < 1e-12
+
+
+def test_cholesky_kat_and_indefinite():
+    S = np.array([[4.0, 2.0], [2.0, 3.0]])
+    x = L.cholesky_inverse(S) @ np.array([6.0, 5.0])
+    assert np.allclose(x, load_kat()["cholesky"]["solve"], rtol=0, atol=1e-14)
+    with pytest.raises(G.IndefiniteMatrixError):
+        L.cholesky_inverse(np.array([[1.0, 2.0], [2.0, 1.0]]))
+
+
+def test_newton_kats():
+    for a, s, q, w, r0, root, its in load_kat()["newton_r"]:
+        got, git = G.newton_r(a, s, q, w, r0)
+        assert got == pytest.approx(root, rel=1e-15, abs=0) and git == its
+
+
+@pytest.mark.parametrize("q", [1.0, 2.0, 4.0, 0.5])
+def test_newton_sweep_vs_oracle(q):
+    rng = np.random.default_rng(int(q * 10))
+    n = 20000
+    a = rng.standard_normal(n) * 3
+    r0 = rng.random(n) * 2 + 0.05
+    w = rng.random(n) + 0.1
+    for sigma in (0.5, 10.0, 3e5):
+        ref = O.newton_sweep(a, sigma, q, w, r0, tol=1e-6)
+        got = G.newton_r_sweep(a, sigma, q, w, r0, tol=1e-6)
+        assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-13
+
+
+def test_psqmr_kats():
+    k = load_kat()
+    p = L.psqmr_dense(np.diag([1.0, 2.0, 3.0]), np.array([1.0, 2.0, 3.0]), tol=1e-12)
+    assert p.iterations == k["psqmr_diag"]["iterations"] and p.converged
+    assert np.allclose(p.x, k["psqmr_diag"]["x"], rtol=0, atol=1e-14)
+    rng = np.random.default_rng(7)
+    B = rng.standard_normal((50, 50))
+    S = B @ B.T + 50 * np.eye(50)
+    b = rng.standard_normal(50)
+    M = np.diag(S).copy()
+    p2 = L.psqmr_dense(S, b, precond_diag=M, tol=1e-10, max_iter=200)
+    ref = k["psqmr_spd50"]
+    assert p2.iterations == ref["iterations"] and p2.converged
+    assert relerr(p2.x, ref["x"]) < 1e-12

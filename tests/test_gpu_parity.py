@@ -1,0 +1,118 @@
+"""Solver parity on the GPU against the reference's own trajectories
+(tests/golden, produced by running the reference) and the CPU oracle.
+
+Tolerances (BASELINE.json north_star): the first 20 iterates agree to 1e-9
+relative in fp64; final w, beta and objective to 1e-6 relative under the
+same stopping rule (with the sigma schedule replayed: the sigma rule is
+chaotic once residuals reach rounding level)."""
+
+import numpy as np
+import pytest
+
+import paper_2305_12019_b200 as G
+from conftest import GOLDEN, TRAJ_CASES, load_traj, problem_for, relerr
+
+pytestmark = pytest.mark.gpu
+
+TOL20 = 1e-9
+BACKEND = {"tiny_direct": "direct", "tiny_smw2": "smw2", "tiny_iter": "iterative", "tiny_iter_c4gen": "iterative",
+           "tiny_direct_q2": "direct"}
+
+
+def run_traj(prob, cfg, full, idx_d=None, idx_n=None, **kw):
+    rows, vecs = [], {k: [] for k in ("w", "u", "rho", "r", "xi", "alpha")}
+
+    def cb(st, res):
+        rows.append([getattr(res, f) for f in G.solver.KKT_FIELDS] + [st.sigma, st.beta])
+        for k in vecs:
+            v = np.array(getattr(st, k), copy=True)
+            if not full:
+                v = v[idx_d] if k in ("w", "u", "rho") else v[idx_n]
+            vecs[k].append(v)
+
+    out = G.sgs_admm_solve(prob, cfg, callback=cb, **kw)
+    return out, np.array(rows), {k: np.array(v) for k, v in vecs.items()}
+
+
+@pytest.mark.parametrize("case", TRAJ_CASES)
+def test_trajectory_first20(case):
+    tr = load_traj(case)
+    prob = problem_for(tr)
+    cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]),
+                         backend=G.Backend(BACKEND.get(case, "auto")))
+    out, h, vecs = run_traj(prob, cfg, bool(tr["full"]), tr["idx_d"], tr["idx_n"])
+    assert out.backend_used.value == str(tr["backend"])
+    k = min(20, len(tr["hist"]))
+    for key in ("w", "u", "rho", "r", "xi", "alpha"):
+        ref = tr["it_" + key][:k]
+        got = vecs[key][:k]
+        for i in range(k):
+            assert relerr(got[i], ref[i]) < TOL20, (key, i)
+    ref_h = tr["hist"][:k]
+    # KKT scalars, sigma, beta
+    # (the normalised residuals can sit at rounding level, e.g. eta_c1 =
+    # |y.alpha|/(1+C) ~ 1e-14, hence the absolute floor)
+    for c in list(range(11)) + [11, 12]:
+        err = np.abs(h[:k, c] - ref_h[:, c])
+        assert np.all(err <= 1e-9 * np.abs(ref_h[:, c]) + 1e-11), (c, err.max())
+    assert np.array_equal(h[:k, 11], ref_h[:, 11])  # sigma sequence identical
+
+
+@pytest.mark.parametrize("case", TRAJ_CASES)
+def test_full_run_counters(case):
+    """Whole short runs: same iteration count, backend; double/psqmr counts
+    within rounding-induced noise; final w within 1e-6 (sigma replayed)."""
+    tr = load_traj(case)
+    prob = problem_for(tr)
+    cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]),
+                         backend=G.Backend(BACKEND.get(case, "auto")))
+    out = G.sgs_admm_solve(prob, cfg, sigma_schedule=tr["hist"][:, 11])
+    assert out.iterations == int(tr["iterations"])
+    assert out.converged == bool(tr["converged"])
+    assert abs(out.double_count - int(tr["double_count"])) <= max(1, int(tr["double_count"]) // 50)
+    assert relerr(out.final_state.w, tr["final_w"]) < 1e-6
+    assert abs(out.final_state.beta - float(tr["final_beta"])) <= 1e-6 * max(1.0, abs(float(tr["final_beta"])))
+
+
+def test_graph_mode_equals_callback_mode():
+    tr = load_traj("tiny_direct")
+    prob = problem_for(tr)
+    cfg = G.SolverConfig(q=prob.q, max_iter=60, backend=G.Backend.DIRECT)
+    a = G.sgs_admm_solve(prob, cfg, use_graph=True)
+    b = G.sgs_admm_solve(prob, cfg, use_graph=False)
+    c, _, _ = run_traj(prob, cfg, True)
+    for o in (b, c):
+        assert np.array_equal(a.final_state.w, o.final_state.w)
+        assert np.array_equal(a.final_state.alpha, o.final_state.alpha)
+        assert a.iterations == o.iterations and a.double_count == o.double_count
+
+
+def test_c1_first20_and_replayed_final():
+    """BASELINE config 1 (d=2000, n=1000, q=1, C=1, 2000 iterations)."""
+    f = GOLDEN / "c1_full.npz"
+    if not f.exists():
+        pytest.skip("c1_full fixture not generated")
+    g = dict(np.load(f))
+    from paper_2305_12019_b200 import synth
+
+    prob = synth.make_problem(synth.CONFIGS["c1"], 0)
+    cfg = G.SolverConfig(q=1.0, max_iter=2000)
+    w20, a20 = [], []
+
+    def cb(st, res):
+        if st.iter <= 20:
+            w20.append(st.w.copy())
+            a20.append(st.alpha.copy())
+        elif st.iter > 20:
+            raise StopIteration
+
+    with pytest.raises(StopIteration):
+        G.sgs_admm_solve(prob, cfg, callback=cb)
+    for i in range(20):
+        assert relerr(w20[i], g["w20"][i]) < TOL20
+        assert relerr(a20[i], g["alpha20"][i]) < TOL20
+    out = G.sgs_admm_solve(prob, cfg, sigma_schedule=g["hist"][:, 11])
+    assert out.iterations == int(g["iterations"]) and out.converged == bool(g["converged"])
+    assert relerr(out.final_state.w, g["final_w"]) < 1e-6
+    assert abs(out.final_state.beta - float(g["final_beta"])) < 1e-6 * max(1, abs(float(g["final_beta"])))
+    assert abs(out.final_residuals.obj_primal - float(g["obj_primal"])) < 1e-6 * abs(float(g["obj_primal"]))
