@@ -310,10 +310,11 @@ class ZOp:
     """Z~ products.  ``csc``: scipy sparse (the reference's own routine);
     ``dense``: BLAS on the sample-major dense array."""
 
-    def __init__(self, z, mode: str = "csc"):
+    def __init__(self, z, mode: str = "csc", gram: str = "same"):
         self.z = z
         self.d, self.n = z.nrows, z.ncols
         self.mode = mode
+        self.gram = gram  # "dense": one-time Gram by dense BLAS (bench CPU leg only)
         if mode == "dense":
             self.S = z.dense_samples() if hasattr(z, "dense_samples") else z.toarray().T.copy()
         elif mode == "csc":
@@ -328,14 +329,21 @@ class ZOp:
     def rmv(self, w):  # Z~^T w (d -> n)
         return self.S @ w if self.mode == "dense" else self.zst @ w
 
-    def zzt(self):
+    def _dense(self):
         if self.mode == "dense":
-            return self.S.T @ self.S
+            return self.S
+        return self.z.dense_samples() if getattr(self.z, "is_dense", False) else self.z.toarray().T
+
+    def zzt(self):
+        if self.mode == "dense" or self.gram == "dense":
+            S = self._dense()
+            return S.T @ S
         return (self.zs @ self.zs.T).toarray()
 
     def ztz(self):
-        if self.mode == "dense":
-            return self.S @ self.S.T
+        if self.mode == "dense" or self.gram == "dense":
+            S = self._dense()
+            return S @ S.T
         return (self.zst @ self.zs).toarray()
 
 
@@ -518,17 +526,20 @@ class OracleResult:
     train_error_pct: float = 0.0
     setup_s: float = 0.0
     loop_s: float = 0.0
+    timed_s: float = 0.0
+    timed_iters: int = 0
 
 
 def solve(prob, cfg: OracleConfig, operator: str = "csc",
           callback: Optional[Callable[[dict, dict], None]] = None,
-          sigma_schedule: Optional[np.ndarray] = None, record: bool = True) -> OracleResult:
+          sigma_schedule: Optional[np.ndarray] = None, record: bool = True, gram: str = "same",
+          time_after: Optional[int] = None) -> OracleResult:
     """solver.py:392-602.  ``sigma_schedule[k]`` (test hook)
     replaces update_sigma's output as the sigma of iteration k (k >= 1)."""
     import time
 
     t0 = time.perf_counter()
-    op = ZOp(prob.z_tilde, operator)
+    op = ZOp(prob.z_tilde, operator, gram)
     n, d = op.n, op.d
     q, C, mu = prob.q, prob.C, cfg.mu
     mu2 = mu * mu
@@ -585,7 +596,10 @@ def solve(prob, cfg: OracleConfig, operator: str = "csc",
     t1 = time.perf_counter()
     res = None
     st = None
+    t_mark = None
     for k in range(cfg.max_iter):
+        if time_after is not None and k == time_after:
+            t_mark = time.perf_counter()
         last_steps[0] = 0
         eps = epsc / (k + 1.0) ** 1.5
         rhs = xi - r - al / sigma
@@ -641,12 +655,15 @@ def solve(prob, cfg: OracleConfig, operator: str = "csc",
             sigma = float(sigma_schedule[k + 1])
         else:
             sigma = sigma_rule(sigma, eta_p(res), eta_d(res))
-    loop_s = time.perf_counter() - t1
+    t_end = time.perf_counter()
+    loop_s = t_end - t1
     scores = beta + y * ztw
     terr = 100.0 * float(np.mean(y * np.sign(scores) <= 0.0))
     return OracleResult(state=st, residuals=res, iterations=st["iter"], converged=conv, backend=kind,
                         psqmr_total=ptot, double_count=dcount, history=hist, train_error_pct=terr,
-                        setup_s=setup_s, loop_s=loop_s)
+                        setup_s=setup_s, loop_s=loop_s,
+                        timed_s=(t_end - t_mark) if t_mark is not None else loop_s,
+                        timed_iters=(st["iter"] - time_after) if t_mark is not None else st["iter"])
 
 
 __all__ = ["DirectSys", "KKT_FIELDS", "KrylovOut", "OracleConfig", "OracleResult", "ProxSys",

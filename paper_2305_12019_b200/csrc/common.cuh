@@ -97,6 +97,20 @@ GDWD_DEV void sum_partials(const double* partials, int np, double (&out)[K]) {
   }
 }
 
+// Block-cooperative fixed-order sum of partials[p*K + k], p in [0, np): thread
+// t sums p = t, t+blockDim, ... in increasing order, then a fixed tree.  All
+// threads must call; the result is valid in thread 0.
+template <int K>
+GDWD_DEV void block_sum_partials(const double* partials, int np, double (&out)[K], double* scratch) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = 0.0;
+  for (int p = threadIdx.x; p < np; p += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] += ld_cg(partials + (size_t)p * K + k);
+  }
+  block_sum<K>(out, scratch);
+}
+
 // 128-bit streaming load (no L1 allocation): X is read once per pass.
 GDWD_DEV double2 ld_stream2(const double* p) {
   double2 r;

@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "gram.cuh"
 #include "solver_ops.cuh"
+#include "spops.cuh"
 #include "zops.cuh"
 
 using namespace gdwd;
@@ -49,32 +50,44 @@ struct DevBuf {
   }
 };
 
-ZmvGeom zmv_geom(int64_t rows, int64_t cols) {
+// Grids are sized from the occupancy calculator: one full wave of resident
+// CTAs (`slots` = blocks/SM x 148), work split evenly, so there is no tail
+// wave and no per-launch CTA churn.
+ZmvGeom zmv_geom(int64_t rows, int64_t cols, int slots) {
   ZmvGeom g;
   g.tiles = (int)((cols + ZMV_TILE - 1) / ZMV_TILE);
-  const int64_t target = NUM_SMS * 8;
-  int64_t segs = (target + g.tiles - 1) / g.tiles;
-  int64_t maxsegs = std::max<int64_t>(1, rows / 16);
-  segs = std::max<int64_t>(1, std::min(segs, maxsegs));
-  g.seg_len = (rows + segs - 1) / segs;
-  if (g.seg_len < 1) g.seg_len = 1;
-  g.segs = (int)((rows + g.seg_len - 1) / g.seg_len);
-  if (g.segs < 1) g.segs = 1;
+  int64_t segs = std::max<int64_t>(1, slots / g.tiles);
+  segs = std::min<int64_t>(segs, std::max<int64_t>(1, rows / 8));
+  g.seg_len = std::max<int64_t>(1, (rows + segs - 1) / segs);
+  g.segs = (int)std::max<int64_t>(1, (rows + g.seg_len - 1) / g.seg_len);
   g.ldp = (cols + 1) / 2 * 2;
   return g;
 }
 
-ZtGeom zt_geom(int64_t rows, int64_t ld) {
+ZtGeom zt_geom(int64_t rows, int64_t ld, int slots) {
   ZtGeom g;
   int64_t cw = std::min<int64_t>((ld + 63) / 64 * 64, ZT_CW);
+  // short matrices: split rows into more chunks until the grid can fill the GPU
+  while (cw > 512 && ((ld + cw - 1) / cw) * ((rows + 7) / 8) < NUM_SMS * 4) cw = (cw / 2 + 63) / 64 * 64;
   g.cw = (int)cw;
   g.chunks = (int)((ld + cw - 1) / cw);
-  int sb = 8;
-  while (sb < 256 && rows * g.chunks / (sb * 2) >= NUM_SMS * 8) sb *= 2;
-  g.sb = sb;
-  g.sblocks = (int)((rows + sb - 1) / sb);
-  if (g.sblocks < 1) g.sblocks = 1;
+  int64_t ranges = std::max<int64_t>(1, slots / g.chunks);
+  ranges = std::min<int64_t>(ranges, std::max<int64_t>(1, (rows + 7) / 8));
+  g.ranges = (int)ranges;
   return g;
+}
+
+template <class K>
+int slots_for(K kernel, int threads, size_t smem) {
+  static std::map<std::pair<const void*, size_t>, int> cache;
+  auto key = std::make_pair((const void*)kernel, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem) != cudaSuccess || nb < 1) nb = 1;
+  const int s = nb * NUM_SMS;
+  cache[key] = s;
+  return s;
 }
 
 int vm_grid(int64_t len) {
@@ -94,6 +107,13 @@ struct gdwd_ctx {
   double* Zs = nullptr;
   bool has_problem = false;
   double C = 0, q = 0, zscale = 0, yty = 0;
+  // sparse Z~: CSC by sample (Z^T w) and CSR by feature (Z t), int32 indices
+  bool has_sparse = false;
+  int64_t nnz = 0;
+  int64_t *csc_ptr = nullptr, *csr_ptr = nullptr;
+  int *csc_idx = nullptr, *csr_idx = nullptr;
+  double *csc_val = nullptr, *csr_val = nullptr;
+  DevBuf tbuf;  // materialised Z t inputs (2 x n)
   DevBuf y, e, wl;
   // scratch
   DevBuf part, npart, tpart;
@@ -149,6 +169,8 @@ static int set_err(gdwd_ctx* c, int code, const std::string& msg) {
   return code;
 }
 
+static MatView zview(const gdwd_ctx* c) { return MatView{c->has_dense ? c->Zs : nullptr, c->n, c->d, c->ldz}; }
+
 #define RC(call)                           \
   do {                                     \
     int rc_ = (call);                      \
@@ -185,18 +207,41 @@ struct Launch {  // counts launches; with profiling on, brackets the launch with
   }
 };
 
+static int sp_grid(int64_t work_threads, int cap) {
+  int64_t b = (work_threads + SP_THREADS - 1) / SP_THREADS;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, cap));
+}
+
+// X.a == nullptr marks the context's sparse Z~ (CSR/CSC pair)
 template <class Op>
 static void run_zmv(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "zmv") {
+  if (!X.a) {
+    const int g1 = sp_grid(ctx->n, NUM_SMS * 4);
+    {
+      Launch L(ctx, "sp_prep");
+      sp_prep_kernel<Op><<<g1, SP_THREADS, 0, ctx->st>>>(op, ctx->n, ctx->tbuf.p, ctx->scr);
+    }
+    Launch L(ctx, tag);
+    SpView A{ctx->csr_ptr, ctx->csr_idx, ctx->csr_val, ctx->d, ctx->n};
+    sp_zmv_kernel<Op><<<sp_grid(ctx->d * 32, NUM_SMS * 8), SP_THREADS, 0, ctx->st>>>(op, A, ctx->tbuf.p, g1, ctx->scr);
+    return;
+  }
   Launch L(ctx, tag);
-  ZmvGeom g = zmv_geom(X.rows, X.cols);
+  ZmvGeom g = zmv_geom(X.rows, X.cols, slots_for(zmv_kernel<Op>, ZMV_THREADS, 0));
   zmv_kernel<Op><<<dim3(g.tiles, g.segs), ZMV_THREADS, 0, ctx->st>>>(op, X, g, ctx->scr);
 }
 template <class Op>
 static void run_zt(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "ztmv") {
   Launch L(ctx, tag);
-  ZtGeom g = zt_geom(X.rows, X.ld);
-  size_t sm = (size_t)(g.cw + g.sb) * sizeof(double);
-  ztmv_kernel<Op><<<dim3(g.chunks, g.sblocks), ZT_THREADS, sm, ctx->st>>>(op, X, g, ctx->scr);
+  if (!X.a) {
+    SpView A{ctx->csc_ptr, ctx->csc_idx, ctx->csc_val, ctx->n, ctx->d};
+    sp_ztmv_kernel<Op, 8><<<sp_grid(ctx->n * 8, NUM_SMS * 8), SP_THREADS, 0, ctx->st>>>(op, A, ctx->scr);
+    return;
+  }
+  const int cw = zt_geom(X.rows, X.ld, NUM_SMS).cw;
+  const size_t sm = (size_t)(cw + ZT_BATCH) * sizeof(double);
+  ZtGeom g = zt_geom(X.rows, X.ld, slots_for(ztmv_kernel<Op>, ZT_THREADS, sm));
+  ztmv_kernel<Op><<<dim3(g.chunks, g.ranges), ZT_THREADS, sm, ctx->st>>>(op, X, g, ctx->scr);
 }
 template <class Op>
 static void run_vm(gdwd_ctx* ctx, const Op& op, int64_t len, const char* tag = "vmap") {
@@ -220,12 +265,13 @@ static void prof_flush(gdwd_ctx* ctx) {
 
 // scratch sized for matrices with (rows, cols)
 static int ensure_scratch(gdwd_ctx* ctx, int64_t rows, int64_t cols) {
-  ZmvGeom zg = zmv_geom(rows, cols);
-  ZtGeom tg = zt_geom(rows, (cols + 1) / 2 * 2);
+  const int maxslots = NUM_SMS * 32;  // upper bound on resident CTAs
+  ZmvGeom zg = zmv_geom(rows, cols, maxslots);
+  ZtGeom tg = zt_geom(rows, (cols + 1) / 2 * 2, maxslots);
   size_t part = std::max<size_t>((size_t)zg.segs * 2 * zg.ldp, tg.chunks > 1 ? (size_t)tg.chunks * rows : 0);
-  size_t npart = (size_t)std::max<int64_t>({(int64_t)zg.segs, (int64_t)tg.sblocks, (int64_t)NUM_SMS * 4}) * 16;
-  size_t tpart = (size_t)zg.tiles * 16 + 16;
-  size_t nt = (size_t)std::max<int64_t>(zg.tiles, tg.sblocks) + 4;
+  size_t npart = (size_t)maxslots * 16;
+  size_t tpart = (size_t)std::max<int64_t>(zg.tiles, NUM_SMS * 8) * 16 + 16;
+  size_t nt = (size_t)std::max<int64_t>(zg.tiles, maxslots) + 4;
   CK(ctx->part.ensure(std::max(part, ctx->part.n)));
   CK(ctx->npart.ensure(std::max(npart, ctx->npart.n)));
   CK(ctx->tpart.ensure(std::max(tpart, ctx->tpart.n)));
@@ -284,6 +330,17 @@ static void fill(gdwd_ctx* ctx, double* p, int64_t n, double v) {
   fill_kernel<<<vm_grid(n), 256, 0, ctx->st>>>(p, n, v);
 }
 
+static void free_sparse(gdwd_ctx* ctx) {
+  for (void* p : {(void*)ctx->csc_ptr, (void*)ctx->csr_ptr, (void*)ctx->csc_idx, (void*)ctx->csr_idx,
+                  (void*)ctx->csc_val, (void*)ctx->csr_val})
+    if (p) cudaFree(p);
+  ctx->csc_ptr = ctx->csr_ptr = nullptr;
+  ctx->csc_idx = ctx->csr_idx = nullptr;
+  ctx->csc_val = ctx->csr_val = nullptr;
+  ctx->has_sparse = false;
+  ctx->nnz = 0;
+}
+
 extern "C" {
 
 int gdwd_version(void) { return 1; }
@@ -314,8 +371,9 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   if (ctx->Zs) cudaFree(ctx->Zs);
+  free_sparse(ctx);
   for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf})
     b->release();
   end_session(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -333,6 +391,7 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
 int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n) {
   if (!ctx || !samples || d < 1 || n < 1) return set_err(ctx, GDWD_ERR_VALUE, "bad dense upload arguments");
   CK(cudaSetDevice(ctx->device));
+  free_sparse(ctx);
   const int64_t ld = (d + 1) / 2 * 2;
   if (ctx->Zs) cudaFree(ctx->Zs);
   ctx->Zs = nullptr;
@@ -350,13 +409,89 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
   return ensure_scratch(ctx, n, d);
 }
 
-int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t*, const int64_t*, const double*, int64_t, int64_t) {
-  return set_err(ctx, GDWD_ERR_UNSUPPORTED, "sparse CSC upload is not built in this version");
+int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx, const double* values, int64_t d,
+                    int64_t n) {
+  if (!ctx || !colptr || d < 1 || n < 1) return set_err(ctx, GDWD_ERR_VALUE, "bad CSC upload arguments");
+  const int64_t nnz = colptr[n];
+  if (colptr[0] != 0 || nnz < 0) return set_err(ctx, GDWD_ERR_VALUE, "colptr endpoints do not match stored entries");
+  if (nnz >= ((int64_t)1 << 31)) return set_err(ctx, GDWD_ERR_UNSUPPORTED, "nnz >= 2^31 per shard");
+  if (nnz > 0 && (!rowidx || !values)) return set_err(ctx, GDWD_ERR_VALUE, "null CSC arrays");
+  // validate + transpose to CSR on the host (counting sort keeps sample order
+  // within each feature row, so row sums accumulate like np.bincount)
+  std::vector<int64_t> rp(d + 1, 0);
+  std::vector<int> ci32((size_t)nnz);
+  for (int64_t i = 0; i < n; ++i) {
+    if (colptr[i + 1] < colptr[i]) return set_err(ctx, GDWD_ERR_VALUE, "colptr must be nondecreasing");
+    for (int64_t k = colptr[i]; k < colptr[i + 1]; ++k) {
+      const int64_t r = rowidx[k];
+      if (r < 0 || r >= d) return set_err(ctx, GDWD_ERR_VALUE, "row index out of bounds");
+      rp[r + 1]++;
+      ci32[k] = (int)r;
+    }
+  }
+  for (int64_t j = 0; j < d; ++j) rp[j + 1] += rp[j];
+  std::vector<int64_t> fillp(rp.begin(), rp.end() - 1);
+  std::vector<int> cidx((size_t)nnz);
+  std::vector<double> cval((size_t)nnz);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = colptr[i]; k < colptr[i + 1]; ++k) {
+      const int64_t pos = fillp[rowidx[k]]++;
+      cidx[pos] = (int)i;
+      cval[pos] = values[k];
+    }
+  CK(cudaSetDevice(ctx->device));
+  free_sparse(ctx);
+  if (ctx->Zs) cudaFree(ctx->Zs);
+  ctx->Zs = nullptr;
+  ctx->has_dense = false;
+  const size_t nz = (size_t)std::max<int64_t>(nnz, 1);
+  CK(cudaMalloc(&ctx->csc_ptr, (n + 1) * sizeof(int64_t)));
+  CK(cudaMalloc(&ctx->csr_ptr, (d + 1) * sizeof(int64_t)));
+  CK(cudaMalloc(&ctx->csc_idx, nz * sizeof(int)));
+  CK(cudaMalloc(&ctx->csr_idx, nz * sizeof(int)));
+  CK(cudaMalloc(&ctx->csc_val, nz * sizeof(double)));
+  CK(cudaMalloc(&ctx->csr_val, nz * sizeof(double)));
+  CK(cudaMemcpy(ctx->csc_ptr, colptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->csr_ptr, rp.data(), (d + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  if (nnz > 0) {
+    CK(cudaMemcpy(ctx->csc_idx, ci32.data(), nnz * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->csr_idx, cidx.data(), nnz * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->csc_val, values, nnz * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->csr_val, cval.data(), nnz * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  CK(ctx->tbuf.ensure((size_t)2 * n));
+  ctx->n = n;
+  ctx->d = d;
+  ctx->ldz = (d + 1) / 2 * 2;
+  ctx->nnz = nnz;
+  ctx->has_sparse = true;
+  ctx->has_problem = false;
+  ctx->data_gen++;
+  return ensure_scratch(ctx, n, d);
+}
+
+// DIRECT / SMW2 on sparse input: materialise the dense sample-major copy once
+// (the Gram and every product then take the dense path)
+static int densify(gdwd_ctx* ctx) {
+  if (ctx->has_dense) return GDWD_OK;
+  const int64_t n = ctx->n, ld = ctx->ldz;
+  size_t freeb = 0, totb = 0;
+  CK(cudaMemGetInfo(&freeb, &totb));
+  if ((double)n * ld * 8.0 > 0.8 * (double)freeb)
+    return set_err(ctx, GDWD_ERR_UNSUPPORTED, "dense copy of the sparse matrix does not fit for this backend");
+  CK(cudaMalloc(&ctx->Zs, (size_t)n * ld * sizeof(double)));
+  CK(cudaMemsetAsync(ctx->Zs, 0, (size_t)n * ld * sizeof(double), ctx->st));
+  SpView A{ctx->csc_ptr, ctx->csc_idx, ctx->csc_val, n, ctx->d};
+  sp_densify_kernel<<<(unsigned)((n + 7) / 8), 256, 0, ctx->st>>>(A, ctx->Zs, ld);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->st));
+  ctx->has_dense = true;
+  return GDWD_OK;
 }
 
 int gdwd_set_problem(gdwd_ctx* ctx, const double* y, const double* e, const double* weights, double C, double q,
                      double z_scale) {
-  if (!ctx || !ctx->has_dense) return set_err(ctx, GDWD_ERR_VALUE, "upload Z~ before set_problem");
+  if (!ctx || !(ctx->has_dense || ctx->has_sparse)) return set_err(ctx, GDWD_ERR_VALUE, "upload Z~ before set_problem");
   if (!y || !e || !weights) return set_err(ctx, GDWD_ERR_VALUE, "null problem vector");
   if (!(C > 0 && q > 0 && z_scale > 0)) return set_err(ctx, GDWD_ERR_VALUE, "C, q and z_scale must be positive");
   CK(cudaSetDevice(ctx->device));
@@ -385,14 +520,14 @@ int gdwd_set_problem(gdwd_ctx* ctx, const double* y, const double* e, const doub
 }
 
 int gdwd_matvec(gdwd_ctx* ctx, const double* v_n, double* out_d) {
-  if (!ctx || !ctx->has_dense || !v_n || !out_d) return set_err(ctx, GDWD_ERR_VALUE, "matvec: no data or null pointer");
+  if (!ctx || !(ctx->has_dense || ctx->has_sparse) || !v_n || !out_d) return set_err(ctx, GDWD_ERR_VALUE, "matvec: no data or null pointer");
   CK(cudaSetDevice(ctx->device));
   double *dv = nullptr, *dout = nullptr;
   CK(cudaMalloc(&dv, ctx->n * sizeof(double)));
   CK(cudaMalloc(&dout, ctx->d * sizeof(double)));
   CK(cudaMemcpyAsync(dv, v_n, ctx->n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
   OpPlainZ op{dv, nullptr, dout, nullptr};
-  run_zmv(ctx, op, MatView{ctx->Zs, ctx->n, ctx->d, ctx->ldz});
+  run_zmv(ctx, op, zview(ctx));
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out_d, dout, ctx->d * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
@@ -402,14 +537,14 @@ int gdwd_matvec(gdwd_ctx* ctx, const double* v_n, double* out_d) {
 }
 
 int gdwd_matvec_t(gdwd_ctx* ctx, const double* v_d, double* out_n) {
-  if (!ctx || !ctx->has_dense || !v_d || !out_n) return set_err(ctx, GDWD_ERR_VALUE, "matvec_t: no data or null pointer");
+  if (!ctx || !(ctx->has_dense || ctx->has_sparse) || !v_d || !out_n) return set_err(ctx, GDWD_ERR_VALUE, "matvec_t: no data or null pointer");
   CK(cudaSetDevice(ctx->device));
   double *dv = nullptr, *dout = nullptr;
   CK(cudaMalloc(&dv, ctx->d * sizeof(double)));
   CK(cudaMalloc(&dout, ctx->n * sizeof(double)));
   CK(cudaMemcpyAsync(dv, v_d, ctx->d * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
   OpPlainZt op{dv, dout};
-  run_zt(ctx, op, MatView{ctx->Zs, ctx->n, ctx->d, ctx->ldz});
+  run_zt(ctx, op, zview(ctx));
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out_n, dout, ctx->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
@@ -434,8 +569,9 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
   if (ctx->fac_gen == ctx->data_gen && ctx->fac_kind == kind && ctx->fac_mu2 == mu2) return GDWD_OK;
   Dev& D = ctx->D;
   const int64_t n = ctx->n, d = ctx->d;
-  MatView Z{ctx->Zs, n, d, ctx->ldz};
+  MatView Z = zview(ctx);
   if (kind == GDWD_BACKEND_DIRECT || kind == GDWD_BACKEND_SMW2) {
+    RC(densify(ctx));
     const int64_t m = (kind == GDWD_BACKEND_DIRECT) ? d + 1 : n;
     const int64_t ld = (m + 1) / 2 * 2;
     CK(ctx->fac.ensure((size_t)m * ld));
@@ -466,8 +602,12 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
       RC(ensure_scratch(ctx, n, d));
     }
   } else {
-    CK(ctx->colsq.ensure(d));
-    colsq_kernel<OpColSqPrep><<<(unsigned)((d + 255) / 256), 256, 0, ctx->st>>>(Z, ctx->colsq.p);
+    if (Z.a) {
+      colsq_kernel<OpColSqPrep><<<(unsigned)((d + 255) / 256), 256, 0, ctx->st>>>(Z, ctx->colsq.p);
+    } else {
+      SpView A{ctx->csr_ptr, ctx->csr_idx, ctx->csr_val, d, n};
+      sp_rowsq_kernel<<<(unsigned)((d + 255) / 256), 256, 0, ctx->st>>>(A, ctx->colsq.p);
+    }
     jacobi_kernel<<<(unsigned)((d + 256) / 256), 256, 0, ctx->st>>>(ctx->colsq.p, d, mu2, ctx->yty,
                                                                      const_cast<double*>(D.jac));
     CK(cudaGetLastError());
@@ -482,7 +622,7 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
 // enqueue one normal-system solve: out = A^{-1} hv (DIRECT / SMW2)
 static void enqueue_solve(gdwd_ctx* ctx, int kind, const double* hv, double* out, int pred) {
   const Dev& D = ctx->D;
-  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  MatView Z = zview(ctx);
   MatView F{ctx->fac.p, ctx->fac_rows, ctx->fac_rows, ctx->ldm};
   if (kind == GDWD_BACKEND_DIRECT) {
     run_zt(ctx, OpGemvSolve{D, hv, out, pred}, F, pred ? "gemv_Ainv_2" : "gemv_Ainv");
@@ -497,7 +637,7 @@ static void enqueue_solve(gdwd_ctx* ctx, int kind, const double* hv, double* out
 static int psqmr_solve(gdwd_ctx* ctx, const double* b, const double* x0, double* out, int pred, double tolmul,
                        int max_steps, int* steps, int* conv, int* active_run) {
   const Dev& D = ctx->D;
-  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  MatView Z = zview(ctx);
   run_zt(ctx, OpApplyZt{D, x0, pred, 0}, Z, "ztmv_psqmr_init");
   run_zmv(ctx, OpInitResidual{D, x0, b, pred}, Z, "zmv_psqmr_init");
   run_vm(ctx, OpPsInit{D, x0, out, pred, tolmul}, D.m, "vmap_psqmr_init");
@@ -534,7 +674,7 @@ static int psqmr_solve(gdwd_ctx* ctx, const double* b, const double* x0, double*
 // the tail shared by every backend: w/ztw commit, Steps 2-3, KKT sample terms
 static void enqueue_tail(gdwd_ctx* ctx) {
   const Dev& D = ctx->D;
-  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  MatView Z = zview(ctx);
   run_vm(ctx, OpCopyIfReuse{D, D.xb, D.x}, D.m, "vmap_copy_x");
   run_zt(ctx, OpZtStore{D, D.x, D.ztw, 1}, Z, "ztmv_ztw_2");
   run_vm(ctx, OpCopyIfReuse{D, D.ztwb, D.ztw}, D.n, "vmap_copy_ztw");
@@ -545,7 +685,7 @@ static void enqueue_tail(gdwd_ctx* ctx) {
 
 static void enqueue_body_fixed(gdwd_ctx* ctx, int kind, bool use_sgs) {
   const Dev& D = ctx->D;
-  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  MatView Z = zview(ctx);
   run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
   enqueue_solve(ctx, kind, D.h, D.xb, 0);
   run_zt(ctx, OpZtNewton{D}, Z, "ztmv_newton");
@@ -557,7 +697,7 @@ static void enqueue_body_fixed(gdwd_ctx* ctx, int kind, bool use_sgs) {
 
 static int body_iterative(gdwd_ctx* ctx, bool use_sgs, int max_steps, int* psqmr_steps) {
   const Dev& D = ctx->D;
-  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  MatView Z = zview(ctx);
   run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
   int steps = 0, conv = 1, ran = 0, rc;
   *psqmr_steps = 0;
@@ -590,7 +730,8 @@ static void end_session(gdwd_ctx* ctx) {
 
 extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const double* sched, int64_t sched_len) {
   if (!ctx || !cfg) return set_err(ctx, GDWD_ERR_VALUE, "null argument");
-  if (!ctx->has_dense || !ctx->has_problem) return set_err(ctx, GDWD_ERR_VALUE, "no problem uploaded");
+  if (!(ctx->has_dense || ctx->has_sparse) || !ctx->has_problem)
+    return set_err(ctx, GDWD_ERR_VALUE, "no problem uploaded");
   if (!(cfg->steplength > 0.0 && cfg->steplength <= 1.618034))
     return set_err(ctx, GDWD_ERR_VALUE, "steplength must lie in (0, 1.618034)");
   if (std::min({cfg->tol_feas, cfg->tol_cgap, cfg->tol_cap}) <= 0)
@@ -665,7 +806,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   // ---- setup: zy, factor / preconditioner ------------------------------------
   CK(cudaEventRecord(ctx->ev_begin, ctx->st));
   RC(ensure_scratch(ctx, n, d));
-  MatView Z{ctx->Zs, n, d, ctx->ldz};
+  MatView Z = zview(ctx);
   run_zmv(ctx, OpPlainZ{ctx->y.p, nullptr, const_cast<double*>(D.zy), nullptr}, Z, "zmv_zy");
   CK(cudaGetLastError());
   RC(build_factor(ctx, kind, mu2));
@@ -728,7 +869,7 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
   if (!ctx || !ctx->in_solve) return set_err(ctx, GDWD_ERR_VALUE, "no solve in progress");
   CK(cudaSetDevice(ctx->device));
   const Dev& D = ctx->D;
-  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  MatView Z = zview(ctx);
   int status = GDWD_OK;
   const int kend = std::min(ctx->max_iter, ctx->k_host + std::max(0, count));
   while (ctx->k_host < kend && !ctx->stopped) {
@@ -797,7 +938,7 @@ extern "C" int gdwd_solve_end(gdwd_ctx* ctx, gdwd_result* out) {
   CK(cudaSetDevice(ctx->device));
   memset(out, 0, sizeof(*out));
   const Dev& D = ctx->D;
-  MatView Z{ctx->Zs, ctx->n, ctx->d, ctx->ldz};
+  MatView Z = zview(ctx);
   // final pass: dual objective / gap / stop test of the last iteration
   run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
   CK(cudaGetLastError());
@@ -1038,15 +1179,15 @@ extern "C" int gdwd_psqmr_dense(int32_t device, const double* A, int64_t m, cons
   double* dA = t.alloc<double>((size_t)m * ld);
   double* vec = t.alloc<double>((size_t)12 * (m + 1));
   Scal* S = t.alloc<Scal>(1);
-  size_t npn = (size_t)NUM_SMS * 4 * 16 + 64;
+  size_t npn = (size_t)NUM_SMS * 32 * 16 + 64;
   double* npart = t.alloc<double>(npn);
   double* part = t.alloc<double>((size_t)8 * (m + 1));
-  unsigned* tk = t.alloc<unsigned>(((m + 7) / 8) + 8);
+  unsigned* tk = t.alloc<unsigned>(NUM_SMS * 32 + 8);
   if (!dA || !vec || !S || !npart || !part || !tk) return GDWD_ERR_CUDA;
   CK(cudaMemset(dA, 0, (size_t)m * ld * 8));
   CK(cudaMemcpy2D(dA, ld * 8, A, m * 8, m * 8, m, cudaMemcpyHostToDevice));
   CK(cudaMemset(vec, 0, (size_t)12 * (m + 1) * 8));
-  CK(cudaMemset(tk, 0, (((m + 7) / 8) + 8) * sizeof(unsigned)));
+  CK(cudaMemset(tk, 0, (NUM_SMS * 32 + 8) * sizeof(unsigned)));
   const int64_t s = m + 1;
   Dev D{};
   D.m = m;
@@ -1071,16 +1212,16 @@ extern "C" int gdwd_psqmr_dense(int32_t device, const double* A, int64_t m, cons
   CK(cudaMemcpy(S, &s0, sizeof(Scal), cudaMemcpyHostToDevice));
   Scratch scr{part, npart, npart + (npn - 32), tk};
   MatView Av{dA, m, m, ld};
-  ZtGeom g = zt_geom(m, ld);
-  size_t sm = (size_t)(g.cw + g.sb) * 8;
-  ztmv_kernel<OpDenseInitRes><<<dim3(g.chunks, g.sblocks), ZT_THREADS, sm>>>(OpDenseInitRes{x0d, bb, D.pr}, Av, g, scr);
+  ZtGeom g = zt_geom(m, ld, NUM_SMS);
+  size_t sm = (size_t)(g.cw + ZT_BATCH) * 8;
+  ztmv_kernel<OpDenseInitRes><<<dim3(g.chunks, g.ranges), ZT_THREADS, sm>>>(OpDenseInitRes{x0d, bb, D.pr}, Av, g, scr);
   vmap_kernel<OpPsInit><<<vm_grid(m), VM_THREADS>>>(OpPsInit{D, x0d, xo, 0, 1.0}, m, scr);
   CK(cudaGetLastError());
   Scal h;
   for (int it = 0; it <= max_iter; ++it) {
     CK(cudaMemcpy(&h, S, sizeof(Scal), cudaMemcpyDeviceToHost));
     if (!h.ps_active || it == max_iter) break;
-    ztmv_kernel<OpDenseApply><<<dim3(g.chunks, g.sblocks), ZT_THREADS, sm>>>(OpDenseApply{D}, Av, g, scr);
+    ztmv_kernel<OpDenseApply><<<dim3(g.chunks, g.ranges), ZT_THREADS, sm>>>(OpDenseApply{D}, Av, g, scr);
     vmap_kernel<OpPsV1><<<vm_grid(m), VM_THREADS>>>(OpPsV1{D}, m, scr);
     vmap_kernel<OpPsV2><<<vm_grid(m), VM_THREADS>>>(OpPsV2{D, xo, 1.0, max_iter}, m, scr);
     CK(cudaGetLastError());

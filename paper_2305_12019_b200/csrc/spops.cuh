@@ -1,0 +1,152 @@
+// Sparse counterparts of zmv / ztmv (zops.cuh) for Z~ stored in both
+// orientations (reference linalg/sparse.py: the scipy CSC view and its .T):
+//
+//   CSR by feature (rowptr[d+1], colidx, val): Z~ t   -- one warp per feature
+//   CSC by sample  (colptr[n+1], rowidx, val): Z~^T w -- G lanes per sample
+//
+// Both use the same Op functors as the dense kernels, so every fused
+// epilogue (Newton prox, h/h2/residual updates, PSQMR scalars) is shared.
+// Z~ t needs its inputs materialised first (each sample appears in many
+// feature rows): sp_prep writes t_r[i] = op.input(i) and the n-sum partials.
+// Indices are int32 (nnz < 2^31 per shard), row pointers int64.  Summation
+// order is fixed (lane-strided, fixed shuffle tree, fixed partial order), so
+// results are deterministic.
+#pragma once
+#include "common.cuh"
+#include "zops.cuh"
+
+namespace gdwd {
+
+struct SpView {
+  const int64_t* ptr;  // rows+1 (CSR: features; CSC: samples)
+  const int* idx;
+  const double* val;
+  int64_t rows;   // number of compressed rows (d for CSR, n for CSC)
+  int64_t other;  // length of the gathered vector (n for CSR, d for CSC)
+};
+
+constexpr int SP_THREADS = 256;
+
+// t_r[i] for all samples + n-sum partials (one partial per CTA)
+template <class Op>
+__global__ void __launch_bounds__(SP_THREADS) sp_prep_kernel(Op op, int64_t n, double* tbuf, Scratch s) {
+  constexpr int R = Op::R, NN = Op::NN;
+  if (op.skip()) return;
+  __shared__ double red[(SP_THREADS / 32) * NN];
+  double nacc[NN];
+#pragma unroll
+  for (int k = 0; k < NN; ++k) nacc[k] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)SP_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SP_THREADS) {
+    double tv[R];
+    op.input(i, tv, nacc);
+#pragma unroll
+    for (int r = 0; r < R; ++r) tbuf[r * n + i] = tv[r];
+  }
+  block_sum<NN>(nacc, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NN; ++k) s.npart[(int64_t)blockIdx.x * NN + k] = nacc[k];
+  }
+}
+
+// v_j = sum_i Z[j,i] t_i (CSR rows = features), epilogue per feature, then
+// the global finaliser sums the prep kernel's nprep n-partials and the
+// per-CTA d-partials.
+template <class Op>
+__global__ void __launch_bounds__(SP_THREADS) sp_zmv_kernel(Op op, SpView A, const double* tbuf, int nprep,
+                                                            Scratch s) {
+  constexpr int R = Op::R, NN = Op::NN, ND = Op::ND;
+  if (op.skip()) return;
+  __shared__ double red[(SP_THREADS / 32) * ND];
+  __shared__ double red2[(SP_THREADS / 32) * (NN > ND ? NN : ND)];
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)SP_THREADS + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * SP_THREADS) >> 5;
+  double dacc[ND];
+#pragma unroll
+  for (int k = 0; k < ND; ++k) dacc[k] = 0.0;
+  for (int64_t j = warp; j < A.rows; j += nwarps) {
+    const int64_t b = A.ptr[j], e = A.ptr[j + 1];
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    for (int64_t k = b + lane; k < e; k += 32) {
+      const double v = __ldg(A.val + k);
+      const int64_t c = __ldg(A.idx + k);
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] += v * tbuf[r * A.other + c];
+    }
+    warp_sum<R>(acc);
+    if (lane == 0) op.epi(j, acc, dacc);
+  }
+  block_sum<ND>(dacc, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < ND; ++k) s.tpart[(int64_t)blockIdx.x * ND + k] = dacc[k];
+  }
+  if (!last_arrival(&s.tickets[0], gridDim.x)) return;
+  double nsum[NN], dsum[ND];
+  block_sum_partials<NN>(s.npart, nprep, nsum, red2);
+  block_sum_partials<ND>(s.tpart, gridDim.x, dsum, red2);
+  if (threadIdx.x == 0) op.fin(nsum, dsum);
+}
+
+// dot_i = sum_j Z[j,i] w_j (CSC columns = samples); G lanes per sample.
+template <class Op, int G>
+__global__ void __launch_bounds__(SP_THREADS) sp_ztmv_kernel(Op op, SpView A, Scratch s) {
+  constexpr int NN = Op::NN;
+  if (op.skip()) return;
+  __shared__ double red[(SP_THREADS / 32) * NN];
+  const int sub = threadIdx.x & (G - 1);
+  const int64_t grp = (blockIdx.x * (int64_t)SP_THREADS + threadIdx.x) / G;
+  const int64_t ngrp = ((int64_t)gridDim.x * SP_THREADS) / G;
+  double nacc[NN];
+#pragma unroll
+  for (int k = 0; k < NN; ++k) nacc[k] = 0.0;
+  // all lanes of a warp iterate the same number of times (shuffles)
+  const int64_t iters = (A.rows + ngrp - 1) / ngrp;
+  for (int64_t t = 0; t < iters; ++t) {
+    const int64_t i = grp + t * ngrp;
+    double acc = 0.0;
+    if (i < A.rows) {
+      const int64_t b = A.ptr[i], e = A.ptr[i + 1];
+      for (int64_t k = b + sub; k < e; k += G) acc += __ldg(A.val + k) * op.wval(__ldg(A.idx + k));
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (sub == 0 && i < A.rows) op.row(i, acc, nacc);
+  }
+  if (!Op::HAS_FIN) return;
+  block_sum<NN>(nacc, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NN; ++k) s.npart[(int64_t)blockIdx.x * NN + k] = nacc[k];
+  }
+  if (!last_arrival(&s.tickets[0], gridDim.x)) return;
+  double nsum[NN];
+  block_sum_partials<NN>(s.npart, gridDim.x, nsum, red);
+  if (threadIdx.x == 0) op.fin(nsum);
+}
+
+// row sums of squares of CSR rows in stored (sample) order: the same
+// sequential order as the reference's np.bincount (sparse.py:66-70)
+__global__ void sp_rowsq_kernel(SpView A, double* out) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= A.rows) return;
+  double s = 0.0;
+  for (int64_t k = A.ptr[j]; k < A.ptr[j + 1]; ++k) {
+    const double v = A.val[k];
+    s += v * v;
+  }
+  out[j] = s;
+}
+
+// scatter a CSC matrix into the dense sample-major layout [n][ld]
+__global__ void sp_densify_kernel(SpView csc, double* Zs, int64_t ld) {
+  const int64_t i = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (i >= csc.rows) return;
+  for (int64_t k = csc.ptr[i] + (threadIdx.x & 31); k < csc.ptr[i + 1]; k += 32)
+    Zs[i * ld + csc.idx[k]] = csc.val[k];
+}
+
+}  // namespace gdwd

@@ -146,28 +146,27 @@ __global__ void __launch_bounds__(ZMV_THREADS) zmv_kernel(Op op, MatView X, ZmvG
     for (int k = 0; k < ND; ++k) s.tpart[(int64_t)tile * ND + k] = dacc[k];
   }
   if (!last_arrival(&s.tickets[gridDim.x], gridDim.x)) return;
-  if (threadIdx.x == 0) {
-    double nsum[NN], dsum[ND];
-    sum_partials<NN>(s.npart, gridDim.y, nsum);
-    sum_partials<ND>(s.tpart, gridDim.x, dsum);
-    op.fin(nsum, dsum);
-  }
+  double nsum[NN], dsum[ND];
+  block_sum_partials<NN>(s.npart, gridDim.y, nsum, red);
+  block_sum_partials<ND>(s.tpart, gridDim.x, dsum, red);
+  if (threadIdx.x == 0) op.fin(nsum, dsum);
 }
 
 // ---------------------------------------------------------------------------
-// ztmv: grid (chunks, sblocks); CTA of 256 threads (8 warps).  The chunk of
-// w (<= ZT_CW columns) is staged in shared memory; each warp computes full
-// row dots over the chunk for its samples; with several chunks the last CTA
-// of a sample block sums the chunk partials in fixed order.  The per-sample
-// epilogue then runs one sample per thread.
+// ztmv: grid (chunks, ranges).  Rows are split into `ranges` contiguous,
+// evenly sized row ranges (one full wave of CTAs, sized from the occupancy
+// calculator); the chunk of w (<= ZT_CW columns) is staged in shared memory
+// and each warp computes row dots over the chunk.  With several chunks the
+// last-arriving CTA of a row range sums the chunk partials in fixed order.
+// The per-sample epilogue runs one sample per thread, ZT_BATCH rows at a time.
 // ---------------------------------------------------------------------------
 constexpr int ZT_THREADS = 256;
 constexpr int ZT_CW = 4096;
+constexpr int ZT_BATCH = 256;
 
 struct ZtGeom {
-  int chunks, sblocks;
-  int cw;   // chunk width (even)
-  int sb;   // samples per block (multiple of 8, <= 256)
+  int chunks, ranges;
+  int cw;  // chunk width (even)
 };
 
 template <class Op>
@@ -175,73 +174,75 @@ __global__ void __launch_bounds__(ZT_THREADS) ztmv_kernel(Op op, MatView X, ZtGe
   constexpr int NN = Op::NN;
   if (op.skip()) return;
   extern __shared__ double zsm[];
-  double* ws = zsm;          // cw
-  double* sdot = zsm + g.cw;  // sb
+  double* ws = zsm;           // cw
+  double* sdot = zsm + g.cw;  // ZT_BATCH
   __shared__ double red[(ZT_THREADS / 32) * NN];
-  const int c = blockIdx.x, sbk = blockIdx.y;
+  const int c = blockIdx.x, rg = blockIdx.y;
   const int64_t c0 = (int64_t)c * g.cw;
   const int64_t clen = (c0 + g.cw < X.ld) ? g.cw : X.ld - c0;
+  const int64_t i0 = X.rows * rg / g.ranges, i1 = X.rows * (rg + 1) / g.ranges;
   for (int jj = threadIdx.x; jj < clen; jj += ZT_THREADS) {
     const int64_t j = c0 + jj;
     ws[jj] = (j < X.cols) ? op.wval(j) : 0.0;
   }
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t i0 = (int64_t)sbk * g.sb;
-  const int nsb = (int)((i0 + g.sb < X.rows) ? g.sb : X.rows - i0);
-  for (int li = warp; li < nsb; li += ZT_THREADS / 32) {
-    const double* p = X.a + (i0 + li) * X.ld + c0;
-    double acc = 0.0;
-    int64_t jj = 2 * lane;
-    for (; jj + 3 * 64 < clen; jj += 4 * 64) {
-      double2 z[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) z[u] = ld_stream2(p + jj + u * 64);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        acc += z[u].x * ws[jj + u * 64];
-        acc += z[u].y * ws[jj + u * 64 + 1];
-      }
-    }
-    for (; jj < clen; jj += 64) {
-      const double2 z = ld_stream2(p + jj);
-      acc += z.x * ws[jj];
-      acc += z.y * ws[jj + 1];
-    }
-    double a1[1] = {acc};
-    warp_sum<1>(a1);
-    if (lane == 0) {
-      if (gridDim.x == 1) sdot[li] = a1[0];
-      else s.part[(int64_t)c * X.rows + i0 + li] = a1[0];
-    }
-  }
-  double dot = 0.0;
-  if (gridDim.x > 1) {
-    if (!last_arrival(&s.tickets[sbk], gridDim.x)) return;
-    if (threadIdx.x < nsb) {
-      for (int cc = 0; cc < (int)gridDim.x; ++cc) dot += ld_cg(s.part + (int64_t)cc * X.rows + i0 + threadIdx.x);
-    }
-  } else {
-    __syncthreads();
-    if (threadIdx.x < nsb) dot = sdot[threadIdx.x];
-  }
+  const bool single = gridDim.x == 1;
   double nacc[NN];
 #pragma unroll
   for (int k = 0; k < NN; ++k) nacc[k] = 0.0;
-  if (threadIdx.x < nsb) op.row(i0 + threadIdx.x, dot, nacc);
+  for (int64_t b0 = i0; b0 < i1; b0 += ZT_BATCH) {
+    const int nb = (int)((b0 + ZT_BATCH < i1) ? ZT_BATCH : i1 - b0);
+    __syncthreads();
+    for (int li = warp; li < nb; li += ZT_THREADS / 32) {
+      const double* p = X.a + (b0 + li) * X.ld + c0;
+      double acc = 0.0;
+      int64_t jj = 2 * lane;
+      for (; jj + 7 * 64 < clen; jj += 8 * 64) {
+        double2 z[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) z[u] = ld_stream2(p + jj + u * 64);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc += z[u].x * ws[jj + u * 64];
+          acc += z[u].y * ws[jj + u * 64 + 1];
+        }
+      }
+      for (; jj < clen; jj += 64) {
+        const double2 z = ld_stream2(p + jj);
+        acc += z.x * ws[jj];
+        acc += z.y * ws[jj + 1];
+      }
+      double a1[1] = {acc};
+      warp_sum<1>(a1);
+      if (lane == 0) {
+        if (single) sdot[li] = a1[0];
+        else s.part[(int64_t)c * X.rows + b0 + li] = a1[0];
+      }
+    }
+    if (single) {
+      __syncthreads();
+      if (threadIdx.x < nb) op.row(b0 + threadIdx.x, sdot[threadIdx.x], nacc);
+    }
+  }
+  if (!single) {
+    if (!last_arrival(&s.tickets[rg], gridDim.x)) return;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += ZT_THREADS) {
+      double dot = 0.0;
+      for (int cc = 0; cc < (int)gridDim.x; ++cc) dot += ld_cg(s.part + (int64_t)cc * X.rows + i);
+      op.row(i, dot, nacc);
+    }
+  }
   if (!Op::HAS_FIN) return;
   block_sum<NN>(nacc, red);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < NN; ++k) s.npart[(int64_t)sbk * NN + k] = nacc[k];
+    for (int k = 0; k < NN; ++k) s.npart[(int64_t)rg * NN + k] = nacc[k];
   }
-  // global ticket lives after the per-sblock slots
-  if (!last_arrival(&s.tickets[(gridDim.x > 1 ? gridDim.y : 0)], gridDim.y)) return;
-  if (threadIdx.x == 0) {
-    double nsum[NN];
-    sum_partials<NN>(s.npart, gridDim.y, nsum);
-    op.fin(nsum);
-  }
+  // global ticket lives after the per-range slots
+  if (!last_arrival(&s.tickets[single ? 0 : gridDim.y], gridDim.y)) return;
+  double nsum[NN];
+  block_sum_partials<NN>(s.npart, gridDim.y, nsum, red);
+  if (threadIdx.x == 0) op.fin(nsum);
 }
 
 // ---------------------------------------------------------------------------
@@ -266,11 +267,9 @@ __global__ void __launch_bounds__(VM_THREADS) vmap_kernel(Op op, int64_t len, Sc
     for (int k = 0; k < NR; ++k) s.npart[(int64_t)blockIdx.x * NR + k] = acc[k];
   }
   if (!last_arrival(&s.tickets[0], gridDim.x)) return;
-  if (threadIdx.x == 0) {
-    double sum[NR];
-    sum_partials<NR>(s.npart, gridDim.x, sum);
-    op.fin(sum);
-  }
+  double sum[NR];
+  block_sum_partials<NR>(s.npart, gridDim.x, sum, red);
+  if (threadIdx.x == 0) op.fin(sum);
 }
 
 }  // namespace gdwd

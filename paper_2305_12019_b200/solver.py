@@ -502,13 +502,11 @@ def newton_r(a: float, sigma: float, q: float, weight: float, r_init: float, tol
 
 
 def matvec(m: SparseMatrixCSC, x: np.ndarray, transpose: bool = False, device: int = 0) -> np.ndarray:
-    """linalg/sparse.py:129-142 on the device (dense-stored matrices)."""
+    """linalg/sparse.py:129-142 on the device (dense or sparse CSC storage)."""
     x = _lib.f64(x)
     expected = m.nrows if transpose else m.ncols
     if x.shape != (expected,):
         raise ValueError(f"dimension mismatch: operand has length {x.shape}, expected ({expected},)")
-    if not m.is_dense:
-        raise NotImplementedError("device matvec of sparse CSC matrices is not built in this version")
     ones = np.ones(m.ncols)
     pd = ProblemData(m, ones, ones, ones, 1.0, 1.0, 1.0)
     dp = DeviceProblem(pd, device)

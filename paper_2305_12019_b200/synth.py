@@ -140,10 +140,9 @@ def sparse_matrix(cfg: SynthConfig, seed: int = 0):
     np.add.at(colptr, c + 1, 1)
     colptr = np.cumsum(colptr)
     # unit-norm columns
-    nrm = np.sqrt(np.add.reduceat(v * v, colptr[:-1])) if v.size else np.ones(n)
-    empty = np.diff(colptr) == 0
-    nrm[empty] = 1.0
-    v = v / np.repeat(nrm, np.diff(colptr))
+    nrm = np.sqrt(np.bincount(c, weights=v * v, minlength=n))
+    nrm[nrm == 0.0] = 1.0
+    v = v / nrm[c]
     x = SparseMatrixCSC(d, n, colptr, r, v)
     gw = _rng(seed, _SALT["wstar"], 0)
     wstar = np.zeros(d)

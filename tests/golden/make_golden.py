@@ -53,6 +53,9 @@ CASES = [
     ("smw2_natural", "c2", 6000, 200, "auto", 40, False),
     ("iter_natural", "c1", 6000, 1500, "auto", 25, False),
     ("direct_q4", "c5", 300, 900, "auto", 60, False),
+    ("tiny_sparse", "c4", 3000, 2000, "iterative", 40, True),
+    ("sparse_natural", "c4", 8000, 30000, "auto", 25, False),
+    ("sparse_direct", "c4", 1500, 4000, "auto", 40, False),
 ]
 SAMPLE = 64  # sampled coordinates per vector for the non-full cases
 

@@ -30,6 +30,26 @@ def test_matvec_both_directions(d, n):
         dp.close()
 
 
+@pytest.mark.parametrize("d,n,dens", [(3000, 2000, 0.001), (500, 7000, 0.02), (40, 30, 0.3)])
+def test_sparse_matvec_both_directions(d, n, dens):
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(d + n)
+    M = sp.random(d, n, density=dens, format="csc", random_state=rng, data_rvs=rng.standard_normal)
+    z = G.sparse.csc_from_scipy(M)
+    assert not z.is_dense
+    ones = np.ones(n)
+    dp = G.DeviceProblem(G.ProblemData(z, ones, ones, ones, 1.0, 1.0, 1.0))
+    try:
+        t = rng.standard_normal(n)
+        w = rng.standard_normal(d)
+        assert relerr(dp.matvec(t), M @ t) < 1e-13
+        assert relerr(dp.rmatvec(w), M.T @ w) < 1e-13
+        assert np.array_equal(dp.matvec(t), dp.matvec(t))
+    finally:
+        dp.close()
+
+
 @pytest.mark.parametrize("rows,cols", [(1000, 300), (130, 2001), (5, 70)])
 def test_gram_dmma(rows, cols):
     rng = np.random.default_rng(rows + cols)

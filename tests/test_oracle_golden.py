@@ -78,7 +78,8 @@ def test_oracle_matches_reference_trajectory(case):
     cfg = O.OracleConfig(max_iter=int(tr["max_iter"]), backend=backend)
     if case.startswith("tiny_"):
         cfg.backend = {"tiny_direct": "direct", "tiny_smw2": "smw2", "tiny_iter": "iterative",
-                       "tiny_iter_c4gen": "iterative", "tiny_direct_q2": "direct"}[case]
+                       "tiny_iter_c4gen": "iterative", "tiny_direct_q2": "direct",
+                       "tiny_sparse": "iterative"}[case]
     out = O.solve(prob, cfg, operator="csc", callback=cb)
     assert out.backend == str(tr["backend"])
     assert out.iterations == int(tr["iterations"])
