@@ -152,7 +152,7 @@ def kernel_bytes(tag: str, n: int, d: int) -> float | None:
         return x + 8.0 * (d + 9 * n)  # w in; ztw, r, xi, alpha, y, w_l read, r+, dr, ztw out
     if tag.startswith("ztmv_smw_s1") or tag.startswith("ztmv_ztw"):
         return x + 8.0 * (d + 2 * n)
-    if tag.startswith("gemv_Ginv"):
+    if tag.startswith("gemv_Ginv") or tag.startswith("gemv_K"):
         return 8.0 * n * n + 8.0 * 3 * n
     if tag.startswith("gemv_Ainv"):
         return 8.0 * (d + 1) ** 2 + 16.0 * (d + 1)
@@ -182,7 +182,7 @@ def run_b200(args, dist: Dist):
     # ---- device-resident timing ----------------------------------------------
     dp = G.device_problem(prob, device)
     ccfg = _lib.GdwdConfig(max_iter=conf.max_iter, backend=0, use_sgs=1, psqmr_switch_steps=50, ell=10, seed=0,
-                           use_graph=1, poll_every=16, steplength=conf.steplength, tol_feas=conf.tol_feas,
+                           use_graph=1, poll_every=16, smw_gram_space=int(not args.x_space), steplength=conf.steplength, tol_feas=conf.tol_feas,
                            tol_cgap=conf.tol_cgap, tol_cap=conf.tol_cap, sigma0=float("nan"),
                            epsilon_c=_eps_c(prob, conf), mu=conf.mu)
     _check(lib.gdwd_solve_begin(dp.ctx, C.byref(ccfg), None, 0), dp.ctx, "begin")
@@ -229,7 +229,7 @@ def run_b200(args, dist: Dist):
                         "gbs": round(b / (avg * 1e-3) / 1e9, 1) if b else None})
     peak, peak_kind = peaks()
     top = next(k for k in kernels if k["gbs"] is not None)
-    x_tags = [k for k in kernels if k["tag"].startswith(("zmv", "ztmv"))]
+    x_tags = [k for k in kernels if k["tag"].startswith(("zmv", "ztmv", "gemv"))]
     x_bytes_iter = sum(kernel_bytes(k["tag"], n, d) * k["launches"] for k in x_tags) / prof_iters
     roofline = {"bound": "hbm", "kernel": top["tag"], "achieved": top["gbs"], "peak": peak, "unit": "GB/s",
                 "frac": round(top["gbs"] / peak, 4), "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
@@ -316,6 +316,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--kkt-iters", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--x-space", action="store_true", help="SMW2 iterations as passes over X (no Gram-space)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     dist = Dist()

@@ -121,7 +121,7 @@ struct gdwd_ctx {
   size_t ntickets = 0;
   Scratch scr{};
   // solver buffers
-  DevBuf nvec, mvec, tabs, histb, fac, facw, colsq;
+  DevBuf nvec, mvec, tabs, histb, fac, facw, colsq, kmat;
   int64_t ldm = 0, fac_rows = 0;
   int fac_kind = 0;
   double fac_mu2 = -1;
@@ -136,7 +136,7 @@ struct gdwd_ctx {
   // solve session (gdwd_solve_begin / _iterate / _end)
   bool in_solve = false;
   int kind = 0, poll = 16, max_iter = 0, max_steps = 50, k_host = 0, psqmr_total = 0;
-  bool use_sgs = true, stopped = false;
+  bool use_sgs = true, stopped = false, gram = false;
   cudaGraphExec_t gexec = nullptr;
   int64_t body_nodes = 0;
   cudaEvent_t ev_begin = nullptr, ev_loop = nullptr, ev_end = nullptr;
@@ -321,6 +321,17 @@ __global__ void assemble_direct_kernel(double* A, int64_t ld, int64_t d, const d
   }
 }
 
+// G = K / mu^2 + I (subsolvers.py:109-110: gram / mu_sq, then += 1 on the diagonal)
+__global__ void g_from_k_kernel(const double* K, double* G, int64_t n, int64_t ld, double mu2) {
+  const int64_t tot = n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / n, j = idx % n;
+    double v = K[i * ld + j] / mu2;
+    if (i == j) v += 1.0;
+    G[i * ld + j] = v;
+  }
+}
+
 __global__ void fill_kernel(double* p, int64_t n, double v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
@@ -373,7 +384,7 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   if (ctx->Zs) cudaFree(ctx->Zs);
   free_sparse(ctx);
   for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat})
     b->release();
   end_session(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -584,7 +595,11 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
       CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, true, 1.0, mu2, ctx->fac.p, ld, ctx->facw.p, ctx->st));
       assemble_direct_kernel<<<(unsigned)((d + 256) / 256), 256, 0, ctx->st>>>(ctx->fac.p, ld, d, D.zy, ctx->yty);
     } else {
-      CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, false, mu2, 1.0, ctx->fac.p, ld, ctx->facw.p, ctx->st));
+      // keep K = Z^T Z for the Gram-space iteration; G = K/mu^2 + I
+      CK(ctx->kmat.ensure((size_t)m * ld));
+      CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, false, 1.0, 0.0, ctx->kmat.p, ld, ctx->facw.p, ctx->st));
+      g_from_k_kernel<<<vm_grid(m * m), 256, 0, ctx->st>>>(ctx->kmat.p, ctx->fac.p, m, ld, mu2);
+      CK(cudaGetLastError());
     }
     CK(cudaMemsetAsync(ctx->dinfo, 0, sizeof(int), ctx->st));
     CK(chol_inverse(ctx->fac.p, ctx->facw.p, ctx->facw.p + (size_t)m * ld, ld, m, ctx->dinfo, ctx->st));
@@ -695,6 +710,49 @@ static void enqueue_body_fixed(gdwd_ctx* ctx, int kind, bool use_sgs) {
   enqueue_tail(ctx);
 }
 
+// Gram-space SMW2 body (see solver_ops.cuh): no pass over X
+static void enqueue_solve_gram(gdwd_ctx* ctx, const double* hv, double* out, int pred) {
+  const Dev& D = ctx->D;
+  MatView K{ctx->kmat.p, ctx->n, ctx->n, ctx->ldm};
+  MatView F{ctx->fac.p, ctx->fac_rows, ctx->fac_rows, ctx->ldm};
+  run_zt(ctx, OpSmwS1{D, hv, pred}, K, pred ? "gemv_K_s1_2" : "gemv_K_s1");
+  run_zt(ctx, OpSmwG{D, hv, pred}, F, pred ? "gemv_Ginv_2" : "gemv_Ginv");
+  run_vm(ctx, GsX{D, hv, out, pred}, ctx->n, pred ? "vmap_gs_x_2" : "vmap_gs_x");
+}
+
+static void enqueue_body_gram(gdwd_ctx* ctx, bool use_sgs) {
+  const Dev& D = ctx->D;
+  const int64_t n = ctx->n;
+  MatView K{ctx->kmat.p, n, n, ctx->ldm};
+  run_zt(ctx, GsKAlpha{D}, K, "gemv_K_alpha");
+  run_vm(ctx, GsRhs{D}, n, "vmap_gs_rhs");
+  enqueue_solve_gram(ctx, D.h, D.xb, 0);
+  run_zt(ctx, OpZtNewton{D}, K, "gemv_K_newton");
+  if (use_sgs) {
+    run_vm(ctx, GsResid1{D}, n, "vmap_gs_resid");
+    run_zt(ctx, GsResid2{D}, K, "gemv_K_resid");
+  } else {
+    run_vm(ctx, OpSetReuse{D}, 1, "vmap_set_reuse");
+  }
+  enqueue_solve_gram(ctx, D.h2, D.x, 1);
+  run_vm(ctx, OpCopyIfReuse{D, D.xb, D.x}, n + 1, "vmap_copy_x");
+  run_zt(ctx, OpZtStore{D, D.x, D.ztw, 1}, K, "gemv_K_ztw_2");
+  run_vm(ctx, OpCopyIfReuse{D, D.ztwb, D.ztw}, n, "vmap_copy_ztw");
+  run_zt(ctx, GsStep2a{D}, K, "gemv_K_step2a");
+  run_vm(ctx, GsStep2b{D}, n, "vmap_gs_step2b");
+  run_zt(ctx, GsStep2c{D}, K, "gemv_K_step2c");
+  run_vm(ctx, OpStep3{D}, n, "vmap_step3_kkt");
+}
+
+// w, u, rho back in feature space (one pass over X for w,u and one for rho)
+static void enqueue_materialize(gdwd_ctx* ctx) {
+  if (!ctx->gram) return;
+  const Dev& D = ctx->D;
+  MatView Z = zview(ctx);
+  run_zmv(ctx, GsMaterialize2{D}, Z, "zmv_materialize");
+  run_zmv(ctx, GsMaterialize1{D}, Z, "zmv_materialize");
+}
+
 static int body_iterative(gdwd_ctx* ctx, bool use_sgs, int max_steps, int* psqmr_steps) {
   const Dev& D = ctx->D;
   MatView Z = zview(ctx);
@@ -747,7 +805,8 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   const int max_iter = cfg->max_iter;
 
   // ---- buffers ------------------------------------------------------------
-  const int NV = 10, MV = 13;
+  const int NV = 12, MV = 16;
+  const bool gram = (kind == GDWD_BACKEND_SMW2) && cfg->smw_gram_space;
   CK(ctx->nvec.ensure((size_t)NV * n));
   CK(ctx->mvec.ensure((size_t)MV * (m + 1)));
   CK(ctx->tabs.ensure((size_t)2 * (max_iter + 2) + (size_t)std::max<int64_t>(sched_len, 1)));
@@ -775,6 +834,15 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   D.u = mv; D.rho = mv + ms; D.h = mv + 2 * ms; D.h2 = mv + 3 * ms; D.xb = mv + 4 * ms; D.x = mv + 5 * ms;
   D.pr = mv + 6 * ms; D.pres = mv + 7 * ms; D.pq = mv + 8 * ms; D.pu = mv + 9 * ms; D.pd = mv + 10 * ms;
   D.pAd = mv + 11 * ms; D.pAq = mv + 12 * ms;
+  D.cres = nv + 10 * n; D.cdiff = nv + 11 * n;
+  D.bot = d;
+  D.wd = D.x; D.ud = D.u; D.rhod = D.rho;
+  if (gram) {
+    // coefficient vectors (n + 1 <= d + 2 slots) in the same buffers; the
+    // d-space outputs get their own slots
+    D.bot = n;
+    D.wd = mv + 13 * ms; D.ud = mv + 14 * ms; D.rhod = mv + 15 * ms;
+  }
   // persistent per-problem vectors: [colsq (d) | zy (d) | jac (m) | jy (n)]
   CK(ctx->colsq.ensure((size_t)d + (size_t)d + m + n + 8));
   D.zy = ctx->colsq.p + d;
@@ -810,7 +878,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   run_zmv(ctx, OpPlainZ{ctx->y.p, nullptr, const_cast<double*>(D.zy), nullptr}, Z, "zmv_zy");
   CK(cudaGetLastError());
   RC(build_factor(ctx, kind, mu2));
-  if (kind != GDWD_BACKEND_ITERATIVE) RC(ensure_scratch(ctx, ctx->fac_rows, ctx->fac_rows));
+  if (kind != GDWD_BACKEND_ITERATIVE) RC(ensure_scratch(ctx, ctx->fac_rows, ctx->fac_rows + 2));
   RC(ensure_scratch(ctx, n, d));
   // initial iterates (solver.py:447-454)
   fill(ctx, D.r, n, 1.0);
@@ -838,6 +906,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
 
   ctx->ps_per_iter.assign(max_iter + 1, 0.0);
   ctx->kind = kind;
+  ctx->gram = gram;
   ctx->use_sgs = cfg->use_sgs != 0;
   ctx->poll = std::max(1, cfg->poll_every);
   ctx->max_iter = max_iter;
@@ -852,7 +921,8 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
     cudaGraph_t graph;
     const int64_t before = ctx->launches;
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
-    enqueue_body_fixed(ctx, kind, ctx->use_sgs);
+    if (gram) enqueue_body_gram(ctx, ctx->use_sgs);
+    else enqueue_body_fixed(ctx, kind, ctx->use_sgs);
     CK(cudaStreamEndCapture(ctx->st, &graph));
     ctx->body_nodes = ctx->launches - before;
     ctx->launches = before;
@@ -883,6 +953,8 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
     } else if (ctx->gexec) {
       CK(cudaGraphLaunch(ctx->gexec, ctx->st));
       ctx->launches += ctx->body_nodes;
+    } else if (ctx->gram) {
+      enqueue_body_gram(ctx, ctx->use_sgs);
     } else {
       enqueue_body_fixed(ctx, ctx->kind, ctx->use_sgs);
     }
@@ -890,7 +962,10 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
     ctx->k_host = k + 1;
     if (ctx->prof) prof_flush(ctx);
     if (cb) {
-      run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");  // completes KKT (dual objective, gap) + stop test
+      // complete the KKT record (dual objective, gap) and the stop test
+      if (ctx->gram) run_zt(ctx, GsKAlpha{D}, MatView{ctx->kmat.p, ctx->n, ctx->n, ctx->ldm}, "gemv_K_alpha");
+      else run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
+      enqueue_materialize(ctx);
       CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
       CK(cudaStreamSynchronize(ctx->st));
       const Scal& s = *ctx->Sh;
@@ -940,7 +1015,9 @@ extern "C" int gdwd_solve_end(gdwd_ctx* ctx, gdwd_result* out) {
   const Dev& D = ctx->D;
   MatView Z = zview(ctx);
   // final pass: dual objective / gap / stop test of the last iteration
-  run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
+  if (ctx->gram) run_zt(ctx, GsKAlpha{D}, MatView{ctx->kmat.p, ctx->n, ctx->n, ctx->ldm}, "gemv_K_alpha");
+  else run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
+  enqueue_materialize(ctx);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_end, ctx->st));
   CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
@@ -964,7 +1041,7 @@ extern "C" int gdwd_solve_end(gdwd_ctx* ctx, gdwd_result* out) {
   out->setup_ms = ctx->setup_ms;
   out->loop_ms = ms_loop;
   double bet = 0.0;
-  CK(cudaMemcpy(&bet, D.x + ctx->d, sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&bet, D.wd + ctx->d, sizeof(double), cudaMemcpyDeviceToHost));
   out->beta = bet;
   for (int f = 0; f < 11; ++f) out->resid[f] = s.eta[f];
   return GDWD_OK;
@@ -1036,7 +1113,7 @@ extern "C" int gdwd_get_state(gdwd_ctx* ctx, double* r, double* xi, double* alph
   const Dev& D = ctx->D;
   const int64_t n = ctx->n, d = ctx->d;
   struct P { double* h; const double* dp; int64_t len; } items[] = {
-      {r, D.r, n}, {xi, D.xi, n}, {alpha, D.al, n}, {ztw, D.ztw, n}, {w, D.x, d}, {u, D.u, d}, {rho, D.rho, d}, {beta, D.x + d, 1}};
+      {r, D.r, n}, {xi, D.xi, n}, {alpha, D.al, n}, {ztw, D.ztw, n}, {w, D.wd, d}, {u, D.ud, d}, {rho, D.rhod, d}, {beta, D.wd + d, 1}};
   for (auto& it : items)
     if (it.h) CK(cudaMemcpyAsync(it.h, it.dp, it.len * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));

@@ -30,10 +30,12 @@ struct Scal {
   double smw_coef, smw_s2;
   double ps_tau, ps_rho, ps_theta, ps_alpha, ps_thnew, ps_cA, ps_cB, ps_rhonew, ps_resn;
   double ys;          // SMW: 1 + ybar^T J^{-1} ybar - 1
+  double ytzw;        // Gram space: y . ztw_bar (= zy . w_bar)
 };
 
 struct Dev {
   int64_t n, d, m;  // m = d + 1
+  int64_t bot;      // index of the scalar slot (beta, h_bot) in x/h vectors: d, or n in Gram space
   double C, q, mu, mu2, zscale, tau, yty, ynorm, kappa, e1, e2, qp1, one_c;
   double tol_feas, tol_cgap, tol_cap;
   int max_iter, sched_len;
@@ -41,6 +43,9 @@ struct Dev {
   double *r, *xi, *al, *ztw, *rnew, *dr, *ztwb, *s1, *g, *tq;
   double *u, *rho, *h, *h2, *xb, *x;
   double *pr, *pres, *pq, *pu, *pd, *pAd, *pAq;
+  // Gram-space SMW2: n-coefficient temporaries and the d-space outputs
+  double *cres, *cdiff;
+  double *wd, *ud, *rhod;
   const double *eps_tab, *tol_tab, *sched;
   double* hist;
   Scal* S;
@@ -111,6 +116,43 @@ GDWD_DEV double newton_margin(double a, double sigma, double q, double wt, doubl
 GDWD_DEV double np_max0(double x) { return isnan(x) ? x : (x > 0.0 ? x : 0.0); }   // np.maximum(x, 0)
 GDWD_DEV double np_min0(double x) { return isnan(x) ? x : (x < 0.0 ? x : 0.0); }   // np.minimum(x, 0)
 
+// Completes iteration k-1 once ||Z alpha||^2 (`zal2`) is known: dual
+// objective, gap, the stopping test (solver.py:293-304,334,548-554); then
+// commits sigma and opens the history row of iteration k.
+GDWD_DEV void finish_previous(const Dev& D, double zal2) {
+  Scal* S = D.S;
+  const int k = S->k;
+  if (k > 0) {
+    const double od = D.kappa * S->sdual - D.zscale * sqrt(zal2);
+    const double op = S->eta[9];
+    const double gap = fabs(op - od) / (1.0 + fabs(op) + fabs(od));
+    S->eta[10] = od;
+    S->eta[8] = gap;
+    double* hr = D.hist + (int64_t)(k - 1) * HIST_W;
+    hr[H_OBJD] = od;
+    hr[H_GAP] = gap;
+    const double* e = S->eta;
+    const double ep = fmax(fmax(e[3], e[4]), e[5]);
+    const double ed = fmax(e[6], e[7]);
+    const double ec = fmax(fmax(e[0], e[1]), e[2]);
+    if (fmax(ep, ed) < D.tol_feas && fmin(ec, gap) < D.tol_cgap && fmax(ec, gap) < D.tol_cap) {
+      S->stopped = 1;
+      S->converged = 1;
+      return;
+    }
+  }
+  if (k >= D.max_iter) {
+    S->stopped = 1;
+    return;
+  }
+  S->sigma = S->sigma_next;
+  double* hr = D.hist + (int64_t)k * HIST_W;
+  hr[H_SIGMA] = S->sigma;
+  hr[H_EPS] = D.eps_tab[k];
+  hr[H_REUSE] = 1.0;
+  hr[H_PSQMR] = 0.0;
+}
+
 // ---------------------------------------------------------------------------
 // KA: h = [-Z(xi - r - a/sigma) + mu^2 u + (mu/sigma) rho ; -y.rhs], fused
 // with Z alpha of the previous iteration (its dual objective, gap and the
@@ -132,38 +174,8 @@ struct OpRhsAlpha {
     da[0] += v[1] * v[1];
   }
   GDWD_DEV void fin(const double (&ns)[NN], const double (&ds)[ND]) const {
-    Scal* S = D.S;
-    D.h[D.d] = -ns[0];
-    const int k = S->k;
-    if (k > 0) {
-      const double od = D.kappa * S->sdual - D.zscale * sqrt(ds[0]);
-      const double op = S->eta[9];
-      const double gap = fabs(op - od) / (1.0 + fabs(op) + fabs(od));
-      S->eta[10] = od;
-      S->eta[8] = gap;
-      double* hr = D.hist + (int64_t)(k - 1) * HIST_W;
-      hr[H_OBJD] = od;
-      hr[H_GAP] = gap;
-      const double* e = S->eta;
-      const double ep = fmax(fmax(e[3], e[4]), e[5]);
-      const double ed = fmax(e[6], e[7]);
-      const double ec = fmax(fmax(e[0], e[1]), e[2]);
-      if (fmax(ep, ed) < D.tol_feas && fmin(ec, gap) < D.tol_cgap && fmax(ec, gap) < D.tol_cap) {
-        S->stopped = 1;
-        S->converged = 1;
-        return;
-      }
-    }
-    if (k >= D.max_iter) {
-      S->stopped = 1;
-      return;
-    }
-    S->sigma = S->sigma_next;
-    double* hr = D.hist + (int64_t)k * HIST_W;
-    hr[H_SIGMA] = S->sigma;
-    hr[H_EPS] = D.eps_tab[k];
-    hr[H_REUSE] = 1.0;
-    hr[H_PSQMR] = 0.0;
+    D.h[D.bot] = -ns[0];
+    finish_previous(D, ds[0]);
   }
 };
 
@@ -204,7 +216,7 @@ struct OpZtNewton {
   GDWD_DEV double wval(int64_t j) const { return D.xb[j]; }
   GDWD_DEV void row(int64_t i, double dot, double (&na)[NN]) const {
     const Scal* S = D.S;
-    const double sig = S->sigma, bb = D.xb[D.d];
+    const double sig = S->sigma, bb = D.xb[D.bot];
     D.ztwb[i] = dot;
     const double a = ((dot + D.y[i] * bb) + D.xi[i]) - D.al[i] / sig;
     const double rn = newton_margin(a, sig, D.q, D.wl[i], D.r[i], D.tol_tab[S->k]);
@@ -213,7 +225,7 @@ struct OpZtNewton {
     D.dr[i] = dri;
     na[0] += D.y[i] * dri;
   }
-  GDWD_DEV void fin(const double (&ns)[NN]) const { D.h2[D.d] = D.h[D.d] + ns[0]; }
+  GDWD_DEV void fin(const double (&ns)[NN]) const { D.h2[D.bot] = D.h[D.bot] + ns[0]; }
 };
 
 // KC: h2 = h + [Z dr; y.dr], reuse residual ||h2 - A [w_bar; beta_bar]||
@@ -227,7 +239,7 @@ struct OpDrZtwb {
     t[1] = D.ztwb[i];
   }
   GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&da)[ND]) const {
-    const double bb = D.xb[D.d];
+    const double bb = D.xb[D.bot];
     const double h2j = D.h[j] + v[0];
     D.h2[j] = h2j;
     const double ax = (v[1] + D.mu2 * D.xb[j]) + D.zy[j] * bb;
@@ -237,8 +249,8 @@ struct OpDrZtwb {
   }
   GDWD_DEV void fin(const double (&)[NN], const double (&ds)[ND]) const {
     Scal* S = D.S;
-    const double bb = D.xb[D.d];
-    const double rb = D.h2[D.d] - (ds[1] + D.yty * bb);
+    const double bb = D.xb[D.bot];
+    const double rb = D.h2[D.bot] - (ds[1] + D.yty * bb);
     const double rr = hypot(sqrt(ds[0]), rb);
     const int reuse = rr <= 5.0 * D.eps_tab[S->k];
     S->reuse = reuse;
@@ -314,7 +326,7 @@ struct OpStep3 {
   Dev D;
   GDWD_DEV bool skip() const { return D.S->stopped; }
   GDWD_DEV void elem(int64_t i, double (&a)[NR]) const {
-    const double sig = D.S->sigma, bet = D.x[D.d];
+    const double sig = D.S->sigma, bet = D.x[D.bot];
     const double C = D.C;
     const double rr = D.rnew[i];
     D.r[i] = rr;
@@ -363,7 +375,7 @@ struct OpStep3 {
     double* hr = D.hist + (int64_t)k * HIST_W;
     for (int f = 0; f < 8; ++f) hr[f] = e[f];
     hr[H_OBJP] = e[9];
-    hr[H_BETA] = D.x[D.d];
+    hr[H_BETA] = D.x[D.bot];
     const double ep = fmax(fmax(e[3], e[4]), e[5]);
     const double ed = fmax(e[6], e[7]);
     if (D.sched && k + 1 < D.sched_len) S->sigma_next = D.sched[k + 1];
@@ -385,7 +397,7 @@ struct OpSmwS1 {  // s1 = Z^T (h/mu^2) + y t2
   GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
   GDWD_DEV double wval(int64_t j) const { return hv[j] / D.mu2; }
   GDWD_DEV void row(int64_t i, double dot, double (&)[NN]) const {
-    const double t2 = hv[D.d] / D.yty;
+    const double t2 = hv[D.bot] / D.yty;
     D.s1[i] = dot + D.y[i] * t2;
   }
   GDWD_DEV void fin(const double (&)[NN]) const {}
@@ -404,7 +416,7 @@ struct OpSmwG {  // g = G^{-1} s1 ; ybar.J^{-1}s
     na[0] += (D.y[i] / D.ynorm) * dot;
   }
   GDWD_DEV void fin(const double (&ns)[NN]) const {
-    const double t2 = hv[D.d] / D.yty;
+    const double t2 = hv[D.bot] / D.yty;
     const double s2 = D.ynorm * t2;
     const double bd = ns[0] + (-s2);
     D.S->smw_coef = bd / D.S->ys;
@@ -430,8 +442,162 @@ struct OpSmwP {  // p1 = Z v[:n]; x = [t1 - p1/mu^2 ; t2 - p2/|y|^2]
   GDWD_DEV void fin(const double (&ns)[NN], const double (&)[ND]) const {
     const double vn = (-D.S->smw_s2) - D.S->smw_coef * (-1.0);
     const double p2 = ns[0] + D.ynorm * vn;
-    out[D.d] = hv[D.d] / D.yty - p2 / D.yty;
+    out[D.bot] = hv[D.bot] / D.yty - p2 / D.yty;
   }
+};
+
+
+// ---------------------------------------------------------------------------
+// Gram-space SMW2.  Every d-vector of the SMW2 iteration stays in span(Z~)
+// (u = rho = w = 0 initially; h, w_bar, w, g, u, rho are linear combinations
+// of Z~ columns), so each is carried as n coefficients c with v = Z~ c and
+// every Z~ / Z~^T product becomes a GEMV with the n x n Gram K = Z~^T Z~
+// (L2-resident) instead of a pass over X.  D.h/h2/xb/x hold coefficients
+// (+ the scalar slot at D.bot = n); D.u / D.rho hold the coefficients of u
+// and rho.  Norms are quadratic forms c^T K c of difference vectors formed
+// first (no cancellation at large sigma).
+// ---------------------------------------------------------------------------
+struct GsKAlpha {  // ||Z alpha||^2 = alpha^T K alpha, then finish iteration k-1
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV double wval(int64_t j) const { return D.al[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&na)[NN]) const { na[0] += D.al[i] * dot; }
+  GDWD_DEV void fin(const double (&ns)[NN]) const { finish_previous(D, ns[0]); }
+};
+
+struct GsRhs {  // c_h = -rhs + mu^2 c_u + (mu/sigma) c_rho ; h_bot = -y.rhs
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void elem(int64_t i, double (&a)[NR]) const {
+    const double sig = D.S->sigma;
+    const double rhs = (D.xi[i] - D.r[i]) - D.al[i] / sig;
+    D.h[i] = (-rhs + D.mu2 * D.u[i]) + (D.mu / sig) * D.rho[i];
+    a[0] += D.y[i] * rhs;
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const { D.h[D.bot] = -s[0]; }
+};
+
+struct GsX {  // x = [t1 - v/mu^2 ; t2 - p2/|y|^2] in coefficients (subsolvers.py:145-151)
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  const double* hv;
+  double* out;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void elem(int64_t i, double (&a)[NR]) const {
+    const double v = D.g[i] - D.S->smw_coef * D.jy[i];
+    out[i] = hv[i] / D.mu2 - v / D.mu2;
+    a[0] += D.y[i] * v;
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const {
+    const double vn = (-D.S->smw_s2) - D.S->smw_coef * (-1.0);
+    const double p2 = s[0] + D.ynorm * vn;
+    out[D.bot] = hv[D.bot] / D.yty - p2 / D.yty;
+  }
+};
+
+struct GsResid1 {  // h2 = h + [dr; y.dr]; c_res = c_h2 - (ztw_bar + mu^2 c_xb + y beta_bar)
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void elem(int64_t i, double (&a)[NR]) const {
+    const double bb = D.xb[D.bot];
+    const double h2 = D.h[i] + D.dr[i];
+    D.h2[i] = h2;
+    const double ax = (D.ztwb[i] + D.mu2 * D.xb[i]) + D.y[i] * bb;
+    D.cres[i] = h2 - ax;
+    a[0] += D.y[i] * D.ztwb[i];
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const { D.S->ytzw = s[0]; }
+};
+
+struct GsResid2 {  // ||res_top||^2 = c_res^T K c_res ; reuse test (solver.py:516-524)
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV double wval(int64_t j) const { return D.cres[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&na)[NN]) const { na[0] += D.cres[i] * dot; }
+  GDWD_DEV void fin(const double (&ns)[NN]) const {
+    Scal* S = D.S;
+    const double bb = D.xb[D.bot];
+    const double rb = D.h2[D.bot] - (S->ytzw + D.yty * bb);
+    const double rr = hypot(sqrt(ns[0] > 0.0 ? ns[0] : 0.0), rb);
+    const int reuse = rr <= 5.0 * D.eps_tab[S->k];
+    S->reuse = reuse;
+    if (!reuse) S->double_count += 1;
+    D.hist[(int64_t)S->k * HIST_W + H_REUSE] = reuse ? 1.0 : 0.0;
+  }
+};
+
+struct GsStep2a {  // g = w - rho/(sigma mu) ; ||g||^2 = c_g^T K c_g
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV double cg(int64_t j) const { return D.x[j] - D.rho[j] / (D.S->sigma * D.mu); }
+  GDWD_DEV double wval(int64_t j) const { return cg(j); }
+  GDWD_DEV void row(int64_t i, double dot, double (&na)[NN]) const { na[0] += cg(i) * dot; }
+  GDWD_DEV void fin(const double (&ns)[NN]) const { D.S->gnorm = sqrt(ns[0] > 0.0 ? ns[0] : 0.0); }
+};
+
+struct GsStep2b {  // u, rho updates in coefficients; c_w - c_u ; ||w||^2 = c_w . ztw
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void elem(int64_t i, double (&a)[NR]) const {
+    const double sig = D.S->sigma, gn = D.S->gnorm;
+    const double wi = D.x[i];
+    const double gi = wi - D.rho[i] / (sig * D.mu);
+    const double ui = (gn <= D.zscale) ? gi : (D.zscale / gn) * gi;
+    D.u[i] = ui;
+    D.rho[i] = D.rho[i] - ((D.tau * sig) * D.mu) * (wi - ui);
+    D.cdiff[i] = wi - ui;
+    a[0] += wi * D.ztw[i];
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const { D.S->w2 = s[0]; }
+};
+
+struct GsStep2c {  // ||w - u||^2 = (c_w - c_u)^T K (c_w - c_u)
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV double wval(int64_t j) const { return D.cdiff[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&na)[NN]) const { na[0] += D.cdiff[i] * dot; }
+  GDWD_DEV void fin(const double (&ns)[NN]) const { D.S->wu2 = ns[0] > 0.0 ? ns[0] : 0.0; }
+};
+
+// d-space iterates from coefficients (end of solve / callback): w, u (+beta)
+struct GsMaterialize2 {
+  static constexpr int R = 2, NN = 1, ND = 1;
+  Dev D;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV void input(int64_t i, double (&t)[R], double (&)[NN]) const {
+    t[0] = D.x[i];
+    t[1] = D.u[i];
+  }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&)[ND]) const {
+    D.wd[j] = v[0];
+    D.ud[j] = v[1];
+  }
+  GDWD_DEV void fin(const double (&)[NN], const double (&)[ND]) const { D.wd[D.d] = D.x[D.bot]; }
+};
+
+struct GsMaterialize1 {  // rho
+  static constexpr int R = 1, NN = 1, ND = 1;
+  Dev D;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV void input(int64_t i, double (&t)[R], double (&)[NN]) const { t[0] = D.rho[i]; }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&)[ND]) const { D.rhod[j] = v[0]; }
+  GDWD_DEV void fin(const double (&)[NN], const double (&)[ND]) const {}
 };
 
 // ---------------------------------------------------------------------------
@@ -464,13 +630,13 @@ struct OpInitResidual {
   GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
   GDWD_DEV void input(int64_t i, double (&t)[R], double (&)[NN]) const { t[0] = D.tq[i]; }
   GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&da)[ND]) const {
-    const double ax = (v[0] + D.mu2 * x0[j]) + D.zy[j] * x0[D.d];
+    const double ax = (v[0] + D.mu2 * x0[j]) + D.zy[j] * x0[D.bot];
     D.pr[j] = b[j] - ax;
     da[0] += D.zy[j] * x0[j];
   }
   GDWD_DEV void fin(const double (&)[NN], const double (&ds)[ND]) const {
-    const double ax = ds[0] + D.yty * x0[D.d];
-    D.pr[D.d] = b[D.d] - ax;
+    const double ax = ds[0] + D.yty * x0[D.bot];
+    D.pr[D.bot] = b[D.bot] - ax;
   }
 };
 
@@ -522,16 +688,16 @@ struct OpPsApply {
   GDWD_DEV void input(int64_t i, double (&t)[R], double (&)[NN]) const { t[0] = D.tq[i]; }
   GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&da)[ND]) const {
     const double qj = D.pq[j];
-    const double aq = (v[0] + D.mu2 * qj) + D.zy[j] * D.pq[D.d];
+    const double aq = (v[0] + D.mu2 * qj) + D.zy[j] * D.pq[D.bot];
     D.pAq[j] = aq;
     da[0] += D.zy[j] * qj;
     da[1] += qj * aq;
   }
   GDWD_DEV void fin(const double (&)[NN], const double (&ds)[ND]) const {
     Scal* S = D.S;
-    const double qd = D.pq[D.d];
+    const double qd = D.pq[D.bot];
     const double aqd = ds[0] + D.yty * qd;
-    D.pAq[D.d] = aqd;
+    D.pAq[D.bot] = aqd;
     const double sg = ds[1] + qd * aqd;
     if (fabs(sg) < TINY) {
       S->ps_brk = 1;

@@ -25,9 +25,15 @@ def run_traj(prob, cfg, full, idx_d=None, idx_n=None, **kw):
 
     def cb(st, res):
         rows.append([getattr(res, f) for f in G.solver.KKT_FIELDS] + [st.sigma, st.beta])
-        # magnitudes of the summands behind the cancellation-prone eta_c1/c2
-        scales.append([np.abs(prob.y * st.alpha).sum() / (1 + prob.C),
-                       (np.abs(st.xi) * (prob.C * prob.e + np.abs(st.alpha))).sum() / (1 + prob.C)])
+        # magnitudes of the vectors each normalised residual is formed from
+        # (the residuals are differences / thresholded sums that can cancel)
+        oc = 1 + prob.C
+        scales.append([np.abs(prob.y * st.alpha).sum() / oc,
+                       (np.abs(st.xi) * (prob.C * prob.e + np.abs(st.alpha))).sum() / oc,
+                       0.0,
+                       (np.linalg.norm(st.r) + np.linalg.norm(st.xi) + abs(st.beta) * np.sqrt(prob.n)) / oc,
+                       np.linalg.norm(st.w) / oc, np.linalg.norm(st.w) / oc,
+                       np.linalg.norm(st.alpha) / oc, (np.linalg.norm(st.alpha) + prob.C * np.sqrt(prob.n)) / oc])
         for k in vecs:
             v = np.array(getattr(st, k), copy=True)
             if not full:
@@ -55,13 +61,13 @@ def test_trajectory_first20(case):
             assert relerr(got[i], ref[i]) < TOL20, (key, i)
     ref_h = tr["hist"][:k]
     # KKT scalars, sigma, beta
-    # eta_c1 = |y.alpha|/(1+C) and eta_c2 = |xi.(Ce-alpha)|/(1+C) are sums that
-    # cancel (to ~1e-14 at times): their error scales with the summands'
-    # magnitude, so those two columns are compared against sum |terms|.
+    # Each normalised residual is a difference or thresholded sum that can
+    # cancel far below its inputs (eta_c1 = |y.alpha|/(1+C) sits at 1e-14 at
+    # times), so its error bound is 1e-9 x the magnitude of its inputs.
     sc = run_traj.scales[:k]
     for c in list(range(11)) + [11, 12]:
         err = np.abs(h[:k, c] - ref_h[:, c])
-        floor = 1e-9 * sc[:, c] if c < 2 else 0.0
+        floor = 1e-9 * sc[:, c] if c < 8 else 0.0
         assert np.all(err <= 1e-9 * np.abs(ref_h[:, c]) + floor + 1e-11), (c, err.max())
     assert np.array_equal(h[:k, 11], ref_h[:, 11])  # sigma sequence identical
 
@@ -82,10 +88,27 @@ def test_full_run_counters(case):
     assert abs(out.final_state.beta - float(tr["final_beta"])) <= 1e-6 * max(1.0, abs(float(tr["final_beta"])))
 
 
-def test_graph_mode_equals_callback_mode():
-    tr = load_traj("tiny_direct")
+@pytest.mark.parametrize("case", ["tiny_smw2", "smw2_natural"])
+def test_smw2_x_space_first20(case):
+    """SMW2 iterated as passes over X (smw_gram_space=False) also matches."""
+    tr = load_traj(case)
     prob = problem_for(tr)
-    cfg = G.SolverConfig(q=prob.q, max_iter=60, backend=G.Backend.DIRECT)
+    cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]), backend=G.Backend.SMW2)
+    out, h, vecs = run_traj(prob, cfg, bool(tr["full"]), tr["idx_d"], tr["idx_n"], smw_gram_space=False)
+    for key in ("w", "u", "rho", "r", "xi", "alpha"):
+        for i in range(20):
+            assert relerr(vecs[key][i], tr["it_" + key][i]) < TOL20, (key, i)
+
+
+def test_graph_mode_equals_callback_mode():
+    for case, be in (("tiny_direct", G.Backend.DIRECT), ("tiny_smw2", G.Backend.SMW2)):
+        _graph_vs_callback(case, be)
+
+
+def _graph_vs_callback(case, be):
+    tr = load_traj(case)
+    prob = problem_for(tr)
+    cfg = G.SolverConfig(q=prob.q, max_iter=60, backend=be)
     a = G.sgs_admm_solve(prob, cfg, use_graph=True)
     b = G.sgs_admm_solve(prob, cfg, use_graph=False)
     c, _, _ = run_traj(prob, cfg, True)
