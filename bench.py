@@ -142,16 +142,17 @@ class Dist:
 # ---------------------------------------------------------------------------
 # algorithmic bytes per launch
 # ---------------------------------------------------------------------------
-def kernel_bytes(tag: str, n: int, d: int) -> float | None:
-    x = 8.0 * n * d
-    if tag.startswith("zmv_rhs_alpha") or tag.startswith("zmv_dr_ztwb"):
-        return x + 8.0 * (2 * n + 2 * d) + 8.0 * 3 * n  # 2 RHS in, 2 d-vectors out, inputs read
-    if tag.startswith("zmv_smw_p"):
-        return x + 8.0 * (3 * n + 2 * d)
-    if tag.startswith("ztmv_newton"):
-        return x + 8.0 * (d + 9 * n)  # w in; ztw, r, xi, alpha, y, w_l read, r+, dr, ztw out
-    if tag.startswith("ztmv_smw_s1") or tag.startswith("ztmv_ztw"):
-        return x + 8.0 * (d + 2 * n)
+def kernel_bytes(tag: str, n: int, d: int, nnz: int | None = None) -> float | None:
+    """Algorithmic HBM bytes of one launch (roofline section):
+    the matrix once plus the vectors read/written.  Sparse X: 12 B per
+    stored entry (f64 value + int32 index) per orientation."""
+    x = 8.0 * n * d if nnz is None else 12.0 * nnz + 8.0 * (max(n, d) + 1)
+    if tag.startswith("zmv_"):
+        return x + 8.0 * (5 * n + 2 * d)   # up to 2 RHS in (+ inputs), 2 d-vectors out
+    if tag.startswith("ztmv_"):
+        return x + 8.0 * (d + 6 * n)       # w in; per-sample epilogue vectors
+    if tag.startswith("sp_prep"):
+        return 8.0 * 6 * n
     if tag.startswith("gemv_Ginv") or tag.startswith("gemv_K"):
         return 8.0 * n * n + 8.0 * 3 * n
     if tag.startswith("gemv_Ainv"):
@@ -175,6 +176,7 @@ def run_b200(args, dist: Dist):
     prob = synth.make_problem(cfg_syn, args.seed)
     gen_s = time.perf_counter() - t0
     n, d = prob.n, prob.d
+    nnz = None if prob.z_tilde.is_dense else prob.z_tilde.nnz
     K, W = args.steps, args.warmup
     total = W + K
     conf = make_config(G, prob, total + 1)
@@ -224,18 +226,19 @@ def run_b200(args, dist: Dist):
     kernels = []
     for tag, (cnt, tot) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
         avg = tot / cnt
-        b = kernel_bytes(tag, n, d)
+        b = kernel_bytes(tag, n, d, nnz)
         kernels.append({"tag": tag, "launches": cnt, "avg_us": round(avg * 1e3, 2), "share": round(tot / prof_total, 4),
                         "gbs": round(b / (avg * 1e-3) / 1e9, 1) if b else None})
     peak, peak_kind = peaks()
     top = next(k for k in kernels if k["gbs"] is not None)
     x_tags = [k for k in kernels if k["tag"].startswith(("zmv", "ztmv", "gemv"))]
-    x_bytes_iter = sum(kernel_bytes(k["tag"], n, d) * k["launches"] for k in x_tags) / prof_iters
+    x_bytes_iter = sum(kernel_bytes(k["tag"], n, d, nnz) * k["launches"] for k in x_tags
+                       if kernel_bytes(k["tag"], n, d, nnz)) / prof_iters
     roofline = {"bound": "hbm", "kernel": top["tag"], "achieved": top["gbs"], "peak": peak, "unit": "GB/s",
                 "frac": round(top["gbs"] / peak, 4), "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
                 "traffic": None,
                 "step_x_stream_gbs": round(x_bytes_iter / (step_ms * 1e-3) / 1e9, 1),
-                "algorithmic_bytes_per_launch": kernel_bytes(top["tag"], n, d)}
+                "algorithmic_bytes_per_launch": kernel_bytes(top["tag"], n, d, nnz)}
 
     # ---- end to end through the public API ------------------------------------
     e2e = None
@@ -246,11 +249,12 @@ def run_b200(args, dist: Dist):
         t1 = time.perf_counter()
         out = G.sgs_admm_solve(prob2, conf2, device=device)
         e2e_s = dist.max(time.perf_counter() - t1)
-        h2d = 8.0 * (n * d + 3 * n)
+        h2d = (8.0 * n * d if nnz is None else 16.0 * nnz + 8.0 * (n + 1)) + 8.0 * 3 * n
         d2h = 8.0 * (4 * n + 3 * d + 1 + 16 * out.iterations)
         e2e = {"value": round(dist.world * out.iterations / e2e_s, 3), "unit": UNIT,
                "h2d_bytes_per_step": round(h2d / out.iterations), "d2h_bytes_per_step": round(d2h / out.iterations),
                "seconds": round(e2e_s, 4), "iterations": out.iterations,
+               "breakdown": {k: round(v, 5) for k, v in (out.timings or {}).items()},
                "note": "sgs_admm_solve from host numpy buffers: X upload, FP64 DMMA Gram + Cholesky inverse, "
                        "iterations, state download"}
         G.solver.device_problem(prob2, device).close()

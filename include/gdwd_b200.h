@@ -97,6 +97,8 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
 /* Sparse Z~ in the reference's CSC layout (int64 colptr/rowidx). */
 int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx, const double* values,
                     int64_t d, int64_t n);
+/* ||Z~||_F^2, reduced on the device at upload (frobenius_norm, sparse.py:63). */
+int gdwd_frobenius_sq(gdwd_ctx* ctx, double* out);
 /* ProblemData vectors and scalars (solver.py:60-71); all length n. */
 int gdwd_set_problem(gdwd_ctx* ctx, const double* y, const double* e, const double* weights, double C,
                      double q, double z_scale);

@@ -26,7 +26,7 @@ SYMBOLS = [
     "gdwd_upload_csc", "gdwd_set_problem", "gdwd_matvec", "gdwd_matvec_t", "gdwd_solve", "gdwd_get_state",
     "gdwd_get_history", "gdwd_newton_sweep", "gdwd_chol_inverse", "gdwd_gram", "gdwd_psqmr_dense",
     "gdwd_solve_begin", "gdwd_solve_iterate", "gdwd_solve_end", "gdwd_time_iterations", "gdwd_set_profile",
-    "gdwd_get_profile", "gdwd_reset_counters",
+    "gdwd_get_profile", "gdwd_reset_counters", "gdwd_frobenius_sq",
 ]
 
 
@@ -82,6 +82,7 @@ def _declare(lib):
         "gdwd_set_profile": (C.c_int, [vp, C.c_int32]),
         "gdwd_get_profile": (C.c_int, [vp, C.c_char_p, _I64, C.POINTER(C.c_int64)]),
         "gdwd_reset_counters": (C.c_int, [vp]),
+        "gdwd_frobenius_sq": (C.c_int, [vp, _P]),
         "gdwd_get_state": (C.c_int, [vp, _P, _P, _P, _P, _P, _P, _P, _P]),
         "gdwd_get_history": (C.c_int, [vp, _P, _I64, C.POINTER(C.c_int64)]),
         "gdwd_newton_sweep": (C.c_int, [C.c_int32, _I64, _P, C.c_double, C.c_double, _P, _P, C.c_double, C.c_int32,

@@ -14,7 +14,10 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <map>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -107,6 +110,10 @@ struct gdwd_ctx {
   double* Zs = nullptr;
   bool has_problem = false;
   double C = 0, q = 0, zscale = 0, yty = 0;
+  double fro2 = -1.0;  // ||Z~||_F^2 (device reduction at upload)
+  double* pin[2] = {nullptr, nullptr};  // pinned staging for uploads
+  cudaEvent_t pin_ev[2] = {nullptr, nullptr};
+  size_t pin_bytes = 0;
   // sparse Z~: CSC by sample (Z^T w) and CSR by feature (Z t), int32 indices
   bool has_sparse = false;
   int64_t nnz = 0;
@@ -321,6 +328,21 @@ __global__ void assemble_direct_kernel(double* A, int64_t ld, int64_t d, const d
   }
 }
 
+// sum of squares over rows x cols (row stride ld) into *out, deterministic
+struct OpSumSq {
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  const double* a;
+  int64_t cols, ld;
+  double* out;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV void elem(int64_t idx, double (&acc)[NR]) const {
+    const double v = a[(idx / cols) * ld + idx % cols];
+    acc[0] += v * v;
+  }
+  GDWD_DEV void fin(const double (&sum)[NR]) const { *out = sum[0]; }
+};
+
 // G = K / mu^2 + I (subsolvers.py:109-110: gram / mu_sq, then += 1 on the diagonal)
 __global__ void g_from_k_kernel(const double* K, double* G, int64_t n, int64_t ld, double mu2) {
   const int64_t tot = n * n;
@@ -339,6 +361,73 @@ __global__ void fill_kernel(double* p, int64_t n, double v) {
 
 static void fill(gdwd_ctx* ctx, double* p, int64_t n, double v) {
   fill_kernel<<<vm_grid(n), 256, 0, ctx->st>>>(p, n, v);
+}
+
+// Host -> device copy of the [n][d] sample matrix into rows of stride ld.
+// Default: one pageable 2-D copy (~10 GB/s measured on the B200 hosts).
+// GDWD_UPLOAD=staged stages through two
+// pinned 64 MB buffers (host threads copy chunk k+1 while the DMA engine
+// drains chunk k); GDWD_UPLOAD=register page-locks the source in place.
+// (Both measured slower per call: pinned allocation / registration cost.)
+static int upload_rows(gdwd_ctx* ctx, const double* src, int64_t d, int64_t n, int64_t ld) {
+  const char* mode = getenv("GDWD_UPLOAD");
+  const size_t row_b = (size_t)d * sizeof(double);
+  const size_t total = row_b * (size_t)n;
+  if (!mode || !strcmp(mode, "pageable")) {
+    CK(cudaMemcpy2DAsync(ctx->Zs, ld * sizeof(double), src, row_b, row_b, n, cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return GDWD_OK;
+  }
+  if (mode && !strcmp(mode, "register")) {
+    CK(cudaHostRegister((void*)src, total, cudaHostRegisterReadOnly));
+    cudaError_t e = cudaMemcpy2DAsync(ctx->Zs, ld * sizeof(double), src, row_b, row_b, n, cudaMemcpyHostToDevice, ctx->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
+    cudaHostUnregister((void*)src);
+    CK(e);
+    return GDWD_OK;
+  }
+  const size_t chunk_rows = std::max<size_t>(1, ((size_t)64 << 20) / row_b);
+  if (!ctx->pin[0]) {
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaMallocHost(&ctx->pin[b], (size_t)64 << 20 < row_b ? row_b : (size_t)64 << 20));
+      CK(cudaEventCreateWithFlags(&ctx->pin_ev[b], cudaEventDisableTiming));
+    }
+    ctx->pin_bytes = (size_t)64 << 20 < row_b ? row_b : (size_t)64 << 20;
+  }
+  if (chunk_rows * row_b > ctx->pin_bytes) return set_err(ctx, GDWD_ERR_CUDA, "staging buffer too small");
+  const unsigned nthr = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  int b = 0;
+  bool used[2] = {false, false};
+  for (int64_t r0 = 0; r0 < n; r0 += (int64_t)chunk_rows, b ^= 1) {
+    const int64_t rows = std::min<int64_t>((int64_t)chunk_rows, n - r0);
+    if (used[b]) CK(cudaEventSynchronize(ctx->pin_ev[b]));
+    const char* s0 = (const char*)(src + r0 * d);
+    char* d0 = (char*)ctx->pin[b];
+    const size_t bytes = (size_t)rows * row_b;
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nthr; ++t) {
+      const size_t lo = bytes * t / nthr, hi = bytes * (t + 1) / nthr;
+      th.emplace_back([=] { memcpy(d0 + lo, s0 + lo, hi - lo); });
+    }
+    for (auto& x : th) x.join();
+    CK(cudaMemcpy2DAsync(ctx->Zs + r0 * ld, ld * sizeof(double), ctx->pin[b], row_b, row_b, rows,
+                         cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaEventRecord(ctx->pin_ev[b], ctx->st));
+    used[b] = true;
+  }
+  CK(cudaStreamSynchronize(ctx->st));
+  return GDWD_OK;
+}
+
+static int compute_fro2(gdwd_ctx* ctx, const double* a, int64_t rows, int64_t cols, int64_t ld) {
+  double* dv = nullptr;
+  CK(cudaMalloc(&dv, sizeof(double)));
+  run_vm(ctx, OpSumSq{a, cols, ld, dv}, rows * cols, "vmap_fro2");
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&ctx->fro2, dv, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  cudaFree(dv);
+  return GDWD_OK;
 }
 
 static void free_sparse(gdwd_ctx* ctx) {
@@ -391,6 +480,10 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   for (cudaEvent_t e : {ctx->ev_begin, ctx->ev_loop, ctx->ev_end, ctx->poll_ev[0], ctx->poll_ev[1]})
     if (e) cudaEventDestroy(e);
   if (ctx->poll_flag) cudaFreeHost(ctx->poll_flag);
+  for (int b = 0; b < 2; ++b) {
+    if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
+    if (ctx->pin_ev[b]) cudaEventDestroy(ctx->pin_ev[b]);
+  }
   if (ctx->tickets) cudaFree(ctx->tickets);
   if (ctx->S) cudaFree(ctx->S);
   if (ctx->Sh) cudaFreeHost(ctx->Sh);
@@ -408,16 +501,15 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
   ctx->Zs = nullptr;
   CK(cudaMalloc(&ctx->Zs, (size_t)n * ld * sizeof(double)));
   if (ld != d) CK(cudaMemsetAsync(ctx->Zs, 0, (size_t)n * ld * sizeof(double), ctx->st));
-  CK(cudaMemcpy2DAsync(ctx->Zs, ld * sizeof(double), samples, d * sizeof(double), d * sizeof(double), n,
-                       cudaMemcpyHostToDevice, ctx->st));
-  CK(cudaStreamSynchronize(ctx->st));
+  RC(upload_rows(ctx, samples, d, n, ld));
   ctx->n = n;
   ctx->d = d;
   ctx->ldz = ld;
   ctx->has_dense = true;
   ctx->has_problem = false;
   ctx->data_gen++;
-  return ensure_scratch(ctx, n, d);
+  RC(ensure_scratch(ctx, n, d));
+  return compute_fro2(ctx, ctx->Zs, n, d, ld);
 }
 
 int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx, const double* values, int64_t d,
@@ -478,7 +570,8 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
   ctx->has_sparse = true;
   ctx->has_problem = false;
   ctx->data_gen++;
-  return ensure_scratch(ctx, n, d);
+  RC(ensure_scratch(ctx, n, d));
+  return nnz > 0 ? compute_fro2(ctx, ctx->csc_val, 1, nnz, nnz) : (ctx->fro2 = 0.0, GDWD_OK);
 }
 
 // DIRECT / SMW2 on sparse input: materialise the dense sample-major copy once
@@ -852,8 +945,9 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   D.hist = ctx->histb.p;
 
   // ---- tables (host pow == Python's float pow) -------------------------------
-  const double eps_c = cfg->epsilon_c;
-  if (isnan(eps_c)) return set_err(ctx, GDWD_ERR_VALUE, "epsilon_c must be supplied by the host layer");
+  // eps constant (solver.py:441-445): 1 / max(1, ||Z~||_F), norm reduced on
+  // the device at upload
+  const double eps_c = isnan(cfg->epsilon_c) ? 1.0 / std::max(1.0, sqrt(ctx->fro2)) : cfg->epsilon_c;
   std::vector<double> tab(2 * (size_t)(max_iter + 2) + (size_t)std::max<int64_t>(sched_len, 1), 0.0);
   const double sqrt_n = sqrt((double)n);
   for (int k = 0; k < max_iter + 2; ++k) {
@@ -1053,6 +1147,12 @@ extern "C" int gdwd_solve(gdwd_ctx* ctx, const gdwd_config* cfg, const double* s
   RC(gdwd_solve_begin(ctx, cfg, sched, sched_len));
   RC(gdwd_solve_iterate(ctx, cfg->max_iter, cb, user, nullptr, nullptr));
   return gdwd_solve_end(ctx, out);
+}
+
+extern "C" int gdwd_frobenius_sq(gdwd_ctx* ctx, double* out) {
+  if (!ctx || !out || ctx->fro2 < 0) return set_err(ctx, GDWD_ERR_VALUE, "no data uploaded");
+  *out = ctx->fro2;
+  return GDWD_OK;
 }
 
 extern "C" int gdwd_set_profile(gdwd_ctx* ctx, int32_t enable) {

@@ -210,6 +210,7 @@ class SolveResult:
     history: Optional[np.ndarray] = None
     setup_ms: float = 0.0
     loop_ms: float = 0.0
+    timings: Optional[dict] = None
 
 
 # ---------------------------------------------------------------------------
@@ -362,6 +363,12 @@ class DeviceProblem:
         arr["beta"] = float(b[0])
         return arr
 
+    def eps_c(self) -> float:
+        """1/max(1, ||Z~||_F) from the device-side norm (solver.py:441-445)."""
+        fro2 = C.c_double()
+        _check(self.lib.gdwd_frobenius_sq(self.ctx, C.byref(fro2)), self.ctx, "frobenius")
+        return 1.0 / max(1.0, math.sqrt(fro2.value))
+
     def history(self, rows: int) -> np.ndarray:
         h = np.zeros((max(rows, 1), 16))
         nr = C.c_int64()
@@ -383,14 +390,11 @@ def device_problem(data: ProblemData, device: Optional[int] = None) -> DevicePro
 
 
 def _eps_c(data: ProblemData, config: SolverConfig) -> float:
-    """solver.py:441-445 (computed on the host exactly as the reference)."""
+    """solver.py:441-445.  NaN asks the library for the default
+    1/max(1, ||Z~||_F), with the norm reduced on the device at upload."""
     if config.epsilon_c is not None:
         return float(config.epsilon_c)
-    fro = getattr(data, "_gdwd_fro", None)
-    if fro is None:
-        fro = data.z_tilde.frobenius_norm()
-        object.__setattr__(data, "_gdwd_fro", fro)
-    return 1.0 / max(1.0, fro)
+    return float("nan")
 
 
 # ---------------------------------------------------------------------------
@@ -410,6 +414,7 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
     in sample-coefficient space with the n x n Gram instead of passes over X)."""
     t_start = time.perf_counter()
     dp = device_problem(data, device)
+    t_up = time.perf_counter()
     lib = dp.lib
     kind = config.backend.resolve(data.n, data.d)
     eps_c = _eps_c(data, config)
@@ -429,7 +434,7 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
             st = dp.state()
             res = KKTResiduals(*[float(resid_p[i]) for i in range(11)])
             state = SolverState(st["r"], st["xi"], st["alpha"], st["w"], st["u"], st["rho"], float(beta),
-                                float(sigma), int(it), eps_c)
+                                float(sigma), int(it), eps_c if eps_c == eps_c else dp.eps_c())
             callback(state, res)
             return 0
         except BaseException as exc:  # propagate after the C call returns
@@ -444,13 +449,14 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
         if rc == _lib.ERR_ABORTED and err:
             raise err[0]
         _check(rc, dp.ctx, "gdwd_solve")
+        t_solved = time.perf_counter()
         st = dp.state()
         hist = dp.history(out.iterations)
     solve_time = time.perf_counter() - t_start
     resid = KKTResiduals(*[float(out.resid[i]) for i in range(11)])
     sigma_last = float(hist[-1, 11]) if len(hist) else float(out.sigma)
     state = SolverState(st["r"], st["xi"], st["alpha"], st["w"], st["u"], st["rho"], st["beta"], sigma_last,
-                        int(out.iterations), eps_c)
+                        int(out.iterations), float(out.eps_c))
     scores = st["beta"] + data.y * st["ztw"]
     train_err = 100.0 * float(np.mean(data.y * np.sign(scores) <= 0.0))
     if meta is None:
@@ -470,7 +476,10 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
                        double_count=int(out.double_count), solve_time=solve_time, read_time=0.0,
                        final_residuals=resid, final_state=state, train_error_pct=train_err, backend_used=kind,
                        C_used=data.C, converged=converged, history=hist, setup_ms=float(out.setup_ms),
-                       loop_ms=float(out.loop_ms))
+                       loop_ms=float(out.loop_ms),
+                       timings={"upload_s": t_up - t_start, "solve_call_s": t_solved - t_up,
+                                "download_s": solve_time - (t_solved - t_start), "setup_ms": float(out.setup_ms),
+                                "loop_ms": float(out.loop_ms)})
 
 
 # ---------------------------------------------------------------------------
