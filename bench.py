@@ -184,7 +184,7 @@ def run_b200(args, dist: Dist):
     # ---- device-resident timing ----------------------------------------------
     dp = G.device_problem(prob, device)
     ccfg = _lib.GdwdConfig(max_iter=conf.max_iter, backend=0, use_sgs=1, psqmr_switch_steps=50, ell=10, seed=0,
-                           use_graph=1, poll_every=16, smw_gram_space=int(not args.x_space), steplength=conf.steplength, tol_feas=conf.tol_feas,
+                           use_graph=1, poll_every=16, smw_gram_space=int(not args.x_space), persistent=int(not args.no_persistent), steplength=conf.steplength, tol_feas=conf.tol_feas,
                            tol_cgap=conf.tol_cgap, tol_cap=conf.tol_cap, sigma0=float("nan"),
                            epsilon_c=_eps_c(prob, conf), mu=conf.mu)
     _check(lib.gdwd_solve_begin(dp.ctx, C.byref(ccfg), None, 0), dp.ctx, "begin")
@@ -321,6 +321,7 @@ def main():
     ap.add_argument("--kkt-iters", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--x-space", action="store_true", help="SMW2 iterations as passes over X (no Gram-space)")
+    ap.add_argument("--no-persistent", action="store_true", help="Gram-space SMW2 as a CUDA graph of kernels")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     dist = Dist()

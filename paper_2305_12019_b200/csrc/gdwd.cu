@@ -26,6 +26,7 @@
 #include "gram.cuh"
 #include "solver_ops.cuh"
 #include "spops.cuh"
+#include "persist.cuh"
 #include "zops.cuh"
 
 using namespace gdwd;
@@ -143,7 +144,8 @@ struct gdwd_ctx {
   // solve session (gdwd_solve_begin / _iterate / _end)
   bool in_solve = false;
   int kind = 0, poll = 16, max_iter = 0, max_steps = 50, k_host = 0, psqmr_total = 0;
-  bool use_sgs = true, stopped = false, gram = false;
+  bool use_sgs = true, stopped = false, gram = false, persistent = false;
+  DevBuf pk_part;
   cudaGraphExec_t gexec = nullptr;
   int64_t body_nodes = 0;
   cudaEvent_t ev_begin = nullptr, ev_loop = nullptr, ev_end = nullptr;
@@ -473,7 +475,7 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   if (ctx->Zs) cudaFree(ctx->Zs);
   free_sparse(ctx);
   for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part})
     b->release();
   end_session(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1001,6 +1003,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   ctx->ps_per_iter.assign(max_iter + 1, 0.0);
   ctx->kind = kind;
   ctx->gram = gram;
+  ctx->persistent = gram && cfg->persistent && !ctx->prof;
   ctx->use_sgs = cfg->use_sgs != 0;
   ctx->poll = std::max(1, cfg->poll_every);
   ctx->max_iter = max_iter;
@@ -1011,7 +1014,15 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   ctx->eps_c = eps_c;
   ctx->setup_ms = setup;
   ctx->poll_pending = 0;
-  if (kind != GDWD_BACKEND_ITERATIVE && cfg->use_graph && !ctx->prof) {
+  if (ctx->persistent) {
+    int nb = 0;
+    const size_t sm = (size_t)(2 * n + 4) * sizeof(double);
+    CK(cudaFuncSetAttribute(gram_smw_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gram_smw_persistent, PK_THREADS, sm));
+    if (nb < 1) ctx->persistent = false;
+    else CK(ctx->pk_part.ensure((size_t)2 * NUM_SMS * PK_NPART));
+  }
+  if (kind != GDWD_BACKEND_ITERATIVE && cfg->use_graph && !ctx->prof && !ctx->persistent) {
     cudaGraph_t graph;
     const int64_t before = ctx->launches;
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
@@ -1036,6 +1047,20 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
   MatView Z = zview(ctx);
   int status = GDWD_OK;
   const int kend = std::min(ctx->max_iter, ctx->k_host + std::max(0, count));
+  if (ctx->persistent && !cb && ctx->k_host < kend && !ctx->stopped) {
+    // one cooperative launch runs all requested iterations (persist.cuh)
+    PKArgs pa{D, ctx->kmat.p, ctx->fac.p, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host, 0, ctx->use_sgs ? 1 : 0};
+    void* args[] = {&pa};
+    const size_t sm = (size_t)(2 * ctx->n + 4) * sizeof(double);
+    {
+      Launch L(ctx, "persistent_gram_smw2");
+      CK(cudaLaunchCooperativeKernel((void*)gram_smw_persistent, dim3(NUM_SMS), dim3(PK_THREADS), args, sm, ctx->st));
+    }
+    CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->k_host = ctx->Sh->stopped ? ctx->Sh->iters_done : kend;
+    ctx->stopped = ctx->Sh->stopped != 0;
+  }
   while (ctx->k_host < kend && !ctx->stopped) {
     const int k = ctx->k_host;
     if (ctx->kind == GDWD_BACKEND_ITERATIVE) {

@@ -1,0 +1,552 @@
+// Persistent cooperative kernel for the Gram-space SMW2 iteration.
+//
+// The SMW2 regime (reference subsolvers.py:94-151, chosen when d > 5000,
+// 5n < d, n <= 2500) has an n x n working set -- the Gram K = Z~^T Z~ and
+// G^{-1} (2 x 32 MB at n = 2000) stay in the 126 MB L2 -- so after the
+// one-time DMMA Gram the iteration is latency-bound, not bandwidth-bound.
+// One cooperative launch runs many iterations: each iteration is a fixed
+// sequence of phases separated by grid barriers; in every phase each CTA
+//   * stages the phase's input n-vector in shared memory, computing it
+//     elementwise from the previous phase's results (every CTA computes the
+//     whole vector, so n-sums over it are available in every CTA without a
+//     cross-CTA reduction),
+//   * does the GEMV rows it owns (one warp per row) and their epilogue,
+//   * writes per-CTA partial sums, which after the barrier every CTA
+//     reduces in the same fixed order.
+// Scalars (sigma, reuse flag, beta, eps_k ...) are therefore replicated in
+// each CTA's shared memory and bit-identical across CTAs; CTA 0 mirrors them
+// to the global Scal record and writes the history rows.
+//
+// Phase map of iteration k (names from solver_ops.cuh / solver.py lines):
+//   A  [K alpha_{k-1} ; K t1]         finish k-1 (obj_d, gap, stop), c_h, s1   :496-499
+//   B  G^{-1} s1                      g, ybar.J^{-1}s                          subsolvers :143-145
+//   C  K c_xb                         x_bar, ztw_bar, Newton r+, dr           :501-504
+//   D  K c_res                        reuse test                               :506-524
+//   E,F,G (re-solve when not reused)  s1', g', K c_x -> ztw                    :524-530
+//   H  K c_g                          ||g||                                    :535-536
+//   I  K (c_w - c_u)                  ||w - u||                                :537,328
+//   J  (elementwise)                  u, rho, r, xi, alpha updates, KKT sums   :533-545
+#pragma once
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "solver_ops.cuh"
+
+namespace gdwd {
+
+namespace cg = cooperative_groups;
+
+constexpr int PK_THREADS = 512;
+constexpr int PK_WARPS = PK_THREADS / 32;
+constexpr int PK_NPART = 10;  // widest cross-CTA sum (KKT terms)
+
+struct PKArgs {
+  Dev D;
+  const double* K;     // n x ld
+  const double* Ginv;  // n x ld
+  int64_t ld;
+  double* part;        // [2][gridDim][PK_NPART]
+  int count;           // iterations to run in this launch
+  int final_pass;      // after the last iteration, run the stop test of the final one
+  int use_sgs;
+};
+
+// replicated scalar state (shared memory)
+struct PKS {
+  int k, stopped, converged, reuse, double_count, iters_done, error;
+  double sigma, sigma_next, hbot, h2bot, beta_b, beta, coef, s2, gnorm, w2, wu2, ytzw, sdual;
+  double eta[11];
+};
+
+// Cross-CTA reduction of per-CTA partials (slot alternates by phase).
+template <int K>
+GDWD_DEV void pk_cross_sum(const double* part, int slot, double (&out)[K], double* red) {
+  const double* p = part + (size_t)slot * gridDim.x * PK_NPART;
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] += ld_cg(p + (size_t)b * PK_NPART + k);
+  }
+  block_sum<K>(out, red);
+}
+
+template <int K>
+GDWD_DEV void pk_write_part(double* part, int slot, const double (&v)[K], double* red) {
+  double t[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) t[k] = v[k];
+  block_sum<K>(t, red);
+  if (threadIdx.x == 0) {
+    double* p = part + ((size_t)slot * gridDim.x + blockIdx.x) * PK_NPART;
+#pragma unroll
+    for (int k = 0; k < K; ++k) p[k] = t[k];
+  }
+}
+
+// dot of K-row i (length n, stride ld) with the staged vector(s); one warp.
+template <int NV>
+GDWD_DEV void pk_row_dot(const double* row, int64_t n, const double* const (&xs)[NV], double (&out)[NV]) {
+  const int lane = threadIdx.x & 31;
+  double acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  int64_t j = 2 * lane;
+  for (; j + 15 * 64 < n; j += 16 * 64) {
+    double2 z[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) z[u] = __ldcg(reinterpret_cast<const double2*>(row + j + u * 64));
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        acc[v] += z[u].x * xs[v][j + u * 64];
+        acc[v] += z[u].y * xs[v][j + u * 64 + 1];
+      }
+    }
+  }
+  for (; j < n; j += 64) {
+    const double2 z = __ldcg(reinterpret_cast<const double2*>(row + j));
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      acc[v] += z.x * xs[v][j];
+      if (j + 1 < n) acc[v] += z.y * xs[v][j + 1];
+    }
+  }
+  warp_sum<NV>(acc);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) out[v] = acc[v];
+}
+
+__global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  const Dev& D = A.D;
+  const int64_t n = D.n;
+  extern __shared__ double pksm[];
+  double* xa = pksm;           // staged vector 1 (n, padded to even)
+  double* xb = pksm + n + 2;   // staged vector 2
+  __shared__ double red[PK_WARPS * PK_NPART];
+  __shared__ PKS S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i0 = n * blockIdx.x / gridDim.x, i1 = n * (blockIdx.x + 1) / gridDim.x;
+  const int nrows = (int)(i1 - i0);
+  const double mu = D.mu, mu2 = D.mu2, yty = D.yty;
+  int slot = 0;
+
+  if (threadIdx.x == 0) {
+    const Scal* G = D.S;
+    S.k = G->k; S.stopped = G->stopped; S.converged = G->converged; S.reuse = G->reuse;
+    S.double_count = G->double_count; S.iters_done = G->iters_done; S.error = G->error;
+    S.sigma = G->sigma; S.sigma_next = G->sigma_next; S.sdual = G->sdual;
+    for (int f = 0; f < 11; ++f) S.eta[f] = G->eta[f];
+  }
+  __syncthreads();
+  // pad the staging buffers' odd tail so paired loads read zeros
+  if (threadIdx.x == 0) {
+    xa[n] = 0.0;
+    xb[n] = 0.0;
+  }
+
+  const int k_end = S.k + A.count;
+  for (int pass = 0;; ++pass) {
+    if (S.stopped) break;
+    const bool last = S.k >= k_end;
+    if (last && !A.final_pass) break;
+    const int k = S.k;
+    // ---------------- phase A: K alpha (finish k-1) and K t1 ---------------
+    {
+      const double sig = S.sigma_next;
+      double yr = 0.0;
+      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+        const double rhs = (D.xi[j] - D.r[j]) - D.al[j] / sig;
+        const double chj = (-rhs + mu2 * D.u[j]) + (mu / sig) * D.rho[j];
+        xa[j] = D.al[j];
+        xb[j] = chj / mu2;
+        yr += D.y[j] * rhs;
+        if (j >= i0 && j < i1) D.h[j] = chj;
+      }
+      double v1[1] = {yr};
+      block_sum<1>(v1, red);
+      if (threadIdx.x == 0) S.hbot = -v1[0];
+      __syncthreads();
+      const double t2 = S.hbot / yty;
+      double qa = 0.0;
+      for (int r = warp; r < nrows; r += PK_WARPS) {
+        const int64_t i = i0 + r;
+        const double* xs[2] = {xa, xb};
+        double o[2];
+        pk_row_dot<2>(A.K + i * A.ld, n, xs, o);
+        if (lane == 0) {
+          qa += D.al[i] * o[0];
+          D.s1[i] = o[1] + D.y[i] * t2;
+        }
+      }
+      double pv[1] = {qa};
+      pk_write_part<1>(A.part, slot, pv, red);
+      grid.sync();
+      double zal2[1];
+      pk_cross_sum<1>(A.part, slot, zal2, red);
+      slot ^= 1;
+      if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) D.h[D.bot] = S.hbot;
+        // finish iteration k-1 (solver.py:293-304,334,548-555)
+        if (k > 0) {
+          const double od = D.kappa * S.sdual - D.zscale * sqrt(zal2[0]);
+          const double op = S.eta[9];
+          const double gap = fabs(op - od) / (1.0 + fabs(op) + fabs(od));
+          S.eta[10] = od;
+          S.eta[8] = gap;
+          if (blockIdx.x == 0) {
+            double* hr = D.hist + (int64_t)(k - 1) * HIST_W;
+            hr[H_OBJD] = od;
+            hr[H_GAP] = gap;
+          }
+          const double ep = fmax(fmax(S.eta[3], S.eta[4]), S.eta[5]);
+          const double ed = fmax(S.eta[6], S.eta[7]);
+          const double ec = fmax(fmax(S.eta[0], S.eta[1]), S.eta[2]);
+          if (fmax(ep, ed) < D.tol_feas && fmin(ec, gap) < D.tol_cgap && fmax(ec, gap) < D.tol_cap) {
+            S.stopped = 1;
+            S.converged = 1;
+          }
+        }
+        if (!S.stopped && k >= D.max_iter) S.stopped = 1;
+        if (!S.stopped && !last) {
+          S.sigma = S.sigma_next;
+          if (blockIdx.x == 0) {
+            double* hr = D.hist + (int64_t)k * HIST_W;
+            hr[H_SIGMA] = S.sigma;
+            hr[H_EPS] = D.eps_tab[k];
+            hr[H_REUSE] = 1.0;
+            hr[H_PSQMR] = 0.0;
+          }
+        }
+      }
+      __syncthreads();
+      if (S.stopped || last) break;
+    }
+    const double sig = S.sigma;
+    const double eps = D.eps_tab[k];
+    // Solve (subsolvers.py:127-151) in coefficients: phases B then C
+    // ---------------- phase B: g = G^{-1} s1 --------------------------------
+    auto phase_ginv = [&]() {
+      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) xa[j] = D.s1[j];
+      __syncthreads();
+      double sy = 0.0;
+      for (int r = warp; r < nrows; r += PK_WARPS) {
+        const int64_t i = i0 + r;
+        const double* xs[1] = {xa};
+        double o[1];
+        pk_row_dot<1>(A.Ginv + i * A.ld, n, xs, o);
+        if (lane == 0) {
+          D.g[i] = o[0];
+          sy += (D.y[i] / D.ynorm) * o[0];
+        }
+      }
+      double pv[1] = {sy};
+      pk_write_part<1>(A.part, slot, pv, red);
+      grid.sync();
+      double s[1];
+      pk_cross_sum<1>(A.part, slot, s, red);
+      slot ^= 1;
+      if (threadIdx.x == 0) {
+        // hv[bot] is h_bot (first solve) or h2_bot (re-solve), set by caller
+        S.coef = (s[0] + (-S.s2)) / D.S->ys;
+      }
+      __syncthreads();
+    };
+    if (threadIdx.x == 0) S.s2 = D.ynorm * (S.hbot / yty);
+    __syncthreads();
+    phase_ginv();
+    // ---------------- phase C: x_bar, K x_bar -> ztw_bar, Newton -------------
+    {
+      // c_xb[j] = h_j/mu^2 - v_j/mu^2, v = g - coef jy  (GsX) ; y.v
+      double yv = 0.0;
+      const double coef = S.coef;
+      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+        const double v = D.g[j] - coef * D.jy[j];
+        const double x = D.h[j] / mu2 - v / mu2;
+        xa[j] = x;
+        yv += D.y[j] * v;
+        if (j >= i0 && j < i1) D.xb[j] = x;
+      }
+      double v1[1] = {yv};
+      block_sum<1>(v1, red);
+      if (threadIdx.x == 0) {
+        const double vn = (-S.s2) - coef * (-1.0);
+        const double p2 = v1[0] + D.ynorm * vn;
+        S.beta_b = S.hbot / yty - p2 / yty;
+        if (blockIdx.x == 0) D.xb[D.bot] = S.beta_b;
+      }
+      __syncthreads();
+      const double bb = S.beta_b;
+      const double tol = D.tol_tab[k];
+      double ydr = 0.0;
+      for (int r = warp; r < nrows; r += PK_WARPS) {
+        const int64_t i = i0 + r;
+        const double* xs[1] = {xa};
+        double o[1];
+        pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
+        if (lane == 0) {
+          const double dot = o[0];
+          D.ztwb[i] = dot;
+          const double a = ((dot + D.y[i] * bb) + D.xi[i]) - D.al[i] / sig;
+          const double rn = newton_margin(a, sig, D.q, D.wl[i], D.r[i], tol);
+          D.rnew[i] = rn;
+          const double dri = rn - D.r[i];
+          D.dr[i] = dri;
+          ydr += D.y[i] * dri;
+        }
+      }
+      double pv[1] = {ydr};
+      pk_write_part<1>(A.part, slot, pv, red);
+      grid.sync();
+      double s[1];
+      pk_cross_sum<1>(A.part, slot, s, red);
+      slot ^= 1;
+      if (threadIdx.x == 0) S.h2bot = S.hbot + s[0];
+      __syncthreads();
+    }
+    // ---------------- phase D: reuse test -------------------------------------
+    if (A.use_sgs) {
+      const double bb = S.beta_b;
+      double ytz = 0.0;
+      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+        const double h2 = D.h[j] + D.dr[j];
+        const double ax = (D.ztwb[j] + mu2 * D.xb[j]) + D.y[j] * bb;
+        xa[j] = h2 - ax;
+        ytz += D.y[j] * D.ztwb[j];
+        if (j >= i0 && j < i1) D.h2[j] = h2;
+      }
+      double v1[1] = {ytz};
+      block_sum<1>(v1, red);
+      if (threadIdx.x == 0) S.ytzw = v1[0];
+      __syncthreads();
+      double q = 0.0;
+      for (int r = warp; r < nrows; r += PK_WARPS) {
+        const int64_t i = i0 + r;
+        const double* xs[1] = {xa};
+        double o[1];
+        pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
+        if (lane == 0) q += xa[i] * o[0];
+      }
+      double pv[1] = {q};
+      pk_write_part<1>(A.part, slot, pv, red);
+      grid.sync();
+      double s[1];
+      pk_cross_sum<1>(A.part, slot, s, red);
+      slot ^= 1;
+      if (threadIdx.x == 0) {
+        const double rb = S.h2bot - (S.ytzw + yty * bb);
+        const double rr = hypot(sqrt(s[0] > 0.0 ? s[0] : 0.0), rb);
+        S.reuse = rr <= 5.0 * eps;
+        if (!S.reuse) S.double_count += 1;
+        if (blockIdx.x == 0) D.hist[(int64_t)k * HIST_W + H_REUSE] = S.reuse ? 1.0 : 0.0;
+      }
+      __syncthreads();
+    } else {
+      if (threadIdx.x == 0) S.reuse = 1;
+      __syncthreads();
+    }
+    const bool reuse = S.reuse != 0;
+    // ---------------- phases E, F, G: re-solve with h2 -------------------------
+    if (!reuse) {
+      // E: s1' = K (h2/mu^2) + y t2'   (h2_j = h_j + dr_j)
+      {
+        const double t2 = S.h2bot / yty;
+        for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) xa[j] = (D.h[j] + D.dr[j]) / mu2;
+        __syncthreads();
+        for (int r = warp; r < nrows; r += PK_WARPS) {
+          const int64_t i = i0 + r;
+          const double* xs[1] = {xa};
+          double o[1];
+          pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
+          if (lane == 0) D.s1[i] = o[0] + D.y[i] * t2;
+        }
+        grid.sync();
+      }
+      if (threadIdx.x == 0) S.s2 = D.ynorm * (S.h2bot / yty);
+      __syncthreads();
+      phase_ginv();  // F
+      // G: x = h2/mu^2 - v/mu^2 ; ztw = K x
+      {
+        double yv = 0.0;
+        const double coef = S.coef;
+        for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+          const double v = D.g[j] - coef * D.jy[j];
+          const double x = (D.h[j] + D.dr[j]) / mu2 - v / mu2;
+          xa[j] = x;
+          yv += D.y[j] * v;
+          if (j >= i0 && j < i1) D.x[j] = x;
+        }
+        double v1[1] = {yv};
+        block_sum<1>(v1, red);
+        if (threadIdx.x == 0) {
+          const double vn = (-S.s2) - coef * (-1.0);
+          const double p2 = v1[0] + D.ynorm * vn;
+          S.beta = S.h2bot / yty - p2 / yty;
+        }
+        __syncthreads();
+        for (int r = warp; r < nrows; r += PK_WARPS) {
+          const int64_t i = i0 + r;
+          const double* xs[1] = {xa};
+          double o[1];
+          pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
+          if (lane == 0) D.ztw[i] = o[0];
+        }
+        grid.sync();
+      }
+    } else {
+      if (threadIdx.x == 0) S.beta = S.beta_b;
+      __syncthreads();
+    }
+    const double* xw = reuse ? D.xb : D.x;     // coefficients of w
+    const double* zw = reuse ? D.ztwb : D.ztw;  // Z^T w
+    // ---------------- phase H: ||g||, ||w||^2 -----------------------------------
+    {
+      double w2 = 0.0;
+      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+        xa[j] = xw[j] - D.rho[j] / (sig * mu);
+        w2 += xw[j] * zw[j];
+      }
+      double v1[1] = {w2};
+      block_sum<1>(v1, red);
+      if (threadIdx.x == 0) S.w2 = v1[0];
+      __syncthreads();
+      double q = 0.0;
+      for (int r = warp; r < nrows; r += PK_WARPS) {
+        const int64_t i = i0 + r;
+        const double* xs[1] = {xa};
+        double o[1];
+        pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
+        if (lane == 0) q += xa[i] * o[0];
+      }
+      double pv[1] = {q};
+      pk_write_part<1>(A.part, slot, pv, red);
+      grid.sync();
+      double s[1];
+      pk_cross_sum<1>(A.part, slot, s, red);
+      slot ^= 1;
+      if (threadIdx.x == 0) S.gnorm = sqrt(s[0] > 0.0 ? s[0] : 0.0);
+      __syncthreads();
+    }
+    // ---------------- phase I: ||w - u|| ----------------------------------------
+    {
+      const double gn = S.gnorm;
+      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+        const double gj = xw[j] - D.rho[j] / (sig * mu);
+        const double uj = (gn <= D.zscale) ? gj : (D.zscale / gn) * gj;
+        xa[j] = xw[j] - uj;
+      }
+      __syncthreads();
+      double q = 0.0;
+      for (int r = warp; r < nrows; r += PK_WARPS) {
+        const int64_t i = i0 + r;
+        const double* xs[1] = {xa};
+        double o[1];
+        pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
+        if (lane == 0) q += xa[i] * o[0];
+      }
+      double pv[1] = {q};
+      pk_write_part<1>(A.part, slot, pv, red);
+      grid.sync();
+      double s[1];
+      pk_cross_sum<1>(A.part, slot, s, red);
+      slot ^= 1;
+      if (threadIdx.x == 0) S.wu2 = s[0] > 0.0 ? s[0] : 0.0;
+      __syncthreads();
+    }
+    // ---------------- phase J: commit u, rho, w; Step 3; KKT terms -------------
+    {
+      const double gn = S.gnorm, bet = S.beta, C = D.C;
+      double acc[PK_NPART];
+#pragma unroll
+      for (int f = 0; f < PK_NPART; ++f) acc[f] = 0.0;
+      for (int64_t i = i0 + threadIdx.x; i < i1; i += PK_THREADS) {
+        // Step 2 commit (solver.py:535-542) in coefficients
+        const double wi = xw[i];
+        const double gi = wi - D.rho[i] / (sig * mu);
+        const double ui = (gn <= D.zscale) ? gi : (D.zscale / gn) * gi;
+        D.u[i] = ui;
+        D.rho[i] = D.rho[i] - ((D.tau * sig) * mu) * (wi - ui);
+        if (reuse) {
+          D.x[i] = wi;
+          D.ztw[i] = zw[i];
+        }
+        // Step 3 + KKT sample terms (OpStep3)
+        const double rr = D.rnew[i];
+        D.r[i] = rr;
+        const double yi = D.y[i], ei = D.e[i], zt = zw[i], ali = D.al[i];
+        const double xv = np_max0((((rr - zt) - yi * bet) + ali / sig) - (C / sig) * ei);
+        D.xi[i] = xv;
+        const double pg = ((zt + yi * bet) + xv) - rr;
+        const double an = ali - (D.tau * sig) * pg;
+        D.al[i] = an;
+        const double wl = D.wl[i];
+        const double s = (D.q * wl) / np_pow(rr, D.qp1);
+        const double d2 = an - s;
+        const double mn = np_min0(an);
+        const double mx = np_max0(an - C * ei);
+        acc[0] += yi * an;
+        acc[1] += xv * (C * ei - an);
+        acc[2] += d2 * d2;
+        acc[3] += pg * pg;
+        acc[4] += mn * mn;
+        acc[5] += mx * mx;
+        acc[6] += wl / np_pow(rr, D.q);
+        acc[7] += ei * xv;
+        acc[8] += np_pow(wl, D.e1) * np_pow(np_max0(an), D.e2);
+        acc[9] += (rr <= 0.0) ? 1.0 : 0.0;
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        D.x[D.bot] = bet;
+      }
+      pk_write_part<PK_NPART>(A.part, slot, acc, red);
+      grid.sync();
+      double s[PK_NPART];
+      pk_cross_sum<PK_NPART>(A.part, slot, s, red);
+      slot ^= 1;
+      if (threadIdx.x == 0) {
+        const double oc = D.one_c;
+        if (s[9] > 0.0) {
+          S.error = 6;
+          S.stopped = 1;
+        } else {
+          double* e = S.eta;
+          e[0] = fabs(s[0]) / oc;
+          e[1] = fabs(s[1]) / oc;
+          e[2] = s[2] / oc;
+          e[3] = sqrt(s[3]) / oc;
+          e[4] = (D.mu * sqrt(S.wu2)) / oc;
+          e[5] = fmax(sqrt(S.w2) - D.zscale, 0.0) / oc;
+          e[6] = sqrt(s[4]) / oc;
+          e[7] = sqrt(s[5]) / oc;
+          e[9] = s[6] + D.C * s[7];
+          S.sdual = s[8];
+          if (blockIdx.x == 0) {
+            double* hr = D.hist + (int64_t)k * HIST_W;
+            for (int f = 0; f < 8; ++f) hr[f] = e[f];
+            hr[H_OBJP] = e[9];
+            hr[H_BETA] = bet;
+          }
+          const double ep = fmax(fmax(e[3], e[4]), e[5]);
+          const double ed = fmax(e[6], e[7]);
+          if (D.sched && k + 1 < D.sched_len) S.sigma_next = D.sched[k + 1];
+          else S.sigma_next = sigma_rule(S.sigma, ep, ed);
+          S.iters_done = k + 1;
+          S.k = k + 1;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // mirror the replicated scalars to the global record
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    Scal* G = D.S;
+    G->k = S.k; G->stopped = S.stopped; G->converged = S.converged; G->reuse = S.reuse;
+    G->double_count = S.double_count; G->iters_done = S.iters_done; G->error = S.error;
+    G->sigma = S.sigma; G->sigma_next = S.sigma_next; G->sdual = S.sdual;
+    for (int f = 0; f < 11; ++f) G->eta[f] = S.eta[f];
+  }
+}
+
+}  // namespace gdwd

@@ -403,7 +403,8 @@ def _eps_c(data: ProblemData, config: SolverConfig) -> float:
 def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[FeatureMeta] = None,
                    callback: Optional[Callable[[SolverState, KKTResiduals], None]] = None, *,
                    sigma_schedule: Optional[np.ndarray] = None, device: Optional[int] = None,
-                   use_graph: bool = True, poll_every: int = 16, smw_gram_space: bool = True) -> SolveResult:
+                   use_graph: bool = True, poll_every: int = 16, smw_gram_space: bool = True,
+                   persistent: bool = True) -> SolveResult:
     """Run the solver to the KKT stopping rule or the iteration cap
     (solver.py:392-602).  ``callback(state, residuals)`` runs after every
     iteration (it forces a device sync and a copy of the iterates).
@@ -411,7 +412,8 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
     Keyword-only B200 extras: ``sigma_schedule`` (test hook: sigma of
     iteration k replaces update_sigma for 1 <= k < len), ``device``,
     ``use_graph``, ``poll_every``, ``smw_gram_space`` (SMW2 regime: iterate
-    in sample-coefficient space with the n x n Gram instead of passes over X)."""
+    in sample-coefficient space with the n x n Gram instead of passes over X),
+    ``persistent`` (Gram-space SMW2: all iterations in one cooperative kernel)."""
     t_start = time.perf_counter()
     dp = device_problem(data, device)
     t_up = time.perf_counter()
@@ -422,6 +424,7 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
         max_iter=int(config.max_iter), backend=_lib.BACKEND_CODE[kind.value], use_sgs=int(bool(config.use_sgs)),
         psqmr_switch_steps=int(config.psqmr_switch_steps), ell=int(config.ell), seed=int(config.seed),
         use_graph=int(bool(use_graph)), poll_every=int(poll_every), smw_gram_space=int(bool(smw_gram_space)),
+        persistent=int(bool(persistent)),
         steplength=float(config.steplength),
         tol_feas=float(config.tol_feas), tol_cgap=float(config.tol_cgap), tol_cap=float(config.tol_cap),
         sigma0=float("nan") if config.sigma0 is None else float(config.sigma0), epsilon_c=eps_c,

@@ -109,8 +109,8 @@ def _graph_vs_callback(case, be):
     tr = load_traj(case)
     prob = problem_for(tr)
     cfg = G.SolverConfig(q=prob.q, max_iter=60, backend=be)
-    a = G.sgs_admm_solve(prob, cfg, use_graph=True)
-    b = G.sgs_admm_solve(prob, cfg, use_graph=False)
+    a = G.sgs_admm_solve(prob, cfg, use_graph=True, persistent=False)
+    b = G.sgs_admm_solve(prob, cfg, use_graph=False, persistent=False)
     c, _, _ = run_traj(prob, cfg, True)
     for o in (b, c):
         assert np.array_equal(a.final_state.w, o.final_state.w)
@@ -147,3 +147,30 @@ def test_c1_first20_and_replayed_final():
     assert relerr(out.final_state.w, g["final_w"]) < 1e-6
     assert abs(out.final_state.beta - float(g["final_beta"])) < 1e-6 * max(1, abs(float(g["final_beta"])))
     assert abs(out.final_residuals.obj_primal - float(g["obj_primal"])) < 1e-6 * abs(float(g["obj_primal"]))
+
+
+@pytest.mark.parametrize("case", ["tiny_smw2", "smw2_natural"])
+def test_persistent_smw2_matches_reference(case):
+    """Gram-space SMW2 in one cooperative launch: iterate 20 against the
+    reference's iterate 20, and the whole short run against the
+    kernel-per-phase graph path."""
+    tr = load_traj(case)
+    prob = problem_for(tr)
+    full = bool(tr["full"])
+    cfg20 = G.SolverConfig(q=prob.q, max_iter=20, backend=G.Backend.SMW2)
+    out = G.sgs_admm_solve(prob, cfg20, persistent=True)
+    st = out.final_state
+    for key in ("w", "u", "rho", "r", "xi", "alpha"):
+        v = getattr(st, key)
+        if not full:
+            v = v[tr["idx_d"]] if key in ("w", "u", "rho") else v[tr["idx_n"]]
+        assert relerr(v, tr["it_" + key][19]) < TOL20, key
+    assert abs(st.beta - tr["hist"][19, 12]) <= 1e-9 * abs(tr["hist"][19, 12]) + 1e-12
+    cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]), backend=G.Backend.SMW2)
+    a = G.sgs_admm_solve(prob, cfg, persistent=True, sigma_schedule=tr["hist"][:, 11])
+    b = G.sgs_admm_solve(prob, cfg, persistent=False, sigma_schedule=tr["hist"][:, 11])
+    assert a.iterations == b.iterations and a.double_count == b.double_count
+    assert relerr(a.final_state.w, b.final_state.w) < 1e-9
+    assert np.array_equal(a.history[:, 11], b.history[:, 11])
+    for c in (2, 9):  # eta_c3, obj_primal (non-cancelling sums)
+        assert np.allclose(a.history[:, c], b.history[:, c], rtol=1e-7, atol=1e-12)

@@ -112,7 +112,7 @@ def test_library_loads_and_exports_every_symbol():
         assert hasattr(lib, s), s
     assert lib.gdwd_version() == 1
     # struct layouts agree with the header (sizes, no compute)
-    assert ctypes.sizeof(_lib.GdwdConfig) == 9 * 4 + 4 + 7 * 8
+    assert ctypes.sizeof(_lib.GdwdConfig) == 10 * 4 + 7 * 8
     assert ctypes.sizeof(_lib.GdwdResult) == 6 * 4 + 5 * 8 + 11 * 8
 
 
