@@ -145,7 +145,7 @@ struct gdwd_ctx {
   bool in_solve = false;
   int kind = 0, poll = 16, max_iter = 0, max_steps = 50, k_host = 0, psqmr_total = 0;
   bool use_sgs = true, stopped = false, gram = false, persistent = false;
-  DevBuf pk_part;
+  DevBuf pk_part, gkmat;
   cudaGraphExec_t gexec = nullptr;
   int64_t body_nodes = 0;
   cudaEvent_t ev_begin = nullptr, ev_loop = nullptr, ev_end = nullptr;
@@ -475,7 +475,7 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   if (ctx->Zs) cudaFree(ctx->Zs);
   free_sparse(ctx);
   for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat})
     b->release();
   end_session(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -705,6 +705,9 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
     ctx->ldm = ld;
     ctx->fac_rows = m;
     if (kind == GDWD_BACKEND_SMW2) {
+      // GK = G^{-1} K for the persistent Gram-space loop (K symmetric)
+      CK(ctx->gkmat.ensure((size_t)m * ld));
+      CK(gemm_f64(ctx->fac.p, ld, 1, ctx->kmat.p, ld, 1, m, m, m, 1.0, 0.0, ctx->gkmat.p, ld, ctx->st));
       OpJyG op{ctx->y.p, D.ynorm, const_cast<double*>(D.jy), ctx->S};
       RC(ensure_scratch(ctx, m, m));
       run_zt(ctx, op, MatView{ctx->fac.p, m, m, ld});
@@ -1049,7 +1052,8 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
   const int kend = std::min(ctx->max_iter, ctx->k_host + std::max(0, count));
   if (ctx->persistent && !cb && ctx->k_host < kend && !ctx->stopped) {
     // one cooperative launch runs all requested iterations (persist.cuh)
-    PKArgs pa{D, ctx->kmat.p, ctx->fac.p, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host, 0, ctx->use_sgs ? 1 : 0};
+    PKArgs pa{D, ctx->kmat.p, ctx->fac.p, ctx->gkmat.p, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host, getenv("GDWD_PK_DIAG") ? atoi(getenv("GDWD_PK_DIAG")) : 0,
+                ctx->use_sgs ? 1 : 0};
     void* args[] = {&pa};
     const size_t sm = (size_t)(2 * ctx->n + 4) * sizeof(double);
     {

@@ -18,14 +18,16 @@
 // to the global Scal record and writes the history rows.
 //
 // Phase map of iteration k (names from solver_ops.cuh / solver.py lines):
-//   A  [K alpha_{k-1} ; K t1]         finish k-1 (obj_d, gap, stop), c_h, s1   :496-499
-//   B  G^{-1} s1                      g, ybar.J^{-1}s                          subsolvers :143-145
+//   A  [K alpha_{k-1} ; GK t1]        finish k-1 (obj_d, gap, stop), c_h, g   :496-499
 //   C  K c_xb                         x_bar, ztw_bar, Newton r+, dr           :501-504
 //   D  K c_res                        reuse test                               :506-524
-//   E,F,G (re-solve when not reused)  s1', g', K c_x -> ztw                    :524-530
-//   H  K c_g                          ||g||                                    :535-536
-//   I  K (c_w - c_u)                  ||w - u||                                :537,328
+//   E,G (re-solve when not reused)    g' = GK t1', then K c_x -> ztw           :524-530
+//   H  K [c_g ; c_w - c_g]            ||g||, ||w - u||                         :535-537,328
 //   J  (elementwise)                  u, rho, r, xi, alpha updates, KKT sums   :533-545
+// with GK = G^{-1} K precomputed once (DMMA GEMM), so the SMW solve's
+// g = G^{-1}(K t1 + y t2) = GK t1 + t2 G^{-1} y needs no separate G^{-1}
+// phase (subsolvers.py:138-143, same math, different association).
+// 5 grid barriers per iteration (7 when Step 1c re-solves).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -44,10 +46,11 @@ struct PKArgs {
   Dev D;
   const double* K;     // n x ld
   const double* Ginv;  // n x ld
+  const double* GK;    // G^{-1} K, n x ld
   int64_t ld;
   double* part;        // [2][gridDim][PK_NPART]
   int count;           // iterations to run in this launch
-  int final_pass;      // after the last iteration, run the stop test of the final one
+  int diag;            // diagnostics: 1 = skip the GEMV rows (barrier/staging floor)
   int use_sgs;
 };
 
@@ -86,29 +89,33 @@ GDWD_DEV void pk_write_part(double* part, int slot, const double (&v)[K], double
 
 // dot of K-row i (length n, stride ld) with the staged vector(s); one warp.
 template <int NV>
-GDWD_DEV void pk_row_dot(const double* row, int64_t n, const double* const (&xs)[NV], double (&out)[NV]) {
+GDWD_DEV void pk_row_dot(const double* const (&rows)[NV], int64_t n, const double* const (&xs)[NV],
+                         double (&out)[NV]) {
   const int lane = threadIdx.x & 31;
   double acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = 0.0;
   int64_t j = 2 * lane;
-  for (; j + 15 * 64 < n; j += 16 * 64) {
-    double2 z[16];
+  constexpr int U = 16 / NV;
+  for (; j + (U - 1) * 64 < n; j += U * 64) {
+    double2 z[NV][U];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) z[u] = __ldcg(reinterpret_cast<const double2*>(row + j + u * 64));
+    for (int v = 0; v < NV; ++v)
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < U; ++u) z[v][u] = __ldcg(reinterpret_cast<const double2*>(rows[v] + j + u * 64));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        acc[v] += z[u].x * xs[v][j + u * 64];
-        acc[v] += z[u].y * xs[v][j + u * 64 + 1];
+        acc[v] += z[v][u].x * xs[v][j + u * 64];
+        acc[v] += z[v][u].y * xs[v][j + u * 64 + 1];
       }
     }
   }
   for (; j < n; j += 64) {
-    const double2 z = __ldcg(reinterpret_cast<const double2*>(row + j));
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
+      const double2 z = __ldcg(reinterpret_cast<const double2*>(rows[v] + j));
       acc[v] += z.x * xs[v][j];
       if (j + 1 < n) acc[v] += z.y * xs[v][j + 1];
     }
@@ -129,8 +136,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
   __shared__ PKS S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = n * blockIdx.x / gridDim.x, i1 = n * (blockIdx.x + 1) / gridDim.x;
-  const int nrows = (int)(i1 - i0);
-  const double mu = D.mu, mu2 = D.mu2, yty = D.yty;
+  const int nrows = A.diag == 1 ? 0 : (int)(i1 - i0);
+  const double mu = D.mu, mu2 = D.mu2, yty = D.yty, ynorm = D.ynorm;
   int slot = 0;
 
   if (threadIdx.x == 0) {
@@ -139,21 +146,35 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
     S.double_count = G->double_count; S.iters_done = G->iters_done; S.error = G->error;
     S.sigma = G->sigma; S.sigma_next = G->sigma_next; S.sdual = G->sdual;
     for (int f = 0; f < 11; ++f) S.eta[f] = G->eta[f];
-  }
-  __syncthreads();
-  // pad the staging buffers' odd tail so paired loads read zeros
-  if (threadIdx.x == 0) {
-    xa[n] = 0.0;
+    xa[n] = 0.0;  // pad the odd tail so paired loads read zeros
     xb[n] = 0.0;
   }
+  __syncthreads();
+
+  // g = GK t1 + t2 G^{-1} y for the staged t1 (xb), rows owned; returns the
+  // partial of ybar.g
+  auto gk_rows = [&](double t2) -> double {
+    double sy = 0.0;
+    for (int r = warp; r < nrows; r += PK_WARPS) {
+      const int64_t i = i0 + r;
+      const double* rows[1] = {A.GK + i * A.ld};
+      const double* xs[1] = {xb};
+      double o[1];
+      pk_row_dot<1>(rows, n, xs, o);
+      if (lane == 0) {
+        const double gi = o[0] + t2 * (ynorm * D.jy[i]);
+        D.g[i] = gi;
+        sy += (D.y[i] / ynorm) * gi;
+      }
+    }
+    return sy;
+  };
 
   const int k_end = S.k + A.count;
-  for (int pass = 0;; ++pass) {
-    if (S.stopped) break;
-    const bool last = S.k >= k_end;
-    if (last && !A.final_pass) break;
+  for (;;) {
+    if (S.stopped || S.k >= k_end) break;
     const int k = S.k;
-    // ---------------- phase A: K alpha (finish k-1) and K t1 ---------------
+    // ---------------- phase A: K alpha (finish k-1) and g = GK t1 ------------
     {
       const double sig = S.sigma_next;
       double yr = 0.0;
@@ -167,31 +188,38 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       }
       double v1[1] = {yr};
       block_sum<1>(v1, red);
-      if (threadIdx.x == 0) S.hbot = -v1[0];
+      if (threadIdx.x == 0) {
+        S.hbot = -v1[0];
+        S.s2 = ynorm * (S.hbot / yty);
+      }
       __syncthreads();
       const double t2 = S.hbot / yty;
-      double qa = 0.0;
+      double qa = 0.0, sy = 0.0;
       for (int r = warp; r < nrows; r += PK_WARPS) {
         const int64_t i = i0 + r;
+        const double* rows[2] = {A.K + i * A.ld, A.GK + i * A.ld};
         const double* xs[2] = {xa, xb};
         double o[2];
-        pk_row_dot<2>(A.K + i * A.ld, n, xs, o);
+        pk_row_dot<2>(rows, n, xs, o);
         if (lane == 0) {
           qa += D.al[i] * o[0];
-          D.s1[i] = o[1] + D.y[i] * t2;
+          const double gi = o[1] + t2 * (ynorm * D.jy[i]);
+          D.g[i] = gi;
+          sy += (D.y[i] / ynorm) * gi;
         }
       }
-      double pv[1] = {qa};
-      pk_write_part<1>(A.part, slot, pv, red);
+      double pv[2] = {qa, sy};
+      pk_write_part<2>(A.part, slot, pv, red);
       grid.sync();
-      double zal2[1];
-      pk_cross_sum<1>(A.part, slot, zal2, red);
+      double tot[2];
+      pk_cross_sum<2>(A.part, slot, tot, red);
       slot ^= 1;
       if (threadIdx.x == 0) {
+        S.coef = (tot[1] + (-S.s2)) / D.S->ys;
         if (blockIdx.x == 0) D.h[D.bot] = S.hbot;
         // finish iteration k-1 (solver.py:293-304,334,548-555)
         if (k > 0) {
-          const double od = D.kappa * S.sdual - D.zscale * sqrt(zal2[0]);
+          const double od = D.kappa * S.sdual - D.zscale * sqrt(tot[0]);
           const double op = S.eta[9];
           const double gap = fabs(op - od) / (1.0 + fabs(op) + fabs(od));
           S.eta[10] = od;
@@ -210,7 +238,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
           }
         }
         if (!S.stopped && k >= D.max_iter) S.stopped = 1;
-        if (!S.stopped && !last) {
+        if (!S.stopped) {
           S.sigma = S.sigma_next;
           if (blockIdx.x == 0) {
             double* hr = D.hist + (int64_t)k * HIST_W;
@@ -222,41 +250,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         }
       }
       __syncthreads();
-      if (S.stopped || last) break;
+      if (S.stopped) break;
     }
     const double sig = S.sigma;
     const double eps = D.eps_tab[k];
-    // Solve (subsolvers.py:127-151) in coefficients: phases B then C
-    // ---------------- phase B: g = G^{-1} s1 --------------------------------
-    auto phase_ginv = [&]() {
-      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) xa[j] = D.s1[j];
-      __syncthreads();
-      double sy = 0.0;
-      for (int r = warp; r < nrows; r += PK_WARPS) {
-        const int64_t i = i0 + r;
-        const double* xs[1] = {xa};
-        double o[1];
-        pk_row_dot<1>(A.Ginv + i * A.ld, n, xs, o);
-        if (lane == 0) {
-          D.g[i] = o[0];
-          sy += (D.y[i] / D.ynorm) * o[0];
-        }
-      }
-      double pv[1] = {sy};
-      pk_write_part<1>(A.part, slot, pv, red);
-      grid.sync();
-      double s[1];
-      pk_cross_sum<1>(A.part, slot, s, red);
-      slot ^= 1;
-      if (threadIdx.x == 0) {
-        // hv[bot] is h_bot (first solve) or h2_bot (re-solve), set by caller
-        S.coef = (s[0] + (-S.s2)) / D.S->ys;
-      }
-      __syncthreads();
-    };
-    if (threadIdx.x == 0) S.s2 = D.ynorm * (S.hbot / yty);
-    __syncthreads();
-    phase_ginv();
     // ---------------- phase C: x_bar, K x_bar -> ztw_bar, Newton -------------
     {
       // c_xb[j] = h_j/mu^2 - v_j/mu^2, v = g - coef jy  (GsX) ; y.v
@@ -273,7 +270,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       block_sum<1>(v1, red);
       if (threadIdx.x == 0) {
         const double vn = (-S.s2) - coef * (-1.0);
-        const double p2 = v1[0] + D.ynorm * vn;
+        const double p2 = v1[0] + ynorm * vn;
         S.beta_b = S.hbot / yty - p2 / yty;
         if (blockIdx.x == 0) D.xb[D.bot] = S.beta_b;
       }
@@ -283,9 +280,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       double ydr = 0.0;
       for (int r = warp; r < nrows; r += PK_WARPS) {
         const int64_t i = i0 + r;
+        const double* rows[1] = {A.K + i * A.ld};
         const double* xs[1] = {xa};
         double o[1];
-        pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
+        pk_row_dot<1>(rows, n, xs, o);
         if (lane == 0) {
           const double dot = o[0];
           D.ztwb[i] = dot;
@@ -300,10 +298,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       double pv[1] = {ydr};
       pk_write_part<1>(A.part, slot, pv, red);
       grid.sync();
-      double s[1];
-      pk_cross_sum<1>(A.part, slot, s, red);
+      double t[1];
+      pk_cross_sum<1>(A.part, slot, t, red);
       slot ^= 1;
-      if (threadIdx.x == 0) S.h2bot = S.hbot + s[0];
+      if (threadIdx.x == 0) S.h2bot = S.hbot + t[0];
       __syncthreads();
     }
     // ---------------- phase D: reuse test -------------------------------------
@@ -324,20 +322,21 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       double q = 0.0;
       for (int r = warp; r < nrows; r += PK_WARPS) {
         const int64_t i = i0 + r;
+        const double* rows[1] = {A.K + i * A.ld};
         const double* xs[1] = {xa};
         double o[1];
-        pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
+        pk_row_dot<1>(rows, n, xs, o);
         if (lane == 0) q += xa[i] * o[0];
       }
       double pv[1] = {q};
       pk_write_part<1>(A.part, slot, pv, red);
       grid.sync();
-      double s[1];
-      pk_cross_sum<1>(A.part, slot, s, red);
+      double t[1];
+      pk_cross_sum<1>(A.part, slot, t, red);
       slot ^= 1;
       if (threadIdx.x == 0) {
         const double rb = S.h2bot - (S.ytzw + yty * bb);
-        const double rr = hypot(sqrt(s[0] > 0.0 ? s[0] : 0.0), rb);
+        const double rr = hypot(sqrt(t[0] > 0.0 ? t[0] : 0.0), rb);
         S.reuse = rr <= 5.0 * eps;
         if (!S.reuse) S.double_count += 1;
         if (blockIdx.x == 0) D.hist[(int64_t)k * HIST_W + H_REUSE] = S.reuse ? 1.0 : 0.0;
@@ -348,27 +347,24 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       __syncthreads();
     }
     const bool reuse = S.reuse != 0;
-    // ---------------- phases E, F, G: re-solve with h2 -------------------------
+    // ---------------- phases E, G: re-solve with h2 ----------------------------
     if (!reuse) {
-      // E: s1' = K (h2/mu^2) + y t2'   (h2_j = h_j + dr_j)
-      {
+      {  // E: g' = GK (h2/mu^2) + t2' G^{-1} y   (h2_j = h_j + dr_j)
         const double t2 = S.h2bot / yty;
-        for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) xa[j] = (D.h[j] + D.dr[j]) / mu2;
+        for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) xb[j] = (D.h[j] + D.dr[j]) / mu2;
+        if (threadIdx.x == 0) S.s2 = ynorm * t2;
         __syncthreads();
-        for (int r = warp; r < nrows; r += PK_WARPS) {
-          const int64_t i = i0 + r;
-          const double* xs[1] = {xa};
-          double o[1];
-          pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
-          if (lane == 0) D.s1[i] = o[0] + D.y[i] * t2;
-        }
+        const double sy = gk_rows(t2);
+        double pv[1] = {sy};
+        pk_write_part<1>(A.part, slot, pv, red);
         grid.sync();
+        double t[1];
+        pk_cross_sum<1>(A.part, slot, t, red);
+        slot ^= 1;
+        if (threadIdx.x == 0) S.coef = (t[0] + (-S.s2)) / D.S->ys;
+        __syncthreads();
       }
-      if (threadIdx.x == 0) S.s2 = D.ynorm * (S.h2bot / yty);
-      __syncthreads();
-      phase_ginv();  // F
-      // G: x = h2/mu^2 - v/mu^2 ; ztw = K x
-      {
+      {  // G: x = h2/mu^2 - v/mu^2 ; ztw = K x
         double yv = 0.0;
         const double coef = S.coef;
         for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
@@ -382,15 +378,16 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         block_sum<1>(v1, red);
         if (threadIdx.x == 0) {
           const double vn = (-S.s2) - coef * (-1.0);
-          const double p2 = v1[0] + D.ynorm * vn;
+          const double p2 = v1[0] + ynorm * vn;
           S.beta = S.h2bot / yty - p2 / yty;
         }
         __syncthreads();
         for (int r = warp; r < nrows; r += PK_WARPS) {
           const int64_t i = i0 + r;
+          const double* rows[1] = {A.K + i * A.ld};
           const double* xs[1] = {xa};
           double o[1];
-          pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
+          pk_row_dot<1>(rows, n, xs, o);
           if (lane == 0) D.ztw[i] = o[0];
         }
         grid.sync();
@@ -401,58 +398,49 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
     }
     const double* xw = reuse ? D.xb : D.x;     // coefficients of w
     const double* zw = reuse ? D.ztwb : D.ztw;  // Z^T w
-    // ---------------- phase H: ||g||, ||w||^2 -----------------------------------
+    // ---------------- phase H: ||g||, ||w - u||, ||w|| ---------------------------
     {
       double w2 = 0.0;
       for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
-        xa[j] = xw[j] - D.rho[j] / (sig * mu);
+        const double gj = xw[j] - D.rho[j] / (sig * mu);
+        xa[j] = gj;
+        xb[j] = xw[j] - gj;  // w - u when u = g (no projection)
         w2 += xw[j] * zw[j];
       }
       double v1[1] = {w2};
       block_sum<1>(v1, red);
       if (threadIdx.x == 0) S.w2 = v1[0];
       __syncthreads();
-      double q = 0.0;
+      double q[3] = {0.0, 0.0, 0.0};
       for (int r = warp; r < nrows; r += PK_WARPS) {
         const int64_t i = i0 + r;
-        const double* xs[1] = {xa};
-        double o[1];
-        pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
-        if (lane == 0) q += xa[i] * o[0];
+        const double* rows[2] = {A.K + i * A.ld, A.K + i * A.ld};
+        const double* xs[2] = {xa, xb};
+        double o[2];
+        pk_row_dot<2>(rows, n, xs, o);
+        if (lane == 0) {
+          q[0] += xa[i] * o[0];  // g^T K g
+          q[1] += xb[i] * o[1];  // d^T K d
+          q[2] += xb[i] * o[0];  // d^T K g
+        }
       }
-      double pv[1] = {q};
-      pk_write_part<1>(A.part, slot, pv, red);
+      pk_write_part<3>(A.part, slot, q, red);
       grid.sync();
-      double s[1];
-      pk_cross_sum<1>(A.part, slot, s, red);
+      double t[3];
+      pk_cross_sum<3>(A.part, slot, t, red);
       slot ^= 1;
-      if (threadIdx.x == 0) S.gnorm = sqrt(s[0] > 0.0 ? s[0] : 0.0);
-      __syncthreads();
-    }
-    // ---------------- phase I: ||w - u|| ----------------------------------------
-    {
-      const double gn = S.gnorm;
-      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
-        const double gj = xw[j] - D.rho[j] / (sig * mu);
-        const double uj = (gn <= D.zscale) ? gj : (D.zscale / gn) * gj;
-        xa[j] = xw[j] - uj;
+      if (threadIdx.x == 0) {
+        const double gg = t[0] > 0.0 ? t[0] : 0.0;
+        S.gnorm = sqrt(gg);
+        if (S.gnorm <= D.zscale) {
+          S.wu2 = t[1] > 0.0 ? t[1] : 0.0;
+        } else {
+          // w - u = d + (1 - s) g with s = z_scale / ||g||
+          const double om = 1.0 - D.zscale / S.gnorm;
+          const double v = t[1] + 2.0 * om * t[2] + om * om * gg;
+          S.wu2 = v > 0.0 ? v : 0.0;
+        }
       }
-      __syncthreads();
-      double q = 0.0;
-      for (int r = warp; r < nrows; r += PK_WARPS) {
-        const int64_t i = i0 + r;
-        const double* xs[1] = {xa};
-        double o[1];
-        pk_row_dot<1>(A.K + i * A.ld, n, xs, o);
-        if (lane == 0) q += xa[i] * o[0];
-      }
-      double pv[1] = {q};
-      pk_write_part<1>(A.part, slot, pv, red);
-      grid.sync();
-      double s[1];
-      pk_cross_sum<1>(A.part, slot, s, red);
-      slot ^= 1;
-      if (threadIdx.x == 0) S.wu2 = s[0] > 0.0 ? s[0] : 0.0;
       __syncthreads();
     }
     // ---------------- phase J: commit u, rho, w; Step 3; KKT terms -------------
@@ -497,31 +485,29 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         acc[8] += np_pow(wl, D.e1) * np_pow(np_max0(an), D.e2);
         acc[9] += (rr <= 0.0) ? 1.0 : 0.0;
       }
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        D.x[D.bot] = bet;
-      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) D.x[D.bot] = bet;
       pk_write_part<PK_NPART>(A.part, slot, acc, red);
       grid.sync();
-      double s[PK_NPART];
-      pk_cross_sum<PK_NPART>(A.part, slot, s, red);
+      double t[PK_NPART];
+      pk_cross_sum<PK_NPART>(A.part, slot, t, red);
       slot ^= 1;
       if (threadIdx.x == 0) {
         const double oc = D.one_c;
-        if (s[9] > 0.0) {
+        if (t[9] > 0.0 && A.diag == 0) {
           S.error = 6;
           S.stopped = 1;
         } else {
           double* e = S.eta;
-          e[0] = fabs(s[0]) / oc;
-          e[1] = fabs(s[1]) / oc;
-          e[2] = s[2] / oc;
-          e[3] = sqrt(s[3]) / oc;
+          e[0] = fabs(t[0]) / oc;
+          e[1] = fabs(t[1]) / oc;
+          e[2] = t[2] / oc;
+          e[3] = sqrt(t[3]) / oc;
           e[4] = (D.mu * sqrt(S.wu2)) / oc;
           e[5] = fmax(sqrt(S.w2) - D.zscale, 0.0) / oc;
-          e[6] = sqrt(s[4]) / oc;
-          e[7] = sqrt(s[5]) / oc;
-          e[9] = s[6] + D.C * s[7];
-          S.sdual = s[8];
+          e[6] = sqrt(t[4]) / oc;
+          e[7] = sqrt(t[5]) / oc;
+          e[9] = t[6] + D.C * t[7];
+          S.sdual = t[8];
           if (blockIdx.x == 0) {
             double* hr = D.hist + (int64_t)k * HIST_W;
             for (int f = 0; f < 8; ++f) hr[f] = e[f];
