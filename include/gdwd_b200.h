@@ -85,6 +85,10 @@ typedef struct {
  * aborts the solve (GDWD_ERR_ABORTED). */
 typedef int (*gdwd_iter_cb)(void* user, int32_t iter, const double* resid11, double sigma, double beta);
 
+/* all-reduce (sum, in place, across the sample shards) of `count` host
+ * doubles; nonzero return aborts.  Used by gdwd_comm_init_host. */
+typedef int (*gdwd_allreduce_cb)(void* user, double* buf, int64_t count);
+
 /* context ------------------------------------------------------------------*/
 int gdwd_ctx_create(int32_t device, gdwd_ctx** out);
 void gdwd_ctx_destroy(gdwd_ctx* ctx);
@@ -103,6 +107,17 @@ int gdwd_frobenius_sq(gdwd_ctx* ctx, double* out);
 /* ProblemData vectors and scalars (solver.py:60-71); all length n. */
 int gdwd_set_problem(gdwd_ctx* ctx, const double* y, const double* e, const double* weights, double C,
                      double q, double z_scale);
+
+/* sample sharding -------------------------------------------
+ * Each rank uploads its contiguous block of samples (columns of Z~) and its
+ * y/e/weights, then joins a communicator; every later product with Z~
+ * all-reduces its d-partial and n-sums (one bundle per reduction point) and
+ * d-space work is replicated.  n_global is the total sample count.  SMW2 is
+ * not sharded (its n x n Gram couples all samples). */
+int gdwd_comm_unique_id(uint8_t* out128);  /* ncclGetUniqueId, on one rank */
+int gdwd_comm_init_nccl(gdwd_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t* id128, int64_t n_global);
+int gdwd_comm_init_host(gdwd_ctx* ctx, int32_t nranks, int32_t rank, gdwd_allreduce_cb cb, void* user,
+                        int64_t n_global);
 
 /* operator seams ------------------------------------------------------------
  * Z~ v  (scipy csc_matvec at solver.py:496,508,517,300; subsolvers.py:146) */

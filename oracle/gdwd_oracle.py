@@ -352,17 +352,18 @@ class ZOp:
 # --------------------------------------------------------------------------
 
 class DirectSys:
-    """subsolvers.py:63-86."""
+    """subsolvers.py:63-86 (``ar``: sum over sample shards)."""
 
-    def __init__(self, op: ZOp, y, mu_sq):
+    def __init__(self, op: ZOp, y, mu_sq, ar=None):
+        ar = ar or (lambda v: v)
         d = op.d
         a = np.empty((d + 1, d + 1))
-        a[:d, :d] = op.zzt()
+        a[:d, :d] = ar(op.zzt())
         a[:d, :d][np.diag_indices(d)] += mu_sq
-        zy = op.mv(y)
+        zy = ar(op.mv(y))
         a[:d, d] = zy
         a[d, :d] = zy
-        a[d, d] = float(y @ y)
+        a[d, d] = float(ar(np.array([float(y @ y)]))[0])
         self.A = a
         self.R = chol_upper(a)
 
@@ -449,30 +450,38 @@ KKT_FIELDS = ("eta_c1", "eta_c2", "eta_c3", "eta_p1", "eta_p2", "eta_p3",
               "eta_d1", "eta_d2", "eta_gap", "obj_primal", "obj_dual")
 
 
-def kkt(op: ZOp, prob, st, mu):
-    """solver.py:311-340; returns a dict with the 11 KKT fields."""
+def kkt(op: ZOp, prob, st, mu, ar=None):
+    """solver.py:311-340; returns a dict with the 11 KKT fields.  ``ar``:
+    sum-all-reduce over sample shards (None: unsharded)."""
+    ar = ar or (lambda v: v)
+
+    def nsum(x):  # a sum over samples
+        return float(ar(np.array([x]))[0])
+
     q, C = prob.q, prob.C
     y, e, wl = prob.y, prob.e, prob.weights
     one_c = 1.0 + C
-    if np.any(st["r"] <= 0.0):
+    if nsum(float(np.any(st["r"] <= 0.0))) > 0:
         raise AssertionError("margin iterate left the positive orthant")
     r, xi, al, w, u, beta = st["r"], st["xi"], st["alpha"], st["w"], st["u"], st["beta"]
     ztw = op.rmv(w)
     s = q * wl / r ** (q + 1.0)
+    pg = ztw + beta * y + xi - r
     out = dict(
-        eta_c1=abs(float(y @ al)) / one_c,
-        eta_c2=abs(float(xi @ (C * e - al))) / one_c,
-        eta_c3=float(np.sum((al - s) ** 2)) / one_c,
-        eta_p1=float(np.linalg.norm(ztw + beta * y + xi - r)) / one_c,
+        eta_c1=abs(nsum(float(y @ al))) / one_c,
+        eta_c2=abs(nsum(float(xi @ (C * e - al)))) / one_c,
+        eta_c3=nsum(float(np.sum((al - s) ** 2))) / one_c,
+        eta_p1=float(np.sqrt(nsum(pg.dot(pg)))) / one_c,
         eta_p2=mu * float(np.linalg.norm(w - u)) / one_c,
         eta_p3=max(float(np.linalg.norm(w)) - prob.z_scale, 0.0) / one_c,
-        eta_d1=float(np.linalg.norm(np.minimum(al, 0.0))) / one_c,
-        eta_d2=float(np.linalg.norm(np.maximum(al - C * e, 0.0))) / one_c,
+        eta_d1=float(np.sqrt(nsum(np.minimum(al, 0.0).dot(np.minimum(al, 0.0))))) / one_c,
+        eta_d2=float(np.sqrt(nsum(np.maximum(al - C * e, 0.0).dot(np.maximum(al - C * e, 0.0))))) / one_c,
     )
-    op_ = float(np.sum(wl / r ** q) + C * (e @ xi))
+    op_ = nsum(float(np.sum(wl / r ** q))) + C * nsum(float(e @ xi))
     kap = (q + 1.0) / q * q ** (1.0 / (q + 1.0))
-    od = float(kap * np.sum(wl ** (1.0 / (q + 1.0)) * np.maximum(al, 0.0) ** (q / (q + 1.0)))
-               - prob.z_scale * np.linalg.norm(op.mv(al)))
+    za = ar(op.mv(al))
+    od = float(kap * nsum(float(np.sum(wl ** (1.0 / (q + 1.0)) * np.maximum(al, 0.0) ** (q / (q + 1.0)))))
+               - prob.z_scale * np.linalg.norm(za))
     out["obj_primal"] = op_
     out["obj_dual"] = od
     out["eta_gap"] = abs(op_ - od) / (1.0 + abs(op_) + abs(od))
@@ -533,40 +542,61 @@ class OracleResult:
 def solve(prob, cfg: OracleConfig, operator: str = "csc",
           callback: Optional[Callable[[dict, dict], None]] = None,
           sigma_schedule: Optional[np.ndarray] = None, record: bool = True, gram: str = "same",
-          time_after: Optional[int] = None) -> OracleResult:
+          time_after: Optional[int] = None, allreduce=None, n_global: Optional[int] = None) -> OracleResult:
     """solver.py:392-602.  ``sigma_schedule[k]`` (test hook)
-    replaces update_sigma's output as the sigma of iteration k (k >= 1)."""
+    replaces update_sigma's output as the sigma of iteration k (k >= 1).
+
+    ``allreduce`` (sum over sample shards) + ``n_global`` restate the sharded
+    decomposition the device path uses (paper_2305_12019_b200/parallel.py):
+    ``prob`` is then this rank's block of samples, every sum over samples is
+    all-reduced and feature-space work is replicated."""
     import time
 
     t0 = time.perf_counter()
     op = ZOp(prob.z_tilde, operator, gram)
     n, d = op.n, op.d
+    ar = allreduce or (lambda v: v)
+    sharded = allreduce is not None
+    ng = n if n_global is None else int(n_global)
+
+    def nsum(x):  # a scalar summed over samples
+        return float(ar(np.array([x]))[0])
+
+    def zmv(t):  # Z~ t summed over the shards
+        return ar(op.mv(t))
     q, C, mu = prob.q, prob.C, cfg.mu
     mu2 = mu * mu
     y, e, wl = prob.y, prob.e, prob.weights
     zs = prob.z_scale
     tau = cfg.steplength
-    rn = math.sqrt(n)
-    kind = select_backend(n, d) if cfg.backend == "auto" else cfg.backend
-    zy = op.mv(y)
-    yty = float(y @ y)
+    rn = math.sqrt(ng)
+    kind = select_backend(ng, d) if cfg.backend == "auto" else cfg.backend
+    zy = zmv(y)
+    yty = nsum(float(y @ y))
     sysm = None
     jac = None
     if kind == "direct":
-        sysm = DirectSys(op, y, mu2)
+        sysm = DirectSys(op, y, mu2, ar=allreduce)
     elif kind == "smw2":
+        if sharded:
+            raise ValueError("SMW2 couples all samples: not sharded")
         sysm = SmwSys(op, y, mu2)
     else:
-        jac = np.concatenate([prob.z_tilde.row_sq_sums() + mu2, [max(yty, mu2)]])
+        jac = np.concatenate([ar(prob.z_tilde.row_sq_sums()) + mu2, [max(yty, mu2)]])
         jac = np.maximum(jac, 1e-12)
 
     def a_apply(v):
         hd, tl = v[:d], v[d]
-        top = op.mv(op.rmv(hd)) + mu2 * hd + zy * tl
+        top = zmv(op.rmv(hd)) + mu2 * hd + zy * tl
         return np.concatenate([top, [float(zy @ hd) + yty * tl]])
 
-    sigma = cfg.sigma0 if cfg.sigma0 is not None else min(10.0 * C, float(n)) ** q
-    epsc = cfg.epsilon_c if cfg.epsilon_c is not None else 1.0 / max(1.0, prob.z_tilde.frobenius_norm())
+    sigma = cfg.sigma0 if cfg.sigma0 is not None else min(10.0 * C, float(ng)) ** q
+    if cfg.epsilon_c is not None:
+        epsc = cfg.epsilon_c
+    elif sharded:
+        epsc = 1.0 / max(1.0, math.sqrt(nsum(float(np.sum(prob.z_tilde.values * prob.z_tilde.values)))))
+    else:
+        epsc = 1.0 / max(1.0, prob.z_tilde.frobenius_norm())
     r = np.ones(n); xi = np.ones(n); al = np.zeros(n)
     w = np.zeros(d); u = np.zeros(d); rho = np.zeros(d)
     beta = 0.0
@@ -589,7 +619,7 @@ def solve(prob, cfg: OracleConfig, operator: str = "csc",
             if o.converged:
                 return o.x
             prox = ProxSys(op, y, mu2, cfg.ell, seed=cfg.seed)
-        shift = prox.fwd(aw) - mu2 * aw - op.mv(aztw)
+        shift = prox.fwd(aw) - mu2 * aw - zmv(aztw)
         return prox.solve(np.concatenate([ht + shift, [hb]]))
 
     hist = []
@@ -603,8 +633,8 @@ def solve(prob, cfg: OracleConfig, operator: str = "csc",
         last_steps[0] = 0
         eps = epsc / (k + 1.0) ** 1.5
         rhs = xi - r - al / sigma
-        ht = -op.mv(rhs) + mu2 * u + (mu / sigma) * rho
-        hb = -float(y @ rhs)
+        ht = -zmv(rhs) + mu2 * u + (mu / sigma) * rho
+        hb = -nsum(float(y @ rhs))
         x = sys_solve(ht, hb, eps, np.concatenate([w, [beta]]), w, ztw)
         wb, bb = x[:d], float(x[d])
         ztwb = op.rmv(wb)
@@ -613,14 +643,14 @@ def solve(prob, cfg: OracleConfig, operator: str = "csc",
         reused = True
         if cfg.use_sgs:
             dr = rnew - r
-            h2t = ht + op.mv(dr)
-            h2b = hb + float(y @ dr)
+            h2t = ht + zmv(dr)
+            h2b = hb + nsum(float(y @ dr))
             if prox is not None:
-                shift = prox.fwd(w) - mu2 * w - op.mv(ztw)
+                shift = prox.fwd(w) - mu2 * w - zmv(ztw)
                 axt = prox.fwd(wb) + zy * bb
                 rt = h2t + shift - axt
             else:
-                axt = op.mv(ztwb) + mu2 * wb + zy * bb
+                axt = zmv(ztwb) + mu2 * wb + zy * bb
                 rt = h2t - axt
             rb = h2b - (float(zy @ wb) + yty * bb)
             if math.hypot(float(np.linalg.norm(rt)), rb) <= 5.0 * eps:
@@ -642,7 +672,7 @@ def solve(prob, cfg: OracleConfig, operator: str = "csc",
         al = al - (tau * sigma) * pg
         rho = rho - (tau * sigma * mu) * (w - u)
         st = dict(r=r, xi=xi, alpha=al, w=w, u=u, rho=rho, beta=beta, sigma=sigma, iter=k + 1, eps_c=epsc)
-        res = kkt(op, prob, st, mu)
+        res = kkt(op, prob, st, mu, ar=allreduce)
         if record:
             hist.append(dict(res, sigma=sigma, beta=beta, reused=reused, psqmr_steps=last_steps[0], eps=eps))
         if callback is not None:
@@ -658,7 +688,7 @@ def solve(prob, cfg: OracleConfig, operator: str = "csc",
     t_end = time.perf_counter()
     loop_s = t_end - t1
     scores = beta + y * ztw
-    terr = 100.0 * float(np.mean(y * np.sign(scores) <= 0.0))
+    terr = 100.0 * nsum(float(np.sum(y * np.sign(scores) <= 0.0))) / ng
     return OracleResult(state=st, residuals=res, iterations=st["iter"], converged=conv, backend=kind,
                         psqmr_total=ptot, double_count=dcount, history=hist, train_error_pct=terr,
                         setup_s=setup_s, loop_s=loop_s,

@@ -26,7 +26,8 @@ SYMBOLS = [
     "gdwd_upload_csc", "gdwd_set_problem", "gdwd_matvec", "gdwd_matvec_t", "gdwd_solve", "gdwd_get_state",
     "gdwd_get_history", "gdwd_newton_sweep", "gdwd_chol_inverse", "gdwd_gram", "gdwd_psqmr_dense",
     "gdwd_solve_begin", "gdwd_solve_iterate", "gdwd_solve_end", "gdwd_time_iterations", "gdwd_set_profile",
-    "gdwd_get_profile", "gdwd_reset_counters", "gdwd_frobenius_sq",
+    "gdwd_get_profile", "gdwd_reset_counters", "gdwd_frobenius_sq", "gdwd_comm_unique_id",
+    "gdwd_comm_init_nccl", "gdwd_comm_init_host",
 ]
 
 
@@ -55,6 +56,7 @@ class GdwdResult(C.Structure):
 
 
 ITER_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.c_double, C.c_double)
+ALLREDUCE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
 
 _lib = None
 _lock = threading.Lock()
@@ -84,6 +86,9 @@ def _declare(lib):
         "gdwd_get_profile": (C.c_int, [vp, C.c_char_p, _I64, C.POINTER(C.c_int64)]),
         "gdwd_reset_counters": (C.c_int, [vp]),
         "gdwd_frobenius_sq": (C.c_int, [vp, _P]),
+        "gdwd_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+        "gdwd_comm_init_nccl": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int64]),
+        "gdwd_comm_init_host": (C.c_int, [vp, C.c_int32, C.c_int32, ALLREDUCE_CB, vp, C.c_int64]),
         "gdwd_get_state": (C.c_int, [vp, _P, _P, _P, _P, _P, _P, _P, _P]),
         "gdwd_get_history": (C.c_int, [vp, _P, _I64, C.POINTER(C.c_int64)]),
         "gdwd_newton_sweep": (C.c_int, [C.c_int32, _I64, _P, C.c_double, C.c_double, _P, _P, C.c_double, C.c_int32,
@@ -130,5 +135,5 @@ def f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
-__all__ = ["BACKEND_CODE", "BACKEND_NAME", "GdwdConfig", "GdwdLibraryError", "GdwdResult", "ITER_CB",
+__all__ = ["ALLREDUCE_CB", "BACKEND_CODE", "BACKEND_NAME", "GdwdConfig", "GdwdLibraryError", "GdwdResult", "ITER_CB",
            "LIB_PATH", "SYMBOLS", "f64", "load", "ptr"]

@@ -8,6 +8,7 @@
 // ITERATIVE body is host-driven because PSQMR's step count is data
 // dependent (one 4-byte flag read per PSQMR step).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -17,6 +18,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <thread>
 #include <string>
 #include <vector>
@@ -30,6 +32,44 @@
 #include "zops.cuh"
 
 using namespace gdwd;
+
+// ---------------------------------------------------------------------------
+// NCCL, bound at run time (dlopen) so the library has no link-time NCCL
+// dependency; the same libnccl.so.2 torch.distributed loads.
+// ---------------------------------------------------------------------------
+namespace nccl {
+typedef struct { char internal[128]; } UniqueId;
+typedef void* Comm;
+typedef int Result;
+enum { Float64 = 8, Sum = 0 };
+struct Api {
+  bool ok = false;
+  Result (*GetUniqueId)(UniqueId*) = nullptr;
+  Result (*CommInitRank)(Comm*, int, UniqueId, int) = nullptr;
+  Result (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  Result (*CommDestroy)(Comm) = nullptr;
+  const char* (*GetErrorString)(Result) = nullptr;
+};
+static Api& api() {
+  static Api a;
+  static bool tried = false;
+  if (tried) return a;
+  tried = true;
+  const char* env = getenv("GDWD_NCCL_LIB");
+  const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+  void* h = nullptr;
+  for (const char* nm : names)
+    if (nm && (h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!h) return a;
+  a.GetUniqueId = (Result(*)(UniqueId*))dlsym(h, "ncclGetUniqueId");
+  a.CommInitRank = (Result(*)(Comm*, int, UniqueId, int))dlsym(h, "ncclCommInitRank");
+  a.AllReduce = (Result(*)(const void*, void*, size_t, int, int, Comm, cudaStream_t))dlsym(h, "ncclAllReduce");
+  a.CommDestroy = (Result(*)(Comm))dlsym(h, "ncclCommDestroy");
+  a.GetErrorString = (const char* (*)(Result))dlsym(h, "ncclGetErrorString");
+  a.ok = a.GetUniqueId && a.CommInitRank && a.AllReduce && a.CommDestroy;
+  return a;
+}
+}  // namespace nccl
 
 namespace {
 
@@ -84,6 +124,8 @@ ZtGeom zt_geom(int64_t rows, int64_t ld, int slots) {
 template <class K>
 int slots_for(K kernel, int threads, size_t smem) {
   static std::map<std::pair<const void*, size_t>, int> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   auto key = std::make_pair((const void*)kernel, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
@@ -146,6 +188,16 @@ struct gdwd_ctx {
   int kind = 0, poll = 16, max_iter = 0, max_steps = 50, k_host = 0, psqmr_total = 0;
   bool use_sgs = true, stopped = false, gram = false, persistent = false;
   DevBuf pk_part, gkmat;
+  // sample sharding: 0 none, 1 NCCL, 2 host all-reduce callback
+  int comm_mode = 0, nranks = 1, rank = 0;
+  int64_t n_global = 0;
+  nccl::Comm comm = nullptr;
+  gdwd_allreduce_cb host_ar = nullptr;
+  void* host_ar_user = nullptr;
+  DevBuf bundle;
+  double* bundle_h = nullptr;  // pinned, host all-reduce mode
+  size_t bundle_h_n = 0;
+  int comm_err = 0;
   cudaGraphExec_t gexec = nullptr;
   int64_t body_nodes = 0;
   cudaEvent_t ev_begin = nullptr, ev_loop = nullptr, ev_end = nullptr;
@@ -221,41 +273,97 @@ static int sp_grid(int64_t work_threads, int cap) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, cap));
 }
 
-// X.a == nullptr marks the context's sparse Z~ (CSR/CSC pair)
+// All-reduce (sum) of `count` doubles at dev across the sample shards.
+static void allreduce(gdwd_ctx* ctx, double* dev, int64_t count) {
+  if (ctx->comm_mode == 1) {
+    Launch L(ctx, "nccl_allreduce");
+    L.c->launches--;  // not one of our kernels
+    const nccl::Result r = nccl::api().AllReduce(dev, dev, (size_t)count, nccl::Float64, nccl::Sum, ctx->comm, ctx->st);
+    if (r != 0 && !ctx->comm_err) ctx->comm_err = r;
+  } else if (ctx->comm_mode == 2) {
+    if ((size_t)count > ctx->bundle_h_n) {
+      if (ctx->bundle_h) cudaFreeHost(ctx->bundle_h);
+      cudaMallocHost(&ctx->bundle_h, (size_t)count * sizeof(double));
+      ctx->bundle_h_n = (size_t)count;
+    }
+    cudaMemcpyAsync(ctx->bundle_h, dev, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->st);
+    cudaStreamSynchronize(ctx->st);
+    if (ctx->host_ar(ctx->host_ar_user, ctx->bundle_h, count) != 0 && !ctx->comm_err) ctx->comm_err = -1;
+    cudaMemcpyAsync(dev, ctx->bundle_h, count * sizeof(double), cudaMemcpyHostToDevice, ctx->st);
+  }
+}
+
+static bool sharded(const gdwd_ctx* ctx) { return ctx->comm_mode != 0; }
+static Scratch scr_bundle(const gdwd_ctx* ctx) {
+  Scratch s = ctx->scr;
+  s.bundle = ctx->bundle.p;
+  return s;
+}
+
+// X.a == nullptr marks the context's sparse Z~ (CSR/CSC pair).  A product
+// with Z~ over sharded samples runs as: local partial kernel -> all-reduce of
+// [Z~_local t | n-sums] -> epilogue kernel on every rank.
 template <class Op>
 static void run_zmv(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "zmv") {
+  const bool sh = sharded(ctx);
+  const Scratch sc = sh ? scr_bundle(ctx) : ctx->scr;
   if (!X.a) {
     const int g1 = sp_grid(ctx->n, NUM_SMS * 4);
     {
       Launch L(ctx, "sp_prep");
       sp_prep_kernel<Op><<<g1, SP_THREADS, 0, ctx->st>>>(op, ctx->n, ctx->tbuf.p, ctx->scr);
     }
+    {
+      Launch L(ctx, tag);
+      SpView A{ctx->csr_ptr, ctx->csr_idx, ctx->csr_val, ctx->d, ctx->n};
+      sp_zmv_kernel<Op><<<sp_grid(ctx->d * 32, NUM_SMS * 8), SP_THREADS, 0, ctx->st>>>(op, A, ctx->tbuf.p, g1, sc);
+    }
+  } else {
     Launch L(ctx, tag);
-    SpView A{ctx->csr_ptr, ctx->csr_idx, ctx->csr_val, ctx->d, ctx->n};
-    sp_zmv_kernel<Op><<<sp_grid(ctx->d * 32, NUM_SMS * 8), SP_THREADS, 0, ctx->st>>>(op, A, ctx->tbuf.p, g1, ctx->scr);
-    return;
+    ZmvGeom g = zmv_geom(X.rows, X.cols, slots_for(zmv_kernel<Op>, ZMV_THREADS, 0));
+    zmv_kernel<Op><<<dim3(g.tiles, g.segs), ZMV_THREADS, 0, ctx->st>>>(op, X, g, sc);
   }
-  Launch L(ctx, tag);
-  ZmvGeom g = zmv_geom(X.rows, X.cols, slots_for(zmv_kernel<Op>, ZMV_THREADS, 0));
-  zmv_kernel<Op><<<dim3(g.tiles, g.segs), ZMV_THREADS, 0, ctx->st>>>(op, X, g, ctx->scr);
+  if (sh) {
+    allreduce(ctx, ctx->bundle.p, (int64_t)Op::R * ctx->d + Op::NN);
+    Launch L(ctx, "zmv_epilogue");
+    zmv_epi_kernel<Op><<<vm_grid(ctx->d), VM_THREADS, 0, ctx->st>>>(op, ctx->bundle.p, ctx->d, ctx->scr);
+  }
 }
 template <class Op>
 static void run_zt(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "ztmv") {
-  Launch L(ctx, tag);
-  if (!X.a) {
-    SpView A{ctx->csc_ptr, ctx->csc_idx, ctx->csc_val, ctx->n, ctx->d};
-    sp_ztmv_kernel<Op, 8><<<sp_grid(ctx->n * 8, NUM_SMS * 8), SP_THREADS, 0, ctx->st>>>(op, A, ctx->scr);
-    return;
+  // sample-space reductions only for products with Z~ itself (not factors)
+  const bool sh = sharded(ctx) && Op::HAS_FIN && (!X.a || X.a == ctx->Zs);
+  const Scratch sc = sh ? scr_bundle(ctx) : ctx->scr;
+  {
+    Launch L(ctx, tag);
+    if (!X.a) {
+      SpView A{ctx->csc_ptr, ctx->csc_idx, ctx->csc_val, ctx->n, ctx->d};
+      sp_ztmv_kernel<Op, 8><<<sp_grid(ctx->n * 8, NUM_SMS * 8), SP_THREADS, 0, ctx->st>>>(op, A, sc);
+    } else {
+      const int cw = zt_geom(X.rows, X.ld, NUM_SMS).cw;
+      const size_t sm = (size_t)(cw + ZT_BATCH) * sizeof(double);
+      ZtGeom g = zt_geom(X.rows, X.ld, slots_for(ztmv_kernel<Op>, ZT_THREADS, sm));
+      ztmv_kernel<Op><<<dim3(g.chunks, g.ranges), ZT_THREADS, sm, ctx->st>>>(op, X, g, sc);
+    }
   }
-  const int cw = zt_geom(X.rows, X.ld, NUM_SMS).cw;
-  const size_t sm = (size_t)(cw + ZT_BATCH) * sizeof(double);
-  ZtGeom g = zt_geom(X.rows, X.ld, slots_for(ztmv_kernel<Op>, ZT_THREADS, sm));
-  ztmv_kernel<Op><<<dim3(g.chunks, g.ranges), ZT_THREADS, sm, ctx->st>>>(op, X, g, ctx->scr);
+  if (sh) {
+    allreduce(ctx, ctx->bundle.p, Op::NN);
+    fin_kernel<Op, Op::NN><<<1, 1, 0, ctx->st>>>(op, ctx->bundle.p);
+  }
 }
+// `samples`: the range is this rank's samples, so the fused sums are
+// all-reduced across shards before fin (d-space ranges are replicated).
 template <class Op>
-static void run_vm(gdwd_ctx* ctx, const Op& op, int64_t len, const char* tag = "vmap") {
-  Launch L(ctx, tag);
-  vmap_kernel<Op><<<vm_grid(len), VM_THREADS, 0, ctx->st>>>(op, len, ctx->scr);
+static void run_vm(gdwd_ctx* ctx, const Op& op, int64_t len, const char* tag = "vmap", bool samples = false) {
+  const bool sh = samples && sharded(ctx) && Op::HAS_FIN;
+  {
+    Launch L(ctx, tag);
+    vmap_kernel<Op><<<vm_grid(len), VM_THREADS, 0, ctx->st>>>(op, len, sh ? scr_bundle(ctx) : ctx->scr);
+  }
+  if (sh) {
+    allreduce(ctx, ctx->bundle.p, Op::NR);
+    fin_kernel<Op, Op::NR><<<1, 1, 0, ctx->st>>>(op, ctx->bundle.p);
+  }
 }
 
 static void prof_flush(gdwd_ctx* ctx) {
@@ -290,7 +398,8 @@ static int ensure_scratch(gdwd_ctx* ctx, int64_t rows, int64_t cols) {
     CK(cudaMemset(ctx->tickets, 0, nt * sizeof(unsigned)));
     ctx->ntickets = nt;
   }
-  ctx->scr = Scratch{ctx->part.p, ctx->npart.p, ctx->tpart.p, ctx->tickets};
+  CK(ctx->bundle.ensure(std::max<size_t>((size_t)2 * cols + 32, ctx->bundle.n)));
+  ctx->scr = Scratch{ctx->part.p, ctx->npart.p, ctx->tpart.p, ctx->tickets, nullptr};
   return GDWD_OK;
 }
 
@@ -318,6 +427,11 @@ __global__ void jacobi_kernel(const double* colsq, int64_t d, double mu2, double
     const double v = yty > mu2 ? yty : mu2;
     jac[j] = v > 1e-12 ? v : 1e-12;
   }
+}
+
+__global__ void add_diag_kernel(double* A, int64_t ld, int64_t d, double v) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < d) A[j * ld + j] += v;
 }
 
 __global__ void assemble_direct_kernel(double* A, int64_t ld, int64_t d, const double* zy, double yty) {
@@ -424,7 +538,7 @@ static int upload_rows(gdwd_ctx* ctx, const double* src, int64_t d, int64_t n, i
 static int compute_fro2(gdwd_ctx* ctx, const double* a, int64_t rows, int64_t cols, int64_t ld) {
   double* dv = nullptr;
   CK(cudaMalloc(&dv, sizeof(double)));
-  run_vm(ctx, OpSumSq{a, cols, ld, dv}, rows * cols, "vmap_fro2");
+  run_vm(ctx, OpSumSq{a, cols, ld, dv}, rows * cols, "vmap_fro2", true);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&ctx->fro2, dv, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
@@ -475,13 +589,15 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   if (ctx->Zs) cudaFree(ctx->Zs);
   free_sparse(ctx);
   for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle})
     b->release();
   end_session(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : {ctx->ev_begin, ctx->ev_loop, ctx->ev_end, ctx->poll_ev[0], ctx->poll_ev[1]})
     if (e) cudaEventDestroy(e);
   if (ctx->poll_flag) cudaFreeHost(ctx->poll_flag);
+  if (ctx->bundle_h) cudaFreeHost(ctx->bundle_h);
+  if (ctx->comm && nccl::api().ok) nccl::api().CommDestroy(ctx->comm);
   for (int b = 0; b < 2; ++b) {
     if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
     if (ctx->pin_ev[b]) cudaEventDestroy(ctx->pin_ev[b]);
@@ -622,6 +738,14 @@ int gdwd_set_problem(gdwd_ctx* ctx, const double* y, const double* e, const doub
   ctx->yty = yty;
   ctx->has_problem = true;
   ctx->data_gen++;
+  if (ctx->comm_mode) {  // a new local problem invalidates the communicator setup
+    if (ctx->comm && nccl::api().ok) nccl::api().CommDestroy(ctx->comm);
+    ctx->comm = nullptr;
+    ctx->comm_mode = 0;
+    ctx->nranks = 1;
+    ctx->rank = 0;
+  }
+  ctx->n_global = n;
   return GDWD_OK;
 }
 
@@ -687,7 +811,14 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
     size_t ws = std::max<size_t>((size_t)gram_workspace_doubles(M, K), (size_t)2 * m * ld);
     CK(ctx->facw.ensure(ws));
     if (kind == GDWD_BACKEND_DIRECT) {
-      CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, true, 1.0, mu2, ctx->fac.p, ld, ctx->facw.p, ctx->st));
+      if (sharded(ctx)) {
+        // local Z_p Z_p^T, summed over the shards once (8 MB at d=1000), then + mu^2 I
+        CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, true, 1.0, 0.0, ctx->fac.p, ld, ctx->facw.p, ctx->st));
+        allreduce(ctx, ctx->fac.p, (int64_t)m * ld);
+        add_diag_kernel<<<(unsigned)((d + 255) / 256), 256, 0, ctx->st>>>(ctx->fac.p, ld, d, mu2);
+      } else {
+        CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, true, 1.0, mu2, ctx->fac.p, ld, ctx->facw.p, ctx->st));
+      }
       assemble_direct_kernel<<<(unsigned)((d + 256) / 256), 256, 0, ctx->st>>>(ctx->fac.p, ld, d, D.zy, ctx->yty);
     } else {
       // keep K = Z^T Z for the Gram-space iteration; G = K/mu^2 + I
@@ -721,6 +852,7 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
       SpView A{ctx->csr_ptr, ctx->csr_idx, ctx->csr_val, d, n};
       sp_rowsq_kernel<<<(unsigned)((d + 255) / 256), 256, 0, ctx->st>>>(A, ctx->colsq.p);
     }
+    if (sharded(ctx)) allreduce(ctx, ctx->colsq.p, d);
     jacobi_kernel<<<(unsigned)((d + 256) / 256), 256, 0, ctx->st>>>(ctx->colsq.p, d, mu2, ctx->yty,
                                                                      const_cast<double*>(D.jac));
     CK(cudaGetLastError());
@@ -793,7 +925,7 @@ static void enqueue_tail(gdwd_ctx* ctx) {
   run_vm(ctx, OpCopyIfReuse{D, D.ztwb, D.ztw}, D.n, "vmap_copy_ztw");
   run_vm(ctx, OpStep2a{D}, D.d, "vmap_step2a");
   run_vm(ctx, OpStep2b{D}, D.d, "vmap_step2b");
-  run_vm(ctx, OpStep3{D}, D.n, "vmap_step3_kkt");
+  run_vm(ctx, OpStep3{D}, D.n, "vmap_step3_kkt", true);
 }
 
 static void enqueue_body_fixed(gdwd_ctx* ctx, int kind, bool use_sgs) {
@@ -897,8 +1029,12 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   CK(cudaSetDevice(ctx->device));
   end_session(ctx);
   const int64_t n = ctx->n, d = ctx->d, m = d + 1;
-  int kind = cfg->backend == GDWD_BACKEND_AUTO ? select_kind(n, d) : cfg->backend;
+  const int64_t ng = ctx->n_global > 0 ? ctx->n_global : n;  // sharded: the global sample count
+  int kind = cfg->backend == GDWD_BACKEND_AUTO ? select_kind(ng, d) : cfg->backend;
   if (kind < 1 || kind > 3) return set_err(ctx, GDWD_ERR_VALUE, "bad backend");
+  if (sharded(ctx) && kind == GDWD_BACKEND_SMW2)
+    return set_err(ctx, GDWD_ERR_UNSUPPORTED,
+                   "SMW2 couples all samples through the n x n Gram: run it unsharded (replicas)");
   const double mu = cfg->mu, mu2 = mu * mu, q = ctx->q, C = ctx->C;
   const int max_iter = cfg->max_iter;
 
@@ -954,7 +1090,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   // the device at upload
   const double eps_c = isnan(cfg->epsilon_c) ? 1.0 / std::max(1.0, sqrt(ctx->fro2)) : cfg->epsilon_c;
   std::vector<double> tab(2 * (size_t)(max_iter + 2) + (size_t)std::max<int64_t>(sched_len, 1), 0.0);
-  const double sqrt_n = sqrt((double)n);
+  const double sqrt_n = sqrt((double)ng);
   for (int k = 0; k < max_iter + 2; ++k) {
     tab[k] = eps_c / pow(k + 1.0, 1.5);
     tab[(max_iter + 2) + k] = tab[k] / sqrt_n;
@@ -968,7 +1104,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   D.sched_len = (int)sched_len;
 
   double sigma0 = cfg->sigma0;
-  if (isnan(sigma0)) sigma0 = pow(std::min(10.0 * C, (double)n), q);
+  if (isnan(sigma0)) sigma0 = pow(std::min(10.0 * C, (double)ng), q);
 
   // ---- setup: zy, factor / preconditioner ------------------------------------
   CK(cudaEventRecord(ctx->ev_begin, ctx->st));
@@ -1006,7 +1142,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   ctx->ps_per_iter.assign(max_iter + 1, 0.0);
   ctx->kind = kind;
   ctx->gram = gram;
-  ctx->persistent = gram && cfg->persistent && !ctx->prof;
+  ctx->persistent = gram && cfg->persistent && !ctx->prof && !sharded(ctx);
   ctx->use_sgs = cfg->use_sgs != 0;
   ctx->poll = std::max(1, cfg->poll_every);
   ctx->max_iter = max_iter;
@@ -1025,7 +1161,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
     if (nb < 1) ctx->persistent = false;
     else CK(ctx->pk_part.ensure((size_t)2 * NUM_SMS * PK_NPART));
   }
-  if (kind != GDWD_BACKEND_ITERATIVE && cfg->use_graph && !ctx->prof && !ctx->persistent) {
+  if (kind != GDWD_BACKEND_ITERATIVE && cfg->use_graph && !ctx->prof && !ctx->persistent && ctx->comm_mode != 2) {
     cudaGraph_t graph;
     const int64_t before = ctx->launches;
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
@@ -1182,6 +1318,64 @@ extern "C" int gdwd_frobenius_sq(gdwd_ctx* ctx, double* out) {
   if (!ctx || !out || ctx->fro2 < 0) return set_err(ctx, GDWD_ERR_VALUE, "no data uploaded");
   *out = ctx->fro2;
   return GDWD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// sample sharding
+// ---------------------------------------------------------------------------
+static int comm_finish_init(gdwd_ctx* ctx, int32_t nranks, int32_t rank, int64_t n_global) {
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  ctx->n_global = n_global;
+  ctx->data_gen++;  // factors depend on the global data
+  // global ||Z~||_F^2 and check of the global sample count
+  DevBuf tmp;
+  CK(tmp.ensure(2));
+  double hv[2] = {ctx->fro2, (double)ctx->n};
+  CK(cudaMemcpy(tmp.p, hv, sizeof(hv), cudaMemcpyHostToDevice));
+  allreduce(ctx, tmp.p, 2);
+  CK(cudaMemcpyAsync(hv, tmp.p, sizeof(hv), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  tmp.release();
+  if (ctx->comm_err) return set_err(ctx, GDWD_ERR_CUDA, "all-reduce failed during communicator setup");
+  if ((int64_t)hv[1] != n_global) return set_err(ctx, GDWD_ERR_VALUE, "shard sizes do not add up to n_global");
+  ctx->fro2 = hv[0];
+  ctx->yty = (double)n_global;  // labels are +-1 (validated in set_problem)
+  return GDWD_OK;
+}
+
+extern "C" int gdwd_comm_unique_id(uint8_t* out128) {
+  if (!out128) return GDWD_ERR_VALUE;
+  if (!nccl::api().ok) return GDWD_ERR_UNSUPPORTED;
+  nccl::UniqueId id;
+  if (nccl::api().GetUniqueId(&id) != 0) return GDWD_ERR_CUDA;
+  memcpy(out128, id.internal, 128);
+  return GDWD_OK;
+}
+
+extern "C" int gdwd_comm_init_nccl(gdwd_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t* id128,
+                                   int64_t n_global) {
+  if (!ctx || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return set_err(ctx, GDWD_ERR_VALUE, "bad comm arguments");
+  if (!ctx->has_problem) return set_err(ctx, GDWD_ERR_VALUE, "set the local problem before the communicator");
+  if (!nccl::api().ok) return set_err(ctx, GDWD_ERR_UNSUPPORTED, "libnccl.so.2 not found");
+  CK(cudaSetDevice(ctx->device));
+  nccl::UniqueId id;
+  memcpy(id.internal, id128, 128);
+  const nccl::Result r = nccl::api().CommInitRank(&ctx->comm, nranks, id, rank);
+  if (r != 0) return set_err(ctx, GDWD_ERR_CUDA, std::string("ncclCommInitRank: ") + nccl::api().GetErrorString(r));
+  ctx->comm_mode = 1;
+  return comm_finish_init(ctx, nranks, rank, n_global);
+}
+
+extern "C" int gdwd_comm_init_host(gdwd_ctx* ctx, int32_t nranks, int32_t rank, gdwd_allreduce_cb cb, void* user,
+                                   int64_t n_global) {
+  if (!ctx || !cb || nranks < 1 || rank < 0 || rank >= nranks) return set_err(ctx, GDWD_ERR_VALUE, "bad comm arguments");
+  if (!ctx->has_problem) return set_err(ctx, GDWD_ERR_VALUE, "set the local problem before the communicator");
+  CK(cudaSetDevice(ctx->device));
+  ctx->host_ar = cb;
+  ctx->host_ar_user = user;
+  ctx->comm_mode = 2;
+  return comm_finish_init(ctx, nranks, rank, n_global);
 }
 
 extern "C" int gdwd_set_profile(gdwd_ctx* ctx, int32_t enable) {

@@ -77,7 +77,14 @@ __global__ void __launch_bounds__(SP_THREADS) sp_zmv_kernel(Op op, SpView A, con
       for (int r = 0; r < R; ++r) acc[r] += v * tbuf[r * A.other + c];
     }
     warp_sum<R>(acc);
-    if (lane == 0) op.epi(j, acc, dacc);
+    if (lane == 0) {
+      if (s.bundle) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) s.bundle[(int64_t)r * A.rows + j] = acc[r];
+      } else {
+        op.epi(j, acc, dacc);
+      }
+    }
   }
   block_sum<ND>(dacc, red);
   if (threadIdx.x == 0) {
@@ -88,7 +95,14 @@ __global__ void __launch_bounds__(SP_THREADS) sp_zmv_kernel(Op op, SpView A, con
   double nsum[NN], dsum[ND];
   block_sum_partials<NN>(s.npart, nprep, nsum, red2);
   block_sum_partials<ND>(s.tpart, gridDim.x, dsum, red2);
-  if (threadIdx.x == 0) op.fin(nsum, dsum);
+  if (threadIdx.x == 0) {
+    if (s.bundle) {
+#pragma unroll
+      for (int k = 0; k < NN; ++k) s.bundle[(int64_t)R * A.rows + k] = nsum[k];
+    } else {
+      op.fin(nsum, dsum);
+    }
+  }
 }
 
 // dot_i = sum_j Z[j,i] w_j (CSC columns = samples); G lanes per sample.
@@ -125,7 +139,14 @@ __global__ void __launch_bounds__(SP_THREADS) sp_ztmv_kernel(Op op, SpView A, Sc
   if (!last_arrival(&s.tickets[0], gridDim.x)) return;
   double nsum[NN];
   block_sum_partials<NN>(s.npart, gridDim.x, nsum, red);
-  if (threadIdx.x == 0) op.fin(nsum);
+  if (threadIdx.x == 0) {
+    if (s.bundle) {
+#pragma unroll
+      for (int k = 0; k < NN; ++k) s.bundle[k] = nsum[k];
+    } else {
+      op.fin(nsum);
+    }
+  }
 }
 
 // row sums of squares of CSR rows in stored (sample) order: the same

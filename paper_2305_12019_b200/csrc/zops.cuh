@@ -29,6 +29,7 @@ struct Scratch {
   double* npart;      // per-CTA n-sum partials
   double* tpart;      // per-tile d-sum partials
   unsigned* tickets;  // zero-initialised ticket counters
+  double* bundle;     // sharded mode: local [R*d vector | n-sums] for the all-reduce (null: fused)
 };
 
 // ---------------------------------------------------------------------------
@@ -121,6 +122,31 @@ __global__ void __launch_bounds__(ZMV_THREADS) zmv_kernel(Op op, MatView X, ZmvG
     }
   }
   if (!last_arrival(&s.tickets[tile], gridDim.y)) return;
+
+  if (s.bundle) {
+    // sharded: publish the local Z~ t (this tile) and the n-sums, no epilogue
+    if (colok) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double v0 = 0.0, v1 = 0.0;
+        for (int sg = 0; sg < (int)gridDim.y; ++sg) {
+          const double2 pv = __ldcg(reinterpret_cast<const double2*>(s.part + ((int64_t)sg * R + r) * g.ldp + j0));
+          v0 += pv.x;
+          v1 += pv.y;
+        }
+        s.bundle[(int64_t)r * X.cols + j0] = v0;
+        if (j0 + 1 < X.cols) s.bundle[(int64_t)r * X.cols + j0 + 1] = v1;
+      }
+    }
+    if (!last_arrival(&s.tickets[gridDim.x], gridDim.x)) return;
+    double nsum[NN];
+    block_sum_partials<NN>(s.npart, gridDim.y, nsum, red);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < NN; ++k) s.bundle[(int64_t)R * X.cols + k] = nsum[k];
+    }
+    return;
+  }
 
   double dacc[ND];
 #pragma unroll
@@ -242,7 +268,14 @@ __global__ void __launch_bounds__(ZT_THREADS) ztmv_kernel(Op op, MatView X, ZtGe
   if (!last_arrival(&s.tickets[single ? 0 : gridDim.y], gridDim.y)) return;
   double nsum[NN];
   block_sum_partials<NN>(s.npart, gridDim.y, nsum, red);
-  if (threadIdx.x == 0) op.fin(nsum);
+  if (threadIdx.x == 0) {
+    if (s.bundle) {
+#pragma unroll
+      for (int k = 0; k < NN; ++k) s.bundle[k] = nsum[k];
+    } else {
+      op.fin(nsum);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -269,7 +302,58 @@ __global__ void __launch_bounds__(VM_THREADS) vmap_kernel(Op op, int64_t len, Sc
   if (!last_arrival(&s.tickets[0], gridDim.x)) return;
   double sum[NR];
   block_sum_partials<NR>(s.npart, gridDim.x, sum, red);
-  if (threadIdx.x == 0) op.fin(sum);
+  if (threadIdx.x == 0) {
+    if (s.bundle) {
+#pragma unroll
+      for (int k = 0; k < NR; ++k) s.bundle[k] = sum[k];
+    } else {
+      op.fin(sum);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Sharded mode: after the all-reduce of the bundle, every rank runs the
+// epilogue on identical data (so replicated d-space state stays identical).
+// ---------------------------------------------------------------------------
+template <class Op>
+__global__ void __launch_bounds__(VM_THREADS) zmv_epi_kernel(Op op, const double* bundle, int64_t d, Scratch s) {
+  constexpr int R = Op::R, NN = Op::NN, ND = Op::ND;
+  if (op.skip()) return;
+  __shared__ double red[(VM_THREADS / 32) * (NN > ND ? NN : ND)];
+  double dacc[ND];
+#pragma unroll
+  for (int k = 0; k < ND; ++k) dacc[k] = 0.0;
+  for (int64_t j = blockIdx.x * (int64_t)VM_THREADS + threadIdx.x; j < d; j += (int64_t)gridDim.x * VM_THREADS) {
+    double v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = bundle[(int64_t)r * d + j];
+    op.epi(j, v, dacc);
+  }
+  block_sum<ND>(dacc, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < ND; ++k) s.tpart[(int64_t)blockIdx.x * ND + k] = dacc[k];
+  }
+  if (!last_arrival(&s.tickets[0], gridDim.x)) return;
+  double dsum[ND];
+  block_sum_partials<ND>(s.tpart, gridDim.x, dsum, red);
+  if (threadIdx.x == 0) {
+    double nsum[NN];
+#pragma unroll
+    for (int k = 0; k < NN; ++k) nsum[k] = bundle[(int64_t)R * d + k];
+    op.fin(nsum, dsum);
+  }
+}
+
+// fin of an n-reducing ztmv / vmap op with the all-reduced sums
+template <class Op, int K>
+__global__ void fin_kernel(Op op, const double* bundle) {
+  if (op.skip()) return;
+  double sum[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) sum[k] = bundle[k];
+  op.fin(sum);
 }
 
 }  // namespace gdwd

@@ -1,0 +1,162 @@
+"""Sample-sharded solves across GPUs.
+
+Z~ is split by contiguous blocks of sample columns; each rank (one process per
+GPU) uploads its block and its slices of y, e and the weights.  Feature-space
+work (w, u, rho, h, the DIRECT factor, PSQMR vectors) is replicated and stays
+bit-identical across ranks; every sum over samples is all-reduced -- the
+d-partial of each Z~ t together with the n-sums of the same pass (one bundle
+per reduction point), the n-sums of the per-sample passes, and once at setup
+Z~y, ||Z~||_F^2, the Jacobi diagonal and (DIRECT) the d x d Gram.
+
+Communicators:
+  * ``NcclCommunicator``: NCCL over NVLink/NVSwitch, bootstrapped with a
+    ``torch.distributed`` broadcast of the NCCL unique id (torchrun launches).
+  * ``HostCommunicator``: all-reduce through a host callback (gloo process
+    groups, or threads emulating ranks on one GPU in tests).
+
+SMW2 couples all samples through its n x n Gram, so it is not sharded
+(``bench.py --gpus N`` runs replicas for config 2).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib
+from .solver import DeviceProblem, ProblemData, _check, device_problem
+from .sparse import SparseMatrixCSC
+
+
+def shard_bounds(n: int, nranks: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced sample block [lo, hi) of `rank`."""
+    if not 0 <= rank < nranks:
+        raise ValueError("rank out of range")
+    return n * rank // nranks, n * (rank + 1) // nranks
+
+
+def shard_problem(data: ProblemData, rank: int, nranks: int) -> ProblemData:
+    """The local ProblemData of `rank`: its block of Z~ columns and the
+    matching slices of y, e and the weights (z_scale, C, q unchanged)."""
+    lo, hi = shard_bounds(data.n, nranks, rank)
+    z = data.z_tilde
+    if z.is_dense:
+        zl = SparseMatrixCSC.from_dense_samples(z.dense_samples()[lo:hi])
+    else:
+        cp = z.colptr
+        a, b = int(cp[lo]), int(cp[hi])
+        zl = SparseMatrixCSC(z.nrows, hi - lo, cp[lo:hi + 1] - a, z.rowidx[a:b], z.values[a:b])
+    return ProblemData(zl, data.y[lo:hi], data.e[lo:hi], data.weights[lo:hi], data.C, data.q, data.z_scale)
+
+
+class HostCommunicator:
+    """Sum-all-reduce through a Python function ``allreduce(np.ndarray) ->
+    np.ndarray`` (e.g. torch.distributed with gloo, or a thread barrier)."""
+
+    def __init__(self, allreduce: Callable[[np.ndarray], np.ndarray], nranks: int, rank: int):
+        self.allreduce, self.nranks, self.rank = allreduce, nranks, rank
+        self._err: list = []
+
+        def _cb(user, buf, count):
+            try:
+                arr = np.ctypeslib.as_array(buf, shape=(count,))
+                arr[:] = self.allreduce(arr.copy())
+                return 0
+            except BaseException as exc:  # pragma: no cover - surfaced by the caller
+                self._err.append(exc)
+                return 1
+
+        self._cfun = _lib.ALLREDUCE_CB(_cb)
+
+    def attach(self, dp: DeviceProblem, n_global: int) -> None:
+        lib = _lib.load()
+        _check(lib.gdwd_comm_init_host(dp.ctx, self.nranks, self.rank, self._cfun, None, int(n_global)), dp.ctx,
+               "comm_init_host")
+        dp.comm = self
+
+
+class NcclCommunicator:
+    """NCCL communicator over the ranks of a torch.distributed group."""
+
+    def __init__(self, nranks: int, rank: int, broadcast_id: Callable[[Optional[bytes]], bytes]):
+        """``broadcast_id(id_or_None)``: rank 0 passes its id, every rank gets it back."""
+        lib = _lib.load()
+        uid = None
+        if rank == 0:
+            buf = (C.c_uint8 * 128)()
+            _check(lib.gdwd_comm_unique_id(buf), None, "nccl unique id")
+            uid = bytes(buf)
+        self.uid = broadcast_id(uid)
+        self.nranks, self.rank = nranks, rank
+
+    @classmethod
+    def from_torch(cls) -> "NcclCommunicator":
+        import torch.distributed as dist
+
+        def bcast(uid):
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            return obj[0]
+
+        return cls(dist.get_world_size(), dist.get_rank(), bcast)
+
+    def attach(self, dp: DeviceProblem, n_global: int) -> None:
+        lib = _lib.load()
+        ida = (C.c_uint8 * 128).from_buffer_copy(self.uid)
+        _check(lib.gdwd_comm_init_nccl(dp.ctx, self.nranks, self.rank, ida, int(n_global)), dp.ctx,
+               "comm_init_nccl")
+        dp.comm = self
+
+
+def attach(local: ProblemData, comm, n_global: int, device: Optional[int] = None) -> DeviceProblem:
+    """Upload the local shard (if not yet resident) and join the communicator;
+    later ``sgs_admm_solve(local, ...)`` calls run sharded."""
+    dp = device_problem(local, device)
+    comm.attach(dp, n_global)
+    return dp
+
+
+def global_train_error(result, local: ProblemData, allreduce: Callable[[np.ndarray], np.ndarray],
+                       n_global: int) -> float:
+    """Train error over all shards (solver.py:558-559): each rank counts its
+    misclassified samples from its slice of y and Z~^T w."""
+    st = result.final_state
+    ztw = result.extras_ztw if hasattr(result, "extras_ztw") else None
+    if ztw is None:
+        ztw = device_problem(local).state()["ztw"]
+    scores = st.beta + local.y * ztw
+    bad = np.array([float(np.sum(local.y * np.sign(scores) <= 0.0))])
+    return 100.0 * float(allreduce(bad)[0]) / n_global
+
+
+class ThreadRanks:
+    """Emulate `nranks` ranks as threads of one process (sum all-reduce via a
+    barrier) -- the host side of virtual-rank tests on a single GPU."""
+
+    def __init__(self, nranks: int):
+        self.nranks = nranks
+        self.barrier = threading.Barrier(nranks)
+        self.slots: list = [None] * nranks
+        self.result = None
+
+    def allreduce_for(self, rank: int) -> Callable[[np.ndarray], np.ndarray]:
+        def ar(x: np.ndarray) -> np.ndarray:
+            self.slots[rank] = x
+            if self.barrier.wait() == 0:
+                acc = self.slots[0].copy()
+                for r in range(1, self.nranks):
+                    acc += self.slots[r]  # fixed rank order: identical on every rank
+                self.result = acc
+            self.barrier.wait()
+            out = self.result.copy()
+            self.barrier.wait()
+            return out
+
+        return ar
+
+
+__all__ = ["HostCommunicator", "NcclCommunicator", "ThreadRanks", "attach", "global_train_error",
+           "shard_bounds", "shard_problem"]
