@@ -180,10 +180,12 @@ def run_b200(args, dist: Dist):
     device = dist.local
     cfg_syn = synth.CONFIGS[args.config]
     t0 = time.perf_counter()
-    prob = synth.make_problem(cfg_syn, args.seed)
+    on_device = 8.0 * cfg_syn.n * cfg_syn.d > 40e9  # config 5: generated in HBM
+    prob = (synth.make_device_problem(cfg_syn, args.seed, device) if on_device
+            else synth.make_problem(cfg_syn, args.seed))
     gen_s = time.perf_counter() - t0
     n, d = prob.n, prob.d
-    nnz = None if prob.z_tilde.is_dense else prob.z_tilde.nnz
+    nnz = None if (prob.z_tilde is None or prob.z_tilde.is_dense) else prob.z_tilde.nnz
     K, W = args.steps, args.warmup
     total = W + K
     conf = make_config(G, prob, total + 1)
@@ -292,7 +294,10 @@ def run_b200(args, dist: Dist):
 
     # ---- end to end through the public API ------------------------------------
     e2e = None
-    if not args.no_e2e:
+    if on_device:
+        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "note": "X generated in HBM (160 GB exceeds host memory); no host-buffer path"}
+    elif not args.no_e2e:
         prob2 = synth.make_problem(cfg_syn, args.seed)  # fresh host ProblemData: nothing resident
         conf2 = make_config(G, prob2, K)
         dist.barrier()
@@ -328,7 +333,8 @@ def run_b200(args, dist: Dist):
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": dist.world, "steps": iters_timed,
         "warmup": W, "ms_per_step": round(step_ms, 5), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: seeded two-Gaussian generator with BASELINE config 2 shapes (paper_2305_12019_b200.synth)",
+        "data": "synthetic: seeded generator with BASELINE %s shapes (paper_2305_12019_b200.synth%s)"
+                % (args.config, ", generated on the device" if on_device else ""),
         "config": {"workload": WORKLOADS.get(args.config, args.config) + (
                        " [Gram-space, persistent cooperative kernel]" if persistent else ""),
                    "d": d, "n": n, "parallelism": "replicas" if dist.world > 1 else "single",
@@ -394,7 +400,7 @@ def main():
         return
     line = run_b200(args, dist)
     if dist.rank == 0:
-        if not args.no_cpu and dist.world == 1:
+        if not args.no_cpu and dist.world == 1 and args.config != "c5":
             line["cpu_baseline"] = run_cpu_oracle(args, args.cpu_steps, 1, "cpu")
         print(json.dumps(line), flush=True)
     dist.close()

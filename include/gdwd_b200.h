@@ -102,6 +102,17 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
 /* Sparse Z~ in the reference's CSC layout (int64 colptr/rowidx). */
 int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx, const double* values,
                     int64_t d, int64_t n);
+/* On-device synthetic data (configs too large for host memory): raw samples
+ * x_i = ytrue_i * shift * 1[j < signal_k] + N(0, I) for global sample indices
+ * offset .. offset+n-1 (counter-based, shard-consistent; kind 0 = two
+ * Gaussians).  Then scale in place to Z~ = X diag(y) / z_scale
+ * (scale_problem, solver.py:253-285).  gdwd_frobenius_sq reports ||X||_F^2
+ * after generation and ||Z~||_F^2 after scaling. */
+int gdwd_generate_dense(gdwd_ctx* ctx, int32_t kind, uint64_t seed, int64_t d, int64_t n, int64_t offset,
+                        int64_t signal_k, double shift);
+int gdwd_scale_dense(gdwd_ctx* ctx, const double* y, double z_scale);
+/* copy the (local) dense samples back as row-major [n][d] (tests, proxies) */
+int gdwd_download_dense(gdwd_ctx* ctx, double* samples);
 /* ||Z~||_F^2, reduced on the device at upload (frobenius_norm, sparse.py:63). */
 int gdwd_frobenius_sq(gdwd_ctx* ctx, double* out);
 /* ProblemData vectors and scalars (solver.py:60-71); all length n. */

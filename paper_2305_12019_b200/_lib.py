@@ -27,7 +27,8 @@ SYMBOLS = [
     "gdwd_get_history", "gdwd_newton_sweep", "gdwd_chol_inverse", "gdwd_gram", "gdwd_psqmr_dense",
     "gdwd_solve_begin", "gdwd_solve_iterate", "gdwd_solve_end", "gdwd_time_iterations", "gdwd_set_profile",
     "gdwd_get_profile", "gdwd_reset_counters", "gdwd_frobenius_sq", "gdwd_comm_unique_id",
-    "gdwd_comm_init_nccl", "gdwd_comm_init_host",
+    "gdwd_comm_init_nccl", "gdwd_comm_init_host", "gdwd_generate_dense", "gdwd_scale_dense",
+    "gdwd_download_dense",
 ]
 
 
@@ -87,6 +88,9 @@ def _declare(lib):
         "gdwd_reset_counters": (C.c_int, [vp]),
         "gdwd_frobenius_sq": (C.c_int, [vp, _P]),
         "gdwd_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+        "gdwd_generate_dense": (C.c_int, [vp, C.c_int32, C.c_uint64, _I64, _I64, _I64, _I64, C.c_double]),
+        "gdwd_scale_dense": (C.c_int, [vp, _P, C.c_double]),
+        "gdwd_download_dense": (C.c_int, [vp, _P]),
         "gdwd_comm_init_nccl": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int64]),
         "gdwd_comm_init_host": (C.c_int, [vp, C.c_int32, C.c_int32, ALLREDUCE_CB, vp, C.c_int64]),
         "gdwd_get_state": (C.c_int, [vp, _P, _P, _P, _P, _P, _P, _P, _P]),

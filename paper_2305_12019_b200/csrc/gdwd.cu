@@ -29,6 +29,7 @@
 #include "solver_ops.cuh"
 #include "spops.cuh"
 #include "persist.cuh"
+#include "synth.cuh"
 #include "zops.cuh"
 
 using namespace gdwd;
@@ -403,7 +404,18 @@ static int ensure_scratch(gdwd_ctx* ctx, int64_t rows, int64_t cols) {
   return GDWD_OK;
 }
 
-// column sums of squares (row_sq_sums, sparse.py:66-70) via zmv with t = x
+// column sums of squares (row_sq_sums, sparse.py:66-70): sequential per
+// column (same order as np.bincount) for moderate n, segmented zmv beyond
+struct OpColSq {
+  static constexpr int R = 1, NN = 1, ND = 1;
+  static constexpr bool SQ = true;
+  double* out;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV void input(int64_t, double (&t)[R], double (&)[NN]) const { t[0] = 1.0; }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&)[ND]) const { out[j] = v[0]; }
+  GDWD_DEV void fin(const double (&)[NN], const double (&)[ND]) const {}
+};
+// (sequential variant below)
 struct OpColSqPrep {};
 template <class Op>
 __global__ void colsq_kernel(MatView X, double* out) {
@@ -711,6 +723,51 @@ static int densify(gdwd_ctx* ctx) {
   return GDWD_OK;
 }
 
+int gdwd_generate_dense(gdwd_ctx* ctx, int32_t kind, uint64_t seed, int64_t d, int64_t n, int64_t offset,
+                        int64_t signal_k, double shift) {
+  if (!ctx || d < 1 || n < 1 || offset < 0) return set_err(ctx, GDWD_ERR_VALUE, "bad generation arguments");
+  if (kind != 0) return set_err(ctx, GDWD_ERR_UNSUPPORTED, "only the two-Gaussian generator runs on the device");
+  CK(cudaSetDevice(ctx->device));
+  free_sparse(ctx);
+  if (ctx->Zs) cudaFree(ctx->Zs);
+  ctx->Zs = nullptr;
+  const int64_t ld = (d + 1) / 2 * 2;
+  CK(cudaMalloc(&ctx->Zs, (size_t)n * ld * sizeof(double)));
+  if (ld != d) CK(cudaMemsetAsync(ctx->Zs, 0, (size_t)n * ld * sizeof(double), ctx->st));
+  gen_gauss_kernel<<<NUM_SMS * 16, 256, 0, ctx->st>>>(ctx->Zs, ld, d, n, offset, seed, signal_k, shift);
+  CK(cudaGetLastError());
+  ctx->n = n;
+  ctx->d = d;
+  ctx->ldz = ld;
+  ctx->has_dense = true;
+  ctx->has_problem = false;
+  ctx->data_gen++;
+  RC(ensure_scratch(ctx, n, d));
+  return compute_fro2(ctx, ctx->Zs, n, d, ld);  // ||X||_F^2 of the raw (local) samples
+}
+
+int gdwd_scale_dense(gdwd_ctx* ctx, const double* y, double z_scale) {
+  if (!ctx || !ctx->has_dense || !y || !(z_scale > 0)) return set_err(ctx, GDWD_ERR_VALUE, "bad scale arguments");
+  CK(cudaSetDevice(ctx->device));
+  DevBuf yd;
+  CK(yd.ensure(ctx->n));
+  CK(cudaMemcpy(yd.p, y, ctx->n * sizeof(double), cudaMemcpyHostToDevice));
+  scale_rows_kernel<<<NUM_SMS * 16, 256, 0, ctx->st>>>(ctx->Zs, ctx->ldz, ctx->d, ctx->n, yd.p, z_scale);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->st));
+  yd.release();
+  ctx->data_gen++;
+  return compute_fro2(ctx, ctx->Zs, ctx->n, ctx->d, ctx->ldz);
+}
+
+int gdwd_download_dense(gdwd_ctx* ctx, double* samples) {
+  if (!ctx || !ctx->has_dense || !samples) return set_err(ctx, GDWD_ERR_VALUE, "no dense data");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpy2D(samples, ctx->d * sizeof(double), ctx->Zs, ctx->ldz * sizeof(double), ctx->d * sizeof(double),
+                  ctx->n, cudaMemcpyDeviceToHost));
+  return GDWD_OK;
+}
+
 int gdwd_set_problem(gdwd_ctx* ctx, const double* y, const double* e, const double* weights, double C, double q,
                      double z_scale) {
   if (!ctx || !(ctx->has_dense || ctx->has_sparse)) return set_err(ctx, GDWD_ERR_VALUE, "upload Z~ before set_problem");
@@ -846,7 +903,12 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
       RC(ensure_scratch(ctx, n, d));
     }
   } else {
-    if (Z.a) {
+    if (Z.a && n >= 65536) {
+      const int comm_mode = ctx->comm_mode;
+      ctx->comm_mode = 0;  // local sums; all-reduced below
+      run_zmv(ctx, OpColSq{ctx->colsq.p}, Z, "zmv_colsq");
+      ctx->comm_mode = comm_mode;
+    } else if (Z.a) {
       colsq_kernel<OpColSqPrep><<<(unsigned)((d + 255) / 256), 256, 0, ctx->st>>>(Z, ctx->colsq.p);
     } else {
       SpView A{ctx->csr_ptr, ctx->csr_idx, ctx->csr_val, d, n};

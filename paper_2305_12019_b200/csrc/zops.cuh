@@ -15,6 +15,8 @@
 // HBM layout: rows are padded to ld (multiple of 2 doubles, zero-filled) so
 // every thread streams 16-byte double2 loads with L1::no_allocate.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace gdwd {
@@ -46,6 +48,12 @@ struct ZmvGeom {
   int64_t seg_len;
   int64_t ldp;  // leading dim of partial rows (>= cols, even)
 };
+
+// Ops may declare SQ = true to accumulate z*z (column sums of squares)
+template <class Op, class = void>
+struct op_sq : std::false_type {};
+template <class Op>
+struct op_sq<Op, std::void_t<decltype(Op::SQ)>> : std::integral_constant<bool, Op::SQ> {};
 
 template <class Op>
 __global__ void __launch_bounds__(ZMV_THREADS) zmv_kernel(Op op, MatView X, ZmvGeom g, Scratch s) {
@@ -92,9 +100,9 @@ __global__ void __launch_bounds__(ZMV_THREADS) zmv_kernel(Op op, MatView X, ZmvG
         for (int u = 0; u < 4; ++u) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            const double t = ts[r][ii + u];
-            acc[r][0] += z[u].x * t;
-            acc[r][1] += z[u].y * t;
+            const double t = op_sq<Op>::value ? 1.0 : ts[r][ii + u];
+            acc[r][0] += z[u].x * (op_sq<Op>::value ? z[u].x : t);
+            acc[r][1] += z[u].y * (op_sq<Op>::value ? z[u].y : t);
           }
         }
       }
@@ -103,8 +111,8 @@ __global__ void __launch_bounds__(ZMV_THREADS) zmv_kernel(Op op, MatView X, ZmvG
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const double t = ts[r][ii];
-          acc[r][0] += z.x * t;
-          acc[r][1] += z.y * t;
+          acc[r][0] += z.x * (op_sq<Op>::value ? z.x : t);
+          acc[r][1] += z.y * (op_sq<Op>::value ? z.y : t);
         }
       }
     }

@@ -76,6 +76,7 @@ class HostCommunicator:
         _check(lib.gdwd_comm_init_host(dp.ctx, self.nranks, self.rank, self._cfun, None, int(n_global)), dp.ctx,
                "comm_init_host")
         dp.comm = self
+        dp.n_global = int(n_global)
 
 
 class NcclCommunicator:
@@ -109,6 +110,7 @@ class NcclCommunicator:
         _check(lib.gdwd_comm_init_nccl(dp.ctx, self.nranks, self.rank, ida, int(n_global)), dp.ctx,
                "comm_init_nccl")
         dp.comm = self
+        dp.n_global = int(n_global)
 
 
 def attach(local: ProblemData, comm, n_global: int, device: Optional[int] = None) -> DeviceProblem:

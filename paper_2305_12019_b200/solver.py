@@ -301,7 +301,7 @@ class DeviceProblem:
     Z~ is uploaded once; repeated solves on the same ProblemData reuse it and
     the cached factorisation."""
 
-    def __init__(self, data: ProblemData, device: int = 0):
+    def __init__(self, data: Optional[ProblemData], device: int = 0):
         lib = _lib.load()
         self.lib = lib
         self.device = int(device)
@@ -309,6 +309,11 @@ class DeviceProblem:
         h = C.c_void_p()
         _check(lib.gdwd_ctx_create(self.device, C.byref(h)), None, "gdwd_ctx_create")
         self.ctx = h
+        self.n_global = None
+        if data is None:  # empty context (device-generated data)
+            self.n = self.d = 0
+            self.fro = None
+            return
         self.n, self.d = data.n, data.d
         z = data.z_tilde
         if z.is_dense:
@@ -418,7 +423,7 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
     dp = device_problem(data, device)
     t_up = time.perf_counter()
     lib = dp.lib
-    kind = config.backend.resolve(data.n, data.d)
+    kind = config.backend.resolve(dp.n_global or data.n, data.d)  # sharded: the global sample count
     eps_c = _eps_c(data, config)
     cfg = _lib.GdwdConfig(
         max_iter=int(config.max_iter), backend=_lib.BACKEND_CODE[kind.value], use_sgs=int(bool(config.use_sgs)),

@@ -171,5 +171,75 @@ def make_problem(cfg: SynthConfig, seed: int = 0):
     return scale_problem(x, y, None, cfg.C, cfg.q, tau=tau)
 
 
-__all__ = ["BLOCK", "CONFIGS", "SynthConfig", "dense_samples", "flip_labels", "make_problem",
-           "raw_data", "sparse_matrix", "true_labels"]
+class DeviceProblemData:
+    """ProblemData-compatible record whose Z~ exists only in HBM (configs that
+    do not fit host memory).  Fields as ProblemData (solver.py:60-71) minus
+    ``z_tilde``; ``y``/``e``/``weights`` are this rank's slices."""
+
+    def __init__(self, dp, y, e, weights, C, q, z_scale, d, n_global):
+        self.y, self.e, self.weights = y, e, weights
+        self.C, self.q, self.z_scale = float(C), float(q), float(z_scale)
+        self._d, self.n_global = int(d), int(n_global)
+        self.z_tilde = None
+        self._gdwd_device = dp
+
+    @property
+    def n(self) -> int:
+        return self.y.size
+
+    @property
+    def d(self) -> int:
+        return self._d
+
+    def download_samples(self) -> np.ndarray:
+        """Row-major [n, d] copy of the local Z~ (tests / proxies)."""
+        from . import _lib
+        from .solver import _check
+
+        out = np.empty((self.n, self.d))
+        dp = self._gdwd_device
+        _check(dp.lib.gdwd_download_dense(dp.ctx, _lib.ptr(out)), dp.ctx, "download")
+        return out
+
+
+def make_device_problem(cfg: SynthConfig, seed: int = 0, device: int = 0, rank: int = 0, nranks: int = 1,
+                        allreduce=None, comm=None) -> DeviceProblemData:
+    """Generate a two-Gaussian config directly in HBM (counter-based stream,
+    shard-consistent), scale it like scale_problem and register it for
+    sgs_admm_solve.  With nranks > 1 this rank holds samples
+    [n*rank/nranks, n*(rank+1)/nranks); ``allreduce`` sums the Frobenius norm
+    across ranks and ``comm`` (parallel.*Communicator) shards the solve."""
+    import ctypes as C
+
+    from . import _lib
+    from .solver import DeviceProblem, _check, compute_weights
+
+    if cfg.kind != "gauss":
+        raise ValueError("device generation covers the two-Gaussian configs")
+    n = cfg.n
+    lo, hi = n * rank // nranks, n * (rank + 1) // nranks
+    dp = DeviceProblem(None, device)
+    lib = dp.lib
+    _check(lib.gdwd_generate_dense(dp.ctx, 0, int(seed) * 1000003 + 17, cfg.d, hi - lo, lo, cfg.signal_k,
+                                   float(cfg.shift)), dp.ctx, "generate")
+    dp.n, dp.d = hi - lo, cfg.d
+    fro2 = C.c_double()
+    _check(lib.gdwd_frobenius_sq(dp.ctx, C.byref(fro2)), dp.ctx, "frobenius")
+    f2 = fro2.value if allreduce is None else float(allreduce(np.array([fro2.value]))[0])
+    z_scale = math.sqrt(math.sqrt(f2))  # sqrt(||X||_F)  (solver.py:265-268)
+    y_all = flip_labels(true_labels(n), cfg.flip, seed)
+    tau = compute_weights(y_all, cfg.q)
+    y = np.ascontiguousarray(y_all[lo:hi])
+    w = np.ascontiguousarray((tau ** cfg.q)[lo:hi])
+    e = np.ones(hi - lo)
+    _check(lib.gdwd_scale_dense(dp.ctx, _lib.ptr(y), z_scale), dp.ctx, "scale")
+    _check(lib.gdwd_set_problem(dp.ctx, _lib.ptr(y), _lib.ptr(e), _lib.ptr(w), float(cfg.C), float(cfg.q),
+                                z_scale), dp.ctx, "set_problem")
+    out = DeviceProblemData(dp, y, e, w, cfg.C, cfg.q, z_scale, cfg.d, n)
+    if comm is not None:
+        comm.attach(dp, n)
+    return out
+
+
+__all__ = ["BLOCK", "CONFIGS", "DeviceProblemData", "SynthConfig", "dense_samples", "flip_labels",
+           "make_device_problem", "make_problem", "raw_data", "sparse_matrix", "true_labels"]
