@@ -159,6 +159,10 @@ int gdwd_time_iterations(gdwd_ctx* ctx, int32_t count, double* ms, int32_t* iter
 int gdwd_set_profile(gdwd_ctx* ctx, int32_t enable);
 int gdwd_get_profile(gdwd_ctx* ctx, char* buf, int64_t buflen, int64_t* launches);
 int gdwd_reset_counters(gdwd_ctx* ctx);
+/* Start vector of the Lanczos run that builds the proximal backend when
+ * PSQMR exceeds psqmr_switch_steps (lanczos.py:85: default_rng(seed)
+ * .standard_normal(d), normalised by the library). */
+int gdwd_set_lanczos_start(gdwd_ctx* ctx, const double* v, int64_t d);
 /* End-of-iteration iterates (SolverState, solver.py:127-140); any pointer may
  * be NULL.  n-vectors: r, xi, alpha, ztw; d-vectors: w, u, rho. */
 int gdwd_get_state(gdwd_ctx* ctx, double* r, double* xi, double* alpha, double* w, double* u, double* rho,

@@ -28,7 +28,7 @@ SYMBOLS = [
     "gdwd_solve_begin", "gdwd_solve_iterate", "gdwd_solve_end", "gdwd_time_iterations", "gdwd_set_profile",
     "gdwd_get_profile", "gdwd_reset_counters", "gdwd_frobenius_sq", "gdwd_comm_unique_id",
     "gdwd_comm_init_nccl", "gdwd_comm_init_host", "gdwd_generate_dense", "gdwd_scale_dense",
-    "gdwd_download_dense",
+    "gdwd_download_dense", "gdwd_set_lanczos_start",
 ]
 
 
@@ -91,6 +91,7 @@ def _declare(lib):
         "gdwd_generate_dense": (C.c_int, [vp, C.c_int32, C.c_uint64, _I64, _I64, _I64, _I64, C.c_double]),
         "gdwd_scale_dense": (C.c_int, [vp, _P, C.c_double]),
         "gdwd_download_dense": (C.c_int, [vp, _P]),
+        "gdwd_set_lanczos_start": (C.c_int, [vp, _P, _I64]),
         "gdwd_comm_init_nccl": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int64]),
         "gdwd_comm_init_host": (C.c_int, [vp, C.c_int32, C.c_int32, ALLREDUCE_CB, vp, C.c_int64]),
         "gdwd_get_state": (C.c_int, [vp, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -189,6 +189,11 @@ struct gdwd_ctx {
   int kind = 0, poll = 16, max_iter = 0, max_steps = 50, k_host = 0, psqmr_total = 0;
   bool use_sgs = true, stopped = false, gram = false, persistent = false;
   DevBuf pk_part, gkmat;
+  // proximal fallback (subsolvers.py:159-256)
+  bool prox = false;
+  int ell = 10;
+  std::vector<double> lz_start;  // Lanczos start vector (numpy default_rng(seed))
+  DevBuf pxbuf;                  // V [L][d] | coefs | sa, hp, tmp, zaz, wold
   // sample sharding: 0 none, 1 NCCL, 2 host all-reduce callback
   int comm_mode = 0, nranks = 1, rank = 0;
   int64_t n_global = 0;
@@ -601,7 +606,7 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   if (ctx->Zs) cudaFree(ctx->Zs);
   free_sparse(ctx);
   for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf})
     b->release();
   end_session(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1045,28 +1050,278 @@ static void enqueue_materialize(gdwd_ctx* ctx) {
   run_zmv(ctx, GsMaterialize1{D}, Z, "zmv_materialize");
 }
 
-static int body_iterative(gdwd_ctx* ctx, bool use_sgs, int max_steps, int* psqmr_steps) {
+// ---------------------------------------------------------------------------
+// proximal fallback
+// ---------------------------------------------------------------------------
+// eigen-decomposition of a symmetric tridiagonal (k <= ~100) by cyclic
+// Jacobi rotations; eigenvalues in `ev`, eigenvectors as columns of S (k x k)
+static void tridiag_eig(const std::vector<double>& a, const std::vector<double>& b, std::vector<double>& ev,
+                        std::vector<double>& S) {
+  const int k = (int)a.size();
+  std::vector<double> M((size_t)k * k, 0.0);
+  for (int i = 0; i < k; ++i) M[i * k + i] = a[i];
+  for (int i = 0; i + 1 < k; ++i) M[i * k + i + 1] = M[(i + 1) * k + i] = b[i];
+  S.assign((size_t)k * k, 0.0);
+  for (int i = 0; i < k; ++i) S[i * k + i] = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) {
+        tot += M[i * k + j] * M[i * k + j];
+        if (i != j) off += M[i * k + j] * M[i * k + j];
+      }
+    if (off <= 1e-32 * tot || off == 0.0) break;
+    for (int p = 0; p < k; ++p)
+      for (int q = p + 1; q < k; ++q) {
+        const double apq = M[p * k + q];
+        if (fabs(apq) < 1e-300) continue;
+        const double theta = (M[q * k + q] - M[p * k + p]) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+        for (int r = 0; r < k; ++r) {  // columns p, q
+          const double mrp = M[r * k + p], mrq = M[r * k + q];
+          M[r * k + p] = c * mrp - sn * mrq;
+          M[r * k + q] = sn * mrp + c * mrq;
+        }
+        for (int r = 0; r < k; ++r) {  // rows p, q
+          const double mpr = M[p * k + r], mqr = M[q * k + r];
+          M[p * k + r] = c * mpr - sn * mqr;
+          M[q * k + r] = sn * mpr + c * mqr;
+        }
+        for (int r = 0; r < k; ++r) {
+          const double srp = S[r * k + p], srq = S[r * k + q];
+          S[r * k + p] = c * srp - sn * srq;
+          S[r * k + q] = sn * srp + c * srq;
+        }
+      }
+  }
+  ev.resize(k);
+  for (int i = 0; i < k; ++i) ev[i] = M[i * k + i];
+}
+
+static double hdot(const double* a, const double* b, int64_t n) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+
+// lanczos_topk (lanczos.py:47-133) on v -> Z~(Z~^T v) with device applies,
+// then the ProximalFactor (subsolvers.py:204-240) uploaded to the device.
+static int build_prox(gdwd_ctx* ctx) {
+  Dev& D = ctx->D;
+  const int64_t d = ctx->d, n = ctx->n;
+  if (d < 2) return set_err(ctx, GDWD_ERR_VALUE, "proximal backend needs d >= 2");
+  const int k = (int)std::min<int64_t>(ctx->ell, d - 1);
+  if (k - 1 > PX_MAXL) return set_err(ctx, GDWD_ERR_UNSUPPORTED, "ell > 17 not supported by the proximal kernels");
+  const int cap = (int)std::min<int64_t>(d, std::max(10 * k, 100));
+  const double tol = 1e-12;
+  if ((int64_t)ctx->lz_start.size() != d) return set_err(ctx, GDWD_ERR_VALUE, "no Lanczos start vector");
+  MatView Z = zview(ctx);
+  DevBuf dv, dw, dt;
+  CK(dv.ensure(d));
+  CK(dw.ensure(d));
+  CK(dt.ensure(n));
+  auto apply = [&](const std::vector<double>& v, std::vector<double>& w) -> int {
+    CK(cudaMemcpyAsync(dv.p, v.data(), d * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+    run_zt(ctx, OpPlainZt{dv.p, dt.p}, Z, "ztmv_lanczos");
+    run_zmv(ctx, OpPlainZ{dt.p, nullptr, dw.p, nullptr}, Z, "zmv_lanczos");
+    CK(cudaMemcpyAsync(w.data(), dw.p, d * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return GDWD_OK;
+  };
+  std::vector<std::vector<double>> basis;
+  std::vector<double> al, be, v(ctx->lz_start), w(d), ev, Sm;
+  {
+    const double nv = sqrt(hdot(v.data(), v.data(), d));
+    for (auto& x : v) x /= nv;
+  }
+  double nest = 0.0;
+  std::vector<double> lam_best;
+  std::vector<std::vector<double>> vec_best;
+  bool ok = false;
+  uint64_t rs = 0x9E3779B97F4A7C15ull;
+  for (int it = 0; it < cap; ++it) {
+    RC(apply(v, w));
+    const double a = hdot(v.data(), w.data(), d);
+    for (int64_t j = 0; j < d; ++j) w[j] = w[j] - a * v[j];
+    if (!basis.empty() && !be.empty() && be.back() != 0.0)
+      for (int64_t j = 0; j < d; ++j) w[j] -= be.back() * basis.back()[j];
+    basis.push_back(v);
+    al.push_back(a);
+    for (int rep = 0; rep < 2; ++rep) {  // full reorthogonalisation, twice
+      std::vector<double> c(basis.size());
+      for (size_t m = 0; m < basis.size(); ++m) c[m] = hdot(basis[m].data(), w.data(), d);
+      for (int64_t j = 0; j < d; ++j) {
+        double s = 0.0;
+        for (size_t m = 0; m < basis.size(); ++m) s += basis[m][j] * c[m];
+        w[j] -= s;
+      }
+    }
+    const double bn = sqrt(hdot(w.data(), w.data(), d));
+    tridiag_eig(al, be, ev, Sm);
+    const int kk = (int)al.size();
+    double mx = 0.0;
+    for (double x : ev) mx = std::max(mx, fabs(x));
+    nest = std::max(nest, mx);
+    std::vector<int> order(kk);
+    for (int i = 0; i < kk; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int x, int y) { return ev[x] > ev[y]; });
+    const int top = std::min(k, kk);
+    bool conv = true;
+    lam_best.assign(top, 0.0);
+    vec_best.assign(top, std::vector<double>(d, 0.0));
+    for (int t = 0; t < top; ++t) {
+      const int c = order[t];
+      lam_best[t] = ev[c];
+      if (fabs(bn * Sm[(size_t)(kk - 1) * kk + c]) > tol * std::max(nest, 1e-300)) conv = false;
+      for (int m = 0; m < kk; ++m) {
+        const double sm = Sm[(size_t)m * kk + c];
+        for (int64_t j = 0; j < d; ++j) vec_best[t][j] += basis[m][j] * sm;
+      }
+    }
+    if (kk >= k && (conv || kk == d)) {
+      ok = true;
+      break;
+    }
+    if (bn <= std::max(nest, 1.0) * 1e-14) {
+      if (kk == d) {
+        ok = true;
+        break;
+      }
+      // invariant subspace: restart orthogonal to the basis (fresh direction)
+      for (int64_t j = 0; j < d; ++j) {
+        rs = rs * 6364136223846793005ull + 1442695040888963407ull;
+        v[j] = ((double)(rs >> 11) / 9007199254740992.0) - 0.5;
+      }
+      for (int rep = 0; rep < 2; ++rep)
+        for (auto& q : basis) {
+          const double c = hdot(q.data(), v.data(), d);
+          for (int64_t j = 0; j < d; ++j) v[j] -= c * q[j];
+        }
+      const double nv = sqrt(hdot(v.data(), v.data(), d));
+      for (auto& x : v) x /= nv;
+      be.push_back(0.0);
+    } else {
+      for (int64_t j = 0; j < d; ++j) v[j] = w[j] / bn;
+      be.push_back(bn);
+    }
+  }
+  if (!ok) return set_err(ctx, GDWD_ERR_LANCZOS, "no convergence to tol=1e-12 within " + std::to_string(cap) + " iterations");
+  // ProximalFactor: inv / fwd coefficients, V[:, :-1], Schur scalar
+  const double mu2 = D.mu2;
+  const int L = k - 1;
+  const double lamk = lam_best[k - 1];
+  const double base = 1.0 / (mu2 + lamk);
+  std::vector<double> cinv(PX_MAXL, 0.0), cfwd(PX_MAXL, 0.0);
+  for (int i = 0; i < L; ++i) {
+    cinv[i] = 1.0 / (mu2 + lam_best[i]) - base;
+    cfwd[i] = lam_best[i] - lamk;
+  }
+  std::vector<double> zy(d);
+  CK(cudaMemcpy(zy.data(), D.zy, d * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<double> iv(d);
+  {
+    std::vector<double> p(L);
+    for (int i = 0; i < L; ++i) p[i] = hdot(vec_best[i].data(), zy.data(), d);
+    for (int64_t j = 0; j < d; ++j) {
+      double s = 0.0;
+      for (int i = 0; i < L; ++i) s += vec_best[i][j] * (cinv[i] * p[i]);
+      iv[j] = base * zy[j] + s;
+    }
+  }
+  const double schur = ctx->yty - hdot(zy.data(), iv.data(), d);
+  if (!(schur > 1e-14)) return set_err(ctx, GDWD_ERR_SCHUR, "Schur scalar is not safely positive");
+  const size_t need = (size_t)PX_MAXL * d + 2 * PX_MAXL + 5 * (size_t)(d + 2);
+  CK(ctx->pxbuf.ensure(need));
+  double* px = ctx->pxbuf.p;
+  for (int i = 0; i < L; ++i)
+    CK(cudaMemcpy(px + (size_t)i * d, vec_best[i].data(), d * sizeof(double), cudaMemcpyHostToDevice));
+  double* cb = px + (size_t)PX_MAXL * d;
+  CK(cudaMemcpy(cb, cinv.data(), PX_MAXL * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(cb + PX_MAXL, cfwd.data(), PX_MAXL * sizeof(double), cudaMemcpyHostToDevice));
+  double* vb = cb + 2 * PX_MAXL;
+  D.pxV = px;
+  D.px_cinv = cb;
+  D.px_cfwd = cb + PX_MAXL;
+  D.px_sa = vb;
+  D.px_hp = vb + (d + 2);
+  D.px_tmp = vb + 2 * (d + 2);
+  D.px_zaz = vb + 3 * (d + 2);
+  D.px_base = base;
+  D.px_fwd0 = mu2 + lamk;
+  D.px_schur = schur;
+  D.px_L = L;
+  ctx->prox = true;
+  return GDWD_OK;
+}
+
+// anchor w kept across the Step-1c PSQMR call (a free (d+1)-slot of mvec)
+static double* px_wold(gdwd_ctx* ctx) { return ctx->mvec.p + 13 * (ctx->d + 2); }
+
+// solve_system in proximal mode (solver.py:484-491) -> out = [w; beta]
+static void prox_solve(gdwd_ctx* ctx, const double* hv, double* out, int pred, bool compute_sa, const double* aw,
+                       const double* aztw) {
   const Dev& D = ctx->D;
+  const int64_t d = ctx->d;
+  MatView Z = zview(ctx);
+  if (compute_sa) {
+    run_zmv(ctx, OpZtwStore{D, aztw, pred}, Z, "zmv_prox_anchor");
+    run_vm(ctx, OpPxDot{D, aw, pred}, d, "vmap_prox");
+    run_vm(ctx, OpPxShift{D, aw, hv, pred}, d, "vmap_prox");
+  } else {
+    run_vm(ctx, OpPxShifted{D, hv, pred}, d, "vmap_prox");
+  }
+  run_vm(ctx, OpPxDot{D, D.px_hp, pred}, d, "vmap_prox");
+  run_vm(ctx, OpPxBeta{D, hv, pred}, d, "vmap_prox");
+  run_vm(ctx, OpPxRhs2{D, pred}, d, "vmap_prox");
+  run_vm(ctx, OpPxDot{D, D.px_tmp, pred}, d, "vmap_prox");
+  run_vm(ctx, OpPxW{D, out, pred}, d, "vmap_prox");
+}
+
+static int body_iterative(gdwd_ctx* ctx, bool use_sgs, int max_steps, int* psqmr_steps) {
+  Dev& D = ctx->D;
   MatView Z = zview(ctx);
   run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
-  int steps = 0, conv = 1, ran = 0, rc;
+  int steps = 0, conv = 1, ran = 0;
   *psqmr_steps = 0;
-  rc = psqmr_solve(ctx, D.h, D.x, D.xb, 0, 1.0, max_steps, &steps, &conv, &ran);
-  if (rc) return rc;
-  if (ctx->Sh->stopped) return GDWD_OK;
-  *psqmr_steps += steps;
-  if (ran && !conv)
-    return set_err(ctx, GDWD_ERR_UNSUPPORTED,
-                   "PSQMR exceeded psqmr_switch_steps: proximal backend switch not built in this version");
+  bool sa_ready = false;  // shift anchor of this iteration computed
+  if (!ctx->prox) {
+    RC(psqmr_solve(ctx, D.h, D.x, D.xb, 0, 1.0, max_steps, &steps, &conv, &ran));
+    if (ctx->Sh->stopped) return GDWD_OK;
+    *psqmr_steps += steps;
+    if (ran && !conv) {  // solver.py:479-483: permanent switch to the proximal backend
+      RC(build_prox(ctx));
+      prox_solve(ctx, D.h, D.xb, 0, true, D.x, D.ztw);
+      sa_ready = true;
+    }
+  } else {
+    prox_solve(ctx, D.h, D.xb, 0, true, D.x, D.ztw);
+    sa_ready = true;
+  }
   run_zt(ctx, OpZtNewton{D}, Z, "ztmv_newton");
-  if (use_sgs) run_zmv(ctx, OpDrZtwb{D}, Z, "zmv_dr_ztwb");
-  else run_vm(ctx, OpSetReuse{D}, 1, "vmap_set_reuse");
-  rc = psqmr_solve(ctx, D.h2, D.xb, D.x, 1, 5.0, max_steps, &steps, &conv, &ran);
-  if (rc) return rc;
-  *psqmr_steps += ran ? steps : 0;
-  if (ran && !conv)
-    return set_err(ctx, GDWD_ERR_UNSUPPORTED,
-                   "PSQMR exceeded psqmr_switch_steps: proximal backend switch not built in this version");
+  if (use_sgs) {
+    if (ctx->prox) {
+      run_zmv(ctx, OpPxH2{D}, Z, "zmv_prox_h2");
+      run_vm(ctx, OpPxDot{D, D.xb, 0}, ctx->d, "vmap_prox");
+      run_vm(ctx, OpPxResid{D}, ctx->d, "vmap_prox_resid");
+    } else {
+      run_zmv(ctx, OpDrZtwb{D}, Z, "zmv_dr_ztwb");
+    }
+  } else {
+    run_vm(ctx, OpSetReuse{D}, 1, "vmap_set_reuse");
+  }
+  if (ctx->prox) {
+    prox_solve(ctx, D.h2, D.x, 1, !sa_ready, D.x, D.ztw);
+  } else {
+    // keep the anchor w of this iteration in case PSQMR gives up below
+    run_vm(ctx, OpCopy{D, D.x, px_wold(ctx)}, D.m, "vmap_copy_x");
+    RC(psqmr_solve(ctx, D.h2, D.xb, D.x, 1, 5.0, max_steps, &steps, &conv, &ran));
+    *psqmr_steps += ran ? steps : 0;
+    if (ran && !conv) {
+      RC(build_prox(ctx));
+      prox_solve(ctx, D.h2, D.x, 1, true, px_wold(ctx), D.ztw);
+    }
+  }
   enqueue_tail(ctx);
   CK(cudaGetLastError());
   return GDWD_OK;
@@ -1204,6 +1459,8 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   ctx->ps_per_iter.assign(max_iter + 1, 0.0);
   ctx->kind = kind;
   ctx->gram = gram;
+  ctx->prox = false;  // every solve starts on PSQMR (solver.py:422)
+  ctx->ell = cfg->ell;
   ctx->persistent = gram && cfg->persistent && !ctx->prof && !sharded(ctx);
   ctx->use_sgs = cfg->use_sgs != 0;
   ctx->poll = std::max(1, cfg->poll_every);
@@ -1374,6 +1631,12 @@ extern "C" int gdwd_solve(gdwd_ctx* ctx, const gdwd_config* cfg, const double* s
   RC(gdwd_solve_begin(ctx, cfg, sched, sched_len));
   RC(gdwd_solve_iterate(ctx, cfg->max_iter, cb, user, nullptr, nullptr));
   return gdwd_solve_end(ctx, out);
+}
+
+extern "C" int gdwd_set_lanczos_start(gdwd_ctx* ctx, const double* v, int64_t d) {
+  if (!ctx || !v || d != ctx->d) return set_err(ctx, GDWD_ERR_VALUE, "start vector must have length d");
+  ctx->lz_start.assign(v, v + d);
+  return GDWD_OK;
 }
 
 extern "C" int gdwd_frobenius_sq(gdwd_ctx* ctx, double* out) {

@@ -31,7 +31,11 @@ struct Scal {
   double ps_tau, ps_rho, ps_theta, ps_alpha, ps_thnew, ps_cA, ps_cB, ps_rhonew, ps_resn;
   double ys;          // SMW: 1 + ybar^T J^{-1} ybar - 1
   double ytzw;        // Gram space: y . ztw_bar (= zy . w_bar)
+  double pv[16];      // proximal: V^T v of the last projection
+  double px_beta;     // proximal: beta of the current solve
 };
+
+constexpr int PX_MAXL = 16;  // ell - 1 <= 16 eigenvectors in the proximal operator
 
 struct Dev {
   int64_t n, d, m;  // m = d + 1
@@ -46,6 +50,13 @@ struct Dev {
   // Gram-space SMW2: n-coefficient temporaries and the d-space outputs
   double *cres, *cdiff;
   double *wd, *ud, *rhod;
+  // proximal backend (subsolvers.py:159-256): V = top-(ell-1) eigenvectors of
+  // Z~ Z~^T, eigenvector-major [L][d]; coefficient vectors for inv / fwd
+  const double* pxV;
+  const double *px_cinv, *px_cfwd;  // 1/(mu^2+lam_i) - base, lam_i - lam_ell
+  double px_base, px_fwd0, px_schur;  // 1/(mu^2+lam_ell), mu^2+lam_ell, Schur scalar
+  int px_L;
+  double *px_sa, *px_hp, *px_tmp, *px_zaz;  // d-vectors
   const double *eps_tab, *tol_tab, *sched;
   double* hist;
   Scal* S;
@@ -202,6 +213,17 @@ struct OpCopyIfReuse {
   const double* src;
   double* dst;
   GDWD_DEV bool skip() const { return D.S->stopped || !D.S->reuse; }
+  GDWD_DEV void elem(int64_t i, double (&)[NR]) const { dst[i] = src[i]; }
+  GDWD_DEV void fin(const double (&)[NR]) const {}
+};
+
+struct OpCopy {  // dst = src
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = false;
+  Dev D;
+  const double* src;
+  double* dst;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
   GDWD_DEV void elem(int64_t i, double (&)[NR]) const { dst[i] = src[i]; }
   GDWD_DEV void fin(const double (&)[NR]) const {}
 };
@@ -773,6 +795,163 @@ struct OpPsV2 {  // d, x, Ad, res updates; ||res||; q = u + beta q
     S->ps_theta = S->ps_thnew;
     if (S->ps_iters >= max_steps) S->ps_active = 0;
   }
+};
+
+
+// ---------------------------------------------------------------------------
+// Proximal backend (subsolvers.py:169-256).  inv(v) = base v + V (c_inv .* V^T v)
+// and fwd(v) = (mu^2 + lam_ell) v + V (c_fwd .* V^T v) over the top-(ell-1)
+// eigenvectors; d-space, replicated across shards.
+// ---------------------------------------------------------------------------
+struct OpPxDot {  // pv = V^T src
+  static constexpr int NR = PX_MAXL;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  const double* src;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void elem(int64_t j, double (&a)[NR]) const {
+    const double v = src[j];
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+      if (i < D.px_L) a[i] += D.pxV[(int64_t)i * D.d + j] * v;
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) D.S->pv[i] = s[i];
+  }
+};
+
+GDWD_DEV double px_lowrank(const Dev& D, int64_t j, const double* coef) {
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < PX_MAXL; ++i)
+    if (i < D.px_L) acc += D.pxV[(int64_t)i * D.d + j] * (coef[i] * D.S->pv[i]);
+  return acc;
+}
+
+// sa = fwd(w) - mu^2 w - Z ztw (solver.py:484-488); hp = h_top + sa
+struct OpPxShift {
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = false;
+  Dev D;
+  const double* aw;
+  const double* hv;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void elem(int64_t j, double (&)[NR]) const {
+    const double fw = D.px_fwd0 * aw[j] + px_lowrank(D, j, D.px_cfwd);
+    const double sa = (fw - D.mu2 * aw[j]) - D.px_zaz[j];
+    D.px_sa[j] = sa;
+    D.px_hp[j] = hv[j] + sa;
+  }
+  GDWD_DEV void fin(const double (&)[NR]) const {}
+};
+
+// hp = h_top + sa with a stored sa (second solve of an iteration)
+struct OpPxShifted {
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = false;
+  Dev D;
+  const double* hv;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void elem(int64_t j, double (&)[NR]) const { D.px_hp[j] = hv[j] + D.px_sa[j]; }
+  GDWD_DEV void fin(const double (&)[NR]) const {}
+};
+
+// beta = (h_bot - zy . inv(hp)) / schur  (solver_proximal first half)
+struct OpPxBeta {
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  const double* hv;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void elem(int64_t j, double (&a)[NR]) const {
+    const double iv = D.px_base * D.px_hp[j] + px_lowrank(D, j, D.px_cinv);
+    a[0] += D.zy[j] * iv;
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const {
+    double beta = (hv[D.bot] - s[0]);
+    beta /= D.px_schur;
+    D.S->px_beta = beta;
+  }
+};
+
+// tmp = hp - zy beta
+struct OpPxRhs2 {
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = false;
+  Dev D;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void elem(int64_t j, double (&)[NR]) const { D.px_tmp[j] = D.px_hp[j] - D.zy[j] * D.S->px_beta; }
+  GDWD_DEV void fin(const double (&)[NR]) const {}
+};
+
+// out = [inv(tmp) ; beta]
+struct OpPxW {
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  double* out;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void elem(int64_t j, double (&)[NR]) const {
+    out[j] = D.px_base * D.px_tmp[j] + px_lowrank(D, j, D.px_cinv);
+  }
+  GDWD_DEV void fin(const double (&)[NR]) const { out[D.bot] = D.S->px_beta; }
+};
+
+// sGS residual in proximal mode (solver.py:510-520): h2 = h + Z dr (epilogue
+// of a Z dr pass), ax = fwd(w_bar) + zy beta_bar, res = h2 + sa - ax
+struct OpPxH2 {
+  static constexpr int R = 1, NN = 1, ND = 1;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void input(int64_t i, double (&t)[R], double (&na)[NN]) const {
+    t[0] = D.dr[i];
+    na[0] += D.y[i] * D.dr[i];
+  }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&)[ND]) const { D.h2[j] = D.h[j] + v[0]; }
+  GDWD_DEV void fin(const double (&ns)[NN], const double (&)[ND]) const { D.h2[D.bot] = D.h[D.bot] + ns[0]; }
+};
+
+struct OpPxResid {
+  static constexpr int NR = 2;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void elem(int64_t j, double (&a)[NR]) const {
+    const double bb = D.xb[D.bot];
+    const double fw = D.px_fwd0 * D.xb[j] + px_lowrank(D, j, D.px_cfwd);
+    const double ax = fw + D.zy[j] * bb;
+    const double rj = (D.h2[j] + D.px_sa[j]) - ax;
+    a[0] += rj * rj;
+    a[1] += D.zy[j] * D.xb[j];
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const {
+    Scal* S = D.S;
+    const double bb = D.xb[D.bot];
+    const double rb = D.h2[D.bot] - (s[1] + D.yty * bb);
+    const double rr = hypot(sqrt(s[0]), rb);
+    const int reuse = rr <= 5.0 * D.eps_tab[S->k];
+    S->reuse = reuse;
+    if (!reuse) S->double_count += 1;
+    D.hist[(int64_t)S->k * HIST_W + H_REUSE] = reuse ? 1.0 : 0.0;
+  }
+};
+
+struct OpZtwStore {  // zaz = Z ztw (the anchor's Z Z^T w term)
+  static constexpr int R = 1, NN = 1, ND = 1;
+  Dev D;
+  const double* src;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void input(int64_t i, double (&t)[R], double (&)[NN]) const { t[0] = src[i]; }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&)[ND]) const { D.px_zaz[j] = v[0]; }
+  GDWD_DEV void fin(const double (&)[NN], const double (&)[ND]) const {}
 };
 
 // ---------------------------------------------------------------------------

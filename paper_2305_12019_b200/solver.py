@@ -435,6 +435,10 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
         sigma0=float("nan") if config.sigma0 is None else float(config.sigma0), epsilon_c=eps_c,
         mu=float(config.mu))
     sched = None if sigma_schedule is None else _lib.f64(sigma_schedule)
+    if kind is SolverKind.ITERATIVE:
+        # start vector of the proximal fallback's Lanczos run (lanczos.py:85)
+        v0 = np.random.default_rng(config.seed).standard_normal(data.d)
+        _check(lib.gdwd_set_lanczos_start(dp.ctx, _lib.ptr(v0), data.d), dp.ctx, "lanczos start")
     err: list = []
 
     def _cb(user, it, resid_p, sigma, beta):

@@ -26,7 +26,8 @@ def load_kat():
 
 
 TRAJ_CASES = ["tiny_direct", "tiny_smw2", "tiny_iter", "tiny_iter_c4gen", "tiny_direct_q2", "smw2_natural",
-              "iter_natural", "direct_q4", "tiny_sparse", "sparse_natural", "sparse_direct"]
+              "iter_natural", "direct_q4", "tiny_sparse", "sparse_natural", "sparse_direct", "prox_tiny",
+              "prox_tiny_q2"]
 
 
 def problem_for(tr):

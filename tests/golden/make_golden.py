@@ -56,6 +56,10 @@ CASES = [
     ("tiny_sparse", "c4", 3000, 2000, "iterative", 40, True),
     ("sparse_natural", "c4", 8000, 30000, "auto", 25, False),
     ("sparse_direct", "c4", 1500, 4000, "auto", 40, False),
+    # proximal fallback (subsolvers.py:159-256): PSQMR budget 2 steps forces the switch
+    ("prox_tiny", "c1", 70, 50, "iterative", 40, True, 0, 2),
+    ("prox_tiny_q2", "c3", 90, 300, "iterative", 40, True, 0, 2),
+    ("prox_lanczos_fail", "c1", 6000, 1500, "auto", 12, False, 0, 3),
 ]
 SAMPLE = 64  # sampled coordinates per vector for the non-full cases
 
@@ -71,11 +75,12 @@ def to_ref(prob):
                             z_scale=prob.z_scale)
 
 
-def run_case(name, cfgname, d, n, backend, max_iter, full, seed=0):
+def run_case(name, cfgname, d, n, backend, max_iter, full, seed=0, switch=50):
     cfg = synth.CONFIGS[cfgname].scaled(d=d, n=n)
     prob = synth.make_problem(cfg, seed)
     rp = to_ref(prob)
-    conf = gdwd.SolverConfig(q=prob.q, max_iter=max_iter, backend=gdwd.Backend(backend))
+    conf = gdwd.SolverConfig(q=prob.q, max_iter=max_iter, backend=gdwd.Backend(backend),
+                             psqmr_switch_steps=switch)
     rows, vecs = [], {k: [] for k in ("w", "u", "rho", "r", "xi", "alpha")}
     rng = np.random.default_rng(1234)
     idx_d = np.sort(rng.choice(d, min(SAMPLE, d), replace=False))
@@ -92,13 +97,22 @@ def run_case(name, cfgname, d, n, backend, max_iter, full, seed=0):
             vecs[k].append(v)
 
     t0 = time.perf_counter()
-    res = gdwd.sgs_admm_solve(rp, conf, callback=cb)
+    try:
+        res = gdwd.sgs_admm_solve(rp, conf, callback=cb)
+    except Exception as exc:  # the reference's own error behaviour is part of the fixture
+        np.savez_compressed(OUT / f"traj_{name}.npz", hist=np.array(rows), idx_d=idx_d, idx_n=idx_n,
+                            error=type(exc).__name__, iterations_before_error=len(rows),
+                            z_sha=z_checksum(prob.z_tilde.values), d=d, n=n, seed=seed, cfg=cfgname,
+                            max_iter=max_iter, full=int(full), switch=switch,
+                            **{"it_" + k: np.array(v) for k, v in vecs.items()})
+        print(f"{name}: reference raised {type(exc).__name__} after {len(rows)} iterations", flush=True)
+        return
     dt = time.perf_counter() - t0
     out = dict(hist=np.array(rows), idx_d=idx_d, idx_n=idx_n, iterations=res.iterations,
                converged=int(res.converged), double_count=res.double_count, psqmr_total=res.psqmr_total,
                backend=res.backend_used.value, final_w=res.final_state.w, final_beta=res.final_state.beta,
                z_sha=z_checksum(prob.z_tilde.values), d=d, n=n, seed=seed, cfg=cfgname, max_iter=max_iter,
-               full=int(full), train_error=res.train_error_pct)
+               full=int(full), train_error=res.train_error_pct, switch=switch)
     for k, v in vecs.items():
         out["it_" + k] = np.array(v)
     np.savez_compressed(OUT / f"traj_{name}.npz", **out)

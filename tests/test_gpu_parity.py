@@ -16,7 +16,8 @@ pytestmark = pytest.mark.gpu
 
 TOL20 = 1e-9
 BACKEND = {"tiny_direct": "direct", "tiny_smw2": "smw2", "tiny_iter": "iterative", "tiny_iter_c4gen": "iterative",
-           "tiny_direct_q2": "direct", "tiny_sparse": "iterative"}
+           "tiny_direct_q2": "direct", "tiny_sparse": "iterative",
+           "prox_tiny": "iterative", "prox_tiny_q2": "iterative"}
 
 
 def run_traj(prob, cfg, full, idx_d=None, idx_n=None, **kw):
@@ -49,8 +50,8 @@ def run_traj(prob, cfg, full, idx_d=None, idx_n=None, **kw):
 def test_trajectory_first20(case):
     tr = load_traj(case)
     prob = problem_for(tr)
-    cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]),
-                         backend=G.Backend(BACKEND.get(case, "auto")))
+    cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]), backend=G.Backend(BACKEND.get(case, "auto")),
+                         psqmr_switch_steps=int(tr["switch"]) if "switch" in tr else 50)
     out, h, vecs = run_traj(prob, cfg, bool(tr["full"]), tr["idx_d"], tr["idx_n"])
     assert out.backend_used.value == str(tr["backend"])
     k = min(20, len(tr["hist"]))
@@ -78,8 +79,8 @@ def test_full_run_counters(case):
     within rounding-induced noise; final w within 1e-6 (sigma replayed)."""
     tr = load_traj(case)
     prob = problem_for(tr)
-    cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]),
-                         backend=G.Backend(BACKEND.get(case, "auto")))
+    cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]), backend=G.Backend(BACKEND.get(case, "auto")),
+                         psqmr_switch_steps=int(tr["switch"]) if "switch" in tr else 50)
     out = G.sgs_admm_solve(prob, cfg, sigma_schedule=tr["hist"][:, 11])
     assert out.iterations == int(tr["iterations"])
     assert out.converged == bool(tr["converged"])
@@ -176,3 +177,11 @@ def test_persistent_smw2_matches_reference(case):
     # rounding; later eta_c3 cancels to ~1e-5 and reflects Newton stop noise
     for c in (2, 9):
         assert np.allclose(a.history[:20, c], b.history[:20, c], rtol=1e-7, atol=1e-12)
+
+
+def test_lanczos_failure_raises_like_reference():
+    tr = load_traj("prox_lanczos_fail")
+    prob = problem_for(tr)
+    cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]), psqmr_switch_steps=int(tr["switch"]))
+    with pytest.raises(G.LanczosConvergenceError):
+        G.sgs_admm_solve(prob, cfg)

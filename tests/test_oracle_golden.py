@@ -75,11 +75,12 @@ def test_oracle_matches_reference_trajectory(case):
             vecs[k].append(v)
 
     backend = "auto"
-    cfg = O.OracleConfig(max_iter=int(tr["max_iter"]), backend=backend)
-    if case.startswith("tiny_"):
+    cfg = O.OracleConfig(max_iter=int(tr["max_iter"]), backend=backend,
+                         psqmr_switch_steps=int(tr["switch"]) if "switch" in tr else 50)
+    if case.startswith(("tiny_", "prox_")):
         cfg.backend = {"tiny_direct": "direct", "tiny_smw2": "smw2", "tiny_iter": "iterative",
                        "tiny_iter_c4gen": "iterative", "tiny_direct_q2": "direct",
-                       "tiny_sparse": "iterative"}[case]
+                       "tiny_sparse": "iterative", "prox_tiny": "iterative", "prox_tiny_q2": "iterative"}[case]
     out = O.solve(prob, cfg, operator="csc", callback=cb)
     assert out.backend == str(tr["backend"])
     assert out.iterations == int(tr["iterations"])
@@ -91,3 +92,13 @@ def test_oracle_matches_reference_trajectory(case):
     assert np.allclose(h[:, :13], tr["hist"][:, :13], rtol=1e-9, atol=1e-14)
     for k, v in vecs.items():
         assert relerr(np.array(v), tr["it_" + k]) < 1e-10, k
+
+
+def test_oracle_lanczos_failure_matches_reference():
+    """The reference raises LanczosConvergenceError when the proximal switch
+    needs eigenpairs Lanczos cannot deliver in 100 steps; so does the oracle."""
+    tr = load_traj("prox_lanczos_fail")
+    assert str(tr["error"]) == "LanczosConvergenceError"
+    prob = problem_for(tr)
+    with pytest.raises(O.LanczosFailed):
+        O.solve(prob, O.OracleConfig(max_iter=int(tr["max_iter"]), psqmr_switch_steps=int(tr["switch"])))
