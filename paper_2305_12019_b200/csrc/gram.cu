@@ -56,16 +56,27 @@ GDWD_DEV void load_slab(const Opnd& op, int64_t R, int64_t K, int64_t r0, int64_
   }
 }
 
+// Shared tiles: operands whose k stride is 1 (KFAST) are kept [r][k] so the
+// coalesced global rows store without bank conflicts; the others [k][r].
+// Both are padded so the DMMA fragment reads (lanes g = lane/4 along r,
+// t4 = lane%4 along k) are conflict-free.
+constexpr int KPAD = 4, RPAD = 8;
+constexpr int TILE_DOUBLES = (BM * (BK + KPAD) > BK * (BM + RPAD)) ? BM * (BK + KPAD) : BK * (BM + RPAD);
+
 template <bool KFAST>
-GDWD_DEV void store_slab(double (*s)[BM + APAD], const double (&reg)[4]) {
+GDWD_DEV void store_slab(double* s, const double (&reg)[4]) {
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     int idx = threadIdx.x + e * GT;
     int kk, rr;
-    if (KFAST) { kk = idx & (BK - 1); rr = idx >> 4; }
-    else       { rr = idx & 63;       kk = idx >> 6; }
-    s[kk][rr] = reg[e];
+    if (KFAST) { kk = idx & (BK - 1); rr = idx >> 4; s[rr * (BK + KPAD) + kk] = reg[e]; }
+    else       { rr = idx & 63;       kk = idx >> 6; s[kk * (BM + RPAD) + rr] = reg[e]; }
   }
+}
+
+template <bool KFAST>
+GDWD_DEV double frag(const double* s, int k, int r) {
+  return KFAST ? s[r * (BK + KPAD) + k] : s[k * (BM + RPAD) + r];
 }
 
 // C-tile partial: Cw[m][n] = sum_{k in slice} A(m,k) B(n,k)
@@ -76,8 +87,8 @@ __global__ void __launch_bounds__(GT) gemm_dmma_kernel(Opnd A, Opnd B, int64_t M
                                                        double beta, double* C, int64_t ldc) {
   const int bm = blockIdx.y, bn = blockIdx.x;
   if (upper_only && bn < bm) return;
-  __shared__ double As[2][BK][BM + APAD];
-  __shared__ double Bs[2][BK][BN + APAD];
+  __shared__ double As[2][TILE_DOUBLES];
+  __shared__ double Bs[2][TILE_DOUBLES];
   const int64_t m0 = (int64_t)bm * BM, n0 = (int64_t)bn * BN;
   const int64_t kb = (int64_t)blockIdx.z * kslice;
   const int64_t ke = (kb + kslice < K) ? kb + kslice : K;
@@ -110,9 +121,9 @@ __global__ void __launch_bounds__(GT) gemm_dmma_kernel(Opnd A, Opnd B, int64_t M
     for (int kk = 0; kk < BK; kk += 4) {
       double af[4], bf[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[buf][kk + t4][wm * 32 + i * 8 + g];
+      for (int i = 0; i < 4; ++i) af[i] = frag<AK>(As[buf], kk + t4, wm * 32 + i * 8 + g);
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = Bs[buf][kk + t4][wn * 16 + j * 8 + g];
+      for (int j = 0; j < 2; ++j) bf[j] = frag<BKF>(Bs[buf], kk + t4, wn * 16 + j * 8 + g);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
