@@ -1474,8 +1474,10 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   ctx->poll_pending = 0;
   if (ctx->persistent) {
     int nb = 0;
-    const size_t sm = (size_t)(2 * n + 4) * sizeof(double);
+    const size_t sm = (size_t)(3 * ((n + 3) / 2 * 2) + 6) * sizeof(double);
     CK(cudaFuncSetAttribute(gram_smw_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    // small shared carveout: the rest of the unified L1 caches this CTA's K rows
+    CK(cudaFuncSetAttribute(gram_smw_persistent, cudaFuncAttributePreferredSharedMemoryCarveout, 25));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gram_smw_persistent, PK_THREADS, sm));
     if (nb < 1) ctx->persistent = false;
     else CK(ctx->pk_part.ensure((size_t)2 * NUM_SMS * PK_NPART));
@@ -1507,16 +1509,61 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
   const int kend = std::min(ctx->max_iter, ctx->k_host + std::max(0, count));
   if (ctx->persistent && !cb && ctx->k_host < kend && !ctx->stopped) {
     // one cooperative launch runs all requested iterations (persist.cuh)
-    PKArgs pa{D, ctx->kmat.p, ctx->fac.p, ctx->gkmat.p, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host, getenv("GDWD_PK_DIAG") ? atoi(getenv("GDWD_PK_DIAG")) : 0,
-                ctx->use_sgs ? 1 : 0};
+    unsigned long long* ts = nullptr;
+    const bool timing = getenv("GDWD_PK_TIMING") != nullptr;
+    if (timing) {
+      CK(cudaMalloc(&ts, 256 * 16 * sizeof(unsigned long long)));
+      CK(cudaMemset(ts, 0, 256 * 16 * sizeof(unsigned long long)));
+    }
+    PKArgs pa{D, ctx->kmat.p, ctx->fac.p, ctx->gkmat.p, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host,
+              getenv("GDWD_PK_DIAG") ? atoi(getenv("GDWD_PK_DIAG")) : 0, ts, ctx->use_sgs ? 1 : 0};
     void* args[] = {&pa};
-    const size_t sm = (size_t)(2 * ctx->n + 4) * sizeof(double);
+    const size_t sm = (size_t)(3 * ((ctx->n + 3) / 2 * 2) + 6) * sizeof(double);
     {
       Launch L(ctx, "persistent_gram_smw2");
       CK(cudaLaunchCooperativeKernel((void*)gram_smw_persistent, dim3(NUM_SMS), dim3(PK_THREADS), args, sm, ctx->st));
     }
     CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
+    if (ts) {  // diagnostics: mean duration between consecutive phase points
+      std::vector<unsigned long long> h(256 * 16);
+      CK(cudaMemcpy(h.data(), ts, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      cudaFree(ts);
+      double acc[16] = {0};
+      int cnt[16] = {0};
+      for (int it = 1; it + 1 < 256; ++it) {
+        const unsigned long long* r = &h[it * 16];
+        if (!r[0] || !h[(it + 1) * 16]) break;
+        unsigned long long prev = r[0];
+        for (int pt = 1; pt <= 10; ++pt) {
+          if (!r[pt]) continue;
+          acc[pt] += (double)(r[pt] - prev);
+          cnt[pt]++;
+          prev = r[pt];
+        }
+        acc[11] += (double)(h[(it + 1) * 16] - prev);
+        cnt[11]++;
+      }
+      const char* names[] = {"", "A work", "A barrier", "C work", "C barrier", "D work", "D barrier",
+                             "E work", "E barrier", "H work", "H barrier", "H tail"};
+      for (int pt = 1; pt <= 11; ++pt)
+        if (cnt[pt]) fprintf(stderr, "[pk timing] %-10s %8.2f us (n=%d)\n", names[pt], acc[pt] / cnt[pt] / 1e3, cnt[pt]);
+      // sub-phase points: 14/15 inside C (after staging / after rows), 11-13 inside H
+      double sub[5] = {0};
+      int sc = 0;
+      for (int it = 1; it + 1 < 256; ++it) {
+        const unsigned long long* r = &h[it * 16];
+        if (!r[0] || !r[14] || !r[11]) break;
+        sub[0] += (double)(r[14] - r[2]);   // A fin + C staging
+        sub[1] += (double)(r[15] - r[14]);  // C rows + Newton
+        sub[2] += (double)(r[11] - (r[8] ? r[8] : r[6]));  // H staging
+        sub[3] += (double)(r[12] - r[11]);  // H rows
+        sub[4] += (double)(r[13] - r[12]);  // Step 3 + KKT terms
+        sc++;
+      }
+      const char* sn[] = {"A fin + C staging", "C rows+Newton", "H staging", "H rows", "H step3"};
+      for (int q = 0; q < 5 && sc; ++q) fprintf(stderr, "[pk timing]   %-18s %8.2f us\n", sn[q], sub[q] / sc / 1e3);
+    }
     ctx->k_host = ctx->Sh->stopped ? ctx->Sh->iters_done : kend;
     ctx->stopped = ctx->Sh->stopped != 0;
   }

@@ -18,16 +18,18 @@
 // to the global Scal record and writes the history rows.
 //
 // Phase map of iteration k (names from solver_ops.cuh / solver.py lines):
-//   A  [K alpha_{k-1} ; GK t1]        finish k-1 (obj_d, gap, stop), c_h, g   :496-499
-//   C  K c_xb                         x_bar, ztw_bar, Newton r+, dr           :501-504
-//   D  K c_res                        reuse test                               :506-524
-//   E,G (re-solve when not reused)    g' = GK t1', then K c_x -> ztw           :524-530
-//   H  K [c_g ; c_w - c_g]            ||g||, ||w - u||                         :535-537,328
-//   J  (elementwise)                  u, rho, r, xi, alpha updates, KKT sums   :533-545
+//   A  [K alpha_{k-1} ; GK t1]   u, rho of k-1 (needs ||g||_{k-1}, applied while
+//                                staging), c_h, g; finish k-1 (obj_d, gap,
+//                                stop test)                               :535-542,496-499
+//   C  K c_xb                    x_bar, ztw_bar, Newton r+, dr            :501-504
+//   D  K c_res                   reuse test                               :506-524
+//   E  GK t1'  (re-solve only)   g'                                       :524-529
+//   H  K [c_x ; c_g ; c_w - c_g] ztw (re-solve only), ||g||, ||w - u||;
+//                                Step 3 and the KKT sample terms          :530-545,311-340
 // with GK = G^{-1} K precomputed once (DMMA GEMM), so the SMW solve's
 // g = G^{-1}(K t1 + y t2) = GK t1 + t2 G^{-1} y needs no separate G^{-1}
 // phase (subsolvers.py:138-143, same math, different association).
-// 5 grid barriers per iteration (7 when Step 1c re-solves).
+// 4 grid barriers per iteration (5 when Step 1c re-solves).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -40,7 +42,7 @@ namespace cg = cooperative_groups;
 
 constexpr int PK_THREADS = 512;
 constexpr int PK_WARPS = PK_THREADS / 32;
-constexpr int PK_NPART = 10;  // widest cross-CTA sum (KKT terms)
+constexpr int PK_NPART = 14;  // widest cross-CTA sum (norms + KKT terms)
 
 struct PKArgs {
   Dev D;
@@ -51,13 +53,15 @@ struct PKArgs {
   double* part;        // [2][gridDim][PK_NPART]
   int count;           // iterations to run in this launch
   int diag;            // diagnostics: 1 = skip the GEMV rows (barrier/staging floor)
+  unsigned long long* tstamp;  // diagnostics: CTA-0 %globaltimer at phase boundaries (null: off)
   int use_sgs;
 };
 
 // replicated scalar state (shared memory)
 struct PKS {
-  int k, stopped, converged, reuse, double_count, iters_done, error;
+  int k, stopped, converged, reuse, double_count, iters_done, error, pending;
   double sigma, sigma_next, hbot, h2bot, beta_b, beta, coef, s2, gnorm, w2, wu2, ytzw, sdual;
+  double sigma_pend;  // sigma of the iteration whose u, rho update is pending
   double eta[11];
 };
 
@@ -102,20 +106,21 @@ GDWD_DEV void pk_row_dot(const double* const (&rows)[NV], int64_t n, const doubl
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int u = 0; u < U; ++u) z[v][u] = __ldcg(reinterpret_cast<const double2*>(rows[v] + j + u * 64));
+      for (int u = 0; u < U; ++u) z[v][u] = __ldg(reinterpret_cast<const double2*>(rows[v] + j + u * 64));
 #pragma unroll
     for (int u = 0; u < U; ++u) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        acc[v] += z[v][u].x * xs[v][j + u * 64];
-        acc[v] += z[v][u].y * xs[v][j + u * 64 + 1];
+        const double2 xv = *reinterpret_cast<const double2*>(xs[v] + j + u * 64);
+        acc[v] += z[v][u].x * xv.x;
+        acc[v] += z[v][u].y * xv.y;
       }
     }
   }
   for (; j < n; j += 64) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const double2 z = __ldcg(reinterpret_cast<const double2*>(rows[v] + j));
+      const double2 z = __ldg(reinterpret_cast<const double2*>(rows[v] + j));
       acc[v] += z.x * xs[v][j];
       if (j + 1 < n) acc[v] += z.y * xs[v][j + 1];
     }
@@ -125,13 +130,55 @@ GDWD_DEV void pk_row_dot(const double* const (&rows)[NV], int64_t n, const doubl
   for (int v = 0; v < NV; ++v) out[v] = acc[v];
 }
 
+// NV right-hand sides against one K row (row loaded once)
+template <int NV>
+GDWD_DEV void pk_row_dot_same(const double* row, int64_t n, const double* const (&xs)[NV], double (&out)[NV]) {
+  const int lane = threadIdx.x & 31;
+  double acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  int64_t j = 2 * lane;
+  for (; j + 15 * 64 < n; j += 16 * 64) {
+    double2 z[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) z[u] = __ldg(reinterpret_cast<const double2*>(row + j + u * 64));
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const double2 xv = *reinterpret_cast<const double2*>(xs[v] + j + u * 64);
+        acc[v] += z[u].x * xv.x;
+        acc[v] += z[u].y * xv.y;
+      }
+    }
+  }
+  for (; j < n; j += 64) {
+    const double2 z = __ldg(reinterpret_cast<const double2*>(row + j));
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      acc[v] += z.x * xs[v][j];
+      if (j + 1 < n) acc[v] += z.y * xs[v][j + 1];
+    }
+  }
+  warp_sum<NV>(acc);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) out[v] = acc[v];
+}
+
+GDWD_DEV unsigned long long pk_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
   cg::grid_group grid = cg::this_grid();
   const Dev& D = A.D;
   const int64_t n = D.n;
   extern __shared__ double pksm[];
   double* xa = pksm;           // staged vector 1 (n, padded to even)
-  double* xb = pksm + n + 2;   // staged vector 2
+  const int64_t ns = (n + 3) / 2 * 2;  // buffer stride: > n, even (16-byte aligned double2 reads)
+  double* xb = pksm + ns;      // staged vector 2 (phase H stages a third at 2 ns)
   __shared__ double red[PK_WARPS * PK_NPART];
   __shared__ PKS S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -142,12 +189,14 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
 
   if (threadIdx.x == 0) {
     const Scal* G = D.S;
-    S.k = G->k; S.stopped = G->stopped; S.converged = G->converged; S.reuse = G->reuse;
+    S.k = G->k; S.stopped = G->stopped; S.converged = G->converged; S.reuse = G->reuse; S.pending = 0;
+    S.gnorm = G->gnorm;
     S.double_count = G->double_count; S.iters_done = G->iters_done; S.error = G->error;
     S.sigma = G->sigma; S.sigma_next = G->sigma_next; S.sdual = G->sdual;
     for (int f = 0; f < 11; ++f) S.eta[f] = G->eta[f];
     xa[n] = 0.0;  // pad the odd tail so paired loads read zeros
     xb[n] = 0.0;
+    pksm[2 * ns + n] = 0.0;
   }
   __syncthreads();
 
@@ -170,17 +219,43 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
     return sy;
   };
 
+  // Step 2's u, rho update of the previous iteration (solver.py:535-542)
+  // needs ||g||, known only after the last barrier of that iteration: phase A
+  // applies it on the fly while staging (every CTA, all j) and the owners
+  // write it back in phase C, where no CTA reads u or rho.
+  auto uv_commit = [&](int64_t j, double& uj, double& rj) {
+    const double sp = S.sigma_pend, gn = S.gnorm;
+    const double wj = D.x[j];
+    const double gj = wj - D.rho[j] / (sp * mu);
+    uj = (gn <= D.zscale) ? gj : (D.zscale / gn) * gj;
+    rj = D.rho[j] - ((D.tau * sp) * mu) * (wj - uj);
+  };
+
   const int k_end = S.k + A.count;
+  const int k_begin = S.k;
+  // CTA-0 timestamps: slot (iteration, point); points: 0 top, then per phase
+  // 2p+1 = arrival at its barrier, 2p+2 = scalars ready after it
+#define PK_TS(pt)                                                                          \
+  do {                                                                                     \
+    if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && S.k - k_begin < 256)            \
+      A.tstamp[(size_t)(S.k - k_begin) * 16 + (pt)] = pk_now();                            \
+  } while (0)
   for (;;) {
     if (S.stopped || S.k >= k_end) break;
     const int k = S.k;
-    // ---------------- phase A: K alpha (finish k-1) and g = GK t1 ------------
+    PK_TS(0);
+    const bool pending = S.pending != 0;
+    // ---------------- phase A: u, rho (k-1); K alpha; g = GK t1 ---------------
     {
       const double sig = S.sigma_next;
       double yr = 0.0;
+      const double sp = S.sigma_pend, gn = S.gnorm;
       for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+        double uj, rj;
+        if (pending) uv_commit(j, uj, rj);
+        else { uj = D.u[j]; rj = D.rho[j]; }
         const double rhs = (D.xi[j] - D.r[j]) - D.al[j] / sig;
-        const double chj = (-rhs + mu2 * D.u[j]) + (mu / sig) * D.rho[j];
+        const double chj = (-rhs + mu2 * uj) + (mu / sig) * rj;
         xa[j] = D.al[j];
         xb[j] = chj / mu2;
         yr += D.y[j] * rhs;
@@ -210,10 +285,12 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       }
       double pv[2] = {qa, sy};
       pk_write_part<2>(A.part, slot, pv, red);
+      PK_TS(1);
       grid.sync();
       double tot[2];
       pk_cross_sum<2>(A.part, slot, tot, red);
       slot ^= 1;
+      PK_TS(2);
       if (threadIdx.x == 0) {
         S.coef = (tot[1] + (-S.s2)) / D.S->ys;
         if (blockIdx.x == 0) D.h[D.bot] = S.hbot;
@@ -256,7 +333,14 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
     const double eps = D.eps_tab[k];
     // ---------------- phase C: x_bar, K x_bar -> ztw_bar, Newton -------------
     {
-      // c_xb[j] = h_j/mu^2 - v_j/mu^2, v = g - coef jy  (GsX) ; y.v
+      if (pending) {  // owners write back the u, rho update applied in phase A
+        for (int64_t j = i0 + threadIdx.x; j < i1; j += PK_THREADS) {
+          double uj, rj;
+          uv_commit(j, uj, rj);
+          D.u[j] = uj;
+          D.rho[j] = rj;
+        }
+      }
       double yv = 0.0;
       const double coef = S.coef;
       for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
@@ -273,8 +357,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         const double p2 = v1[0] + ynorm * vn;
         S.beta_b = S.hbot / yty - p2 / yty;
         if (blockIdx.x == 0) D.xb[D.bot] = S.beta_b;
+        S.pending = 0;
       }
       __syncthreads();
+      PK_TS(14);
       const double bb = S.beta_b;
       const double tol = D.tol_tab[k];
       double ydr = 0.0;
@@ -295,12 +381,15 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
           ydr += D.y[i] * dri;
         }
       }
+      PK_TS(15);
       double pv[1] = {ydr};
       pk_write_part<1>(A.part, slot, pv, red);
+      PK_TS(3);
       grid.sync();
       double t[1];
       pk_cross_sum<1>(A.part, slot, t, red);
       slot ^= 1;
+      PK_TS(4);
       if (threadIdx.x == 0) S.h2bot = S.hbot + t[0];
       __syncthreads();
     }
@@ -330,10 +419,12 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       }
       double pv[1] = {q};
       pk_write_part<1>(A.part, slot, pv, red);
+      PK_TS(5);
       grid.sync();
       double t[1];
       pk_cross_sum<1>(A.part, slot, t, red);
       slot ^= 1;
+      PK_TS(6);
       if (threadIdx.x == 0) {
         const double rb = S.h2bot - (S.ytzw + yty * bb);
         const double rr = hypot(sqrt(t[0] > 0.0 ? t[0] : 0.0), rb);
@@ -347,151 +438,139 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       __syncthreads();
     }
     const bool reuse = S.reuse != 0;
-    // ---------------- phases E, G: re-solve with h2 ----------------------------
+    // ---------------- phase E: g' = GK (h2/mu^2) + t2' G^{-1} y ----------------
     if (!reuse) {
-      {  // E: g' = GK (h2/mu^2) + t2' G^{-1} y   (h2_j = h_j + dr_j)
-        const double t2 = S.h2bot / yty;
-        for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) xb[j] = (D.h[j] + D.dr[j]) / mu2;
-        if (threadIdx.x == 0) S.s2 = ynorm * t2;
-        __syncthreads();
-        const double sy = gk_rows(t2);
-        double pv[1] = {sy};
-        pk_write_part<1>(A.part, slot, pv, red);
-        grid.sync();
-        double t[1];
-        pk_cross_sum<1>(A.part, slot, t, red);
-        slot ^= 1;
-        if (threadIdx.x == 0) S.coef = (t[0] + (-S.s2)) / D.S->ys;
-        __syncthreads();
-      }
-      {  // G: x = h2/mu^2 - v/mu^2 ; ztw = K x
-        double yv = 0.0;
-        const double coef = S.coef;
-        for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+      const double t2 = S.h2bot / yty;
+      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) xb[j] = (D.h[j] + D.dr[j]) / mu2;
+      if (threadIdx.x == 0) S.s2 = ynorm * t2;
+      __syncthreads();
+      const double sy = gk_rows(t2);
+      double pv[1] = {sy};
+      pk_write_part<1>(A.part, slot, pv, red);
+      PK_TS(7);
+      grid.sync();
+      double t[1];
+      pk_cross_sum<1>(A.part, slot, t, red);
+      slot ^= 1;
+      PK_TS(8);
+      if (threadIdx.x == 0) S.coef = (t[0] + (-S.s2)) / D.S->ys;
+      __syncthreads();
+    }
+    // ---------------- phase H: [ztw ;] ||g||, ||w-u||, ||w||; Step 3, KKT --------
+    {
+      // w coefficients: x_bar when reused, else x = h2/mu^2 - v/mu^2 (GsX)
+      double* xw = pksm;              // staged w
+      double* xg = pksm + ns;      // staged g
+      double* xd = pksm + 2 * ns;  // staged w - g
+      double yv = 0.0;
+      const double coef = S.coef;
+      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+        double wj;
+        if (reuse) {
+          wj = D.xb[j];
+        } else {
           const double v = D.g[j] - coef * D.jy[j];
-          const double x = (D.h[j] + D.dr[j]) / mu2 - v / mu2;
-          xa[j] = x;
+          wj = (D.h[j] + D.dr[j]) / mu2 - v / mu2;
           yv += D.y[j] * v;
-          if (j >= i0 && j < i1) D.x[j] = x;
         }
-        double v1[1] = {yv};
-        block_sum<1>(v1, red);
-        if (threadIdx.x == 0) {
+        const double gj = wj - D.rho[j] / (sig * mu);
+        xw[j] = wj;
+        xg[j] = gj;
+        xd[j] = wj - gj;  // w - u when u = g (no projection)
+        if (j >= i0 && j < i1) D.x[j] = wj;
+      }
+      double v1[1] = {yv};
+      block_sum<1>(v1, red);
+      if (threadIdx.x == 0) {
+        if (reuse) {
+          S.beta = S.beta_b;
+        } else {
           const double vn = (-S.s2) - coef * (-1.0);
           const double p2 = v1[0] + ynorm * vn;
           S.beta = S.h2bot / yty - p2 / yty;
         }
-        __syncthreads();
-        for (int r = warp; r < nrows; r += PK_WARPS) {
-          const int64_t i = i0 + r;
-          const double* rows[1] = {A.K + i * A.ld};
-          const double* xs[1] = {xa};
-          double o[1];
-          pk_row_dot<1>(rows, n, xs, o);
-          if (lane == 0) D.ztw[i] = o[0];
-        }
-        grid.sync();
-      }
-    } else {
-      if (threadIdx.x == 0) S.beta = S.beta_b;
-      __syncthreads();
-    }
-    const double* xw = reuse ? D.xb : D.x;     // coefficients of w
-    const double* zw = reuse ? D.ztwb : D.ztw;  // Z^T w
-    // ---------------- phase H: ||g||, ||w - u||, ||w|| ---------------------------
-    {
-      double w2 = 0.0;
-      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
-        const double gj = xw[j] - D.rho[j] / (sig * mu);
-        xa[j] = gj;
-        xb[j] = xw[j] - gj;  // w - u when u = g (no projection)
-        w2 += xw[j] * zw[j];
-      }
-      double v1[1] = {w2};
-      block_sum<1>(v1, red);
-      if (threadIdx.x == 0) S.w2 = v1[0];
-      __syncthreads();
-      double q[3] = {0.0, 0.0, 0.0};
-      for (int r = warp; r < nrows; r += PK_WARPS) {
-        const int64_t i = i0 + r;
-        const double* rows[2] = {A.K + i * A.ld, A.K + i * A.ld};
-        const double* xs[2] = {xa, xb};
-        double o[2];
-        pk_row_dot<2>(rows, n, xs, o);
-        if (lane == 0) {
-          q[0] += xa[i] * o[0];  // g^T K g
-          q[1] += xb[i] * o[1];  // d^T K d
-          q[2] += xb[i] * o[0];  // d^T K g
-        }
-      }
-      pk_write_part<3>(A.part, slot, q, red);
-      grid.sync();
-      double t[3];
-      pk_cross_sum<3>(A.part, slot, t, red);
-      slot ^= 1;
-      if (threadIdx.x == 0) {
-        const double gg = t[0] > 0.0 ? t[0] : 0.0;
-        S.gnorm = sqrt(gg);
-        if (S.gnorm <= D.zscale) {
-          S.wu2 = t[1] > 0.0 ? t[1] : 0.0;
-        } else {
-          // w - u = d + (1 - s) g with s = z_scale / ||g||
-          const double om = 1.0 - D.zscale / S.gnorm;
-          const double v = t[1] + 2.0 * om * t[2] + om * om * gg;
-          S.wu2 = v > 0.0 ? v : 0.0;
-        }
+        if (blockIdx.x == 0) D.x[D.bot] = S.beta;
       }
       __syncthreads();
-    }
-    // ---------------- phase J: commit u, rho, w; Step 3; KKT terms -------------
-    {
-      const double gn = S.gnorm, bet = S.beta, C = D.C;
+      PK_TS(11);
       double acc[PK_NPART];
 #pragma unroll
       for (int f = 0; f < PK_NPART; ++f) acc[f] = 0.0;
-      for (int64_t i = i0 + threadIdx.x; i < i1; i += PK_THREADS) {
-        // Step 2 commit (solver.py:535-542) in coefficients
-        const double wi = xw[i];
-        const double gi = wi - D.rho[i] / (sig * mu);
-        const double ui = (gn <= D.zscale) ? gi : (D.zscale / gn) * gi;
-        D.u[i] = ui;
-        D.rho[i] = D.rho[i] - ((D.tau * sig) * mu) * (wi - ui);
+      for (int r = warp; r < nrows; r += PK_WARPS) {
+        const int64_t i = i0 + r;
+        const double* Ki = A.K + i * A.ld;
+        double o[3];
         if (reuse) {
-          D.x[i] = wi;
-          D.ztw[i] = zw[i];
+          const double* xs[2] = {xg, xd};
+          double o2[2];
+          pk_row_dot_same<2>(Ki, n, xs, o2);
+          o[0] = D.ztwb[i];
+          o[1] = o2[0];
+          o[2] = o2[1];
+        } else {
+          const double* xs[3] = {xw, xg, xd};
+          pk_row_dot_same<3>(Ki, n, xs, o);
         }
-        // Step 3 + KKT sample terms (OpStep3)
-        const double rr = D.rnew[i];
-        D.r[i] = rr;
-        const double yi = D.y[i], ei = D.e[i], zt = zw[i], ali = D.al[i];
-        const double xv = np_max0((((rr - zt) - yi * bet) + ali / sig) - (C / sig) * ei);
-        D.xi[i] = xv;
-        const double pg = ((zt + yi * bet) + xv) - rr;
-        const double an = ali - (D.tau * sig) * pg;
-        D.al[i] = an;
-        const double wl = D.wl[i];
-        const double s = (D.q * wl) / np_pow(rr, D.qp1);
-        const double d2 = an - s;
-        const double mn = np_min0(an);
-        const double mx = np_max0(an - C * ei);
-        acc[0] += yi * an;
-        acc[1] += xv * (C * ei - an);
-        acc[2] += d2 * d2;
-        acc[3] += pg * pg;
-        acc[4] += mn * mn;
-        acc[5] += mx * mx;
-        acc[6] += wl / np_pow(rr, D.q);
-        acc[7] += ei * xv;
-        acc[8] += np_pow(wl, D.e1) * np_pow(np_max0(an), D.e2);
-        acc[9] += (rr <= 0.0) ? 1.0 : 0.0;
+        if (lane == 0) {
+          D.ztw[i] = o[0];
+          acc[10] += xg[i] * o[1];  // g^T K g
+          acc[11] += xd[i] * o[2];  // d^T K d
+          acc[12] += xd[i] * o[1];  // d^T K g
+          acc[13] += xw[i] * o[0];  // w^T K w = ||w||^2
+        }
       }
-      if (blockIdx.x == 0 && threadIdx.x == 0) D.x[D.bot] = bet;
+      PK_TS(12);
+      __syncthreads();  // ztw of this CTA's rows is visible to its threads
+      {
+        // Step 3 + KKT sample terms (solver.py:533,538-541,311-333; OpStep3)
+        const double bet = S.beta, C = D.C;
+        for (int64_t i = i0 + threadIdx.x; i < i1; i += PK_THREADS) {
+          const double rr = D.rnew[i];
+          D.r[i] = rr;
+          const double yi = D.y[i], ei = D.e[i], zt = D.ztw[i], ali = D.al[i];
+          const double xv = np_max0((((rr - zt) - yi * bet) + ali / sig) - (C / sig) * ei);
+          D.xi[i] = xv;
+          const double pg = ((zt + yi * bet) + xv) - rr;
+          const double an = ali - (D.tau * sig) * pg;
+          D.al[i] = an;
+          const double wl = D.wl[i];
+          const double s = (D.q * wl) / np_pow(rr, D.qp1);
+          const double d2 = an - s;
+          const double mn = np_min0(an);
+          const double mx = np_max0(an - C * ei);
+          acc[0] += yi * an;
+          acc[1] += xv * (C * ei - an);
+          acc[2] += d2 * d2;
+          acc[3] += pg * pg;
+          acc[4] += mn * mn;
+          acc[5] += mx * mx;
+          acc[6] += wl / np_pow(rr, D.q);
+          acc[7] += ei * xv;
+          acc[8] += np_pow(wl, D.e1) * np_pow(np_max0(an), D.e2);
+          acc[9] += (rr <= 0.0) ? 1.0 : 0.0;
+        }
+      }
+      PK_TS(13);
       pk_write_part<PK_NPART>(A.part, slot, acc, red);
+      PK_TS(9);
       grid.sync();
       double t[PK_NPART];
       pk_cross_sum<PK_NPART>(A.part, slot, t, red);
       slot ^= 1;
+      PK_TS(10);
       if (threadIdx.x == 0) {
+        const double gg = t[10] > 0.0 ? t[10] : 0.0;
+        S.gnorm = sqrt(gg);
+        if (S.gnorm <= D.zscale) {
+          S.wu2 = t[11] > 0.0 ? t[11] : 0.0;
+        } else {  // w - u = d + (1 - s) g with s = z_scale / ||g||
+          const double om = 1.0 - D.zscale / S.gnorm;
+          const double v = t[11] + 2.0 * om * t[12] + om * om * gg;
+          S.wu2 = v > 0.0 ? v : 0.0;
+        }
+        S.w2 = t[13];
+        S.pending = 1;
+        S.sigma_pend = S.sigma;
         const double oc = D.one_c;
         if (t[9] > 0.0 && A.diag == 0) {
           S.error = 6;
@@ -512,7 +591,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
             double* hr = D.hist + (int64_t)k * HIST_W;
             for (int f = 0; f < 8; ++f) hr[f] = e[f];
             hr[H_OBJP] = e[9];
-            hr[H_BETA] = bet;
+            hr[H_BETA] = S.beta;
           }
           const double ep = fmax(fmax(e[3], e[4]), e[5]);
           const double ed = fmax(e[6], e[7]);
@@ -525,12 +604,25 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       __syncthreads();
     }
   }
+  // a pending u, rho update is committed before the launch returns
+  if (S.pending) {
+    for (int64_t j = i0 + threadIdx.x; j < i1; j += PK_THREADS) {
+      double uj, rj;
+      uv_commit(j, uj, rj);
+      D.u[j] = uj;
+      D.rho[j] = rj;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) S.pending = 0;
+    __syncthreads();
+  }
   // mirror the replicated scalars to the global record
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     Scal* G = D.S;
     G->k = S.k; G->stopped = S.stopped; G->converged = S.converged; G->reuse = S.reuse;
     G->double_count = S.double_count; G->iters_done = S.iters_done; G->error = S.error;
-    G->sigma = S.sigma; G->sigma_next = S.sigma_next; G->sdual = S.sdual;
+    G->sigma = S.sigma; G->sigma_next = S.sigma_next; G->sdual = S.sdual; G->gnorm = S.gnorm;
+    G->wu2 = S.wu2; G->w2 = S.w2;
     for (int f = 0; f < 11; ++f) G->eta[f] = S.eta[f];
   }
 }
