@@ -180,7 +180,7 @@ def run_b200(args, dist: Dist):
     device = dist.local
     cfg_syn = synth.CONFIGS[args.config]
     t0 = time.perf_counter()
-    on_device = 8.0 * cfg_syn.n * cfg_syn.d > 40e9  # config 5: generated in HBM
+    on_device = cfg_syn.kind != "sparse" and 8.0 * cfg_syn.n * cfg_syn.d > 40e9  # config 5: in HBM
     prob = (synth.make_device_problem(cfg_syn, args.seed, device) if on_device
             else synth.make_problem(cfg_syn, args.seed))
     gen_s = time.perf_counter() - t0

@@ -344,7 +344,7 @@ static void run_zt(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "zt
     Launch L(ctx, tag);
     if (!X.a) {
       SpView A{ctx->csc_ptr, ctx->csc_idx, ctx->csc_val, ctx->n, ctx->d};
-      sp_ztmv_kernel<Op, 8><<<sp_grid(ctx->n * 8, NUM_SMS * 8), SP_THREADS, 0, ctx->st>>>(op, A, sc);
+      sp_ztmv_kernel<Op, 8><<<sp_grid(ctx->n, NUM_SMS * 8), SP_THREADS, 0, ctx->st>>>(op, A, sc);
     } else {
       const int cw = zt_geom(X.rows, X.ld, NUM_SMS).cw;
       const size_t sm = (size_t)(cw + ZT_BATCH) * sizeof(double);

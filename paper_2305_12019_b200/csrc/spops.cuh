@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(SP_THREADS) sp_prep_kernel(Op op, int64_t n, d
     double tv[R];
     op.input(i, tv, nacc);
 #pragma unroll
-    for (int r = 0; r < R; ++r) tbuf[r * n + i] = tv[r];
+    for (int r = 0; r < R; ++r) tbuf[i * R + r] = tv[r];  // interleaved: one gather per nnz
   }
   block_sum<NN>(nacc, red);
   if (threadIdx.x == 0) {
@@ -70,11 +70,27 @@ __global__ void __launch_bounds__(SP_THREADS) sp_zmv_kernel(Op op, SpView A, con
     double acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
-    for (int64_t k = b + lane; k < e; k += 32) {
+    int64_t k = b + lane;
+    for (; k + 32 < e; k += 64) {  // two nnz per lane in flight
+      const double v0 = __ldg(A.val + k), v1 = __ldg(A.val + k + 32);
+      const int64_t c0 = __ldg(A.idx + k), c1 = __ldg(A.idx + k + 32);
+      double t0[R], t1[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        t0[r] = tbuf[c0 * R + r];
+        t1[r] = tbuf[c1 * R + r];
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc[r] += v0 * t0[r];
+        acc[r] += v1 * t1[r];
+      }
+    }
+    for (; k < e; k += 32) {
       const double v = __ldg(A.val + k);
       const int64_t c = __ldg(A.idx + k);
 #pragma unroll
-      for (int r = 0; r < R; ++r) acc[r] += v * tbuf[r * A.other + c];
+      for (int r = 0; r < R; ++r) acc[r] += v * tbuf[c * R + r];
     }
     warp_sum<R>(acc);
     if (lane == 0) {
@@ -105,31 +121,40 @@ __global__ void __launch_bounds__(SP_THREADS) sp_zmv_kernel(Op op, SpView A, con
   }
 }
 
-// dot_i = sum_j Z[j,i] w_j (CSC columns = samples); G lanes per sample.
+// dot_i = sum_j Z[j,i] w_j (CSC columns = samples).  A warp takes 32
+// consecutive samples: in 32/G rounds each group of G lanes reduces one
+// sample's dot, which is parked in the lane with that sample's index; then
+// all 32 lanes run the per-sample epilogue (Newton etc.) together.
 template <class Op, int G>
 __global__ void __launch_bounds__(SP_THREADS) sp_ztmv_kernel(Op op, SpView A, Scratch s) {
   constexpr int NN = Op::NN;
+  constexpr int GROUPS = 32 / G;
   if (op.skip()) return;
   __shared__ double red[(SP_THREADS / 32) * NN];
-  const int sub = threadIdx.x & (G - 1);
-  const int64_t grp = (blockIdx.x * (int64_t)SP_THREADS + threadIdx.x) / G;
-  const int64_t ngrp = ((int64_t)gridDim.x * SP_THREADS) / G;
+  const int lane = threadIdx.x & 31, sub = lane & (G - 1), grp = lane / G;
+  const int64_t warp = (blockIdx.x * (int64_t)SP_THREADS + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * SP_THREADS) >> 5;
   double nacc[NN];
 #pragma unroll
   for (int k = 0; k < NN; ++k) nacc[k] = 0.0;
-  // all lanes of a warp iterate the same number of times (shuffles)
-  const int64_t iters = (A.rows + ngrp - 1) / ngrp;
-  for (int64_t t = 0; t < iters; ++t) {
-    const int64_t i = grp + t * ngrp;
-    double acc = 0.0;
-    if (i < A.rows) {
-      const int64_t b = A.ptr[i], e = A.ptr[i + 1];
-      for (int64_t k = b + sub; k < e; k += G) acc += __ldg(A.val + k) * op.wval(__ldg(A.idx + k));
-    }
+  for (int64_t base = warp * 32; base < A.rows; base += nwarps * 32) {
+    double mine = 0.0;
 #pragma unroll
-    for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (sub == 0 && i < A.rows) op.row(i, acc, nacc);
+    for (int t = 0; t < G; ++t) {
+      const int64_t i = base + grp * G + t;  // sample handled by this group in round t
+      double acc = 0.0;
+      if (i < A.rows) {
+        const int64_t b = A.ptr[i], e = A.ptr[i + 1];
+        for (int64_t k = b + sub; k < e; k += G) acc += __ldg(A.val + k) * op.wval(__ldg(A.idx + k));
+      }
+#pragma unroll
+      for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (sub == t) mine = acc;  // lane grp*G + t owns sample base + grp*G + t
+    }
+    const int64_t i = base + lane;
+    if (i < A.rows) op.row(i, mine, nacc);
   }
+  (void)GROUPS;
   if (!Op::HAS_FIN) return;
   block_sum<NN>(nacc, red);
   if (threadIdx.x == 0) {

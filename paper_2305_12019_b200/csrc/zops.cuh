@@ -92,12 +92,12 @@ __global__ void __launch_bounds__(ZMV_THREADS) zmv_kernel(Op op, MatView X, ZmvG
     if (colok) {
       const double* p = X.a + c0 * X.ld + j0;
       int ii = 0;
-      for (; ii + 4 <= cn; ii += 4) {
-        double2 z[4];
+      for (; ii + 8 <= cn; ii += 8) {  // 8 rows x 16 B in flight per thread
+        double2 z[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) z[u] = ld_stream2(p + (int64_t)(ii + u) * X.ld);
+        for (int u = 0; u < 8; ++u) z[u] = ld_stream2(p + (int64_t)(ii + u) * X.ld);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const double t = op_sq<Op>::value ? 1.0 : ts[r][ii + u];
