@@ -1256,7 +1256,7 @@ static int build_prox(gdwd_ctx* ctx) {
 }
 
 // anchor w kept across the Step-1c PSQMR call (a free (d+1)-slot of mvec)
-static double* px_wold(gdwd_ctx* ctx) { return ctx->mvec.p + 13 * (ctx->d + 2); }
+static double* px_wold(gdwd_ctx* ctx) { return ctx->mvec.p + 13 * ((ctx->d + 3) / 2 * 2); }
 
 // solve_system in proximal mode (solver.py:484-491) -> out = [w; beta]
 static void prox_solve(gdwd_ctx* ctx, const double* hv, double* out, int pred, bool compute_sa, const double* aw,
@@ -1358,8 +1358,8 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   // ---- buffers ------------------------------------------------------------
   const int NV = 12, MV = 16;
   const bool gram = (kind == GDWD_BACKEND_SMW2) && cfg->smw_gram_space;
-  CK(ctx->nvec.ensure((size_t)NV * n));
-  CK(ctx->mvec.ensure((size_t)MV * (m + 1)));
+  CK(ctx->nvec.ensure((size_t)NV * ((n + 1) / 2 * 2)));
+  CK(ctx->mvec.ensure((size_t)MV * ((m + 2) / 2 * 2)));
   CK(ctx->tabs.ensure((size_t)2 * (max_iter + 2) + (size_t)std::max<int64_t>(sched_len, 1)));
   CK(ctx->histb.ensure((size_t)(max_iter + 1) * HIST_W));
   if (!ctx->poll_flag) CK(cudaMallocHost(&ctx->poll_flag, 2 * sizeof(int)));
@@ -1377,15 +1377,18 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   D.tol_feas = cfg->tol_feas; D.tol_cgap = cfg->tol_cgap; D.tol_cap = cfg->tol_cap;
   D.max_iter = max_iter;
   D.y = ctx->y.p; D.e = ctx->e.p; D.wl = ctx->wl.p;
+  // every vector slot starts 16-byte aligned (even strides): double2 loads
+  // and bulk (TMA) copies of whole vectors
+  const int64_t nst = (n + 1) / 2 * 2;
   double* nv = ctx->nvec.p;
-  D.r = nv; D.xi = nv + n; D.al = nv + 2 * n; D.ztw = nv + 3 * n; D.rnew = nv + 4 * n; D.dr = nv + 5 * n;
-  D.ztwb = nv + 6 * n; D.s1 = nv + 7 * n; D.g = nv + 8 * n; D.tq = nv + 9 * n;
+  D.r = nv; D.xi = nv + nst; D.al = nv + 2 * nst; D.ztw = nv + 3 * nst; D.rnew = nv + 4 * nst;
+  D.dr = nv + 5 * nst; D.ztwb = nv + 6 * nst; D.s1 = nv + 7 * nst; D.g = nv + 8 * nst; D.tq = nv + 9 * nst;
   double* mv = ctx->mvec.p;
-  const int64_t ms = m + 1;
+  const int64_t ms = (m + 2) / 2 * 2;
   D.u = mv; D.rho = mv + ms; D.h = mv + 2 * ms; D.h2 = mv + 3 * ms; D.xb = mv + 4 * ms; D.x = mv + 5 * ms;
   D.pr = mv + 6 * ms; D.pres = mv + 7 * ms; D.pq = mv + 8 * ms; D.pu = mv + 9 * ms; D.pd = mv + 10 * ms;
   D.pAd = mv + 11 * ms; D.pAq = mv + 12 * ms;
-  D.cres = nv + 10 * n; D.cdiff = nv + 11 * n;
+  D.cres = nv + 10 * nst; D.cdiff = nv + 11 * nst;
   D.bot = d;
   D.wd = D.x; D.ud = D.u; D.rhod = D.rho;
   if (gram) {
@@ -1394,11 +1397,13 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
     D.bot = n;
     D.wd = mv + 13 * ms; D.ud = mv + 14 * ms; D.rhod = mv + 15 * ms;
   }
-  // persistent per-problem vectors: [colsq (d) | zy (d) | jac (m) | jy (n)]
-  CK(ctx->colsq.ensure((size_t)d + (size_t)d + m + n + 8));
-  D.zy = ctx->colsq.p + d;
-  D.jac = ctx->colsq.p + 2 * d;
-  D.jy = ctx->colsq.p + 2 * d + m;
+  // persistent per-problem vectors: [colsq (d) | zy (d) | jac (m) | jy (n)],
+  // each segment at an even (16-byte aligned) offset
+  const int64_t dst2 = (d + 1) / 2 * 2, mst2 = (m + 1) / 2 * 2;
+  CK(ctx->colsq.ensure((size_t)2 * dst2 + mst2 + nst + 8));
+  D.zy = ctx->colsq.p + dst2;
+  D.jac = ctx->colsq.p + 2 * dst2;
+  D.jy = ctx->colsq.p + 2 * dst2 + mst2;
   D.S = ctx->S;
   D.hist = ctx->histb.p;
 
@@ -1432,7 +1437,8 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   RC(build_factor(ctx, kind, mu2));
   if (kind != GDWD_BACKEND_ITERATIVE) RC(ensure_scratch(ctx, ctx->fac_rows, ctx->fac_rows + 2));
   RC(ensure_scratch(ctx, n, d));
-  // initial iterates (solver.py:447-454)
+  // initial iterates (solver.py:447-454); padding slots zeroed first
+  CK(cudaMemsetAsync(ctx->nvec.p, 0, (size_t)NV * nst * sizeof(double), ctx->st));
   fill(ctx, D.r, n, 1.0);
   fill(ctx, D.xi, n, 1.0);
   fill(ctx, D.al, n, 0.0);
@@ -1474,11 +1480,14 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   ctx->poll_pending = 0;
   if (ctx->persistent) {
     int nb = 0;
-    const size_t sm = (size_t)(3 * ((n + 3) / 2 * 2) + 6) * sizeof(double);
-    CK(cudaFuncSetAttribute(gram_smw_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    // small shared carveout: the rest of the unified L1 caches this CTA's K rows
-    CK(cudaFuncSetAttribute(gram_smw_persistent, cudaFuncAttributePreferredSharedMemoryCarveout, 25));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gram_smw_persistent, PK_THREADS, sm));
+    // 11 vector slots: 3 staged, 6 bulk-copied inputs, y and G^{-1} y/|y|
+    const size_t sm = (size_t)(11 * ((n + 3) / 2 * 2)) * sizeof(double);
+    if (sm > 220 * 1024 || cudaFuncSetAttribute(gram_smw_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)sm) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->persistent = false;
+    }
+    if (ctx->persistent) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gram_smw_persistent, PK_THREADS, sm));
     if (nb < 1) ctx->persistent = false;
     else CK(ctx->pk_part.ensure((size_t)2 * NUM_SMS * PK_NPART));
   }
@@ -1518,7 +1527,7 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
     PKArgs pa{D, ctx->kmat.p, ctx->fac.p, ctx->gkmat.p, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host,
               getenv("GDWD_PK_DIAG") ? atoi(getenv("GDWD_PK_DIAG")) : 0, ts, ctx->use_sgs ? 1 : 0};
     void* args[] = {&pa};
-    const size_t sm = (size_t)(3 * ((ctx->n + 3) / 2 * 2) + 6) * sizeof(double);
+    const size_t sm = (size_t)(11 * ((ctx->n + 3) / 2 * 2)) * sizeof(double);
     {
       Launch L(ctx, "persistent_gram_smw2");
       CK(cudaLaunchCooperativeKernel((void*)gram_smw_persistent, dim3(NUM_SMS), dim3(PK_THREADS), args, sm, ctx->st));

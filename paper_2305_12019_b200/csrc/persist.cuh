@@ -179,6 +179,24 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
   double* xa = pksm;           // staged vector 1 (n, padded to even)
   const int64_t ns = (n + 3) / 2 * 2;  // buffer stride: > n, even (16-byte aligned double2 reads)
   double* xb = pksm + ns;      // staged vector 2 (phase H stages a third at 2 ns)
+  // bulk-copied phase inputs (6 slots) and the constant vectors y, G^{-1} y/|y|
+  double* in0 = pksm + 3 * ns;
+  auto IN = [&](int v) { return in0 + v * ns; };
+  const double* sy = pksm + 9 * ns;
+  const double* sjy = pksm + 10 * ns;
+  __shared__ unsigned long long bar;
+  unsigned parity = 0;
+  const unsigned vbytes = (unsigned)(((n + 1) / 2 * 2) * sizeof(double));
+  // thread 0: copy `cnt` whole n-vectors into the input slots; all wait
+  auto fetch = [&](int cnt, const double* const* src, double* const* dst) {
+    if (threadIdx.x == 0) {
+      fence_proxy_async_global();
+      mbar_arrive_expect_tx(&bar, cnt * vbytes);
+      for (int v = 0; v < cnt; ++v) bulk_g2s(dst[v], src[v], vbytes, &bar);
+    }
+    mbar_wait(&bar, parity);
+    parity ^= 1;
+  };
   __shared__ double red[PK_WARPS * PK_NPART];
   __shared__ PKS S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -197,8 +215,15 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
     xa[n] = 0.0;  // pad the odd tail so paired loads read zeros
     xb[n] = 0.0;
     pksm[2 * ns + n] = 0.0;
+    mbar_init(&bar, 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
+  {
+    const double* src[2] = {D.y, D.jy};
+    double* dst[2] = {pksm + 9 * ns, pksm + 10 * ns};
+    fetch(2, src, dst);
+  }
 
   // g = GK t1 + t2 G^{-1} y for the staged t1 (xb), rows owned; returns the
   // partial of ybar.g
@@ -250,15 +275,25 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       const double sig = S.sigma_next;
       double yr = 0.0;
       const double sp = S.sigma_pend, gn = S.gnorm;
+      {
+        const double* src[6] = {D.xi, D.r, D.al, D.u, D.rho, D.x};
+        double* dst[6] = {IN(0), IN(1), IN(2), IN(3), IN(4), IN(5)};
+        fetch(pending ? 6 : 5, src, dst);
+      }
       for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
-        double uj, rj;
-        if (pending) uv_commit(j, uj, rj);
-        else { uj = D.u[j]; rj = D.rho[j]; }
-        const double rhs = (D.xi[j] - D.r[j]) - D.al[j] / sig;
+        double uj = IN(3)[j], rj = IN(4)[j];
+        if (pending) {  // uv_commit
+          const double wj = IN(5)[j];
+          const double gj = wj - rj / (sp * mu);
+          uj = (gn <= D.zscale) ? gj : (D.zscale / gn) * gj;
+          rj = rj - ((D.tau * sp) * mu) * (wj - uj);
+        }
+        const double alj = IN(2)[j];
+        const double rhs = (IN(0)[j] - IN(1)[j]) - alj / sig;
         const double chj = (-rhs + mu2 * uj) + (mu / sig) * rj;
-        xa[j] = D.al[j];
+        xa[j] = alj;
         xb[j] = chj / mu2;
-        yr += D.y[j] * rhs;
+        yr += sy[j] * rhs;
         if (j >= i0 && j < i1) D.h[j] = chj;
       }
       double v1[1] = {yr};
@@ -343,11 +378,16 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       }
       double yv = 0.0;
       const double coef = S.coef;
+      {
+        const double* src[2] = {D.g, D.h};
+        double* dst[2] = {IN(0), IN(1)};
+        fetch(2, src, dst);
+      }
       for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
-        const double v = D.g[j] - coef * D.jy[j];
-        const double x = D.h[j] / mu2 - v / mu2;
+        const double v = IN(0)[j] - coef * sjy[j];
+        const double x = IN(1)[j] / mu2 - v / mu2;
         xa[j] = x;
-        yv += D.y[j] * v;
+        yv += sy[j] * v;
         if (j >= i0 && j < i1) D.xb[j] = x;
       }
       double v1[1] = {yv};
@@ -397,11 +437,16 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
     if (A.use_sgs) {
       const double bb = S.beta_b;
       double ytz = 0.0;
+      {
+        const double* src[4] = {D.h, D.dr, D.ztwb, D.xb};
+        double* dst[4] = {IN(0), IN(1), IN(2), IN(3)};
+        fetch(4, src, dst);
+      }
       for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
-        const double h2 = D.h[j] + D.dr[j];
-        const double ax = (D.ztwb[j] + mu2 * D.xb[j]) + D.y[j] * bb;
+        const double h2 = IN(0)[j] + IN(1)[j];
+        const double ax = (IN(2)[j] + mu2 * IN(3)[j]) + sy[j] * bb;
         xa[j] = h2 - ax;
-        ytz += D.y[j] * D.ztwb[j];
+        ytz += sy[j] * IN(2)[j];
         if (j >= i0 && j < i1) D.h2[j] = h2;
       }
       double v1[1] = {ytz};
@@ -441,7 +486,12 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
     // ---------------- phase E: g' = GK (h2/mu^2) + t2' G^{-1} y ----------------
     if (!reuse) {
       const double t2 = S.h2bot / yty;
-      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) xb[j] = (D.h[j] + D.dr[j]) / mu2;
+      {
+        const double* src[2] = {D.h, D.dr};
+        double* dst[2] = {IN(0), IN(1)};
+        fetch(2, src, dst);
+      }
+      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) xb[j] = (IN(0)[j] + IN(1)[j]) / mu2;
       if (threadIdx.x == 0) S.s2 = ynorm * t2;
       __syncthreads();
       const double sy = gk_rows(t2);
@@ -464,16 +514,21 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       double* xd = pksm + 2 * ns;  // staged w - g
       double yv = 0.0;
       const double coef = S.coef;
+      {
+        const double* src[4] = {D.rho, reuse ? D.xb : D.g, D.h, D.dr};
+        double* dst[4] = {IN(0), IN(1), IN(2), IN(3)};
+        fetch(reuse ? 2 : 4, src, dst);
+      }
       for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
         double wj;
         if (reuse) {
-          wj = D.xb[j];
+          wj = IN(1)[j];
         } else {
-          const double v = D.g[j] - coef * D.jy[j];
-          wj = (D.h[j] + D.dr[j]) / mu2 - v / mu2;
-          yv += D.y[j] * v;
+          const double v = IN(1)[j] - coef * sjy[j];
+          wj = (IN(2)[j] + IN(3)[j]) / mu2 - v / mu2;
+          yv += sy[j] * v;
         }
-        const double gj = wj - D.rho[j] / (sig * mu);
+        const double gj = wj - IN(0)[j] / (sig * mu);
         xw[j] = wj;
         xg[j] = gj;
         xd[j] = wj - gj;  // w - u when u = g (no projection)
