@@ -53,6 +53,15 @@ UNIT = "iter/s"
 CONFIG_NAME = "c2"
 
 
+def traffic_of(tag):
+    """DRAM bytes per launch from a committed ncu capture (profiles/traffic.json)."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    t = json.loads(p.read_text()).get(tag)
+    return t
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -251,17 +260,22 @@ def run_b200(args, dist: Dist):
         mats = float(np.sum(np.where(reused > 0.5, 5, 7)))
         alg = 8.0 * n * n * mats
         ach = alg / (t_ms * 1e-3) / 1e9
+        tr = traffic_of("gram_smw_persistent")
         roofline = {"bound": "hbm", "kernel": "gram_smw_persistent", "achieved": round(ach, 1), "peak": peak,
                     "unit": "GB/s", "frac": round(ach / peak, 4),
-                    "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs", "traffic": None,
+                    "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
+                    "traffic": round(tr["per_iteration"] * iters_timed) if tr else None,
                     "algorithmic_bytes_per_launch": alg,
-                    "note": "K and G^-1 K (2 x %.0f MB) are L2-resident; the loop is barrier/L2-latency bound "
-                            "(one launch, %d grid barriers per iteration)" % (8 * n * n / 1e6, 5)}
+                    "note": "K and G^-1 K (2 x %.0f MB) are L2-resident (ncu: DRAM traffic = the one cold load, "
+                            "L2 hit 96.7%%); the loop is barrier/L2-latency bound (one launch, 4-5 grid barriers "
+                            "per iteration)" % (8 * n * n / 1e6)}
     else:
         top = next(k for k in kernels if k["gbs"] is not None)
+        tr = traffic_of(top["tag"]) if args.config == "c2" else None
         roofline = {"bound": "hbm", "kernel": top["tag"], "achieved": top["gbs"], "peak": peak, "unit": "GB/s",
                     "frac": round(top["gbs"] / peak, 4), "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
-                    "traffic": None, "algorithmic_bytes_per_launch": kernel_bytes(top["tag"], n, d, nnz)}
+                    "traffic": tr["bytes"] if tr else None,
+                    "algorithmic_bytes_per_launch": kernel_bytes(top["tag"], n, d, nnz)}
     roofline["step_matrix_stream_gbs"] = round(x_bytes_iter / (step_ms * 1e-3) / 1e9, 1)
     roofline_x = None
     if args.config == "c2" and not args.x_space:
@@ -287,8 +301,11 @@ def run_b200(args, dist: Dist):
                 roofline_x = roofline_x or {"kernels": {}}
                 roofline_x["kernels"][tag] = round(gbs, 1)
         if best:
+            trx = traffic_of(best[0])
             roofline_x.update({"bound": "hbm", "best_kernel": best[0], "achieved": round(best[1], 1), "peak": peak,
                                "unit": "GB/s", "frac": round(best[1] / peak, 4),
+                               "traffic": trx["bytes"] if trx else None,
+                               "algorithmic_bytes_per_launch": kernel_bytes(best[0], n, d, nnz),
                                "note": "X-space SMW2 (smw_gram_space=0): each kernel streams X = %.0f MB"
                                        % (8 * n * d / 1e6)})
 
