@@ -171,6 +171,33 @@ def make_problem(cfg: SynthConfig, seed: int = 0):
     return scale_problem(x, y, None, cfg.C, cfg.q, tau=tau)
 
 
+def make_variant_problem(cfgname: str, d: int, n: int, seed: int = 0, **var):
+    """A scaled config with option / edge-case variations (test fixtures):
+    ``q``, ``C``, ``shift`` override the config; ``e_random`` draws a
+    max-normalised e in [0.2, 1]; ``holes`` (sparse) empties every 17th
+    sample and feature 3.  Other keys (solver options) are ignored here."""
+    import dataclasses
+
+    from .solver import compute_weights, scale_problem
+    from .sparse import csc_from_scipy
+
+    cfg = CONFIGS[cfgname].scaled(d=d, n=n)
+    over = {k: var[k] for k in ("q", "C", "shift") if k in var}
+    if over:
+        cfg = dataclasses.replace(cfg, **over)
+    x, y = raw_data(cfg, seed)
+    if var.get("holes") and not x.is_dense:
+        m = x.scipy.tolil()
+        m[:, ::17] = 0.0
+        m[3, :] = 0.0
+        x = csc_from_scipy(m.tocsc())
+    e = None
+    if var.get("e_random"):
+        e = np.random.default_rng(seed + 99).uniform(0.2, 1.0, size=n)
+        e[0] = 1.0
+    return scale_problem(x, y, e, cfg.C, cfg.q, tau=compute_weights(y, cfg.q))
+
+
 class DeviceProblemData:
     """ProblemData-compatible record whose Z~ exists only in HBM (configs that
     do not fit host memory).  Fields as ProblemData (solver.py:60-71) minus

@@ -61,6 +61,26 @@ CASES = [
     ("prox_tiny_q2", "c3", 90, 300, "iterative", 40, True, 0, 2),
     ("prox_lanczos_fail", "c1", 6000, 1500, "auto", 12, False, 0, 3),
 ]
+# option / edge-case variants: (name, cfg, d, n, backend, max_iter, full, variations)
+VARIANTS = [
+    ("var_nosgs", "c1", 61, 45, "direct", 40, True, dict(use_sgs=False)),
+    ("var_q_half", "c1", 50, 41, "direct", 40, True, dict(q=0.5)),
+    ("var_q3_mu2", "c1", 48, 60, "iterative", 40, True, dict(q=3.0, mu=2.0)),
+    ("var_opts", "c2", 80, 15, "smw2", 40, True, dict(sigma0=3.0, epsilon_c=0.05, steplength=1.2, mu=0.7)),
+    ("var_e_random", "c1", 40, 55, "direct", 40, True, dict(e_random=True, C=3.0)),
+    ("var_odd", "c3", 37, 53, "direct", 40, True, dict()),
+    ("var_sparse_holes", "c4", 700, 400, "iterative", 30, True, dict(holes=True)),
+    ("var_min_direct", "c1", 1, 2, "direct", 30, True, dict()),
+    ("var_min_smw", "c1", 3, 2, "smw2", 30, True, dict()),
+    ("var_min_iter", "c1", 2, 3, "iterative", 30, True, dict()),
+    ("var_d1_smw", "c1", 1, 5, "smw2", 30, True, dict()),
+    ("var_converge", "c1", 30, 60, "direct", 600, True,
+     dict(C=10.0, shift=2.0, tol_feas=1e-3, tol_cgap=0.03, tol_cap=0.3)),
+    ("var_converge_smw", "c2", 120, 20, "smw2", 600, True,
+     dict(C=10.0, shift=2.0, tol_feas=1e-3, tol_cgap=0.03, tol_cap=0.3)),
+    ("var_converge_iter", "c1", 30, 60, "iterative", 600, True,
+     dict(C=10.0, shift=2.0, tol_feas=1e-3, tol_cgap=0.03, tol_cap=0.3)),
+]
 SAMPLE = 64  # sampled coordinates per vector for the non-full cases
 
 
@@ -75,12 +95,17 @@ def to_ref(prob):
                             z_scale=prob.z_scale)
 
 
-def run_case(name, cfgname, d, n, backend, max_iter, full, seed=0, switch=50):
-    cfg = synth.CONFIGS[cfgname].scaled(d=d, n=n)
-    prob = synth.make_problem(cfg, seed)
+variant_problem = synth.make_variant_problem
+
+
+SOLVER_KEYS = ("use_sgs", "mu", "sigma0", "epsilon_c", "steplength", "tol_feas", "tol_cgap", "tol_cap")
+
+
+def run_case(name, cfgname, d, n, backend, max_iter, full, seed=0, switch=50, **var):
+    prob = variant_problem(cfgname, d, n, seed, **var)
     rp = to_ref(prob)
     conf = gdwd.SolverConfig(q=prob.q, max_iter=max_iter, backend=gdwd.Backend(backend),
-                             psqmr_switch_steps=switch)
+                             psqmr_switch_steps=switch, **{k: var[k] for k in SOLVER_KEYS if k in var})
     rows, vecs = [], {k: [] for k in ("w", "u", "rho", "r", "xi", "alpha")}
     rng = np.random.default_rng(1234)
     idx_d = np.sort(rng.choice(d, min(SAMPLE, d), replace=False))
@@ -101,7 +126,7 @@ def run_case(name, cfgname, d, n, backend, max_iter, full, seed=0, switch=50):
         res = gdwd.sgs_admm_solve(rp, conf, callback=cb)
     except Exception as exc:  # the reference's own error behaviour is part of the fixture
         np.savez_compressed(OUT / f"traj_{name}.npz", hist=np.array(rows), idx_d=idx_d, idx_n=idx_n,
-                            error=type(exc).__name__, iterations_before_error=len(rows),
+                            error=type(exc).__name__, iterations_before_error=len(rows), variant=json.dumps(var),
                             z_sha=z_checksum(prob.z_tilde.values), d=d, n=n, seed=seed, cfg=cfgname,
                             max_iter=max_iter, full=int(full), switch=switch,
                             **{"it_" + k: np.array(v) for k, v in vecs.items()})
@@ -112,7 +137,8 @@ def run_case(name, cfgname, d, n, backend, max_iter, full, seed=0, switch=50):
                converged=int(res.converged), double_count=res.double_count, psqmr_total=res.psqmr_total,
                backend=res.backend_used.value, final_w=res.final_state.w, final_beta=res.final_state.beta,
                z_sha=z_checksum(prob.z_tilde.values), d=d, n=n, seed=seed, cfg=cfgname, max_iter=max_iter,
-               full=int(full), train_error=res.train_error_pct, switch=switch)
+               full=int(full), train_error=res.train_error_pct, switch=switch,
+               variant=json.dumps(var))
     for k, v in vecs.items():
         out["it_" + k] = np.array(v)
     np.savez_compressed(OUT / f"traj_{name}.npz", **out)
@@ -190,6 +216,9 @@ def main():
     for c in CASES:
         if a.only in (None, c[0]):
             run_case(*c)
+    for name, cfgname, d, n, backend, mi, full, var in VARIANTS:
+        if a.only in (None, name, "variants"):
+            run_case(name, cfgname, d, n, backend, mi, full, **var)
     if not a.quick and a.only in (None, "c1"):
         run_c1_full()
 

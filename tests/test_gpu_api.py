@@ -1,0 +1,86 @@
+"""Public-API behaviour on the device path that the reference defines
+outside the numerics: callback contract and abort (solver.py:546), repeated
+solves on a resident problem, max_iter edge, operand validation, backend
+switches on one uploaded matrix."""
+
+import numpy as np
+import pytest
+
+import paper_2305_12019_b200 as G
+from conftest import load_traj, problem_for
+
+pytestmark = pytest.mark.gpu
+
+
+class Stop(Exception):
+    pass
+
+
+def test_callback_exception_propagates_and_context_recovers():
+    prob = problem_for(load_traj("tiny_direct"))
+    cfg = G.SolverConfig(q=prob.q, max_iter=50, backend=G.Backend.DIRECT)
+    seen = []
+
+    def cb(st, res):
+        seen.append(st.iter)
+        if st.iter == 7:
+            raise Stop("user stop")
+
+    with pytest.raises(Stop):
+        G.sgs_admm_solve(prob, cfg, callback=cb)
+    assert seen == list(range(1, 8))
+    # the resident problem is still usable, and a fresh solve is unaffected
+    a = G.sgs_admm_solve(prob, cfg)
+    b = G.sgs_admm_solve(prob, cfg)
+    assert a.iterations == 50 and np.array_equal(a.final_state.w, b.final_state.w)
+
+
+def test_callback_sees_every_iteration_with_reference_fields():
+    tr = load_traj("tiny_smw2")
+    prob = problem_for(tr)
+    cfg = G.SolverConfig(q=prob.q, max_iter=12, backend=G.Backend.SMW2)
+    rows = []
+    out = G.sgs_admm_solve(prob, cfg, callback=lambda st, res: rows.append((st.iter, st.sigma, res.eta_p)))
+    assert [r[0] for r in rows] == list(range(1, 13))
+    assert out.history.shape[0] == 12
+    assert np.array_equal(np.array([r[1] for r in rows]), tr["hist"][:12, 11])
+
+
+def test_max_iter_one_and_result_fields():
+    tr = load_traj("tiny_iter")
+    prob = problem_for(tr)
+    out = G.sgs_admm_solve(prob, G.SolverConfig(q=prob.q, max_iter=1, backend=G.Backend.ITERATIVE))
+    assert out.iterations == 1 and not out.converged
+    assert out.backend_used.value == "iterative"
+    assert out.final_state.w.shape == (prob.d,) and out.final_state.alpha.shape == (prob.n,)
+    assert np.isfinite(out.final_state.beta)
+    for key in ("w", "alpha", "r", "xi"):
+        ref = tr["it_" + key][0]
+        got = getattr(out.final_state, key)
+        assert np.linalg.norm(got - ref) <= 1e-9 * max(np.linalg.norm(ref), 1e-300), key
+
+
+def test_backend_switch_on_one_resident_matrix():
+    """DIRECT, SMW2 and ITERATIVE on the same uploaded Z~ each reproduce the
+    reference's backend-specific first iterate (factor caches keyed by backend)."""
+    prob = problem_for(load_traj("tiny_direct"))
+    outs = {}
+    for be in (G.Backend.DIRECT, G.Backend.SMW2, G.Backend.ITERATIVE, G.Backend.DIRECT):
+        outs.setdefault(be, []).append(G.sgs_admm_solve(prob, G.SolverConfig(q=prob.q, max_iter=15, backend=be)))
+    d0, d1 = outs[G.Backend.DIRECT]
+    assert np.array_equal(d0.final_state.w, d1.final_state.w)
+    # exact solves agree with each other to rounding
+    s = outs[G.Backend.SMW2][0]
+    assert np.linalg.norm(s.final_state.w - d0.final_state.w) <= 1e-8 * np.linalg.norm(d0.final_state.w)
+
+
+def test_matvec_operand_validation():
+    prob = problem_for(load_traj("tiny_direct"))
+    dp = G.solver.device_problem(prob)
+    with pytest.raises(ValueError):
+        dp.matvec(np.ones(prob.n + 1))
+    with pytest.raises(ValueError):
+        dp.rmatvec(np.ones(prob.d + 1))
+    v = np.random.default_rng(0).standard_normal(prob.n)
+    ref = prob.z_tilde.scipy @ v
+    assert np.allclose(dp.matvec(v), ref, rtol=1e-13, atol=1e-13)

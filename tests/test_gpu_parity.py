@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import paper_2305_12019_b200 as G
-from conftest import GOLDEN, TRAJ_CASES, load_traj, problem_for, relerr
+from conftest import GOLDEN, TRAJ_CASES, VAR_CASES, load_traj, problem_for, relerr, solver_options
 
 pytestmark = pytest.mark.gpu
 
@@ -18,6 +18,16 @@ TOL20 = 1e-9
 BACKEND = {"tiny_direct": "direct", "tiny_smw2": "smw2", "tiny_iter": "iterative", "tiny_iter_c4gen": "iterative",
            "tiny_direct_q2": "direct", "tiny_sparse": "iterative",
            "prox_tiny": "iterative", "prox_tiny_q2": "iterative"}
+
+
+def config_for(case, tr, prob, **over):
+    """SolverConfig the fixture was generated with (backend requested
+    explicitly for tiny / variant cases, auto otherwise)."""
+    be = str(tr["backend"]) if case.startswith("var_") else BACKEND.get(case, "auto")
+    kw = dict(q=prob.q, max_iter=int(tr["max_iter"]), backend=G.Backend(be),
+              psqmr_switch_steps=int(tr["switch"]) if "switch" in tr else 50, **solver_options(tr))
+    kw.update(over)
+    return G.SolverConfig(**kw)
 
 
 def run_traj(prob, cfg, full, idx_d=None, idx_n=None, **kw):
@@ -46,12 +56,11 @@ def run_traj(prob, cfg, full, idx_d=None, idx_n=None, **kw):
     return out, np.array(rows), {k: np.array(v) for k, v in vecs.items()}
 
 
-@pytest.mark.parametrize("case", TRAJ_CASES)
+@pytest.mark.parametrize("case", TRAJ_CASES + VAR_CASES)
 def test_trajectory_first20(case):
     tr = load_traj(case)
     prob = problem_for(tr)
-    cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]), backend=G.Backend(BACKEND.get(case, "auto")),
-                         psqmr_switch_steps=int(tr["switch"]) if "switch" in tr else 50)
+    cfg = config_for(case, tr, prob)
     out, h, vecs = run_traj(prob, cfg, bool(tr["full"]), tr["idx_d"], tr["idx_n"])
     assert out.backend_used.value == str(tr["backend"])
     k = min(20, len(tr["hist"]))
@@ -73,14 +82,13 @@ def test_trajectory_first20(case):
     assert np.array_equal(h[:k, 11], ref_h[:, 11])  # sigma sequence identical
 
 
-@pytest.mark.parametrize("case", TRAJ_CASES)
+@pytest.mark.parametrize("case", TRAJ_CASES + VAR_CASES)
 def test_full_run_counters(case):
     """Whole short runs: same iteration count, backend; double/psqmr counts
     within rounding-induced noise; final w within 1e-6 (sigma replayed)."""
     tr = load_traj(case)
     prob = problem_for(tr)
-    cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]), backend=G.Backend(BACKEND.get(case, "auto")),
-                         psqmr_switch_steps=int(tr["switch"]) if "switch" in tr else 50)
+    cfg = config_for(case, tr, prob)
     out = G.sgs_admm_solve(prob, cfg, sigma_schedule=tr["hist"][:, 11])
     assert out.iterations == int(tr["iterations"])
     assert out.converged == bool(tr["converged"])

@@ -6,7 +6,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from conftest import TRAJ_CASES, load_kat, load_traj, problem_for, relerr
+from conftest import TRAJ_CASES, VAR_CASES, load_kat, solver_options, load_traj, problem_for, relerr
 from oracle import gdwd_oracle as O
 
 
@@ -58,7 +58,7 @@ def _hist_row(res, st):
     return [res[f] for f in O.KKT_FIELDS] + [st["sigma"], st["beta"]]
 
 
-@pytest.mark.parametrize("case", TRAJ_CASES)
+@pytest.mark.parametrize("case", TRAJ_CASES + VAR_CASES)
 def test_oracle_matches_reference_trajectory(case):
     tr = load_traj(case)
     prob = problem_for(tr)
@@ -76,13 +76,16 @@ def test_oracle_matches_reference_trajectory(case):
 
     backend = "auto"
     cfg = O.OracleConfig(max_iter=int(tr["max_iter"]), backend=backend,
-                         psqmr_switch_steps=int(tr["switch"]) if "switch" in tr else 50)
+                         psqmr_switch_steps=int(tr["switch"]) if "switch" in tr else 50, **solver_options(tr))
+    if case.startswith("var_"):
+        cfg.backend = str(tr["backend"])
     if case.startswith(("tiny_", "prox_")):
         cfg.backend = {"tiny_direct": "direct", "tiny_smw2": "smw2", "tiny_iter": "iterative",
                        "tiny_iter_c4gen": "iterative", "tiny_direct_q2": "direct",
                        "tiny_sparse": "iterative", "prox_tiny": "iterative", "prox_tiny_q2": "iterative"}[case]
     out = O.solve(prob, cfg, operator="csc", callback=cb)
     assert out.backend == str(tr["backend"])
+    assert out.converged == bool(tr["converged"])
     assert out.iterations == int(tr["iterations"])
     assert out.double_count == int(tr["double_count"])
     assert out.psqmr_total == int(tr["psqmr_total"])
