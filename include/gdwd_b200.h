@@ -52,7 +52,7 @@ typedef struct {
   int32_t seed;
   int32_t use_graph;          /* capture the iteration body in a CUDA graph (DIRECT/SMW2) */
   int32_t poll_every;         /* host polls the device stop flag every k iterations      */
-  int32_t smw_gram_space;     /* SMW2: iterate in n-coefficient space with K = Z~^T Z~   */
+  int32_t smw_gram_space;     /* SMW2 with n <= d: iterate in n-coefficient space, K = Z~^T Z~ */
   int32_t persistent;         /* Gram-space SMW2: run iterations in one cooperative kernel */
   double steplength;
   double tol_feas;

@@ -1357,7 +1357,9 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
 
   // ---- buffers ------------------------------------------------------------
   const int NV = 12, MV = 16;
-  const bool gram = (kind == GDWD_BACKEND_SMW2) && cfg->smw_gram_space;
+  // Gram space pays off (and keeps w exactly representable) only when n <= d,
+  // SMW2's own regime; an explicitly requested SMW2 with d < n iterates over X.
+  const bool gram = (kind == GDWD_BACKEND_SMW2) && cfg->smw_gram_space && n <= d;
   CK(ctx->nvec.ensure((size_t)NV * ((n + 1) / 2 * 2)));
   CK(ctx->mvec.ensure((size_t)MV * ((m + 2) / 2 * 2)));
   CK(ctx->tabs.ensure((size_t)2 * (max_iter + 2) + (size_t)std::max<int64_t>(sched_len, 1)));
