@@ -26,7 +26,6 @@ namespace gdwd {
 namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16, GT = 256;
-constexpr int APAD = 8;
 
 // operand element (row r in [0,R), k) with strides (sr, sk)
 struct Opnd {
