@@ -574,6 +574,51 @@ static void free_sparse(gdwd_ctx* ctx) {
   ctx->nnz = 0;
 }
 
+// Diagnostics (GDWD_PK_TIMING): per-CTA %globaltimer stamps of the persistent
+// kernel; for every phase point, the mean over iterations of the earliest,
+// median and latest CTA relative to the iteration's first CTA start.
+static void pk_timing_report(unsigned long long* ts, size_t tsn) {
+  std::vector<unsigned long long> h(tsn);
+  if (cudaMemcpy(h.data(), ts, tsn * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  cudaFree(ts);
+  const int NP = 32;
+  const char* names[NP] = {"top", "A arrive", "A release", "C arrive", "C release", "D arrive", "D release",
+                           "E arrive", "E release", "H arrive", "H release", "H staged", "H rows", "H step3",
+                           "C staged", "C rows", "C scalars", "C writeback", "C waited", "C loop",
+                           "D waited", "D staged", "", "", "A waited", "A loop", "A staged", "", "", "", "", ""};
+  double mn[NP] = {0}, md[NP] = {0}, mx[NP] = {0};
+  int cnt[NP] = {0};
+  std::vector<double> v;
+  for (int it = 1; it + 1 < PK_TS_ITERS; ++it) {
+    const unsigned long long* r = &h[(size_t)it * NUM_SMS * NP];
+    unsigned long long t0 = ~0ull;
+    bool ok = true;
+    for (int b = 0; b < NUM_SMS; ++b) {
+      if (!r[b * NP]) ok = false;
+      else t0 = std::min(t0, r[b * NP]);
+    }
+    if (!ok) break;
+    for (int pt = 0; pt < NP; ++pt) {
+      v.clear();
+      for (int b = 0; b < NUM_SMS; ++b)
+        if (r[b * NP + pt]) v.push_back((double)(r[b * NP + pt] - t0));
+      if ((int)v.size() != NUM_SMS) continue;
+      std::sort(v.begin(), v.end());
+      mn[pt] += v.front();
+      md[pt] += v[v.size() / 2];
+      mx[pt] += v.back();
+      cnt[pt]++;
+    }
+  }
+  const int order[] = {0, 24, 25, 26, 1, 2, 16, 17, 18, 19, 14, 15, 3, 4, 20, 21, 5, 6, 7, 8, 11, 12, 13, 9, 10};
+  fprintf(stderr, "[pk timing] point        first    median    last   (us from iteration start)\n");
+  for (int pt : order) {
+    if (cnt[pt])
+      fprintf(stderr, "[pk timing] %-12s %8.2f %8.2f %8.2f (n=%d)\n", names[pt], mn[pt] / cnt[pt] / 1e3,
+              md[pt] / cnt[pt] / 1e3, mx[pt] / cnt[pt] / 1e3, cnt[pt]);
+  }
+}
+
 extern "C" {
 
 int gdwd_version(void) { return 1; }
@@ -885,6 +930,8 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
     } else {
       // keep K = Z^T Z for the Gram-space iteration; G = K/mu^2 + I
       CK(ctx->kmat.ensure((size_t)m * ld));
+      // zero pad columns: the persistent kernel's paired loads read them (times 0)
+      CK(cudaMemsetAsync(ctx->kmat.p, 0, (size_t)m * ld * sizeof(double), ctx->st));
       CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, false, 1.0, 0.0, ctx->kmat.p, ld, ctx->facw.p, ctx->st));
       g_from_k_kernel<<<vm_grid(m * m), 256, 0, ctx->st>>>(ctx->kmat.p, ctx->fac.p, m, ld, mu2);
       CK(cudaGetLastError());
@@ -900,6 +947,7 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
     if (kind == GDWD_BACKEND_SMW2) {
       // GK = G^{-1} K for the persistent Gram-space loop (K symmetric)
       CK(ctx->gkmat.ensure((size_t)m * ld));
+      CK(cudaMemsetAsync(ctx->gkmat.p, 0, (size_t)m * ld * sizeof(double), ctx->st));
       CK(gemm_f64(ctx->fac.p, ld, 1, ctx->kmat.p, ld, 1, m, m, m, 1.0, 0.0, ctx->gkmat.p, ld, ctx->st));
       OpJyG op{ctx->y.p, D.ynorm, const_cast<double*>(D.jy), ctx->S};
       RC(ensure_scratch(ctx, m, m));
@@ -1522,9 +1570,10 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
     // one cooperative launch runs all requested iterations (persist.cuh)
     unsigned long long* ts = nullptr;
     const bool timing = getenv("GDWD_PK_TIMING") != nullptr;
+    const size_t tsn = (size_t)PK_TS_ITERS * NUM_SMS * 32;
     if (timing) {
-      CK(cudaMalloc(&ts, 256 * 16 * sizeof(unsigned long long)));
-      CK(cudaMemset(ts, 0, 256 * 16 * sizeof(unsigned long long)));
+      CK(cudaMalloc(&ts, tsn * sizeof(unsigned long long)));
+      CK(cudaMemset(ts, 0, tsn * sizeof(unsigned long long)));
     }
     PKArgs pa{D, ctx->kmat.p, ctx->fac.p, ctx->gkmat.p, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host,
               getenv("GDWD_PK_DIAG") ? atoi(getenv("GDWD_PK_DIAG")) : 0, ts, ctx->use_sgs ? 1 : 0};
@@ -1536,45 +1585,7 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
     }
     CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
-    if (ts) {  // diagnostics: mean duration between consecutive phase points
-      std::vector<unsigned long long> h(256 * 16);
-      CK(cudaMemcpy(h.data(), ts, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-      cudaFree(ts);
-      double acc[16] = {0};
-      int cnt[16] = {0};
-      for (int it = 1; it + 1 < 256; ++it) {
-        const unsigned long long* r = &h[it * 16];
-        if (!r[0] || !h[(it + 1) * 16]) break;
-        unsigned long long prev = r[0];
-        for (int pt = 1; pt <= 10; ++pt) {
-          if (!r[pt]) continue;
-          acc[pt] += (double)(r[pt] - prev);
-          cnt[pt]++;
-          prev = r[pt];
-        }
-        acc[11] += (double)(h[(it + 1) * 16] - prev);
-        cnt[11]++;
-      }
-      const char* names[] = {"", "A work", "A barrier", "C work", "C barrier", "D work", "D barrier",
-                             "E work", "E barrier", "H work", "H barrier", "H tail"};
-      for (int pt = 1; pt <= 11; ++pt)
-        if (cnt[pt]) fprintf(stderr, "[pk timing] %-10s %8.2f us (n=%d)\n", names[pt], acc[pt] / cnt[pt] / 1e3, cnt[pt]);
-      // sub-phase points: 14/15 inside C (after staging / after rows), 11-13 inside H
-      double sub[5] = {0};
-      int sc = 0;
-      for (int it = 1; it + 1 < 256; ++it) {
-        const unsigned long long* r = &h[it * 16];
-        if (!r[0] || !r[14] || !r[11]) break;
-        sub[0] += (double)(r[14] - r[2]);   // A fin + C staging
-        sub[1] += (double)(r[15] - r[14]);  // C rows + Newton
-        sub[2] += (double)(r[11] - (r[8] ? r[8] : r[6]));  // H staging
-        sub[3] += (double)(r[12] - r[11]);  // H rows
-        sub[4] += (double)(r[13] - r[12]);  // Step 3 + KKT terms
-        sc++;
-      }
-      const char* sn[] = {"A fin + C staging", "C rows+Newton", "H staging", "H rows", "H step3"};
-      for (int q = 0; q < 5 && sc; ++q) fprintf(stderr, "[pk timing]   %-18s %8.2f us\n", sn[q], sub[q] / sc / 1e3);
-    }
+    if (ts) pk_timing_report(ts, tsn);
     ctx->k_host = ctx->Sh->stopped ? ctx->Sh->iters_done : kend;
     ctx->stopped = ctx->Sh->stopped != 0;
   }

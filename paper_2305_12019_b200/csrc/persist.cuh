@@ -22,14 +22,14 @@
 //                                staging), c_h, g; finish k-1 (obj_d, gap,
 //                                stop test)                               :535-542,496-499
 //   C  K c_xb                    x_bar, ztw_bar, Newton r+, dr            :501-504
-//   D  K c_res                   reuse test                               :506-524
-//   E  GK t1'  (re-solve only)   g'                                       :524-529
+//   D  [K c_res ; GK dr/mu^2]    reuse test; the re-solve g' speculatively
+//                                (GK t1 kept from A, linearity)           :506-529
 //   H  K [c_x ; c_g ; c_w - c_g] ztw (re-solve only), ||g||, ||w - u||;
 //                                Step 3 and the KKT sample terms          :530-545,311-340
 // with GK = G^{-1} K precomputed once (DMMA GEMM), so the SMW solve's
 // g = G^{-1}(K t1 + y t2) = GK t1 + t2 G^{-1} y needs no separate G^{-1}
 // phase (subsolvers.py:138-143, same math, different association).
-// 4 grid barriers per iteration (5 when Step 1c re-solves).
+// 4 grid barriers per iteration (3 with use_sgs = False).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -43,6 +43,7 @@ namespace cg = cooperative_groups;
 constexpr int PK_THREADS = 512;
 constexpr int PK_WARPS = PK_THREADS / 32;
 constexpr int PK_NPART = 14;  // widest cross-CTA sum (norms + KKT terms)
+constexpr int PK_TS_ITERS = 64;  // diagnostics: iterations timestamped (every CTA)
 
 struct PKArgs {
   Dev D;
@@ -50,7 +51,7 @@ struct PKArgs {
   const double* Ginv;  // n x ld
   const double* GK;    // G^{-1} K, n x ld
   int64_t ld;
-  double* part;        // [2][gridDim][PK_NPART]
+  double* part;        // [2][PK_NPART][gridDim] (per value, CTAs contiguous: coalesced cross-CTA reads)
   int count;           // iterations to run in this launch
   int diag;            // diagnostics: 1 = skip the GEMV rows (barrier/staging floor)
   unsigned long long* tstamp;  // diagnostics: CTA-0 %globaltimer at phase boundaries (null: off)
@@ -65,33 +66,94 @@ struct PKS {
   double eta[11];
 };
 
-// Cross-CTA reduction of per-CTA partials (slot alternates by phase).
+// Cross-CTA reduction of per-CTA partials (slot alternates by phase), the
+// same fixed order in every CTA so the totals are bitwise identical
+// everywhere.  Small K: thread b loads CTA b's values, a shuffle tree per
+// warp, then every thread adds the per-warp sums in warp order.  Wide K
+// (the KKT bundle): warp k sums value k over the CTAs (8 loads in flight per
+// lane, then a shuffle tree) -- avoids K-wide shuffle trees in 5 warps.
+// (The next writer of `red` starts with a __syncthreads.)
 template <int K>
 GDWD_DEV void pk_cross_sum(const double* part, int slot, double (&out)[K], double* red) {
-  const double* p = part + (size_t)slot * gridDim.x * PK_NPART;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* p = part + (size_t)slot * PK_NPART * gridDim.x;
+  if constexpr (K <= 4) {
+    double v[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) out[k] = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    for (int k = 0; k < K; ++k) v[k] = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += PK_THREADS) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) out[k] += ld_cg(p + (size_t)b * PK_NPART + k);
+      for (int k = 0; k < K; ++k) v[k] += ld_cg(p + (size_t)k * gridDim.x + b);
+    }
+    const int nw = min(PK_WARPS, ((int)gridDim.x + 31) / 32);
+    if (warp < nw) {
+      warp_sum<K>(v);
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) red[warp * K + k] = v[k];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += red[w * K + k];
+      out[k] = t;
+    }
+  } else {
+    static_assert(K <= PK_WARPS, "one warp per value");
+    if (warp < K) {
+      const double* pk = p + (size_t)warp * gridDim.x;
+      double v[1] = {0.0};
+      for (int b0 = 0; b0 < (int)gridDim.x; b0 += 32 * 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = b0 + lane + 32 * u;
+          x[u] = b < (int)gridDim.x ? ld_cg(pk + b) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[0] += x[u];
+      }
+      warp_sum<1>(v);
+      if (lane == 0) red[warp] = v[0];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = red[k];
   }
-  block_sum<K>(out, red);
 }
 
+// This CTA's partials of K values held by lane 0 of each warp (row results):
+// per-warp values through shared memory, a shuffle tree in warp 0, stored
+// value-major ([slot][k][CTA]) for the coalesced cross-CTA sum.
 template <int K>
-GDWD_DEV void pk_write_part(double* part, int slot, const double (&v)[K], double* red) {
-  double t[K];
+GDWD_DEV void pk_write_lane0(double* part, int slot, const double (&v)[K], double* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();  // earlier readers of red are done
+  if (lane == 0) {
 #pragma unroll
-  for (int k = 0; k < K; ++k) t[k] = v[k];
-  block_sum<K>(t, red);
-  if (threadIdx.x == 0) {
-    double* p = part + ((size_t)slot * gridDim.x + blockIdx.x) * PK_NPART;
+    for (int k = 0; k < K; ++k) red[warp * K + k] = v[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double t[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) p[k] = t[k];
+    for (int k = 0; k < K; ++k) t[k] = lane < PK_WARPS ? red[lane * K + k] : 0.0;
+    warp_sum<K>(t);
+    if (lane == 0) {
+      double* p = part + (size_t)slot * gridDim.x * PK_NPART + blockIdx.x;
+#pragma unroll
+      for (int k = 0; k < K; ++k) p[(size_t)k * gridDim.x] = t[k];
+    }
   }
 }
 
 // dot of K-row i (length n, stride ld) with the staged vector(s); one warp.
+// Rows are consumed in batches of U chunks of 64 doubles (one double2 per
+// lane per chunk), loads predicated at the ragged end so every batch keeps
+// U loads in flight per lane; the pad column of K and of the staged vectors
+// is zero.  Per-lane accumulation order is ascending j, then the shuffle tree.
 template <int NV>
 GDWD_DEV void pk_row_dot(const double* const (&rows)[NV], int64_t n, const double* const (&xs)[NV],
                          double (&out)[NV]) {
@@ -99,30 +161,27 @@ GDWD_DEV void pk_row_dot(const double* const (&rows)[NV], int64_t n, const doubl
   double acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-  int64_t j = 2 * lane;
   constexpr int U = 16 / NV;
-  for (; j + (U - 1) * 64 < n; j += U * 64) {
+  for (int64_t j0 = 2 * lane; j0 < n + 2 * lane; j0 += U * 64) {
     double2 z[NV][U];
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int u = 0; u < U; ++u) z[v][u] = __ldg(reinterpret_cast<const double2*>(rows[v] + j + u * 64));
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = j0 + u * 64;
+        z[v][u] = j < n ? __ldg(reinterpret_cast<const double2*>(rows[v] + j)) : make_double2(0.0, 0.0);
+      }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + u * 64;
+      if (j < n) {
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const double2 xv = *reinterpret_cast<const double2*>(xs[v] + j + u * 64);
-        acc[v] += z[v][u].x * xv.x;
-        acc[v] += z[v][u].y * xv.y;
+        for (int v = 0; v < NV; ++v) {
+          const double2 xv = *reinterpret_cast<const double2*>(xs[v] + j);
+          acc[v] += z[v][u].x * xv.x;
+          acc[v] += z[v][u].y * xv.y;
+        }
       }
-    }
-  }
-  for (; j < n; j += 64) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const double2 z = __ldg(reinterpret_cast<const double2*>(rows[v] + j));
-      acc[v] += z.x * xs[v][j];
-      if (j + 1 < n) acc[v] += z.y * xs[v][j + 1];
     }
   }
   warp_sum<NV>(acc);
@@ -137,27 +196,24 @@ GDWD_DEV void pk_row_dot_same(const double* row, int64_t n, const double* const 
   double acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-  int64_t j = 2 * lane;
-  for (; j + 15 * 64 < n; j += 16 * 64) {
+  for (int64_t j0 = 2 * lane; j0 < n + 2 * lane; j0 += 16 * 64) {
     double2 z[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) z[u] = __ldg(reinterpret_cast<const double2*>(row + j + u * 64));
+    for (int u = 0; u < 16; ++u) {
+      const int64_t j = j0 + u * 64;
+      z[u] = j < n ? __ldg(reinterpret_cast<const double2*>(row + j)) : make_double2(0.0, 0.0);
+    }
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
+      const int64_t j = j0 + u * 64;
+      if (j < n) {
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const double2 xv = *reinterpret_cast<const double2*>(xs[v] + j + u * 64);
-        acc[v] += z[u].x * xv.x;
-        acc[v] += z[u].y * xv.y;
+        for (int v = 0; v < NV; ++v) {
+          const double2 xv = *reinterpret_cast<const double2*>(xs[v] + j);
+          acc[v] += z[u].x * xv.x;
+          acc[v] += z[u].y * xv.y;
+        }
       }
-    }
-  }
-  for (; j < n; j += 64) {
-    const double2 z = __ldg(reinterpret_cast<const double2*>(row + j));
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      acc[v] += z.x * xs[v][j];
-      if (j + 1 < n) acc[v] += z.y * xs[v][j + 1];
     }
   }
   warp_sum<NV>(acc);
@@ -187,15 +243,29 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
   __shared__ unsigned long long bar;
   unsigned parity = 0;
   const unsigned vbytes = (unsigned)(((n + 1) / 2 * 2) * sizeof(double));
-  // thread 0: copy `cnt` whole n-vectors into the input slots; all wait
-  auto fetch = [&](int cnt, const double* const* src, double* const* dst) {
+  // Phase inputs are bulk-copied by thread 0 right after the grid barrier
+  // that makes them final (overlapping the cross-CTA sum and the scalar
+  // section); every issue is matched by exactly one wait of all threads.
+  auto issue = [&](int cnt, const double* const* src, double* const* dst) {
     if (threadIdx.x == 0) {
       fence_proxy_async_global();
       mbar_arrive_expect_tx(&bar, cnt * vbytes);
       for (int v = 0; v < cnt; ++v) bulk_g2s(dst[v], src[v], vbytes, &bar);
     }
+  };
+  auto wait_in = [&]() {
     mbar_wait(&bar, parity);
     parity ^= 1;
+  };
+  auto fetch = [&](int cnt, const double* const* src, double* const* dst) {
+    issue(cnt, src, dst);
+    wait_in();
+  };
+  // phase A inputs: xi, r, alpha, u, rho, x (x only read when an update is pending)
+  auto issue_a = [&]() {
+    const double* src[6] = {D.xi, D.r, D.al, D.u, D.rho, D.x};
+    double* dst[6] = {IN(0), IN(1), IN(2), IN(3), IN(4), IN(5)};
+    issue(6, src, dst);
   };
   __shared__ double red[PK_WARPS * PK_NPART];
   __shared__ PKS S;
@@ -225,25 +295,6 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
     fetch(2, src, dst);
   }
 
-  // g = GK t1 + t2 G^{-1} y for the staged t1 (xb), rows owned; returns the
-  // partial of ybar.g
-  auto gk_rows = [&](double t2) -> double {
-    double sy = 0.0;
-    for (int r = warp; r < nrows; r += PK_WARPS) {
-      const int64_t i = i0 + r;
-      const double* rows[1] = {A.GK + i * A.ld};
-      const double* xs[1] = {xb};
-      double o[1];
-      pk_row_dot<1>(rows, n, xs, o);
-      if (lane == 0) {
-        const double gi = o[0] + t2 * (ynorm * D.jy[i]);
-        D.g[i] = gi;
-        sy += (D.y[i] / ynorm) * gi;
-      }
-    }
-    return sy;
-  };
-
   // Step 2's u, rho update of the previous iteration (solver.py:535-542)
   // needs ||g||, known only after the last barrier of that iteration: phase A
   // applies it on the fly while staging (every CTA, all j) and the owners
@@ -258,15 +309,19 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
 
   const int k_end = S.k + A.count;
   const int k_begin = S.k;
-  // CTA-0 timestamps: slot (iteration, point); points: 0 top, then per phase
+  // per-CTA timestamps: slot (iteration, CTA, point); points: 0 top, then per phase
   // 2p+1 = arrival at its barrier, 2p+2 = scalars ready after it
 #define PK_TS(pt)                                                                          \
   do {                                                                                     \
-    if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && S.k - k_begin < 256)            \
-      A.tstamp[(size_t)(S.k - k_begin) * 16 + (pt)] = pk_now();                            \
+    if (A.tstamp && threadIdx.x == 0 && S.k - k_begin < PK_TS_ITERS)                       \
+      A.tstamp[((size_t)(S.k - k_begin) * gridDim.x + blockIdx.x) * 32 + (pt)] = pk_now(); \
   } while (0)
+  issue_a();
   for (;;) {
-    if (S.stopped || S.k >= k_end) break;
+    if (S.stopped || S.k >= k_end) {
+      wait_in();
+      break;
+    }
     const int k = S.k;
     PK_TS(0);
     const bool pending = S.pending != 0;
@@ -275,11 +330,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       const double sig = S.sigma_next;
       double yr = 0.0;
       const double sp = S.sigma_pend, gn = S.gnorm;
-      {
-        const double* src[6] = {D.xi, D.r, D.al, D.u, D.rho, D.x};
-        double* dst[6] = {IN(0), IN(1), IN(2), IN(3), IN(4), IN(5)};
-        fetch(pending ? 6 : 5, src, dst);
-      }
+      wait_in();
+      PK_TS(24);
       for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
         double uj = IN(3)[j], rj = IN(4)[j];
         if (pending) {  // uv_commit
@@ -296,6 +348,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         yr += sy[j] * rhs;
         if (j >= i0 && j < i1) D.h[j] = chj;
       }
+      PK_TS(25);
       double v1[1] = {yr};
       block_sum<1>(v1, red);
       if (threadIdx.x == 0) {
@@ -303,6 +356,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         S.s2 = ynorm * (S.hbot / yty);
       }
       __syncthreads();
+      PK_TS(26);
       const double t2 = S.hbot / yty;
       double qa = 0.0, sy = 0.0;
       for (int r = warp; r < nrows; r += PK_WARPS) {
@@ -313,15 +367,21 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         pk_row_dot<2>(rows, n, xs, o);
         if (lane == 0) {
           qa += D.al[i] * o[0];
+          D.s1[i] = o[1];  // GK t1, reused by phase D's re-solve
           const double gi = o[1] + t2 * (ynorm * D.jy[i]);
           D.g[i] = gi;
           sy += (D.y[i] / ynorm) * gi;
         }
       }
       double pv[2] = {qa, sy};
-      pk_write_part<2>(A.part, slot, pv, red);
+      pk_write_lane0<2>(A.part, slot, pv, red);
       PK_TS(1);
       grid.sync();
+      {  // phase C inputs: g (rows of all CTAs), h
+        const double* src[2] = {D.g, D.h};
+        double* dst[2] = {IN(0), IN(1)};
+        issue(2, src, dst);
+      }
       double tot[2];
       pk_cross_sum<2>(A.part, slot, tot, red);
       slot ^= 1;
@@ -362,10 +422,14 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         }
       }
       __syncthreads();
-      if (S.stopped) break;
+      if (S.stopped) {
+        wait_in();
+        break;
+      }
     }
     const double sig = S.sigma;
     const double eps = D.eps_tab[k];
+    PK_TS(16);
     // ---------------- phase C: x_bar, K x_bar -> ztw_bar, Newton -------------
     {
       if (pending) {  // owners write back the u, rho update applied in phase A
@@ -376,13 +440,11 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
           D.rho[j] = rj;
         }
       }
+      PK_TS(17);
       double yv = 0.0;
       const double coef = S.coef;
-      {
-        const double* src[2] = {D.g, D.h};
-        double* dst[2] = {IN(0), IN(1)};
-        fetch(2, src, dst);
-      }
+      wait_in();
+      PK_TS(18);
       for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
         const double v = IN(0)[j] - coef * sjy[j];
         const double x = IN(1)[j] / mu2 - v / mu2;
@@ -390,6 +452,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         yv += sy[j] * v;
         if (j >= i0 && j < i1) D.xb[j] = x;
       }
+      PK_TS(19);
       double v1[1] = {yv};
       block_sum<1>(v1, red);
       if (threadIdx.x == 0) {
@@ -423,9 +486,18 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       }
       PK_TS(15);
       double pv[1] = {ydr};
-      pk_write_part<1>(A.part, slot, pv, red);
+      pk_write_lane0<1>(A.part, slot, pv, red);
       PK_TS(3);
       grid.sync();
+      if (A.use_sgs) {  // phase D inputs
+        const double* src[4] = {D.h, D.dr, D.ztwb, D.xb};
+        double* dst[4] = {IN(0), IN(1), IN(2), IN(3)};
+        issue(4, src, dst);
+      } else {  // phase H inputs (Step 1c skipped: w = x_bar)
+        const double* src[2] = {D.rho, D.xb};
+        double* dst[2] = {IN(0), IN(1)};
+        issue(2, src, dst);
+      }
       double t[1];
       pk_cross_sum<1>(A.part, slot, t, red);
       slot ^= 1;
@@ -433,19 +505,22 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       if (threadIdx.x == 0) S.h2bot = S.hbot + t[0];
       __syncthreads();
     }
-    // ---------------- phase D: reuse test -------------------------------------
+    // ---------------- phase D: reuse test + speculative re-solve -------------
+    // Step 1c's residual q = r^T K r (r = h2 - A x_bar, solver.py:506-524) and,
+    // in the same row sweep, the re-solve g' = G^{-1}K (h2/mu^2) + t2' G^{-1}y
+    // = [GK t1 (kept from phase A) + GK (dr/mu^2)] + t2' G^{-1}y, used if the
+    // test fails (subsolvers.py:138-143 by linearity; one barrier instead of two).
     if (A.use_sgs) {
       const double bb = S.beta_b;
+      const double t2 = S.h2bot / yty;
       double ytz = 0.0;
-      {
-        const double* src[4] = {D.h, D.dr, D.ztwb, D.xb};
-        double* dst[4] = {IN(0), IN(1), IN(2), IN(3)};
-        fetch(4, src, dst);
-      }
+      wait_in();
+      PK_TS(20);
       for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
         const double h2 = IN(0)[j] + IN(1)[j];
         const double ax = (IN(2)[j] + mu2 * IN(3)[j]) + sy[j] * bb;
         xa[j] = h2 - ax;
+        xb[j] = IN(1)[j] / mu2;
         ytz += sy[j] * IN(2)[j];
         if (j >= i0 && j < i1) D.h2[j] = h2;
       }
@@ -453,28 +528,43 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       block_sum<1>(v1, red);
       if (threadIdx.x == 0) S.ytzw = v1[0];
       __syncthreads();
-      double q = 0.0;
+      PK_TS(21);
+      double q = 0.0, syg = 0.0;
       for (int r = warp; r < nrows; r += PK_WARPS) {
         const int64_t i = i0 + r;
-        const double* rows[1] = {A.K + i * A.ld};
-        const double* xs[1] = {xa};
-        double o[1];
-        pk_row_dot<1>(rows, n, xs, o);
-        if (lane == 0) q += xa[i] * o[0];
+        const double* rows[2] = {A.K + i * A.ld, A.GK + i * A.ld};
+        const double* xs[2] = {xa, xb};
+        double o[2];
+        pk_row_dot<2>(rows, n, xs, o);
+        if (lane == 0) {
+          q += xa[i] * o[0];
+          const double gi = (D.s1[i] + o[1]) + t2 * (ynorm * D.jy[i]);
+          D.g[i] = gi;
+          syg += (D.y[i] / ynorm) * gi;
+        }
       }
-      double pv[1] = {q};
-      pk_write_part<1>(A.part, slot, pv, red);
+      double pv[2] = {q, syg};
+      pk_write_lane0<2>(A.part, slot, pv, red);
       PK_TS(5);
       grid.sync();
-      double t[1];
-      pk_cross_sum<1>(A.part, slot, t, red);
+      {  // H inputs: rho, x_bar (reused) or g' (re-solved) with h, dr
+        const double* src[5] = {D.rho, D.xb, D.h, D.dr, D.g};
+        double* dst[5] = {IN(0), IN(1), IN(2), IN(3), IN(4)};
+        issue(5, src, dst);
+      }
+      double t[2];
+      pk_cross_sum<2>(A.part, slot, t, red);
       slot ^= 1;
       PK_TS(6);
       if (threadIdx.x == 0) {
         const double rb = S.h2bot - (S.ytzw + yty * bb);
         const double rr = hypot(sqrt(t[0] > 0.0 ? t[0] : 0.0), rb);
         S.reuse = rr <= 5.0 * eps;
-        if (!S.reuse) S.double_count += 1;
+        if (!S.reuse) {
+          S.double_count += 1;
+          S.s2 = ynorm * t2;
+          S.coef = (t[1] + (-S.s2)) / D.S->ys;
+        }
         if (blockIdx.x == 0) D.hist[(int64_t)k * HIST_W + H_REUSE] = S.reuse ? 1.0 : 0.0;
       }
       __syncthreads();
@@ -483,29 +573,6 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       __syncthreads();
     }
     const bool reuse = S.reuse != 0;
-    // ---------------- phase E: g' = GK (h2/mu^2) + t2' G^{-1} y ----------------
-    if (!reuse) {
-      const double t2 = S.h2bot / yty;
-      {
-        const double* src[2] = {D.h, D.dr};
-        double* dst[2] = {IN(0), IN(1)};
-        fetch(2, src, dst);
-      }
-      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) xb[j] = (IN(0)[j] + IN(1)[j]) / mu2;
-      if (threadIdx.x == 0) S.s2 = ynorm * t2;
-      __syncthreads();
-      const double sy = gk_rows(t2);
-      double pv[1] = {sy};
-      pk_write_part<1>(A.part, slot, pv, red);
-      PK_TS(7);
-      grid.sync();
-      double t[1];
-      pk_cross_sum<1>(A.part, slot, t, red);
-      slot ^= 1;
-      PK_TS(8);
-      if (threadIdx.x == 0) S.coef = (t[0] + (-S.s2)) / D.S->ys;
-      __syncthreads();
-    }
     // ---------------- phase H: [ztw ;] ||g||, ||w-u||, ||w||; Step 3, KKT --------
     {
       // w coefficients: x_bar when reused, else x = h2/mu^2 - v/mu^2 (GsX)
@@ -514,17 +581,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       double* xd = pksm + 2 * ns;  // staged w - g
       double yv = 0.0;
       const double coef = S.coef;
-      {
-        const double* src[4] = {D.rho, reuse ? D.xb : D.g, D.h, D.dr};
-        double* dst[4] = {IN(0), IN(1), IN(2), IN(3)};
-        fetch(reuse ? 2 : 4, src, dst);
-      }
+      wait_in();  // slots: rho, x_bar, h, dr, g' (no-sgs: rho, x_bar)
       for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
         double wj;
         if (reuse) {
           wj = IN(1)[j];
         } else {
-          const double v = IN(1)[j] - coef * sjy[j];
+          const double v = IN(4)[j] - coef * sjy[j];
           wj = (IN(2)[j] + IN(3)[j]) / mu2 - v / mu2;
           yv += sy[j] * v;
         }
@@ -579,7 +642,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       {
         // Step 3 + KKT sample terms (solver.py:533,538-541,311-333; OpStep3)
         const double bet = S.beta, C = D.C;
-        for (int64_t i = i0 + threadIdx.x; i < i1; i += PK_THREADS) {
+        for (int64_t i = i0 + threadIdx.x; warp == 0 && i < i1; i += 32) {  // warp 0: the CTA's samples
           const double rr = D.rnew[i];
           D.r[i] = rr;
           const double yi = D.y[i], ei = D.e[i], zt = D.ztw[i], ali = D.al[i];
@@ -606,9 +669,27 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         }
       }
       PK_TS(13);
-      pk_write_part<PK_NPART>(A.part, slot, acc, red);
+      // partials: KKT sample terms from warp 0 (the CTA's <= 32 samples),
+      // row terms from lane 0 of every warp
+      __syncthreads();
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) red[warp * 4 + q] = acc[10 + q];
+      }
+      __syncthreads();
+      if (warp == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[10 + q] = lane < PK_WARPS ? red[lane * 4 + q] : 0.0;
+        warp_sum<PK_NPART>(acc);
+        if (lane == 0) {
+          double* p = A.part + (size_t)slot * gridDim.x * PK_NPART + blockIdx.x;
+#pragma unroll
+          for (int f = 0; f < PK_NPART; ++f) p[(size_t)f * gridDim.x] = acc[f];
+        }
+      }
       PK_TS(9);
       grid.sync();
+      issue_a();  // next iteration's phase A inputs (waited at the loop top or in A)
       double t[PK_NPART];
       pk_cross_sum<PK_NPART>(A.part, slot, t, red);
       slot ^= 1;
