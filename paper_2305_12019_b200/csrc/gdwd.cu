@@ -1538,7 +1538,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
       ctx->persistent = false;
     }
     if (ctx->persistent) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gram_smw_persistent, PK_THREADS, sm));
-    if (nb < 1) ctx->persistent = false;
+    if (nb < 1 || n > (int64_t)PK_MAX_OWN * NUM_SMS) ctx->persistent = false;
     else CK(ctx->pk_part.ensure((size_t)2 * NUM_SMS * PK_NPART));
   }
   if (kind != GDWD_BACKEND_ITERATIVE && cfg->use_graph && !ctx->prof && !ctx->persistent && ctx->comm_mode != 2) {

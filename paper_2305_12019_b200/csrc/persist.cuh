@@ -43,7 +43,8 @@ namespace cg = cooperative_groups;
 constexpr int PK_THREADS = 512;
 constexpr int PK_WARPS = PK_THREADS / 32;
 constexpr int PK_NPART = 14;  // widest cross-CTA sum (norms + KKT terms)
-constexpr int PK_TS_ITERS = 64;  // diagnostics: iterations timestamped (every CTA)
+constexpr int PK_TS_ITERS = 64;
+constexpr int PK_MAX_OWN = 64;   // samples per CTA (host: n <= PK_MAX_OWN * grid)  // diagnostics: iterations timestamped (every CTA)
 
 struct PKArgs {
   Dev D;
@@ -273,6 +274,9 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
   const int64_t i0 = n * blockIdx.x / gridDim.x, i1 = n * (blockIdx.x + 1) / gridDim.x;
   const int nrows = A.diag == 1 ? 0 : (int)(i1 - i0);
   const double mu = D.mu, mu2 = D.mu2, yty = D.yty, ynorm = D.ynorm;
+  const bool mu2_one = mu2 == 1.0;  // x / 1.0 == x exactly: skip the division
+  const double ys = D.S->ys;          // SMW scalar, fixed for the solve
+  __shared__ double own_u[PK_MAX_OWN], own_rho[PK_MAX_OWN];
   int slot = 0;
 
   if (threadIdx.x == 0) {
@@ -323,6 +327,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       break;
     }
     const int k = S.k;
+    const double eps = D.eps_tab[k], tol = D.tol_tab[k];  // issued early, used in C / D
     PK_TS(0);
     const bool pending = S.pending != 0;
     // ---------------- phase A: u, rho (k-1); K alpha; g = GK t1 ---------------
@@ -332,7 +337,12 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       const double sp = S.sigma_pend, gn = S.gnorm;
       wait_in();
       PK_TS(24);
-      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+#pragma unroll 1
+      for (int64_t j0 = threadIdx.x; j0 < n; j0 += 4 * PK_THREADS)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // 4 independent elements in flight per thread
+        const int64_t j = j0 + u * PK_THREADS;
+        if (j >= n) break;
         double uj = IN(3)[j], rj = IN(4)[j];
         if (pending) {  // uv_commit
           const double wj = IN(5)[j];
@@ -344,9 +354,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         const double rhs = (IN(0)[j] - IN(1)[j]) - alj / sig;
         const double chj = (-rhs + mu2 * uj) + (mu / sig) * rj;
         xa[j] = alj;
-        xb[j] = chj / mu2;
+        xb[j] = mu2_one ? chj : chj / mu2;
         yr += sy[j] * rhs;
-        if (j >= i0 && j < i1) D.h[j] = chj;
+        if (j >= i0 && j < i1) {
+          D.h[j] = chj;
+          own_u[j - i0] = uj;  // written back in phase C (WAR: other CTAs are still copying u, rho)
+          own_rho[j - i0] = rj;
+        }
       }
       PK_TS(25);
       double v1[1] = {yr};
@@ -387,7 +401,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       slot ^= 1;
       PK_TS(2);
       if (threadIdx.x == 0) {
-        S.coef = (tot[1] + (-S.s2)) / D.S->ys;
+        S.coef = (tot[1] + (-S.s2)) / ys;
         if (blockIdx.x == 0) D.h[D.bot] = S.hbot;
         // finish iteration k-1 (solver.py:293-304,334,548-555)
         if (k > 0) {
@@ -428,16 +442,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       }
     }
     const double sig = S.sigma;
-    const double eps = D.eps_tab[k];
     PK_TS(16);
     // ---------------- phase C: x_bar, K x_bar -> ztw_bar, Newton -------------
     {
       if (pending) {  // owners write back the u, rho update applied in phase A
         for (int64_t j = i0 + threadIdx.x; j < i1; j += PK_THREADS) {
-          double uj, rj;
-          uv_commit(j, uj, rj);
-          D.u[j] = uj;
-          D.rho[j] = rj;
+          D.u[j] = own_u[j - i0];
+          D.rho[j] = own_rho[j - i0];
         }
       }
       PK_TS(17);
@@ -445,9 +456,14 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       const double coef = S.coef;
       wait_in();
       PK_TS(18);
-      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+#pragma unroll 1
+      for (int64_t j0 = threadIdx.x; j0 < n; j0 += 4 * PK_THREADS)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // 4 independent elements in flight per thread
+        const int64_t j = j0 + u * PK_THREADS;
+        if (j >= n) break;
         const double v = IN(0)[j] - coef * sjy[j];
-        const double x = IN(1)[j] / mu2 - v / mu2;
+        const double x = mu2_one ? IN(1)[j] - v : IN(1)[j] / mu2 - v / mu2;
         xa[j] = x;
         yv += sy[j] * v;
         if (j >= i0 && j < i1) D.xb[j] = x;
@@ -465,7 +481,6 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       __syncthreads();
       PK_TS(14);
       const double bb = S.beta_b;
-      const double tol = D.tol_tab[k];
       double ydr = 0.0;
       for (int r = warp; r < nrows; r += PK_WARPS) {
         const int64_t i = i0 + r;
@@ -516,11 +531,16 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       double ytz = 0.0;
       wait_in();
       PK_TS(20);
-      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+#pragma unroll 1
+      for (int64_t j0 = threadIdx.x; j0 < n; j0 += 4 * PK_THREADS)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // 4 independent elements in flight per thread
+        const int64_t j = j0 + u * PK_THREADS;
+        if (j >= n) break;
         const double h2 = IN(0)[j] + IN(1)[j];
         const double ax = (IN(2)[j] + mu2 * IN(3)[j]) + sy[j] * bb;
         xa[j] = h2 - ax;
-        xb[j] = IN(1)[j] / mu2;
+        xb[j] = mu2_one ? IN(1)[j] : IN(1)[j] / mu2;
         ytz += sy[j] * IN(2)[j];
         if (j >= i0 && j < i1) D.h2[j] = h2;
       }
@@ -563,7 +583,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         if (!S.reuse) {
           S.double_count += 1;
           S.s2 = ynorm * t2;
-          S.coef = (t[1] + (-S.s2)) / D.S->ys;
+          S.coef = (t[1] + (-S.s2)) / ys;
         }
         if (blockIdx.x == 0) D.hist[(int64_t)k * HIST_W + H_REUSE] = S.reuse ? 1.0 : 0.0;
       }
@@ -582,13 +602,18 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       double yv = 0.0;
       const double coef = S.coef;
       wait_in();  // slots: rho, x_bar, h, dr, g' (no-sgs: rho, x_bar)
-      for (int64_t j = threadIdx.x; j < n; j += PK_THREADS) {
+#pragma unroll 1
+      for (int64_t j0 = threadIdx.x; j0 < n; j0 += 4 * PK_THREADS)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // 4 independent elements in flight per thread
+        const int64_t j = j0 + u * PK_THREADS;
+        if (j >= n) break;
         double wj;
         if (reuse) {
           wj = IN(1)[j];
         } else {
           const double v = IN(4)[j] - coef * sjy[j];
-          wj = (IN(2)[j] + IN(3)[j]) / mu2 - v / mu2;
+          wj = mu2_one ? (IN(2)[j] + IN(3)[j]) - v : (IN(2)[j] + IN(3)[j]) / mu2 - v / mu2;
           yv += sy[j] * v;
         }
         const double gj = wj - IN(0)[j] / (sig * mu);

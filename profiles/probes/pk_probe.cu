@@ -131,11 +131,78 @@ __device__ double reduce_phase(double* part, int slot, double x, double* red, cg
   return o;
 }
 
+// two rows per warp sharing the x loads; NX right-hand sides
+template <int U, int NX>
+__device__ void rowdot2(const double* r0, const double* r1, int n, const double* x, double* o) {
+  const int lane = threadIdx.x & 31;
+  double a0[NX], a1[NX];
+  for (int v = 0; v < NX; ++v) a0[v] = a1[v] = 0;
+  for (int j0 = 2 * lane; j0 < n + 2 * lane; j0 += U * 64) {
+    double2 z0[U], z1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int j = j0 + u * 64;
+      z0[u] = j < n ? __ldg(reinterpret_cast<const double2*>(r0 + j)) : make_double2(0, 0);
+      z1[u] = j < n ? __ldg(reinterpret_cast<const double2*>(r1 + j)) : make_double2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int j = j0 + u * 64;
+      if (j < n) {
+#pragma unroll
+        for (int v = 0; v < NX; ++v) {
+          double2 xv = *reinterpret_cast<const double2*>(x + v * 2048 + j);
+          a0[v] += z0[u].x * xv.x + z0[u].y * xv.y;
+          a1[v] += z1[u].x * xv.x + z1[u].y * xv.y;
+        }
+      }
+    }
+  }
+  for (int v = 0; v < NX; ++v) {
+#pragma unroll
+    for (int q = 16; q; q >>= 1) {
+      a0[v] += __shfl_xor_sync(0xffffffffu, a0[v], q);
+      a1[v] += __shfl_xor_sync(0xffffffffu, a1[v], q);
+    }
+    o[v] = a0[v] + a1[v];
+  }
+}
+template <int U, int NX>
+__device__ void rowdot1(const double* r0, int n, const double* x, double* o) {
+  const int lane = threadIdx.x & 31;
+  double a0[NX];
+  for (int v = 0; v < NX; ++v) a0[v] = 0;
+  for (int j0 = 2 * lane; j0 < n + 2 * lane; j0 += U * 64) {
+    double2 z0[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int j = j0 + u * 64;
+      z0[u] = j < n ? __ldg(reinterpret_cast<const double2*>(r0 + j)) : make_double2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int j = j0 + u * 64;
+      if (j < n) {
+#pragma unroll
+        for (int v = 0; v < NX; ++v) {
+          double2 xv = *reinterpret_cast<const double2*>(x + v * 2048 + j);
+          a0[v] += z0[u].x * xv.x + z0[u].y * xv.y;
+        }
+      }
+    }
+  }
+  for (int v = 0; v < NX; ++v) {
+#pragma unroll
+    for (int q = 16; q; q >>= 1) a0[v] += __shfl_xor_sync(0xffffffffu, a0[v], q);
+    o[v] = a0[v];
+  }
+}
+
 __global__ void __launch_bounds__(512, 1) probe(Args A) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = threadIdx.x; j < A.n + 2; j += blockDim.x) sm[j] = 1.0;
+  for (int j = threadIdx.x; j < 3 * 2048; j += blockDim.x) sm[j] = 1.0;
   __syncthreads();
   const int n = A.n;
   double acc = 0;
@@ -144,7 +211,26 @@ __global__ void __launch_bounds__(512, 1) probe(Args A) {
   const int i0 = (long)n * blockIdx.x / gridDim.x, i1 = (long)n * (blockIdx.x + 1) / gridDim.x;
   for (int p = 0; p < A.phases; ++p) {
     const double* K = (p & 1) ? A.K1 : A.K0;
-    if (A.sweep) {
+    if (A.sweep >= 100) {  // 100 + 10*pairs + NX
+      const int pairs = (A.sweep / 10) % 10, nx = A.sweep % 10;
+      double o[3];
+      if (pairs) {
+        for (int r = 2 * warp; r < i1 - i0; r += 32) {
+          const double* r0 = K + (size_t)(i0 + r) * A.ld;
+          const double* r1 = r + 1 < i1 - i0 ? r0 + A.ld : r0;
+          if (nx == 1) rowdot2<8, 1>(r0, r1, n, sm, o);
+          else rowdot2<8, 3>(r0, r1, n, sm, o);
+          if (lane == 0) acc += o[0];
+        }
+      } else {
+        for (int r = warp; r < i1 - i0; r += 16) {
+          const double* r0 = K + (size_t)(i0 + r) * A.ld;
+          if (nx == 1) rowdot1<16, 1>(r0, n, sm, o);
+          else rowdot1<16, 3>(r0, n, sm, o);
+          if (lane == 0) acc += o[0];
+        }
+      }
+    } else if (A.sweep) {
       if (A.rows_split == 1) {
         for (int r = warp; r < i1 - i0; r += 16) {
           double d = A.sweep == 8 ? rowdot<8>(K + (size_t)(i0 + r) * A.ld, n, sm)
@@ -194,12 +280,9 @@ int main() {
   double* part;
   cudaMalloc(&part, 2 * 148 * 14 * 8);
   struct Cfg { const char* name; int sweep, custom, split, nred; } cfgs[] = {
-      {"grid.sync only", 0, 0, 1, 0}, {"custom barrier only", 0, 1, 1, 0}, {"sweep U16 + grid.sync", 16, 0, 1, 0},
-      {"sweep U8 + grid.sync", 8, 0, 1, 0}, {"sweep split2 + grid.sync", 16, 0, 2, 0},
-      {"sweep U16 + custom barrier", 16, 1, 1, 0},
-      {"reduce K=1 grid.sync", 0, 0, 1, 1}, {"reduce K=2 grid.sync", 0, 0, 1, 2}, {"reduce K=14 grid.sync", 0, 0, 1, 14},
-      {"reduce K=1 custom", 0, 1, 1, 1}, {"reduce K=14 custom", 0, 1, 1, 14},
-      {"sweep + reduce K=14", 16, 0, 1, 14}};
+      {"grid.sync only", 0, 0, 1, 0}, {"sweep U16 + grid.sync", 16, 0, 1, 0},
+      {"1 row/warp, 1 rhs", 101, 0, 1, 0}, {"2 rows/warp, 1 rhs", 111, 0, 1, 0},
+      {"1 row/warp, 3 rhs", 103, 0, 1, 0}, {"2 rows/warp, 3 rhs", 113, 0, 1, 0}};
   for (auto& c : cfgs) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemset(bar, 0, 4);
