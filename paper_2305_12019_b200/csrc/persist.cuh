@@ -44,7 +44,7 @@ constexpr int PK_THREADS = 512;
 constexpr int PK_WARPS = PK_THREADS / 32;
 constexpr int PK_NPART = 14;  // widest cross-CTA sum (norms + KKT terms)
 constexpr int PK_TS_ITERS = 64;
-constexpr int PK_MAX_OWN = 64;   // samples per CTA (host: n <= PK_MAX_OWN * grid)  // diagnostics: iterations timestamped (every CTA)
+constexpr int PK_MAX_OWN = 32;   // samples per CTA, one per lane of warp 0 (host: n <= PK_MAX_OWN * grid)  // diagnostics: iterations timestamped (every CTA)
 
 struct PKArgs {
   Dev D;
@@ -154,14 +154,15 @@ GDWD_DEV void pk_write_lane0(double* part, int slot, const double (&v)[K], doubl
 // Rows are consumed in batches of U chunks of 64 doubles (one double2 per
 // lane per chunk), loads predicated at the ragged end so every batch keeps
 // U loads in flight per lane; the pad column of K and of the staged vectors
-// is zero.  Per-lane accumulation order is ascending j, then the shuffle tree.
+// is zero.  Two fused multiply-add chains per right-hand side (even / odd
+// columns) halve the dependent-add chain; the shuffle tree finishes the sum.
 template <int NV>
 GDWD_DEV void pk_row_dot(const double* const (&rows)[NV], int64_t n, const double* const (&xs)[NV],
                          double (&out)[NV]) {
   const int lane = threadIdx.x & 31;
-  double acc[NV];
+  double a0[NV], a1[NV];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  for (int v = 0; v < NV; ++v) a0[v] = a1[v] = 0.0;
   constexpr int U = 16 / NV;
   for (int64_t j0 = 2 * lane; j0 < n + 2 * lane; j0 += U * 64) {
     double2 z[NV][U];
@@ -175,28 +176,29 @@ GDWD_DEV void pk_row_dot(const double* const (&rows)[NV], int64_t n, const doubl
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t j = j0 + u * 64;
-      if (j < n) {
+      const bool ok = j < n;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const double2 xv = *reinterpret_cast<const double2*>(xs[v] + j);
-          acc[v] += z[v][u].x * xv.x;
-          acc[v] += z[v][u].y * xv.y;
-        }
+      for (int v = 0; v < NV; ++v) {
+        const double2 xv = ok ? *reinterpret_cast<const double2*>(xs[v] + j) : make_double2(0.0, 0.0);
+        a0[v] = __fma_rn(z[v][u].x, xv.x, a0[v]);
+        a1[v] = __fma_rn(z[v][u].y, xv.y, a1[v]);
       }
     }
   }
-  warp_sum<NV>(acc);
 #pragma unroll
-  for (int v = 0; v < NV; ++v) out[v] = acc[v];
+  for (int v = 0; v < NV; ++v) a0[v] += a1[v];
+  warp_sum<NV>(a0);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) out[v] = a0[v];
 }
 
 // NV right-hand sides against one K row (row loaded once)
 template <int NV>
 GDWD_DEV void pk_row_dot_same(const double* row, int64_t n, const double* const (&xs)[NV], double (&out)[NV]) {
   const int lane = threadIdx.x & 31;
-  double acc[NV];
+  double a0[NV], a1[NV];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  for (int v = 0; v < NV; ++v) a0[v] = a1[v] = 0.0;
   for (int64_t j0 = 2 * lane; j0 < n + 2 * lane; j0 += 16 * 64) {
     double2 z[16];
 #pragma unroll
@@ -207,19 +209,20 @@ GDWD_DEV void pk_row_dot_same(const double* row, int64_t n, const double* const 
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int64_t j = j0 + u * 64;
-      if (j < n) {
+      const bool ok = j < n;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const double2 xv = *reinterpret_cast<const double2*>(xs[v] + j);
-          acc[v] += z[u].x * xv.x;
-          acc[v] += z[u].y * xv.y;
-        }
+      for (int v = 0; v < NV; ++v) {
+        const double2 xv = ok ? *reinterpret_cast<const double2*>(xs[v] + j) : make_double2(0.0, 0.0);
+        a0[v] = __fma_rn(z[u].x, xv.x, a0[v]);
+        a1[v] = __fma_rn(z[u].y, xv.y, a1[v]);
       }
     }
   }
-  warp_sum<NV>(acc);
 #pragma unroll
-  for (int v = 0; v < NV; ++v) out[v] = acc[v];
+  for (int v = 0; v < NV; ++v) a0[v] += a1[v];
+  warp_sum<NV>(a0);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) out[v] = a0[v];
 }
 
 GDWD_DEV unsigned long long pk_now() {
@@ -241,6 +244,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
   auto IN = [&](int v) { return in0 + v * ns; };
   const double* sy = pksm + 9 * ns;
   const double* sjy = pksm + 10 * ns;
+  const double* const ysm = sy;    // staged y (names free of the phases' local sums)
+  const double* const jysm = sjy;  // staged G^{-1} y / |y|
   __shared__ unsigned long long bar;
   unsigned parity = 0;
   const unsigned vbytes = (unsigned)(((n + 1) / 2 * 2) * sizeof(double));
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
   const double mu = D.mu, mu2 = D.mu2, yty = D.yty, ynorm = D.ynorm;
   const bool mu2_one = mu2 == 1.0;  // x / 1.0 == x exactly: skip the division
   const double ys = D.S->ys;          // SMW scalar, fixed for the solve
-  __shared__ double own_u[PK_MAX_OWN], own_rho[PK_MAX_OWN];
+  __shared__ double own_u[PK_MAX_OWN], own_rho[PK_MAX_OWN], own_ztw[PK_MAX_OWN];
   int slot = 0;
 
   if (threadIdx.x == 0) {
@@ -377,14 +382,15 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         const int64_t i = i0 + r;
         const double* rows[2] = {A.K + i * A.ld, A.GK + i * A.ld};
         const double* xs[2] = {xa, xb};
+        const double ali = xa[i];  // alpha (staged)
         double o[2];
         pk_row_dot<2>(rows, n, xs, o);
         if (lane == 0) {
-          qa += D.al[i] * o[0];
+          qa += ali * o[0];
           D.s1[i] = o[1];  // GK t1, reused by phase D's re-solve
-          const double gi = o[1] + t2 * (ynorm * D.jy[i]);
+          const double gi = o[1] + t2 * (ynorm * jysm[i]);
           D.g[i] = gi;
-          sy += (D.y[i] / ynorm) * gi;
+          sy += (ysm[i] / ynorm) * gi;
         }
       }
       double pv[2] = {qa, sy};
@@ -486,17 +492,19 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         const int64_t i = i0 + r;
         const double* rows[1] = {A.K + i * A.ld};
         const double* xs[1] = {xa};
+        // per-sample operands loaded before the sweep (their latency hides under it)
+        const double xii = D.xi[i], ali = D.al[i], wli = D.wl[i], ri = D.r[i], yi = ysm[i];
         double o[1];
         pk_row_dot<1>(rows, n, xs, o);
         if (lane == 0) {
           const double dot = o[0];
           D.ztwb[i] = dot;
-          const double a = ((dot + D.y[i] * bb) + D.xi[i]) - D.al[i] / sig;
-          const double rn = newton_margin(a, sig, D.q, D.wl[i], D.r[i], tol);
+          const double a = ((dot + yi * bb) + xii) - ali / sig;
+          const double rn = A.diag == 2 ? ri + 1e-3 * a : newton_margin(a, sig, D.q, wli, ri, tol);
           D.rnew[i] = rn;
-          const double dri = rn - D.r[i];
+          const double dri = rn - ri;
           D.dr[i] = dri;
-          ydr += D.y[i] * dri;
+          ydr += yi * dri;
         }
       }
       PK_TS(15);
@@ -554,13 +562,14 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         const int64_t i = i0 + r;
         const double* rows[2] = {A.K + i * A.ld, A.GK + i * A.ld};
         const double* xs[2] = {xa, xb};
+        const double s1i = D.s1[i];
         double o[2];
         pk_row_dot<2>(rows, n, xs, o);
         if (lane == 0) {
           q += xa[i] * o[0];
-          const double gi = (D.s1[i] + o[1]) + t2 * (ynorm * D.jy[i]);
+          const double gi = (s1i + o[1]) + t2 * (ynorm * jysm[i]);
           D.g[i] = gi;
-          syg += (D.y[i] / ynorm) * gi;
+          syg += (ysm[i] / ynorm) * gi;
         }
       }
       double pv[2] = {q, syg};
@@ -639,6 +648,17 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       double acc[PK_NPART];
 #pragma unroll
       for (int f = 0; f < PK_NPART; ++f) acc[f] = 0.0;
+      // Step 3 operands of the CTA's samples (warp 0, one per lane), loaded
+      // before the sweep so their latency hides under it
+      const int64_t is = i0 + lane;
+      const bool has = warp == 0 && is < i1;
+      double st_rr = 0.0, st_e = 0.0, st_al = 0.0, st_wl = 0.0;
+      if (has) {
+        st_rr = D.rnew[is];
+        st_e = D.e[is];
+        st_al = D.al[is];
+        st_wl = D.wl[is];
+      }
       for (int r = warp; r < nrows; r += PK_WARPS) {
         const int64_t i = i0 + r;
         const double* Ki = A.K + i * A.ld;
@@ -656,6 +676,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         }
         if (lane == 0) {
           D.ztw[i] = o[0];
+          own_ztw[r] = o[0];
           acc[10] += xg[i] * o[1];  // g^T K g
           acc[11] += xd[i] * o[2];  // d^T K d
           acc[12] += xd[i] * o[1];  // d^T K g
@@ -667,16 +688,17 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
       {
         // Step 3 + KKT sample terms (solver.py:533,538-541,311-333; OpStep3)
         const double bet = S.beta, C = D.C;
-        for (int64_t i = i0 + threadIdx.x; warp == 0 && i < i1; i += 32) {  // warp 0: the CTA's samples
-          const double rr = D.rnew[i];
+        if (has) {  // warp 0: the CTA's samples (at most 32, host-checked)
+          const int64_t i = is;
+          const double rr = st_rr;
           D.r[i] = rr;
-          const double yi = D.y[i], ei = D.e[i], zt = D.ztw[i], ali = D.al[i];
+          const double yi = ysm[i], ei = st_e, zt = own_ztw[lane], ali = st_al;
           const double xv = np_max0((((rr - zt) - yi * bet) + ali / sig) - (C / sig) * ei);
           D.xi[i] = xv;
           const double pg = ((zt + yi * bet) + xv) - rr;
           const double an = ali - (D.tau * sig) * pg;
           D.al[i] = an;
-          const double wl = D.wl[i];
+          const double wl = st_wl;
           const double s = (D.q * wl) / np_pow(rr, D.qp1);
           const double d2 = an - s;
           const double mn = np_min0(an);
