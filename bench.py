@@ -176,6 +176,25 @@ def kernel_bytes(tag: str, n: int, d: int, nnz: int | None = None) -> float | No
     return None
 
 
+def pinned_problem(G, prob):
+    """The same ProblemData with Z~'s stored values in page-locked host memory
+    (the e2e contract: inputs copied from pinned host buffers).  Built outside
+    the timed region; the library sees an ordinary numpy array."""
+    import torch
+
+    z = prob.z_tilde
+    if not torch.cuda.is_available():
+        return prob
+    buf = torch.empty(z.values.size, dtype=torch.float64, pin_memory=True).numpy()
+    buf[:] = z.values
+    if z.is_dense:
+        zp = G.SparseMatrixCSC.from_dense_samples(buf.reshape(z.ncols, z.nrows))
+    else:
+        zp = G.SparseMatrixCSC(z.nrows, z.ncols, z.colptr, z.rowidx, buf)
+    pinned_problem.keep = buf  # the pinned block lives as long as the run
+    return G.ProblemData(zp, prob.y, prob.e, prob.weights, prob.C, prob.q, prob.z_scale)
+
+
 def make_config(G, prob, iters):
     return G.SolverConfig(q=prob.q, max_iter=iters)
 
@@ -315,7 +334,7 @@ def run_b200(args, dist: Dist):
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                "note": "X generated in HBM (160 GB exceeds host memory); no host-buffer path"}
     elif not args.no_e2e:
-        prob2 = synth.make_problem(cfg_syn, args.seed)  # fresh host ProblemData: nothing resident
+        prob2 = pinned_problem(G, synth.make_problem(cfg_syn, args.seed))  # fresh host data: nothing resident
         conf2 = make_config(G, prob2, K)
         dist.barrier()
         t1 = time.perf_counter()
@@ -327,8 +346,8 @@ def run_b200(args, dist: Dist):
                "h2d_bytes_per_step": round(h2d / out.iterations), "d2h_bytes_per_step": round(d2h / out.iterations),
                "seconds": round(e2e_s, 4), "iterations": out.iterations,
                "breakdown": {k: round(v, 5) for k, v in (out.timings or {}).items()},
-               "note": "sgs_admm_solve from host numpy buffers: X upload, FP64 DMMA Gram + Cholesky inverse, "
-                       "iterations, state download"}
+               "note": "sgs_admm_solve from host numpy buffers (X in pinned host memory): X upload, FP64 DMMA "
+                       "Gram + Cholesky inverse, iterations, state download"}
         G.solver.device_problem(prob2, device).close()
 
     # ---- time to KKT 1e-5 (feasibility) from the device history ----------------

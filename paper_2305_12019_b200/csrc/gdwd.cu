@@ -487,6 +487,17 @@ __global__ void g_from_k_kernel(const double* K, double* G, int64_t n, int64_t l
   }
 }
 
+// G^{-1} K = G^{-1} mu^2 (G - I) = mu^2 (I - G^{-1}) for G = K / mu^2 + I:
+// the persistent loop's GK from the explicit inverse, elementwise.
+__global__ void gk_from_ginv_kernel(const double* Gi, double* GK, int64_t n, int64_t ld, double mu2) {
+  const int64_t tot = n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / n, j = idx % n;
+    const double v = (i == j ? 1.0 : 0.0) - Gi[i * ld + j];
+    GK[i * ld + j] = mu2 == 1.0 ? v : mu2 * v;
+  }
+}
+
 __global__ void fill_kernel(double* p, int64_t n, double v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
@@ -586,37 +597,42 @@ static void pk_timing_report(unsigned long long* ts, size_t tsn) {
                            "E arrive", "E release", "H arrive", "H release", "H staged", "H rows", "H step3",
                            "C staged", "C rows", "C scalars", "C writeback", "C waited", "C loop",
                            "D waited", "D staged", "", "", "A waited", "A loop", "A staged", "", "", "", "", ""};
-  double mn[NP] = {0}, md[NP] = {0}, mx[NP] = {0};
-  int cnt[NP] = {0};
+  // per-CTA SM-clock intervals between consecutive points (1.965 GHz), the
+  // median and the slowest CTA, averaged over iterations
+  const int order[] = {0, 24, 25, 26, 1, 2, 16, 17, 18, 19, 14, 15, 3, 4, 20, 21, 5, 6, 11, 12, 13, 9, 10};
+  const int no = sizeof(order) / sizeof(order[0]);
+  std::vector<double> sum_med(no, 0.0), sum_max(no, 0.0);
+  int cnt = 0;
   std::vector<double> v;
   for (int it = 1; it + 1 < PK_TS_ITERS; ++it) {
     const unsigned long long* r = &h[(size_t)it * NUM_SMS * NP];
-    unsigned long long t0 = ~0ull;
+    const unsigned long long* rn = &h[(size_t)(it + 1) * NUM_SMS * NP];
     bool ok = true;
-    for (int b = 0; b < NUM_SMS; ++b) {
-      if (!r[b * NP]) ok = false;
-      else t0 = std::min(t0, r[b * NP]);
-    }
+    for (int b = 0; b < NUM_SMS && ok; ++b)
+      for (int q = 0; q < no; ++q)
+        if (!r[b * NP + order[q]] || !rn[b * NP]) ok = false;
     if (!ok) break;
-    for (int pt = 0; pt < NP; ++pt) {
+    for (int q = 0; q < no; ++q) {
       v.clear();
-      for (int b = 0; b < NUM_SMS; ++b)
-        if (r[b * NP + pt]) v.push_back((double)(r[b * NP + pt] - t0));
-      if ((int)v.size() != NUM_SMS) continue;
+      for (int b = 0; b < NUM_SMS; ++b) {
+        const unsigned long long t0 = r[b * NP + order[q]];
+        const unsigned long long t1 = q + 1 < no ? r[b * NP + order[q + 1]] : rn[b * NP];
+        v.push_back((double)(long long)(t1 - t0) / 1965.0);
+      }
       std::sort(v.begin(), v.end());
-      mn[pt] += v.front();
-      md[pt] += v[v.size() / 2];
-      mx[pt] += v.back();
-      cnt[pt]++;
+      sum_med[q] += v[v.size() / 2];
+      sum_max[q] += v.back();
     }
+    cnt++;
   }
-  const int order[] = {0, 24, 25, 26, 1, 2, 16, 17, 18, 19, 14, 15, 3, 4, 20, 21, 5, 6, 7, 8, 11, 12, 13, 9, 10};
-  fprintf(stderr, "[pk timing] point        first    median    last   (us from iteration start)\n");
-  for (int pt : order) {
-    if (cnt[pt])
-      fprintf(stderr, "[pk timing] %-12s %8.2f %8.2f %8.2f (n=%d)\n", names[pt], mn[pt] / cnt[pt] / 1e3,
-              md[pt] / cnt[pt] / 1e3, mx[pt] / cnt[pt] / 1e3, cnt[pt]);
+  if (!cnt) return;
+  double tot = 0.0;
+  fprintf(stderr, "[pk timing] interval from point   median-CTA us   slowest-CTA us\n");
+  for (int q = 0; q < no; ++q) {
+    tot += sum_med[q] / cnt;
+    fprintf(stderr, "[pk timing] %-14s %10.2f %10.2f\n", names[order[q]], sum_med[q] / cnt, sum_max[q] / cnt);
   }
+  fprintf(stderr, "[pk timing] sum of medians %.2f us over %d iterations\n", tot, cnt);
 }
 
 extern "C" {
@@ -902,13 +918,41 @@ static int select_kind(int64_t n, int64_t d) {  // subsolvers.py:42-55
 }
 
 // One-time factorisation (cached per data generation / kind / mu^2).
+// Diagnostics (GDWD_SETUP_TIMING): stream-ordered marks through the setup,
+// printed as deltas when the solve begins.
+struct SetupTimer {
+  cudaStream_t st;
+  bool on;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  explicit SetupTimer(cudaStream_t s) : st(s), on(getenv("GDWD_SETUP_TIMING") != nullptr) { mark("start"); }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.emplace_back(name, e);
+  }
+  ~SetupTimer() {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+      fprintf(stderr, "[setup timing] %-22s %8.3f ms\n", ev[i].first, ms);
+    }
+    for (auto& p : ev) cudaEventDestroy(p.second);
+  }
+};
+
 static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
   if (ctx->fac_gen == ctx->data_gen && ctx->fac_kind == kind && ctx->fac_mu2 == mu2) return GDWD_OK;
   Dev& D = ctx->D;
   const int64_t n = ctx->n, d = ctx->d;
   MatView Z = zview(ctx);
+  SetupTimer T(ctx->st);
   if (kind == GDWD_BACKEND_DIRECT || kind == GDWD_BACKEND_SMW2) {
     RC(densify(ctx));
+    T.mark("densify");
     const int64_t m = (kind == GDWD_BACKEND_DIRECT) ? d + 1 : n;
     const int64_t ld = (m + 1) / 2 * 2;
     CK(ctx->fac.ensure((size_t)m * ld));
@@ -933,11 +977,14 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
       // zero pad columns: the persistent kernel's paired loads read them (times 0)
       CK(cudaMemsetAsync(ctx->kmat.p, 0, (size_t)m * ld * sizeof(double), ctx->st));
       CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, false, 1.0, 0.0, ctx->kmat.p, ld, ctx->facw.p, ctx->st));
+      T.mark("gram K = Z^T Z");
       g_from_k_kernel<<<vm_grid(m * m), 256, 0, ctx->st>>>(ctx->kmat.p, ctx->fac.p, m, ld, mu2);
       CK(cudaGetLastError());
+      T.mark("G = K/mu^2 + I");
     }
     CK(cudaMemsetAsync(ctx->dinfo, 0, sizeof(int), ctx->st));
     CK(chol_inverse(ctx->fac.p, ctx->facw.p, ctx->facw.p + (size_t)m * ld, ld, m, ctx->dinfo, ctx->st));
+    T.mark("cholesky inverse");
     int info = 0;
     CK(cudaMemcpyAsync(&info, ctx->dinfo, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
@@ -945,15 +992,18 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
     ctx->ldm = ld;
     ctx->fac_rows = m;
     if (kind == GDWD_BACKEND_SMW2) {
-      // GK = G^{-1} K for the persistent Gram-space loop (K symmetric)
+      // GK = G^{-1} K for the persistent Gram-space loop, = mu^2 (I - G^{-1})
       CK(ctx->gkmat.ensure((size_t)m * ld));
       CK(cudaMemsetAsync(ctx->gkmat.p, 0, (size_t)m * ld * sizeof(double), ctx->st));
-      CK(gemm_f64(ctx->fac.p, ld, 1, ctx->kmat.p, ld, 1, m, m, m, 1.0, 0.0, ctx->gkmat.p, ld, ctx->st));
+      gk_from_ginv_kernel<<<vm_grid(m * m), 256, 0, ctx->st>>>(ctx->fac.p, ctx->gkmat.p, m, ld, mu2);
+      CK(cudaGetLastError());
+      T.mark("GK = mu^2 (I - G^-1)");
       OpJyG op{ctx->y.p, D.ynorm, const_cast<double*>(D.jy), ctx->S};
       RC(ensure_scratch(ctx, m, m));
       run_zt(ctx, op, MatView{ctx->fac.p, m, m, ld});
       CK(cudaGetLastError());
       RC(ensure_scratch(ctx, n, d));
+      T.mark("G^-1 y");
     }
   } else {
     if (Z.a && n >= 65536) {

@@ -351,7 +351,9 @@ cudaError_t chol_inverse(double* A, double* Li, double* T, int64_t ld, int64_t m
   zero_kernel<<<grid_for(m * m), 256, 0, st>>>(Li, m, m, ld);
   cudaError_t e = chol_rec(A, Li, T, ld, m, 0, info, st);
   if (e != cudaSuccess) return e;
-  // A^{-1} = Li^T Li : C(i,j) = sum_k Li[k][i] Li[k][j]
+  // A^{-1} = Li^T Li : C(i,j) = sum_k Li[k][i] Li[k][j] -- symmetric: upper
+  // tiles on the DMMA SYRK path, mirrored (T is the workspace)
+  if (gram_slices(m, m) == 1) return gram_syrk(Li, m, m, ld, true, 1.0, 0.0, A, ld, T, st);
   return gemm_f64(Li, 1, ld, Li, 1, ld, m, m, m, 1.0, 0.0, A, ld, st);
 }
 

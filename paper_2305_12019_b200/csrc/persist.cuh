@@ -225,10 +225,8 @@ GDWD_DEV void pk_row_dot_same(const double* row, int64_t n, const double* const 
   for (int v = 0; v < NV; ++v) out[v] = a0[v];
 }
 
-GDWD_DEV unsigned long long pk_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
+GDWD_DEV unsigned long long pk_now() {  // SM cycle counter (exact intervals within a CTA)
+  return clock64();
 }
 
 __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
@@ -252,8 +250,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
   // Phase inputs are bulk-copied by thread 0 right after the grid barrier
   // that makes them final (overlapping the cross-CTA sum and the scalar
   // section); every issue is matched by exactly one wait of all threads.
+  // issued by lane 0 of the last warp, which takes no part in the cross-CTA
+  // sums that follow a barrier
   auto issue = [&](int cnt, const double* const* src, double* const* dst) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == PK_THREADS - 32) {
       fence_proxy_async_global();
       mbar_arrive_expect_tx(&bar, cnt * vbytes);
       for (int v = 0; v < cnt; ++v) bulk_g2s(dst[v], src[v], vbytes, &bar);
