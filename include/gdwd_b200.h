@@ -136,6 +136,24 @@ int gdwd_matvec(gdwd_ctx* ctx, const double* v_n, double* out_d);
 /* Z~^T v (scipy csr_matvec at solver.py:501,530,322; subsolvers.py:140)   */
 int gdwd_matvec_t(gdwd_ctx* ctx, const double* v_d, double* out_n);
 
+/* scoring a trained model (decision_values / predict / train_error,
+ * solver.py:610-642) over the uploaded samples X (raw, d x n, as uploaded by
+ * gdwd_upload_dense / gdwd_upload_csc): scores = beta + X^T w, w of the
+ * uploaded length d (callers pad or truncate the composite weights, as
+ * decision_values does).  scores (n) may be NULL.  If y (n) is not NULL,
+ * *wrong receives the number of samples with y_i * sgn(score_i) <= 0 (a zero
+ * score counts as wrong for both classes).  One fused pass over X. */
+int gdwd_score(gdwd_ctx* ctx, const double* w, double beta, const double* y, double* scores, int64_t* wrong);
+
+/* the distance statistic of compute_penalty_C (solver.py:193-232): over the
+ * uploaded raw samples, the median Euclidean distance between the samples
+ * ia[0..na) and ib[0..nb) (the two classes after the caller's seeded
+ * subsampling, solver.py:208-213), exact-zero distances dropped; Gram on the
+ * FP64 tensor cores, exact median by radix selection.  *positives receives
+ * the number of positive distances (0: all zero, *median = 0). */
+int gdwd_between_class_median(gdwd_ctx* ctx, const int64_t* ia, int64_t na, const int64_t* ib, int64_t nb,
+                              double* median, int64_t* positives);
+
 /* the solver ----------------------------------------------------------------
  * sgs_admm_solve (solver.py:392-602).  sigma_schedule (nullable, test hook):
  * sigma of iteration k for 1 <= k < sched_len replaces update_sigma. */

@@ -696,7 +696,68 @@ def solve(prob, cfg: OracleConfig, operator: str = "csc",
                         timed_iters=(st["iter"] - time_after) if t_mark is not None else st["iter"])
 
 
+# ---------------------------------------------------------------------------
+# Penalty parameter (solver.py:190-232)
+# ---------------------------------------------------------------------------
+def penalty_C(x_csc, y, q, seed=0, limit=2000):
+    """solver.py:193-232: C from the median between-class distance; classes
+    subsampled (default_rng(seed).choice, sorted) beyond `limit`; exact zero
+    distances dropped.  Returns (C, dist)."""
+    y = np.asarray(y, dtype=np.float64)
+    n = y.size
+    pos = np.flatnonzero(y > 0)
+    neg = np.flatnonzero(y < 0)
+    if pos.size == 0 or neg.size == 0:
+        raise ValueError("single class")
+    rng = np.random.default_rng(seed)
+    if pos.size > limit:
+        pos = np.sort(rng.choice(pos, limit, replace=False))
+    if neg.size > limit:
+        neg = np.sort(rng.choice(neg, limit, replace=False))
+    a = x_csc[:, pos]
+    b = x_csc[:, neg]
+    sq_a = np.asarray(a.multiply(a).sum(axis=0)).ravel()
+    sq_b = np.asarray(b.multiply(b).sum(axis=0)).ravel()
+    d2 = sq_a[:, None] + sq_b[None, :] - 2.0 * (a.T @ b).toarray()
+    np.maximum(d2, 0.0, out=d2)
+    dists = np.sqrt(d2.ravel())
+    dists = dists[dists > 0.0]
+    if dists.size == 0:
+        raise ValueError("all between-class distances are zero")
+    dist = float(np.median(dists))
+    c = 10.0 ** (q + 1.0) * max(1.0, 10.0 ** (q - 1.0) * math.log(n) * max(1000.0, float(x_csc.shape[0]))
+                                ** (1.0 / 3.0) / dist ** (q + 1.0))
+    return c, dist
+
+
+# ---------------------------------------------------------------------------
+# Applying a model (solver.py:610-642)
+# ---------------------------------------------------------------------------
+def decision_values(w_composite, beta, x_csc):
+    """solver.py:610-629: beta + x^T w with the weights padded with zeros or
+    cut to the input dimension (x: scipy CSC, features x samples)."""
+    d_in, d_tr = x_csc.shape[0], w_composite.size
+    if d_in == d_tr:
+        w_eff = w_composite
+    elif d_in > d_tr:
+        w_eff = np.concatenate([w_composite, np.zeros(d_in - d_tr)])
+    else:
+        w_eff = w_composite[:d_in]
+    return beta + x_csc.T @ w_eff
+
+
+def predict(w_composite, beta, x_csc):
+    """solver.py:632-636: where(score > 0, +1, -1) (zero -> -1, as the code does)."""
+    return np.where(decision_values(w_composite, beta, x_csc) > 0.0, 1.0, -1.0)
+
+
+def train_error(w_composite, beta, x_csc, y):
+    """solver.py:639-642: y sign(score) <= 0 is wrong (zero scores included)."""
+    y = np.asarray(y, dtype=np.float64)
+    return 100.0 * float(np.mean(y * np.sign(decision_values(w_composite, beta, x_csc)) <= 0.0))
+
+
 __all__ = ["DirectSys", "KKT_FIELDS", "KrylovOut", "OracleConfig", "OracleResult", "ProxSys",
-           "SmwSys", "ZOp", "bisect_margin", "chol_apply", "chol_upper", "class_weights", "kkt",
-           "lanczos_topk", "newton_scalar", "newton_sweep", "psqmr", "select_backend", "sigma_rule",
-           "solve"]
+           "SmwSys", "ZOp", "bisect_margin", "penalty_C", "chol_apply", "chol_upper", "class_weights", "decision_values", "kkt",
+           "lanczos_topk", "newton_scalar", "newton_sweep", "predict", "psqmr", "select_backend", "sigma_rule",
+           "solve", "train_error"]

@@ -32,6 +32,8 @@ from .solver import (
     update_sigma,
 )
 from .sparse import SparseFormatError, SparseMatrixCSC, csc_from_dense, csc_from_triplets
+from .scoring import decision_values, predict, train_error
+from .penalty import compute_penalty_C
 
 __version__ = "0.1.0"
 
@@ -40,5 +42,6 @@ __all__ = [
     "LanczosConvergenceError", "ModelFile", "ProblemData", "SingleClassError", "SolveResult", "SolverConfig",
     "SolverKind", "SolverState", "SparseFormatError", "SparseMatrixCSC", "compute_weights", "csc_from_dense",
     "csc_from_triplets", "device_problem", "identity_meta", "matvec", "newton_r", "newton_r_sweep",
-    "scale_problem", "select_solver", "sgs_admm_solve", "update_sigma",
+    "scale_problem", "select_solver", "sgs_admm_solve", "update_sigma", "decision_values", "predict",
+    "train_error", "compute_penalty_C",
 ]

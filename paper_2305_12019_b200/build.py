@@ -20,7 +20,8 @@ HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libgdwd_b200.so"
 SOURCES = ["gdwd.cu", "gram.cu"]
-HEADERS = ["common.cuh", "zops.cuh", "solver_ops.cuh", "gram.cuh", "spops.cuh", "persist.cuh"]
+HEADERS = ["common.cuh", "zops.cuh", "solver_ops.cuh", "gram.cuh", "spops.cuh", "persist.cuh", "synth.cuh",
+           "select.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -28,6 +28,7 @@
 #include "gram.cuh"
 #include "solver_ops.cuh"
 #include "spops.cuh"
+#include "select.cuh"
 #include "persist.cuh"
 #include "synth.cuh"
 #include "zops.cuh"
@@ -903,6 +904,104 @@ int gdwd_matvec_t(gdwd_ctx* ctx, const double* v_d, double* out_n) {
   CK(cudaStreamSynchronize(ctx->st));
   cudaFree(dv);
   cudaFree(dout);
+  return GDWD_OK;
+}
+
+int gdwd_score(gdwd_ctx* ctx, const double* w, double beta, const double* y, double* scores, int64_t* wrong) {
+  if (!ctx || !(ctx->has_dense || ctx->has_sparse) || !w)
+    return set_err(ctx, GDWD_ERR_VALUE, "score: no data or null weights");
+  if (y && !wrong) return set_err(ctx, GDWD_ERR_VALUE, "score: y given without a count output");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t n = ctx->n, d = ctx->d;
+  // [w (d) | scores (n) | y (n) | count]
+  double* buf = nullptr;
+  CK(cudaMalloc(&buf, (size_t)(d + 2 * n + 2) * sizeof(double)));
+  double *dw = buf, *dout = buf + d, *dy = buf + d + n, *dcnt = buf + d + 2 * n;
+  CK(cudaMemcpyAsync(dw, w, d * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  if (y) CK(cudaMemcpyAsync(dy, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  RC(ensure_scratch(ctx, n, d));
+  const int comm_mode = ctx->comm_mode;
+  ctx->comm_mode = 0;  // local samples only
+  OpScore op{dw, beta, y ? dy : nullptr, scores ? dout : nullptr, dcnt};
+  run_zt(ctx, op, zview(ctx), "ztmv_score");
+  ctx->comm_mode = comm_mode;
+  CK(cudaGetLastError());
+  double cnt = 0.0;
+  if (scores) CK(cudaMemcpyAsync(scores, dout, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  if (y) CK(cudaMemcpyAsync(&cnt, dcnt, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  cudaFree(buf);
+  if (wrong) *wrong = y ? (int64_t)cnt : 0;
+  return GDWD_OK;
+}
+
+int gdwd_between_class_median(gdwd_ctx* ctx, const int64_t* ia, int64_t na, const int64_t* ib, int64_t nb,
+                              double* median, int64_t* positives) {
+  if (!ctx || !(ctx->has_dense || ctx->has_sparse) || !ia || !ib || !median || !positives || na < 1 || nb < 1)
+    return set_err(ctx, GDWD_ERR_VALUE, "between_class_median: bad arguments");
+  for (int64_t t = 0; t < na; ++t)
+    if (ia[t] < 0 || ia[t] >= ctx->n) return set_err(ctx, GDWD_ERR_VALUE, "sample index out of range");
+  for (int64_t t = 0; t < nb; ++t)
+    if (ib[t] < 0 || ib[t] >= ctx->n) return set_err(ctx, GDWD_ERR_VALUE, "sample index out of range");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t d = ctx->d, ldd = (d + 1) / 2 * 2, ldg = (nb + 1) / 2 * 2, tot = na * nb;
+  // [A (na x ldd) | B (nb x ldd) | G (na x ldg) | dist (tot) | sqa | sqb] + index / counter block
+  const size_t nd = (size_t)(na + nb) * ldd + (size_t)na * ldg + (size_t)tot + na + nb;
+  double* buf = nullptr;
+  CK(cudaMalloc(&buf, nd * sizeof(double)));
+  double *A = buf, *B = A + na * ldd, *Gm = B + nb * ldd, *dist = Gm + na * ldg, *sqa = dist + tot, *sqb = sqa + na;
+  int64_t* idx = nullptr;
+  CK(cudaMalloc(&idx, (size_t)(na + nb + 2 + 256 + 1) * sizeof(int64_t)));
+  int64_t *dia = idx, *dib = idx + na;
+  unsigned long long* state = reinterpret_cast<unsigned long long*>(idx + na + nb);
+  unsigned long long* hist = state + 2;
+  unsigned long long* zeros = hist + 256;
+  CK(cudaMemcpyAsync(dia, ia, na * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(dib, ib, nb * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemsetAsync(state, 0, (2 + 256 + 1) * sizeof(unsigned long long), ctx->st));
+  CK(cudaMemsetAsync(A, 0, (size_t)(na + nb) * ldd * sizeof(double), ctx->st));
+  if (ctx->has_dense) {
+    gather_rows_kernel<<<(unsigned)((na + 7) / 8), 256, 0, ctx->st>>>(ctx->Zs, ctx->ldz, dia, na, d, A, ldd);
+    gather_rows_kernel<<<(unsigned)((nb + 7) / 8), 256, 0, ctx->st>>>(ctx->Zs, ctx->ldz, dib, nb, d, B, ldd);
+  } else {
+    SpView S{ctx->csc_ptr, ctx->csc_idx, ctx->csc_val, ctx->n, d};
+    gather_csc_kernel<<<(unsigned)((na + 7) / 8), 256, 0, ctx->st>>>(S, dia, na, A, ldd);
+    gather_csc_kernel<<<(unsigned)((nb + 7) / 8), 256, 0, ctx->st>>>(S, dib, nb, B, ldd);
+  }
+  row_sq_kernel<<<(unsigned)((na + 7) / 8), 256, 0, ctx->st>>>(A, ldd, na, d, sqa);
+  row_sq_kernel<<<(unsigned)((nb + 7) / 8), 256, 0, ctx->st>>>(B, ldd, nb, d, sqb);
+  CK(cudaGetLastError());
+  CK(gemm_f64(A, ldd, 1, B, ldd, 1, na, nb, d, 1.0, 0.0, Gm, ldg, ctx->st));  // G = A B^T (DMMA)
+  between_dist_kernel<<<NUM_SMS * 8, 256, 0, ctx->st>>>(Gm, ldg, sqa, sqb, na, nb, dist, zeros);
+  CK(cudaGetLastError());
+  unsigned long long z = 0;
+  CK(cudaMemcpyAsync(&z, zeros, sizeof(z), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  const int64_t m = tot - (int64_t)z;
+  *positives = m;
+  *median = 0.0;
+  if (m > 0) {
+    // zeros are the smallest values, so the j-th positive is order statistic z + j
+    const int64_t ks[2] = {(int64_t)z + (m - 1) / 2, (int64_t)z + m / 2};
+    double v[2] = {0.0, 0.0};
+    for (int q = 0; q < (ks[0] == ks[1] ? 1 : 2); ++q) {
+      const unsigned long long st0[2] = {0ull, (unsigned long long)ks[q]};
+      CK(cudaMemcpyAsync(state, st0, sizeof(st0), cudaMemcpyHostToDevice, ctx->st));
+      for (int shift = 56; shift >= 0; shift -= 8) {
+        radix_hist_kernel<<<NUM_SMS * 4, 256, 0, ctx->st>>>(dist, tot, state, shift, hist);
+        radix_pick_kernel<<<1, 32, 0, ctx->st>>>(hist, state, shift);
+      }
+      CK(cudaGetLastError());
+      unsigned long long bits = 0;
+      CK(cudaMemcpyAsync(&bits, state, sizeof(bits), cudaMemcpyDeviceToHost, ctx->st));
+      CK(cudaStreamSynchronize(ctx->st));
+      memcpy(&v[q], &bits, sizeof(double));
+    }
+    // np.median: the middle value, or the mean of the two middle values
+    *median = (ks[0] == ks[1]) ? v[0] : (v[0] + v[1]) / 2.0;
+  }
+  cudaFree(buf);
+  cudaFree(idx);
   return GDWD_OK;
 }
 

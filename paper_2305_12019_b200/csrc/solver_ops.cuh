@@ -985,6 +985,29 @@ struct OpPlainZt {  // out = Z^T w
   GDWD_DEV void fin(const double (&)[NN]) const {}
 };
 
+// scores = beta + X^T w and the train-error count y sgn(score) <= 0
+// (solver.py:610-642; np.sign(0) = 0 counts as wrong, NaN never does)
+struct OpScore {
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = true;
+  const double* w;
+  double beta;
+  const double* y;  // nullable
+  double* out;      // nullable
+  double* wrong;    // device scalar (count as a double: exact below 2^53)
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV double wval(int64_t j) const { return w[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&na)[NN]) const {
+    const double s = beta + dot;
+    if (out) out[i] = s;
+    if (y) {
+      const double sg = s > 0.0 ? 1.0 : (s < 0.0 ? -1.0 : s);  // np.sign (0 and NaN pass through)
+      na[0] += (y[i] * sg <= 0.0) ? 1.0 : 0.0;
+    }
+  }
+  GDWD_DEV void fin(const double (&ns)[NN]) const { *wrong = ns[0]; }
+};
+
 struct OpJyG {  // jy = G^{-1} (y/|y|) ; ys = 1 + (y/|y|).jy - 1  (subsolvers.py:114-117)
   static constexpr int NN = 1;
   static constexpr bool HAS_FIN = true;

@@ -26,7 +26,7 @@ class SparseFormatError(ValueError):
 class SparseMatrixCSC:
     """Immutable CSC matrix; ``values[colptr[j]:colptr[j+1]]`` is column j."""
 
-    __slots__ = ("nrows", "ncols", "_colptr", "_rowidx", "values", "_dense", "_scipy")
+    __slots__ = ("nrows", "ncols", "_colptr", "_rowidx", "values", "_dense", "_scipy", "_device")
 
     def __init__(self, nrows: int, ncols: int, colptr, rowidx, values):
         self.nrows = int(nrows)
@@ -36,6 +36,7 @@ class SparseMatrixCSC:
         self.values = np.ascontiguousarray(values, dtype=np.float64)
         self._dense = False
         self._scipy = None
+        self._device = None  # scoring.DeviceMatrix cache
         cp = self._colptr
         if cp.shape != (self.ncols + 1,):
             raise SparseFormatError("colptr must have length ncols+1")
@@ -63,6 +64,7 @@ class SparseMatrixCSC:
         self._rowidx = None
         self._dense = self.nrows > 0
         self._scipy = None
+        self._device = None
         return self
 
     # -- reference fields --------------------------------------------------

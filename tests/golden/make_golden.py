@@ -40,6 +40,7 @@ from gdwd.linalg import SparseMatrixCSC as RefCSC  # noqa: E402
 from gdwd.linalg import cholesky_factorize, cholesky_solve, lanczos_topk, psqmr  # noqa: E402
 
 from paper_2305_12019_b200 import synth  # noqa: E402
+from make_golden_inputs import penalty_inputs  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 
@@ -206,6 +207,49 @@ def kats():
     print("kat.json written")
 
 
+def make_scoring():
+    """Reference decision_values / predict / train_error (solver.py:610-642)
+    on raw dense and sparse matrices, with models trained by the reference;
+    test matrices wider and narrower than the training dimension."""
+    out = {}
+    for tag, cfgname, d, n in (("dense", "c1", 60, 40), ("sparse", "c4", 3000, 500)):
+        cfg = synth.CONFIGS[cfgname].scaled(d=d, n=n)
+        x, y = synth.raw_data(cfg, 5)
+        rx = RefCSC(nrows=x.nrows, ncols=x.ncols, colptr=x.colptr, rowidx=x.rowidx, values=x.values)
+        tau = gdwd.compute_weights(y, cfg.q)
+        prob = gdwd.scale_problem(rx, y, None, cfg.C, cfg.q, tau=tau)
+        res = gdwd.sgs_admm_solve(prob, gdwd.SolverConfig(q=cfg.q, max_iter=60))
+        model = res.model
+        out[f"{tag}_w"] = model.w
+        out[f"{tag}_beta"] = model.beta
+        out[f"{tag}_y"] = y
+        out[f"{tag}_scores"] = gdwd.solver.decision_values(model, rx)
+        out[f"{tag}_pred"] = gdwd.predict(model, rx)
+        out[f"{tag}_err"] = gdwd.train_error(model, rx, y)
+        for extra, dd in (("wide", d + 7), ("narrow", d - 5)):
+            cfg2 = synth.CONFIGS[cfgname].scaled(d=dd, n=n // 2)
+            x2, y2 = synth.raw_data(cfg2, 6)
+            rx2 = RefCSC(nrows=x2.nrows, ncols=x2.ncols, colptr=x2.colptr, rowidx=x2.rowidx, values=x2.values)
+            out[f"{tag}_{extra}_scores"] = gdwd.solver.decision_values(model, rx2)
+            out[f"{tag}_{extra}_err"] = gdwd.train_error(model, rx2, y2)
+            out[f"{tag}_{extra}_d"] = dd
+        out[f"{tag}_n"] = n
+        out[f"{tag}_d"] = d
+    np.savez_compressed(OUT / "scoring.npz", **out)
+    print("scoring.npz:", {k: float(v) for k, v in out.items() if k.endswith("_err")})
+
+
+def make_penalty():
+    """Reference compute_penalty_C (solver.py:193-232) values."""
+    out = {}
+    for name, (x, y, q, seed) in penalty_inputs().items():
+        rx = RefCSC(nrows=x.nrows, ncols=x.ncols, colptr=x.colptr, rowidx=x.rowidx, values=x.values)
+        c, dist = gdwd.compute_penalty_C(rx, y, q, seed=seed)
+        out[name] = {"C": c, "dist": dist, "q": q, "seed": seed}
+    (OUT / "penalty.json").write_text(json.dumps(out, indent=1))
+    print("penalty.json:", out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
@@ -219,6 +263,10 @@ def main():
     for name, cfgname, d, n, backend, mi, full, var in VARIANTS:
         if a.only in (None, name, "variants"):
             run_case(name, cfgname, d, n, backend, mi, full, **var)
+    if a.only in (None, "scoring"):
+        make_scoring()
+    if a.only in (None, "penalty"):
+        make_penalty()
     if not a.quick and a.only in (None, "c1"):
         run_c1_full()
 
