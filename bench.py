@@ -334,6 +334,12 @@ def run_b200(args, dist: Dist):
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                "note": "X generated in HBM (160 GB exceeds host memory); no host-buffer path"}
     elif not args.no_e2e:
+        # one untimed end-to-end call first (a warm process: allocator pool,
+        # module loading), on its own copy that is then released
+        prob_w = pinned_problem(G, synth.make_problem(cfg_syn, args.seed))
+        G.sgs_admm_solve(prob_w, make_config(G, prob_w, min(K, 20)), device=device)
+        G.solver.device_problem(prob_w, device).close()
+        del prob_w
         prob2 = pinned_problem(G, synth.make_problem(cfg_syn, args.seed))  # fresh host data: nothing resident
         conf2 = make_config(G, prob2, K)
         dist.barrier()
@@ -365,6 +371,11 @@ def run_b200(args, dist: Dist):
                "solve_s_device": round((out3.setup_ms + out3.loop_ms) / 1e3, 4),
                "setup_ms": round(out3.setup_ms, 3)}
 
+    # ---- SURVEY 8(f) rows beside the path: scoring and the penalty-C statistic --
+    nxt = None
+    if not args.no_next and not on_device and dist.rank == 0:
+        nxt = measure_next_rows(G, prob, device, args)
+
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": dist.world, "steps": iters_timed,
         "warmup": W, "ms_per_step": round(step_ms, 5), "higher_is_better": True, "scaling": "weak",
@@ -378,9 +389,57 @@ def run_b200(args, dist: Dist):
                    "setup_ms": round(setup_ms, 3), "gen_s": round(gen_s, 2)},
         "roofline": roofline, "roofline_x_stream": roofline_x, "kernels": kernels[:12],
         "gpu_launches": int(launches.value),
-        "clocks": clk.summary(), "e2e": e2e, "time_to_kkt": ttk,
+        "clocks": clk.summary(), "e2e": e2e, "time_to_kkt": ttk, "next_rows": nxt,
     }
     return line
+
+
+def measure_next_rows(G, prob, device, args):
+    """decision_values / train_error (solver.py:610-642) and the penalty-C
+    distance statistic (solver.py:193-232) on the workload's matrix: device
+    time per call (host buffers in and out) and the oracle's on the host."""
+    import time as _t
+
+    from oracle import gdwd_oracle as O
+    from paper_2305_12019_b200 import ModelFile, identity_meta, scoring
+
+    x, y = prob.z_tilde, prob.y
+    w = np.random.default_rng(3).standard_normal(x.nrows) / np.sqrt(x.nrows)
+    model = ModelFile(q=prob.q, C=prob.C, z_scale=1.0, mu=1.0, feature_meta=identity_meta(x.nrows), w=w, beta=0.1)
+    dm = scoring.device_matrix(x, device)  # upload once (resident, like a served model's inputs)
+    scoring.train_error(model, x, y, device)
+    reps = 20
+    t = _t.perf_counter()
+    for _ in range(reps):
+        scoring.decision_values(model, x, device)
+    dev_s = (_t.perf_counter() - t) / reps
+    t = _t.perf_counter()
+    for _ in range(reps):
+        scoring.train_error(model, x, y, device)
+    dev_err_s = (_t.perf_counter() - t) / reps
+    xs = x.scipy
+    t = _t.perf_counter()
+    O.decision_values(w, 0.1, xs)
+    cpu_s = _t.perf_counter() - t
+    out = {"scoring": {"samples": x.ncols, "device_s_per_call": round(dev_s, 6),
+                       "device_samples_per_s": round(x.ncols / dev_s, 1),
+                       "train_error_s_per_call": round(dev_err_s, 6),
+                       "oracle_s_per_call": round(cpu_s, 6),
+                       "note": "matrix resident in HBM; w in and scores out through host buffers"}}
+    if x.ncols <= 20000:
+        G.compute_penalty_C(x, y, prob.q)
+        t = _t.perf_counter()
+        c, dist_ = G.compute_penalty_C(x, y, prob.q)
+        pen_s = _t.perf_counter() - t
+        pairs = int(min((y > 0).sum(), 2000) * min((y < 0).sum(), 2000))
+        pen = {"C": c, "dist": dist_, "device_s": round(pen_s, 5), "pairs": pairs, "oracle_s": None}
+        if pairs * x.nrows <= 2e9:  # the oracle's sparse between-class product is slow: bounded
+            t = _t.perf_counter()
+            O.penalty_C(xs, y, prob.q)
+            pen["oracle_s"] = round(_t.perf_counter() - t, 4)
+        out["penalty_C"] = pen
+    dm.close()
+    return out
 
 
 def run_cpu_oracle(args, K: int, W: int, label: str):
@@ -410,6 +469,7 @@ def main():
     ap.add_argument("--config", default=CONFIG_NAME)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the scoring / penalty-C measurements")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--kkt-iters", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=6)

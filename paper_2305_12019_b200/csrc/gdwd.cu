@@ -77,20 +77,42 @@ namespace {
 
 constexpr int NUM_SMS = 148;
 
+// Device memory comes from the device's default stream-ordered pool, whose
+// release threshold is raised at context creation: freed blocks stay
+// reserved, so repeated solves and fresh contexts (e2e: a new problem each
+// call) reuse memory without driver mapping calls.  The allocation is
+// complete when dmalloc returns (usable from any stream); frees are ordered
+// on the context's stream after the work that uses the block.
+static cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t st) {
+  cudaError_t e = cudaMallocAsync(p, std::max<size_t>(bytes, 16), st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return e;
+}
+static void dfree(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+static void keep_pool_reserved(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+  uint64_t thr = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+}
+
 struct DevBuf {
   double* p = nullptr;
   size_t n = 0;
+  cudaStream_t st = nullptr;  // the owning context's stream
   cudaError_t ensure(size_t cnt) {
     if (cnt <= n && p) return cudaSuccess;
-    if (p) cudaFree(p);
+    dfree(p, st);
     p = nullptr;
     n = 0;
-    cudaError_t e = cudaMalloc(&p, std::max<size_t>(cnt, 1) * sizeof(double));
+    cudaError_t e = dmalloc((void**)&p, std::max<size_t>(cnt, 1) * sizeof(double), st);
     if (e == cudaSuccess) n = cnt;
     return e;
   }
   void release() {
-    if (p) cudaFree(p);
+    dfree(p, st);
     p = nullptr;
     n = 0;
   }
@@ -400,8 +422,8 @@ static int ensure_scratch(gdwd_ctx* ctx, int64_t rows, int64_t cols) {
   CK(ctx->npart.ensure(std::max(npart, ctx->npart.n)));
   CK(ctx->tpart.ensure(std::max(tpart, ctx->tpart.n)));
   if (nt > ctx->ntickets) {
-    if (ctx->tickets) cudaFree(ctx->tickets);
-    CK(cudaMalloc(&ctx->tickets, nt * sizeof(unsigned)));
+    dfree(ctx->tickets, ctx->st);
+    CK(dmalloc((void**)&ctx->tickets, nt * sizeof(unsigned), ctx->st));
     CK(cudaMemset(ctx->tickets, 0, nt * sizeof(unsigned)));
     ctx->ntickets = nt;
   }
@@ -578,7 +600,7 @@ static int compute_fro2(gdwd_ctx* ctx, const double* a, int64_t rows, int64_t co
 static void free_sparse(gdwd_ctx* ctx) {
   for (void* p : {(void*)ctx->csc_ptr, (void*)ctx->csr_ptr, (void*)ctx->csc_idx, (void*)ctx->csr_idx,
                   (void*)ctx->csc_val, (void*)ctx->csr_val})
-    if (p) cudaFree(p);
+    dfree(p, ctx->st);
   ctx->csc_ptr = ctx->csr_ptr = nullptr;
   ctx->csc_idx = ctx->csr_idx = nullptr;
   ctx->csc_val = ctx->csr_val = nullptr;
@@ -649,6 +671,12 @@ int gdwd_ctx_create(int32_t device, gdwd_ctx** out) {
   ctx->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) {
+    keep_pool_reserved(device);
+    for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf})
+      b->st = ctx->st;
+  }
   if (e == cudaSuccess) e = cudaMalloc(&ctx->S, sizeof(Scal));
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->Sh, sizeof(Scal));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->dinfo, sizeof(int));
@@ -665,7 +693,7 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
-  if (ctx->Zs) cudaFree(ctx->Zs);
+  dfree(ctx->Zs, ctx->st);
   free_sparse(ctx);
   for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
                     &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf})
@@ -681,7 +709,7 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
     if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
     if (ctx->pin_ev[b]) cudaEventDestroy(ctx->pin_ev[b]);
   }
-  if (ctx->tickets) cudaFree(ctx->tickets);
+  dfree(ctx->tickets, ctx->st);
   if (ctx->S) cudaFree(ctx->S);
   if (ctx->Sh) cudaFreeHost(ctx->Sh);
   if (ctx->dinfo) cudaFree(ctx->dinfo);
@@ -694,9 +722,9 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
   CK(cudaSetDevice(ctx->device));
   free_sparse(ctx);
   const int64_t ld = (d + 1) / 2 * 2;
-  if (ctx->Zs) cudaFree(ctx->Zs);
+  dfree(ctx->Zs, ctx->st);
   ctx->Zs = nullptr;
-  CK(cudaMalloc(&ctx->Zs, (size_t)n * ld * sizeof(double)));
+  CK(dmalloc((void**)&ctx->Zs, (size_t)n * ld * sizeof(double), ctx->st));
   if (ld != d) CK(cudaMemsetAsync(ctx->Zs, 0, (size_t)n * ld * sizeof(double), ctx->st));
   RC(upload_rows(ctx, samples, d, n, ld));
   ctx->n = n;
@@ -741,16 +769,16 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
     }
   CK(cudaSetDevice(ctx->device));
   free_sparse(ctx);
-  if (ctx->Zs) cudaFree(ctx->Zs);
+  dfree(ctx->Zs, ctx->st);
   ctx->Zs = nullptr;
   ctx->has_dense = false;
   const size_t nz = (size_t)std::max<int64_t>(nnz, 1);
-  CK(cudaMalloc(&ctx->csc_ptr, (n + 1) * sizeof(int64_t)));
-  CK(cudaMalloc(&ctx->csr_ptr, (d + 1) * sizeof(int64_t)));
-  CK(cudaMalloc(&ctx->csc_idx, nz * sizeof(int)));
-  CK(cudaMalloc(&ctx->csr_idx, nz * sizeof(int)));
-  CK(cudaMalloc(&ctx->csc_val, nz * sizeof(double)));
-  CK(cudaMalloc(&ctx->csr_val, nz * sizeof(double)));
+  CK(dmalloc((void**)&ctx->csc_ptr, (n + 1) * sizeof(int64_t), ctx->st));
+  CK(dmalloc((void**)&ctx->csr_ptr, (d + 1) * sizeof(int64_t), ctx->st));
+  CK(dmalloc((void**)&ctx->csc_idx, nz * sizeof(int), ctx->st));
+  CK(dmalloc((void**)&ctx->csr_idx, nz * sizeof(int), ctx->st));
+  CK(dmalloc((void**)&ctx->csc_val, nz * sizeof(double), ctx->st));
+  CK(dmalloc((void**)&ctx->csr_val, nz * sizeof(double), ctx->st));
   CK(cudaMemcpy(ctx->csc_ptr, colptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->csr_ptr, rp.data(), (d + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
   if (nnz > 0) {
@@ -780,7 +808,7 @@ static int densify(gdwd_ctx* ctx) {
   CK(cudaMemGetInfo(&freeb, &totb));
   if ((double)n * ld * 8.0 > 0.8 * (double)freeb)
     return set_err(ctx, GDWD_ERR_UNSUPPORTED, "dense copy of the sparse matrix does not fit for this backend");
-  CK(cudaMalloc(&ctx->Zs, (size_t)n * ld * sizeof(double)));
+  CK(dmalloc((void**)&ctx->Zs, (size_t)n * ld * sizeof(double), ctx->st));
   CK(cudaMemsetAsync(ctx->Zs, 0, (size_t)n * ld * sizeof(double), ctx->st));
   SpView A{ctx->csc_ptr, ctx->csc_idx, ctx->csc_val, n, ctx->d};
   sp_densify_kernel<<<(unsigned)((n + 7) / 8), 256, 0, ctx->st>>>(A, ctx->Zs, ld);
@@ -796,10 +824,10 @@ int gdwd_generate_dense(gdwd_ctx* ctx, int32_t kind, uint64_t seed, int64_t d, i
   if (kind != 0) return set_err(ctx, GDWD_ERR_UNSUPPORTED, "only the two-Gaussian generator runs on the device");
   CK(cudaSetDevice(ctx->device));
   free_sparse(ctx);
-  if (ctx->Zs) cudaFree(ctx->Zs);
+  dfree(ctx->Zs, ctx->st);
   ctx->Zs = nullptr;
   const int64_t ld = (d + 1) / 2 * 2;
-  CK(cudaMalloc(&ctx->Zs, (size_t)n * ld * sizeof(double)));
+  CK(dmalloc((void**)&ctx->Zs, (size_t)n * ld * sizeof(double), ctx->st));
   if (ld != d) CK(cudaMemsetAsync(ctx->Zs, 0, (size_t)n * ld * sizeof(double), ctx->st));
   gen_gauss_kernel<<<NUM_SMS * 16, 256, 0, ctx->st>>>(ctx->Zs, ld, d, n, offset, seed, signal_k, shift);
   CK(cudaGetLastError());
@@ -877,16 +905,16 @@ int gdwd_matvec(gdwd_ctx* ctx, const double* v_n, double* out_d) {
   if (!ctx || !(ctx->has_dense || ctx->has_sparse) || !v_n || !out_d) return set_err(ctx, GDWD_ERR_VALUE, "matvec: no data or null pointer");
   CK(cudaSetDevice(ctx->device));
   double *dv = nullptr, *dout = nullptr;
-  CK(cudaMalloc(&dv, ctx->n * sizeof(double)));
-  CK(cudaMalloc(&dout, ctx->d * sizeof(double)));
+  CK(dmalloc((void**)&dv, ctx->n * sizeof(double), ctx->st));
+  CK(dmalloc((void**)&dout, ctx->d * sizeof(double), ctx->st));
   CK(cudaMemcpyAsync(dv, v_n, ctx->n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
   OpPlainZ op{dv, nullptr, dout, nullptr};
   run_zmv(ctx, op, zview(ctx));
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out_d, dout, ctx->d * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
-  cudaFree(dv);
-  cudaFree(dout);
+  dfree(dv, ctx->st);
+  dfree(dout, ctx->st);
   return GDWD_OK;
 }
 
@@ -894,16 +922,16 @@ int gdwd_matvec_t(gdwd_ctx* ctx, const double* v_d, double* out_n) {
   if (!ctx || !(ctx->has_dense || ctx->has_sparse) || !v_d || !out_n) return set_err(ctx, GDWD_ERR_VALUE, "matvec_t: no data or null pointer");
   CK(cudaSetDevice(ctx->device));
   double *dv = nullptr, *dout = nullptr;
-  CK(cudaMalloc(&dv, ctx->d * sizeof(double)));
-  CK(cudaMalloc(&dout, ctx->n * sizeof(double)));
+  CK(dmalloc((void**)&dv, ctx->d * sizeof(double), ctx->st));
+  CK(dmalloc((void**)&dout, ctx->n * sizeof(double), ctx->st));
   CK(cudaMemcpyAsync(dv, v_d, ctx->d * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
   OpPlainZt op{dv, dout};
   run_zt(ctx, op, zview(ctx));
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out_n, dout, ctx->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
-  cudaFree(dv);
-  cudaFree(dout);
+  dfree(dv, ctx->st);
+  dfree(dout, ctx->st);
   return GDWD_OK;
 }
 
@@ -915,7 +943,7 @@ int gdwd_score(gdwd_ctx* ctx, const double* w, double beta, const double* y, dou
   const int64_t n = ctx->n, d = ctx->d;
   // [w (d) | scores (n) | y (n) | count]
   double* buf = nullptr;
-  CK(cudaMalloc(&buf, (size_t)(d + 2 * n + 2) * sizeof(double)));
+  CK(dmalloc((void**)&buf, (size_t)(d + 2 * n + 2) * sizeof(double), ctx->st));
   double *dw = buf, *dout = buf + d, *dy = buf + d + n, *dcnt = buf + d + 2 * n;
   CK(cudaMemcpyAsync(dw, w, d * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
   if (y) CK(cudaMemcpyAsync(dy, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
@@ -930,7 +958,7 @@ int gdwd_score(gdwd_ctx* ctx, const double* w, double beta, const double* y, dou
   if (scores) CK(cudaMemcpyAsync(scores, dout, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
   if (y) CK(cudaMemcpyAsync(&cnt, dcnt, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
-  cudaFree(buf);
+  dfree(buf, ctx->st);
   if (wrong) *wrong = y ? (int64_t)cnt : 0;
   return GDWD_OK;
 }
@@ -948,10 +976,10 @@ int gdwd_between_class_median(gdwd_ctx* ctx, const int64_t* ia, int64_t na, cons
   // [A (na x ldd) | B (nb x ldd) | G (na x ldg) | dist (tot) | sqa | sqb] + index / counter block
   const size_t nd = (size_t)(na + nb) * ldd + (size_t)na * ldg + (size_t)tot + na + nb;
   double* buf = nullptr;
-  CK(cudaMalloc(&buf, nd * sizeof(double)));
+  CK(dmalloc((void**)&buf, nd * sizeof(double), ctx->st));
   double *A = buf, *B = A + na * ldd, *Gm = B + nb * ldd, *dist = Gm + na * ldg, *sqa = dist + tot, *sqb = sqa + na;
   int64_t* idx = nullptr;
-  CK(cudaMalloc(&idx, (size_t)(na + nb + 2 + 256 + 1) * sizeof(int64_t)));
+  CK(dmalloc((void**)&idx, (size_t)(na + nb + 2 + 256 + 1) * sizeof(int64_t), ctx->st));
   int64_t *dia = idx, *dib = idx + na;
   unsigned long long* state = reinterpret_cast<unsigned long long*>(idx + na + nb);
   unsigned long long* hist = state + 2;
@@ -1000,8 +1028,8 @@ int gdwd_between_class_median(gdwd_ctx* ctx, const int64_t* ia, int64_t na, cons
     // np.median: the middle value, or the mean of the two middle values
     *median = (ks[0] == ks[1]) ? v[0] : (v[0] + v[1]) / 2.0;
   }
-  cudaFree(buf);
-  cudaFree(idx);
+  dfree(buf, ctx->st);
+  dfree(idx, ctx->st);
   return GDWD_OK;
 }
 
