@@ -145,6 +145,13 @@ int gdwd_matvec_t(gdwd_ctx* ctx, const double* v_d, double* out_n);
  * score counts as wrong for both classes).  One fused pass over X. */
 int gdwd_score(gdwd_ctx* ctx, const double* w, double beta, const double* y, double* scores, int64_t* wrong);
 
+/* kkt_residuals (solver.py:311-340) of an iterate (r, xi, alpha: n; w, u: d;
+ * beta) for the uploaded problem: out11 = [eta_c1, eta_c2, eta_c3, eta_p1,
+ * eta_p2, eta_p3, eta_d1, eta_d2, eta_gap, obj_primal, obj_dual].
+ * GDWD_ERR_ASSERT if some r_i <= 0 (solver.py:319-320). */
+int gdwd_kkt_residuals(gdwd_ctx* ctx, const double* r, const double* xi, const double* alpha, const double* w,
+                       const double* u, double beta, double mu, double* out11);
+
 /* the distance statistic of compute_penalty_C (solver.py:193-232): over the
  * uploaded raw samples, the median Euclidean distance between the samples
  * ia[0..na) and ib[0..nb) (the two classes after the caller's seeded

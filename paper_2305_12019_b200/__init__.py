@@ -23,7 +23,10 @@ from .solver import (
     SolverState,
     compute_weights,
     device_problem,
+    dual_objective,
+    kkt_residuals,
     matvec,
+    primal_objective,
     newton_r,
     newton_r_sweep,
     scale_problem,
@@ -43,5 +46,5 @@ __all__ = [
     "SolverKind", "SolverState", "SparseFormatError", "SparseMatrixCSC", "compute_weights", "csc_from_dense",
     "csc_from_triplets", "device_problem", "identity_meta", "matvec", "newton_r", "newton_r_sweep",
     "scale_problem", "select_solver", "sgs_admm_solve", "update_sigma", "decision_values", "predict",
-    "train_error", "compute_penalty_C",
+    "train_error", "compute_penalty_C", "kkt_residuals", "primal_objective", "dual_objective",
 ]

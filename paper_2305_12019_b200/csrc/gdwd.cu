@@ -963,6 +963,54 @@ int gdwd_score(gdwd_ctx* ctx, const double* w, double beta, const double* y, dou
   return GDWD_OK;
 }
 
+int gdwd_kkt_residuals(gdwd_ctx* ctx, const double* r, const double* xi, const double* alpha, const double* w,
+                       const double* u, double beta, double mu, double* out11) {
+  if (!ctx || !ctx->has_problem) return set_err(ctx, GDWD_ERR_VALUE, "kkt_residuals: no problem uploaded");
+  if (!r || !xi || !alpha || !w || !u || !out11) return set_err(ctx, GDWD_ERR_VALUE, "kkt_residuals: null argument");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t n = ctx->n, d = ctx->d;
+  double* buf = nullptr;  // [r | xi | alpha (n each) | w | u (d each) | sums (13)]
+  CK(dmalloc((void**)&buf, (size_t)(3 * n + 2 * d + 16) * sizeof(double), ctx->st));
+  KktArgs K{buf, buf + n, buf + 2 * n, buf + 3 * n, buf + 3 * n + d, ctx->y.p, ctx->e.p, ctx->wl.p, beta, ctx->C,
+            ctx->q, ctx->q + 1.0, 1.0 / (ctx->q + 1.0), ctx->q / (ctx->q + 1.0), buf + 3 * n + 2 * d};
+  CK(cudaMemcpyAsync(buf, r, n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(buf + n, xi, n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(buf + 2 * n, alpha, n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(buf + 3 * n, w, d * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(buf + 3 * n + d, u, d * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  RC(ensure_scratch(ctx, n, d));
+  const int comm_mode = ctx->comm_mode;
+  ctx->comm_mode = 0;  // a local iterate
+  MatView Z = zview(ctx);
+  run_zt(ctx, OpKktZt{K}, Z, "ztmv_kkt");
+  run_zmv(ctx, OpKktZa{K}, Z, "zmv_kkt");
+  run_vm(ctx, OpKktD{K}, d, "vmap_kkt");
+  ctx->comm_mode = comm_mode;
+  CK(cudaGetLastError());
+  double t[13];
+  CK(cudaMemcpyAsync(t, K.out, sizeof(t), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  dfree(buf, ctx->st);
+  if (t[9] > 0.0) return set_err(ctx, GDWD_ERR_ASSERT, "margin iterate left the positive orthant");
+  // the reference's scalar assembly (solver.py:323-340)
+  const double C = ctx->C, oc = 1.0 + C, q = ctx->q;
+  const double kappa = (q + 1.0) / q * pow(q, 1.0 / (q + 1.0));
+  out11[0] = fabs(t[0]) / oc;
+  out11[1] = fabs(t[1]) / oc;
+  out11[2] = t[2] / oc;
+  out11[3] = sqrt(t[3]) / oc;
+  out11[4] = mu * sqrt(t[11]) / oc;
+  out11[5] = std::max(sqrt(t[12]) - ctx->zscale, 0.0) / oc;
+  out11[6] = sqrt(t[4]) / oc;
+  out11[7] = sqrt(t[5]) / oc;
+  const double op = t[6] + C * t[7];
+  const double od = kappa * t[8] - ctx->zscale * sqrt(t[10]);
+  out11[8] = fabs(op - od) / (1.0 + fabs(op) + fabs(od));
+  out11[9] = op;
+  out11[10] = od;
+  return GDWD_OK;
+}
+
 int gdwd_between_class_median(gdwd_ctx* ctx, const int64_t* ia, int64_t na, const int64_t* ib, int64_t nb,
                               double* median, int64_t* positives) {
   if (!ctx || !(ctx->has_dense || ctx->has_sparse) || !ia || !ib || !median || !positives || na < 1 || nb < 1)

@@ -985,6 +985,69 @@ struct OpPlainZt {  // out = Z^T w
   GDWD_DEV void fin(const double (&)[NN]) const {}
 };
 
+// kkt_residuals (solver.py:311-340) of a caller-supplied iterate, without
+// touching solver state.  Sample sums in the Z~^T w pass, ||Z~ alpha||^2 in
+// the Z~ alpha pass, the d-space norms in a map; out[0..13) receives
+// [y.a, xi.(Ce - a), |a - s|^2, |p|^2, |min(a,0)|^2, |max(a - Ce,0)|^2,
+//  sum wl / r^q, e.xi, sum wl^(1/(q+1)) max(a,0)^(q/(q+1)), #(r <= 0),
+//  ||Z~ a||^2, ||w - u||^2, ||w||^2].
+struct KktArgs {
+  const double *r, *xi, *al, *w, *u, *y, *e, *wl;
+  double beta, C, q, qp1, e1, e2;
+  double* out;
+};
+struct OpKktZt {
+  static constexpr int NN = 10;
+  static constexpr bool HAS_FIN = true;
+  KktArgs K;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV double wval(int64_t j) const { return K.w[j]; }
+  GDWD_DEV void row(int64_t i, double dot, double (&a)[NN]) const {
+    const double rr = K.r[i], xv = K.xi[i], an = K.al[i], yi = K.y[i], ei = K.e[i], wl = K.wl[i], C = K.C;
+    const double s = (K.q * wl) / np_pow(rr, K.qp1);
+    const double d2 = an - s;
+    const double pg = ((dot + K.beta * yi) + xv) - rr;
+    const double mn = np_min0(an), mx = np_max0(an - C * ei);
+    a[0] += yi * an;
+    a[1] += xv * (C * ei - an);
+    a[2] += d2 * d2;
+    a[3] += pg * pg;
+    a[4] += mn * mn;
+    a[5] += mx * mx;
+    a[6] += wl / np_pow(rr, K.q);
+    a[7] += ei * xv;
+    a[8] += np_pow(wl, K.e1) * np_pow(np_max0(an), K.e2);
+    a[9] += (rr <= 0.0) ? 1.0 : 0.0;
+  }
+  GDWD_DEV void fin(const double (&a)[NN]) const {
+#pragma unroll
+    for (int f = 0; f < NN; ++f) K.out[f] = a[f];
+  }
+};
+struct OpKktZa {  // ||Z~ alpha||^2
+  static constexpr int R = 1, NN = 1, ND = 1;
+  KktArgs K;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV void input(int64_t i, double (&t)[R], double (&)[NN]) const { t[0] = K.al[i]; }
+  GDWD_DEV void epi(int64_t, const double (&v)[R], double (&da)[ND]) const { da[0] += v[0] * v[0]; }
+  GDWD_DEV void fin(const double (&)[NN], const double (&ds)[ND]) const { K.out[10] = ds[0]; }
+};
+struct OpKktD {  // ||w - u||^2, ||w||^2
+  static constexpr int NR = 2;
+  static constexpr bool HAS_FIN = true;
+  KktArgs K;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV void elem(int64_t j, double (&a)[NR]) const {
+    const double wj = K.w[j], dj = wj - K.u[j];
+    a[0] += dj * dj;
+    a[1] += wj * wj;
+  }
+  GDWD_DEV void fin(const double (&a)[NR]) const {
+    K.out[11] = a[0];
+    K.out[12] = a[1];
+  }
+};
+
 // scores = beta + X^T w and the train-error count y sgn(score) <= 0
 // (solver.py:610-642; np.sign(0) = 0 counts as wrong, NaN never does)
 struct OpScore {

@@ -394,6 +394,38 @@ def device_problem(data: ProblemData, device: Optional[int] = None) -> DevicePro
     return dev
 
 
+def kkt_residuals(state: SolverState, data: ProblemData, mu: float = 1.0) -> KKTResiduals:
+    """Normalized optimality residuals of an iterate (solver.py:311-340), on
+    the device: one Z~^T w pass with the sample sums, one Z~ alpha pass, one
+    d-space map; AssertionError if r left the positive orthant."""
+    dp = device_problem(data)
+    n, d = data.n, data.d
+    vec = {k: _lib.f64(getattr(state, k)) for k in ("r", "xi", "alpha", "w", "u")}
+    for k, v in vec.items():
+        if v.shape != ((n,) if k in ("r", "xi", "alpha") else (d,)):
+            raise ValueError(f"dimension mismatch: state.{k} has shape {v.shape}")
+    out = np.empty(11)
+    _check(dp.lib.gdwd_kkt_residuals(dp.ctx, _lib.ptr(vec["r"]), _lib.ptr(vec["xi"]), _lib.ptr(vec["alpha"]),
+                                     _lib.ptr(vec["w"]), _lib.ptr(vec["u"]), float(state.beta), float(mu),
+                                     _lib.ptr(out)), dp.ctx, "kkt_residuals")
+    return KKTResiduals(*[float(v) for v in out])
+
+
+def primal_objective(data: ProblemData, r: np.ndarray, xi: np.ndarray) -> float:
+    """sum w / r^q + C e.xi (solver.py:306-308), from the device KKT pass."""
+    z_n, z_d = np.zeros(data.n), np.zeros(data.d)
+    st = SolverState(r, xi, z_n, z_d, z_d, z_d, 0.0, 1.0, 0, 0.0)
+    return kkt_residuals(st, data).obj_primal
+
+
+def dual_objective(data: ProblemData, alpha: np.ndarray) -> float:
+    """kappa sum w^(1/(q+1)) max(a,0)^(q/(q+1)) - z_scale ||Z~ a||
+    (solver.py:291-303), from the device KKT pass."""
+    z_d = np.zeros(data.d)
+    st = SolverState(np.ones(data.n), np.zeros(data.n), alpha, z_d, z_d, z_d, 0.0, 1.0, 0, 0.0)
+    return kkt_residuals(st, data).obj_dual
+
+
 def _eps_c(data: ProblemData, config: SolverConfig) -> float:
     """solver.py:441-445.  NaN asks the library for the default
     1/max(1, ||Z~||_F), with the norm reduced on the device at upload."""

@@ -42,6 +42,19 @@ def objective_scales(prob, st, res):
     return [(sp + sd) / (1.0 + abs(res.obj_primal) + abs(res.obj_dual)), sp, sd]
 
 
+def residual_scales(prob, st, res):
+    """Magnitudes of the vectors each normalised residual is formed from
+    (the residuals are differences / thresholded sums that can cancel)."""
+    oc = 1 + prob.C
+    return ([np.abs(prob.y * st.alpha).sum() / oc,
+             (np.abs(st.xi) * (prob.C * prob.e + np.abs(st.alpha))).sum() / oc,
+             0.0,
+             (np.linalg.norm(st.r) + np.linalg.norm(st.xi) + abs(st.beta) * np.sqrt(prob.n)) / oc,
+             np.linalg.norm(st.w) / oc, np.linalg.norm(st.w) / oc,
+             np.linalg.norm(st.alpha) / oc, (np.linalg.norm(st.alpha) + prob.C * np.sqrt(prob.n)) / oc]
+            + objective_scales(prob, st, res))
+
+
 def run_traj(prob, cfg, full, idx_d=None, idx_n=None, **kw):
     rows, vecs = [], {k: [] for k in ("w", "u", "rho", "r", "xi", "alpha")}
     scales = []
@@ -50,14 +63,7 @@ def run_traj(prob, cfg, full, idx_d=None, idx_n=None, **kw):
         rows.append([getattr(res, f) for f in G.solver.KKT_FIELDS] + [st.sigma, st.beta])
         # magnitudes of the vectors each normalised residual is formed from
         # (the residuals are differences / thresholded sums that can cancel)
-        oc = 1 + prob.C
-        scales.append([np.abs(prob.y * st.alpha).sum() / oc,
-                       (np.abs(st.xi) * (prob.C * prob.e + np.abs(st.alpha))).sum() / oc,
-                       0.0,
-                       (np.linalg.norm(st.r) + np.linalg.norm(st.xi) + abs(st.beta) * np.sqrt(prob.n)) / oc,
-                       np.linalg.norm(st.w) / oc, np.linalg.norm(st.w) / oc,
-                       np.linalg.norm(st.alpha) / oc, (np.linalg.norm(st.alpha) + prob.C * np.sqrt(prob.n)) / oc]
-                      + objective_scales(prob, st, res))
+        scales.append(residual_scales(prob, st, res))
         for k in vecs:
             v = np.array(getattr(st, k), copy=True)
             if not full:
@@ -206,3 +212,28 @@ def test_lanczos_failure_raises_like_reference():
     cfg = G.SolverConfig(q=prob.q, max_iter=int(tr["max_iter"]), psqmr_switch_steps=int(tr["switch"]))
     with pytest.raises(G.LanczosConvergenceError):
         G.sgs_admm_solve(prob, cfg)
+
+
+@pytest.mark.parametrize("case", ["tiny_direct", "tiny_smw2", "tiny_iter", "var_q_half", "var_e_random",
+                                  "var_opts"])
+def test_kkt_residuals_of_reference_iterates(case):
+    """kkt_residuals (solver.py:311-340) on the device, applied to the
+    reference's own iterates, reproduces the residuals the reference recorded
+    for them."""
+    from conftest import solver_options
+
+    tr = load_traj(case)
+    prob = problem_for(tr)
+    mu = solver_options(tr).get("mu", 1.0)
+    for k in (0, 5, 19):
+        st = G.SolverState(tr["it_r"][k], tr["it_xi"][k], tr["it_alpha"][k], tr["it_w"][k], tr["it_u"][k],
+                           tr["it_rho"][k], float(tr["hist"][k, 12]), float(tr["hist"][k, 11]), k + 1, 0.0)
+        res = G.kkt_residuals(st, prob, mu)
+        got = np.array([getattr(res, f) for f in G.solver.KKT_FIELDS])
+        ref = tr["hist"][k, :11]
+        sc = np.array(residual_scales(prob, st, res))
+        assert np.all(np.abs(got - ref) <= 1e-12 * np.abs(ref) + 1e-12 * sc + 1e-14), (k, got - ref)
+    bad = G.SolverState(-tr["it_r"][0], tr["it_xi"][0], tr["it_alpha"][0], tr["it_w"][0], tr["it_u"][0],
+                        tr["it_rho"][0], 0.0, 1.0, 1, 0.0)
+    with pytest.raises(AssertionError):
+        G.kkt_residuals(bad, prob)
