@@ -161,6 +161,30 @@ int gdwd_kkt_residuals(gdwd_ctx* ctx, const double* r, const double* xi, const d
 int gdwd_between_class_median(gdwd_ctx* ctx, const int64_t* ia, int64_t na, const int64_t* ib, int64_t nb,
                               double* median, int64_t* positives);
 
+/* LIBSVM ingest (ingest.py:102-211), native and multi-threaded -----------------
+ * gdwd_libsvm_parse: parse a file (path) or an in-memory buffer (text, len)
+ * with the reference grammar; on a malformed line returns GDWD_ERR_VALUE with
+ * *err_line (1-based; 0 = "no samples in input") and the reference's message
+ * in err_msg.  Samples become CSC columns, exact zeros dropped; labels are
+ * NaN on unlabeled lines (label mapping to {-1,+1} is the caller's,
+ * ingest.py:90-99).  threads <= 0: all host cores. */
+typedef struct gdwd_libsvm gdwd_libsvm;
+int gdwd_libsvm_parse(const char* path, const char* text, int64_t text_len, int32_t require_labels,
+                      int32_t threads, gdwd_libsvm** out, int64_t* err_line, char* err_msg, int64_t err_cap);
+int gdwd_libsvm_sizes(const gdwd_libsvm* p, int64_t* n, int64_t* d, int64_t* nnz, int32_t* unlabeled);
+int gdwd_libsvm_copy(const gdwd_libsvm* p, int64_t* colptr, int64_t* rowidx, double* values, double* labels,
+                     int64_t* label_lines);
+void gdwd_libsvm_free(gdwd_libsvm* p);
+/* preprocess (ingest.py:185-211) of a CSC matrix: kept features (max-abs > 0)
+ * with their max-abs scales, entries divided by their feature's max-abs
+ * (zero quotients pruned) and rows renumbered.  Output capacities: kept_ids,
+ * scales: d; new_colptr: n + 1; new_rowidx, new_values: nnz (may be NULL to
+ * query *new_nnz).  GDWD_ERR_VALUE when every feature is zero
+ * (*kept_count = 0) or on a non-finite / out-of-range entry. */
+int gdwd_preprocess_csc(int64_t d, int64_t n, const int64_t* colptr, const int64_t* rowidx, const double* values,
+                        int32_t threads, int64_t* kept_count, int64_t* kept_ids, double* scales, int64_t* new_colptr,
+                        int64_t* new_rowidx, double* new_values, int64_t* new_nnz);
+
 /* the solver ----------------------------------------------------------------
  * sgs_admm_solve (solver.py:392-602).  sigma_schedule (nullable, test hook):
  * sigma of iteration k for 1 <= k < sched_len replaces update_sigma. */

@@ -37,6 +37,7 @@ from .solver import (
 from .sparse import SparseFormatError, SparseMatrixCSC, csc_from_dense, csc_from_triplets
 from .scoring import decision_values, predict, train_error
 from .penalty import compute_penalty_C
+from .ingest import ModelFormatError, ParseError, RawDataset, parse_libsvm, preprocess, read_model, write_model
 
 __version__ = "0.1.0"
 
@@ -46,5 +47,6 @@ __all__ = [
     "SolverKind", "SolverState", "SparseFormatError", "SparseMatrixCSC", "compute_weights", "csc_from_dense",
     "csc_from_triplets", "device_problem", "identity_meta", "matvec", "newton_r", "newton_r_sweep",
     "scale_problem", "select_solver", "sgs_admm_solve", "update_sigma", "decision_values", "predict",
-    "train_error", "compute_penalty_C", "kkt_residuals", "primal_objective", "dual_objective",
+    "train_error", "compute_penalty_C", "kkt_residuals", "primal_objective", "dual_objective", "ModelFormatError",
+    "ParseError", "RawDataset", "parse_libsvm", "preprocess", "read_model", "write_model",
 ]

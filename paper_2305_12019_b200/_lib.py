@@ -23,7 +23,8 @@ BACKEND_NAME = {v: k for k, v in BACKEND_CODE.items()}
 # exported symbols (checked by the CPU test-suite against include/gdwd_b200.h)
 SYMBOLS = [
     "gdwd_ctx_create", "gdwd_ctx_destroy", "gdwd_last_error", "gdwd_version", "gdwd_upload_dense",
-    "gdwd_upload_csc", "gdwd_set_problem", "gdwd_matvec", "gdwd_matvec_t", "gdwd_score", "gdwd_between_class_median", "gdwd_kkt_residuals", "gdwd_solve", "gdwd_get_state",
+    "gdwd_upload_csc", "gdwd_set_problem", "gdwd_matvec", "gdwd_matvec_t", "gdwd_score", "gdwd_between_class_median", "gdwd_kkt_residuals", "gdwd_libsvm_parse", "gdwd_libsvm_sizes",
+    "gdwd_libsvm_copy", "gdwd_libsvm_free", "gdwd_preprocess_csc", "gdwd_solve", "gdwd_get_state",
     "gdwd_get_history", "gdwd_newton_sweep", "gdwd_chol_inverse", "gdwd_gram", "gdwd_psqmr_dense",
     "gdwd_solve_begin", "gdwd_solve_iterate", "gdwd_solve_end", "gdwd_time_iterations", "gdwd_set_profile",
     "gdwd_get_profile", "gdwd_reset_counters", "gdwd_frobenius_sq", "gdwd_comm_unique_id",
@@ -80,6 +81,16 @@ def _declare(lib):
         "gdwd_matvec_t": (C.c_int, [vp, _P, _P]),
         "gdwd_score": (C.c_int, [vp, _P, C.c_double, _P, _P, C.POINTER(C.c_int64)]),
         "gdwd_kkt_residuals": (C.c_int, [vp, _P, _P, _P, _P, _P, C.c_double, C.c_double, _P]),
+        "gdwd_libsvm_parse": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int64, C.c_int32, C.c_int32, C.POINTER(vp),
+                                        C.POINTER(C.c_int64), C.c_char_p, C.c_int64]),
+        "gdwd_libsvm_sizes": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int32)]),
+        "gdwd_libsvm_copy": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P, _P,
+                                       C.POINTER(C.c_int64)]),
+        "gdwd_libsvm_free": (None, [vp]),
+        "gdwd_preprocess_csc": (C.c_int, [C.c_int64, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P,
+                                          C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P,
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P, C.POINTER(C.c_int64)]),
         "gdwd_between_class_median": (C.c_int, [vp, C.POINTER(C.c_int64), C.c_int64, C.POINTER(C.c_int64),
                                                 C.c_int64, _P, C.POINTER(C.c_int64)]),
         "gdwd_solve": (C.c_int, [vp, C.POINTER(GdwdConfig), _P, _I64, ITER_CB, vp, C.POINTER(GdwdResult)]),

@@ -19,14 +19,14 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libgdwd_b200.so"
-SOURCES = ["gdwd.cu", "gram.cu"]
+SOURCES = ["gdwd.cu", "gram.cu", "ingest.cpp"]
 HEADERS = ["common.cuh", "zops.cuh", "solver_ops.cuh", "gram.cuh", "spops.cuh", "persist.cuh", "synth.cuh",
            "select.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
-    "-Xcompiler", "-fPIC,-O2", "-shared", "-cudart", "shared",
+    "-Xcompiler", "-fPIC,-O2,-pthread", "-shared", "-cudart", "shared",
 ]
 
 

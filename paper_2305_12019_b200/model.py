@@ -1,7 +1,7 @@
 """Model records returned by the solver (reference ``ingest.py:39-87``).
 
-Only the types the solver's ``SolveResult`` carries are mirrored here;
-LIBSVM parsing and JSON model I/O are out of scope.
+The records the solver's ``SolveResult`` carries; LIBSVM parsing,
+preprocessing and the JSON model file are in ``ingest.py``.
 """
 
 from __future__ import annotations

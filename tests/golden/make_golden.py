@@ -40,7 +40,7 @@ from gdwd.linalg import SparseMatrixCSC as RefCSC  # noqa: E402
 from gdwd.linalg import cholesky_factorize, cholesky_solve, lanczos_topk, psqmr  # noqa: E402
 
 from paper_2305_12019_b200 import synth  # noqa: E402
-from make_golden_inputs import penalty_inputs  # noqa: E402
+from make_golden_inputs import LIBSVM_CASES, big_libsvm, penalty_inputs  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 
@@ -250,6 +250,41 @@ def make_penalty():
     print("penalty.json:", out)
 
 
+def make_ingest():
+    """Reference parse_libsvm / preprocess (ingest.py:102-211) outputs and
+    error messages on the LIBSVM_CASES texts and a large seeded text."""
+    import io
+
+    out = {}
+    for name, text, req in LIBSVM_CASES + [("big", big_libsvm(), True)]:
+        rec = {"require_labels": req}
+        try:
+            raw = gdwd.parse_libsvm(io.StringIO(text, newline=None), require_labels=req)
+        except gdwd.ParseError as exc:
+            rec["error"] = str(exc)
+            rec["line_no"] = exc.line_no
+            out[name] = rec
+            continue
+        x = raw.X
+        arrays = {"colptr": x.colptr, "rowidx": x.rowidx, "values": x.values}
+        rec.update({"n": x.ncols, "d": x.nrows, "nnz": int(x.values.size),
+                    "labels": None if raw.labels is None else raw.labels.tolist()})
+        try:
+            xc, _, meta = gdwd.preprocess(raw)
+            arrays.update({"pcolptr": xc.colptr, "prowidx": xc.rowidx, "pvalues": xc.values,
+                           "kept": meta.kept_ids, "scales": meta.scales})
+        except ValueError as exc:
+            rec["preprocess_error"] = str(exc)
+        if name == "big":
+            rec["sha"] = {k: hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest() for k, v in arrays.items()}
+            rec["labels"] = hashlib.sha256(np.asarray(raw.labels).tobytes()).hexdigest()
+        else:
+            rec.update({k: v.tolist() for k, v in arrays.items()})
+        out[name] = rec
+    (OUT / "ingest.json").write_text(json.dumps(out, indent=1))
+    print("ingest.json:", {k: v.get("error", v.get("n")) for k, v in out.items()})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
@@ -267,6 +302,8 @@ def main():
         make_scoring()
     if a.only in (None, "penalty"):
         make_penalty()
+    if a.only in (None, "ingest"):
+        make_ingest()
     if not a.quick and a.only in (None, "c1"):
         run_c1_full()
 
