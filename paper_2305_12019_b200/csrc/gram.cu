@@ -196,9 +196,11 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
     __syncthreads();
     for (int i = j + 1 + t; i < m; i += blockDim.x) L[i][j] = L[i][j] / L[j][j];
     __syncthreads();
-    for (int idx = t; idx < 64 * 64; idx += blockDim.x) {
-      int i = idx >> 6, k = idx & 63;
-      if (k > j && i >= k && i < m) L[i][k] -= L[i][j] * L[k][j];
+    // trailing lower triangle only: (i, k) with j < k <= i < m
+    const int w = m - j - 1;
+    for (int idx = t; idx < w * w; idx += blockDim.x) {
+      const int i = j + 1 + idx / w, k = j + 1 + idx % w;
+      if (k <= i) L[i][k] -= L[i][j] * L[k][j];
     }
     __syncthreads();
   }
@@ -306,16 +308,19 @@ cudaError_t gram_syrk(const double* Zs, int64_t R, int64_t Lc, int64_t ldz, bool
 
 namespace {
 
+#ifndef CHOL_LEAF
+#define CHOL_LEAF 32  // diagonal blocks factored by one CTA (<= 64); the recursion's critical path
+#endif
 // Recursive blocked Cholesky + triangular inverse (lower):
 //   A (m x m, ld) is overwritten by L; Li (ld) receives L^{-1}; T scratch.
 cudaError_t chol_rec(double* A, double* Li, double* T, int64_t ld, int64_t m, int64_t off, int* info,
                      cudaStream_t st) {
-  if (m <= 64) {
+  if (m <= CHOL_LEAF) {
     potrf_trtri_small<<<1, 256, 0, st>>>(A, ld, Li, ld, (int)m, info, off);
     return cudaGetLastError();
   }
-  int64_t m1 = ((m / 2) + 63) / 64 * 64;
-  if (m1 >= m) m1 = m - 64;
+  int64_t m1 = ((m / 2) + CHOL_LEAF - 1) / CHOL_LEAF * CHOL_LEAF;
+  if (m1 >= m) m1 = m - CHOL_LEAF;
   const int64_t m2 = m - m1;
   double* A11 = A;
   double* A21 = A + m1 * ld;
