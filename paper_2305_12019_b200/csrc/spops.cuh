@@ -26,6 +26,7 @@ struct SpView {
 };
 
 constexpr int SP_THREADS = 256;
+constexpr int SPU = 4;  // nonzeros per lane in flight in the gather loops
 
 // t_r[i] for all samples + n-sum partials (one partial per CTA)
 template <class Op>
@@ -70,27 +71,29 @@ __global__ void __launch_bounds__(SP_THREADS) sp_zmv_kernel(Op op, SpView A, con
     double acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
-    int64_t k = b + lane;
-    for (; k + 32 < e; k += 64) {  // two nnz per lane in flight
-      const double v0 = __ldg(A.val + k), v1 = __ldg(A.val + k + 32);
-      const int64_t c0 = __ldg(A.idx + k), c1 = __ldg(A.idx + k + 32);
-      double t0[R], t1[R];
+    // SPU nnz per lane in flight: all index / value loads of a batch, then
+    // all gathers, then the accumulation (lane order k, k+32, ... as before)
+    for (int64_t k0 = b + lane; k0 < e; k0 += 32 * SPU) {
+      double v[SPU];
+      int c[SPU];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        t0[r] = tbuf[c0 * R + r];
-        t1[r] = tbuf[c1 * R + r];
+      for (int u = 0; u < SPU; ++u) {  // clamped, not predicated: never past the row's end
+        const int64_t k = k0 + 32 * u, kk = k < e ? k : e - 1;
+        const double vv = __ldg(A.val + kk);
+        v[u] = k < e ? vv : 0.0;
+        c[u] = __ldg(A.idx + kk);
       }
+      double tg[SPU][R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        acc[r] += v0 * t0[r];
-        acc[r] += v1 * t1[r];
-      }
-    }
-    for (; k < e; k += 32) {
-      const double v = __ldg(A.val + k);
-      const int64_t c = __ldg(A.idx + k);
+      for (int u = 0; u < SPU; ++u)
 #pragma unroll
-      for (int r = 0; r < R; ++r) acc[r] += v * tbuf[c * R + r];
+        for (int r = 0; r < R; ++r) tg[u][r] = tbuf[(int64_t)c[u] * R + r];
+#pragma unroll
+      for (int u = 0; u < SPU; ++u)
+        if (k0 + 32 * u < e) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] += v[u] * tg[u][r];
+        }
     }
     warp_sum<R>(acc);
     if (lane == 0) {
@@ -145,7 +148,24 @@ __global__ void __launch_bounds__(SP_THREADS) sp_ztmv_kernel(Op op, SpView A, Sc
       double acc = 0.0;
       if (i < A.rows) {
         const int64_t b = A.ptr[i], e = A.ptr[i + 1];
-        for (int64_t k = b + sub; k < e; k += G) acc += __ldg(A.val + k) * op.wval(__ldg(A.idx + k));
+        // SPU entries per lane in flight: index / value loads, then gathers
+        for (int64_t k0 = b + sub; k0 < e; k0 += (int64_t)G * SPU) {
+          double v[SPU];
+          int c[SPU];
+#pragma unroll
+          for (int u = 0; u < SPU; ++u) {  // clamped, not predicated: never past the sample's end
+            const int64_t k = k0 + (int64_t)G * u, kk = k < e ? k : e - 1;
+            const double vv = __ldg(A.val + kk);
+            v[u] = k < e ? vv : 0.0;
+            c[u] = __ldg(A.idx + kk);
+          }
+          double wg[SPU];
+#pragma unroll
+          for (int u = 0; u < SPU; ++u) wg[u] = op.wval(c[u]);
+#pragma unroll
+          for (int u = 0; u < SPU; ++u)
+            if (k0 + (int64_t)G * u < e) acc += v[u] * wg[u];
+        }
       }
 #pragma unroll
       for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
