@@ -84,7 +84,9 @@ constexpr int NUM_SMS = 148;
 // complete when dmalloc returns (usable from any stream); frees are ordered
 // on the context's stream after the work that uses the block.
 static cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t st) {
-  cudaError_t e = cudaMallocAsync(p, std::max<size_t>(bytes, 16), st);
+  // + 512 B of slack: pool blocks are packed, and vector loads near the end
+  // of a ragged row may be issued speculatively
+  cudaError_t e = cudaMallocAsync(p, std::max<size_t>(bytes, 16) + 512, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   return e;
 }
