@@ -54,6 +54,9 @@ typedef struct {
   int32_t poll_every;         /* host polls the device stop flag every k iterations      */
   int32_t smw_gram_space;     /* SMW2 with n <= d: iterate in n-coefficient space, K = Z~^T Z~ */
   int32_t persistent;         /* Gram-space SMW2: run iterations in one cooperative kernel */
+  int32_t iter_gram;          /* ITERATIVE, dense: PSQMR operator A v from the d x d Gram
+                                 Z~ Z~^T (formed once on the FP64 tensor cores) instead of two
+                                 passes over X; 0 auto (d <= n/4 and it fits), 1 on, -1 off */
   double steplength;
   double tol_feas;
   double tol_cgap;

@@ -42,7 +42,7 @@ class GdwdConfig(C.Structure):
         ("max_iter", C.c_int32), ("backend", C.c_int32), ("use_sgs", C.c_int32),
         ("psqmr_switch_steps", C.c_int32), ("ell", C.c_int32), ("seed", C.c_int32),
         ("use_graph", C.c_int32), ("poll_every", C.c_int32), ("smw_gram_space", C.c_int32),
-        ("persistent", C.c_int32),
+        ("persistent", C.c_int32), ("iter_gram", C.c_int32),
         ("steplength", C.c_double), ("tol_feas", C.c_double), ("tol_cgap", C.c_double),
         ("tol_cap", C.c_double), ("sigma0", C.c_double), ("epsilon_c", C.c_double), ("mu", C.c_double),
     ]

@@ -213,6 +213,10 @@ struct gdwd_ctx {
   bool in_solve = false;
   int kind = 0, poll = 16, max_iter = 0, max_steps = 50, k_host = 0, psqmr_total = 0;
   bool use_sgs = true, stopped = false, gram = false, persistent = false;
+  bool iter_gram = false;  // ITERATIVE with the d x d Gram operator (gdmat)
+  DevBuf gdmat;
+  int64_t ldg = 0;
+  int fac_iter_gram = 0;
   DevBuf pk_part, gkmat;
   // proximal fallback (subsolvers.py:159-256)
   bool prox = false;
@@ -676,7 +680,7 @@ int gdwd_ctx_create(int32_t device, gdwd_ctx** out) {
   if (e == cudaSuccess) {
     keep_pool_reserved(device);
     for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat})
       b->st = ctx->st;
   }
   if (e == cudaSuccess) e = cudaMalloc(&ctx->S, sizeof(Scal));
@@ -698,7 +702,7 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   dfree(ctx->Zs, ctx->st);
   free_sparse(ctx);
   for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat})
     b->release();
   end_session(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1122,7 +1126,9 @@ struct SetupTimer {
 };
 
 static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
-  if (ctx->fac_gen == ctx->data_gen && ctx->fac_kind == kind && ctx->fac_mu2 == mu2) return GDWD_OK;
+  if (ctx->fac_gen == ctx->data_gen && ctx->fac_kind == kind && ctx->fac_mu2 == mu2 &&
+      ctx->fac_iter_gram == (int)ctx->iter_gram)
+    return GDWD_OK;
   Dev& D = ctx->D;
   const int64_t n = ctx->n, d = ctx->d;
   MatView Z = zview(ctx);
@@ -1198,11 +1204,22 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
     jacobi_kernel<<<(unsigned)((d + 256) / 256), 256, 0, ctx->st>>>(ctx->colsq.p, d, mu2, ctx->yty,
                                                                      const_cast<double*>(D.jac));
     CK(cudaGetLastError());
+    if (ctx->iter_gram) {
+      // PSQMR operator block Z~ Z~^T, once (sharded: local Gram, summed once)
+      const int64_t ld = (d + 1) / 2 * 2;
+      CK(ctx->gdmat.ensure((size_t)d * ld));
+      CK(ctx->facw.ensure((size_t)gram_workspace_doubles(d, n)));
+      CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, true, 1.0, 0.0, ctx->gdmat.p, ld, ctx->facw.p, ctx->st));
+      if (sharded(ctx)) allreduce(ctx, ctx->gdmat.p, d * ld);
+      ctx->ldg = ld;
+      T.mark("iterative Gram Z Z^T");
+    }
   }
   CK(cudaStreamSynchronize(ctx->st));
   ctx->fac_gen = ctx->data_gen;
   ctx->fac_kind = kind;
   ctx->fac_mu2 = mu2;
+  ctx->fac_iter_gram = (int)ctx->iter_gram;
   return GDWD_OK;
 }
 
@@ -1225,8 +1242,13 @@ static int psqmr_solve(gdwd_ctx* ctx, const double* b, const double* x0, double*
                        int max_steps, int* steps, int* conv, int* active_run) {
   const Dev& D = ctx->D;
   MatView Z = zview(ctx);
-  run_zt(ctx, OpApplyZt{D, x0, pred, 0}, Z, "ztmv_psqmr_init");
-  run_zmv(ctx, OpInitResidual{D, x0, b, pred}, Z, "zmv_psqmr_init");
+  const MatView Gd{ctx->gdmat.p, ctx->d, ctx->d, ctx->ldg};
+  if (ctx->iter_gram) {
+    run_zt(ctx, OpInitResidualGram{D, x0, b, pred}, Gd, "gemv_gram_psqmr_init");
+  } else {
+    run_zt(ctx, OpApplyZt{D, x0, pred, 0}, Z, "ztmv_psqmr_init");
+    run_zmv(ctx, OpInitResidual{D, x0, b, pred}, Z, "zmv_psqmr_init");
+  }
   run_vm(ctx, OpPsInit{D, x0, out, pred, tolmul}, D.m, "vmap_psqmr_init");
   CK(cudaGetLastError());
   *steps = 0;
@@ -1247,8 +1269,12 @@ static int psqmr_solve(gdwd_ctx* ctx, const double* b, const double* x0, double*
       return GDWD_OK;
     }
     if (it == max_steps) break;
-    run_zt(ctx, OpApplyZt{D, D.pq, 0, 1}, Z, "ztmv_psqmr_apply");
-    run_zmv(ctx, OpPsApply{D}, Z, "zmv_psqmr_apply");
+    if (ctx->iter_gram) {
+      run_zt(ctx, OpPsApplyGram{D}, Gd, "gemv_gram_psqmr_apply");
+    } else {
+      run_zt(ctx, OpApplyZt{D, D.pq, 0, 1}, Z, "ztmv_psqmr_apply");
+      run_zmv(ctx, OpPsApply{D}, Z, "zmv_psqmr_apply");
+    }
     run_vm(ctx, OpPsV1{D}, D.m, "vmap_psqmr_v1");
     run_vm(ctx, OpPsV2{D, out, tolmul, max_steps}, D.m, "vmap_psqmr_v2");
     CK(cudaGetLastError());
@@ -1711,6 +1737,19 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   MatView Z = zview(ctx);
   run_zmv(ctx, OpPlainZ{ctx->y.p, nullptr, const_cast<double*>(D.zy), nullptr}, Z, "zmv_zy");
   CK(cudaGetLastError());
+  // ITERATIVE on dense data: the d x d Gram as PSQMR's operator when it is
+  // much smaller than X (d <= n/4, n the global count) and fits in memory
+  ctx->iter_gram = false;
+  if (kind == GDWD_BACKEND_ITERATIVE && ctx->has_dense && cfg->iter_gram >= 0) {
+    bool want = cfg->iter_gram == 1 || 4 * d <= ng;
+    if (want && !(ctx->gdmat.p && ctx->fac_gen == ctx->data_gen)) {
+      size_t freeb = 0, totb = 0;
+      CK(cudaMemGetInfo(&freeb, &totb));
+      const double need = 8.0 * ((double)d * ((d + 1) / 2 * 2) + (double)gram_workspace_doubles(d, n)) * 1.05;
+      want = need < (double)freeb;
+    }
+    ctx->iter_gram = want;
+  }
   RC(build_factor(ctx, kind, mu2));
   if (kind != GDWD_BACKEND_ITERATIVE) RC(ensure_scratch(ctx, ctx->fac_rows, ctx->fac_rows + 2));
   RC(ensure_scratch(ctx, n, d));

@@ -730,6 +730,58 @@ struct OpPsApply {
   }
 };
 
+// The same two PSQMR operator applications with A's block Z~ Z~^T taken
+// from the explicit d x d Gram Gd (symmetric: row j of Gd dotted with the
+// top of the vector is (Z~ Z~^T v)_j): one GEMV over Gd instead of a Z~^T
+// pass and a Z~ pass.  Rows are features; the "sample sums" of the row
+// kernel are the feature sums of OpPsApply / OpInitResidual.
+struct OpPsApplyGram {
+  static constexpr int NN = 2;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped || !D.S->ps_active; }
+  GDWD_DEV double wval(int64_t j) const { return D.pq[j]; }
+  GDWD_DEV void row(int64_t j, double dot, double (&da)[NN]) const {
+    const double qj = D.pq[j];
+    const double aq = (dot + D.mu2 * qj) + D.zy[j] * D.pq[D.bot];
+    D.pAq[j] = aq;
+    da[0] += D.zy[j] * qj;
+    da[1] += qj * aq;
+  }
+  GDWD_DEV void fin(const double (&ds)[NN]) const {
+    Scal* S = D.S;
+    const double qd = D.pq[D.bot];
+    const double aqd = ds[0] + D.yty * qd;
+    D.pAq[D.bot] = aqd;
+    const double sg = ds[1] + qd * aqd;
+    if (fabs(sg) < TINY) {
+      S->ps_brk = 1;
+      S->ps_active = 0;
+      return;
+    }
+    S->ps_alpha = S->ps_rho / sg;
+  }
+};
+struct OpInitResidualGram {
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  const double* x0;
+  const double* b;
+  int pred;
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV double wval(int64_t j) const { return x0[j]; }
+  GDWD_DEV void row(int64_t j, double dot, double (&da)[NN]) const {
+    const double ax = (dot + D.mu2 * x0[j]) + D.zy[j] * x0[D.bot];
+    D.pr[j] = b[j] - ax;
+    da[0] += D.zy[j] * x0[j];
+  }
+  GDWD_DEV void fin(const double (&ds)[NN]) const {
+    const double ax = ds[0] + D.yty * x0[D.bot];
+    D.pr[D.bot] = b[D.bot] - ax;
+  }
+};
+
 struct OpPsV1 {  // r -= alpha Aq ; u = M^{-1} r ; ||u||, r.u
   static constexpr int NR = 2;
   static constexpr bool HAS_FIN = true;

@@ -441,7 +441,7 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
                    callback: Optional[Callable[[SolverState, KKTResiduals], None]] = None, *,
                    sigma_schedule: Optional[np.ndarray] = None, device: Optional[int] = None,
                    use_graph: bool = True, poll_every: int = 16, smw_gram_space: bool = True,
-                   persistent: bool = True) -> SolveResult:
+                   persistent: bool = True, iter_gram: Optional[bool] = None) -> SolveResult:
     """Run the solver to the KKT stopping rule or the iteration cap
     (solver.py:392-602).  ``callback(state, residuals)`` runs after every
     iteration (it forces a device sync and a copy of the iterates).
@@ -450,7 +450,9 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
     iteration k replaces update_sigma for 1 <= k < len), ``device``,
     ``use_graph``, ``poll_every``, ``smw_gram_space`` (SMW2 regime: iterate
     in sample-coefficient space with the n x n Gram instead of passes over X),
-    ``persistent`` (Gram-space SMW2: all iterations in one cooperative kernel)."""
+    ``persistent`` (Gram-space SMW2: all iterations in one cooperative kernel),
+    ``iter_gram`` (ITERATIVE on dense data: PSQMR's operator from the d x d
+    Gram formed once on the FP64 tensor cores; None = automatic for d <= n/4)."""
     t_start = time.perf_counter()
     dp = device_problem(data, device)
     t_up = time.perf_counter()
@@ -461,7 +463,7 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
         max_iter=int(config.max_iter), backend=_lib.BACKEND_CODE[kind.value], use_sgs=int(bool(config.use_sgs)),
         psqmr_switch_steps=int(config.psqmr_switch_steps), ell=int(config.ell), seed=int(config.seed),
         use_graph=int(bool(use_graph)), poll_every=int(poll_every), smw_gram_space=int(bool(smw_gram_space)),
-        persistent=int(bool(persistent)),
+        persistent=int(bool(persistent)), iter_gram=0 if iter_gram is None else (1 if iter_gram else -1),
         steplength=float(config.steplength),
         tol_feas=float(config.tol_feas), tol_cgap=float(config.tol_cgap), tol_cap=float(config.tol_cap),
         sigma0=float("nan") if config.sigma0 is None else float(config.sigma0), epsilon_c=eps_c,

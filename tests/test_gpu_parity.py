@@ -237,3 +237,23 @@ def test_kkt_residuals_of_reference_iterates(case):
                         tr["it_rho"][0], 0.0, 1.0, 1, 0.0)
     with pytest.raises(AssertionError):
         G.kkt_residuals(bad, prob)
+
+
+@pytest.mark.parametrize("case", ["tiny_iter", "tiny_iter_c4gen", "iter_natural", "var_q3_mu2", "var_converge_iter",
+                                  "prox_tiny"])
+def test_iter_gram_operator_matches_reference(case):
+    """ITERATIVE with PSQMR's operator from the d x d Gram (iter_gram=True):
+    the same iterates as the reference's two-pass operator -- first 20 to
+    1e-9, the whole run's counters and final w under sigma replay."""
+    tr = load_traj(case)
+    prob = problem_for(tr)
+    cfg = config_for(case, tr, prob)
+    out, h, vecs = run_traj(prob, cfg, bool(tr["full"]), tr["idx_d"], tr["idx_n"], iter_gram=True)
+    k = min(20, len(tr["hist"]))
+    for key in ("w", "u", "rho", "r", "xi", "alpha"):
+        for i in range(k):
+            assert relerr(vecs[key][i], tr["it_" + key][i]) < TOL20, (key, i)
+    out2 = G.sgs_admm_solve(prob, cfg, sigma_schedule=tr["hist"][:, 11], iter_gram=True)
+    assert out2.iterations == int(tr["iterations"]) and out2.converged == bool(tr["converged"])
+    assert abs(out2.psqmr_total - int(tr["psqmr_total"])) <= max(2, int(tr["psqmr_total"]) // 50)
+    assert relerr(out2.final_state.w, tr["final_w"]) < 1e-6
