@@ -127,7 +127,10 @@ ZmvGeom zmv_geom(int64_t rows, int64_t cols, int slots) {
   ZmvGeom g;
   g.tiles = (int)((cols + ZMV_TILE - 1) / ZMV_TILE);
   int64_t segs = std::max<int64_t>(1, slots / g.tiles);
-  segs = std::min<int64_t>(segs, std::max<int64_t>(1, rows / 8));
+  // at least 32 rows per segment: short matrices (c1: 1000 samples) are
+  // bound by the last CTA's in-order sum over segment partials, not by the
+  // stream (measured: 125 -> 31 segments, c1 8.8k -> 10.5k it/s)
+  segs = std::min<int64_t>(segs, std::max<int64_t>(1, rows / 32));
   g.seg_len = std::max<int64_t>(1, (rows + segs - 1) / segs);
   g.segs = (int)std::max<int64_t>(1, (rows + g.seg_len - 1) / g.seg_len);
   g.ldp = (cols + 1) / 2 * 2;

@@ -137,10 +137,19 @@ __global__ void __launch_bounds__(ZMV_THREADS) zmv_kernel(Op op, MatView X, ZmvG
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         double v0 = 0.0, v1 = 0.0;
-        for (int sg = 0; sg < (int)gridDim.y; ++sg) {
-          const double2 pv = __ldcg(reinterpret_cast<const double2*>(s.part + ((int64_t)sg * R + r) * g.ldp + j0));
-          v0 += pv.x;
-          v1 += pv.y;
+        const int S = (int)gridDim.y;
+        for (int sg0 = 0; sg0 < S; sg0 += 8) {  // segment order, 8 loads in flight
+          double2 pv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            pv[u] = sg0 + u < S ? __ldcg(reinterpret_cast<const double2*>(s.part + ((int64_t)(sg0 + u) * R + r) * g.ldp + j0))
+                                : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (sg0 + u < S) {
+              v0 += pv[u].x;
+              v1 += pv[u].y;
+            }
         }
         s.bundle[(int64_t)r * X.cols + j0] = v0;
         if (j0 + 1 < X.cols) s.bundle[(int64_t)r * X.cols + j0 + 1] = v1;
@@ -163,13 +172,25 @@ __global__ void __launch_bounds__(ZMV_THREADS) zmv_kernel(Op op, MatView X, ZmvG
     double v0[R], v1[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v0[r] = v1[r] = 0.0;
-    for (int sg = 0; sg < (int)gridDim.y; ++sg) {
+    // segment partials summed in segment order, 8 loads in flight
+    const int S = (int)gridDim.y;
+    for (int sg0 = 0; sg0 < S; sg0 += 8) {
+      double2 pv[8][R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const double2 pv = __ldcg(reinterpret_cast<const double2*>(s.part + ((int64_t)sg * R + r) * g.ldp + j0));
-        v0[r] += pv.x;
-        v1[r] += pv.y;
-      }
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          pv[u][r] = sg0 + u < S ? __ldcg(reinterpret_cast<const double2*>(s.part + ((int64_t)(sg0 + u) * R + r) * g.ldp + j0))
+                                 : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (sg0 + u < S) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            v0[r] += pv[u][r].x;
+            v1[r] += pv[u][r].y;
+          }
+        }
     }
     op.epi(j0, v0, dacc);
     if (j0 + 1 < X.cols) op.epi(j0 + 1, v1, dacc);
