@@ -1663,7 +1663,14 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   const int NV = 12, MV = 16;
   // Gram space pays off (and keeps w exactly representable) only when n <= d,
   // SMW2's own regime; an explicitly requested SMW2 with d < n iterates over X.
-  const bool gram = (kind == GDWD_BACKEND_SMW2) && cfg->smw_gram_space && n <= d;
+  // DIRECT with few samples (2n <= d, unsharded, n within the persistent
+  // kernel's shared-memory budget): the same exact solve done in sample space
+  // with SMW2's Gram-space machinery; still reported as DIRECT.  The (d+1)^2
+  // factor becomes an n x n one and the iteration runs in one cooperative
+  // kernel (c1: n = 1000, d = 2000).
+  int skind = kind;
+  if (kind == GDWD_BACKEND_DIRECT && cfg->smw_gram_space && !sharded(ctx) && 2 * n <= d && n <= 2500) skind = GDWD_BACKEND_SMW2;
+  const bool gram = (skind == GDWD_BACKEND_SMW2) && cfg->smw_gram_space && n <= d;
   CK(ctx->nvec.ensure((size_t)NV * ((n + 1) / 2 * 2)));
   CK(ctx->mvec.ensure((size_t)MV * ((m + 2) / 2 * 2)));
   CK(ctx->tabs.ensure((size_t)2 * (max_iter + 2) + (size_t)std::max<int64_t>(sched_len, 1)));
@@ -1753,7 +1760,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
     }
     ctx->iter_gram = want;
   }
-  RC(build_factor(ctx, kind, mu2));
+  RC(build_factor(ctx, skind, mu2));
   if (kind != GDWD_BACKEND_ITERATIVE) RC(ensure_scratch(ctx, ctx->fac_rows, ctx->fac_rows + 2));
   RC(ensure_scratch(ctx, n, d));
   // initial iterates (solver.py:447-454); padding slots zeroed first

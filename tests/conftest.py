@@ -30,7 +30,8 @@ TRAJ_CASES = ["tiny_direct", "tiny_smw2", "tiny_iter", "tiny_iter_c4gen", "tiny_
               "prox_tiny_q2"]
 # option / edge-case variants (make_golden.py VARIANTS): backend requested explicitly
 VAR_CASES = ["var_nosgs", "var_q_half", "var_q3_mu2", "var_opts", "var_e_random", "var_odd", "var_sparse_holes",
-             "var_min_direct", "var_min_smw", "var_min_iter", "var_d1_smw", "var_converge", "var_converge_smw", "var_converge_iter"]
+             "var_min_direct", "var_min_smw", "var_min_iter", "var_d1_smw", "var_direct_gram",
+             "var_direct_gram_nosgs", "var_direct_gram_converge", "var_converge", "var_converge_smw", "var_converge_iter"]
 SOLVER_KEYS = ("use_sgs", "mu", "sigma0", "epsilon_c", "steplength", "tol_feas", "tol_cgap", "tol_cap")
 
 

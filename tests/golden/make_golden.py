@@ -75,6 +75,11 @@ VARIANTS = [
     ("var_min_smw", "c1", 3, 2, "smw2", 30, True, dict()),
     ("var_min_iter", "c1", 2, 3, "iterative", 30, True, dict()),
     ("var_d1_smw", "c1", 1, 5, "smw2", 30, True, dict()),
+    # DIRECT with 2n <= d: solved in sample space on the device (same exact solve)
+    ("var_direct_gram", "c1", 200, 60, "direct", 40, True, dict()),
+    ("var_direct_gram_nosgs", "c1", 160, 50, "direct", 30, True, dict(use_sgs=False)),
+    ("var_direct_gram_converge", "c2", 120, 20, "direct", 600, True,
+     dict(C=10.0, shift=2.0, tol_feas=1e-3, tol_cgap=0.03, tol_cap=0.3)),
     ("var_converge", "c1", 30, 60, "direct", 600, True,
      dict(C=10.0, shift=2.0, tol_feas=1e-3, tol_cgap=0.03, tol_cap=0.3)),
     ("var_converge_smw", "c2", 120, 20, "smw2", 600, True,
