@@ -96,6 +96,8 @@ typedef int (*gdwd_allreduce_cb)(void* user, double* buf, int64_t count);
 int gdwd_ctx_create(int32_t device, gdwd_ctx** out);
 void gdwd_ctx_destroy(gdwd_ctx* ctx);
 const char* gdwd_last_error(const gdwd_ctx* ctx);
+/* sizeof(gdwd_config), sizeof(gdwd_result) as compiled (binding layout check) */
+void gdwd_abi_sizes(int64_t* config_bytes, int64_t* result_bytes);
 int gdwd_version(void);
 
 /* data ----------------------------------------------------------------------

@@ -23,7 +23,7 @@ BACKEND_NAME = {v: k for k, v in BACKEND_CODE.items()}
 # exported symbols (checked by the CPU test-suite against include/gdwd_b200.h)
 SYMBOLS = [
     "gdwd_ctx_create", "gdwd_ctx_destroy", "gdwd_last_error", "gdwd_version", "gdwd_upload_dense",
-    "gdwd_upload_csc", "gdwd_set_problem", "gdwd_matvec", "gdwd_matvec_t", "gdwd_score", "gdwd_between_class_median", "gdwd_kkt_residuals", "gdwd_libsvm_parse", "gdwd_libsvm_sizes",
+    "gdwd_upload_csc", "gdwd_set_problem", "gdwd_matvec", "gdwd_matvec_t", "gdwd_abi_sizes", "gdwd_score", "gdwd_between_class_median", "gdwd_kkt_residuals", "gdwd_libsvm_parse", "gdwd_libsvm_sizes",
     "gdwd_libsvm_copy", "gdwd_libsvm_free", "gdwd_preprocess_csc", "gdwd_solve", "gdwd_get_state",
     "gdwd_get_history", "gdwd_newton_sweep", "gdwd_chol_inverse", "gdwd_gram", "gdwd_psqmr_dense",
     "gdwd_solve_begin", "gdwd_solve_iterate", "gdwd_solve_end", "gdwd_time_iterations", "gdwd_set_profile",
@@ -74,6 +74,7 @@ def _declare(lib):
         "gdwd_ctx_destroy": (None, [vp]),
         "gdwd_last_error": (C.c_char_p, [vp]),
         "gdwd_version": (C.c_int, []),
+        "gdwd_abi_sizes": (None, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "gdwd_upload_dense": (C.c_int, [vp, _P, _I64, _I64]),
         "gdwd_upload_csc": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P, _I64, _I64]),
         "gdwd_set_problem": (C.c_int, [vp, _P, _P, _P, C.c_double, C.c_double, C.c_double]),

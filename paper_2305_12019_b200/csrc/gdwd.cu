@@ -671,6 +671,11 @@ extern "C" {
 
 int gdwd_version(void) { return 1; }
 
+void gdwd_abi_sizes(int64_t* config_bytes, int64_t* result_bytes) {
+  if (config_bytes) *config_bytes = (int64_t)sizeof(gdwd_config);
+  if (result_bytes) *result_bytes = (int64_t)sizeof(gdwd_result);
+}
+
 const char* gdwd_last_error(const gdwd_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int gdwd_ctx_create(int32_t device, gdwd_ctx** out) {

@@ -111,9 +111,11 @@ def test_library_loads_and_exports_every_symbol():
     for s in _header_symbols():
         assert hasattr(lib, s), s
     assert lib.gdwd_version() == 1
-    # struct layouts agree with the header (sizes, no compute)
-    assert ctypes.sizeof(_lib.GdwdConfig) == 10 * 4 + 7 * 8
-    assert ctypes.sizeof(_lib.GdwdResult) == 6 * 4 + 5 * 8 + 11 * 8
+    # struct layouts agree with the compiled header (sizes, no compute)
+    cb, rb = ctypes.c_int64(), ctypes.c_int64()
+    lib.gdwd_abi_sizes(ctypes.byref(cb), ctypes.byref(rb))
+    assert ctypes.sizeof(_lib.GdwdConfig) == cb.value == 11 * 4 + 4 + 7 * 8
+    assert ctypes.sizeof(_lib.GdwdResult) == rb.value == 6 * 4 + 5 * 8 + 11 * 8
 
 
 def test_no_cpu_fallback_in_product_package():
