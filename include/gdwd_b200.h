@@ -226,8 +226,10 @@ int gdwd_get_state(gdwd_ctx* ctx, double* r, double* xi, double* alpha, double* 
 int gdwd_get_history(gdwd_ctx* ctx, double* hist, int64_t max_rows, int64_t* rows);
 
 /* standalone kernels (unit-test seams) -------------------------------------*/
-/* newton_r_sweep (subsolvers.py:321-364); scalar_form=1 gives newton_r
- * (subsolvers.py:283-318) per coordinate, iters (nullable) its counts. */
+/* newton_r_sweep (subsolvers.py:321-364); scalar_form bit 0 gives newton_r
+ * (subsolvers.py:283-318) per coordinate, iters (nullable) its counts; bit 1
+ * runs one warp per coordinate (the persistent kernel's warp-parallel
+ * bisection; same roots and counts). */
 int gdwd_newton_sweep(int32_t device, int64_t n, const double* a, double sigma, double q, const double* weights,
                       const double* r_init, double tol, int32_t max_newton, int32_t scalar_form, double* out,
                       int32_t* iters);

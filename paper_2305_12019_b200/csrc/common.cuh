@@ -54,7 +54,10 @@ GDWD_DEV double np_pow(double x, double e) {
   if (e == 0.0) return 1.0;
   const double ae = fabs(e);
   // x > 0 with x^|e| and its error terms far from overflow / underflow
-  if (ae <= 16.0 && ae == rint(ae) && x > 0.0 && isfinite(x) && (abs(ilogb(x)) + 1) * (int)ae < 960)
+  // binary exponent from the bits (== ilogb for normal x; a subnormal reads
+  // -1023 and fails the bound exactly as ilogb's <= -1023 would)
+  const int ex = (int)((__double_as_longlong(x) >> 52) & 0x7ff) - 1023;
+  if (ae <= 16.0 && ae == rint(ae) && x > 0.0 && isfinite(x) && (abs(ex) + 1) * (int)ae < 960)
     return pow_int_dd(x, (int)e);
   return pow(x, e);
 }

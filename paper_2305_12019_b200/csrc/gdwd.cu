@@ -2197,7 +2197,8 @@ extern "C" int gdwd_newton_sweep(int32_t device, int64_t n, const double* a, dou
   CK(cudaMemcpy(dw, w, n * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dr, r0, n * 8, cudaMemcpyHostToDevice));
   OpNewtonSweep op{da, dw, dr, dout, dit, sigma, q, tol, max_newton, scalar_form};
-  vmap_kernel<OpNewtonSweep><<<vm_grid(n), VM_THREADS>>>(op, n, Scratch{});
+  if (scalar_form & 2) newton_warp_kernel<<<(unsigned)std::min<int64_t>((n + 7) / 8, 4 * NUM_SMS), 256>>>(op, n);
+  else vmap_kernel<OpNewtonSweep><<<vm_grid(n), VM_THREADS>>>(op, n, Scratch{});
   CK(cudaGetLastError());
   CK(cudaMemcpy(out, dout, n * 8, cudaMemcpyDeviceToHost));
   if (iters) CK(cudaMemcpy(iters, dit, n * 4, cudaMemcpyDeviceToHost));

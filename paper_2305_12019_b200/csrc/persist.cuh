@@ -496,11 +496,14 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent(PKArgs A) {
         const double xii = D.xi[i], ali = D.al[i], wli = D.wl[i], ri = D.r[i], yi = ysm[i];
         double o[1];
         pk_row_dot<1>(rows, n, xs, o);
+        // every lane holds the same dot (butterfly sums commute bitwise), so
+        // the whole warp runs the Newton / bisection solve (warp-parallel
+        // bisection levels); lane 0 stores
+        const double dot = o[0];
+        const double a = ((dot + yi * bb) + xii) - ali / sig;
+        const double rn = A.diag == 2 ? ri + 1e-3 * a : newton_margin_warp(a, sig, D.q, wli, ri, tol);
         if (lane == 0) {
-          const double dot = o[0];
           D.ztwb[i] = dot;
-          const double a = ((dot + yi * bb) + xii) - ali / sig;
-          const double rn = A.diag == 2 ? ri + 1e-3 * a : newton_margin(a, sig, D.q, wli, ri, tol);
           D.rnew[i] = rn;
           const double dri = rn - ri;
           D.dr[i] = dri;

@@ -83,10 +83,77 @@ GDWD_DEV double bisect_margin(double a, double sigma, double q, double wt, doubl
     const double mid = 0.5 * (lo + hi);
     const double gg = sigma * (mid - a) - (q * wt) / np_pow(mid, q + 1.0);
     if (fabs(gg) <= tol) return mid;
-    if (gg < 0.0) lo = mid; else hi = mid;
+    // Once lo and hi are adjacent doubles, mid rounds onto one of them and
+    // the bracket can stop changing; from then on every remaining step
+    // repeats the same mid, residual and branch (the 1e-17 width test never
+    // fires below one ulp), so leaving now returns the same 0.5*(lo+hi) the
+    // reference reaches after all 200 steps.
+    if (gg < 0.0) {
+      if (mid == lo) break;
+      lo = mid;
+    } else {
+      if (mid == hi) break;
+      hi = mid;
+    }
     if (hi - lo <= 1e-17 * (1.0 > hi ? 1.0 : hi)) break;
   }
   return 0.5 * (lo + hi);
+}
+
+// bisect_margin run by a whole warp (all 32 lanes call it with the same
+// arguments and get the same root).  Each round, lane m evaluates the
+// residual at node m of the next five levels of the bisection tree (31
+// nodes, breadth-first; a node's bracket is rebuilt from its path with the
+// same mid = 0.5*(lo+hi) roundings) together with the per-node outcomes of
+// the sequential step -- exit (|g| <= tol), stuck bracket, the child bracket
+// and its width test.  Ballots of those flags let every lane walk the five
+// levels with integer operations; the value returned (or the bracket carried
+// into the next round) is then shuffled from the lane of the node where the
+// walk stopped.  Brackets, mids and exits are the sequential routine's, one
+// residual evaluation per five steps.
+GDWD_DEV double bisect_margin_warp(double a, double sigma, double q, double wt, double tol) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  double lo = 1e-12;
+  double hi = (a > 0.0 ? a : 0.0) + pow((q * wt) / sigma, 1.0 / (q + 2.0)) + 1.0;
+  const int m1 = lane + 1;  // 1-based heap index of this lane's node (lane 31: unused)
+  const int depth = 31 - __clz(m1);
+  int it = 0;
+  for (;;) {
+    double nlo = lo, nhi = hi;
+    for (int l = depth - 1; l >= 0; --l) {  // path bit 1: residual < 0, lo = mid
+      const double mid = 0.5 * (nlo + nhi);
+      if ((m1 >> l) & 1) nlo = mid;
+      else nhi = mid;
+    }
+    const double mid = 0.5 * (nlo + nhi);
+    const double gg = sigma * (mid - a) - (q * wt) / np_pow(mid, q + 1.0);
+    const bool neg = gg < 0.0;
+    const double clo = neg ? mid : nlo, chi = neg ? nhi : mid;  // the bracket after this step
+    const unsigned bneg = __ballot_sync(FULL, neg);
+    const unsigned bret = __ballot_sync(FULL, fabs(gg) <= tol || (neg ? mid == nlo : mid == nhi));
+    const unsigned bwid = __ballot_sync(FULL, chi - clo <= 1e-17 * (1.0 > chi ? 1.0 : chi));
+    int node = 0, par = 0, src = -1;
+    bool child = false;
+#pragma unroll
+    for (int lev = 0; lev < 5; ++lev) {
+      const unsigned b = 1u << node;
+      if (bret & b) {  // |g| <= tol returns mid; a stuck bracket returns 0.5*(lo+hi) = the same mid
+        src = node;
+        break;
+      }
+      if (++it >= 200 || (bwid & b)) {  // loop end / width break: 0.5*(lo+hi) of the new bracket
+        src = node;
+        child = true;
+        break;
+      }
+      par = node;
+      node = 2 * node + ((bneg & b) ? 2 : 1);
+    }
+    if (src >= 0) return __shfl_sync(FULL, child ? 0.5 * (clo + chi) : mid, src);
+    lo = __shfl_sync(FULL, clo, par);
+    hi = __shfl_sync(FULL, chi, par);
+  }
 }
 
 // One coordinate of newton_r_sweep (subsolvers.py:321-364): same update and
@@ -94,8 +161,9 @@ GDWD_DEV double bisect_margin(double a, double sigma, double q, double wt, doubl
 // ``* s**(-(q+1))``).  scalar_form=1 reproduces the scalar newton_r
 // (subsolvers.py:283-318), which uses the first form throughout; *iters
 // receives its iteration count.
-GDWD_DEV double newton_margin(double a, double sigma, double q, double wt, double r0, double tol,
-                              int max_newton = 50, int scalar_form = 0, int* iters = nullptr) {
+template <bool WARP>
+GDWD_DEV double newton_margin_t(double a, double sigma, double q, double wt, double r0, double tol,
+                                int max_newton, int scalar_form, int* iters) {
   const double mq = -q, qp1 = q + 1.0;
   const double c = (q * wt) / sigma;
   double s = r0;
@@ -105,12 +173,19 @@ GDWD_DEV double newton_margin(double a, double sigma, double q, double wt, doubl
     if (iters) *iters = 0;
     return s;
   }
+  // iterates whose residual was tested in the form later iterates use (the
+  // sweep tests r0 with the other form, so it is not recorded there)
+  double seen[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) seen[j] = NAN;
+  if (scalar_form) seen[0] = s;
   for (it = 0; it < max_newton; ++it) {
     const double sp = np_pow(s, qp1);
     const double nxt = (s * ((q + 2.0) * c + a * sp)) / ((q + 1.0) * c + sp * s);
     if (!isfinite(nxt) || nxt <= 0.0) {
       if (iters) *iters = it;
-      return bisect_margin(a, sigma, q, wt, tol);
+      if constexpr (WARP) return bisect_margin_warp(a, sigma, q, wt, tol);
+      else return bisect_margin(a, sigma, q, wt, tol);
     }
     s = nxt;
     foc = scalar_form ? (mq * wt) / np_pow(s, qp1) + sigma * (s - a)
@@ -119,9 +194,30 @@ GDWD_DEV double newton_margin(double a, double sigma, double q, double wt, doubl
       if (iters) *iters = it + 1;
       return s;
     }
+    // The update is a fixed map of s: once it returns to an iterate already
+    // tested (a fixed point or a cycle of length <= 8) every later iterate
+    // and residual repeats, |foc| <= tol can no longer happen, and the
+    // reference ends in the same bisection after max_newton updates.
+    bool cyc = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) cyc |= s == seen[j];
+    if (cyc) break;
+#pragma unroll
+    for (int j = 7; j > 0; --j) seen[j] = seen[j - 1];
+    seen[0] = s;
   }
   if (iters) *iters = max_newton;
-  return bisect_margin(a, sigma, q, wt, tol);
+  if constexpr (WARP) return bisect_margin_warp(a, sigma, q, wt, tol);
+  else return bisect_margin(a, sigma, q, wt, tol);
+}
+GDWD_DEV double newton_margin(double a, double sigma, double q, double wt, double r0, double tol,
+                              int max_newton = 50, int scalar_form = 0, int* iters = nullptr) {
+  return newton_margin_t<false>(a, sigma, q, wt, r0, tol, max_newton, scalar_form, iters);
+}
+// the same root computed by a whole warp (uniform arguments in all lanes)
+GDWD_DEV double newton_margin_warp(double a, double sigma, double q, double wt, double r0, double tol,
+                                   int max_newton = 50, int scalar_form = 0, int* iters = nullptr) {
+  return newton_margin_t<true>(a, sigma, q, wt, r0, tol, max_newton, scalar_form, iters);
 }
 
 GDWD_DEV double np_max0(double x) { return isnan(x) ? x : (x > 0.0 ? x : 0.0); }   // np.maximum(x, 0)
@@ -1150,10 +1246,25 @@ struct OpNewtonSweep {  // standalone newton_r_sweep / newton_r (subsolvers.py:2
   GDWD_DEV bool skip() const { return false; }
   GDWD_DEV void elem(int64_t i, double (&)[NR]) const {
     int it = 0;
-    out[i] = newton_margin(a[i], sigma, q, w[i], r0[i], tol, max_newton, scalar_form, &it);
+    out[i] = newton_margin(a[i], sigma, q, w[i], r0[i], tol, max_newton, scalar_form & 1, &it);
     if (iters) iters[i] = it;
   }
   GDWD_DEV void fin(const double (&)[NR]) const {}
 };
+
+// the same sweep with one warp per coordinate (newton_margin_warp, the form
+// the persistent Gram-space kernel uses)
+__global__ void newton_warp_kernel(OpNewtonSweep op, int64_t n) {
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    int it = 0;
+    const double r = newton_margin_warp(op.a[i], op.sigma, op.q, op.w[i], op.r0[i], op.tol, op.max_newton,
+                                        op.scalar_form & 1, &it);
+    if ((threadIdx.x & 31) == 0) {
+      op.out[i] = r;
+      if (op.iters) op.iters[i] = it;
+    }
+  }
+}
 
 }  // namespace gdwd

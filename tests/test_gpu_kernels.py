@@ -1,5 +1,7 @@
 """GPU kernel parity through the C ABI (run on a B200: pytest -m gpu)."""
 
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -95,6 +97,58 @@ def test_newton_sweep_vs_oracle(q):
         ref = O.newton_sweep(a, sigma, q, w, r0, tol=1e-6)
         got = G.newton_r_sweep(a, sigma, q, w, r0, tol=1e-6)
         assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-13
+
+
+@pytest.mark.parametrize("q", [1.0, 2.0, 0.5])
+def test_newton_sweep_bisection_regime(q):
+    """Large sigma (config 2 drives it past 1e12): |foc| <= tol needs s to
+    better than an ulp, Newton stalls on a fixed point or 2-cycle and the
+    reference finishes in its 200-step bisection.  The device leaves both
+    loops once their state repeats; the roots must not move."""
+    rng = np.random.default_rng(int(q * 100))
+    n = 1500
+    a = rng.standard_normal(n) * 3
+    r0 = rng.random(n) * 2 + 0.05
+    w = rng.random(n) + 0.1
+    for sigma, tol in ((1e10, 1e-7), (1e13, 1e-8), (3e15, 1e-9)):
+        ref = O.newton_sweep(a, sigma, q, w, r0, tol=tol)
+        got = G.newton_r_sweep(a, sigma, q, w, r0, tol=tol)
+        assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-13
+    for i in range(40):  # scalar form: root and the reported Newton count
+        ref, rit = O.newton_scalar(float(a[i]), 1e13, q, float(w[i]), float(r0[i]), tol=1e-8)
+        got, git = G.newton_r(float(a[i]), 1e13, q, float(w[i]), float(r0[i]), tol=1e-8)
+        assert got == pytest.approx(ref, rel=1e-13, abs=0) and git == rit
+
+
+def _newton_dev(a, sigma, q, w, r0, tol, form):
+    from paper_2305_12019_b200 import _lib
+    a, w, r0 = (np.ascontiguousarray(v, dtype=np.float64) for v in (a, w, r0))
+    out = np.empty_like(a)
+    its = np.zeros(a.size, dtype=np.int32)
+    lib = _lib.load()
+    assert lib.gdwd_newton_sweep(0, a.size, _lib.ptr(a), float(sigma), float(q), _lib.ptr(w), _lib.ptr(r0),
+                                 float(tol), 50, form, _lib.ptr(out),
+                                 its.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))) == 0
+    return out, its
+
+
+@pytest.mark.parametrize("q", [1.0, 2.0, 4.0, 0.5])
+def test_newton_warp_form_matches(q):
+    """The warp-cooperative Newton + bisection (persistent kernel) returns the
+    per-thread form's roots bit for bit, and its Newton counts, in every
+    regime (converging Newton, stalled Newton + bisection)."""
+    rng = np.random.default_rng(int(q * 7))
+    n = 4000
+    a = rng.standard_normal(n) * 3
+    r0 = rng.random(n) * 2 + 0.05
+    w = rng.random(n) + 0.1
+    for sigma, tol in ((0.5, 1e-6), (3e5, 1e-6), (1e13, 1e-8), (3e15, 1e-9)):
+        for form in (0, 1):
+            ref, rit = _newton_dev(a, sigma, q, w, r0, tol, form)
+            got, git = _newton_dev(a, sigma, q, w, r0, tol, form | 2)
+            assert np.array_equal(got, ref) and np.array_equal(git, rit)
+        o = O.newton_sweep(a[:300], sigma, q, w[:300], r0[:300], tol=tol)
+        assert np.max(np.abs(got[:300] - o) / np.abs(o)) < 1e-13
 
 
 def test_psqmr_kats():
