@@ -279,19 +279,19 @@ def run_b200(args, dist: Dist):
         (kind_name == "smw2" and n <= d) or (kind_name == "direct" and 2 * n <= d))
     if persistent:
         # one cooperative launch per timed region: algorithmic bytes = the n x n
-        # matrices streamed per iteration (K, G^{-1}K: 2 in phase A, 1 in C,
-        # 2 in D with the speculative re-solve, 1 in H)
-        alg = 8.0 * n * n * 6.0 * iters_timed
+        # matrices streamed per iteration (persist3.cuh: K and G^{-1}K once in
+        # phase A, once in phase D with the speculative re-solve)
+        alg = 8.0 * n * n * 4.0 * iters_timed
         ach = alg / (t_ms * 1e-3) / 1e9
-        tr = traffic_of("gram_smw_persistent") if args.config == "c2" else None
-        roofline = {"bound": "hbm", "kernel": "gram_smw_persistent", "achieved": round(ach, 1), "peak": peak,
+        tr = traffic_of("gram_smw_persistent3") if args.config == "c2" else None
+        roofline = {"bound": "hbm", "kernel": "gram_smw_persistent3", "achieved": round(ach, 1), "peak": peak,
                     "unit": "GB/s", "frac": round(ach / peak, 4),
                     "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
                     "traffic": round(tr["per_iteration"] * iters_timed) if tr else None,
                     "algorithmic_bytes_per_launch": alg,
                     "note": "K and G^-1 K (2 x %.0f MB) are L2-resident (ncu: DRAM traffic = the one cold load, "
                             "L2 hit 97%%); the loop is bound by the SMs' L2 read rate and grid-barrier latency (one "
-                            "launch, 4 grid barriers per iteration)" % (8 * n * n / 1e6)}
+                            "launch, 3 grid barriers and 2 row sweeps of K and G^-1 K per iteration)" % (8 * n * n / 1e6)}
     else:
         top = next(k for k in kernels if k["gbs"] is not None)
         tr = traffic_of(top["tag"]) if args.config == "c2" else None

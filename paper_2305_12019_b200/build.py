@@ -20,7 +20,7 @@ HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libgdwd_b200.so"
 SOURCES = ["gdwd.cu", "gram.cu", "ingest.cpp"]
-HEADERS = ["common.cuh", "zops.cuh", "solver_ops.cuh", "gram.cuh", "spops.cuh", "persist.cuh", "synth.cuh",
+HEADERS = ["common.cuh", "zops.cuh", "solver_ops.cuh", "gram.cuh", "spops.cuh", "persist.cuh", "persist3.cuh", "synth.cuh",
            "select.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

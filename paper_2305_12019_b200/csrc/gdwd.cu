@@ -30,6 +30,7 @@
 #include "spops.cuh"
 #include "select.cuh"
 #include "persist.cuh"
+#include "persist3.cuh"
 #include "synth.cuh"
 #include "zops.cuh"
 
@@ -221,6 +222,7 @@ struct gdwd_ctx {
   int64_t ldg = 0;
   int fac_iter_gram = 0;
   DevBuf pk_part, gkmat;
+  int pk_version = 3;
   // proximal fallback (subsolvers.py:159-256)
   bool prox = false;
   int ell = 10;
@@ -1193,8 +1195,12 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
       RC(ensure_scratch(ctx, m, m));
       run_zt(ctx, op, MatView{ctx->fac.p, m, m, ld});
       CK(cudaGetLastError());
+      // fixed vectors of the 3-barrier persistent kernel (persist3.cuh)
+      run_zt(ctx, OpGemvStore{D.jy, 1.0, const_cast<double*>(D.kap)}, MatView{ctx->kmat.p, m, m, ld});
+      run_zt(ctx, OpGemvStore{ctx->y.p, D.ynorm, const_cast<double*>(D.gam)}, MatView{ctx->gkmat.p, m, m, ld});
+      CK(cudaGetLastError());
       RC(ensure_scratch(ctx, n, d));
-      T.mark("G^-1 y");
+      T.mark("G^-1 y, K G^-1 y, GK y");
     }
   } else {
     if (Z.a && n >= 65536) {
@@ -1718,10 +1724,12 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   // persistent per-problem vectors: [colsq (d) | zy (d) | jac (m) | jy (n)],
   // each segment at an even (16-byte aligned) offset
   const int64_t dst2 = (d + 1) / 2 * 2, mst2 = (m + 1) / 2 * 2;
-  CK(ctx->colsq.ensure((size_t)2 * dst2 + mst2 + nst + 8));
+  CK(ctx->colsq.ensure((size_t)2 * dst2 + mst2 + 3 * nst + 8));
   D.zy = ctx->colsq.p + dst2;
   D.jac = ctx->colsq.p + 2 * dst2;
   D.jy = ctx->colsq.p + 2 * dst2 + mst2;
+  D.kap = D.jy + nst;
+  D.gam = D.jy + 2 * nst;
   D.S = ctx->S;
   D.hist = ctx->histb.p;
 
@@ -1779,12 +1787,13 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   {
     CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
-    const double ys = ctx->Sh->ys;  // computed by build_factor (SMW2)
+    const double ys = ctx->Sh->ys, yjy = ctx->Sh->yjy;  // computed by build_factor (SMW2)
     Scal s0;
     memset(&s0, 0, sizeof(s0));
     s0.sigma = sigma0;
     s0.sigma_next = sigma0;
     s0.ys = ys;
+    s0.yjy = yjy;
     *ctx->Sh = s0;
     CK(cudaMemcpyAsync(ctx->S, ctx->Sh, sizeof(Scal), cudaMemcpyHostToDevice, ctx->st));
   }
@@ -1813,12 +1822,15 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
     int nb = 0;
     // 11 vector slots: 3 staged, 6 bulk-copied inputs, y and G^{-1} y/|y|
     const size_t sm = (size_t)(11 * ((n + 3) / 2 * 2)) * sizeof(double);
-    if (sm > 220 * 1024 || cudaFuncSetAttribute(gram_smw_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)sm) != cudaSuccess) {
+    // kernel version: 3 barriers per iteration (default) or the 4-barrier
+    // association (GDWD_PK_VERSION=2, kept for A/B checks)
+    ctx->pk_version = (getenv("GDWD_PK_VERSION") && atoi(getenv("GDWD_PK_VERSION")) == 2) ? 2 : 3;
+    const void* kfn = ctx->pk_version == 3 ? (const void*)gram_smw_persistent3 : (const void*)gram_smw_persistent;
+    if (sm > 220 * 1024 || cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
       cudaGetLastError();
       ctx->persistent = false;
     }
-    if (ctx->persistent) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gram_smw_persistent, PK_THREADS, sm));
+    if (ctx->persistent) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, PK_THREADS, sm));
     if (nb < 1 || n > (int64_t)PK_MAX_OWN * NUM_SMS) ctx->persistent = false;
     else CK(ctx->pk_part.ensure((size_t)2 * NUM_SMS * PK_NPART));
   }
@@ -1856,11 +1868,19 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
       CK(cudaMalloc(&ts, tsn * sizeof(unsigned long long)));
       CK(cudaMemset(ts, 0, tsn * sizeof(unsigned long long)));
     }
-    PKArgs pa{D, ctx->kmat.p, ctx->fac.p, ctx->gkmat.p, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host,
-              getenv("GDWD_PK_DIAG") ? atoi(getenv("GDWD_PK_DIAG")) : 0, ts, ctx->use_sgs ? 1 : 0};
-    void* args[] = {&pa};
+    const int diag = getenv("GDWD_PK_DIAG") ? atoi(getenv("GDWD_PK_DIAG")) : 0;
     const size_t sm = (size_t)(11 * ((ctx->n + 3) / 2 * 2)) * sizeof(double);
-    {
+    if (ctx->pk_version == 3) {
+      // 3 grid barriers per iteration (persist3.cuh)
+      PK3Args pa{D, ctx->kmat.p, ctx->gkmat.p, D.kap, D.gam, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host,
+                 diag, ts, ctx->use_sgs ? 1 : 0};
+      void* args[] = {&pa};
+      Launch L(ctx, "persistent_gram_smw2");
+      CK(cudaLaunchCooperativeKernel((void*)gram_smw_persistent3, dim3(NUM_SMS), dim3(PK_THREADS), args, sm, ctx->st));
+    } else {
+      PKArgs pa{D, ctx->kmat.p, ctx->fac.p, ctx->gkmat.p, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host, diag, ts,
+                ctx->use_sgs ? 1 : 0};
+      void* args[] = {&pa};
       Launch L(ctx, "persistent_gram_smw2");
       CK(cudaLaunchCooperativeKernel((void*)gram_smw_persistent, dim3(NUM_SMS), dim3(PK_THREADS), args, sm, ctx->st));
     }

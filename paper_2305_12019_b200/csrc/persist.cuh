@@ -64,6 +64,7 @@ struct PKS {
   int k, stopped, converged, reuse, double_count, iters_done, error, pending;
   double sigma, sigma_next, hbot, h2bot, beta_b, beta, coef, s2, gnorm, w2, wu2, ytzw, sdual;
   double sigma_pend;  // sigma of the iteration whose u, rho update is pending
+  double cp;          // persist3: t2 |y| - coef of the current SMW solve
   double eta[11];
 };
 

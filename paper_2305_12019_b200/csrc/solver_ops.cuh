@@ -30,6 +30,7 @@ struct Scal {
   double smw_coef, smw_s2;
   double ps_tau, ps_rho, ps_theta, ps_alpha, ps_thnew, ps_cA, ps_cB, ps_rhonew, ps_resn;
   double ys;          // SMW: 1 + ybar^T J^{-1} ybar - 1
+  double yjy;         // SMW: ybar^T G^{-1} ybar (the sum inside ys)
   double ytzw;        // Gram space: y . ztw_bar (= zy . w_bar)
   double pv[16];      // proximal: V^T v of the last projection
   double px_beta;     // proximal: beta of the current solve
@@ -44,6 +45,7 @@ struct Dev {
   double tol_feas, tol_cgap, tol_cap;
   int max_iter, sched_len;
   const double *y, *e, *wl, *zy, *jac, *jy;
+  const double *kap, *gam;  // Gram-space SMW2: K jy, GK (y/|y|)
   double *r, *xi, *al, *ztw, *rnew, *dr, *ztwb, *s1, *g, *tq;
   double *u, *rho, *h, *h2, *xb, *x;
   double *pr, *pres, *pq, *pu, *pd, *pAd, *pAq;
@@ -1232,7 +1234,23 @@ struct OpJyG {  // jy = G^{-1} (y/|y|) ; ys = 1 + (y/|y|).jy - 1  (subsolvers.py
     jy[i] = dot;
     na[0] += (y[i] / ynorm) * dot;
   }
-  GDWD_DEV void fin(const double (&ns)[NN]) const { S->ys = 1.0 + ns[0] - 1.0; }
+  GDWD_DEV void fin(const double (&ns)[NN]) const {
+    S->ys = 1.0 + ns[0] - 1.0;
+    S->yjy = ns[0];
+  }
+};
+
+// out = M v (rows of an n x n Gram-space matrix), v[j] / vscale
+struct OpGemvStore {
+  static constexpr int NN = 1;
+  static constexpr bool HAS_FIN = false;
+  const double* v;
+  double vscale;
+  double* out;
+  GDWD_DEV bool skip() const { return false; }
+  GDWD_DEV double wval(int64_t j) const { return v[j] / vscale; }
+  GDWD_DEV void row(int64_t i, double dot, double (&)[NN]) const { out[i] = dot; }
+  GDWD_DEV void fin(const double (&)[NN]) const {}
 };
 
 struct OpNewtonSweep {  // standalone newton_r_sweep / newton_r (subsolvers.py:283-364)

@@ -257,3 +257,34 @@ def test_iter_gram_operator_matches_reference(case):
     assert out2.iterations == int(tr["iterations"]) and out2.converged == bool(tr["converged"])
     assert abs(out2.psqmr_total - int(tr["psqmr_total"])) <= max(2, int(tr["psqmr_total"]) // 50)
     assert relerr(out2.final_state.w, tr["final_w"]) < 1e-6
+
+
+@pytest.mark.parametrize("version", ["3", "2"])
+@pytest.mark.parametrize("case", TRAJ_CASES + VAR_CASES)
+def test_persistent_iterates_match_reference(case, version, monkeypatch):
+    """The persistent Gram-space kernel (SMW2, and DIRECT with 2n <= d) run
+    for k = 1, 2, 7, 20 iterations in one launch, no callback: its state after
+    iteration k against the reference's iterate k (1e-9 relative), for the
+    3-barrier association (default) and the 4-barrier one.  Cases outside
+    the Gram-space regime run the graph path (same check)."""
+    monkeypatch.setenv("GDWD_PK_VERSION", version)
+    tr = load_traj(case)
+    prob = problem_for(tr)
+    full = bool(tr["full"])
+    nref = len(tr["it_w"])
+    for k in (1, 2, 7, 20):
+        if k > nref:
+            break
+        cfg = config_for(case, tr, prob, max_iter=k)
+        out = G.sgs_admm_solve(prob, cfg, persistent=True, sigma_schedule=tr["hist"][:, 11])
+        if out.iterations < k:  # stopping rule fired earlier in the reference too
+            assert out.iterations == int(tr["iterations"])
+            break
+        st = out.final_state
+        for key in ("w", "u", "rho", "r", "xi", "alpha"):
+            v = getattr(st, key)
+            if not full:
+                v = v[tr["idx_d"]] if key in ("w", "u", "rho") else v[tr["idx_n"]]
+            assert relerr(v, tr["it_" + key][k - 1]) < TOL20, (key, k)
+        b = tr["hist"][k - 1, 12]
+        assert abs(st.beta - b) <= 1e-9 * abs(b) + 1e-12, k
