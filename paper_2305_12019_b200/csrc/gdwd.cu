@@ -622,7 +622,7 @@ static void free_sparse(gdwd_ctx* ctx) {
 // Diagnostics (GDWD_PK_TIMING): per-CTA %globaltimer stamps of the persistent
 // kernel; for every phase point, the mean over iterations of the earliest,
 // median and latest CTA relative to the iteration's first CTA start.
-static void pk_timing_report(unsigned long long* ts, size_t tsn) {
+static void pk_timing_report(unsigned long long* ts, size_t tsn, int version) {
   std::vector<unsigned long long> h(tsn);
   if (cudaMemcpy(h.data(), ts, tsn * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) return;
   cudaFree(ts);
@@ -633,8 +633,14 @@ static void pk_timing_report(unsigned long long* ts, size_t tsn) {
                            "D waited", "D staged", "", "", "A waited", "A loop", "A staged", "", "", "", "", ""};
   // per-CTA SM-clock intervals between consecutive points (1.965 GHz), the
   // median and the slowest CTA, averaged over iterations
-  const int order[] = {0, 24, 25, 26, 1, 2, 16, 17, 18, 19, 14, 15, 3, 4, 20, 21, 5, 6, 11, 12, 13, 9, 10};
-  const int no = sizeof(order) / sizeof(order[0]);
+  const int order2[] = {0, 24, 25, 26, 1, 2, 16, 17, 18, 19, 14, 15, 3, 4, 20, 21, 5, 6, 11, 12, 13, 9, 10};
+  // persist3.cuh points, in time order (interval named by its start point)
+  const char* names3[15] = {"A wait in", "A staging", "A sum+scal", "A rows", "A partials", "B1 barrier",
+                            "B1 scalars", "D staging", "D rows", "D partials", "B2 barrier", "B2 scal+H rows",
+                            "H partials", "B3 barrier", "B3 scalars"};
+  const int order3[] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14};
+  const int* order = version == 3 ? order3 : order2;
+  const int no = version == 3 ? 15 : (int)(sizeof(order2) / sizeof(order2[0]));
   std::vector<double> sum_med(no, 0.0), sum_max(no, 0.0);
   int cnt = 0;
   std::vector<double> v;
@@ -664,9 +670,36 @@ static void pk_timing_report(unsigned long long* ts, size_t tsn) {
   fprintf(stderr, "[pk timing] interval from point   median-CTA us   slowest-CTA us\n");
   for (int q = 0; q < no; ++q) {
     tot += sum_med[q] / cnt;
-    fprintf(stderr, "[pk timing] %-14s %10.2f %10.2f\n", names[order[q]], sum_med[q] / cnt, sum_max[q] / cnt);
+    fprintf(stderr, "[pk timing] %-14s %10.2f %10.2f\n", version == 3 ? names3[q] : names[order[q]], sum_med[q] / cnt,
+            sum_max[q] / cnt);
   }
   fprintf(stderr, "[pk timing] sum of medians %.2f us over %d iterations\n", tot, cnt);
+  if (version != 3) return;
+  // arrival skew: per-CTA time from leaving one barrier's cross-sum to
+  // arriving at the next barrier (median / slowest CTA), and the barrier
+  // interval of the median CTA
+  struct Seg { const char* name; int a, b; bool wrap; };
+  const Seg segs[] = {{"B3 exit -> B1 arrive", 14, 5, true}, {"B1 exit -> B2 arrive", 6, 10, false},
+                      {"B2 exit -> B3 arrive", 11, 13, false}};
+  for (const Seg& g : segs) {
+    double smed = 0.0, smax = 0.0;
+    int c2 = 0;
+    for (int it = 1; it + 1 < PK_TS_ITERS && c2 < cnt; ++it, ++c2) {
+      const unsigned long long* r = &h[(size_t)it * NUM_SMS * NP];
+      const unsigned long long* rn = &h[(size_t)(it + 1) * NUM_SMS * NP];
+      v.clear();
+      for (int b = 0; b < NUM_SMS; ++b) {
+        const unsigned long long t0 = r[b * NP + g.a];
+        const unsigned long long t1 = g.wrap ? rn[b * NP + g.b] : r[b * NP + g.b];
+        v.push_back((double)(long long)(t1 - t0) / 1965.0);
+      }
+      std::sort(v.begin(), v.end());
+      smed += v[v.size() / 2];
+      smax += v.back();
+    }
+    if (c2) fprintf(stderr, "[pk timing] path %-22s median %6.2f slowest %6.2f us (skew %.2f)\n", g.name, smed / c2,
+                    smax / c2, (smax - smed) / c2);
+  }
 }
 
 extern "C" {
@@ -1832,7 +1865,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
     }
     if (ctx->persistent) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, PK_THREADS, sm));
     if (nb < 1 || n > (int64_t)PK_MAX_OWN * NUM_SMS) ctx->persistent = false;
-    else CK(ctx->pk_part.ensure((size_t)2 * NUM_SMS * PK_NPART));
+    else CK(ctx->pk_part.ensure((size_t)2 * NUM_SMS * PK_NPART + 8));  // + barrier counter
   }
   if (kind != GDWD_BACKEND_ITERATIVE && cfg->use_graph && !ctx->prof && !ctx->persistent && ctx->comm_mode != 2) {
     cudaGraph_t graph;
@@ -1872,8 +1905,13 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
     const size_t sm = (size_t)(11 * ((ctx->n + 3) / 2 * 2)) * sizeof(double);
     if (ctx->pk_version == 3) {
       // 3 grid barriers per iteration (persist3.cuh)
+      unsigned* ctr = nullptr;
+      if (!(getenv("GDWD_PK_BAR") && atoi(getenv("GDWD_PK_BAR")) == 0)) {
+        ctr = reinterpret_cast<unsigned*>(ctx->pk_part.p + (size_t)2 * NUM_SMS * PK_NPART);
+        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), ctx->st));
+      }
       PK3Args pa{D, ctx->kmat.p, ctx->gkmat.p, D.kap, D.gam, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host,
-                 diag, ts, ctx->use_sgs ? 1 : 0};
+                 diag, ts, ctx->use_sgs ? 1 : 0, ctr};
       void* args[] = {&pa};
       Launch L(ctx, "persistent_gram_smw2");
       CK(cudaLaunchCooperativeKernel((void*)gram_smw_persistent3, dim3(NUM_SMS), dim3(PK_THREADS), args, sm, ctx->st));
@@ -1886,7 +1924,7 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
     }
     CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
-    if (ts) pk_timing_report(ts, tsn);
+    if (ts) pk_timing_report(ts, tsn, ctx->pk_version);
     ctx->k_host = ctx->Sh->stopped ? ctx->Sh->iters_done : kend;
     ctx->stopped = ctx->Sh->stopped != 0;
   }

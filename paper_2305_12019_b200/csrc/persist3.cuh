@@ -93,6 +93,7 @@ struct PK3Args {
   int diag;  // 1 = skip the row sweeps (barrier / staging floor)
   unsigned long long* tstamp;
   int use_sgs;
+  unsigned* ctr;  // grid barrier counter, zero at launch (null: cooperative-groups grid.sync)
 };
 
 __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A) {
@@ -138,6 +139,26 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
     const double* src[4] = {D.xi, D.r, D.al, D.x};
     double* dst[4] = {s0, s1, s2, s3};
     issue(4, src, dst);
+  };
+  // Grid barrier: one release-add per CTA on a counter that only grows, then
+  // an acquire poll for this barrier's target (bar.sync before and after
+  // carries the ordering to and from the CTA's other threads); no fence.sc.
+  unsigned bar_target = 0;
+  auto pk_bar = [&]() {
+    if (!A.ctr) {
+      grid.sync();
+      return;
+    }
+    __syncthreads();
+    bar_target += gridDim.x;
+    if (threadIdx.x == 0) {
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.ctr) : "memory");
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(A.ctr) : "memory");
+      } while ((int)(v - bar_target) < 0);
+    }
+    __syncthreads();
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = n * blockIdx.x / gridDim.x, i1 = n * (blockIdx.x + 1) / gridDim.x;
@@ -263,7 +284,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
         const double xbi = mu2_one ? hi - vi : hi / mu2 - vi / mu2;
         const double ztwbi = mu2_one ? s1i - cp * kapi : s1i - (cp * kapi) / mu2;
         const double a = ((ztwbi + yi * bb) + xii) - ali / sig;
-        const double rn = newton_margin_warp(a, sig, D.q, wli, ri, tol);
+        double rn;
+        if (A.diag == 2) rn = ri + 1e-3 * a;  // diagnostics: no Newton solve
+        else if (A.diag == 3) rn = __shfl_sync(0xffffffffu, lane == 0 ? newton_margin(a, sig, D.q, wli, ri, tol) : 0.0, 0);
+        else rn = newton_margin_warp(a, sig, D.q, wli, ri, tol);
         const double dri = rn - ri;
         if (lane == 0) {
           qa += ali * oK[0];
@@ -284,7 +308,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
       double pv[2] = {qa, ydr};
       pk_write_lane0<2>(A.part, slot, pv, red);
       PK3_TS(5);
-      grid.sync();
+      pk_bar();
       if (A.use_sgs) {  // phase D inputs
         const double* src[3] = {D.dr, D.xb, D.ztwb};
         double* dst[3] = {s0, s1, s2};
@@ -386,7 +410,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
       double pv[3] = {q, syg, yg};
       pk_write_lane0<3>(A.part, slot, pv, red);
       PK3_TS(10);
-      grid.sync();
+      pk_bar();
       double t[3];
       pk_cross_sum<3>(A.part, slot, t, red);
       slot ^= 1;
@@ -488,7 +512,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
         }
       }
       PK3_TS(13);
-      grid.sync();
+      pk_bar();
       issue_a();  // next iteration's phase A inputs
       double t[PK_NPART];
       pk_cross_sum<PK_NPART>(A.part, slot, t, red);

@@ -77,12 +77,12 @@ __global__ void __launch_bounds__(T, 1) probe(Args A) {
         if (A.mode == 1) st_ll(llvec + (size_t)v * n + i, x, f);
         else A.vec[(size_t)v * n + i] = x;
       }
-    if (threadIdx.x < NP && A.mode != 3) {
+    if (threadIdx.x < NP && A.mode != 3 && A.mode != 8 && A.mode != 9) {
       const double x = sm[threadIdx.x] + 1.0;
       if (A.mode == 1) st_ll(llpart + (size_t)threadIdx.x * gridDim.x + blockIdx.x, x, f);
       else A.part[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = x;
     }
-    if (A.mode == 0 || A.mode >= 3) {
+    if (A.mode == 0 || (A.mode >= 3 && A.mode < 8)) {
       if (A.mode == 7) {
         __syncthreads();
         if (threadIdx.x == 0) { __threadfence(); }
@@ -114,6 +114,68 @@ __global__ void __launch_bounds__(T, 1) probe(Args A) {
           "r"(parity)
           : "memory");
       if (A.mode == 0 || A.mode == 6) parity ^= 1;
+      __syncthreads();
+    } else if (A.mode >= 8) {
+      // barrier + partials in one trip: per-CTA LL words (value, epoch) written
+      // after a release fence (mode 8) or none (9); mode 10: release/acquire flag + ld.cg partials
+      uint4* lp = llpart;
+      if (A.mode == 10) {
+        __syncthreads();
+        if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(A.flags + blockIdx.x), "r"(f) : "memory");
+        if (threadIdx.x < gridDim.x) {
+          unsigned g;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(A.flags + threadIdx.x) : "memory");
+          } while ((int)(g - f) < 0);
+        }
+        __syncthreads();
+      } else {
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          if (A.mode == 8 && threadIdx.x == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          __syncwarp();
+          if (threadIdx.x < NP) st_ll(lp + (size_t)blockIdx.x * 16 + threadIdx.x, sm[threadIdx.x] + 1.0, f);
+        }
+        if (threadIdx.x < gridDim.x) {
+          const uint4* q = lp + (size_t)threadIdx.x * 16;
+          double s = 0.0;
+          for (int k = 0; k < NP; ++k) {
+            uint4 r;
+            do { r = ld_ll(q + k); } while (r.y != f || r.w != f);
+            s += ll_val(r);
+          }
+          if (A.mode == 8) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          acc += s * 1e-300;
+        }
+        __syncthreads();
+      }
+      if (threadIdx.x == T - 32) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        const unsigned bytes = (unsigned)(n * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(V * bytes)
+                     : "memory");
+        for (int v = 0; v < V; ++v)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(sm + v * n)),
+              "l"(A.vec + (size_t)v * n), "r"(bytes), "r"(smem_u32(&bar))
+              : "memory");
+      }
+      if (A.mode == 10) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (warp < NP) {
+          double s = 0.0;
+          for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(A.part + (size_t)warp * gridDim.x + b);
+          for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == 0) red[warp] = s;
+        }
+      }
+      asm volatile(
+          "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}" ::"r"(
+              smem_u32(&bar)),
+          "r"(parity)
+          : "memory");
+      parity ^= 1;
       __syncthreads();
     } else if (A.mode == 1) {
       // poll all V*n entries + NP*grid partials; up to 16 entries per thread in flight
@@ -214,7 +276,7 @@ int main() {
   cudaMalloc(&vec, 3 * 2048 * 8);
   cudaMalloc(&part, 16 * G * 8);
   cudaMalloc(&llvec, 2 * 3 * 2048 * 16);
-  cudaMalloc(&llpart, 2 * 16 * G * 16);
+  cudaMalloc(&llpart, 2 * 16 * G * 16 + 16 * G * 16);
   cudaMalloc(&flags, G * 4);
   cudaMemset(llvec, 0, 2 * 3 * 2048 * 16);
   cudaMemset(llpart, 0, 2 * 16 * G * 16);
@@ -226,11 +288,11 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   unsigned epoch = 1;
-  const char* names[] = {"grid.sync+TMA", "LL poll", "flag+loads", "sync only", "stores+sync", "+partials", "+TMA only", "stores+fence"};
+  const char* names[] = {"grid.sync+TMA", "LL poll", "flag+loads", "sync only", "stores+sync", "+partials", "+TMA only", "stores+fence", "LL part+fence", "LL part nofence", "rel/acq flag"};
   for (int n : {1000, 2000})
-    for (int V : {1, 3})
-      for (int NP : {2})
-        for (int mode = 0; mode < 8; ++mode) {
+    for (int V : {3})
+      for (int NP : {3, 14})
+        for (int mode : {0, 3, 8, 9, 10}) {
           float best = 1e9;
           for (int rep = 0; rep < 3; ++rep) {
             Args A{n, V, NP, 400, mode, vec, part, llvec, llpart, flags, out, epoch};
