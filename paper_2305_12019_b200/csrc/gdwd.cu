@@ -1858,7 +1858,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
     // kernel version: 3 barriers per iteration (default) or the 4-barrier
     // association (GDWD_PK_VERSION=2, kept for A/B checks)
     ctx->pk_version = (getenv("GDWD_PK_VERSION") && atoi(getenv("GDWD_PK_VERSION")) == 2) ? 2 : 3;
-    const void* kfn = ctx->pk_version == 3 ? (const void*)gram_smw_persistent3 : (const void*)gram_smw_persistent;
+    const void* kfn = ctx->pk_version == 3 ? (const void*)gram_smw_persistent3<0> : (const void*)gram_smw_persistent;
     if (sm > 220 * 1024 || cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
       cudaGetLastError();
       ctx->persistent = false;
@@ -1910,11 +1910,20 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
         ctr = reinterpret_cast<unsigned*>(ctx->pk_part.p + (size_t)2 * NUM_SMS * PK_NPART);
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), ctx->st));
       }
+      // own rows of K and GK resident in tensor memory when n <= 1024 (<= 7
+      // rows per CTA, 8 ceil(n/64) words per lane and row).  K alone (n <=
+      // 2048) measured slower than streaming both from L2 (c2: 42.7 vs 37.8
+      // us/iteration, same run): the GK stream stays latency-bound and the
+      // TMEM words cost the registers that kept 16 loads in flight.
+      int tmem = ctx->n <= 1024 ? 2 : 0;
+      if (getenv("GDWD_PK_TMEM")) tmem = std::min(tmem, atoi(getenv("GDWD_PK_TMEM")));
       PK3Args pa{D, ctx->kmat.p, ctx->gkmat.p, D.kap, D.gam, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host,
                  diag, ts, ctx->use_sgs ? 1 : 0, ctr};
       void* args[] = {&pa};
+      const void* kfn = tmem == 2 ? (const void*)gram_smw_persistent3<2> : (const void*)gram_smw_persistent3<0>;
+      CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       Launch L(ctx, "persistent_gram_smw2");
-      CK(cudaLaunchCooperativeKernel((void*)gram_smw_persistent3, dim3(NUM_SMS), dim3(PK_THREADS), args, sm, ctx->st));
+      CK(cudaLaunchCooperativeKernel(kfn, dim3(NUM_SMS), dim3(PK_THREADS), args, sm, ctx->st));
     } else {
       PKArgs pa{D, ctx->kmat.p, ctx->fac.p, ctx->gkmat.p, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host, diag, ts,
                 ctx->use_sgs ? 1 : 0};

@@ -81,6 +81,124 @@ GDWD_DEV void pk_row_dot_ab(const double* ra, const double* const (&xa)[NA], con
   for (int v = 0; v < NB; ++v) ob[v] = a0[NA + v];
 }
 
+
+// ---------------------------------------------------------------------------
+// Tensor memory as a resident store for the CTA's own Gram rows.  TMEM is 128
+// lanes x 512 columns x 32 bit per SM and a warp reaches only its lane
+// quarter (warp % 4), so warp w keeps its row (r = w, at most 16 rows per CTA)
+// in quarter w % 4, row block w / 4.  Lane l holds the row's columns
+// 2l + 64u, 2l + 64u + 1 (u < U = ceil(n/64)) as 4 words per chunk u -- the
+// same distribution the L2 row dot uses, so a 32x32b load of 32 words hands
+// each lane 8 chunks.  Reads run at ~400 B/cycle/SM (profiles/probes/
+// tmem_probe.cu) against ~110 B/cycle/SM from L2.
+// ---------------------------------------------------------------------------
+GDWD_DEV void tm_ld32(uint32_t addr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+}
+GDWD_DEV void tm_ld16(uint32_t addr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(addr));
+}
+GDWD_DEV void tm_st4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+GDWD_DEV void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+GDWD_DEV void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// copy row `row` (length n, zero beyond n) into this warp's TMEM block at `addr`
+GDWD_DEV void tm_put_row(uint32_t addr, const double* row, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int U = (int)((n + 63) / 64);
+  for (int u = 0; u < U; ++u) {
+    const int64_t j = 2 * lane + 64 * (int64_t)u;
+    const double2 z = j < n ? __ldg(reinterpret_cast<const double2*>(row + j)) : make_double2(0.0, 0.0);
+    tm_st4(addr + 4 * u, __double2loint(z.x), __double2hiint(z.x), __double2loint(z.y), __double2hiint(z.y));
+  }
+  tm_wait_st();
+}
+
+// Row a from TMEM against NA staged vectors, row b against NB staged vectors
+// with b from TMEM (B_TM) or streamed from L2; same chunk order, FMA chains
+// and butterfly as pk_row_dot_ab.
+template <int NA, int NB, bool B_TM>
+GDWD_DEV void pk_row_dot_tm(uint32_t ta, const double* const (&xa)[NA], uint32_t tb, const double* rb,
+                            const double* const (&xb)[NB], int64_t n, double (&oa)[NA], double (&ob)[NB]) {
+  const int lane = threadIdx.x & 31;
+  double a0[NA + NB], a1[NA + NB];
+#pragma unroll
+  for (int v = 0; v < NA + NB; ++v) a0[v] = a1[v] = 0.0;
+  const int U = (int)((n + 63) / 64);
+  // B from L2: 16 chunks (16 double2 loads per lane) in flight per batch --
+  // the row's latency is its number of L2 round trips; A (and B_TM) from
+  // TMEM in 8-chunk loads inside the batch
+  constexpr int UB = B_TM ? 8 : 16;
+  for (int u0 = 0; u0 < U; u0 += UB) {
+    double2 zb[B_TM ? 1 : UB];
+    if constexpr (!B_TM) {
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int64_t j = 2 * lane + 64 * (int64_t)(u0 + u);
+        zb[u] = j < n ? __ldg(reinterpret_cast<const double2*>(rb + j)) : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < UB / 4; ++h) {  // TMEM words of 4 chunks at a time (register budget)
+      if (u0 + 4 * h >= U) break;        // warp-uniform: never address past the row block
+      uint32_t wa[16], wb[B_TM ? 16 : 1];
+      tm_ld16(ta + 4 * (u0 + 4 * h), wa);
+      if constexpr (B_TM) tm_ld16(tb + 4 * (u0 + 4 * h), wb);
+      tm_wait_ld();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j = 2 * lane + 64 * (int64_t)(u0 + 4 * h + u);
+        const bool ok = j < n;
+        // chunks past the row (>= U) read a neighbouring block: zero them
+        const double kx = ok ? __hiloint2double(wa[4 * u + 1], wa[4 * u]) : 0.0;
+        const double ky = ok ? __hiloint2double(wa[4 * u + 3], wa[4 * u + 2]) : 0.0;
+#pragma unroll
+        for (int v = 0; v < NA; ++v) {
+          const double2 x = ok ? *reinterpret_cast<const double2*>(xa[v] + j) : make_double2(0.0, 0.0);
+          a0[v] = __fma_rn(kx, x.x, a0[v]);
+          a1[v] = __fma_rn(ky, x.y, a1[v]);
+        }
+        double gx, gy;
+        if constexpr (B_TM) {
+          gx = ok ? __hiloint2double(wb[4 * u + 1], wb[4 * u]) : 0.0;
+          gy = ok ? __hiloint2double(wb[4 * u + 3], wb[4 * u + 2]) : 0.0;
+        } else {
+          gx = zb[4 * h + u].x;
+          gy = zb[4 * h + u].y;
+        }
+#pragma unroll
+        for (int v = 0; v < NB; ++v) {
+          const double2 x = ok ? *reinterpret_cast<const double2*>(xb[v] + j) : make_double2(0.0, 0.0);
+          a0[NA + v] = __fma_rn(gx, x.x, a0[NA + v]);
+          a1[NA + v] = __fma_rn(gy, x.y, a1[NA + v]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NA + NB; ++v) a0[v] += a1[v];
+  warp_sum<NA + NB>(a0);
+#pragma unroll
+  for (int v = 0; v < NA; ++v) oa[v] = a0[v];
+#pragma unroll
+  for (int v = 0; v < NB; ++v) ob[v] = a0[NA + v];
+}
+
 struct PK3Args {
   Dev D;
   const double* K;    // n x ld
@@ -96,6 +214,7 @@ struct PK3Args {
   unsigned* ctr;  // grid barrier counter, zero at launch (null: cooperative-groups grid.sync)
 };
 
+template <int TM>  // own rows in TMEM: 0 none, 1 K, 2 K and GK (host picks by n)
 __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A) {
   cg::grid_group grid = cg::this_grid();
   const Dev& D = A.D;
@@ -188,6 +307,25 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
     wait_in();
     if (threadIdx.x == 0) srho[n] = 0.0;  // bulk copies of odd n bring the pad slot along
   }
+  // own Gram rows into tensor memory (once per launch)
+  __shared__ uint32_t tm_base;
+  uint32_t tmK = 0, tmG = 0;
+  if (TM) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tm_base)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t blk = 4u * (uint32_t)((n + 63) / 64) * (uint32_t)TM;  // columns per row block
+    tmK = tm_base + ((uint32_t)(32 * (warp & 3)) << 16) + blk * (uint32_t)(warp >> 2);
+    tmG = tmK + blk / 2;
+    if (warp < nsweep) {
+      tm_put_row(tmK, A.K + (i0 + warp) * A.ld, n);
+      if (TM == 2) tm_put_row(tmG, A.GK + (i0 + warp) * A.ld, n);
+    }
+  }
   // Step 3 operands that do not change during the solve
   if (warp == 0 && lane < nrows) {
     ot_e[lane] = D.e[i0 + lane];
@@ -218,29 +356,45 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
       wait_in();  // xi r alpha x
       if (threadIdx.x == 0) s2[n] = 0.0;  // alpha is swept: zero pad (synced by block_sum)
       PK3_TS(1);
+      // 4 independent elements per thread, predicated (no early exit), so
+      // their division chains overlap; uniform factors computed once
+      const double spmu = sp * mu, tsm = (D.tau * sp) * mu, mus = mu / sig;
+      const bool proj = !(gn <= D.zscale);
+      const double zsg = proj ? D.zscale / gn : 1.0;
 #pragma unroll 1
-      for (int64_t j0 = threadIdx.x; j0 < n; j0 += 4 * PK_THREADS)
+      for (int64_t j0 = threadIdx.x; j0 < n; j0 += 4 * PK_THREADS) {
+        double rhs[4], t1[4], ch[4], uu[4], rr[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int64_t j = j0 + u * PK_THREADS;
-          if (j >= n) break;
+          const int64_t j = j0 + u * PK_THREADS < n ? j0 + u * PK_THREADS : j0;
           double uj = su[j], rj = srho[j];
           if (pending) {  // Step 2 of iteration k-1 (solver.py:535-542)
             const double wj = s3[j];
-            const double gj = wj - rj / (sp * mu);
-            uj = (gn <= D.zscale) ? gj : (D.zscale / gn) * gj;
-            rj = rj - ((D.tau * sp) * mu) * (wj - uj);
-            su[j] = uj;
-            srho[j] = rj;
+            const double gj = wj - rj / spmu;
+            uj = proj ? zsg * gj : gj;
+            rj = rj - tsm * (wj - uj);
           }
-          const double rhs = (s0[j] - s1[j]) - s2[j] / sig;
-          const double chj = (-rhs + mu2 * uj) + (mu / sig) * rj;
-          sh[j] = chj;
-          const double t1 = mu2_one ? chj : chj / mu2;
-          st1[j] = t1;
-          yr += sy[j] * rhs;
-          gt += sgam[j] * t1;
+          rhs[u] = (s0[j] - s1[j]) - s2[j] / sig;
+          ch[u] = (-rhs[u] + mu2 * uj) + mus * rj;
+          t1[u] = mu2_one ? ch[u] : ch[u] / mu2;
+          uu[u] = uj;
+          rr[u] = rj;
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t j = j0 + u * PK_THREADS;
+          if (j < n) {
+            if (pending) {
+              su[j] = uu[u];
+              srho[j] = rr[u];
+            }
+            sh[j] = ch[u];
+            st1[j] = t1[u];
+            yr += sy[j] * rhs[u];
+            gt += sgam[j] * t1[u];
+          }
+        }
+      }
       PK3_TS(2);
       double v2[2] = {yr, gt};
       block_sum<2>(v2, red);
@@ -275,7 +429,9 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
         {
           const double* xa[2] = {s2, srho};
           const double* xg[1] = {st1};
-          pk_row_dot_ab<2, 1>(Ki, xa, GKi, xg, n, oK, oG);  // [K alpha, K rho], GK t1
+          if (TM == 2) pk_row_dot_tm<2, 1, true>(tmK, xa, tmG, GKi, xg, n, oK, oG);
+          else if (TM) pk_row_dot_tm<2, 1, false>(tmK, xa, tmG, GKi, xg, n, oK, oG);
+          else pk_row_dot_ab<2, 1>(Ki, xa, GKi, xg, n, oK, oG);  // [K alpha, K rho], GK t1
         }
         // every lane holds the same sums (butterfly), so all lanes run Newton
         const double s1i = oG[0];
@@ -371,18 +527,27 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
       if (threadIdx.x == 0) s0[n] = s3[n] = 0.0;  // swept vectors: zero pads (synced by block_sum)
       PK3_TS(7);
 #pragma unroll 1
-      for (int64_t j0 = threadIdx.x; j0 < n; j0 += 4 * PK_THREADS)
+      for (int64_t j0 = threadIdx.x; j0 < n; j0 += 4 * PK_THREADS) {
+        double cr[4], dm[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int64_t j = j0 + u * PK_THREADS;
-          if (j >= n) break;
+          const int64_t j = j0 + u * PK_THREADS < n ? j0 + u * PK_THREADS : j0;
           const double drj = s0[j];
           const double h2 = sh[j] + drj;
           const double ax = (s2[j] + mu2 * s1[j]) + sy[j] * bb;
-          s3[j] = h2 - ax;  // c_res
-          if (!mu2_one) st1[j] = drj / mu2;
-          ytz += sy[j] * s2[j];
+          cr[u] = h2 - ax;  // c_res
+          dm[u] = mu2_one ? drj : drj / mu2;
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t j = j0 + u * PK_THREADS;
+          if (j < n) {
+            s3[j] = cr[u];
+            if (!mu2_one) st1[j] = dm[u];
+            ytz += sy[j] * s2[j];
+          }
+        }
+      }
       double v1[1] = {ytz};
       block_sum<1>(v1, red);
       if (threadIdx.x == 0) S.ytzw = v1[0];
@@ -396,7 +561,17 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
         const double* xs[2] = {s3, sdr};
         const double s1i = o_s1[r], jyi = sjy[i], yi = sy[i];
         double o[2];
-        pk_row_dot<2>(rows, n, xs, o);
+        if (TM) {
+          const double* xa1[1] = {s3};
+          const double* xb1[1] = {sdr};
+          double oa[1], ob[1];
+          if (TM == 2) pk_row_dot_tm<1, 1, true>(tmK, xa1, tmG, rows[1], xb1, n, oa, ob);
+          else pk_row_dot_tm<1, 1, false>(tmK, xa1, tmG, rows[1], xb1, n, oa, ob);
+          o[0] = oa[0];
+          o[1] = ob[0];
+        } else {
+          pk_row_dot<2>(rows, n, xs, o);
+        }
         if (lane == 0) {
           q += s3[i] * o[0];
           const double gpi = (s1i + o[1]) + t2 * (ynorm * jyi);
@@ -581,6 +756,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
     D.rho[j] = srho[j];
   }
   __syncthreads();
+  if (TM && warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm_base));
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     Scal* G = D.S;
     G->k = S.k; G->stopped = S.stopped; G->converged = S.converged; G->reuse = S.reuse;

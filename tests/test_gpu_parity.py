@@ -259,15 +259,20 @@ def test_iter_gram_operator_matches_reference(case):
     assert relerr(out2.final_state.w, tr["final_w"]) < 1e-6
 
 
-@pytest.mark.parametrize("version", ["3", "2"])
+@pytest.mark.parametrize("version", ["3", "3-l2", "2"])
 @pytest.mark.parametrize("case", TRAJ_CASES + VAR_CASES)
 def test_persistent_iterates_match_reference(case, version, monkeypatch):
     """The persistent Gram-space kernel (SMW2, and DIRECT with 2n <= d) run
     for k = 1, 2, 7, 20 iterations in one launch, no callback: its state after
     iteration k against the reference's iterate k (1e-9 relative), for the
-    3-barrier association (default) and the 4-barrier one.  Cases outside
+    3-barrier association (default; own rows from tensor memory or L2) and
+    the 4-barrier one.  Cases outside
     the Gram-space regime run the graph path (same check)."""
-    monkeypatch.setenv("GDWD_PK_VERSION", version)
+    # "3": 3-barrier kernel (rows in tensor memory at these sizes), "3-l2":
+    # the same streaming its rows from L2 (the n > 1024 path), "2": 4-barrier
+    monkeypatch.setenv("GDWD_PK_VERSION", version[0])
+    if version == "3-l2":
+        monkeypatch.setenv("GDWD_PK_TMEM", "0")
     tr = load_traj(case)
     prob = problem_for(tr)
     full = bool(tr["full"])
