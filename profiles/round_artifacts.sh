@@ -17,5 +17,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gram_smw_persistent -c 1 \
   -o $O/ncu_persistent_c2 python profiles/run_c2.py 200 > $O/ncu_full.log 2>&1
 ncu -i $O/ncu_persistent_c2.ncu-rep --page raw --csv > $O/ncu_persistent_c2_raw.csv 2>/dev/null
+python profiles/ncu_summary.py $O/ncu_persistent_c2_raw.csv > $O/ncu_persistent_c2_summary.csv
+# per-phase timing of the persistent kernel (CTA clock stamps), c2 and c1
+GDWD_PK_TIMING=1 timeout 300 python profiles/run_c2.py 100 > $O/persistent_phase_timing.txt 2>&1
 timeout 1500 python bench.py --config c5 --no-cpu --no-next > $O/bench_c5.json 2> $O/bench_c5.err
 echo done
