@@ -174,17 +174,23 @@ __global__ void syrk_finish_kernel(const double* W, int64_t ldw, int64_t wslice,
   }
 }
 
-// Dense factor + inverse of one diagonal block (m <= 64) in shared memory:
-// A = L L^T (L lower), Linv = L^{-1}.  Upper parts are written as zeros.
+// Dense factor + inverse of one diagonal block (m <= LEAF_MAX) in shared
+// memory: A = L L^T (L lower), Linv = L^{-1}.  Upper parts are written as
+// zeros.  The inverse is a forward substitution on the identity with every
+// column in flight at once (thread c owns column c, reads only shared
+// memory); each of the m steps is one division after an FMA chain over the
+// already-final entries (two chains, even / odd k).
+constexpr int LEAF_MAX = 48;  // two (LEAF_MAX x LEAF_MAX+1) doubles in static shared memory
 __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t ldl, int m, int* info,
                                   int64_t offset) {
-  __shared__ double L[64][65];
+  __shared__ double L[LEAF_MAX][LEAF_MAX + 1];
+  __shared__ double Li[LEAF_MAX][LEAF_MAX + 1];
   __shared__ int bad;
   const int t = threadIdx.x;
   if (t == 0) bad = 0;
-  for (int idx = t; idx < 64 * 64; idx += blockDim.x) {
-    int i = idx >> 6, j = idx & 63;
-    L[i][j] = (i < m && j < m && j <= i) ? A[i * lda + j] : 0.0;
+  for (int idx = t; idx < m * m; idx += blockDim.x) {
+    const int i = idx / m, j = idx % m;
+    L[i][j] = (j <= i) ? A[i * lda + j] : 0.0;
   }
   __syncthreads();
   for (int j = 0; j < m; ++j) {
@@ -196,30 +202,46 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
     __syncthreads();
     for (int i = j + 1 + t; i < m; i += blockDim.x) L[i][j] = L[i][j] / L[j][j];
     __syncthreads();
-    // trailing lower triangle only: (i, k) with j < k <= i < m
-    const int w = m - j - 1;
-    for (int idx = t; idx < w * w; idx += blockDim.x) {
-      const int i = j + 1 + idx / w, k = j + 1 + idx % w;
-      if (k <= i) L[i][k] -= L[i][j] * L[k][j];
+    // trailing lower triangle only: (i, k) with j < k <= i < m; thread t
+    // takes column k = j+1 + t%32 of rows i = j+1 + t/32 + 8q (no integer
+    // division in the loop; blockDim = 256)
+    {
+      const int k = j + 1 + (t & 31);
+      if (k < m) {
+        const double lkj = L[k][j];
+        for (int i = j + 1 + (t >> 5); i < m; i += 8)
+          if (k <= i) L[i][k] -= L[i][j] * lkj;
+      }
+      for (int k2 = j + 33 + (t & 31); k2 < m; k2 += 32) {  // m > 33 only
+        const double lkj = L[k2][j];
+        for (int i = j + 1 + (t >> 5); i < m; i += 8)
+          if (k2 <= i) L[i][k2] -= L[i][j] * lkj;
+      }
     }
     __syncthreads();
   }
-  // Linv by forward substitution, one column per thread, written straight
-  // to global memory (each thread re-reads only its own column)
-  if (t < 64) {
+  if (t < m) {
     const int c = t;
     for (int i = 0; i < m; ++i) {
-      if (c >= m) break;
-      if (i < c) { Linv[i * ldl + c] = 0.0; continue; }
-      double s = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; ++k) s -= L[i][k] * Linv[k * ldl + c];
-      Linv[i * ldl + c] = s / L[i][i];
+      if (i < c) {
+        Li[i][c] = 0.0;
+        continue;
+      }
+      double s0 = (i == c) ? 1.0 : 0.0, s1 = 0.0;
+      int k = c;
+      for (; k + 1 < i; k += 2) {
+        s0 -= L[i][k] * Li[k][c];
+        s1 -= L[i][k + 1] * Li[k + 1][c];
+      }
+      if (k < i) s0 -= L[i][k] * Li[k][c];
+      Li[i][c] = (s0 + s1) / L[i][i];
     }
   }
   __syncthreads();
   for (int idx = t; idx < m * m; idx += blockDim.x) {
-    int i = idx / m, j = idx % m;
+    const int i = idx / m, j = idx % m;
     A[i * lda + j] = (j <= i) ? L[i][j] : 0.0;
+    Linv[i * ldl + j] = Li[i][j];
   }
   if (t == 0 && bad && info) atomicCAS(info, 0, (int)offset + 1);
 }
@@ -309,8 +331,9 @@ cudaError_t gram_syrk(const double* Zs, int64_t R, int64_t Lc, int64_t ldz, bool
 namespace {
 
 #ifndef CHOL_LEAF
-#define CHOL_LEAF 32  // diagonal blocks factored by one CTA (<= 64); the recursion's critical path
+#define CHOL_LEAF 32  // diagonal blocks factored by one CTA; the recursion's critical path
 #endif
+static_assert(CHOL_LEAF <= LEAF_MAX, "leaf larger than potrf_trtri_small's shared arrays");
 // Recursive blocked Cholesky + triangular inverse (lower):
 //   A (m x m, ld) is overwritten by L; Li (ld) receives L^{-1}; T scratch.
 cudaError_t chol_rec(double* A, double* Li, double* T, int64_t ld, int64_t m, int64_t off, int* info,
