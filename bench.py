@@ -162,8 +162,15 @@ class Dist:
 def kernel_bytes(tag: str, n: int, d: int, nnz: int | None = None) -> float | None:
     """Algorithmic HBM bytes of one launch (roofline section):
     the matrix once plus the vectors read/written.  Sparse X: 12 B per
-    stored entry (f64 value + int32 index) per orientation."""
+    stored entry (f64 value + int32 index) for the CSR products, 10 B for
+    the feature-blocked Z~^T w (16-bit indices)."""
     x = 8.0 * n * d if nnz is None else 12.0 * nnz + 8.0 * (max(n, d) + 1)
+    if nnz is not None and tag.startswith("ztmv_"):
+        # feature-blocked sliced ELL (spops.cuh): f64 value + 16-bit block-local
+        # index per entry, per-(sample, block) permutation and count (2 + 2 B);
+        # the slices' padding is overhead, not algorithmic bytes
+        nb = -(-d // 8192)
+        return 10.0 * nnz + 4.0 * n * nb + 8.0 * (d + 6 * n)
     if tag.startswith("zmv_"):
         return x + 8.0 * (5 * n + 2 * d)   # up to 2 RHS in (+ inputs), 2 d-vectors out
     if tag.startswith("ztmv_"):

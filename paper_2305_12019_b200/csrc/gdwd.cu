@@ -77,6 +77,17 @@ static Api& api() {
 namespace {
 
 constexpr int NUM_SMS = 148;
+// feature-blocked sliced ELL (sp_ztmv_fb_kernel): block width, parts (CTAs)
+// and slice rows per lane in flight
+constexpr int FB_COLS = 8192;
+constexpr int FB_PARTS = 2 * NUM_SMS;
+constexpr size_t FB_SMEM_MAX = 100 * 1024;
+#ifndef FB_H
+#define FB_H 2
+#endif
+#ifndef FB_U
+#define FB_U 8
+#endif
 
 // Device memory comes from the device's default stream-ordered pool, whose
 // release threshold is raised at context creation: freed blocks stay
@@ -193,6 +204,13 @@ struct gdwd_ctx {
   int64_t *csc_ptr = nullptr, *csr_ptr = nullptr;
   int *csc_idx = nullptr, *csr_idx = nullptr;
   double *csc_val = nullptr, *csr_val = nullptr;
+  // feature-blocked CSC (spops.cuh FbView) for Z~^T w
+  int* fb_ptr = nullptr;
+  unsigned short *fb_perm = nullptr, *fb_cnt = nullptr, *fb_idx = nullptr;
+  double* fb_val = nullptr;
+  int fb_nb = 0, fb_parts = 0, fb_S = 0, fb_Q = 0;
+  int64_t fb_entries = 0;  // padded entries
+  bool sp_blocked = getenv("GDWD_SP_BLOCKED") ? atoi(getenv("GDWD_SP_BLOCKED")) != 0 : true;
   DevBuf tbuf;  // materialised Z t inputs (2 x n)
   DevBuf y, e, wl;
   // scratch
@@ -376,7 +394,17 @@ static void run_zt(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "zt
   const Scratch sc = sh ? scr_bundle(ctx) : ctx->scr;
   {
     Launch L(ctx, tag);
-    if (!X.a) {
+    if (!X.a && ctx->fb_parts && ctx->sp_blocked) {
+      FbView A{ctx->fb_ptr, ctx->fb_perm, ctx->fb_cnt, ctx->fb_idx, ctx->fb_val, ctx->n, ctx->d,
+               ctx->fb_nb, FB_COLS, ctx->fb_parts, ctx->fb_S, ctx->fb_Q};
+      const size_t sm = (size_t)(FB_COLS + ctx->fb_S) * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(sp_ztmv_fb_kernel<Op, FB_H, FB_U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_SMEM_MAX);
+        attr = true;
+      }
+      sp_ztmv_fb_kernel<Op, FB_H, FB_U><<<ctx->fb_parts, SP_THREADS, sm, ctx->st>>>(op, A, sc);
+    } else if (!X.a) {
       SpView A{ctx->csc_ptr, ctx->csc_idx, ctx->csc_val, ctx->n, ctx->d};
       sp_ztmv_kernel<Op, 8><<<sp_grid(ctx->n, NUM_SMS * 8), SP_THREADS, 0, ctx->st>>>(op, A, sc);
     } else {
@@ -610,11 +638,17 @@ static int compute_fro2(gdwd_ctx* ctx, const double* a, int64_t rows, int64_t co
 
 static void free_sparse(gdwd_ctx* ctx) {
   for (void* p : {(void*)ctx->csc_ptr, (void*)ctx->csr_ptr, (void*)ctx->csc_idx, (void*)ctx->csr_idx,
-                  (void*)ctx->csc_val, (void*)ctx->csr_val})
+                  (void*)ctx->csc_val, (void*)ctx->csr_val, (void*)ctx->fb_ptr, (void*)ctx->fb_idx,
+                  (void*)ctx->fb_val, (void*)ctx->fb_perm, (void*)ctx->fb_cnt})
     dfree(p, ctx->st);
   ctx->csc_ptr = ctx->csr_ptr = nullptr;
   ctx->csc_idx = ctx->csr_idx = nullptr;
   ctx->csc_val = ctx->csr_val = nullptr;
+  ctx->fb_ptr = nullptr;
+  ctx->fb_idx = ctx->fb_perm = ctx->fb_cnt = nullptr;
+  ctx->fb_val = nullptr;
+  ctx->fb_nb = ctx->fb_parts = ctx->fb_S = ctx->fb_Q = 0;
+  ctx->fb_entries = 0;
   ctx->has_sparse = false;
   ctx->nnz = 0;
 }
@@ -793,29 +827,76 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
   if (colptr[0] != 0 || nnz < 0) return set_err(ctx, GDWD_ERR_VALUE, "colptr endpoints do not match stored entries");
   if (nnz >= ((int64_t)1 << 31)) return set_err(ctx, GDWD_ERR_UNSUPPORTED, "nnz >= 2^31 per shard");
   if (nnz > 0 && (!rowidx || !values)) return set_err(ctx, GDWD_ERR_VALUE, "null CSC arrays");
+  const bool tmark = getenv("GDWD_SETUP_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto hmark = [&](const char* what) {
+    if (!tmark) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[upload timing] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   // validate + transpose to CSR on the host (counting sort keeps sample order
-  // within each feature row, so row sums accumulate like np.bincount)
-  std::vector<int64_t> rp(d + 1, 0);
+  // within each feature row, so row sums accumulate like np.bincount), on
+  // all host cores: threads own contiguous sample ranges, per-thread row
+  // histograms give every (thread, row) its output offset, so the scatter
+  // keeps sample order.  The error reported is the first one in sample order
+  // (a sample's colptr before its indices), as a sequential pass finds it.
+  const int T = (int)std::max<int64_t>(1, std::min<int64_t>({16, (int64_t)std::thread::hardware_concurrency(), n / 1024 + 1}));
+  auto par = [&](auto&& fn) {
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t) th.emplace_back([&, t]() { fn(t, n * t / T, n * (t + 1) / T); });
+    for (auto& x : th) x.join();
+  };
+  std::vector<int64_t> bad_ptr(T, n), bad_idx(T, n);
+  par([&](int t, int64_t i0, int64_t i1) {
+    for (int64_t i = i0; i < i1; ++i)
+      if (colptr[i + 1] < colptr[i]) {
+        bad_ptr[t] = i;
+        break;
+      }
+  });
+  const int64_t first_ptr = *std::min_element(bad_ptr.begin(), bad_ptr.end());
+  std::vector<std::vector<int64_t>> hist(T);
   std::vector<int> ci32((size_t)nnz);
-  for (int64_t i = 0; i < n; ++i) {
-    if (colptr[i + 1] < colptr[i]) return set_err(ctx, GDWD_ERR_VALUE, "colptr must be nondecreasing");
-    for (int64_t k = colptr[i]; k < colptr[i + 1]; ++k) {
-      const int64_t r = rowidx[k];
-      if (r < 0 || r >= d) return set_err(ctx, GDWD_ERR_VALUE, "row index out of bounds");
-      rp[r + 1]++;
-      ci32[k] = (int)r;
+  par([&](int t, int64_t i0, int64_t i1) {
+    hist[t].assign(d, 0);
+    int64_t* h = hist[t].data();
+    for (int64_t i = i0; i < std::min(i1, first_ptr); ++i)
+      for (int64_t k = colptr[i]; k < colptr[i + 1]; ++k) {
+        const int64_t r = rowidx[k];
+        if (r < 0 || r >= d) {
+          bad_idx[t] = i;
+          return;
+        }
+        h[r]++;
+        ci32[k] = (int)r;
+      }
+  });
+  const int64_t first_idx = *std::min_element(bad_idx.begin(), bad_idx.end());
+  if (first_idx < n && first_idx < first_ptr) return set_err(ctx, GDWD_ERR_VALUE, "row index out of bounds");
+  if (first_ptr < n) return set_err(ctx, GDWD_ERR_VALUE, "colptr must be nondecreasing");
+  std::vector<int64_t> rp(d + 1, 0);
+  for (int64_t j = 0; j < d; ++j) {  // row starts, then each thread's offset within the row
+    int64_t o = rp[j];
+    for (int t = 0; t < T; ++t) {
+      const int64_t c = hist[t][j];
+      hist[t][j] = o;
+      o += c;
     }
+    rp[j + 1] = o;
   }
-  for (int64_t j = 0; j < d; ++j) rp[j + 1] += rp[j];
-  std::vector<int64_t> fillp(rp.begin(), rp.end() - 1);
   std::vector<int> cidx((size_t)nnz);
   std::vector<double> cval((size_t)nnz);
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t k = colptr[i]; k < colptr[i + 1]; ++k) {
-      const int64_t pos = fillp[rowidx[k]]++;
-      cidx[pos] = (int)i;
-      cval[pos] = values[k];
-    }
+  par([&](int t, int64_t i0, int64_t i1) {
+    int64_t* fillp = hist[t].data();
+    for (int64_t i = i0; i < i1; ++i)
+      for (int64_t k = colptr[i]; k < colptr[i + 1]; ++k) {
+        const int64_t pos = fillp[rowidx[k]]++;
+        cidx[pos] = (int)i;
+        cval[pos] = values[k];
+      }
+  });
+  hmark("validate + CSR transpose");
   CK(cudaSetDevice(ctx->device));
   free_sparse(ctx);
   dfree(ctx->Zs, ctx->st);
@@ -835,6 +916,112 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
     CK(cudaMemcpy(ctx->csr_idx, cidx.data(), nnz * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->csc_val, values, nnz * sizeof(double), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->csr_val, cval.data(), nnz * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  // feature-blocked CSC: parts of S samples (one CTA each, 2 per SM) x
+  // feature blocks of FB_COLS; within (part, block) the samples in order,
+  // each sample's entries in CSC order, 16-bit block-local feature indices
+  hmark("CSC + CSR to device");
+  // feature-blocked sliced ELL (spops.cuh FbView): parts of S samples (one
+  // CTA each) x feature blocks of FB_COLS; per (part, block) the samples
+  // sorted by entry count (descending, then index) in slices of 32, entries
+  // column-major within a slice, 16-bit block-local indices
+  const int fb_S = (int)((n + FB_PARTS - 1) / FB_PARTS);
+  if (nnz > 0 && fb_S < 65535 && (size_t)(FB_COLS + fb_S) * sizeof(double) <= FB_SMEM_MAX) {
+    const int parts = FB_PARTS, S = fb_S, Q = (S + 31) / 32;
+    const int nb = (int)((d + FB_COLS - 1) / FB_COLS);
+    std::vector<int> sbase((size_t)parts * nb * (Q + 1));
+    std::vector<unsigned short> perm((size_t)parts * nb * 32 * Q, 0xffff), cnt((size_t)parts * nb * 32 * Q, 0);
+    // parts are independent: built on all host cores into per-part arrays,
+    // slice starts relative to the part, then concatenated
+    std::vector<std::vector<unsigned short>> pidx(parts);
+    std::vector<std::vector<double>> pval(parts);
+    auto build_part = [&](int p) {
+      const int64_t a = std::min<int64_t>(n, (int64_t)p * S), z = std::min<int64_t>(n, a + S);
+      std::vector<int> start((size_t)nb * (S + 1), 0);
+      for (int64_t i = a; i < z; ++i)
+        for (int64_t k = colptr[i]; k < colptr[i + 1]; ++k) start[(size_t)(rowidx[k] / FB_COLS) * (S + 1) + (i - a) + 1]++;
+      for (size_t t = 1; t < start.size(); ++t) start[t] += start[t - 1];
+      const int64_t pn = colptr[z] - colptr[a];
+      std::vector<unsigned short> lidx((size_t)pn);
+      std::vector<double> lval((size_t)pn);
+      {
+        std::vector<int> cur(start);
+        for (int64_t i = a; i < z; ++i)
+          for (int64_t k = colptr[i]; k < colptr[i + 1]; ++k) {
+            const int64_t r = rowidx[k], f = r / FB_COLS;
+            const int at = cur[(size_t)f * (S + 1) + (i - a)]++;
+            lidx[at] = (unsigned short)(r - f * FB_COLS);
+            lval[at] = values[k];
+          }
+      }
+      std::vector<int> ord(S);
+      auto& sv = pval[p];
+      auto& si = pidx[p];
+      for (int f = 0; f < nb; ++f) {
+        const int* st = &start[(size_t)f * (S + 1)];
+        auto count = [&](int ls) { return ls < (int)(z - a) ? st[ls + 1] - st[ls] : 0; };
+        for (int ls = 0; ls < S; ++ls) ord[ls] = ls;
+        std::sort(ord.begin(), ord.end(), [&](int x, int y) {
+          const int cx = count(x), cy = count(y);
+          return cx != cy ? cx > cy : x < y;
+        });
+        const size_t pf = (size_t)p * nb + f;
+        for (int q = 0; q < Q; ++q) {
+          sbase[pf * (Q + 1) + q] = (int)sv.size();
+          const int len = count(ord[32 * q]);
+          const size_t b = sv.size();
+          sv.resize(b + (size_t)32 * len, 0.0);
+          si.resize(b + (size_t)32 * len, 0);
+          for (int l = 0; l < 32 && 32 * q + l < S; ++l) {
+            const int ls = ord[32 * q + l], c = count(ls);
+            perm[pf * 32 * Q + 32 * q + l] = ls < (int)(z - a) ? (unsigned short)ls : 0xffff;
+            cnt[pf * 32 * Q + 32 * q + l] = (unsigned short)c;
+            for (int j = 0; j < c; ++j) {
+              sv[b + (size_t)32 * j + l] = lval[st[ls] + j];
+              si[b + (size_t)32 * j + l] = lidx[st[ls] + j];
+            }
+          }
+        }
+        sbase[pf * (Q + 1) + Q] = (int)sv.size();
+      }
+    };
+    {
+      const unsigned nthr = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+      std::vector<std::thread> th;
+      for (unsigned t = 0; t < nthr; ++t)
+        th.emplace_back([&, t]() {
+          for (int p = (int)t; p < parts; p += (int)nthr) build_part(p);
+        });
+      for (auto& x : th) x.join();
+    }
+    hmark("sliced ELL build (threads)");
+    std::vector<size_t> poff(parts + 1, 0);
+    for (int p = 0; p < parts; ++p) poff[p + 1] = poff[p] + pval[p].size();
+    for (int p = 0; p < parts; ++p)
+      for (size_t t = (size_t)p * nb * (Q + 1); t < (size_t)(p + 1) * nb * (Q + 1); ++t) sbase[t] += (int)poff[p];
+    if (poff[parts] < ((size_t)1 << 31)) {
+      const size_t ne = std::max<size_t>(poff[parts], 1);
+      CK(dmalloc((void**)&ctx->fb_ptr, sbase.size() * sizeof(int), ctx->st));
+      CK(dmalloc((void**)&ctx->fb_perm, perm.size() * sizeof(unsigned short), ctx->st));
+      CK(dmalloc((void**)&ctx->fb_cnt, cnt.size() * sizeof(unsigned short), ctx->st));
+      CK(dmalloc((void**)&ctx->fb_idx, ne * sizeof(unsigned short), ctx->st));
+      CK(dmalloc((void**)&ctx->fb_val, ne * sizeof(double), ctx->st));
+      CK(cudaMemcpy(ctx->fb_ptr, sbase.data(), sbase.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ctx->fb_perm, perm.data(), perm.size() * sizeof(unsigned short), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ctx->fb_cnt, cnt.data(), cnt.size() * sizeof(unsigned short), cudaMemcpyHostToDevice));
+      for (int p = 0; p < parts; ++p)
+        if (!pval[p].empty()) {
+          CK(cudaMemcpy(ctx->fb_idx + poff[p], pidx[p].data(), pidx[p].size() * sizeof(unsigned short),
+                        cudaMemcpyHostToDevice));
+          CK(cudaMemcpy(ctx->fb_val + poff[p], pval[p].data(), pval[p].size() * sizeof(double), cudaMemcpyHostToDevice));
+        }
+      ctx->fb_nb = nb;
+      ctx->fb_parts = parts;
+      ctx->fb_S = S;
+      ctx->fb_Q = Q;
+      ctx->fb_entries = (int64_t)poff[parts];
+    }
+    hmark("sliced ELL concat + to device");
   }
   CK(ctx->tbuf.ensure((size_t)2 * n));
   ctx->n = n;

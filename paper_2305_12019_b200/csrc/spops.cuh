@@ -194,6 +194,117 @@ __global__ void __launch_bounds__(SP_THREADS) sp_ztmv_kernel(Op op, SpView A, Sc
   }
 }
 
+// ---------------------------------------------------------------------------
+// Feature-blocked, sliced-ELL storage for Z~^T w.  The plain CSC kernel is
+// bound by its gathers of w (random 8-byte reads of a d-vector, one L1TEX
+// tag lookup each).  Here the samples are split into `parts` contiguous
+// ranges (one CTA each) and the features into blocks of `fb` (<= 65535):
+// the CTA stages w's block in shared memory (op.wval, the values the CSC
+// kernel gathers) and gathers from there.  Within (part, block) the samples
+// are ordered by their entry count (descending) and cut into slices of 32;
+// slice q stores its entries column-major (entry j of the slice's lane l at
+// base_q + 32 j + l), padded to the slice's longest sample, so a warp reads
+// 32 consecutive values and 16-bit block-local indices per step -- fully
+// coalesced -- and each lane sums its own sample's entries in CSC order.
+// Each sample's running dot stays in shared memory across the blocks (block
+// order fixed: deterministic); the per-sample epilogue runs at the end.
+//   sbase[(p*nb + f)*(Q+1) + q]: first padded entry of slice q (Q = S/32 slices)
+//   perm / cnt[((p*nb + f)*Q + q)*32 + l]: local sample (0xffff: none) and entry count of lane l
+// ---------------------------------------------------------------------------
+struct FbView {
+  const int* sbase;
+  const unsigned short* perm;
+  const unsigned short* cnt;
+  const unsigned short* idx;
+  const double* val;
+  int64_t n, d;
+  int nb, fb, parts, S, Q;
+};
+
+template <class Op, int H, int U>
+__global__ void __launch_bounds__(SP_THREADS) sp_ztmv_fb_kernel(Op op, FbView A, Scratch s) {
+  constexpr int NN = Op::NN;
+  if (op.skip()) return;
+  extern __shared__ double fbsm[];
+  double* wsm = fbsm;          // [fb] staged w block
+  double* dot = fbsm + A.fb;   // [S] running dots of the part's samples
+  __shared__ double red[(SP_THREADS / 32) * NN];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int p = blockIdx.x;
+  const int64_t s0 = (int64_t)p * A.S;
+  const int ns = s0 < A.n ? (int)min((int64_t)A.S, A.n - s0) : 0;
+  for (int f = 0; f < A.nb; ++f) {
+    const int64_t j0 = (int64_t)f * A.fb;
+    const int jn = (int)min((int64_t)A.fb, A.d - j0);
+    __syncthreads();  // the previous block's gathers are done
+    for (int j = threadIdx.x; j < jn; j += SP_THREADS) wsm[j] = op.wval(j0 + j);
+    __syncthreads();
+    const int64_t pf = (int64_t)p * A.nb + f;
+    const int* sb = A.sbase + pf * (A.Q + 1);
+    // H slices per warp at a time (H*U rows in flight per lane)
+    for (int q0 = H * warp; q0 < A.Q; q0 += H * (SP_THREADS / 32)) {
+      int b[H], len[H], ls[H], c[H];
+      double acc[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        acc[h] = 0.0;
+        const int q = q0 + h < A.Q ? q0 + h : q0;
+        b[h] = sb[q];
+        len[h] = q0 + h < A.Q ? (sb[q + 1] - b[h]) >> 5 : 0;
+        const int64_t pl = (pf * A.Q + q) * 32 + lane;
+        ls[h] = q0 + h < A.Q ? A.perm[pl] : 0xffff;
+        c[h] = A.cnt[pl];
+      }
+      int lmax = 0;
+#pragma unroll
+      for (int h = 0; h < H; ++h) lmax = len[h] > lmax ? len[h] : lmax;
+      for (int j0 = 0; j0 < lmax; j0 += U) {
+        double v[H][U];
+        int ix[H][U];
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {  // clamped rows of the slice: never past its end
+            const int j = j0 + u < len[h] ? j0 + u : (len[h] > 0 ? len[h] - 1 : 0);
+            const int64_t at = (int64_t)b[h] + 32 * j + lane;
+            v[h][u] = len[h] > 0 ? __ldg(A.val + at) : 0.0;
+            ix[h][u] = len[h] > 0 ? __ldg(A.idx + at) : 0;
+          }
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (j0 + u < c[h]) acc[h] += v[h][u] * wsm[ix[h][u]];
+      }
+#pragma unroll
+      for (int h = 0; h < H; ++h)
+        if (ls[h] < ns) dot[ls[h]] = (f == 0) ? acc[h] : dot[ls[h]] + acc[h];  // pad lanes: ls = 0xffff
+    }
+  }
+  __syncthreads();
+  double nacc[NN];
+#pragma unroll
+  for (int k = 0; k < NN; ++k) nacc[k] = 0.0;
+  for (int ls = threadIdx.x; ls < ns; ls += SP_THREADS) op.row(s0 + ls, dot[ls], nacc);
+  if (!Op::HAS_FIN) return;
+  block_sum<NN>(nacc, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NN; ++k) s.npart[(int64_t)blockIdx.x * NN + k] = nacc[k];
+  }
+  if (!last_arrival(&s.tickets[0], gridDim.x)) return;
+  double nsum[NN];
+  block_sum_partials<NN>(s.npart, gridDim.x, nsum, red);
+  if (threadIdx.x == 0) {
+    if (s.bundle) {
+#pragma unroll
+      for (int k = 0; k < NN; ++k) s.bundle[k] = nsum[k];
+    } else {
+      op.fin(nsum);
+    }
+  }
+}
+
 // row sums of squares of CSR rows in stored (sample) order: the same
 // sequential order as the reference's np.bincount (sparse.py:66-70)
 __global__ void sp_rowsq_kernel(SpView A, double* out) {

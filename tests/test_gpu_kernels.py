@@ -52,6 +52,31 @@ def test_sparse_matvec_both_directions(d, n, dens):
         dp.close()
 
 
+@pytest.mark.parametrize("d,n,dens", [(20000, 1000, 0.002), (30000, 90000, 0.0005), (8193, 297, 0.01)])
+@pytest.mark.parametrize("blocked", ["1", "0"])
+def test_sparse_rmatvec_feature_blocked(d, n, dens, blocked, monkeypatch):
+    """Z~^T w through the feature-blocked sliced-ELL kernel (spops.cuh) and the
+    plain CSC kernel: several feature blocks of 8192, fewer samples than CTA
+    parts, a sample count that does not divide, empty samples."""
+    import scipy.sparse as sp
+
+    monkeypatch.setenv("GDWD_SP_BLOCKED", blocked)
+    rng = np.random.default_rng(d + n)
+    M = sp.random(d, n, density=dens, format="csc", random_state=rng, data_rvs=rng.standard_normal)
+    z = G.sparse.csc_from_scipy(M)
+    ones = np.ones(n)
+    dp = G.DeviceProblem(G.ProblemData(z, ones, ones, ones, 1.0, 1.0, 1.0))
+    try:
+        for _ in range(2):
+            w = rng.standard_normal(d)
+            got = dp.rmatvec(w)
+            ref = M.T @ w
+            assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(M).T @ np.abs(w))
+            assert np.array_equal(got, dp.rmatvec(w))
+    finally:
+        dp.close()
+
+
 @pytest.mark.parametrize("rows,cols", [(1000, 300), (130, 2001), (5, 70)])
 def test_gram_dmma(rows, cols):
     rng = np.random.default_rng(rows + cols)
