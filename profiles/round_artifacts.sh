@@ -20,5 +20,10 @@ ncu -i $O/ncu_persistent_c2.ncu-rep --page raw --csv > $O/ncu_persistent_c2_raw.
 python profiles/ncu_summary.py $O/ncu_persistent_c2_raw.csv > $O/ncu_persistent_c2_summary.csv
 # per-phase timing of the persistent kernel (CTA clock stamps), c2 and c1
 GDWD_PK_TIMING=1 timeout 300 python profiles/run_c2.py 100 > $O/persistent_phase_timing.txt 2>&1
+# one full capture of the feature-blocked sparse Z~^T w kernel (config 4)
+timeout 900 ncu --set full --clock-control none -k regex:sp_ztmv_fb_kernel -s 2 -c 1 -o $O/ncu_c4_sp_ztmv_fb \
+  python bench.py --config c4 --no-cpu --no-next --no-e2e --steps 3 --warmup 3 > $O/ncu_fb.log 2>&1
+ncu -i $O/ncu_c4_sp_ztmv_fb.ncu-rep --page raw --csv > $O/ncu_c4_sp_ztmv_fb_raw.csv 2>/dev/null
+python profiles/ncu_summary.py $O/ncu_c4_sp_ztmv_fb_raw.csv > $O/ncu_c4_sp_ztmv_fb.csv
 timeout 1500 python bench.py --config c5 --no-cpu --no-next > $O/bench_c5.json 2> $O/bench_c5.err
 echo done
