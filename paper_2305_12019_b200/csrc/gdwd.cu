@@ -79,8 +79,14 @@ namespace {
 constexpr int NUM_SMS = 148;
 // feature-blocked sliced ELL (sp_ztmv_fb_kernel): block width, parts (CTAs)
 // and slice rows per lane in flight
-constexpr int FB_COLS = 8192;
-constexpr int FB_PARTS = 2 * NUM_SMS;
+#ifndef FB_COLS_V
+#define FB_COLS_V 8192
+#endif
+#ifndef FB_PARTS_PER_SM
+#define FB_PARTS_PER_SM 2
+#endif
+constexpr int FB_COLS = FB_COLS_V;
+constexpr int FB_PARTS = FB_PARTS_PER_SM * NUM_SMS;
 constexpr size_t FB_SMEM_MAX = 100 * 1024;
 #ifndef FB_H
 #define FB_H 2
@@ -195,6 +201,19 @@ struct gdwd_ctx {
   bool has_problem = false;
   double C = 0, q = 0, zscale = 0, yty = 0;
   double fro2 = -1.0;  // ||Z~||_F^2 (device reduction at upload)
+  // overlapped dense upload (pinned source): row chunks on a copy stream,
+  // the SMW Gram block-rows on a second stream as the chunks land
+  static constexpr int UP_NCH = 8;
+  cudaStream_t cst = nullptr, gst = nullptr;
+  cudaEvent_t up_ev[UP_NCH] = {}, gram_ev = nullptr, st_ev = nullptr;
+  int64_t up_r[UP_NCH + 1] = {};
+  bool up_pending = false;    // copies of the current Zs may be in flight
+  int64_t zs_gen = 0;         // bumped whenever the dense Z~ (Zs) changes
+  int64_t k_gen = -1;         // zs_gen whose Gram K = Z~ Z~^T (kmat) was formed at upload
+  bool fro2_pending = false;  // fro2_h holds the value once st is synchronized
+  double* fro2_h = nullptr;   // pinned
+  double* fro2_d = nullptr;
+  DevBuf gram_ws;             // split-K workspace of the upload's chunked Gram
   double* pin[2] = {nullptr, nullptr};  // pinned staging for uploads
   cudaEvent_t pin_ev[2] = {nullptr, nullptr};
   size_t pin_bytes = 0;
@@ -625,6 +644,37 @@ static int upload_rows(gdwd_ctx* ctx, const double* src, int64_t d, int64_t n, i
   return GDWD_OK;
 }
 
+// one page-locked double per context from a process-wide block (contexts are
+// created inside timed end-to-end calls; cudaMallocHost is milliseconds)
+static double* pinned_slot() {
+  static std::mutex mu;
+  static double* block = nullptr;
+  static int used = 0, cap = 0;
+  std::lock_guard<std::mutex> g(mu);
+  if (used == cap) {
+    cap = 4096;
+    used = 0;
+    if (cudaMallocHost(&block, cap * sizeof(double)) != cudaSuccess) return nullptr;
+  }
+  return block + used++;
+}
+
+// ||Z~||_F^2 on the host, waiting for a deferred reduction if one is queued
+static double get_fro2(gdwd_ctx* ctx) {
+  if (ctx->fro2_pending) {
+    cudaStreamSynchronize(ctx->st);
+    ctx->fro2 = *ctx->fro2_h;
+    ctx->fro2_pending = false;
+  }
+  return ctx->fro2;
+}
+
+// the host buffer of an overlapped upload is borrowed until its copies land
+static void finish_upload(gdwd_ctx* ctx) {
+  if (ctx->cst) cudaStreamSynchronize(ctx->cst);
+  ctx->up_pending = false;
+}
+
 static int compute_fro2(gdwd_ctx* ctx, const double* a, int64_t rows, int64_t cols, int64_t ld) {
   double* dv = nullptr;
   CK(cudaMalloc(&dv, sizeof(double)));
@@ -757,7 +807,7 @@ int gdwd_ctx_create(int32_t device, gdwd_ctx** out) {
   if (e == cudaSuccess) {
     keep_pool_reserved(device);
     for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat, &ctx->gram_ws})
       b->st = ctx->st;
   }
   if (e == cudaSuccess) e = cudaMalloc(&ctx->S, sizeof(Scal));
@@ -776,10 +826,20 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
+  if (ctx->cst) {
+    cudaStreamSynchronize(ctx->cst);
+    cudaStreamSynchronize(ctx->gst);
+    for (cudaEvent_t e : ctx->up_ev) cudaEventDestroy(e);
+    cudaEventDestroy(ctx->gram_ev);
+    cudaEventDestroy(ctx->st_ev);
+    cudaStreamDestroy(ctx->cst);
+    cudaStreamDestroy(ctx->gst);
+    dfree(ctx->fro2_d, ctx->st);
+  }
   dfree(ctx->Zs, ctx->st);
   free_sparse(ctx);
   for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat, &ctx->gram_ws})
     b->release();
   end_session(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -809,7 +869,82 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
   ctx->Zs = nullptr;
   CK(dmalloc((void**)&ctx->Zs, (size_t)n * ld * sizeof(double), ctx->st));
   if (ld != d) CK(cudaMemsetAsync(ctx->Zs, 0, (size_t)n * ld * sizeof(double), ctx->st));
+  // Sample-space regimes (n <= 2500, n <= d: SMW2, DIRECT with 2n <= d) with
+  // a page-locked source: the matrix is copied in UP_NCH feature-column
+  // chunks on a copy stream while the Gram consumes each chunk as it lands
+  // (second stream); ctx->st waits for the last copy and the Gram, so every
+  // other consumer sees the whole matrix.  ||Z~||_F^2 is reduced on st and
+  // read lazily.
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, samples) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  finish_upload(ctx);
+  if (pinned && n <= 2500 && n <= d && d >= 4 * gdwd_ctx::UP_NCH && !sharded(ctx) && !getenv("GDWD_UPLOAD")) {
+    if (!ctx->cst) {
+      CK(cudaStreamCreateWithFlags(&ctx->cst, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&ctx->gst, cudaStreamNonBlocking));
+      for (auto& e : ctx->up_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->gram_ev, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->st_ev, cudaEventDisableTiming));
+      ctx->fro2_h = pinned_slot();
+      CK(dmalloc((void**)&ctx->fro2_d, sizeof(double), ctx->st));
+    }
+    CK(cudaEventRecord(ctx->st_ev, ctx->st));  // allocation / pad memset first
+    CK(cudaStreamWaitEvent(ctx->cst, ctx->st_ev, 0));
+    const size_t row_b = (size_t)d * sizeof(double);
+    // In the sample-space regimes (n <= 2500, n <= d: SMW2, DIRECT with 2n <=
+    // d) the n x n Gram K = Z~ Z~^T is formed here on a second stream as the
+    // chunks land: the chunks are feature columns, so each adds its own
+    // K_c = Z~[:, c] Z~[:, c]^T (DMMA SYRK) to K in chunk order.
+    const bool gram = true;
+    const int64_t ldk = (n + 1) / 2 * 2;
+    const int64_t cw = (d + gdwd_ctx::UP_NCH - 1) / gdwd_ctx::UP_NCH;
+    for (int c = 0; c <= gdwd_ctx::UP_NCH; ++c) ctx->up_r[c] = std::min<int64_t>(d, cw * c);
+    if (gram) {
+      CK(ctx->kmat.ensure((size_t)n * ldk));
+      CK(cudaMemsetAsync(ctx->kmat.p, 0, (size_t)n * ldk * sizeof(double), ctx->st));
+      CK(ctx->gram_ws.ensure((size_t)gram_workspace_doubles(n, cw)));
+      CK(cudaEventRecord(ctx->st_ev, ctx->st));
+      CK(cudaStreamWaitEvent(ctx->gst, ctx->st_ev, 0));
+    }
+    for (int c = 0; c < gdwd_ctx::UP_NCH; ++c) {
+      const int64_t c0 = ctx->up_r[c], c1 = ctx->up_r[c + 1];
+      if (c1 > c0)
+        CK(cudaMemcpy2DAsync(ctx->Zs + c0, ld * sizeof(double), samples + c0, row_b, (c1 - c0) * sizeof(double), n,
+                             cudaMemcpyHostToDevice, ctx->cst));
+      CK(cudaEventRecord(ctx->up_ev[c], ctx->cst));
+      if (gram && c1 > c0) {
+        CK(cudaStreamWaitEvent(ctx->gst, ctx->up_ev[c], 0));
+        CK(gram_syrk(ctx->Zs + c0, n, c1 - c0, ld, false, 1.0, 0.0, ctx->kmat.p, ldk, ctx->gram_ws.p, ctx->gst,
+                     c > 0));
+      }
+    }
+    CK(cudaStreamWaitEvent(ctx->st, ctx->up_ev[gdwd_ctx::UP_NCH - 1], 0));
+    if (gram) {
+      CK(cudaEventRecord(ctx->gram_ev, ctx->gst));
+      CK(cudaStreamWaitEvent(ctx->st, ctx->gram_ev, 0));
+    }
+    ctx->up_pending = true;
+    ctx->n = n;
+    ctx->d = d;
+    ctx->ldz = ld;
+    ctx->has_dense = true;
+    ctx->has_problem = false;
+    ctx->data_gen++;
+    ctx->zs_gen++;
+    ctx->k_gen = gram ? ctx->zs_gen : -1;
+    RC(ensure_scratch(ctx, n, d));
+    run_vm(ctx, OpSumSq{ctx->Zs, d, ld, ctx->fro2_d}, n * d, "vmap_fro2", false);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->fro2_h, ctx->fro2_d, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    ctx->fro2_pending = true;
+    // the host buffer is only borrowed for the call: wait for the copies
+    // (the Gram block-rows and the norm may still be running)
+    finish_upload(ctx);
+    return GDWD_OK;
+  }
   RC(upload_rows(ctx, samples, d, n, ld));
+  ctx->zs_gen++;
   ctx->n = n;
   ctx->d = d;
   ctx->ldz = ld;
@@ -901,6 +1036,7 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
   free_sparse(ctx);
   dfree(ctx->Zs, ctx->st);
   ctx->Zs = nullptr;
+  ctx->zs_gen++;
   ctx->has_dense = false;
   const size_t nz = (size_t)std::max<int64_t>(nnz, 1);
   CK(dmalloc((void**)&ctx->csc_ptr, (n + 1) * sizeof(int64_t), ctx->st));
@@ -1048,6 +1184,7 @@ static int densify(gdwd_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->Zs, 0, (size_t)n * ld * sizeof(double), ctx->st));
   SpView A{ctx->csc_ptr, ctx->csc_idx, ctx->csc_val, n, ctx->d};
   sp_densify_kernel<<<(unsigned)((n + 7) / 8), 256, 0, ctx->st>>>(A, ctx->Zs, ld);
+  ctx->zs_gen++;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->st));
   ctx->has_dense = true;
@@ -1066,6 +1203,7 @@ int gdwd_generate_dense(gdwd_ctx* ctx, int32_t kind, uint64_t seed, int64_t d, i
   CK(dmalloc((void**)&ctx->Zs, (size_t)n * ld * sizeof(double), ctx->st));
   if (ld != d) CK(cudaMemsetAsync(ctx->Zs, 0, (size_t)n * ld * sizeof(double), ctx->st));
   gen_gauss_kernel<<<NUM_SMS * 16, 256, 0, ctx->st>>>(ctx->Zs, ld, d, n, offset, seed, signal_k, shift);
+  ctx->zs_gen++;
   CK(cudaGetLastError());
   ctx->n = n;
   ctx->d = d;
@@ -1084,6 +1222,7 @@ int gdwd_scale_dense(gdwd_ctx* ctx, const double* y, double z_scale) {
   CK(yd.ensure(ctx->n));
   CK(cudaMemcpy(yd.p, y, ctx->n * sizeof(double), cudaMemcpyHostToDevice));
   scale_rows_kernel<<<NUM_SMS * 16, 256, 0, ctx->st>>>(ctx->Zs, ctx->ldz, ctx->d, ctx->n, yd.p, z_scale);
+  ctx->zs_gen++;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->st));
   yd.release();
@@ -1386,10 +1525,16 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
       assemble_direct_kernel<<<(unsigned)((d + 256) / 256), 256, 0, ctx->st>>>(ctx->fac.p, ld, d, D.zy, ctx->yty);
     } else {
       // keep K = Z^T Z for the Gram-space iteration; G = K/mu^2 + I
-      CK(ctx->kmat.ensure((size_t)m * ld));
-      // zero pad columns: the persistent kernel's paired loads read them (times 0)
-      CK(cudaMemsetAsync(ctx->kmat.p, 0, (size_t)m * ld * sizeof(double), ctx->st));
-      CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, false, 1.0, 0.0, ctx->kmat.p, ld, ctx->facw.p, ctx->st));
+      if (ctx->k_gen != ctx->zs_gen) {
+        CK(ctx->kmat.ensure((size_t)m * ld));
+        // zero pad columns: the persistent kernel's paired loads read them (times 0)
+        CK(cudaMemsetAsync(ctx->kmat.p, 0, (size_t)m * ld * sizeof(double), ctx->st));
+      }
+      if (ctx->k_gen == ctx->zs_gen) {
+        // K was formed during the upload, chunk by chunk as the rows landed
+      } else {
+        CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, false, 1.0, 0.0, ctx->kmat.p, ld, ctx->facw.p, ctx->st));
+      }
       T.mark("gram K = Z^T Z");
       g_from_k_kernel<<<vm_grid(m * m), 256, 0, ctx->st>>>(ctx->kmat.p, ctx->fac.p, m, ld, mu2);
       CK(cudaGetLastError());
@@ -1956,7 +2101,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   // ---- tables (host pow == Python's float pow) -------------------------------
   // eps constant (solver.py:441-445): 1 / max(1, ||Z~||_F), norm reduced on
   // the device at upload
-  const double eps_c = isnan(cfg->epsilon_c) ? 1.0 / std::max(1.0, sqrt(ctx->fro2)) : cfg->epsilon_c;
+  const double eps_c = isnan(cfg->epsilon_c) ? 1.0 / std::max(1.0, sqrt(get_fro2(ctx))) : cfg->epsilon_c;
   std::vector<double> tab(2 * (size_t)(max_iter + 2) + (size_t)std::max<int64_t>(sched_len, 1), 0.0);
   const double sqrt_n = sqrt((double)ng);
   for (int k = 0; k < max_iter + 2; ++k) {
@@ -2244,7 +2389,7 @@ extern "C" int gdwd_set_lanczos_start(gdwd_ctx* ctx, const double* v, int64_t d)
 }
 
 extern "C" int gdwd_frobenius_sq(gdwd_ctx* ctx, double* out) {
-  if (!ctx || !out || ctx->fro2 < 0) return set_err(ctx, GDWD_ERR_VALUE, "no data uploaded");
+  if (!ctx || !out || get_fro2(ctx) < 0) return set_err(ctx, GDWD_ERR_VALUE, "no data uploaded");
   *out = ctx->fro2;
   return GDWD_OK;
 }
@@ -2260,7 +2405,7 @@ static int comm_finish_init(gdwd_ctx* ctx, int32_t nranks, int32_t rank, int64_t
   // global ||Z~||_F^2 and check of the global sample count
   DevBuf tmp;
   CK(tmp.ensure(2));
-  double hv[2] = {ctx->fro2, (double)ctx->n};
+  double hv[2] = {get_fro2(ctx), (double)ctx->n};
   CK(cudaMemcpy(tmp.p, hv, sizeof(hv), cudaMemcpyHostToDevice));
   allreduce(ctx, tmp.p, 2);
   CK(cudaMemcpyAsync(hv, tmp.p, sizeof(hv), cudaMemcpyDeviceToHost, ctx->st));

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(GT) gemm_dmma_kernel(Opnd A, Opnd B, int64_t M
 // Sum split-K partials in slice order, symmetric fill from the upper
 // triangle, C[i][j] = S[min][max] / div + (i==j ? shift : 0).
 __global__ void syrk_finish_kernel(const double* W, int64_t ldw, int64_t wslice, int nslice, int64_t M,
-                                   double div, double shift, double* C, int64_t ldc) {
+                                   double div, double shift, double* C, int64_t ldc, bool accumulate) {
   const int64_t tot = M * M;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -170,7 +170,7 @@ __global__ void syrk_finish_kernel(const double* W, int64_t ldw, int64_t wslice,
     for (int z = 0; z < nslice; ++z) s += W[z * wslice + a * ldw + b];
     double v = (div == 1.0) ? s : s / div;
     if (i == j) v += shift;
-    C[i * ldc + j] = v;
+    C[i * ldc + j] = accumulate ? C[i * ldc + j] + v : v;
   }
 }
 
@@ -307,7 +307,7 @@ int gram_slices(int64_t M, int64_t K) {
 //   trans_k = false: C (R x R) = Zs Zs^T   (sum over columns, "SMW":   Z^T Z)
 // then C = C / div + shift * I.  W: workspace of gram_workspace_doubles.
 cudaError_t gram_syrk(const double* Zs, int64_t R, int64_t Lc, int64_t ldz, bool sum_over_rows, double div,
-                      double shift, double* C, int64_t ldc, double* W, cudaStream_t st) {
+                      double shift, double* C, int64_t ldc, double* W, cudaStream_t st, bool accumulate) {
   const int64_t M = sum_over_rows ? Lc : R;
   const int64_t K = sum_over_rows ? R : Lc;
   const int ns = gram_slices(M, K);
@@ -324,7 +324,7 @@ cudaError_t gram_syrk(const double* Zs, int64_t R, int64_t Lc, int64_t ldz, bool
     gemm_dmma_kernel<true, true><<<grid, GT, 0, st>>>(A, A, M, M, K, kslice, W, M, M * M, true, 1.0, 0.0,
                                                       nullptr, 0);
   }
-  syrk_finish_kernel<<<grid_for(M * M), 256, 0, st>>>(W, M, M * M, ns, M, div, shift, C, ldc);
+  syrk_finish_kernel<<<grid_for(M * M), 256, 0, st>>>(W, M, M * M, ns, M, div, shift, C, ldc, accumulate);
   return cudaGetLastError();
 }
 

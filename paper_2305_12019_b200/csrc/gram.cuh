@@ -10,7 +10,7 @@ cudaError_t gemm_f64(const double* a, int64_t sam, int64_t sak, const double* b,
 int gram_slices(int64_t M, int64_t K);
 int64_t gram_workspace_doubles(int64_t M, int64_t K);
 cudaError_t gram_syrk(const double* Zs, int64_t R, int64_t Lc, int64_t ldz, bool sum_over_rows, double div,
-                      double shift, double* C, int64_t ldc, double* W, cudaStream_t st);
+                      double shift, double* C, int64_t ldc, double* W, cudaStream_t st, bool accumulate = false);
 cudaError_t chol_inverse(double* A, double* Li, double* T, int64_t ld, int64_t m, int* info, cudaStream_t st);
 
 }  // namespace gdwd
