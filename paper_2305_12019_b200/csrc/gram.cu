@@ -176,72 +176,85 @@ __global__ void syrk_finish_kernel(const double* W, int64_t ldw, int64_t wslice,
 
 // Dense factor + inverse of one diagonal block (m <= LEAF_MAX) in shared
 // memory: A = L L^T (L lower), Linv = L^{-1}.  Upper parts are written as
-// zeros.  The inverse is a forward substitution on the identity with every
-// column in flight at once (thread c owns column c, reads only shared
-// memory); each of the m steps is one division after an FMA chain over the
-// already-final entries (two chains, even / odd k).
-constexpr int LEAF_MAX = 48;  // two (LEAF_MAX x LEAF_MAX+1) doubles in static shared memory
+// zeros.  Factor: per column every thread takes sqrt of the pivot itself
+// (no serial section), divides its row's entry, and after one barrier
+// applies its rank-1 updates.  Inverse by recursive doubling: with the
+// inverses of the diagonal s x s blocks known, each 2s x 2s diagonal block
+// gets its off-diagonal block -Li22 (L21 Li11); all blocks of a level are
+// independent (log2(m) levels, two barriers each).  blockDim = 256.
+constexpr int LEAF_MAX = 40;  // three (LEAF_MAX x LEAF_MAX+1) doubles in static shared memory
 __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t ldl, int m, int* info,
                                   int64_t offset) {
   __shared__ double L[LEAF_MAX][LEAF_MAX + 1];
   __shared__ double Li[LEAF_MAX][LEAF_MAX + 1];
+  __shared__ double Tm[LEAF_MAX][LEAF_MAX + 1];
   __shared__ int bad;
   const int t = threadIdx.x;
   if (t == 0) bad = 0;
-  for (int idx = t; idx < m * m; idx += blockDim.x) {
-    const int i = idx / m, j = idx % m;
-    L[i][j] = (j <= i) ? A[i * lda + j] : 0.0;
+  for (int idx = t; idx < LEAF_MAX * LEAF_MAX; idx += blockDim.x) {
+    const int i = idx / LEAF_MAX, j = idx % LEAF_MAX;
+    L[i][j] = (i < m && j <= i) ? A[i * lda + j] : 0.0;
+    Li[i][j] = 0.0;
   }
   __syncthreads();
   for (int j = 0; j < m; ++j) {
-    if (t == 0) {
-      double dj = L[j][j];
-      if (!(dj > 0.0)) { bad = 1; dj = 1.0; }
-      L[j][j] = sqrt(dj);
+    double dj = L[j][j];
+    if (!(dj > 0.0)) {
+      if (t == 0) bad = 1;
+      dj = 1.0;
     }
+    const double r = sqrt(dj);
+    __syncthreads();  // everyone has read the pivot
+    if (t == j) L[j][j] = r;
+    else if (t > j && t < m) L[t][j] = L[t][j] / r;
     __syncthreads();
-    for (int i = j + 1 + t; i < m; i += blockDim.x) L[i][j] = L[i][j] / L[j][j];
-    __syncthreads();
-    // trailing lower triangle only: (i, k) with j < k <= i < m; thread t
-    // takes column k = j+1 + t%32 of rows i = j+1 + t/32 + 8q (no integer
-    // division in the loop; blockDim = 256)
-    {
-      const int k = j + 1 + (t & 31);
-      if (k < m) {
-        const double lkj = L[k][j];
-        for (int i = j + 1 + (t >> 5); i < m; i += 8)
-          if (k <= i) L[i][k] -= L[i][j] * lkj;
-      }
-      for (int k2 = j + 33 + (t & 31); k2 < m; k2 += 32) {  // m > 33 only
-        const double lkj = L[k2][j];
-        for (int i = j + 1 + (t >> 5); i < m; i += 8)
-          if (k2 <= i) L[i][k2] -= L[i][j] * lkj;
-      }
+    // trailing lower triangle: thread t takes column k = j+1 + t%32 of rows
+    // i = j+1 + t/32 + 8q
+    const int k = j + 1 + (t & 31);
+    if (k < m) {
+      const double lkj = L[k][j];
+      for (int i = j + 1 + (t >> 5); i < m; i += 8)
+        if (k <= i) L[i][k] -= L[i][j] * lkj;
+    }
+    for (int k2 = j + 33 + (t & 31); k2 < m; k2 += 32) {  // m > 33 only
+      const double lkj = L[k2][j];
+      for (int i = j + 1 + (t >> 5); i < m; i += 8)
+        if (k2 <= i) L[i][k2] -= L[i][j] * lkj;
     }
     __syncthreads();
   }
-  if (t < m) {
-    const int c = t;
-    for (int i = 0; i < m; ++i) {
-      if (i < c) {
-        Li[i][c] = 0.0;
-        continue;
-      }
-      double s0 = (i == c) ? 1.0 : 0.0, s1 = 0.0;
-      int k = c;
-      for (; k + 1 < i; k += 2) {
-        s0 -= L[i][k] * Li[k][c];
-        s1 -= L[i][k + 1] * Li[k + 1][c];
-      }
-      if (k < i) s0 -= L[i][k] * Li[k][c];
-      Li[i][c] = (s0 + s1) / L[i][i];
-    }
-  }
+  if (t < m) Li[t][t] = 1.0 / L[t][t];
   __syncthreads();
+  for (int s = 1; s < m; s *= 2) {
+    const int nent = (m + 2 * s - 1) / (2 * s) * s * s;  // 2s-blocks x (s x s) entries
+    // T = L21 Li11 for every 2s-block (rows b+s.., cols b..b+s)
+    for (int e = t; e < nent; e += blockDim.x) {
+      const int b = (e / (s * s)) * 2 * s, i = (e % (s * s)) / s, jj = e % s;
+      const int row = b + s + i, col = b + jj;
+      if (row < m) {
+        double acc = 0.0;
+        for (int kk = jj; kk < s; ++kk) acc += L[row][b + kk] * Li[b + kk][col];
+        Tm[row][col] = acc;
+      }
+    }
+    __syncthreads();
+    // Li21 = -Li22 T
+    for (int e = t; e < nent; e += blockDim.x) {
+      const int b = (e / (s * s)) * 2 * s, i = (e % (s * s)) / s, jj = e % s;
+      const int row = b + s + i, col = b + jj;
+      if (row < m) {
+        double acc = 0.0;
+        for (int kk = 0; kk <= i; ++kk)
+          if (b + s + kk < m) acc += Li[row][b + s + kk] * Tm[b + s + kk][col];
+        Li[row][col] = -acc;
+      }
+    }
+    __syncthreads();
+  }
   for (int idx = t; idx < m * m; idx += blockDim.x) {
     const int i = idx / m, j = idx % m;
     A[i * lda + j] = (j <= i) ? L[i][j] : 0.0;
-    Linv[i * ldl + j] = Li[i][j];
+    Linv[i * ldl + j] = (j <= i) ? Li[i][j] : 0.0;
   }
   if (t == 0 && bad && info) atomicCAS(info, 0, (int)offset + 1);
 }
