@@ -182,12 +182,14 @@ __global__ void syrk_finish_kernel(const double* W, int64_t ldw, int64_t wslice,
 // inverses of the diagonal s x s blocks known, each 2s x 2s diagonal block
 // gets its off-diagonal block -Li22 (L21 Li11); all blocks of a level are
 // independent (log2(m) levels, two barriers each).  blockDim = 256.
-constexpr int LEAF_MAX = 40;  // three (LEAF_MAX x LEAF_MAX+1) doubles in static shared memory
+constexpr int LEAF_MAX = 64;  // three (LEAF_MAX x LEAF_MAX+1) doubles in dynamic shared memory
+constexpr size_t LEAF_SMEM = (size_t)3 * LEAF_MAX * (LEAF_MAX + 1) * sizeof(double);
 __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t ldl, int m, int* info,
                                   int64_t offset) {
-  __shared__ double L[LEAF_MAX][LEAF_MAX + 1];
-  __shared__ double Li[LEAF_MAX][LEAF_MAX + 1];
-  __shared__ double Tm[LEAF_MAX][LEAF_MAX + 1];
+  extern __shared__ double leaf_sm[];
+  auto L = reinterpret_cast<double (*)[LEAF_MAX + 1]>(leaf_sm);
+  auto Li = reinterpret_cast<double (*)[LEAF_MAX + 1]>(leaf_sm + LEAF_MAX * (LEAF_MAX + 1));
+  auto Tm = reinterpret_cast<double (*)[LEAF_MAX + 1]>(leaf_sm + 2 * LEAF_MAX * (LEAF_MAX + 1));
   __shared__ int bad;
   const int t = threadIdx.x;
   if (t == 0) bad = 0;
@@ -344,7 +346,7 @@ cudaError_t gram_syrk(const double* Zs, int64_t R, int64_t Lc, int64_t ldz, bool
 namespace {
 
 #ifndef CHOL_LEAF
-#define CHOL_LEAF 32  // diagonal blocks factored by one CTA; the recursion's critical path
+#define CHOL_LEAF 64  // diagonal blocks factored by one CTA; the recursion's critical path
 #endif
 static_assert(CHOL_LEAF <= LEAF_MAX, "leaf larger than potrf_trtri_small's shared arrays");
 // Recursive blocked Cholesky + triangular inverse (lower):
@@ -352,7 +354,12 @@ static_assert(CHOL_LEAF <= LEAF_MAX, "leaf larger than potrf_trtri_small's share
 cudaError_t chol_rec(double* A, double* Li, double* T, int64_t ld, int64_t m, int64_t off, int* info,
                      cudaStream_t st) {
   if (m <= CHOL_LEAF) {
-    potrf_trtri_small<<<1, 256, 0, st>>>(A, ld, Li, ld, (int)m, info, off);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(potrf_trtri_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LEAF_SMEM);
+      attr = true;
+    }
+    potrf_trtri_small<<<1, 256, LEAF_SMEM, st>>>(A, ld, Li, ld, (int)m, info, off);
     return cudaGetLastError();
   }
   int64_t m1 = ((m / 2) + CHOL_LEAF - 1) / CHOL_LEAF * CHOL_LEAF;
