@@ -293,3 +293,32 @@ def test_persistent_iterates_match_reference(case, version, monkeypatch):
             assert relerr(v, tr["it_" + key][k - 1]) < TOL20, (key, k)
         b = tr["hist"][k - 1, 12]
         assert abs(st.beta - b) <= 1e-9 * abs(b) + 1e-12, k
+
+
+@pytest.mark.parametrize("case", ["tiny_smw2", "smw2_natural", "var_direct_gram", "var_odd", "var_q3_mu2"])
+def test_pinned_upload_with_overlapped_gram(case):
+    """A page-locked matrix takes the overlapped upload (feature-column chunks
+    on a copy stream, the Gram accumulated chunk by chunk on a second stream):
+    the solve matches the reference's iterates like the pageable path, and
+    the Frobenius norm (epsilon constant) is the same."""
+    torch = pytest.importorskip("torch")
+    tr = load_traj(case)
+    prob = problem_for(tr)
+    z = prob.z_tilde
+    if not z.is_dense or z.ncols > 2500 or z.ncols > z.nrows:
+        pytest.skip("not a sample-space (n <= 2500, n <= d) dense case")
+    buf = torch.empty(z.values.size, dtype=torch.float64, pin_memory=True).numpy()
+    buf[:] = z.values
+    zp = G.SparseMatrixCSC.from_dense_samples(buf.reshape(z.ncols, z.nrows))
+    pp = G.ProblemData(zp, prob.y, prob.e, prob.weights, prob.C, prob.q, prob.z_scale)
+    cfg = config_for(case, tr, prob, max_iter=20)
+    a = G.sgs_admm_solve(pp, cfg)
+    b = G.sgs_admm_solve(prob, cfg)
+    full = bool(tr["full"])
+    for key in ("w", "r", "alpha"):
+        v = getattr(a.final_state, key)
+        if not full:
+            v = v[tr["idx_d"]] if key == "w" else v[tr["idx_n"]]
+        assert relerr(v, tr["it_" + key][19]) < TOL20, key
+        assert relerr(getattr(a.final_state, key), getattr(b.final_state, key)) < 1e-11, key
+    assert a.final_state.eps_c == b.final_state.eps_c
