@@ -13,6 +13,17 @@
 
 namespace gdwd {
 
+// True the first time it is called for the current device with this flag
+// word (one bit per device): per-device one-time setup such as
+// cudaFuncSetAttribute, which applies to the current device only.
+inline bool once_per_device(unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (__atomic_fetch_or(&mask, bit, __ATOMIC_RELAXED) & bit) return false;
+  return true;
+}
+
 constexpr int WARP = 32;
 
 // ---------------------------------------------------------------------------

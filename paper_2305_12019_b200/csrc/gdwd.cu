@@ -417,11 +417,9 @@ static void run_zt(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "zt
       FbView A{ctx->fb_ptr, ctx->fb_perm, ctx->fb_cnt, ctx->fb_idx, ctx->fb_val, ctx->n, ctx->d,
                ctx->fb_nb, FB_COLS, ctx->fb_parts, ctx->fb_S, ctx->fb_Q};
       const size_t sm = (size_t)(FB_COLS + ctx->fb_S) * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
+      static unsigned long long attr = 0;
+      if (once_per_device(attr))
         cudaFuncSetAttribute(sp_ztmv_fb_kernel<Op, FB_H, FB_U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_SMEM_MAX);
-        attr = true;
-      }
       sp_ztmv_fb_kernel<Op, FB_H, FB_U><<<ctx->fb_parts, SP_THREADS, sm, ctx->st>>>(op, A, sc);
     } else if (!X.a) {
       SpView A{ctx->csc_ptr, ctx->csc_idx, ctx->csc_val, ctx->n, ctx->d};

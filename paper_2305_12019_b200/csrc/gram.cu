@@ -354,11 +354,9 @@ static_assert(CHOL_LEAF <= LEAF_MAX, "leaf larger than potrf_trtri_small's share
 cudaError_t chol_rec(double* A, double* Li, double* T, int64_t ld, int64_t m, int64_t off, int* info,
                      cudaStream_t st) {
   if (m <= CHOL_LEAF) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    if (once_per_device(attr))
       cudaFuncSetAttribute(potrf_trtri_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LEAF_SMEM);
-      attr = true;
-    }
     potrf_trtri_small<<<1, 256, LEAF_SMEM, st>>>(A, ld, Li, ld, (int)m, info, off);
     return cudaGetLastError();
   }

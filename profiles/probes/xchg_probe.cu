@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(T, 1) probe(Args A) {
         if (A.mode == 1) st_ll(llvec + (size_t)v * n + i, x, f);
         else A.vec[(size_t)v * n + i] = x;
       }
-    if (threadIdx.x < NP && A.mode != 3 && A.mode != 8 && A.mode != 9) {
+    if (threadIdx.x < NP && A.mode != 3 && A.mode != 8 && A.mode != 9 && A.mode != 12) {
       const double x = sm[threadIdx.x] + 1.0;
       if (A.mode == 1) st_ll(llpart + (size_t)threadIdx.x * gridDim.x + blockIdx.x, x, f);
       else A.part[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = x;
@@ -114,6 +114,67 @@ __global__ void __launch_bounds__(T, 1) probe(Args A) {
           "r"(parity)
           : "memory");
       if (A.mode == 0 || A.mode == 6) parity ^= 1;
+      __syncthreads();
+    } else if (A.mode == 11 || A.mode == 12) {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      uint4* lp = llpart;
+      if (A.mode == 11) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.flags + 0) : "memory");
+          unsigned v;
+          const unsigned target = (f - A.epoch0 + 1) * gridDim.x;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(A.flags + 0) : "memory");
+          } while ((int)(v - target) < 0);
+        }
+        __syncthreads();
+      } else {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          for (int k = 0; k < NP; ++k) st_ll(lp + (size_t)blockIdx.x * 16 + k, sm[k] + 1.0, f);
+        }
+        if (threadIdx.x < gridDim.x) {
+          const uint4* q = lp + (size_t)threadIdx.x * 16;
+          uint4 r[16];
+          bool ok;
+          do {
+            ok = true;
+            for (int k = 0; k < NP; ++k) r[k] = ld_ll(q + k);
+            for (int k = 0; k < NP; ++k) ok &= (r[k].y == f && r[k].w == f);
+          } while (!ok);
+          double s = 0.0;
+          for (int k = 0; k < NP; ++k) s += ll_val(r[k]);
+          acc += s * 1e-300;
+        }
+        if (lane == 0 && warp * 32 < (int)gridDim.x) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        __syncthreads();
+      }
+      if (threadIdx.x == T - 32) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        const unsigned bytes = (unsigned)(n * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(V * bytes)
+                     : "memory");
+        for (int v = 0; v < V; ++v)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(sm + v * n)),
+              "l"(A.vec + (size_t)v * n), "r"(bytes), "r"(smem_u32(&bar))
+              : "memory");
+      }
+      if (A.mode == 11 && warp < NP) {
+        double s = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(A.part + (size_t)warp * gridDim.x + b);
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) red[warp] = s;
+      }
+      asm volatile(
+          "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}" ::"r"(
+              smem_u32(&bar)),
+          "r"(parity)
+          : "memory");
+      parity ^= 1;
       __syncthreads();
     } else if (A.mode >= 8) {
       // barrier + partials in one trip: per-CTA LL words (value, epoch) written
@@ -288,13 +349,14 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   unsigned epoch = 1;
-  const char* names[] = {"grid.sync+TMA", "LL poll", "flag+loads", "sync only", "stores+sync", "+partials", "+TMA only", "stores+fence", "LL part+fence", "LL part nofence", "rel/acq flag"};
+  const char* names[] = {"grid.sync+TMA", "LL poll", "flag+loads", "sync only", "stores+sync", "+partials", "+TMA only", "stores+fence", "LL part+fence", "LL part nofence", "rel/acq flag", "red.rel bar+ldcg", "LL+fence batched"};
   for (int n : {1000, 2000})
     for (int V : {3})
       for (int NP : {3, 14})
-        for (int mode : {0, 3, 8, 9, 10}) {
+        for (int mode : {11, 12}) {
           float best = 1e9;
           for (int rep = 0; rep < 3; ++rep) {
+            cudaMemset(flags, 0, G * 4);
             Args A{n, V, NP, 400, mode, vec, part, llvec, llpart, flags, out, epoch};
             epoch += 400;
             void* args[] = {&A};
