@@ -15,11 +15,12 @@
 //     prox (Step 1b) runs in the same phase as the first sweep;
 //   * the re-solved w = (h + dr)/mu^2 - v'/mu^2 has
 //       K w = GK t1 + GK dr/mu^2 - c'' kap/mu^2         (c'' = t2' |y| - coef');
-//   * K g = K w - K rho/(sigma mu), K (w - g) = K rho/(sigma mu), with K rho
-//     a second right-hand side of the first sweep.
+//   * K g = K w - K rho/(sigma mu), K (w - g) = K rho/(sigma mu); K rho of
+//     the own rows is swept once per launch and then follows rho's update
+//     by linearity (K rho -= tau sigma mu (K w - K u), K u = s K g).
 // Phases of iteration k:
 //   A  stage u, rho (k-1 commit), c_h, t1; local sums -> coef, beta_bar;
-//      rows: [K alpha, K rho ; GK t1] -> ztw_bar, x_bar, Newton r+, dr
+//      rows: [K alpha ; GK t1] -> ztw_bar, x_bar, Newton r+, dr
 //   -- barrier 1: alpha^T K alpha (finish k-1: dual objective, stop test), y.dr
 //   D  stage c_res = h2 - A x_bar, dr/mu^2;  rows: [K c_res ; GK dr/mu^2]
 //   -- barrier 2: c_res^T K c_res (reuse test), ybar.g', y.g'
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
   __shared__ PKS S;
   // owned rows (r = i - i0): values carried between the phases of an iteration
   __shared__ double o_al[PK3_MAXR], o_s1[PK3_MAXR], o_ztwb[PK3_MAXR], o_xb[PK3_MAXR], o_rn[PK3_MAXR],
-      o_dr[PK3_MAXR], o_krho[PK3_MAXR], o_gdr[PK3_MAXR], o_gp[PK3_MAXR];
+      o_dr[PK3_MAXR], o_krho[PK3_MAXR], o_gdr[PK3_MAXR], o_gp[PK3_MAXR], o_kw[PK3_MAXR], o_kg[PK3_MAXR];
   __shared__ double ot_e[PK3_MAXR], ot_wl[PK3_MAXR];  // Step 3 operands
   unsigned parity = 0;
   const unsigned vbytes = (unsigned)(((n + 1) / 2 * 2) * sizeof(double));
@@ -326,6 +327,16 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
       if (TM == 2) tm_put_row(tmG, A.GK + (i0 + warp) * A.ld, n);
     }
   }
+  // K rho of the own rows, swept once per launch (u, rho may have been
+  // advanced outside this kernel); within the launch it follows rho's update
+  // by linearity: K rho -= tau sigma mu (K w - K u), K u = s K g
+  for (int r = warp; r < nsweep; r += PK_WARPS) {
+    const double* rows[1] = {A.K + (i0 + r) * A.ld};
+    const double* xs[1] = {srho};
+    double o[1];
+    pk_row_dot<1>(rows, n, xs, o);
+    if (lane == 0) o_krho[r] = o[0];
+  }
   // Step 3 operands that do not change during the solve
   if (warp == 0 && lane < nrows) {
     ot_e[lane] = D.e[i0 + lane];
@@ -395,6 +406,11 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
           }
         }
       }
+      if (pending && warp == 0 && lane < nsweep) {  // K rho of the own rows, same update
+        const double kgr = o_kg[lane];
+        const double kur = proj ? zsg * kgr : kgr;
+        o_krho[lane] = o_krho[lane] - tsm * (o_kw[lane] - kur);
+      }
       PK3_TS(2);
       double v2[2] = {yr, gt};
       block_sum<2>(v2, red);
@@ -425,13 +441,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
         const double* GKi = A.GK + i * A.ld;
         const double xii = s0[i], ri = s1[i], ali = s2[i], wli = D.wl[i], kapi = A.kap[i];
         const double yi = sy[i], jyi = sjy[i], hi = sh[i];
-        double oK[2], oG[1];
+        double oK[1], oG[1];
         {
-          const double* xa[2] = {s2, srho};
+          const double* xa[1] = {s2};
           const double* xg[1] = {st1};
-          if (TM == 2) pk_row_dot_tm<2, 1, true>(tmK, xa, tmG, GKi, xg, n, oK, oG);
-          else if (TM) pk_row_dot_tm<2, 1, false>(tmK, xa, tmG, GKi, xg, n, oK, oG);
-          else pk_row_dot_ab<2, 1>(Ki, xa, GKi, xg, n, oK, oG);  // [K alpha, K rho], GK t1
+          if (TM == 2) pk_row_dot_tm<1, 1, true>(tmK, xa, tmG, GKi, xg, n, oK, oG);
+          else if (TM) pk_row_dot_tm<1, 1, false>(tmK, xa, tmG, GKi, xg, n, oK, oG);
+          else pk_row_dot_ab<1, 1>(Ki, xa, GKi, xg, n, oK, oG);  // K alpha, GK t1
         }
         // every lane holds the same sums (butterfly), so all lanes run Newton
         const double s1i = oG[0];
@@ -457,7 +473,6 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
           o_xb[r] = xbi;
           o_rn[r] = rn;
           o_dr[r] = dri;
-          o_krho[r] = oK[1];
         }
       }
       PK3_TS(4);
@@ -646,6 +661,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
         const double di = wi - gi;                     // w - u when u = g (no projection)
         const double kdi = o_krho[r] / (sig * mu);     // K (w - g)
         const double kgi = kwi - kdi;                  // K g
+        o_kw[r] = kwi;
+        o_kg[r] = kgi;
         acc[10] = gi * kgi;
         acc[11] = di * kdi;
         acc[12] = di * kgi;
