@@ -2246,11 +2246,16 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
       // us/iteration, same run): the GK stream stays latency-bound and the
       // TMEM words cost the registers that kept 16 loads in flight.
       int tmem = ctx->n <= 1024 ? 2 : 0;
-      if (getenv("GDWD_PK_TMEM")) tmem = std::min(tmem, atoi(getenv("GDWD_PK_TMEM")));
+      if (getenv("GDWD_PK_TMEM")) {  // diagnostics: 0 L2 only, 1 K in TMEM (n <= 2048), 2 K and GK (n <= 1024)
+        const int want = atoi(getenv("GDWD_PK_TMEM"));
+        tmem = want >= 2 && ctx->n <= 1024 ? 2 : (want >= 1 && ctx->n <= 2048 ? 1 : 0);
+      }
       PK3Args pa{D, ctx->kmat.p, ctx->gkmat.p, D.kap, D.gam, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host,
                  diag, ts, ctx->use_sgs ? 1 : 0, ctr};
       void* args[] = {&pa};
-      const void* kfn = tmem == 2 ? (const void*)gram_smw_persistent3<2> : (const void*)gram_smw_persistent3<0>;
+      const void* kfn = tmem == 2   ? (const void*)gram_smw_persistent3<2>
+                        : tmem == 1 ? (const void*)gram_smw_persistent3<1>
+                                    : (const void*)gram_smw_persistent3<0>;
       CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       Launch L(ctx, "persistent_gram_smw2");
       CK(cudaLaunchCooperativeKernel(kfn, dim3(NUM_SMS), dim3(PK_THREADS), args, sm, ctx->st));
