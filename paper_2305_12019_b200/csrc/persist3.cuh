@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
   __shared__ double o_al[PK3_MAXR], o_s1[PK3_MAXR], o_ztwb[PK3_MAXR], o_xb[PK3_MAXR], o_rn[PK3_MAXR],
       o_dr[PK3_MAXR], o_krho[PK3_MAXR], o_gdr[PK3_MAXR], o_gp[PK3_MAXR], o_kw[PK3_MAXR], o_kg[PK3_MAXR];
   __shared__ double ot_e[PK3_MAXR], ot_wl[PK3_MAXR];  // Step 3 operands
+  __shared__ double sc_scal[8];  // scalar results of side-by-side chains
   unsigned parity = 0;
   const unsigned vbytes = (unsigned)(((n + 1) / 2 * 2) * sizeof(double));
   auto issue = [&](int cnt, const double* const* src, double* const* dst) {
@@ -605,22 +606,31 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
       pk_cross_sum<3>(A.part, slot, t, red);
       slot ^= 1;
       PK3_TS(11);
+      // the reuse test (warp 0) and the re-solve's scalars (warp 1,
+      // speculatively) are independent chains: run them side by side
       if (threadIdx.x == 0) {
         const double rb = S.h2bot - (S.ytzw + yty * bb);
         const double rr = hypot(sqrt(t[0] > 0.0 ? t[0] : 0.0), rb);
         S.reuse = rr <= 5.0 * eps;
+      } else if (threadIdx.x == 32) {
+        const double s2 = ynorm * t2;
+        const double coef = (t[1] + (-s2)) / ys;
+        const double yv = t[2] - coef * (ynorm * yjy);
+        const double vn = (-s2) - coef * (-1.0);
+        const double p2 = yv + ynorm * vn;
+        sc_scal[0] = coef;
+        sc_scal[1] = t2 * ynorm - coef;  // c''
+        sc_scal[2] = S.h2bot / yty - p2 / yty;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
         if (S.reuse) {
           S.beta = bb;
         } else {
           S.double_count += 1;
-          const double s2 = ynorm * t2;
-          const double coef = (t[1] + (-s2)) / ys;
-          const double yv = t[2] - coef * (ynorm * yjy);
-          const double vn = (-s2) - coef * (-1.0);
-          const double p2 = yv + ynorm * vn;
-          S.coef = coef;
-          S.cp = t2 * ynorm - coef;  // c''
-          S.beta = S.h2bot / yty - p2 / yty;
+          S.coef = sc_scal[0];
+          S.cp = sc_scal[1];
+          S.beta = sc_scal[2];
         }
         if (blockIdx.x == 0) {
           D.hist[(int64_t)k * HIST_W + H_REUSE] = S.reuse ? 1.0 : 0.0;
@@ -710,33 +720,50 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
       pk_cross_sum<PK_NPART>(A.part, slot, t, red);
       slot ^= 1;
       PK3_TS(14);
-      if (threadIdx.x == 0) {
-        const double gg = t[10] > 0.0 ? t[10] : 0.0;
-        S.gnorm = sqrt(gg);
-        if (S.gnorm <= D.zscale) {
-          S.wu2 = t[11] > 0.0 ? t[11] : 0.0;
-        } else {  // w - u = d + (1 - s) g with s = z_scale / ||g||
-          const double om = 1.0 - D.zscale / S.gnorm;
-          const double v = t[11] + 2.0 * om * t[12] + om * om * gg;
-          S.wu2 = v > 0.0 ? v : 0.0;
+      // the eight normalised residuals by lane 0 of warps 0-7 side by side
+      // (one sqrt and one division each; warp 4 also forms ||g|| and ||w-u||)
+      if (lane == 0 && warp < 8) {
+        const double oc = D.one_c;
+        double ev;
+        switch (warp) {
+          case 0: ev = fabs(t[0]) / oc; break;
+          case 1: ev = fabs(t[1]) / oc; break;
+          case 2: ev = t[2] / oc; break;
+          case 3: ev = sqrt(t[3]) / oc; break;
+          case 4: {
+            const double gg = t[10] > 0.0 ? t[10] : 0.0;
+            const double gn = sqrt(gg);
+            double wu2;
+            if (gn <= D.zscale) {
+              wu2 = t[11] > 0.0 ? t[11] : 0.0;
+            } else {  // w - u = d + (1 - s) g with s = z_scale / ||g||
+              const double om = 1.0 - D.zscale / gn;
+              const double v = t[11] + 2.0 * om * t[12] + om * om * gg;
+              wu2 = v > 0.0 ? v : 0.0;
+            }
+            S.gnorm = gn;
+            S.wu2 = wu2;
+            ev = (D.mu * sqrt(wu2)) / oc;
+            break;
+          }
+          case 5: ev = fmax(sqrt(t[13]) - D.zscale, 0.0) / oc; break;
+          case 6: ev = sqrt(t[4]) / oc; break;
+          default: ev = sqrt(t[5]) / oc; break;
         }
+        sc_scal[warp] = ev;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
         S.w2 = t[13];
         S.pending = 1;
         S.sigma_pend = S.sigma;
-        const double oc = D.one_c;
         if (t[9] > 0.0 && A.diag == 0) {
           S.error = 6;
           S.stopped = 1;
         } else {
           double* e = S.eta;
-          e[0] = fabs(t[0]) / oc;
-          e[1] = fabs(t[1]) / oc;
-          e[2] = t[2] / oc;
-          e[3] = sqrt(t[3]) / oc;
-          e[4] = (D.mu * sqrt(S.wu2)) / oc;
-          e[5] = fmax(sqrt(S.w2) - D.zscale, 0.0) / oc;
-          e[6] = sqrt(t[4]) / oc;
-          e[7] = sqrt(t[5]) / oc;
+#pragma unroll
+          for (int f = 0; f < 8; ++f) e[f] = sc_scal[f];
           e[9] = t[6] + D.C * t[7];
           S.sdual = t[8];
           if (blockIdx.x == 0) {
