@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
   // owned rows (r = i - i0): values carried between the phases of an iteration
   __shared__ double o_al[PK3_MAXR], o_s1[PK3_MAXR], o_ztwb[PK3_MAXR], o_xb[PK3_MAXR], o_rn[PK3_MAXR],
       o_dr[PK3_MAXR], o_krho[PK3_MAXR], o_gdr[PK3_MAXR], o_gp[PK3_MAXR], o_kw[PK3_MAXR], o_kg[PK3_MAXR];
-  __shared__ double ot_e[PK3_MAXR], ot_wl[PK3_MAXR];  // Step 3 operands
+  __shared__ double ot_e[PK3_MAXR], ot_wl[PK3_MAXR], ot_pw[PK3_MAXR];  // Step 3 operands, w^(1/(q+1))
   __shared__ double sc_scal[8];  // scalar results of side-by-side chains
   unsigned parity = 0;
   const unsigned vbytes = (unsigned)(((n + 1) / 2 * 2) * sizeof(double));
@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
   if (warp == 0 && lane < nrows) {
     ot_e[lane] = D.e[i0 + lane];
     ot_wl[lane] = D.wl[i0 + lane];
+    ot_pw[lane] = np_pow(D.wl[i0 + lane], D.e1);
   }
   const int k_end = S.k + A.count;
   const int k_begin = S.k;
@@ -370,7 +371,9 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
       PK3_TS(1);
       // 4 independent elements per thread, predicated (no early exit), so
       // their division chains overlap; uniform factors computed once
-      const double spmu = sp * mu, tsm = (D.tau * sp) * mu, mus = mu / sig;
+      // rho / (sigma mu) on coefficients (not an elementwise quantity of the
+      // reference, whose rho is a d-vector): one reciprocal, a multiply each
+      const double spmu = sp * mu, ispmu = 1.0 / spmu, tsm = (D.tau * sp) * mu, mus = mu / sig;
       const bool proj = !(gn <= D.zscale);
       const double zsg = proj ? D.zscale / gn : 1.0;
 #pragma unroll 1
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
           double uj = su[j], rj = srho[j];
           if (pending) {  // Step 2 of iteration k-1 (solver.py:535-542)
             const double wj = s3[j];
-            const double gj = wj - rj / spmu;
+            const double gj = wj - rj * ispmu;
             uj = proj ? zsg * gj : gj;
             rj = rj - tsm * (wj - uj);
           }
@@ -667,9 +670,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
           const double kap = A.kap[i];
           kwi = (o_s1[r] + o_gdr[r]) - (mu2_one ? cpp * kap : (cpp * kap) / mu2);
         }
-        const double gi = wi - srho[i] / (sig * mu);
+        const double isgmu = 1.0 / (sig * mu);
+        const double gi = wi - srho[i] * isgmu;
         const double di = wi - gi;                     // w - u when u = g (no projection)
-        const double kdi = o_krho[r] / (sig * mu);     // K (w - g)
+        const double kdi = o_krho[r] * isgmu;          // K (w - g)
         const double kgi = kwi - kdi;                  // K g
         o_kw[r] = kwi;
         o_kg[r] = kgi;
@@ -701,7 +705,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
         acc[5] = mx * mx;
         acc[6] = wl / np_pow(rr, D.q);
         acc[7] = ei * xv;
-        acc[8] = np_pow(wl, D.e1) * np_pow(np_max0(an), D.e2);
+        acc[8] = ot_pw[r] * np_pow(np_max0(an), D.e2);
         acc[9] = (rr <= 0.0) ? 1.0 : 0.0;
       }
       PK3_TS(12);
@@ -789,7 +793,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
     const double sp = S.sigma_pend, gn = S.gnorm;
     for (int64_t j = i0 + threadIdx.x; j < i1; j += PK_THREADS) {
       const double wj = D.x[j];
-      const double gj = wj - srho[j] / (sp * mu);
+      const double gj = wj - srho[j] * (1.0 / (sp * mu));  // as in the staging loop
       const double uj = (gn <= D.zscale) ? gj : (D.zscale / gn) * gj;
       srho[j] = srho[j] - ((D.tau * sp) * mu) * (wj - uj);
       su[j] = uj;
