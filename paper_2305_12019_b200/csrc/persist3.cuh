@@ -362,6 +362,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
     PK3_TS(0);
     const bool pending = S.pending != 0;
     const double sig = S.sigma_next;  // sigma of iteration k (committed after barrier 1)
+    double h2bot_l = 0.0;             // h2's scalar slot (every thread, after barrier 1)
     // ------------- phase A: u, rho (k-1); c_h, t1; sweep [K alpha, K rho ; GK t1]; Newton ----
     {
       const double sp = S.sigma_pend, gn = S.gnorm;
@@ -493,8 +494,12 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
       pk_cross_sum<2>(A.part, slot, tot, red);
       slot ^= 1;
       PK3_TS(6);
+      h2bot_l = S.hbot + tot[1];
+      // thread 0 finishes iteration k-1 while the other warps start phase D;
+      // the stop decision is read after D's first block barrier (phase D
+      // writes only per-iteration scratch before then)
       if (threadIdx.x == 0) {
-        S.h2bot = S.hbot + tot[1];
+        S.h2bot = h2bot_l;
         if (blockIdx.x == 0) {
           D.h[D.bot] = S.hbot;
           D.xb[D.bot] = S.beta_b;
@@ -531,16 +536,11 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
           }
         }
       }
-      __syncthreads();
-      if (S.stopped) {
-        if (A.use_sgs) wait_in();
-        break;
-      }
     }
     // ---------------- phase D: Step 1c residual, speculative re-solve -------------
     if (A.use_sgs) {
       const double bb = S.beta_b;
-      const double t2 = S.h2bot / yty;
+      const double t2 = h2bot_l / yty;
       double ytz = 0.0;
       wait_in();  // dr x_bar ztw_bar
       if (threadIdx.x == 0) s0[n] = s3[n] = 0.0;  // swept vectors: zero pads (synced by block_sum)
@@ -571,6 +571,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
       block_sum<1>(v1, red);
       if (threadIdx.x == 0) S.ytzw = v1[0];
       __syncthreads();
+      if (S.stopped) break;  // iteration k-1 was the last (decided after barrier 1)
       PK3_TS(8);
       const double* sdr = mu2_one ? s0 : st1;
       double q = 0.0, syg = 0.0, yg = 0.0;
@@ -642,6 +643,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
       }
       __syncthreads();
     } else {
+      __syncthreads();
+      if (S.stopped) break;
       if (threadIdx.x == 0) {
         S.reuse = 1;
         S.beta = S.beta_b;
