@@ -84,3 +84,45 @@ def test_matvec_operand_validation():
     v = np.random.default_rng(0).standard_normal(prob.n)
     ref = prob.z_tilde.scipy @ v
     assert np.allclose(dp.matvec(v), ref, rtol=1e-13, atol=1e-13)
+
+
+def test_csc_upload_validation_reports_first_error_in_sample_order():
+    """gdwd_upload_csc validates on all host cores; the error reported is the
+    one a sequential pass meets first (a sample's colptr before its row
+    indices), with the reference's exception type (ValueError code)."""
+    import ctypes as C
+
+    from paper_2305_12019_b200 import _lib
+
+    lib = _lib.load()
+    ctx = C.c_void_p()
+    assert lib.gdwd_ctx_create(0, C.byref(ctx)) == 0
+    try:
+        n, d, per = 20000, 300, 3
+        rng = np.random.default_rng(5)
+        colptr = np.arange(0, per * (n + 1), per, dtype=np.int64)
+        rowidx = np.sort(rng.integers(0, d, size=(n, per)), axis=1).ravel().astype(np.int64)
+        vals = rng.standard_normal(per * n)
+
+        def up(cp, ri):
+            return lib.gdwd_upload_csc(ctx, cp.ctypes.data_as(C.POINTER(C.c_int64)),
+                                       ri.ctypes.data_as(C.POINTER(C.c_int64)), _lib.ptr(vals), d, n)
+
+        assert up(colptr, rowidx) == 0
+        bad_i = rowidx.copy()
+        bad_i[per * 12345 + 1] = d  # index out of range at sample 12345
+        bad_p = colptr.copy()
+        bad_p[15000] = bad_p[15001] + 1  # colptr decreases at sample 15000
+        assert up(colptr, bad_i) == 2
+        assert b"row index out of bounds" in lib.gdwd_last_error(ctx)
+        assert up(bad_p, rowidx) == 2
+        assert b"nondecreasing" in lib.gdwd_last_error(ctx)
+        both = bad_p.copy()
+        assert up(both, bad_i) == 2  # the index error comes first in sample order
+        assert b"row index out of bounds" in lib.gdwd_last_error(ctx)
+        late_i = rowidx.copy()
+        late_i[per * 17000] = -1
+        assert up(bad_p, late_i) == 2  # the colptr error comes first
+        assert b"nondecreasing" in lib.gdwd_last_error(ctx)
+    finally:
+        lib.gdwd_ctx_destroy(ctx)
