@@ -18,6 +18,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <vector>
+
 #include "common.cuh"
 #include "gram.cuh"
 
@@ -351,8 +353,32 @@ namespace {
 static_assert(CHOL_LEAF <= LEAF_MAX, "leaf larger than potrf_trtri_small's shared arrays");
 // Recursive blocked Cholesky + triangular inverse (lower):
 //   A (m x m, ld) is overwritten by L; Li (ld) receives L^{-1}; T scratch.
+// Side stream of the recursion (per thread and device): L21 L11^{-1}, the
+// first factor of the off-diagonal inverse block, does not depend on the
+// lower-right factorisation and runs beside it.
+struct CholAux {
+  cudaStream_t side = nullptr;
+  int dev = -1;
+};
+static cudaStream_t chol_side_stream() {
+  static thread_local CholAux aux[8];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  CholAux& a = aux[dev & 7];
+  if (!a.side || a.dev != dev) {
+    cudaStreamCreateWithFlags(&a.side, cudaStreamNonBlocking);
+    a.dev = dev;
+  }
+  return a.side;
+}
+
+// Recursive blocked Cholesky + triangular inverse (lower):
+//   Li (ld) receives L^{-1}; A's diagonal leaf blocks receive L, its other
+//   blocks are scratch afterwards; T (m x m, ld) holds L's off-diagonal
+//   blocks in place (block (2,1) of this level at T + m1 ld, the lower-right
+//   recursion in T's lower-right block), so no copy back is needed.
 cudaError_t chol_rec(double* A, double* Li, double* T, int64_t ld, int64_t m, int64_t off, int* info,
-                     cudaStream_t st) {
+                     cudaStream_t st, cudaStream_t side, std::vector<cudaEvent_t>& evs) {
   if (m <= CHOL_LEAF) {
     static unsigned long long attr = 0;
     if (once_per_device(attr))
@@ -369,22 +395,31 @@ cudaError_t chol_rec(double* A, double* Li, double* T, int64_t ld, int64_t m, in
   double* L11i = Li;
   double* L21i = Li + m1 * ld;
   double* L22i = Li + m1 * ld + m1;
-  cudaError_t e = chol_rec(A11, L11i, T, ld, m1, off, info, st);
+  double* L21 = T + m1 * ld;
+  cudaError_t e = chol_rec(A11, L11i, T, ld, m1, off, info, st, side, evs);
   if (e != cudaSuccess) return e;
-  // T = A21 * L11i^T   (m2 x m1): A(i,k)=A21[i][k], B(j,k)=L11i[j][k]
-  e = gemm_f64(A21, ld, 1, L11i, ld, 1, m2, m1, m1, 1.0, 0.0, T, ld, st);
+  // L21 = A21 * L11i^T   (m2 x m1): A(i,k)=A21[i][k], B(j,k)=L11i[j][k]
+  e = gemm_f64(A21, ld, 1, L11i, ld, 1, m2, m1, m1, 1.0, 0.0, L21, ld, st);
   if (e != cudaSuccess) return e;
-  copy2d_kernel<<<grid_for(m2 * m1), 256, 0, st>>>(T, ld, A21, ld, m2, m1);  // L21
   // A22 -= L21 L21^T
-  e = gemm_f64(A21, ld, 1, A21, ld, 1, m2, m2, m1, -1.0, 1.0, A22, ld, st);
+  e = gemm_f64(L21, ld, 1, L21, ld, 1, m2, m2, m1, -1.0, 1.0, A22, ld, st);
   if (e != cudaSuccess) return e;
-  e = chol_rec(A22, L22i, T, ld, m2, off + m1, info, st);
+  // beside the lower-right recursion: A21 <- L21 * L11i (A(i,k)=L21[i][k], B(j,k)=L11i[k][j])
+  cudaEvent_t ev_fork, ev_join;
+  cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
+  evs.push_back(ev_fork);
+  evs.push_back(ev_join);
+  if ((e = cudaEventRecord(ev_fork, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return e;
+  e = gemm_f64(L21, ld, 1, L11i, 1, ld, m2, m1, m1, 1.0, 0.0, A21, ld, side);
   if (e != cudaSuccess) return e;
-  // T = L21 * L11i  (m2 x m1): A(i,k)=L21[i][k], B(j,k)=L11i[k][j]
-  e = gemm_f64(A21, ld, 1, L11i, 1, ld, m2, m1, m1, 1.0, 0.0, T, ld, st);
+  if ((e = cudaEventRecord(ev_join, side)) != cudaSuccess) return e;
+  e = chol_rec(A22, L22i, T + m1 * ld + m1, ld, m2, off + m1, info, st, side, evs);
   if (e != cudaSuccess) return e;
-  // L21i = -L22i * T : A(i,k)=L22i[i][k], B(j,k)=T[k][j]
-  e = gemm_f64(L22i, ld, 1, T, 1, ld, m2, m1, m2, -1.0, 0.0, L21i, ld, st);
+  if ((e = cudaStreamWaitEvent(st, ev_join, 0)) != cudaSuccess) return e;
+  // L21i = -L22i * (L21 L11i) : A(i,k)=L22i[i][k], B(j,k)=A21[k][j]
+  e = gemm_f64(L22i, ld, 1, A21, 1, ld, m2, m1, m2, -1.0, 0.0, L21i, ld, st);
   return e;
 }
 
@@ -395,7 +430,9 @@ cudaError_t chol_rec(double* A, double* Li, double* T, int64_t ld, int64_t m, in
 // pivot block, 0 on success.  Returns launch errors only.
 cudaError_t chol_inverse(double* A, double* Li, double* T, int64_t ld, int64_t m, int* info, cudaStream_t st) {
   zero_kernel<<<grid_for(m * m), 256, 0, st>>>(Li, m, m, ld);
-  cudaError_t e = chol_rec(A, Li, T, ld, m, 0, info, st);
+  std::vector<cudaEvent_t> evs;
+  cudaError_t e = chol_rec(A, Li, T, ld, m, 0, info, st, chol_side_stream(), evs);
+  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);  // released once the recorded work completes
   if (e != cudaSuccess) return e;
   // A^{-1} = Li^T Li : C(i,j) = sum_k Li[k][i] Li[k][j] -- symmetric: upper
   // tiles on the DMMA SYRK path, mirrored (T is the workspace)
