@@ -2241,11 +2241,11 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
         CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), ctx->st));
       }
       // own rows of K and GK resident in tensor memory when n <= 1024 (<= 7
-      // rows per CTA, 8 ceil(n/64) words per lane and row).  K alone (n <=
-      // 2048) measured slower than streaming both from L2 (c2: 42.7 vs 37.8
-      // us/iteration, same run): the GK stream stays latency-bound and the
-      // TMEM words cost the registers that kept 16 loads in flight.
-      int tmem = ctx->n <= 1024 ? 2 : 0;
+      // rows per CTA, 8 ceil(n/64) words per lane and row); K alone up to
+      // n = 2048, GK streamed from L2 in 8-chunk groups whose loads overlap
+      // the group's TMEM words (c2: 24.9 vs 27.0 us/iteration streaming both;
+      // a fused 16-load variant spilled in-flight registers and was slower).
+      int tmem = ctx->n <= 1024 ? 2 : (ctx->n <= 2048 ? 1 : 0);
       if (getenv("GDWD_PK_TMEM")) {  // diagnostics: 0 L2 only, 1 K in TMEM (n <= 2048), 2 K and GK (n <= 1024)
         const int want = atoi(getenv("GDWD_PK_TMEM"));
         tmem = want >= 2 && ctx->n <= 1024 ? 2 : (want >= 1 && ctx->n <= 2048 ? 1 : 0);

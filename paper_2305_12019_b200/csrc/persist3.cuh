@@ -200,6 +200,71 @@ GDWD_DEV void pk_row_dot_tm(uint32_t ta, const double* const (&xa)[NA], uint32_t
   for (int v = 0; v < NB; ++v) ob[v] = a0[NA + v];
 }
 
+GDWD_DEV void tm_ld8(uint32_t addr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+}
+
+// Row a from TMEM, row b streamed from L2 (K resident, GK not: n <= 2048).
+// Per 8-chunk group: the group's 8 L2 loads of b are issued first, the TMEM
+// words of a (one 32x32b.x32 load) and their FMAs run while they are in
+// flight, then b is consumed (64 live registers, no spills).  Per-chain chunk
+// order, FMA chains and butterfly are those of pk_row_dot_ab (bitwise the
+// same sums).
+template <int NA, int NB>
+GDWD_DEV void pk_row_dot_tm1(uint32_t ta, const double* const (&xa)[NA], const double* rb,
+                             const double* const (&xb)[NB], int64_t n, double (&oa)[NA], double (&ob)[NB]) {
+  const int lane = threadIdx.x & 31;
+  double a0[NA + NB], a1[NA + NB];
+#pragma unroll
+  for (int v = 0; v < NA + NB; ++v) a0[v] = a1[v] = 0.0;
+  const int U = (int)((n + 63) / 64);
+#pragma unroll 1
+  for (int u0 = 0; u0 < U; u0 += 8) {
+    double2 zb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t j = 2 * lane + 64 * (int64_t)(u0 + u);
+      zb[u] = j < n ? __ldg(reinterpret_cast<const double2*>(rb + j)) : make_double2(0.0, 0.0);
+    }
+    uint32_t wa[32];
+    tm_ld32(ta + 4 * u0, wa);  // past U: a neighbouring block (inside the allocation), zeroed below
+    tm_wait_ld();
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t j = 2 * lane + 64 * (int64_t)(u0 + u);
+      const bool ok = j < n;
+      const double kx = ok ? __hiloint2double(wa[4 * u + 1], wa[4 * u]) : 0.0;
+      const double ky = ok ? __hiloint2double(wa[4 * u + 3], wa[4 * u + 2]) : 0.0;
+#pragma unroll
+      for (int v = 0; v < NA; ++v) {
+        const double2 x = ok ? *reinterpret_cast<const double2*>(xa[v] + j) : make_double2(0.0, 0.0);
+        a0[v] = __fma_rn(kx, x.x, a0[v]);
+        a1[v] = __fma_rn(ky, x.y, a1[v]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t j = 2 * lane + 64 * (int64_t)(u0 + u);
+      const bool ok = j < n;
+#pragma unroll
+      for (int v = 0; v < NB; ++v) {
+        const double2 x = ok ? *reinterpret_cast<const double2*>(xb[v] + j) : make_double2(0.0, 0.0);
+        a0[NA + v] = __fma_rn(zb[u].x, x.x, a0[NA + v]);
+        a1[NA + v] = __fma_rn(zb[u].y, x.y, a1[NA + v]);
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NA + NB; ++v) a0[v] += a1[v];
+  warp_sum<NA + NB>(a0);
+#pragma unroll
+  for (int v = 0; v < NA; ++v) oa[v] = a0[v];
+#pragma unroll
+  for (int v = 0; v < NB; ++v) ob[v] = a0[NA + v];
+}
+
 struct PK3Args {
   Dev D;
   const double* K;    // n x ld
@@ -451,7 +516,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
           const double* xa[1] = {s2};
           const double* xg[1] = {st1};
           if (TM == 2) pk_row_dot_tm<1, 1, true>(tmK, xa, tmG, GKi, xg, n, oK, oG);
-          else if (TM) pk_row_dot_tm<1, 1, false>(tmK, xa, tmG, GKi, xg, n, oK, oG);
+          else if (TM) pk_row_dot_tm1<1, 1>(tmK, xa, GKi, xg, n, oK, oG);
           else pk_row_dot_ab<1, 1>(Ki, xa, GKi, xg, n, oK, oG);  // K alpha, GK t1
         }
         // every lane holds the same sums (butterfly), so all lanes run Newton
@@ -586,7 +651,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
           const double* xb1[1] = {sdr};
           double oa[1], ob[1];
           if (TM == 2) pk_row_dot_tm<1, 1, true>(tmK, xa1, tmG, rows[1], xb1, n, oa, ob);
-          else pk_row_dot_tm<1, 1, false>(tmK, xa1, tmG, rows[1], xb1, n, oa, ob);
+          else pk_row_dot_tm1<1, 1>(tmK, xa1, rows[1], xb1, n, oa, ob);
           o[0] = oa[0];
           o[1] = ob[0];
         } else {

@@ -259,7 +259,7 @@ def test_iter_gram_operator_matches_reference(case):
     assert relerr(out2.final_state.w, tr["final_w"]) < 1e-6
 
 
-@pytest.mark.parametrize("version", ["3", "3-l2", "2"])
+@pytest.mark.parametrize("version", ["3", "3-l2", "3-k", "2"])
 @pytest.mark.parametrize("case", TRAJ_CASES + VAR_CASES)
 def test_persistent_iterates_match_reference(case, version, monkeypatch):
     """The persistent Gram-space kernel (SMW2, and DIRECT with 2n <= d) run
@@ -269,10 +269,13 @@ def test_persistent_iterates_match_reference(case, version, monkeypatch):
     the 4-barrier one.  Cases outside
     the Gram-space regime run the graph path (same check)."""
     # "3": 3-barrier kernel (rows in tensor memory at these sizes), "3-l2":
-    # the same streaming its rows from L2 (the n > 1024 path), "2": 4-barrier
+    # the same streaming its rows from L2, "3-k": K rows in tensor memory and
+    # GK from L2 (the 1024 < n <= 2048 path), "2": 4-barrier
     monkeypatch.setenv("GDWD_PK_VERSION", version[0])
     if version == "3-l2":
         monkeypatch.setenv("GDWD_PK_TMEM", "0")
+    if version == "3-k":
+        monkeypatch.setenv("GDWD_PK_TMEM", "1")
     tr = load_traj(case)
     prob = problem_for(tr)
     full = bool(tr["full"])
@@ -322,3 +325,25 @@ def test_pinned_upload_with_overlapped_gram(case):
         assert relerr(v, tr["it_" + key][19]) < TOL20, key
         assert relerr(getattr(a.final_state, key), getattr(b.final_state, key)) < 1e-11, key
     assert a.final_state.eps_c == b.final_state.eps_c
+
+
+@pytest.mark.parametrize("d,n", [(6000, 1500), (5000, 2047)])
+def test_persistent_k_in_tensor_memory(d, n, monkeypatch):
+    """1024 < n <= 2048: own K rows resident in tensor memory, GK rows
+    streamed from L2 (the c2 path).  Same sums as streaming both rows from L2
+    (same chunk order and FMA chains), and the kernel-per-phase graph path's
+    iterates to 1e-9."""
+    from paper_2305_12019_b200 import synth
+
+    prob = synth.make_variant_problem("c2", d, n, seed=3)
+    cfg = G.SolverConfig(q=prob.q, max_iter=20, backend=G.Backend.SMW2)
+    tm = G.sgs_admm_solve(prob, cfg, persistent=True)
+    monkeypatch.setenv("GDWD_PK_TMEM", "0")
+    l2 = G.sgs_admm_solve(prob, cfg, persistent=True)
+    graph = G.sgs_admm_solve(prob, cfg, persistent=False)
+    assert tm.iterations == l2.iterations == graph.iterations == 20
+    for key in ("w", "u", "rho", "r", "xi", "alpha"):
+        a, b, c = (getattr(o.final_state, key) for o in (tm, l2, graph))
+        assert relerr(a, b) < 1e-13, key
+        assert relerr(a, c) < TOL20, key
+    assert abs(tm.final_state.beta - graph.final_state.beta) <= 1e-9 * abs(graph.final_state.beta) + 1e-12
