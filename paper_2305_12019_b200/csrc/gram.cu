@@ -178,9 +178,7 @@ __global__ void syrk_finish_kernel(const double* W, int64_t ldw, int64_t wslice,
 
 // Dense factor + inverse of one diagonal block (m <= LEAF_MAX) in shared
 // memory: A = L L^T (L lower), Linv = L^{-1}.  Upper parts are written as
-// zeros.  Factor: per column every thread takes sqrt of the pivot itself
-// (no serial section), divides its row's entry, and after one barrier
-// applies its rank-1 updates.  Inverse by recursive doubling: with the
+// zeros.  Factor: 8-column panels (below).  Inverse by recursive doubling: with the
 // inverses of the diagonal s x s blocks known, each 2s x 2s diagonal block
 // gets its off-diagonal block -Li22 (L21 Li11); all blocks of a level are
 // independent (log2(m) levels, two barriers each).  blockDim = 256.
@@ -201,29 +199,61 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
     Li[i][j] = 0.0;
   }
   __syncthreads();
-  for (int j = 0; j < m; ++j) {
-    double dj = L[j][j];
-    if (!(dj > 0.0)) {
-      if (t == 0) bad = 1;
-      dj = 1.0;
+  // Factor in 8-column panels.  Warp 0 factors the panel in registers (lane l
+  // owns rows p0 + l and p0 + 32 + l; pivots and L[k][j] by shuffles, no
+  // block barrier per column), then the whole block applies the panel's
+  // rank-8 update to the trailing triangle, subtracting the 8 products in
+  // column order (the same sequence of roundings as column-by-column
+  // rank-1 updates).  The per-column chain is one rsqrt (<= 1 ulp) instead
+  // of an IEEE sqrt and division behind two block barriers.
+  for (int p0 = 0; p0 < m; p0 += 8) {
+    const int pw = m - p0 < 8 ? m - p0 : 8;
+    if (t < 32) {
+      const int ra = p0 + t, rb = p0 + 32 + t;
+      double Pa[8], Pb[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        Pa[c] = (ra < m && c < pw) ? L[ra][p0 + c] : 0.0;
+        Pb[c] = (rb < m && c < pw) ? L[rb][p0 + c] : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < pw) {
+          double d = __shfl_sync(0xffffffffu, Pa[c], c);
+          if (!(d > 0.0)) {
+            if (t == 0) bad = 1;
+            d = 1.0;
+          }
+          const double rinv = rsqrt(d), r = d * rinv;
+          if (t == c) Pa[c] = r;
+          else if (t > c) Pa[c] = Pa[c] * rinv;
+          Pb[c] = Pb[c] * rinv;
+#pragma unroll
+          for (int c2 = c + 1; c2 < 8; ++c2) {
+            const double lk = __shfl_sync(0xffffffffu, Pa[c], c2);  // L[p0+c2][p0+c]
+            Pa[c2] = Pa[c2] - Pa[c] * lk;
+            Pb[c2] = Pb[c2] - Pb[c] * lk;
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < pw) {
+          if (ra < m && t >= c) L[ra][p0 + c] = Pa[c];
+          if (rb < m) L[rb][p0 + c] = Pb[c];
+        }
+      }
     }
-    const double r = sqrt(dj);
-    __syncthreads();  // everyone has read the pivot
-    if (t == j) L[j][j] = r;
-    else if (t > j && t < m) L[t][j] = L[t][j] / r;
     __syncthreads();
-    // trailing lower triangle: thread t takes column k = j+1 + t%32 of rows
-    // i = j+1 + t/32 + 8q
-    const int k = j + 1 + (t & 31);
-    if (k < m) {
-      const double lkj = L[k][j];
-      for (int i = j + 1 + (t >> 5); i < m; i += 8)
-        if (k <= i) L[i][k] -= L[i][j] * lkj;
-    }
-    for (int k2 = j + 33 + (t & 31); k2 < m; k2 += 32) {  // m > 33 only
-      const double lkj = L[k2][j];
-      for (int i = j + 1 + (t >> 5); i < m; i += 8)
-        if (k2 <= i) L[i][k2] -= L[i][j] * lkj;
+    const int q0 = p0 + pw, R = m - q0;
+    for (int idx = t; idx < R * R; idx += blockDim.x) {
+      const int ii = idx / R, kk = idx - ii * R;
+      if (kk <= ii) {
+        const int i = q0 + ii, k = q0 + kk;
+        double acc = L[i][k];
+        for (int c = 0; c < pw; ++c) acc = acc - L[i][p0 + c] * L[k][p0 + c];
+        L[i][k] = acc;
+      }
     }
     __syncthreads();
   }

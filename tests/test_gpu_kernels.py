@@ -97,6 +97,20 @@ def test_cholesky_inverse(m):
     assert relerr(inv, np.linalg.inv(S)) < 1e-12
 
 
+@pytest.mark.parametrize("m", [64, 200, 1000])
+def test_cholesky_inverse_ill_conditioned(m):
+    """Eigenvalues spread over 1e0..1e8: the leaf panels' rsqrt pivots and
+    rank-8 updates keep the inverse at numpy's backward-stable accuracy."""
+    rng = np.random.default_rng(m + 7)
+    Q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    S = (Q * np.logspace(0, 8, m)) @ Q.T
+    S = (S + S.T) / 2
+    inv = L.cholesky_inverse(S)
+    ref = np.linalg.inv(S)
+    assert relerr(inv, ref) < 1e-7
+    assert relerr(inv @ S, np.eye(m)) < 1e-7
+
+
 def test_cholesky_kat_and_indefinite():
     S = np.array([[4.0, 2.0], [2.0, 3.0]])
     x = L.cholesky_inverse(S) @ np.array([6.0, 5.0])
