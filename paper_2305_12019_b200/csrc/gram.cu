@@ -178,10 +178,8 @@ __global__ void syrk_finish_kernel(const double* W, int64_t ldw, int64_t wslice,
 
 // Dense factor + inverse of one diagonal block (m <= LEAF_MAX) in shared
 // memory: A = L L^T (L lower), Linv = L^{-1}.  Upper parts are written as
-// zeros.  Factor: 8-column panels (below).  Inverse by recursive doubling: with the
-// inverses of the diagonal s x s blocks known, each 2s x 2s diagonal block
-// gets its off-diagonal block -Li22 (L21 Li11); all blocks of a level are
-// independent (log2(m) levels, two barriers each).  blockDim = 256.
+// zeros.  Factor: 8-column panels; inverse: forward substitution, 8 columns
+// per warp (below).  blockDim = 256.
 constexpr int LEAF_MAX = 64;  // three (LEAF_MAX x LEAF_MAX+1) doubles in dynamic shared memory
 constexpr size_t LEAF_SMEM = (size_t)3 * LEAF_MAX * (LEAF_MAX + 1) * sizeof(double);
 __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t ldl, int m, int* info,
@@ -199,6 +197,9 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
     Li[i][j] = 0.0;
   }
   __syncthreads();
+#ifdef LEAF_TIMING
+  const long long lt0 = clock64();
+#endif
   // Factor in 8-column panels.  Warp 0 factors the panel in registers (lane l
   // owns rows p0 + l and p0 + 32 + l; pivots and L[k][j] by shuffles, no
   // block barrier per column), then the whole block applies the panel's
@@ -225,8 +226,8 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
             d = 1.0;
           }
           const double rinv = rsqrt(d), r = d * rinv;
-          if (t == c) Pa[c] = r;
-          else if (t > c) Pa[c] = Pa[c] * rinv;
+          const double sc = Pa[c] * rinv;  // selects, not branches: no divergence per column
+          Pa[c] = t == c ? r : (t > c ? sc : Pa[c]);
           Pb[c] = Pb[c] * rinv;
 #pragma unroll
           for (int c2 = c + 1; c2 < 8; ++c2) {
@@ -245,46 +246,86 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
       }
     }
     __syncthreads();
+    // trailing triangle: thread t owns column k = q0 + (t & 63) (its 8
+    // panel multipliers in registers) and rows i = q0 + (t >> 6) + 4 s >= k
     const int q0 = p0 + pw, R = m - q0;
-    for (int idx = t; idx < R * R; idx += blockDim.x) {
-      const int ii = idx / R, kk = idx - ii * R;
-      if (kk <= ii) {
-        const int i = q0 + ii, k = q0 + kk;
-        double acc = L[i][k];
-        for (int c = 0; c < pw; ++c) acc = acc - L[i][p0 + c] * L[k][p0 + c];
-        L[i][k] = acc;
+    const int kk = t & 63;
+    if (kk < R) {
+      const int k = q0 + kk;
+      double lk[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) lk[c] = c < pw ? L[k][p0 + c] : 0.0;
+#pragma unroll 4
+      for (int ii = t >> 6; ii < R; ii += 4) {
+        if (ii >= kk) {
+          const int i = q0 + ii;
+          double acc = L[i][k];
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (c < pw) acc = acc - L[i][p0 + c] * lk[c];
+          L[i][k] = acc;
+        }
       }
     }
     __syncthreads();
   }
-  if (t < m) Li[t][t] = 1.0 / L[t][t];
+#ifdef LEAF_TIMING
+  const long long lt1 = clock64();
+#endif
+  // Inverse by forward substitution, L X = I: each warp solves 8 columns
+  // c0 .. c0+7 (lane l holds rows l and l + 32 of each); step j turns b_j
+  // into x_j = b_j / L_jj (one shuffle per column) and subtracts
+  // L[i][j] x_j from the rows below -- no block barrier, m - c0 steps.
+  if (t < m) Tm[0][t] = 1.0 / L[t][t];
   __syncthreads();
-  for (int s = 1; s < m; s *= 2) {
-    const int nent = (m + 2 * s - 1) / (2 * s) * s * s;  // 2s-blocks x (s x s) entries
-    // T = L21 Li11 for every 2s-block (rows b+s.., cols b..b+s)
-    for (int e = t; e < nent; e += blockDim.x) {
-      const int b = (e / (s * s)) * 2 * s, i = (e % (s * s)) / s, jj = e % s;
-      const int row = b + s + i, col = b + jj;
-      if (row < m) {
-        double acc = 0.0;
-        for (int kk = jj; kk < s; ++kk) acc += L[row][b + kk] * Li[b + kk][col];
-        Tm[row][col] = acc;
+  {
+    // column blocks paired long/short per SM sub-partition (warps w, w + 4)
+    const int w = t >> 5, l = t & 31, c0 = 8 * (w < 4 ? w : 11 - w);
+    if (c0 < m) {
+      double Xa[8], Xb[8];
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        Xa[cc] = l == c0 + cc ? 1.0 : 0.0;
+        Xb[cc] = l + 32 == c0 + cc ? 1.0 : 0.0;
+      }
+      // rows <= j have la = lb = 0 (x - 0 * y == x): selects only, no branch
+      for (int j = c0; j < (m < 32 ? m : 32); ++j) {
+        const double dj = Tm[0][j];
+        const double la = l > j ? L[l][j] : 0.0;
+        const double lb = l + 32 < m ? L[l + 32][j] : 0.0;
+        const bool own = l == j;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const double xj = __shfl_sync(0xffffffffu, Xa[cc], j) * dj;
+          const double ua = Xa[cc] - la * xj;
+          Xb[cc] = Xb[cc] - lb * xj;
+          Xa[cc] = own ? xj : ua;
+        }
+      }
+      for (int j = c0 > 32 ? c0 : 32; j < m; ++j) {  // rows < 32 are final
+        const double dj = Tm[0][j];
+        const double lb = l + 32 > j && l + 32 < m ? L[l + 32][j] : 0.0;
+        const bool own = l == j - 32;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const double xj = __shfl_sync(0xffffffffu, Xb[cc], j - 32) * dj;
+          const double ub = Xb[cc] - lb * xj;
+          Xb[cc] = own ? xj : ub;
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        if (c0 + cc < m) {
+          if (l < m) Li[l][c0 + cc] = Xa[cc];
+          if (l + 32 < m) Li[l + 32][c0 + cc] = Xb[cc];
+        }
       }
     }
-    __syncthreads();
-    // Li21 = -Li22 T
-    for (int e = t; e < nent; e += blockDim.x) {
-      const int b = (e / (s * s)) * 2 * s, i = (e % (s * s)) / s, jj = e % s;
-      const int row = b + s + i, col = b + jj;
-      if (row < m) {
-        double acc = 0.0;
-        for (int kk = 0; kk <= i; ++kk)
-          if (b + s + kk < m) acc += Li[row][b + s + kk] * Tm[b + s + kk][col];
-        Li[row][col] = -acc;
-      }
-    }
-    __syncthreads();
   }
+  __syncthreads();
+#ifdef LEAF_TIMING
+  if (t == 0 && offset == 0) printf("[leaf] m=%d factor %lld inverse %lld cycles\n", m, lt1 - lt0, clock64() - lt1);
+#endif
   for (int idx = t; idx < m * m; idx += blockDim.x) {
     const int i = idx / m, j = idx % m;
     A[i * lda + j] = (j <= i) ? L[i][j] : 0.0;
