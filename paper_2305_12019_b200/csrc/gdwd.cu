@@ -203,7 +203,7 @@ struct gdwd_ctx {
   double fro2 = -1.0;  // ||Z~||_F^2 (device reduction at upload)
   // overlapped dense upload (pinned source): row chunks on a copy stream,
   // the SMW Gram block-rows on a second stream as the chunks land
-  static constexpr int UP_NCH = 8;
+  static constexpr int UP_NCH = 16;
   cudaStream_t cst = nullptr, gst = nullptr;
   cudaEvent_t up_ev[UP_NCH] = {}, gram_ev = nullptr, st_ev = nullptr;
   int64_t up_r[UP_NCH + 1] = {};
