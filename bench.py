@@ -297,7 +297,7 @@ def run_b200(args, dist: Dist):
                     "traffic": round(tr["per_iteration"] * iters_timed) if tr else None,
                     "algorithmic_bytes_per_launch": alg,
                     "note": "K and G^-1 K (2 x %.0f MB) never leave the chip after the one cold load (ncu: DRAM "
-                            "traffic = that load, L2 hit 97%%): each CTA's own K rows sit in tensor memory for "
+                            "traffic = that load, L2 hit 95%%): each CTA's own K rows sit in tensor memory for "
                             "n <= 2048 (K and G^-1 K for n <= 1024), the rest is read from L2; the loop is bound "
                             "by L2 / tensor-memory row latency and grid-barrier latency (one launch, 3 grid "
                             "barriers and 2 row sweeps of K and G^-1 K per iteration)" % (8 * n * n / 1e6)}
