@@ -85,14 +85,21 @@ template <bool AK, bool BKF>
 __global__ void __launch_bounds__(GT) gemm_dmma_kernel(Opnd A, Opnd B, int64_t M, int64_t N, int64_t K,
                                                        int64_t kslice, double* W, int64_t ldw,
                                                        int64_t wslice, bool upper_only, double alpha,
-                                                       double beta, double* C, int64_t ldc) {
+                                                       double beta, double* C, int64_t ldc, int tri = 0) {
   const int bm = blockIdx.y, bn = blockIdx.x;
   if (upper_only && bn < bm) return;
+  if ((tri & GEMM_C_LOWER) && bn > bm) return;
   __shared__ double As[2][TILE_DOUBLES];
   __shared__ double Bs[2][TILE_DOUBLES];
   const int64_t m0 = (int64_t)bm * BM, n0 = (int64_t)bn * BN;
-  const int64_t kb = (int64_t)blockIdx.z * kslice;
-  const int64_t ke = (kb + kslice < K) ? kb + kslice : K;
+  int64_t kb = (int64_t)blockIdx.z * kslice;
+  int64_t ke = (kb + kslice < K) ? kb + kslice : K;
+  // k ranges where a triangular operand is zero for every row of the tile
+  // (tile origins are multiples of BK, so kb stays slab-aligned)
+  if ((tri & GEMM_B_KLE_N) && n0 + BN < ke) ke = n0 + BN;
+  if ((tri & GEMM_A_KLE_M) && m0 + BM < ke) ke = m0 + BM;
+  if ((tri & GEMM_B_KGE_N) && n0 > kb) kb = n0;
+  if ((tri & GEMM_A_KGE_M) && m0 > kb) kb = m0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp >> 2, wn = warp & 3;
   const int g = lane >> 2, t4 = lane & 3;
@@ -360,18 +367,19 @@ int grid_for(int64_t tot) {
 // A(m,k) = a[m*sam + k*sak]; B(n,k) = b[n*sbn + k*sbk].
 cudaError_t gemm_f64(const double* a, int64_t sam, int64_t sak, const double* b, int64_t sbn,
                      int64_t sbk, int64_t M, int64_t N, int64_t K, double alpha, double beta, double* C,
-                     int64_t ldc, cudaStream_t st) {
+                     int64_t ldc, cudaStream_t st, int tri) {
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), 1);
   Opnd A{a, sam, sak}, B{b, sbn, sbk};
   const bool ak = (sak == 1), bk = (sbk == 1);
   if (ak && bk)
-    gemm_dmma_kernel<true, true><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc);
+    gemm_dmma_kernel<true, true><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc, tri);
   else if (ak)
-    gemm_dmma_kernel<true, false><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc);
+    gemm_dmma_kernel<true, false><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc, tri);
   else if (bk)
-    gemm_dmma_kernel<false, true><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc);
+    gemm_dmma_kernel<false, true><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc, tri);
   else
-    gemm_dmma_kernel<false, false><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc);
+    gemm_dmma_kernel<false, false><<<grid, GT, 0, st>>>(A, B, M, N, K, K, nullptr, 0, 0, false, alpha, beta, C, ldc,
+                                                        tri);
   return cudaGetLastError();
 }
 
@@ -470,10 +478,10 @@ cudaError_t chol_rec(double* A, double* Li, double* T, int64_t ld, int64_t m, in
   cudaError_t e = chol_rec(A11, L11i, T, ld, m1, off, info, st, side, evs);
   if (e != cudaSuccess) return e;
   // L21 = A21 * L11i^T   (m2 x m1): A(i,k)=A21[i][k], B(j,k)=L11i[j][k]
-  e = gemm_f64(A21, ld, 1, L11i, ld, 1, m2, m1, m1, 1.0, 0.0, L21, ld, st);
+  e = gemm_f64(A21, ld, 1, L11i, ld, 1, m2, m1, m1, 1.0, 0.0, L21, ld, st, GEMM_B_KLE_N);
   if (e != cudaSuccess) return e;
-  // A22 -= L21 L21^T
-  e = gemm_f64(L21, ld, 1, L21, ld, 1, m2, m2, m1, -1.0, 1.0, A22, ld, st);
+  // A22 -= L21 L21^T (lower tiles: the recursion reads only A22's lower triangle)
+  e = gemm_f64(L21, ld, 1, L21, ld, 1, m2, m2, m1, -1.0, 1.0, A22, ld, st, GEMM_C_LOWER);
   if (e != cudaSuccess) return e;
   // beside the lower-right recursion: A21 <- L21 * L11i (A(i,k)=L21[i][k], B(j,k)=L11i[k][j])
   cudaEvent_t ev_fork, ev_join;
@@ -483,14 +491,14 @@ cudaError_t chol_rec(double* A, double* Li, double* T, int64_t ld, int64_t m, in
   evs.push_back(ev_join);
   if ((e = cudaEventRecord(ev_fork, st)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return e;
-  e = gemm_f64(L21, ld, 1, L11i, 1, ld, m2, m1, m1, 1.0, 0.0, A21, ld, side);
+  e = gemm_f64(L21, ld, 1, L11i, 1, ld, m2, m1, m1, 1.0, 0.0, A21, ld, side, GEMM_B_KGE_N);
   if (e != cudaSuccess) return e;
   if ((e = cudaEventRecord(ev_join, side)) != cudaSuccess) return e;
   e = chol_rec(A22, L22i, T + m1 * ld + m1, ld, m2, off + m1, info, st, side, evs);
   if (e != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(st, ev_join, 0)) != cudaSuccess) return e;
   // L21i = -L22i * (L21 L11i) : A(i,k)=L22i[i][k], B(j,k)=A21[k][j]
-  e = gemm_f64(L22i, ld, 1, A21, 1, ld, m2, m1, m2, -1.0, 0.0, L21i, ld, st);
+  e = gemm_f64(L22i, ld, 1, A21, 1, ld, m2, m1, m2, -1.0, 0.0, L21i, ld, st, GEMM_A_KLE_M);
   return e;
 }
 
@@ -508,7 +516,7 @@ cudaError_t chol_inverse(double* A, double* Li, double* T, int64_t ld, int64_t m
   // A^{-1} = Li^T Li : C(i,j) = sum_k Li[k][i] Li[k][j] -- symmetric: upper
   // tiles on the DMMA SYRK path, mirrored (T is the workspace)
   if (gram_slices(m, m) == 1) return gram_syrk(Li, m, m, ld, true, 1.0, 0.0, A, ld, T, st);
-  return gemm_f64(Li, 1, ld, Li, 1, ld, m, m, m, 1.0, 0.0, A, ld, st);
+  return gemm_f64(Li, 1, ld, Li, 1, ld, m, m, m, 1.0, 0.0, A, ld, st, GEMM_A_KGE_M | GEMM_B_KGE_N);
 }
 
 }  // namespace gdwd
