@@ -207,65 +207,66 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
 #ifdef LEAF_TIMING
   const long long lt0 = clock64();
 #endif
-  // Factor in 8-column panels.  Warp 0 factors the panel in registers (lane l
-  // owns rows p0 + l and p0 + 32 + l; pivots and L[k][j] by shuffles, no
-  // block barrier per column), then the whole block applies the panel's
-  // rank-8 update to the trailing triangle, subtracting the 8 products in
-  // column order (the same sequence of roundings as column-by-column
-  // rank-1 updates).  The per-column chain is one rsqrt (<= 1 ulp) instead
-  // of an IEEE sqrt and division behind two block barriers.
-  for (int p0 = 0; p0 < m; p0 += 8) {
+  // Factor in 8-column panels.  Warp 0 factors a panel in registers (lane l
+  // owns rows p0 + l and p0 + 32 + l; pivots and L[k][j] by shuffles, an
+  // rsqrt per pivot (<= 1 ulp) instead of an IEEE sqrt and division, no
+  // block barrier per column).  Look-ahead: in round p warp 0 applies panel
+  // p's rank-8 update to panel p+1's columns and factors panel p+1 while the
+  // other warps apply it to the columns beyond -- one block barrier per
+  // panel, the bulk update off the critical path.  Updates subtract the 8
+  // products in column order (the roundings of column-by-column rank-1
+  // updates).
+  auto factor_panel = [&](int p0) {  // warp 0
     const int pw = m - p0 < 8 ? m - p0 : 8;
-    if (t < 32) {
-      const int ra = p0 + t, rb = p0 + 32 + t;
-      double Pa[8], Pb[8];
+    const int ra = p0 + t, rb = p0 + 32 + t;
+    double Pa[8], Pb[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        Pa[c] = (ra < m && c < pw) ? L[ra][p0 + c] : 0.0;
-        Pb[c] = (rb < m && c < pw) ? L[rb][p0 + c] : 0.0;
-      }
+    for (int c = 0; c < 8; ++c) {
+      Pa[c] = (ra < m && c < pw) ? L[ra][p0 + c] : 0.0;
+      Pb[c] = (rb < m && c < pw) ? L[rb][p0 + c] : 0.0;
+    }
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if (c < pw) {
-          double d = __shfl_sync(0xffffffffu, Pa[c], c);
-          if (!(d > 0.0)) {
-            if (t == 0) bad = 1;
-            d = 1.0;
-          }
-          const double rinv = rsqrt(d), r = d * rinv;
-          const double sc = Pa[c] * rinv;  // selects, not branches: no divergence per column
-          Pa[c] = t == c ? r : (t > c ? sc : Pa[c]);
-          Pb[c] = Pb[c] * rinv;
-#pragma unroll
-          for (int c2 = c + 1; c2 < 8; ++c2) {
-            const double lk = __shfl_sync(0xffffffffu, Pa[c], c2);  // L[p0+c2][p0+c]
-            Pa[c2] = Pa[c2] - Pa[c] * lk;
-            Pb[c2] = Pb[c2] - Pb[c] * lk;
-          }
+    for (int c = 0; c < 8; ++c) {
+      if (c < pw) {
+        double d = __shfl_sync(0xffffffffu, Pa[c], c);
+        if (!(d > 0.0)) {
+          if (t == 0) bad = 1;
+          d = 1.0;
         }
-      }
+        const double rinv = rsqrt(d), r = d * rinv;
+        const double sc = Pa[c] * rinv;  // selects, not branches: no divergence per column
+        Pa[c] = t == c ? r : (t > c ? sc : Pa[c]);
+        Pb[c] = Pb[c] * rinv;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if (c < pw) {
-          if (ra < m && t >= c) L[ra][p0 + c] = Pa[c];
-          if (rb < m) L[rb][p0 + c] = Pb[c];
+        for (int c2 = c + 1; c2 < 8; ++c2) {
+          const double lk = __shfl_sync(0xffffffffu, Pa[c], c2);  // L[p0+c2][p0+c]
+          Pa[c2] = Pa[c2] - Pa[c] * lk;
+          Pb[c2] = Pb[c2] - Pb[c] * lk;
         }
       }
     }
-    __syncthreads();
-    // trailing triangle: thread t owns column k = q0 + (t & 63) (its 8
-    // panel multipliers in registers) and rows i = q0 + (t >> 6) + 4 s >= k
-    const int q0 = p0 + pw, R = m - q0;
-    const int kk = t & 63;
-    if (kk < R) {
-      const int k = q0 + kk;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (c < pw) {
+        if (ra < m && t >= c) L[ra][p0 + c] = Pa[c];
+        if (rb < m) L[rb][p0 + c] = Pb[c];
+      }
+    }
+  };
+  // panel (p0, pw) applied to columns [kb, ke): worker u of nthr owns column
+  // k = kb + u % ncol (its 8 multipliers in registers) and rows
+  // i = kb + u / ncol + 4 s >= k
+  auto update_cols = [&](int p0, int pw, int kb, int ke, int u, int nthr) {
+    const int ncol = ke - kb;
+    for (int idx = u; idx < 4 * ncol; idx += nthr) {
+      const int kk = idx % ncol, ph = idx / ncol, k = kb + kk;
       double lk[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) lk[c] = c < pw ? L[k][p0 + c] : 0.0;
 #pragma unroll 4
-      for (int ii = t >> 6; ii < R; ii += 4) {
+      for (int ii = ph; ii < m - kb; ii += 4) {
         if (ii >= kk) {
-          const int i = q0 + ii;
+          const int i = kb + ii;
           double acc = L[i][k];
 #pragma unroll
           for (int c = 0; c < 8; ++c)
@@ -273,6 +274,19 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
           L[i][k] = acc;
         }
       }
+    }
+  };
+  if (t < 32) factor_panel(0);
+  __syncthreads();
+  for (int p0 = 0; p0 + 8 < m; p0 += 8) {  // panel p0 is factored; q0 = p0 + 8 < m
+    const int q0 = p0 + 8;
+    const int q1 = q0 + 8 < m ? q0 + 8 : m;
+    if (t < 32) {
+      update_cols(p0, 8, q0, q1, t, 32);
+      __syncwarp();
+      factor_panel(q0);
+    } else if (q1 < m) {
+      update_cols(p0, 8, q1, m, t - 32, blockDim.x - 32);
     }
     __syncthreads();
   }
