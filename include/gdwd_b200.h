@@ -134,6 +134,10 @@ int gdwd_comm_unique_id(uint8_t* out128);  /* ncclGetUniqueId, on one rank */
 int gdwd_comm_init_nccl(gdwd_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t* id128, int64_t n_global);
 int gdwd_comm_init_host(gdwd_ctx* ctx, int32_t nranks, int32_t rank, gdwd_allreduce_cb cb, void* user,
                         int64_t n_global);
+/* Sum of a host vector over the shards of the attached communicator (identity
+ * when unsharded): the host-side n-sums such as the global train error
+ * (solver.py:558-559). */
+int gdwd_allreduce_host(gdwd_ctx* ctx, double* buf, int64_t count);
 
 /* operator seams ------------------------------------------------------------
  * Z~ v  (scipy csc_matvec at solver.py:496,508,517,300; subsolvers.py:146) */
@@ -240,6 +244,9 @@ int gdwd_chol_inverse(int32_t device, const double* S, int64_t m, double* inv_ou
  * sum_over_rows=1: X^T X (cols x cols, "Z Z^T" of subsolvers.py:76)
  * sum_over_rows=0: X X^T (rows x rows, "Z^T Z" of subsolvers.py:109)
  * result = gram / div + shift * I. */
+/* device time (ms, mean of reps) of the one-time FP64 DMMA Gram of the
+ * resident dense Z~ (bench: the Gram's tensor-pipe roofline) */
+int gdwd_time_gram(gdwd_ctx* ctx, int32_t reps, double* ms);
 int gdwd_gram(int32_t device, const double* X, int64_t rows, int64_t cols, int32_t sum_over_rows, double div,
               double shift, double* out);
 /* psqmr (linalg/psqmr.py:27-95) with a dense symmetric operator A (m x m,

@@ -21,6 +21,7 @@ from .solver import (
     SolverConfig,
     SolverKind,
     SolverState,
+    as_problem,
     compute_weights,
     device_problem,
     dual_objective,
@@ -44,7 +45,7 @@ __version__ = "0.1.0"
 __all__ = [
     "Backend", "DegenerateSchurError", "DeviceProblem", "FeatureMeta", "IndefiniteMatrixError", "KKTResiduals",
     "LanczosConvergenceError", "ModelFile", "ProblemData", "SingleClassError", "SolveResult", "SolverConfig",
-    "SolverKind", "SolverState", "SparseFormatError", "SparseMatrixCSC", "compute_weights", "csc_from_dense",
+    "SolverKind", "SolverState", "SparseFormatError", "as_problem", "SparseMatrixCSC", "compute_weights", "csc_from_dense",
     "csc_from_triplets", "device_problem", "identity_meta", "matvec", "newton_r", "newton_r_sweep",
     "scale_problem", "select_solver", "sgs_admm_solve", "update_sigma", "decision_values", "predict",
     "train_error", "compute_penalty_C", "kkt_residuals", "primal_objective", "dual_objective", "ModelFormatError",

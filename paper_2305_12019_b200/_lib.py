@@ -29,7 +29,7 @@ SYMBOLS = [
     "gdwd_solve_begin", "gdwd_solve_iterate", "gdwd_solve_end", "gdwd_time_iterations", "gdwd_set_profile",
     "gdwd_get_profile", "gdwd_reset_counters", "gdwd_frobenius_sq", "gdwd_comm_unique_id",
     "gdwd_comm_init_nccl", "gdwd_comm_init_host", "gdwd_generate_dense", "gdwd_scale_dense",
-    "gdwd_download_dense", "gdwd_set_lanczos_start",
+    "gdwd_download_dense", "gdwd_set_lanczos_start", "gdwd_allreduce_host", "gdwd_time_gram",
 ]
 
 
@@ -110,6 +110,8 @@ def _declare(lib):
         "gdwd_set_lanczos_start": (C.c_int, [vp, _P, _I64]),
         "gdwd_comm_init_nccl": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int64]),
         "gdwd_comm_init_host": (C.c_int, [vp, C.c_int32, C.c_int32, ALLREDUCE_CB, vp, C.c_int64]),
+        "gdwd_allreduce_host": (C.c_int, [vp, _P, _I64]),
+        "gdwd_time_gram": (C.c_int, [vp, C.c_int32, _P]),
         "gdwd_get_state": (C.c_int, [vp, _P, _P, _P, _P, _P, _P, _P, _P]),
         "gdwd_get_history": (C.c_int, [vp, _P, _I64, C.POINTER(C.c_int64)]),
         "gdwd_newton_sweep": (C.c_int, [C.c_int32, _I64, _P, C.c_double, C.c_double, _P, _P, C.c_double, C.c_int32,

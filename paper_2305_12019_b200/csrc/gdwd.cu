@@ -259,7 +259,6 @@ struct gdwd_ctx {
   int64_t ldg = 0;
   int fac_iter_gram = 0;
   DevBuf pk_part, gkmat;
-  int pk_version = 3;
   // proximal fallback (subsolvers.py:159-256)
   bool prox = false;
   int ell = 10;
@@ -674,6 +673,7 @@ static void finish_upload(gdwd_ctx* ctx) {
 }
 
 static int compute_fro2(gdwd_ctx* ctx, const double* a, int64_t rows, int64_t cols, int64_t ld) {
+  ctx->fro2_pending = false;  // a deferred reduction of earlier data must not overwrite this value
   double* dv = nullptr;
   CK(cudaMalloc(&dv, sizeof(double)));
   run_vm(ctx, OpSumSq{a, cols, ld, dv}, rows * cols, "vmap_fro2", true);
@@ -1166,7 +1166,10 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
   ctx->has_problem = false;
   ctx->data_gen++;
   RC(ensure_scratch(ctx, n, d));
-  return nnz > 0 ? compute_fro2(ctx, ctx->csc_val, 1, nnz, nnz) : (ctx->fro2 = 0.0, GDWD_OK);
+  if (nnz > 0) return compute_fro2(ctx, ctx->csc_val, 1, nnz, nnz);
+  ctx->fro2_pending = false;
+  ctx->fro2 = 0.0;
+  return GDWD_OK;
 }
 
 // DIRECT / SMW2 on sparse input: materialise the dense sample-major copy once
@@ -2185,10 +2188,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
     int nb = 0;
     // 11 vector slots: 3 staged, 6 bulk-copied inputs, y and G^{-1} y/|y|
     const size_t sm = (size_t)(11 * ((n + 3) / 2 * 2)) * sizeof(double);
-    // kernel version: 3 barriers per iteration (default) or the 4-barrier
-    // association (GDWD_PK_VERSION=2, kept for A/B checks)
-    ctx->pk_version = (getenv("GDWD_PK_VERSION") && atoi(getenv("GDWD_PK_VERSION")) == 2) ? 2 : 3;
-    const void* kfn = ctx->pk_version == 3 ? (const void*)gram_smw_persistent3<0> : (const void*)gram_smw_persistent;
+    const void* kfn = (const void*)gram_smw_persistent3<0>;
     if (sm > 220 * 1024 || cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
       cudaGetLastError();
       ctx->persistent = false;
@@ -2233,42 +2233,45 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
     }
     const int diag = getenv("GDWD_PK_DIAG") ? atoi(getenv("GDWD_PK_DIAG")) : 0;
     const size_t sm = (size_t)(11 * ((ctx->n + 3) / 2 * 2)) * sizeof(double);
-    if (ctx->pk_version == 3) {
-      // 3 grid barriers per iteration (persist3.cuh)
-      unsigned* ctr = nullptr;
-      if (!(getenv("GDWD_PK_BAR") && atoi(getenv("GDWD_PK_BAR")) == 0)) {
-        ctr = reinterpret_cast<unsigned*>(ctx->pk_part.p + (size_t)2 * NUM_SMS * PK_NPART);
-        CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), ctx->st));
-      }
-      // own rows of K and GK resident in tensor memory when n <= 1024 (<= 7
-      // rows per CTA, 8 ceil(n/64) words per lane and row); K alone up to
-      // n = 2048, GK streamed from L2 in 8-chunk groups whose loads overlap
-      // the group's TMEM words (c2: 24.9 vs 27.0 us/iteration streaming both;
-      // a fused 16-load variant spilled in-flight registers and was slower).
-      int tmem = ctx->n <= 1024 ? 2 : (ctx->n <= 2048 ? 1 : 0);
-      if (getenv("GDWD_PK_TMEM")) {  // diagnostics: 0 L2 only, 1 K in TMEM (n <= 2048), 2 K and GK (n <= 1024)
-        const int want = atoi(getenv("GDWD_PK_TMEM"));
-        tmem = want >= 2 && ctx->n <= 1024 ? 2 : (want >= 1 && ctx->n <= 2048 ? 1 : 0);
-      }
-      PK3Args pa{D, ctx->kmat.p, ctx->gkmat.p, D.kap, D.gam, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host,
-                 diag, ts, ctx->use_sgs ? 1 : 0, ctr};
-      void* args[] = {&pa};
-      const void* kfn = tmem == 2   ? (const void*)gram_smw_persistent3<2>
-                        : tmem == 1 ? (const void*)gram_smw_persistent3<1>
-                                    : (const void*)gram_smw_persistent3<0>;
-      CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      Launch L(ctx, "persistent_gram_smw2");
-      CK(cudaLaunchCooperativeKernel(kfn, dim3(NUM_SMS), dim3(PK_THREADS), args, sm, ctx->st));
-    } else {
-      PKArgs pa{D, ctx->kmat.p, ctx->fac.p, ctx->gkmat.p, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host, diag, ts,
-                ctx->use_sgs ? 1 : 0};
-      void* args[] = {&pa};
-      Launch L(ctx, "persistent_gram_smw2");
-      CK(cudaLaunchCooperativeKernel((void*)gram_smw_persistent, dim3(NUM_SMS), dim3(PK_THREADS), args, sm, ctx->st));
+    // 3 grid barriers per iteration (persist3.cuh)
+    unsigned* ctr = nullptr;
+    if (!(getenv("GDWD_PK_BAR") && atoi(getenv("GDWD_PK_BAR")) == 0)) {
+      ctr = reinterpret_cast<unsigned*>(ctx->pk_part.p + (size_t)2 * NUM_SMS * PK_NPART);
+      CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), ctx->st));
     }
+    // own rows of K and GK resident in tensor memory when n <= 1024 (<= 7
+    // rows per CTA, 8 ceil(n/64) words per lane and row); K alone up to
+    // n = 2048, GK streamed from L2 in 8-chunk groups whose loads overlap
+    // the group's TMEM words (c2: 24.9 vs 27.0 us/iteration streaming both;
+    // a fused 16-load variant spilled in-flight registers and was slower).
+    int tmem = ctx->n <= 1024 ? 2 : (ctx->n <= 2048 ? 1 : 0);
+    if (getenv("GDWD_PK_TMEM")) {  // diagnostics: 0 L2 only, 1 K in TMEM (n <= 2048), 2 K and GK (n <= 1024)
+      const int want = atoi(getenv("GDWD_PK_TMEM"));
+      tmem = want >= 2 && ctx->n <= 1024 ? 2 : (want >= 1 && ctx->n <= 2048 ? 1 : 0);
+    }
+    PK3Args pa{D, ctx->kmat.p, ctx->gkmat.p, D.kap, D.gam, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host,
+               diag, ts, ctx->use_sgs ? 1 : 0, ctr};
+    void* args[] = {&pa};
+    const void* kfn = tmem == 2   ? (const void*)gram_smw_persistent3<2>
+                      : tmem == 1 ? (const void*)gram_smw_persistent3<1>
+                                  : (const void*)gram_smw_persistent3<0>;
+    // the TMEM variants allocate all 512 columns per CTA while spinning on
+    // grid barriers: a second CTA on the same SM would block in tcgen05.alloc
+    // forever.  One CTA per SM holds today by register pressure; enforce it by
+    // padding the dynamic shared memory past half an SM if that ever changes.
+    size_t sm_launch = sm;
+    if (tmem) {
+      int nb_tm = 0;
+      CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb_tm, kfn, PK_THREADS, sm));
+      if (nb_tm > 1) sm_launch = std::max(sm, (size_t)120 * 1024);
+    }
+    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_launch));
+    Launch L(ctx, "persistent_gram_smw2");
+    CK(cudaLaunchCooperativeKernel(kfn, dim3(NUM_SMS), dim3(PK_THREADS), args, sm_launch, ctx->st));
     CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
-    if (ts) pk_timing_report(ts, tsn, ctx->pk_version);
+    if (ts) pk_timing_report(ts, tsn, 3);
     ctx->k_host = ctx->Sh->stopped ? ctx->Sh->iters_done : kend;
     ctx->stopped = ctx->Sh->stopped != 0;
   }
@@ -2455,6 +2458,23 @@ extern "C" int gdwd_comm_init_host(gdwd_ctx* ctx, int32_t nranks, int32_t rank, 
   return comm_finish_init(ctx, nranks, rank, n_global);
 }
 
+// Sum of a host vector over the shards of the attached communicator (the
+// identity without one): the host side's n-sums, e.g. the global train error.
+extern "C" int gdwd_allreduce_host(gdwd_ctx* ctx, double* buf, int64_t count) {
+  if (!ctx || (!buf && count > 0) || count < 0) return set_err(ctx, GDWD_ERR_VALUE, "bad all-reduce arguments");
+  if (!ctx->comm_mode || count == 0) return GDWD_OK;
+  CK(cudaSetDevice(ctx->device));
+  DevBuf tmp;
+  CK(tmp.ensure(count));
+  CK(cudaMemcpyAsync(tmp.p, buf, count * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  allreduce(ctx, tmp.p, count);
+  CK(cudaMemcpyAsync(buf, tmp.p, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  tmp.release();
+  if (ctx->comm_err) return set_err(ctx, GDWD_ERR_CUDA, "all-reduce failed");
+  return GDWD_OK;
+}
+
 extern "C" int gdwd_set_profile(gdwd_ctx* ctx, int32_t enable) {
   if (!ctx) return GDWD_ERR_VALUE;
   ctx->prof = enable != 0;
@@ -2489,6 +2509,7 @@ extern "C" int gdwd_reset_counters(gdwd_ctx* ctx) {
 // the solve's stream, with a synchronize on both sides.
 extern "C" int gdwd_time_iterations(gdwd_ctx* ctx, int32_t count, double* ms, int32_t* iters_done) {
   if (!ctx || !ctx->in_solve || !ms) return set_err(ctx, GDWD_ERR_VALUE, "no solve in progress");
+  CK(cudaSetDevice(ctx->device));  // events belong to the context's device (one host thread per GPU)
   CK(cudaStreamSynchronize(ctx->st));
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
@@ -2643,6 +2664,37 @@ extern "C" int gdwd_gram(int32_t device, const double* X, int64_t rows, int64_t 
   CK(cudaMemcpy2D(dX, ld * 8, X, cols * 8, cols * 8, rows, cudaMemcpyHostToDevice));
   CK(gram_syrk(dX, rows, cols, ld, sum_over_rows != 0, div, shift, C, M, W, 0));
   CK(cudaMemcpy(outp, C, (size_t)M * M * 8, cudaMemcpyDeviceToHost));
+  return GDWD_OK;
+}
+
+// Device time of the one-time Gram of the resident dense Z~ (the FP64
+// tensor-core SYRK the DIRECT / SMW2 / Gram-operator setups run): the smaller
+// side's Gram, averaged over `reps` launches after one warm-up (CUDA events).
+extern "C" int gdwd_time_gram(gdwd_ctx* ctx, int32_t reps, double* ms) {
+  if (!ctx || !ms || reps < 1) return set_err(ctx, GDWD_ERR_VALUE, "bad arguments");
+  if (!ctx->has_dense) return set_err(ctx, GDWD_ERR_VALUE, "no dense data");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t n = ctx->n, d = ctx->d;
+  const bool rows = n >= d;  // Z~ Z~^T (d x d) when samples dominate, else Z~^T Z~ (n x n)
+  const int64_t M = rows ? d : n, K = rows ? n : d, ld = (M + 1) / 2 * 2;
+  DevBuf c, w;
+  CK(c.ensure((size_t)M * ld));
+  CK(w.ensure((size_t)gram_workspace_doubles(M, K)));
+  CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, rows, 1.0, 0.0, c.p, ld, w.p, ctx->st));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaEventRecord(a, ctx->st));
+  for (int r = 0; r < reps; ++r) CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, rows, 1.0, 0.0, c.p, ld, w.p, ctx->st));
+  CK(cudaEventRecord(b, ctx->st));
+  CK(cudaEventSynchronize(b));
+  float f = 0.f;
+  cudaEventElapsedTime(&f, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  c.release();
+  w.release();
+  *ms = f / reps;
   return GDWD_OK;
 }
 

@@ -14,6 +14,9 @@ Communicators:
   * ``HostCommunicator``: all-reduce through a host callback (gloo process
     groups, or threads emulating ranks on one GPU in tests).
 
+``solve_on_devices`` (also ``sgs_admm_solve(..., devices=[...])``) drives all
+ranks from one process, one host thread per GPU.
+
 SMW2 couples all samples through its n x n Gram, so it is not sharded
 (``bench.py --gpus N`` runs replicas for config 2).
 """
@@ -134,6 +137,68 @@ def global_train_error(result, local: ProblemData, allreduce: Callable[[np.ndarr
     return 100.0 * float(allreduce(bad)[0]) / n_global
 
 
+def solve_on_devices(data: ProblemData, config, devices, comm: str = "nccl", **kw):
+    """``sgs_admm_solve`` sharded over several GPUs from ONE process (SURVEY.md
+    section 5: one host thread per device, NCCL over NVLink between them), so a
+    multi-GPU solve is still a plain call -- no torchrun.
+
+    ``data`` is the global problem; rank r gets the r-th contiguous block of
+    samples and drives ``devices[r]``.  ``comm="host"`` exchanges through a
+    host all-reduce instead (``ThreadRanks``; lets several ranks share one GPU
+    in tests, their kernels never waiting on one another).  Returns rank 0's
+    SolveResult with the sample-space iterates (r, xi, alpha) of all ranks
+    concatenated; feature-space state is replicated and bit-identical."""
+    from .solver import as_problem, sgs_admm_solve
+
+    data = as_problem(data)
+    devices = [int(x) for x in devices]
+    world = len(devices)
+    if world < 1:
+        raise ValueError("need at least one device")
+    if kw.get("callback") is not None:
+        raise NotImplementedError("per-iteration callbacks need the global iterate; use devices=None")
+    if comm not in ("nccl", "host"):
+        raise ValueError("comm must be 'nccl' or 'host'")
+    n = data.n
+    locals_ = [shard_problem(data, r, world) for r in range(world)]
+    for r in range(world):  # uploads in rank order (host memory bandwidth is shared anyway)
+        device_problem(locals_[r], devices[r])
+    ranks = ThreadRanks(world)
+    if comm == "nccl":
+        lib = _lib.load()
+        buf = (C.c_uint8 * 128)()
+        _check(lib.gdwd_comm_unique_id(buf), None, "nccl unique id")
+        uid = bytes(buf)
+    outs: list = [None] * world
+    errs: list = []
+
+    def run(r: int) -> None:
+        try:
+            if comm == "nccl":
+                cm = NcclCommunicator(world, r, lambda _id: uid)
+            else:
+                cm = HostCommunicator(ranks.allreduce_for(r), world, r)
+            attach(locals_[r], cm, n, devices[r])
+            outs[r] = sgs_admm_solve(locals_[r], config, device=devices[r], **kw)
+        except BaseException as exc:
+            errs.append(exc)
+            ranks.barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,), name=f"gdwd-rank{r}") for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    real = [e for e in errs if not isinstance(e, threading.BrokenBarrierError)]
+    if errs:
+        raise (real or errs)[0]
+    out = outs[0]
+    st = out.final_state
+    for key in ("r", "xi", "alpha"):
+        setattr(st, key, np.concatenate([getattr(o.final_state, key) for o in outs]))
+    return out
+
+
 class ThreadRanks:
     """Emulate `nranks` ranks as threads of one process (sum all-reduce via a
     barrier) -- the host side of virtual-rank tests on a single GPU."""
@@ -161,4 +226,4 @@ class ThreadRanks:
 
 
 __all__ = ["HostCommunicator", "NcclCommunicator", "ThreadRanks", "attach", "global_train_error",
-           "shard_bounds", "shard_problem"]
+           "shard_bounds", "shard_problem", "solve_on_devices"]

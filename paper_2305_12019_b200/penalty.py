@@ -46,6 +46,9 @@ def compute_penalty_C(x: SparseMatrixCSC, y: np.ndarray, q: float, seed: int = 0
     with ``dist`` the median between-class Euclidean distance (classes
     subsampled to 2000 points each beyond that size; exact zero distances
     excluded) -- solver.py:193-232."""
+    from .sparse import as_csc
+
+    x = as_csc(x)
     y = np.asarray(y, dtype=np.float64)
     n = y.size
     pos = np.flatnonzero(y > 0)

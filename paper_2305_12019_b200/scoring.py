@@ -26,7 +26,7 @@ import numpy as np
 from . import _lib
 from .model import ModelFile
 from .solver import DeviceProblem, _check
-from .sparse import SparseMatrixCSC
+from .sparse import SparseMatrixCSC, as_csc
 
 
 class DeviceMatrix(DeviceProblem):
@@ -64,6 +64,7 @@ class DeviceMatrix(DeviceProblem):
 
 def device_matrix(x: SparseMatrixCSC, device: Optional[int] = None) -> DeviceMatrix:
     """The (cached) device copy of a raw sample matrix."""
+    x = as_csc(x)
     want = 0 if device is None else int(device)
     dev = getattr(x, "_device", None)
     if dev is None or dev.ctx is None or dev.device != want:

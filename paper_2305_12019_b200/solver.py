@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _lib
 from .model import FeatureMeta, ModelFile, identity_meta
-from .sparse import SparseMatrixCSC
+from .sparse import SparseMatrixCSC, as_csc
 
 
 # ---------------------------------------------------------------------------
@@ -398,6 +398,7 @@ def kkt_residuals(state: SolverState, data: ProblemData, mu: float = 1.0) -> KKT
     """Normalized optimality residuals of an iterate (solver.py:311-340), on
     the device: one Z~^T w pass with the sample sums, one Z~ alpha pass, one
     d-space map; AssertionError if r left the positive orthant."""
+    data = as_problem(data)
     dp = device_problem(data)
     n, d = data.n, data.d
     vec = {k: _lib.f64(getattr(state, k)) for k in ("r", "xi", "alpha", "w", "u")}
@@ -426,6 +427,30 @@ def dual_objective(data: ProblemData, alpha: np.ndarray) -> float:
     return kkt_residuals(st, data).obj_dual
 
 
+def as_problem(data) -> ProblemData:
+    """The package's ProblemData for ``data``: itself, a device-generated
+    problem (``z_tilde`` is None), or -- drop-in use -- the reference's own
+    ``gdwd.ProblemData`` holding a reference ``SparseMatrixCSC`` (solver.py:60-95,
+    linalg/sparse.py:20-50), converted once and cached on the object (a fully
+    stored CSC becomes the zero-copy dense sample layout)."""
+    if isinstance(data, ProblemData) or getattr(data, "z_tilde", 0) is None:
+        return data
+    cached = getattr(data, "_gdwd_problem", None)
+    if cached is not None:
+        return cached
+    try:
+        z = data.z_tilde
+        fields = (data.y, data.e, data.weights, data.C, data.q, data.z_scale)
+    except AttributeError as exc:
+        raise TypeError(f"expected a ProblemData, got {type(data).__name__}") from exc
+    out = ProblemData(as_csc(z), *fields)
+    try:
+        object.__setattr__(data, "_gdwd_problem", out)
+    except (AttributeError, TypeError):
+        pass
+    return out
+
+
 def _eps_c(data: ProblemData, config: SolverConfig) -> float:
     """solver.py:441-445.  NaN asks the library for the default
     1/max(1, ||Z~||_F), with the norm reduced on the device at upload."""
@@ -441,7 +466,8 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
                    callback: Optional[Callable[[SolverState, KKTResiduals], None]] = None, *,
                    sigma_schedule: Optional[np.ndarray] = None, device: Optional[int] = None,
                    use_graph: bool = True, poll_every: int = 16, smw_gram_space: bool = True,
-                   persistent: bool = True, iter_gram: Optional[bool] = None) -> SolveResult:
+                   persistent: bool = True, iter_gram: Optional[bool] = None,
+                   devices: Optional[list] = None) -> SolveResult:
     """Run the solver to the KKT stopping rule or the iteration cap
     (solver.py:392-602).  ``callback(state, residuals)`` runs after every
     iteration (it forces a device sync and a copy of the iterates).
@@ -452,8 +478,19 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
     in sample-coefficient space with the n x n Gram instead of passes over X),
     ``persistent`` (Gram-space SMW2: all iterations in one cooperative kernel),
     ``iter_gram`` (ITERATIVE on dense data: PSQMR's operator from the d x d
-    Gram formed once on the FP64 tensor cores; None = automatic for d <= n/4)."""
+    Gram formed once on the FP64 tensor cores; None = automatic for d <= n/4),
+    ``devices`` (a list of GPUs: the samples are sharded over them from this
+    one process, parallel.solve_on_devices)."""
+    if devices is not None and len(devices) > 1:
+        from .parallel import solve_on_devices
+
+        return solve_on_devices(data, config, devices, meta=meta, callback=callback, sigma_schedule=sigma_schedule,
+                                use_graph=use_graph, poll_every=poll_every, smw_gram_space=smw_gram_space,
+                                persistent=persistent, iter_gram=iter_gram)
+    if devices is not None and len(devices) == 1:
+        device = int(devices[0])
     t_start = time.perf_counter()
+    data = as_problem(data)
     dp = device_problem(data, device)
     t_up = time.perf_counter()
     lib = dp.lib
@@ -503,8 +540,13 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
     sigma_last = float(hist[-1, 11]) if len(hist) else float(out.sigma)
     state = SolverState(st["r"], st["xi"], st["alpha"], st["w"], st["u"], st["rho"], st["beta"], sigma_last,
                         int(out.iterations), float(out.eps_c))
+    # train error over ALL samples (solver.py:557-559): a sharded rank counts
+    # its own misclassified samples and the counts are summed over the shards
     scores = st["beta"] + data.y * st["ztw"]
-    train_err = 100.0 * float(np.mean(data.y * np.sign(scores) <= 0.0))
+    bad = np.array([float(np.sum(data.y * np.sign(scores) <= 0.0))])
+    if dp.n_global:
+        _check(lib.gdwd_allreduce_host(dp.ctx, _lib.ptr(bad), 1), dp.ctx, "train error all-reduce")
+    train_err = 100.0 * (float(bad[0]) / float(dp.n_global or data.n))
     if meta is None:
         meta = identity_meta(data.d)
     converged = bool(out.converged)
@@ -575,5 +617,5 @@ def matvec(m: SparseMatrixCSC, x: np.ndarray, transpose: bool = False, device: i
 
 __all__ = ["Backend", "DegenerateSchurError", "DeviceProblem", "IndefiniteMatrixError", "KKTResiduals",
            "KKT_FIELDS", "LanczosConvergenceError", "ProblemData", "SingleClassError", "SolveResult",
-           "SolverConfig", "SolverKind", "SolverState", "compute_weights", "device_problem", "matvec",
+           "SolverConfig", "SolverKind", "SolverState", "as_problem", "compute_weights", "device_problem", "matvec",
            "newton_r", "newton_r_sweep", "scale_problem", "select_solver", "sgs_admm_solve", "update_sigma"]

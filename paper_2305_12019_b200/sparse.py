@@ -135,6 +135,22 @@ class SparseMatrixCSC:
         return SparseMatrixCSC(self.nrows, self.ncols, self.colptr.copy(), self.rowidx.copy(), values)
 
 
+def as_csc(x) -> SparseMatrixCSC:
+    """``x`` itself, or -- drop-in use -- a reference ``SparseMatrixCSC``
+    (reference linalg/sparse.py:20-50: nrows, ncols, colptr, rowidx, values)
+    converted once and cached on that object."""
+    if isinstance(x, SparseMatrixCSC):
+        return x
+    conv = getattr(x, "_gdwd_csc", None)
+    if conv is None:
+        conv = SparseMatrixCSC(x.nrows, x.ncols, x.colptr, x.rowidx, x.values)
+        try:
+            object.__setattr__(x, "_gdwd_csc", conv)
+        except (AttributeError, TypeError):
+            pass
+    return conv
+
+
 def csc_from_scipy(m) -> SparseMatrixCSC:
     """reference ``sparse.py:82-94``: duplicates summed, zeros pruned, sorted."""
     import scipy.sparse as sp
@@ -186,5 +202,5 @@ def csr_of(z: SparseMatrixCSC):
             m.indices.astype(np.int32), m.data.astype(np.float64))
 
 
-__all__ = ["SparseFormatError", "SparseMatrixCSC", "csc_from_dense", "csc_from_scipy",
+__all__ = ["SparseFormatError", "SparseMatrixCSC", "as_csc", "csc_from_dense", "csc_from_scipy",
            "csc_from_triplets", "csr_of"]

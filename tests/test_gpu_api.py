@@ -126,3 +126,72 @@ def test_csc_upload_validation_reports_first_error_in_sample_order():
         assert b"nondecreasing" in lib.gdwd_last_error(ctx)
     finally:
         lib.gdwd_ctx_destroy(ctx)
+
+
+def test_frobenius_after_pinned_upload_then_scale():
+    """A pinned dense upload defers its ||X||_F^2 read-back; a later
+    scale_dense must not be overwritten by that stale value."""
+    import ctypes as C
+    import math
+
+    import torch
+
+    from paper_2305_12019_b200 import _lib
+    from paper_2305_12019_b200.solver import DeviceProblem, _check
+
+    rng = np.random.default_rng(5)
+    n, d = 300, 1600  # pinned + n <= d: the chunked overlapped upload path
+    X = rng.standard_normal((n, d))
+    pin = torch.empty(n * d, dtype=torch.float64, pin_memory=True).numpy()
+    pin[:] = X.reshape(-1)
+    dp = DeviceProblem(None, 0)
+    lib = dp.lib
+    _check(lib.gdwd_upload_dense(dp.ctx, _lib.ptr(pin), d, n), dp.ctx, "upload")
+    y = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    zs = 7.5
+    _check(lib.gdwd_scale_dense(dp.ctx, _lib.ptr(y), zs), dp.ctx, "scale")
+    f2 = C.c_double()
+    _check(lib.gdwd_frobenius_sq(dp.ctx, C.byref(f2)), dp.ctx, "fro")
+    want = float(np.sum((X / zs) ** 2))
+    assert math.isclose(f2.value, want, rel_tol=1e-12), (f2.value, want, float(np.sum(X * X)))
+    dp.close()
+
+
+def test_reference_problem_data_is_accepted_as_is():
+    """Drop-in: a ProblemData shaped like the reference's (its own dataclass
+    holding a CSC with int64 colptr/rowidx, solver.py:60-71, sparse.py:20-50)
+    solves without conversion by the caller, dense and sparse."""
+    from dataclasses import dataclass
+
+    @dataclass(frozen=True)
+    class RefCSC:
+        nrows: int
+        ncols: int
+        colptr: np.ndarray
+        rowidx: np.ndarray
+        values: np.ndarray
+
+    @dataclass(frozen=True)
+    class RefProblem:
+        z_tilde: RefCSC
+        y: np.ndarray
+        e: np.ndarray
+        weights: np.ndarray
+        C: float
+        q: float
+        z_scale: float
+
+    for name in ("tiny_direct", "tiny_sparse"):
+        prob = problem_for(load_traj(name))
+        z = prob.z_tilde
+        rz = RefCSC(z.nrows, z.ncols, np.array(z.colptr), np.array(z.rowidx), np.array(z.values))
+        rp = RefProblem(rz, prob.y, prob.e, prob.weights, prob.C, prob.q, prob.z_scale)
+        cfg = G.SolverConfig(q=prob.q, max_iter=15)
+        a = G.sgs_admm_solve(prob, cfg)
+        b = G.sgs_admm_solve(rp, cfg)
+        assert G.as_problem(rp) is G.as_problem(rp)  # converted once, cached
+        assert a.iterations == b.iterations and a.double_count == b.double_count
+        assert np.array_equal(a.final_state.w, b.final_state.w)
+        assert a.train_error_pct == b.train_error_pct
+        kk = G.kkt_residuals(b.final_state, rp)
+        assert np.isfinite(kk.eta_p)

@@ -31,7 +31,9 @@ def test_generator_statistics_and_sharding():
     assert np.allclose(Xp, X, rtol=1e-14, atol=1e-14)
 
 
-@pytest.mark.parametrize("d,n", [(2000, 9000), (6000, 12000)])
+# (6000, 30000): d > 5000 and d <= n/4 -- ITERATIVE with the Gram operator and
+# q = 4, the path config 5 itself takes (iter_gram automatic)
+@pytest.mark.parametrize("d,n", [(2000, 9000), (6000, 12000), (6000, 30000)])
 def test_c5_proxy_first20(d, n):
     cfg = synth.CONFIGS["c5"].scaled(d=d, n=n)
     dev = synth.make_device_problem(cfg, seed=0)

@@ -259,19 +259,17 @@ def test_iter_gram_operator_matches_reference(case):
     assert relerr(out2.final_state.w, tr["final_w"]) < 1e-6
 
 
-@pytest.mark.parametrize("version", ["3", "3-l2", "3-k", "2"])
+@pytest.mark.parametrize("version", ["3", "3-l2", "3-k"])
 @pytest.mark.parametrize("case", TRAJ_CASES + VAR_CASES)
 def test_persistent_iterates_match_reference(case, version, monkeypatch):
     """The persistent Gram-space kernel (SMW2, and DIRECT with 2n <= d) run
     for k = 1, 2, 7, 20 iterations in one launch, no callback: its state after
     iteration k against the reference's iterate k (1e-9 relative), for the
     3-barrier association (default; own rows from tensor memory or L2) and
-    the 4-barrier one.  Cases outside
-    the Gram-space regime run the graph path (same check)."""
+    Cases outside the Gram-space regime run the graph path (same check)."""
     # "3": 3-barrier kernel (rows in tensor memory at these sizes), "3-l2":
     # the same streaming its rows from L2, "3-k": K rows in tensor memory and
-    # GK from L2 (the 1024 < n <= 2048 path), "2": 4-barrier
-    monkeypatch.setenv("GDWD_PK_VERSION", version[0])
+    # GK from L2 (the 1024 < n <= 2048 path)
     if version == "3-l2":
         monkeypatch.setenv("GDWD_PK_TMEM", "0")
     if version == "3-k":

@@ -75,3 +75,54 @@ def test_two_virtual_ranks_match_unsharded(case):
         assert relerr(o.final_state.alpha, ref.final_state.alpha[lo:hi]) < 1e-9
     assert abs(a.final_residuals.obj_primal - ref.final_residuals.obj_primal) <= 1e-9 * abs(
         ref.final_residuals.obj_primal)
+
+
+def _ref_solve(case):
+    name, d, n, backend, iters = case
+    prob = synth.make_problem(synth.CONFIGS[name].scaled(d=d, n=n), 0)
+    cfg = G.SolverConfig(q=prob.q, max_iter=iters, backend=G.Backend(backend))
+    return prob, cfg, G.sgs_admm_solve(prob, cfg)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] + c[3] for c in CASES])
+def test_solve_on_devices_one_process(case):
+    """The single-process multi-device entry point (sgs_admm_solve(...,
+    devices=[...])): two ranks on one GPU through the host exchange, and one
+    NCCL rank; global train error and concatenated sample-space iterates."""
+    prob, cfg, ref = _ref_solve(case)
+    for devices, comm in (([0, 0], "host"), ([0], "nccl")):
+        out = parallel.solve_on_devices(prob, cfg, devices, comm=comm)
+        assert out.iterations == ref.iterations and out.double_count == ref.double_count, comm
+        assert relerr(out.final_state.w, ref.final_state.w) < 1e-9, comm
+        assert relerr(out.final_state.alpha, ref.final_state.alpha) < 1e-9, comm
+        assert out.final_state.alpha.shape == ref.final_state.alpha.shape
+        assert out.train_error_pct == ref.train_error_pct, comm
+
+
+def test_two_processes_gloo_one_gpu(tmp_path):
+    """Two OS processes (gloo over 127.0.0.1), each running the library's
+    sharded path on its half of the samples; the replicated state is
+    bit-identical on both and matches the unsharded solve."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    case = CASES[0]
+    prob, cfg, ref = _ref_solve(case)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    worker = os.path.join(os.path.dirname(__file__), "sharded_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), "2", str(port), str(tmp_path / f"r{r}.npz"),
+                               case[0], str(case[1]), str(case[2]), case[3], str(case[4])])
+             for r in range(2)]
+    for p in procs:
+        assert p.wait(timeout=600) == 0
+    a, b = (np.load(tmp_path / f"r{r}.npz") for r in range(2))
+    assert np.array_equal(a["w"], b["w"]) and float(a["beta"]) == float(b["beta"])
+    assert int(a["iterations"]) == ref.iterations and int(a["double_count"]) == ref.double_count
+    assert relerr(a["w"], ref.final_state.w) < 1e-9
+    assert relerr(np.concatenate([a["alpha"], b["alpha"]]), ref.final_state.alpha) < 1e-9
+    assert float(a["train_error"]) == float(b["train_error"]) == ref.train_error_pct
+    assert abs(float(a["obj_primal"]) - ref.final_residuals.obj_primal) <= 1e-9 * abs(ref.final_residuals.obj_primal)
