@@ -38,7 +38,9 @@ def test_b200_arm_line():
     assert BASE_KEYS <= set(j) and "impl" not in j
     assert j["steps"] == 20 and j["warmup"] == 3 and j["value"] > 0 and j["dtype"] == "f64"
     r = j["roofline"]
-    assert r["bound"] in ("hbm", "tensor") and r["unit"] in ("GB/s", "TFLOP/s") and r["peak"] > 0
+    # "l2": the Gram-space persistent kernel keeps its matrices on chip and is
+    # reported against the probe-measured L2 read rate (profiles/r02/peaks_probe.json)
+    assert r["bound"] in ("hbm", "tensor", "l2") and r["unit"] in ("GB/s", "TFLOP/s") and r["peak"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
     e = j["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
