@@ -183,6 +183,8 @@ def kernel_bytes(tag: str, n: int, d: int, nnz: int | None = None) -> float | No
     if nnz is not None and tag.startswith("ztmv_"):
         nb = -(-d // 8192)
         return 10.0 * nnz + 4.0 * n * nb + 8.0 * (d + 6 * n)
+    if tag.startswith("zft_"):
+        return x + 8.0 * (3 * d + 10 * n)  # X once, w in, 6 sample vectors in / 4 out, 2 d-products out
     if tag.startswith("zmv_"):
         return x + 8.0 * (5 * n + 2 * d)   # up to 2 RHS in (+ inputs), 2 d-vectors out
     if tag.startswith("ztmv_"):

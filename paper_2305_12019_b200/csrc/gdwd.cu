@@ -32,6 +32,7 @@
 #include "persist.cuh"
 #include "persist3.cuh"
 #include "synth.cuh"
+#include "zft.cuh"
 #include "zops.cuh"
 
 using namespace gdwd;
@@ -255,6 +256,11 @@ struct gdwd_ctx {
   int kind = 0, poll = 16, max_iter = 0, max_steps = 50, k_host = 0, psqmr_total = 0;
   bool use_sgs = true, stopped = false, gram = false, persistent = false;
   bool iter_gram = false;  // ITERATIVE with the d x d Gram operator (gdmat)
+  bool ft = false;         // X-space loop with the fused tail pass (zft.cuh)
+  bool ps_graph = false;   // ITERATIVE body captured with device-resident PSQMR (WHILE nodes)
+  cudaStream_t cap_st = nullptr;  // capture-to-graph stream for conditional bodies
+  int64_t ps_step_nodes = 0;      // kernels per device-resident PSQMR step (launch accounting)
+  bool hist_ps_dev = false;       // the last solve's history holds device-recorded PSQMR steps
   DevBuf gdmat;
   int64_t ldg = 0;
   int fac_iter_gram = 0;
@@ -336,6 +342,11 @@ struct Launch {  // counts launches; with profiling on, brackets the launch with
     }
   }
   ~Launch() {
+    static const bool dbg = getenv("GDWD_DEBUG_LAUNCH") != nullptr;
+    if (dbg) {
+      const cudaError_t e = cudaPeekAtLastError();
+      if (e != cudaSuccess) fprintf(stderr, "gdwd launch %s: %s\n", tag, cudaGetErrorString(e));
+    }
     if (c->prof) {
       cudaEvent_t b = c->take_event();
       cudaEventRecord(b, c->st);
@@ -450,6 +461,143 @@ static void run_vm(gdwd_ctx* ctx, const Op& op, int64_t len, const char* tag = "
   }
 }
 
+// Fused dot -> epilogue -> axpy pass (zft.cuh) geometry: the smallest
+// cluster whose feature slices fit the column threads' registers (<= 12
+// columns per thread), rows per stage and stages from the shared-memory
+// budget.  cs = 0: not eligible (d > 8 x 12 x 512).
+struct FtPlan {
+  int cs = 0, dw = 0, tr = 0, ns = 0, cpt = 0;
+};
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+static FtPlan ft_plan(int64_t d) {
+  FtPlan p;
+  for (int cs = std::max(1, env_int("GDWD_FT_CS", 1)); cs <= FT_CSMAX; cs *= 2) {  // (env: tuning experiments)
+    const int64_t dw = ((d + cs - 1) / cs + 1) / 2 * 2;
+    const int64_t c = (dw + FT_CW - 1) / FT_CW;
+    if (c <= 12) {
+      p.cs = cs;
+      p.dw = (int)dw;
+      p.cpt = c <= 2 ? 2 : (c <= 4 ? 4 : (c <= 8 ? 8 : 12));
+      break;
+    }
+  }
+  if (!p.cs) return p;
+  const int64_t rb = (int64_t)p.dw * 8;
+  p.tr = (int)std::max<int64_t>(1, std::min<int64_t>(ft_trm(p.cpt), 98304 / rb));
+  p.ns = (int)std::max<int64_t>(2, std::min<int64_t>(4, 196608 / (p.tr * rb)));
+  if (env_int("GDWD_FT_TR", 0) > 0) p.tr = std::min(env_int("GDWD_FT_TR", 0), ft_trm(p.cpt));
+  if (env_int("GDWD_FT_NS", 0) > 1) p.ns = std::min(env_int("GDWD_FT_NS", 0), 8);
+  // stages + the slice of w <= 210 KB
+  while ((p.ns * p.tr + 1) * rb > 210 * 1024 && p.tr > 1) --p.tr;
+  if ((p.ns * p.tr + 1) * rb > 210 * 1024) p.cs = 0;
+  return p;
+}
+static bool ft_enabled() {
+  const char* e = getenv("GDWD_FT");
+  return !(e && atoi(e) == 0);
+}
+
+// (the occupancy query and attribute set run the first time a geometry is
+// seen on a device; solve_begin calls run_ft with prepare_only before any
+// graph capture, where they are not allowed)
+template <class Op, int CPT>
+static void launch_ft(gdwd_ctx* ctx, const Op& op, MatView X, const FtPlan& p, FtGeom& g, const Scratch& sc,
+                      bool prepare_only) {
+  auto kfn = zft_kernel<Op, CPT>;
+  g = FtGeom{p.cs, 0, p.dw, p.tr, p.ns, (X.cols + 1) / 2 * 2};
+  const size_t sm = ft_smem_bytes(g, Op::R);
+  static std::map<std::pair<int, size_t>, int> cache;  // (device x cs, smem) -> co-resident clusters
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)p.cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(FT_THREADS);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = ctx->st;
+  cfg.attrs = at;
+  cfg.numAttrs = p.cs > 1 ? 1 : 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    // the attribute is per function and device: only ever raise it (a smaller
+    // geometry seen later must not shrink it under a cached larger one)
+    static size_t attr_max[64] = {};
+    if (prepare_only && sm > attr_max[dev & 63]) {
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr_max[dev & 63] = sm;
+    }
+    auto key = std::make_pair(dev * 16 + p.cs, sm);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+      int nc = 0;
+      if (p.cs > 1) {
+        cfg.gridDim = dim3(p.cs * (NUM_SMS / p.cs));
+        if (cudaOccupancyMaxActiveClusters(&nc, kfn, &cfg) != cudaSuccess) nc = 0;
+      } else {
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, FT_THREADS, sm) != cudaSuccess) nb = 0;
+        nc = nb * NUM_SMS;
+      }
+      cudaGetLastError();
+      it = cache.emplace(key, std::max(nc, 1)).first;
+    }
+    g.clusters = it->second;
+  }
+  if (prepare_only) return;
+  cfg.gridDim = dim3(g.clusters * p.cs);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, op, X, g, sc);
+  if (e != cudaSuccess && getenv("GDWD_DEBUG_LAUNCH"))
+    fprintf(stderr, "zft launch: %s (grid %d x %d, smem %zu)\n", cudaGetErrorString(e), g.clusters, p.cs, sm);
+}
+
+// One fused pass; the per-cluster partials are summed (cluster order) by the
+// reduce kernel, which runs the per-feature epilogue and fin -- or, sharded,
+// publishes the local products and n-sums for the all-reduce.
+template <class Op>
+static void run_ft(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "zft", bool prepare_only = false) {
+  const bool sh = sharded(ctx);
+  const Scratch sc = sh ? scr_bundle(ctx) : ctx->scr;
+  const FtPlan p = ft_plan(X.cols);
+  FtGeom g{};
+  if (prepare_only) {
+    switch (p.cpt) {
+      case 2: launch_ft<Op, 2>(ctx, op, X, p, g, sc, true); break;
+      case 4: launch_ft<Op, 4>(ctx, op, X, p, g, sc, true); break;
+      case 8: launch_ft<Op, 8>(ctx, op, X, p, g, sc, true); break;
+      default: launch_ft<Op, 12>(ctx, op, X, p, g, sc, true); break;
+    }
+    if (getenv("GDWD_FT_DEBUG"))
+      fprintf(stderr, "zft plan: d=%lld cs=%d dw=%d cpt=%d tr=%d ns=%d clusters=%d smem=%zu\n", (long long)X.cols,
+              p.cs, p.dw, p.cpt, p.tr, p.ns, g.clusters, ft_smem_bytes(g, Op::R));
+    return;
+  }
+  {
+    Launch L(ctx, tag);
+    switch (p.cpt) {
+      case 2: launch_ft<Op, 2>(ctx, op, X, p, g, sc, false); break;
+      case 4: launch_ft<Op, 4>(ctx, op, X, p, g, sc, false); break;
+      case 8: launch_ft<Op, 8>(ctx, op, X, p, g, sc, false); break;
+      default: launch_ft<Op, 12>(ctx, op, X, p, g, sc, false); break;
+    }
+  }
+  {
+    Launch L(ctx, "zft_reduce");
+    zft_reduce_kernel<Op><<<(unsigned)((X.cols + 31) / 32), FTR_THREADS, 0, ctx->st>>>(op, X.cols, g.clusters, g.ldp, sc);
+  }
+  if (sh) {
+    allreduce(ctx, ctx->bundle.p, (int64_t)Op::R * ctx->d + Op::NN);
+    Launch L(ctx, "zmv_epilogue");
+    zmv_epi_kernel<Op><<<vm_grid(ctx->d), VM_THREADS, 0, ctx->st>>>(op, ctx->bundle.p, ctx->d, ctx->scr);
+  }
+}
+
 static void prof_flush(gdwd_ctx* ctx) {
   if (ctx->prof_pending.empty()) return;
   cudaStreamSynchronize(ctx->st);
@@ -470,6 +618,7 @@ static int ensure_scratch(gdwd_ctx* ctx, int64_t rows, int64_t cols) {
   ZmvGeom zg = zmv_geom(rows, cols, maxslots);
   ZtGeom tg = zt_geom(rows, (cols + 1) / 2 * 2, maxslots);
   size_t part = std::max<size_t>((size_t)zg.segs * 2 * zg.ldp, tg.chunks > 1 ? (size_t)tg.chunks * rows : 0);
+  part = std::max<size_t>(part, (size_t)NUM_SMS * 2 * zg.ldp);  // fused tail: <= 148 clusters x 2 products
   size_t npart = (size_t)maxslots * 16;
   size_t tpart = (size_t)std::max<int64_t>(zg.tiles, NUM_SMS * 8) * 16 + 16;
   size_t nt = (size_t)std::max<int64_t>(zg.tiles, maxslots) + 4;
@@ -802,6 +951,7 @@ int gdwd_ctx_create(int32_t device, gdwd_ctx** out) {
   ctx->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap_st, cudaStreamNonBlocking);
   if (e == cudaSuccess) {
     keep_pool_reserved(device);
     for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
@@ -824,6 +974,7 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
+  if (ctx->cap_st) cudaStreamDestroy(ctx->cap_st);
   if (ctx->cst) {
     cudaStreamSynchronize(ctx->cst);
     cudaStreamSynchronize(ctx->gst);
@@ -1664,11 +1815,98 @@ static int psqmr_solve(gdwd_ctx* ctx, const double* b, const double* x0, double*
   return GDWD_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident PSQMR: the step loop is a CUDA-graph WHILE node whose
+// condition a one-thread kernel sets from the device scalars (active and not
+// stopped) -- no host synchronisation inside a solve.  Same kernels, same
+// order, same recurrence as psqmr_solve (psqmr.py:65-93).
+// ---------------------------------------------------------------------------
+__global__ void ps_cond_kernel(const Scal* S, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, (!S->stopped && S->ps_active) ? 1u : 0u);
+}
+
+// Append WHILE(h) { body() } to the capture on ctx->st; body() enqueues on
+// ctx->st, which is pointed at a capture-to-graph stream meanwhile.
+template <class F>
+static int capture_while(gdwd_ctx* ctx, cudaGraphConditionalHandle h, F&& body) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(ctx->st, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, deps, nd, &cp));
+  cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+  CK(cudaStreamUpdateCaptureDependencies(ctx->st, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaStream_t outer = ctx->st;
+  ctx->st = ctx->cap_st;
+  const int64_t before = ctx->launches;
+  cudaError_t e = cudaStreamBeginCaptureToGraph(ctx->cap_st, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    body();
+    cudaGraph_t tmp = nullptr;
+    e = cudaStreamEndCapture(ctx->cap_st, &tmp);
+  }
+  ctx->ps_step_nodes = ctx->launches - before + 1;  // + the condition kernel
+  ctx->launches = before;
+  ctx->st = outer;
+  CK(e);
+  return GDWD_OK;
+}
+
+static int psqmr_dev(gdwd_ctx* ctx, const double* b, const double* x0, double* out, int pred, double tolmul,
+                     int which) {
+  const Dev& D = ctx->D;
+  MatView Z = zview(ctx);
+  const MatView Gd{ctx->gdmat.p, ctx->d, ctx->d, ctx->ldg};
+  if (ctx->iter_gram) {
+    run_zt(ctx, OpInitResidualGram{D, x0, b, pred}, Gd, "gemv_gram_psqmr_init");
+  } else {
+    run_zt(ctx, OpApplyZt{D, x0, pred, 0}, Z, "ztmv_psqmr_init");
+    run_zmv(ctx, OpInitResidual{D, x0, b, pred}, Z, "zmv_psqmr_init");
+  }
+  run_vm(ctx, OpPsInit{D, x0, out, pred, tolmul}, D.m, "vmap_psqmr_init");
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamGetCaptureInfo(ctx->st, &cs, nullptr, &g, nullptr, nullptr));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+  ps_cond_kernel<<<1, 1, 0, ctx->st>>>(ctx->S, h);
+  ctx->launches++;
+  const int max_steps = ctx->max_steps;
+  RC(capture_while(ctx, h, [&]() {
+    if (ctx->iter_gram) {
+      run_zt(ctx, OpPsApplyGram{D}, Gd, "gemv_gram_psqmr_apply");
+    } else {
+      run_zt(ctx, OpApplyZt{D, D.pq, 0, 1}, Z, "ztmv_psqmr_apply");
+      run_zmv(ctx, OpPsApply{D}, Z, "zmv_psqmr_apply");
+    }
+    run_vm(ctx, OpPsV1{D}, D.m, "vmap_psqmr_v1");
+    run_vm(ctx, OpPsV2{D, out, tolmul, max_steps}, D.m, "vmap_psqmr_v2");
+    ps_cond_kernel<<<1, 1, 0, ctx->st>>>(ctx->S, h);
+  }));
+  run_vm(ctx, OpPsEnd{D, pred, which}, 1, "vmap_psqmr_end");
+  return GDWD_OK;
+}
+
 // the tail shared by every backend: w/ztw commit, Steps 2-3, KKT sample terms
 static void enqueue_tail(gdwd_ctx* ctx) {
   const Dev& D = ctx->D;
   MatView Z = zview(ctx);
   run_vm(ctx, OpCopyIfReuse{D, D.xb, D.x}, D.m, "vmap_copy_x");
+  if (ctx->ft) {
+    // Step 2 (d-space), then Z~^T w, Step 3 and Z~ [xi - r, alpha] in one pass
+    run_vm(ctx, OpStep2a{D}, D.d, "vmap_step2a");
+    run_vm(ctx, OpStep2b{D}, D.d, "vmap_step2b");
+    run_ft(ctx, OpTail{D}, Z, "zft_tail");
+    run_vm(ctx, OpKktTail{D}, D.n, "vmap_kkt_tail", true);
+    return;
+  }
   run_zt(ctx, OpZtStore{D, D.x, D.ztw, 1}, Z, "ztmv_ztw_2");
   run_vm(ctx, OpCopyIfReuse{D, D.ztwb, D.ztw}, D.n, "vmap_copy_ztw");
   run_vm(ctx, OpStep2a{D}, D.d, "vmap_step2a");
@@ -1676,10 +1914,18 @@ static void enqueue_tail(gdwd_ctx* ctx) {
   run_vm(ctx, OpStep3{D}, D.n, "vmap_step3_kkt", true);
 }
 
+// h of this iteration and the completion of the previous one (dual
+// objective, gap, stopping test): one X pass, or a d-space map after a fused tail
+static void enqueue_rhs(gdwd_ctx* ctx) {
+  const Dev& D = ctx->D;
+  if (ctx->ft) run_vm(ctx, OpRhsParts{D}, D.d, "vmap_rhs_parts");
+  else run_zmv(ctx, OpRhsAlpha{D}, zview(ctx), "zmv_rhs_alpha");
+}
+
 static void enqueue_body_fixed(gdwd_ctx* ctx, int kind, bool use_sgs) {
   const Dev& D = ctx->D;
   MatView Z = zview(ctx);
-  run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
+  enqueue_rhs(ctx);
   enqueue_solve(ctx, kind, D.h, D.xb, 0);
   run_zt(ctx, OpZtNewton{D}, Z, "ztmv_newton");
   if (use_sgs) run_zmv(ctx, OpDrZtwb{D}, Z, "zmv_dr_ztwb");
@@ -1962,7 +2208,7 @@ static void prox_solve(gdwd_ctx* ctx, const double* hv, double* out, int pred, b
 static int body_iterative(gdwd_ctx* ctx, bool use_sgs, int max_steps, int* psqmr_steps) {
   Dev& D = ctx->D;
   MatView Z = zview(ctx);
-  run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
+  enqueue_rhs(ctx);
   int steps = 0, conv = 1, ran = 0;
   *psqmr_steps = 0;
   bool sa_ready = false;  // shift anchor of this iteration computed
@@ -2008,6 +2254,63 @@ static int body_iterative(gdwd_ctx* ctx, bool use_sgs, int max_steps, int* psqmr
   return GDWD_OK;
 }
 
+// ITERATIVE body with both PSQMR solves device-resident (captured once per
+// solve; the proximal switch is handled by the host, prox_resume)
+static int body_iterative_dev(gdwd_ctx* ctx, bool use_sgs) {
+  const Dev& D = ctx->D;
+  MatView Z = zview(ctx);
+  enqueue_rhs(ctx);
+  RC(psqmr_dev(ctx, D.h, D.x, D.xb, 0, 1.0, 1));
+  run_zt(ctx, OpZtNewton{D}, Z, "ztmv_newton");
+  if (use_sgs) run_zmv(ctx, OpDrZtwb{D}, Z, "zmv_dr_ztwb");
+  else run_vm(ctx, OpSetReuse{D}, 1, "vmap_set_reuse");
+  run_vm(ctx, OpCopy{D, D.x, px_wold(ctx)}, D.m, "vmap_copy_x");
+  RC(psqmr_dev(ctx, D.h2, D.xb, D.x, 1, 5.0, 2));
+  enqueue_tail(ctx);
+  return GDWD_OK;
+}
+
+// A device-resident PSQMR solve of iteration k did not converge (OpPsEnd:
+// error 7, need_prox = which solve): build the proximal backend and finish
+// iteration k on the host path exactly as body_iterative does after its
+// switch (solver.py:479-491).  Returns 1 when it resumed, 0 when the stop
+// had another cause.
+static int prox_resume(gdwd_ctx* ctx, bool use_sgs, int* resumed) {
+  *resumed = 0;
+  CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  Scal& s = *ctx->Sh;
+  if (s.error != 7) return GDWD_OK;
+  const int k = s.k, which = s.need_prox;
+  s.error = 0;
+  s.need_prox = 0;
+  s.stopped = 0;
+  CK(cudaMemcpyAsync(ctx->S, ctx->Sh, sizeof(Scal), cudaMemcpyHostToDevice, ctx->st));
+  const Dev& D = ctx->D;
+  MatView Z = zview(ctx);
+  RC(build_prox(ctx));
+  if (which == 1) {
+    prox_solve(ctx, D.h, D.xb, 0, true, D.x, D.ztw);
+    run_zt(ctx, OpZtNewton{D}, Z, "ztmv_newton");
+    if (use_sgs) {
+      run_zmv(ctx, OpPxH2{D}, Z, "zmv_prox_h2");
+      run_vm(ctx, OpPxDot{D, D.xb, 0}, ctx->d, "vmap_prox");
+      run_vm(ctx, OpPxResid{D}, ctx->d, "vmap_prox_resid");
+    } else {
+      run_vm(ctx, OpSetReuse{D}, 1, "vmap_set_reuse");
+    }
+    prox_solve(ctx, D.h2, D.x, 1, false, D.x, D.ztw);
+  } else {
+    prox_solve(ctx, D.h2, D.x, 1, true, px_wold(ctx), D.ztw);
+  }
+  enqueue_tail(ctx);
+  CK(cudaGetLastError());
+  ctx->k_host = k + 1;
+  ctx->stopped = false;
+  *resumed = 1;
+  return GDWD_OK;
+}
+
 static void end_session(gdwd_ctx* ctx) {
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   ctx->gexec = nullptr;
@@ -2037,7 +2340,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   const int max_iter = cfg->max_iter;
 
   // ---- buffers ------------------------------------------------------------
-  const int NV = 12, MV = 16;
+  const int NV = 12, MV = 18;
   // Gram space pays off (and keeps w exactly representable) only when n <= d,
   // SMW2's own regime; an explicitly requested SMW2 with d < n iterates over X.
   // DIRECT with few samples (2n <= d, unsharded, n within the persistent
@@ -2079,6 +2382,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   D.pr = mv + 6 * ms; D.pres = mv + 7 * ms; D.pq = mv + 8 * ms; D.pu = mv + 9 * ms; D.pd = mv + 10 * ms;
   D.pAd = mv + 11 * ms; D.pAq = mv + 12 * ms;
   D.cres = nv + 10 * nst; D.cdiff = nv + 11 * nst;
+  D.zp0 = mv + 16 * ms; D.zp1 = mv + 17 * ms;  // fused tail products, zero before iteration 1
   D.bot = d;
   D.wd = D.x; D.ud = D.u; D.rhod = D.rho;
   if (gram) {
@@ -2174,6 +2478,10 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   ctx->prox = false;  // every solve starts on PSQMR (solver.py:422)
   ctx->ell = cfg->ell;
   ctx->persistent = gram && cfg->persistent && !ctx->prof && !sharded(ctx);
+  // fused tail over dense X (zft.cuh): iterates start at r = xi = 1, alpha = 0
+  // (solver.py:447-454), so the products it hands to iteration 1 are exactly 0
+  ctx->ft = !gram && ctx->has_dense && ft_enabled() && ft_plan(d).cs > 0;
+  if (ctx->ft) run_ft(ctx, OpTail{D}, Z, "zft_tail", true);
   ctx->use_sgs = cfg->use_sgs != 0;
   ctx->poll = std::max(1, cfg->poll_every);
   ctx->max_iter = max_iter;
@@ -2197,13 +2505,22 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
     if (nb < 1 || n > (int64_t)PK_MAX_OWN * NUM_SMS) ctx->persistent = false;
     else CK(ctx->pk_part.ensure((size_t)2 * NUM_SMS * PK_NPART + 8));  // + barrier counter
   }
-  if (kind != GDWD_BACKEND_ITERATIVE && cfg->use_graph && !ctx->prof && !ctx->persistent && ctx->comm_mode != 2) {
+  // ITERATIVE: the whole body with device-resident PSQMR (graph WHILE nodes),
+  // unsharded (an NCCL all-reduce inside a conditional body is not relied on)
+  ctx->ps_graph = kind == GDWD_BACKEND_ITERATIVE && cfg->use_graph && !ctx->prof && !sharded(ctx) &&
+                  env_int("GDWD_PSQMR_GRAPH", 1) != 0;
+  if ((kind != GDWD_BACKEND_ITERATIVE || ctx->ps_graph) && cfg->use_graph && !ctx->prof && !ctx->persistent &&
+      ctx->comm_mode != 2) {
     cudaGraph_t graph;
     const int64_t before = ctx->launches;
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
-    if (gram) enqueue_body_gram(ctx, ctx->use_sgs);
+    int rc = GDWD_OK;
+    if (kind == GDWD_BACKEND_ITERATIVE) rc = body_iterative_dev(ctx, ctx->use_sgs);
+    else if (gram) enqueue_body_gram(ctx, ctx->use_sgs);
     else enqueue_body_fixed(ctx, kind, ctx->use_sgs);
-    CK(cudaStreamEndCapture(ctx->st, &graph));
+    const cudaError_t ce = cudaStreamEndCapture(ctx->st, &graph);
+    RC(rc);
+    CK(ce);
     ctx->body_nodes = ctx->launches - before;
     ctx->launches = before;
     CK(cudaGraphInstantiate(&ctx->gexec, graph, 0));
@@ -2275,63 +2592,86 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
     ctx->k_host = ctx->Sh->stopped ? ctx->Sh->iters_done : kend;
     ctx->stopped = ctx->Sh->stopped != 0;
   }
-  while (ctx->k_host < kend && !ctx->stopped) {
-    const int k = ctx->k_host;
-    if (ctx->kind == GDWD_BACKEND_ITERATIVE) {
-      int steps = 0;
-      status = body_iterative(ctx, ctx->use_sgs, ctx->max_steps, &steps);
-      if (status) break;
-      ctx->psqmr_total += steps;
-      ctx->ps_per_iter[k] = steps;
-    } else if (ctx->gexec) {
-      CK(cudaGraphLaunch(ctx->gexec, ctx->st));
-      ctx->launches += ctx->body_nodes;
-    } else if (ctx->gram) {
-      enqueue_body_gram(ctx, ctx->use_sgs);
-    } else {
-      enqueue_body_fixed(ctx, ctx->kind, ctx->use_sgs);
+  // the callback of iteration k: complete its KKT record (dual objective,
+  // gap, stop test), materialise w/u/rho, hand the row to the host
+  auto callback = [&](int k, bool* stop) -> int {
+    *stop = false;
+    if (ctx->gram) run_zt(ctx, GsKAlpha{D}, MatView{ctx->kmat.p, ctx->n, ctx->n, ctx->ldm}, "gemv_K_alpha");
+    else enqueue_rhs(ctx);
+    enqueue_materialize(ctx);
+    CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    const Scal& s = *ctx->Sh;
+    if (s.error) {
+      *stop = true;
+      return GDWD_OK;
     }
-    CK(cudaGetLastError());
-    ctx->k_host = k + 1;
-    if (ctx->prof) prof_flush(ctx);
-    if (cb) {
-      // complete the KKT record (dual objective, gap) and the stop test
-      if (ctx->gram) run_zt(ctx, GsKAlpha{D}, MatView{ctx->kmat.p, ctx->n, ctx->n, ctx->ldm}, "gemv_K_alpha");
-      else run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
-      enqueue_materialize(ctx);
-      CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
-      CK(cudaStreamSynchronize(ctx->st));
-      const Scal& s = *ctx->Sh;
-      if (s.error) {
-        ctx->stopped = true;
-        break;
+    if (s.iters_done == k + 1) {
+      double hrow[HIST_W];
+      CK(cudaMemcpy(hrow, D.hist + (int64_t)k * HIST_W, sizeof(hrow), cudaMemcpyDeviceToHost));
+      double res11[11];
+      for (int f = 0; f < 11; ++f)
+        res11[f] = (f < 8) ? hrow[f] : (f == 8 ? hrow[H_GAP] : (f == 9 ? hrow[H_OBJP] : hrow[H_OBJD]));
+      if (cb(user, k + 1, res11, hrow[H_SIGMA], hrow[H_BETA]) != 0)
+        return set_err(ctx, GDWD_ERR_ABORTED, "callback requested abort");
+    }
+    *stop = s.stopped != 0;
+    return GDWD_OK;
+  };
+  for (;;) {
+    while (ctx->k_host < kend && !ctx->stopped) {
+      const int k = ctx->k_host;
+      const bool iter_host = ctx->kind == GDWD_BACKEND_ITERATIVE && (!ctx->ps_graph || !ctx->gexec || ctx->prox);
+      if (iter_host) {
+        int steps = 0;
+        status = body_iterative(ctx, ctx->use_sgs, ctx->max_steps, &steps);
+        if (status) break;
+        ctx->psqmr_total += steps;
+        ctx->ps_per_iter[k] = steps;
+      } else if (ctx->gexec) {
+        CK(cudaGraphLaunch(ctx->gexec, ctx->st));
+        ctx->launches += ctx->body_nodes;
+      } else if (ctx->gram) {
+        enqueue_body_gram(ctx, ctx->use_sgs);
+      } else {
+        enqueue_body_fixed(ctx, ctx->kind, ctx->use_sgs);
       }
-      if (s.iters_done == k + 1) {
-        double hrow[HIST_W];
-        CK(cudaMemcpy(hrow, D.hist + (int64_t)k * HIST_W, sizeof(hrow), cudaMemcpyDeviceToHost));
-        double res11[11];
-        for (int f = 0; f < 11; ++f)
-          res11[f] = (f < 8) ? hrow[f] : (f == 8 ? hrow[H_GAP] : (f == 9 ? hrow[H_OBJP] : hrow[H_OBJD]));
-        if (cb(user, k + 1, res11, hrow[H_SIGMA], hrow[H_BETA]) != 0) {
-          status = set_err(ctx, GDWD_ERR_ABORTED, "callback requested abort");
-          break;
+      CK(cudaGetLastError());
+      ctx->k_host = k + 1;
+      if (ctx->prof) prof_flush(ctx);
+      if (cb) {
+        bool stop = false;
+        status = callback(k, &stop);
+        if (status) break;
+        ctx->stopped = stop;
+      } else if (iter_host && !ctx->prox) {
+        ctx->stopped = ctx->Sh->stopped != 0;  // synced inside the PSQMR loop
+      } else if ((k + 1) % ctx->poll == 0) {
+        // lagged poll: read the flag copied one poll interval ago (the GPU
+        // still has this interval queued, so it never idles on the host)
+        const int sl = ctx->poll_slot;
+        CK(cudaMemcpyAsync(ctx->poll_flag + sl, &ctx->S->stopped, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaEventRecord(ctx->poll_ev[sl], ctx->st));
+        if (ctx->poll_pending) {
+          CK(cudaEventSynchronize(ctx->poll_ev[sl ^ 1]));
+          if (ctx->poll_flag[sl ^ 1]) ctx->stopped = true;
         }
+        ctx->poll_pending = 1;
+        ctx->poll_slot = sl ^ 1;
       }
-      ctx->stopped = s.stopped != 0;
-    } else if (ctx->kind == GDWD_BACKEND_ITERATIVE) {
-      ctx->stopped = ctx->Sh->stopped != 0;  // synced inside the PSQMR loop
-    } else if ((k + 1) % ctx->poll == 0) {
-      // lagged poll: read the flag copied one poll interval ago (the GPU
-      // still has this interval queued, so it never idles on the host)
-      const int sl = ctx->poll_slot;
-      CK(cudaMemcpyAsync(ctx->poll_flag + sl, &ctx->S->stopped, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
-      CK(cudaEventRecord(ctx->poll_ev[sl], ctx->st));
-      if (ctx->poll_pending) {
-        CK(cudaEventSynchronize(ctx->poll_ev[sl ^ 1]));
-        if (ctx->poll_flag[sl ^ 1]) ctx->stopped = true;
-      }
-      ctx->poll_pending = 1;
-      ctx->poll_slot = sl ^ 1;
+    }
+    // a device-resident PSQMR solve that needs the proximal switch stopped
+    // the graph iterations: finish that iteration on the host and go on
+    if (status || !ctx->ps_graph || ctx->prox || !(ctx->stopped || ctx->k_host >= kend)) break;
+    int resumed = 0;
+    status = prox_resume(ctx, ctx->use_sgs, &resumed);
+    if (status || !resumed) break;
+    ctx->poll_pending = 0;
+    if (cb) {
+      bool stop = false;
+      status = callback(ctx->k_host - 1, &stop);
+      if (status) break;
+      ctx->stopped = stop;
     }
   }
   if (ctx->prof) prof_flush(ctx);
@@ -2349,7 +2689,7 @@ extern "C" int gdwd_solve_end(gdwd_ctx* ctx, gdwd_result* out) {
   MatView Z = zview(ctx);
   // final pass: dual objective / gap / stop test of the last iteration
   if (ctx->gram) run_zt(ctx, GsKAlpha{D}, MatView{ctx->kmat.p, ctx->n, ctx->n, ctx->ldm}, "gemv_K_alpha");
-  else run_zmv(ctx, OpRhsAlpha{D}, Z, "zmv_rhs_alpha");
+  else enqueue_rhs(ctx);
   enqueue_materialize(ctx);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_end, ctx->st));
@@ -2362,11 +2702,13 @@ extern "C" int gdwd_solve_end(gdwd_ctx* ctx, gdwd_result* out) {
   end_session(ctx);
   if (s.error == 6) return set_err(ctx, GDWD_ERR_ASSERT, "margin iterate left the positive orthant");
   ctx->hist_rows = s.iters_done;
+  ctx->hist_ps_dev = ctx->ps_graph;
   ctx->last_kind = ctx->kind;
   out->iterations = s.iters_done;
   out->converged = s.converged;
   out->backend = ctx->kind;
-  out->psqmr_total = ctx->psqmr_total;
+  out->psqmr_total = ctx->psqmr_total + s.ps_total;  // host-driven + device-resident PSQMR steps
+  if (ctx->ps_graph) ctx->launches += (int64_t)s.ps_total * ctx->ps_step_nodes;
   out->double_count = s.double_count;
   out->status = 0;
   out->sigma = s.sigma;
@@ -2546,7 +2888,10 @@ extern "C" int gdwd_get_history(gdwd_ctx* ctx, double* hist, int64_t max_rows, i
   int64_t nr = std::min(max_rows, ctx->hist_rows);
   if (nr > 0) {
     CK(cudaMemcpy(hist, ctx->histb.p, nr * HIST_W * sizeof(double), cudaMemcpyDeviceToHost));
-    for (int64_t k = 0; k < nr && k < (int64_t)ctx->ps_per_iter.size(); ++k) hist[k * HIST_W + H_PSQMR] = ctx->ps_per_iter[k];
+    // host-driven PSQMR counts its steps on the host; the device-resident
+    // one records them in the history itself (OpPsEnd)
+    if (!ctx->hist_ps_dev)
+      for (int64_t k = 0; k < nr && k < (int64_t)ctx->ps_per_iter.size(); ++k) hist[k * HIST_W + H_PSQMR] = ctx->ps_per_iter[k];
   }
   *rows = nr;
   return GDWD_OK;

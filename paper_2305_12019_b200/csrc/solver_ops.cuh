@@ -34,6 +34,7 @@ struct Scal {
   double ytzw;        // Gram space: y . ztw_bar (= zy . w_bar)
   double pv[16];      // proximal: V^T v of the last projection
   double px_beta;     // proximal: beta of the current solve
+  double ft_ys, ft_ya, ft_zal2;  // fused tail: y.(xi - r), y.alpha, ||Z~ alpha||^2 after Step 3
 };
 
 constexpr int PX_MAXL = 16;  // ell - 1 <= 16 eigenvectors in the proximal operator
@@ -51,6 +52,8 @@ struct Dev {
   double *pr, *pres, *pq, *pu, *pd, *pAd, *pAq;
   // Gram-space SMW2: n-coefficient temporaries and the d-space outputs
   double *cres, *cdiff;
+  // fused tail (zft.cuh): Z~ (xi - r) and Z~ alpha after Step 3
+  double *zp0, *zp1;
   double *wd, *ud, *rhod;
   // proximal backend (subsolvers.py:159-256): V = top-(ell-1) eigenvectors of
   // Z~ Z~^T, eigenvector-major [L][d]; coefficient vectors for inv / fwd
@@ -506,6 +509,127 @@ struct OpStep3 {
 };
 
 // ---------------------------------------------------------------------------
+// Fused tail of an X-space iteration (zft.cuh, SURVEY App. C fusion P2): one
+// pass over X computes ztw = Z~^T w after a re-solve (solver.py:530; the
+// reused ztw_bar otherwise, :521-522), Step 3 with the KKT sample sums
+// (solver.py:538-541, 311-333) exactly as OpStep3, and the next iteration's
+// products Z~ (xi - r) and Z~ alpha.  The next right-hand side
+// Z~ (xi - r - alpha/sigma) is then Z~ (xi - r) - (Z~ alpha)/sigma_next
+// (OpRhsParts, no pass over X): the same vector up to rounding.
+// ---------------------------------------------------------------------------
+struct OpTail {
+  static constexpr int R = 2, NN = 2, ND = 1;
+  struct Pf {
+    double rn, y, e, al, zb;  // prefetched per-sample inputs
+  };
+  struct U {
+    double sig, bet, tsig, csig;  // sigma, beta, tau*sigma, C/sigma
+    int reuse;
+  };
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV bool need_dot() const { return !D.S->reuse; }
+  GDWD_DEV double wval(int64_t j) const { return D.x[j]; }
+  GDWD_DEV U uniform() const {
+    const Scal* S = D.S;
+    U u;
+    u.sig = S->sigma;
+    u.bet = D.x[D.bot];
+    u.tsig = D.tau * u.sig;
+    u.csig = D.C / u.sig;
+    u.reuse = S->reuse;
+    return u;
+  }
+  GDWD_DEV void prefetch(int64_t i, Pf& p) const {
+    p.rn = D.rnew[i];
+    p.y = D.y[i];
+    p.e = D.e[i];
+    p.al = D.al[i];
+    p.zb = D.ztwb[i];
+  }
+  // the OpStep3 elementwise update (same expressions); sums y.(xi - r), y.alpha
+  GDWD_DEV void input(int64_t i, double dot, const Pf& p, const U& u, double (&t)[R], bool write,
+                      double (&na)[NN]) const {
+    const double rr = p.rn;
+    const double yi = p.y, ei = p.e, zt = u.reuse ? p.zb : dot, ali = p.al;
+    const double xv = np_max0((((rr - zt) - yi * u.bet) + ali / u.sig) - u.csig * ei);
+    const double pg = ((zt + yi * u.bet) + xv) - rr;
+    const double an = ali - u.tsig * pg;
+    if (write) {
+      D.ztw[i] = zt;
+      D.r[i] = rr;
+      D.xi[i] = xv;
+      D.al[i] = an;
+      na[0] += yi * (xv - rr);
+      na[1] += yi * an;
+    }
+    t[0] = xv - rr;
+    t[1] = an;
+  }
+  GDWD_DEV void epi(int64_t j, const double (&v)[R], double (&da)[ND]) const {
+    D.zp0[j] = v[0];
+    D.zp1[j] = v[1];
+    da[0] += v[1] * v[1];
+  }
+  GDWD_DEV void fin(const double (&s)[NN], const double (&ds)[ND]) const {
+    Scal* S = D.S;
+    S->ft_ys = s[0];
+    S->ft_ya = s[1];
+    S->ft_zal2 = ds[0];
+  }
+};
+
+// KKT sample sums of Step 3 after the fused tail (OpStep3's sums and fin,
+// from the stored r, xi, alpha, ztw; pg recomputed with the same expression)
+struct OpKktTail {
+  static constexpr int NR = 10;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void elem(int64_t i, double (&a)[NR]) const {
+    const double bet = D.x[D.bot], C = D.C;
+    const double rr = D.r[i], yi = D.y[i], ei = D.e[i], zt = D.ztw[i], xv = D.xi[i], an = D.al[i];
+    const double pg = ((zt + yi * bet) + xv) - rr;
+    const double wl = D.wl[i];
+    const double s = (D.q * wl) / np_pow(rr, D.qp1);
+    const double d2 = an - s;
+    const double mn = np_min0(an);
+    const double mx = np_max0(an - C * ei);
+    a[0] += yi * an;
+    a[1] += xv * (C * ei - an);
+    a[2] += d2 * d2;
+    a[3] += pg * pg;
+    a[4] += mn * mn;
+    a[5] += mx * mx;
+    a[6] += wl / np_pow(rr, D.q);
+    a[7] += ei * xv;
+    a[8] += np_pow(wl, D.e1) * np_pow(np_max0(an), D.e2);
+    a[9] += (rr <= 0.0) ? 1.0 : 0.0;
+  }
+  GDWD_DEV void fin(const double (&s)[NR]) const { OpStep3{D}.fin(s); }
+};
+
+// h = [-(Z~(xi - r) - Z~ alpha / sigma) + mu^2 u + (mu/sigma) rho ;
+//      -(y.(xi - r) - y.alpha / sigma)] from the fused tail's products, and
+// the previous iteration's dual objective, gap and stopping test (the
+// OpRhsAlpha fin) -- a d-space map, no pass over X.
+struct OpRhsParts {
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  GDWD_DEV bool skip() const { return D.S->stopped; }
+  GDWD_DEV void elem(int64_t j, double (&)[NR]) const {
+    const double sig = D.S->sigma_next;
+    D.h[j] = (-(D.zp0[j] - D.zp1[j] / sig) + D.mu2 * D.u[j]) + (D.mu / sig) * D.rho[j];
+  }
+  GDWD_DEV void fin(const double (&)[NR]) const {
+    Scal* S = D.S;
+    D.h[D.bot] = -(S->ft_ys - S->ft_ya / S->sigma_next);
+    finish_previous(D, S->ft_zal2);
+  }
+};
+
+// ---------------------------------------------------------------------------
 // SMW solve (subsolvers.py:127-151) with the explicit G^{-1}
 // ---------------------------------------------------------------------------
 struct OpSmwS1 {  // s1 = Z^T (h/mu^2) + y t2
@@ -947,6 +1071,32 @@ struct OpPsV2 {  // d, x, Ad, res updates; ||res||; q = u + beta q
   }
 };
 
+
+// End of a device-resident PSQMR call (psqmr.py:65-93 as captured in a CUDA
+// graph WHILE node): the step count joins the totals and the history; a run
+// that did not converge (step cap or breakdown) is the permanent switch to
+// the proximal backend (solver.py:479-483), which the host builds -- the
+// solve stops here (every later kernel is a no-op) with error 7 and the
+// number of the failed solve, and the host resumes the iteration.
+struct OpPsEnd {
+  static constexpr int NR = 1;
+  static constexpr bool HAS_FIN = true;
+  Dev D;
+  int pred;   // 1: the Step-1c re-solve (skipped when the reuse test passed)
+  int which;  // 1: first solve of the iteration, 2: the re-solve
+  GDWD_DEV bool skip() const { return D.S->stopped || (pred && D.S->reuse); }
+  GDWD_DEV void elem(int64_t, double (&)[NR]) const {}
+  GDWD_DEV void fin(const double (&)[NR]) const {
+    Scal* S = D.S;
+    S->ps_total += S->ps_iters;
+    D.hist[(int64_t)S->k * HIST_W + H_PSQMR] += (double)S->ps_iters;
+    if (!S->ps_conv) {
+      S->error = 7;
+      S->need_prox = which;
+      S->stopped = 1;
+    }
+  }
+};
 
 // ---------------------------------------------------------------------------
 // Proximal backend (subsolvers.py:169-256).  inv(v) = base v + V (c_inv .* V^T v)
