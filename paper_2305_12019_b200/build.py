@@ -20,8 +20,6 @@ HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libgdwd_b200.so"
 SOURCES = ["gdwd.cu", "gram.cu", "ingest.cpp"]
-HEADERS = ["common.cuh", "zops.cuh", "solver_ops.cuh", "gram.cuh", "spops.cuh", "persist.cuh", "persist3.cuh", "synth.cuh",
-           "select.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -34,7 +32,8 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES + HEADERS] + [HERE.parent / "include" / "gdwd_b200.h"]
+    deps = [CSRC / s for s in SOURCES] + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [
+        HERE.parent / "include" / "gdwd_b200.h"]
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 
 

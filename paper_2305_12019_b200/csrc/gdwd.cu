@@ -257,6 +257,7 @@ struct gdwd_ctx {
   bool use_sgs = true, stopped = false, gram = false, persistent = false;
   bool iter_gram = false;  // ITERATIVE with the d x d Gram operator (gdmat)
   bool ft = false;         // X-space loop with the fused tail pass (zft.cuh)
+  unsigned long long* ft_ts = nullptr;  // GDWD_FT_TIMING stamps (diagnostics)
   bool ps_graph = false;   // ITERATIVE body captured with device-resident PSQMR (WHILE nodes)
   cudaStream_t cap_st = nullptr;  // capture-to-graph stream for conditional bodies
   int64_t ps_step_nodes = 0;      // kernels per device-resident PSQMR step (launch accounting)
@@ -462,11 +463,11 @@ static void run_vm(gdwd_ctx* ctx, const Op& op, int64_t len, const char* tag = "
 }
 
 // Fused dot -> epilogue -> axpy pass (zft.cuh) geometry: the smallest
-// cluster whose feature slices fit the column threads' registers (<= 12
-// columns per thread), rows per stage and stages from the shared-memory
-// budget.  cs = 0: not eligible (d > 8 x 12 x 512).
+// cluster whose feature slices fit the axpy threads' registers (<= 8 column
+// pairs per thread); stages of ~32 KB, as many as fit 192 KB with the slice
+// of w.  cs = 0: not eligible (d > 8 x 5120).
 struct FtPlan {
-  int cs = 0, dw = 0, tr = 0, ns = 0, cpt = 0;
+  int cs = 0, dw = 0, tr = 0, ns = 0, p2 = 0;
 };
 static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
@@ -474,25 +475,25 @@ static int env_int(const char* name, int dflt) {
 }
 static FtPlan ft_plan(int64_t d) {
   FtPlan p;
-  for (int cs = std::max(1, env_int("GDWD_FT_CS", 1)); cs <= FT_CSMAX; cs *= 2) {  // (env: tuning experiments)
-    const int64_t dw = ((d + cs - 1) / cs + 1) / 2 * 2;
-    const int64_t c = (dw + FT_CW - 1) / FT_CW;
-    if (c <= 12) {
-      p.cs = cs;
-      p.dw = (int)dw;
-      p.cpt = c <= 2 ? 2 : (c <= 4 ? 4 : (c <= 8 ? 8 : 12));
-      break;
-    }
-  }
-  if (!p.cs) return p;
+  // one CTA per feature range (cs = 1): the cluster variants (cs > 1, wide
+  // d) were measured slower than the two unfused passes (zft.cuh header)
+  const int cs = std::max(1, env_int("GDWD_FT_CS", 1));  // (env: tuning experiments)
+  const int64_t dw = ((d + cs - 1) / cs + 1) / 2 * 2;
+  const int need = ft_pairs((int)std::min<int64_t>(dw, 1 << 20));
+  if (need > 8) return p;
+  p.cs = cs;
+  p.dw = (int)dw;
+  p.p2 = need <= 1 ? 1 : (need <= 2 ? 2 : (need <= 4 ? 4 : 8));
   const int64_t rb = (int64_t)p.dw * 8;
-  p.tr = (int)std::max<int64_t>(1, std::min<int64_t>(ft_trm(p.cpt), 98304 / rb));
-  p.ns = (int)std::max<int64_t>(2, std::min<int64_t>(4, 196608 / (p.tr * rb)));
-  if (env_int("GDWD_FT_TR", 0) > 0) p.tr = std::min(env_int("GDWD_FT_TR", 0), ft_trm(p.cpt));
-  if (env_int("GDWD_FT_NS", 0) > 1) p.ns = std::min(env_int("GDWD_FT_NS", 0), 8);
-  // stages + the slice of w <= 210 KB
-  while ((p.ns * p.tr + 1) * rb > 210 * 1024 && p.tr > 1) --p.tr;
-  if ((p.ns * p.tr + 1) * rb > 210 * 1024) p.cs = 0;
+  p.tr = (int)std::max<int64_t>(1, std::min<int64_t>(ft_tra(p.p2), 65536 / rb));
+  if (env_int("GDWD_FT_TR", 0) > 0) p.tr = std::min(env_int("GDWD_FT_TR", 0), ft_tra(p.p2));
+  p.ns = (int)std::min<int64_t>(FT_NSMAX, 196608 / (p.tr * rb));
+  if (env_int("GDWD_FT_NS", 0) > 1) p.ns = std::min(env_int("GDWD_FT_NS", 0), FT_NSMAX);
+  // each tile carries ~2 us of dot and hand-off latency: the pass pays off
+  // only with >= 32 KB tiles and 3 stages in flight (measured, zft.cuh)
+  const bool forced = env_int("GDWD_FT_FORCE", 0) != 0;
+  if (!forced && (p.tr * rb < 32 * 1024 || p.ns < 3 || cs != 1)) p.cs = 0;
+  if ((p.ns * p.tr + 1) * rb > 208 * 1024 || p.ns < 2) p.cs = 0;
   return p;
 }
 static bool ft_enabled() {
@@ -503,10 +504,10 @@ static bool ft_enabled() {
 // (the occupancy query and attribute set run the first time a geometry is
 // seen on a device; solve_begin calls run_ft with prepare_only before any
 // graph capture, where they are not allowed)
-template <class Op, int CPT>
+template <class Op, int P2>
 static void launch_ft(gdwd_ctx* ctx, const Op& op, MatView X, const FtPlan& p, FtGeom& g, const Scratch& sc,
                       bool prepare_only) {
-  auto kfn = zft_kernel<Op, CPT>;
+  auto kfn = zft_kernel<Op, P2>;
   g = FtGeom{p.cs, 0, p.dw, p.tr, p.ns, (X.cols + 1) / 2 * 2};
   const size_t sm = ft_smem_bytes(g, Op::R);
   static std::map<std::pair<int, size_t>, int> cache;  // (device x cs, smem) -> co-resident clusters
@@ -550,7 +551,16 @@ static void launch_ft(gdwd_ctx* ctx, const Op& op, MatView X, const FtPlan& p, F
     }
     g.clusters = it->second;
   }
-  if (prepare_only) return;
+  if (prepare_only) {
+    if (getenv("GDWD_FT_TIMING")) {  // diagnostics: stamps of the last launch, ft_timing_report
+      static unsigned long long* buf = nullptr;
+      if (!buf) cudaMalloc(&buf, sizeof(unsigned long long) * FT_TS_TILES * FT_TS_PTS);
+      cudaMemset(buf, 0, sizeof(unsigned long long) * FT_TS_TILES * FT_TS_PTS);
+      cudaMemcpyToSymbol(g_ft_ts, &buf, sizeof(buf));
+      ctx->ft_ts = buf;
+    }
+    return;
+  }
   cfg.gridDim = dim3(g.clusters * p.cs);
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, op, X, g, sc);
   if (e != cudaSuccess && getenv("GDWD_DEBUG_LAUNCH"))
@@ -567,24 +577,24 @@ static void run_ft(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "zf
   const FtPlan p = ft_plan(X.cols);
   FtGeom g{};
   if (prepare_only) {
-    switch (p.cpt) {
+    switch (p.p2) {
+      case 1: launch_ft<Op, 1>(ctx, op, X, p, g, sc, true); break;
       case 2: launch_ft<Op, 2>(ctx, op, X, p, g, sc, true); break;
       case 4: launch_ft<Op, 4>(ctx, op, X, p, g, sc, true); break;
-      case 8: launch_ft<Op, 8>(ctx, op, X, p, g, sc, true); break;
-      default: launch_ft<Op, 12>(ctx, op, X, p, g, sc, true); break;
+      default: launch_ft<Op, 8>(ctx, op, X, p, g, sc, true); break;
     }
     if (getenv("GDWD_FT_DEBUG"))
-      fprintf(stderr, "zft plan: d=%lld cs=%d dw=%d cpt=%d tr=%d ns=%d clusters=%d smem=%zu\n", (long long)X.cols,
-              p.cs, p.dw, p.cpt, p.tr, p.ns, g.clusters, ft_smem_bytes(g, Op::R));
+      fprintf(stderr, "zft plan: d=%lld cs=%d dw=%d p2=%d tr=%d ns=%d clusters=%d smem=%zu\n", (long long)X.cols,
+              p.cs, p.dw, p.p2, p.tr, p.ns, g.clusters, ft_smem_bytes(g, Op::R));
     return;
   }
   {
     Launch L(ctx, tag);
-    switch (p.cpt) {
+    switch (p.p2) {
+      case 1: launch_ft<Op, 1>(ctx, op, X, p, g, sc, false); break;
       case 2: launch_ft<Op, 2>(ctx, op, X, p, g, sc, false); break;
       case 4: launch_ft<Op, 4>(ctx, op, X, p, g, sc, false); break;
-      case 8: launch_ft<Op, 8>(ctx, op, X, p, g, sc, false); break;
-      default: launch_ft<Op, 12>(ctx, op, X, p, g, sc, false); break;
+      default: launch_ft<Op, 8>(ctx, op, X, p, g, sc, false); break;
     }
   }
   {
@@ -2340,7 +2350,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   const int max_iter = cfg->max_iter;
 
   // ---- buffers ------------------------------------------------------------
-  const int NV = 12, MV = 18;
+  const int NV = 13, MV = 18;
   // Gram space pays off (and keeps w exactly representable) only when n <= d,
   // SMW2's own regime; an explicitly requested SMW2 with d < n iterates over X.
   // DIRECT with few samples (2n <= d, unsharded, n within the persistent
@@ -2381,7 +2391,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   D.u = mv; D.rho = mv + ms; D.h = mv + 2 * ms; D.h2 = mv + 3 * ms; D.xb = mv + 4 * ms; D.x = mv + 5 * ms;
   D.pr = mv + 6 * ms; D.pres = mv + 7 * ms; D.pq = mv + 8 * ms; D.pu = mv + 9 * ms; D.pd = mv + 10 * ms;
   D.pAd = mv + 11 * ms; D.pAq = mv + 12 * ms;
-  D.cres = nv + 10 * nst; D.cdiff = nv + 11 * nst;
+  D.cres = nv + 10 * nst; D.cdiff = nv + 11 * nst; D.aln = nv + 12 * nst;
   D.zp0 = mv + 16 * ms; D.zp1 = mv + 17 * ms;  // fused tail products, zero before iteration 1
   D.bot = d;
   D.wd = D.x; D.ud = D.u; D.rhod = D.rho;
@@ -2681,9 +2691,39 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
   return status;
 }
 
+// GDWD_FT_TIMING: median per-tile intervals of the fused pass's roles (CTA 0, last launch)
+static void ft_timing_report(gdwd_ctx* ctx) {
+  std::vector<unsigned long long> h((size_t)FT_TS_TILES * FT_TS_PTS);
+  cudaMemcpy(h.data(), ctx->ft_ts, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  struct Iv { const char* name; int a, b; bool next; };
+  const Iv ivs[] = {{"prod: wait empty", 0, 1, false}, {"dot: wait xfree", 2, 13, false}, {"dot: fma loop", 13, 14, false},
+                    {"dot: shuffle sums", 14, 15, false}, {"dot: publish", 15, 3, false},
+                    {"axpy: wait full", 4, 5, false}, {"axpy: wait ts", 5, 6, false}, {"axpy: axpy", 6, 7, false},
+                    {"sw: wait dots", 8, 9, false}, {"sw: combine+input", 9, 10, false}, {"sw: prefetch+wait tsfree", 10, 11, false},
+                    {"sw: ts handoff", 11, 12, false}, {"sw: period", 8, 8, true}, {"axpy: period", 4, 4, true},
+                    {"prod: period", 0, 0, true}};
+  for (const Iv& iv : ivs) {
+    std::vector<double> v;
+    for (int t = 4; t + 1 < FT_TS_TILES; ++t) {
+      const unsigned long long* a = &h[(size_t)t * FT_TS_PTS];
+      const unsigned long long* b = iv.next ? &h[(size_t)(t + 1) * FT_TS_PTS] : a;
+      if (!a[iv.a] || !b[iv.b]) continue;
+      v.push_back((double)(b[iv.b] - a[iv.a]));
+    }
+    if (v.empty()) continue;
+    std::sort(v.begin(), v.end());
+    fprintf(stderr, "zft timing %-26s median %7.0f ns  p90 %7.0f ns  (n=%zu)\n", iv.name, v[v.size() / 2],
+            v[v.size() * 9 / 10], v.size());
+  }
+}
+
 extern "C" int gdwd_solve_end(gdwd_ctx* ctx, gdwd_result* out) {
   if (!ctx || !ctx->in_solve || !out) return set_err(ctx, GDWD_ERR_VALUE, "no solve in progress");
   CK(cudaSetDevice(ctx->device));
+  if (ctx->ft_ts) {
+    cudaDeviceSynchronize();
+    ft_timing_report(ctx);
+  }
   memset(out, 0, sizeof(*out));
   const Dev& D = ctx->D;
   MatView Z = zview(ctx);
@@ -2760,7 +2800,10 @@ static int comm_finish_init(gdwd_ctx* ctx, int32_t nranks, int32_t rank, int64_t
   CK(cudaStreamSynchronize(ctx->st));
   tmp.release();
   if (ctx->comm_err) return set_err(ctx, GDWD_ERR_CUDA, "all-reduce failed during communicator setup");
-  if ((int64_t)hv[1] != n_global) return set_err(ctx, GDWD_ERR_VALUE, "shard sizes do not add up to n_global");
+  if ((int64_t)hv[1] != n_global)
+    return set_err(ctx, GDWD_ERR_VALUE, "shard sizes do not add up to n_global (sum " + std::to_string(hv[1]) +
+                                            ", n_global " + std::to_string(n_global) + ", local " +
+                                            std::to_string(ctx->n) + ")");
   ctx->fro2 = hv[0];
   ctx->yty = (double)n_global;  // labels are +-1 (validated in set_problem)
   return GDWD_OK;

@@ -54,6 +54,7 @@ struct Dev {
   double *cres, *cdiff;
   // fused tail (zft.cuh): Z~ (xi - r) and Z~ alpha after Step 3
   double *zp0, *zp1;
+  double* aln;  // alpha after the fused tail's Step 3 (alpha itself is still being read)
   double *wd, *ud, *rhod;
   // proximal backend (subsolvers.py:159-256): V = top-(ell-1) eigenvectors of
   // Z~ Z~^T, eigenvector-major [L][d]; coefficient vectors for inv / fwd
@@ -540,12 +541,16 @@ struct OpTail {
     u.reuse = S->reuse;
     return u;
   }
-  GDWD_DEV void prefetch(int64_t i, Pf& p) const {
-    p.rn = D.rnew[i];
-    p.y = D.y[i];
-    p.e = D.e[i];
-    p.al = D.al[i];
-    p.zb = D.ztwb[i];
+  static constexpr int NPF = 5;  // per-sample inputs, staged by cp.async (zft.cuh)
+  GDWD_DEV const double* pf_src(int f, int64_t i) const {
+    return (f == 0 ? D.rnew : f == 1 ? D.y : f == 2 ? D.e : f == 3 ? D.al : D.ztwb) + i;
+  }
+  GDWD_DEV void load_pf(const double* slot, Pf& p) const {
+    p.rn = slot[0];
+    p.y = slot[1];
+    p.e = slot[2];
+    p.al = slot[3];
+    p.zb = slot[4];
   }
   // the OpStep3 elementwise update (same expressions); sums y.(xi - r), y.alpha
   GDWD_DEV void input(int64_t i, double dot, const Pf& p, const U& u, double (&t)[R], bool write,
@@ -559,7 +564,7 @@ struct OpTail {
       D.ztw[i] = zt;
       D.r[i] = rr;
       D.xi[i] = xv;
-      D.al[i] = an;
+      D.aln[i] = an;  // into alpha by OpKktTail: other ranks of the cluster may still read alpha
       na[0] += yi * (xv - rr);
       na[1] += yi * an;
     }
@@ -588,7 +593,8 @@ struct OpKktTail {
   GDWD_DEV bool skip() const { return D.S->stopped; }
   GDWD_DEV void elem(int64_t i, double (&a)[NR]) const {
     const double bet = D.x[D.bot], C = D.C;
-    const double rr = D.r[i], yi = D.y[i], ei = D.e[i], zt = D.ztw[i], xv = D.xi[i], an = D.al[i];
+    const double rr = D.r[i], yi = D.y[i], ei = D.e[i], zt = D.ztw[i], xv = D.xi[i], an = D.aln[i];
+    D.al[i] = an;
     const double pg = ((zt + yi * bet) + xv) - rr;
     const double wl = D.wl[i];
     const double s = (D.q * wl) / np_pow(rr, D.qp1);
