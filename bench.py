@@ -146,6 +146,9 @@ class Dist:
 
             backend = "nccl" if torch.cuda.is_available() else "gloo"
             if backend == "nccl":
+                from paper_2305_12019_b200.parallel import pin_nccl_determinism
+
+                pin_nccl_determinism()  # before torch's NCCL reads its parameters
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend=backend)
             self.dist, self.torch = dist, torch

@@ -240,8 +240,8 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
 #pragma unroll
         for (int c2 = c + 1; c2 < 8; ++c2) {
           const double lk = __shfl_sync(0xffffffffu, Pa[c], c2);  // L[p0+c2][p0+c]
-          Pa[c2] = Pa[c2] - Pa[c] * lk;
-          Pb[c2] = Pb[c2] - Pb[c] * lk;
+          Pa[c2] = __fma_rn(-Pa[c], lk, Pa[c2]);
+          Pb[c2] = __fma_rn(-Pb[c], lk, Pb[c2]);
         }
       }
     }
@@ -270,7 +270,7 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
           double acc = L[i][k];
 #pragma unroll
           for (int c = 0; c < 8; ++c)
-            if (c < pw) acc = acc - L[i][p0 + c] * lk[c];
+            if (c < pw) acc = __fma_rn(-L[i][p0 + c], lk[c], acc);
           L[i][k] = acc;
         }
       }
@@ -318,8 +318,8 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {
           const double xj = __shfl_sync(0xffffffffu, Xa[cc], j) * dj;
-          const double ua = Xa[cc] - la * xj;
-          Xb[cc] = Xb[cc] - lb * xj;
+          const double ua = __fma_rn(-la, xj, Xa[cc]);
+          Xb[cc] = __fma_rn(-lb, xj, Xb[cc]);
           Xa[cc] = own ? xj : ua;
         }
       }
@@ -330,7 +330,7 @@ __global__ void potrf_trtri_small(double* A, int64_t lda, double* Linv, int64_t 
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {
           const double xj = __shfl_sync(0xffffffffu, Xb[cc], j - 32) * dj;
-          const double ub = Xb[cc] - lb * xj;
+          const double ub = __fma_rn(-lb, xj, Xb[cc]);
           Xb[cc] = own ? xj : ub;
         }
       }

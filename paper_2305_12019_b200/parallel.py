@@ -24,6 +24,7 @@ SMW2 couples all samples through its n x n Gram, so it is not sharded
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from typing import Callable, Optional
 
@@ -82,11 +83,23 @@ class HostCommunicator:
         dp.n_global = int(n_global)
 
 
+def pin_nccl_determinism() -> None:
+    """Fix NCCL's algorithm and protocol (ring, simple) unless the user chose
+    them: the fp64 sum of an all-reduce is then formed in the same order on
+    every run, so sharded solves are bitwise reproducible run to run (NVLS /
+    tree selection can otherwise change with message size or topology).
+    Must run before the first NCCL communicator of the process (NCCL reads
+    these once); bench.py calls it before torch.distributed's own init."""
+    os.environ.setdefault("NCCL_ALGO", "Ring")
+    os.environ.setdefault("NCCL_PROTO", "Simple")
+
+
 class NcclCommunicator:
     """NCCL communicator over the ranks of a torch.distributed group."""
 
     def __init__(self, nranks: int, rank: int, broadcast_id: Callable[[Optional[bytes]], bytes]):
         """``broadcast_id(id_or_None)``: rank 0 passes its id, every rank gets it back."""
+        pin_nccl_determinism()
         lib = _lib.load()
         uid = None
         if rank == 0:
