@@ -231,6 +231,15 @@ struct gdwd_ctx {
   int fb_nb = 0, fb_parts = 0, fb_S = 0, fb_Q = 0;
   int64_t fb_entries = 0;  // padded entries
   bool sp_blocked = getenv("GDWD_SP_BLOCKED") ? atoi(getenv("GDWD_SP_BLOCKED")) != 0 : true;
+  // sample-blocked sliced ELL for Z~ t (spops.cuh SbView)
+  double* sb_val = nullptr;
+  unsigned short* sb_idx = nullptr;
+  int64_t* sb_base = nullptr;
+  int *sb_h = nullptr, *sb_perm = nullptr, *sb_chunk = nullptr;
+  int sb_nb = 0, sb_nslpb = 0;
+  int64_t sb_entries = 0;
+  DevBuf sb_part;  // [nb][d][R] partials
+  bool sp_sb = getenv("GDWD_SP_SB") ? atoi(getenv("GDWD_SP_SB")) != 0 : true;
   DevBuf tbuf;  // materialised Z t inputs (2 x n)
   DevBuf y, e, wl;
   // scratch
@@ -401,7 +410,21 @@ static void run_zmv(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "z
       Launch L(ctx, "sp_prep");
       sp_prep_kernel<Op><<<g1, SP_THREADS, 0, ctx->st>>>(op, ctx->n, ctx->tbuf.p, ctx->scr);
     }
-    {
+    if (ctx->sb_nb && ctx->sp_sb) {
+      SbView A{ctx->sb_val, ctx->sb_idx, ctx->sb_base, ctx->sb_h, ctx->sb_perm, ctx->sb_chunk, ctx->sb_nslpb,
+               ctx->sb_nb, ctx->n, ctx->d};
+      const size_t sm = (size_t)SB_S * Op::R * sizeof(double);
+      static unsigned long long attr = 0;
+      if (once_per_device(attr)) cudaFuncSetAttribute(sp_zmv_sb_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      {
+        Launch L(ctx, tag);
+        sp_zmv_sb_kernel<Op><<<SB_CHUNKS / (Op::R == 1 ? 1 : 2), sb_threads<Op::R>(), sm, ctx->st>>>(
+            op, A, ctx->tbuf.p, ctx->sb_part.p);
+      }
+      Launch L(ctx, "sp_zmv_sb_reduce");
+      sp_zmv_sb_reduce_kernel<Op><<<(unsigned)((ctx->d + 31) / 32), SP_THREADS, 0, ctx->st>>>(op, ctx->sb_part.p,
+                                                                                          ctx->sb_nb, ctx->d, g1, sc);
+    } else {
       Launch L(ctx, tag);
       SpView A{ctx->csr_ptr, ctx->csr_idx, ctx->csr_val, ctx->d, ctx->n};
       sp_zmv_kernel<Op><<<sp_grid(ctx->d * 32, NUM_SMS * 8), SP_THREADS, 0, ctx->st>>>(op, A, ctx->tbuf.p, g1, sc);
@@ -431,7 +454,7 @@ static void run_zt(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "zt
       static unsigned long long attr = 0;
       if (once_per_device(attr))
         cudaFuncSetAttribute(sp_ztmv_fb_kernel<Op, FB_H, FB_U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FB_SMEM_MAX);
-      sp_ztmv_fb_kernel<Op, FB_H, FB_U><<<ctx->fb_parts, SP_THREADS, sm, ctx->st>>>(op, A, sc);
+      sp_ztmv_fb_kernel<Op, FB_H, FB_U><<<ctx->fb_parts, FB_THREADS, sm, ctx->st>>>(op, A, sc);
     } else if (!X.a) {
       SpView A{ctx->csc_ptr, ctx->csc_idx, ctx->csc_val, ctx->n, ctx->d};
       sp_ztmv_kernel<Op, 8><<<sp_grid(ctx->n, NUM_SMS * 8), SP_THREADS, 0, ctx->st>>>(op, A, sc);
@@ -631,6 +654,7 @@ static int ensure_scratch(gdwd_ctx* ctx, int64_t rows, int64_t cols) {
   part = std::max<size_t>(part, (size_t)NUM_SMS * 2 * zg.ldp);  // fused tail: <= 148 clusters x 2 products
   size_t npart = (size_t)maxslots * 16;
   size_t tpart = (size_t)std::max<int64_t>(zg.tiles, NUM_SMS * 8) * 16 + 16;
+  tpart = std::max<size_t>(tpart, (size_t)((cols + 31) / 32) * 4 + 16);  // per-32-feature reduce CTAs (ND <= 4)
   size_t nt = (size_t)std::max<int64_t>(zg.tiles, maxslots) + 4;
   CK(ctx->part.ensure(std::max(part, ctx->part.n)));
   CK(ctx->npart.ensure(std::max(npart, ctx->npart.n)));
@@ -846,8 +870,15 @@ static int compute_fro2(gdwd_ctx* ctx, const double* a, int64_t rows, int64_t co
 static void free_sparse(gdwd_ctx* ctx) {
   for (void* p : {(void*)ctx->csc_ptr, (void*)ctx->csr_ptr, (void*)ctx->csc_idx, (void*)ctx->csr_idx,
                   (void*)ctx->csc_val, (void*)ctx->csr_val, (void*)ctx->fb_ptr, (void*)ctx->fb_idx,
-                  (void*)ctx->fb_val, (void*)ctx->fb_perm, (void*)ctx->fb_cnt})
+                  (void*)ctx->fb_val, (void*)ctx->fb_perm, (void*)ctx->fb_cnt, (void*)ctx->sb_val, (void*)ctx->sb_idx,
+                  (void*)ctx->sb_base, (void*)ctx->sb_h, (void*)ctx->sb_perm, (void*)ctx->sb_chunk})
     dfree(p, ctx->st);
+  ctx->sb_val = nullptr;
+  ctx->sb_idx = nullptr;
+  ctx->sb_base = nullptr;
+  ctx->sb_h = ctx->sb_perm = ctx->sb_chunk = nullptr;
+  ctx->sb_nb = ctx->sb_nslpb = 0;
+  ctx->sb_entries = 0;
   ctx->csc_ptr = ctx->csr_ptr = nullptr;
   ctx->csc_idx = ctx->csr_idx = nullptr;
   ctx->csc_val = ctx->csr_val = nullptr;
@@ -965,7 +996,7 @@ int gdwd_ctx_create(int32_t device, gdwd_ctx** out) {
   if (e == cudaSuccess) {
     keep_pool_reserved(device);
     for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat, &ctx->gram_ws})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat, &ctx->gram_ws, &ctx->sb_part})
       b->st = ctx->st;
   }
   if (e == cudaSuccess) e = cudaMalloc(&ctx->S, sizeof(Scal));
@@ -998,7 +1029,7 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   dfree(ctx->Zs, ctx->st);
   free_sparse(ctx);
   for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat, &ctx->gram_ws})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat, &ctx->gram_ws, &ctx->sb_part})
     b->release();
   end_session(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1318,7 +1349,105 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
     }
     hmark("sliced ELL concat + to device");
   }
-  CK(ctx->tbuf.ensure((size_t)2 * n));
+  // sample-blocked sliced ELL for Z~ t (spops.cuh SbView): blocks of SB_S
+  // samples; per block every feature, sorted by its entry count in the block
+  // (descending, then index), 32 per slice, entries column-major in sample
+  // order with 16-bit block-local sample indices
+  if (nnz > 0 && d < ((int64_t)1 << 31) / 32) {
+    const int nb = (int)((n + SB_S - 1) / SB_S);
+    const int nslpb = (int)((d + 31) / 32);
+    const int64_t nsl = (int64_t)nb * nslpb;
+    std::vector<int> hh((size_t)nsl, 0), pp((size_t)nsl * 32, -1);
+    std::vector<int64_t> bb((size_t)nsl + 1, 0);
+    // per block, per feature: the entry range of row j inside the block
+    std::vector<int64_t> bnd((size_t)(nb + 1) * d);
+    par([&](int t, int64_t, int64_t) {
+      for (int64_t j = d * t / T; j < d * (t + 1) / T; ++j) {
+        int64_t k = rp[j];
+        for (int b = 0; b <= nb; ++b) {
+          const int64_t lim = std::min<int64_t>(n, (int64_t)b * SB_S);
+          while (k < rp[j + 1] && cidx[k] < lim) ++k;
+          bnd[(size_t)b * d + j] = k;
+        }
+      }
+    });
+    // slice heights and orders per block (threads over blocks)
+    {
+      std::vector<std::thread> th;
+      const int nthr = std::max(1, std::min(nb, T));
+      for (int t = 0; t < nthr; ++t)
+        th.emplace_back([&, t]() {
+          std::vector<int> ord(d);
+          for (int b = t; b < nb; b += nthr) {
+            const int64_t* lo = &bnd[(size_t)b * d];
+            const int64_t* hi = &bnd[(size_t)(b + 1) * d];
+            for (int64_t j = 0; j < d; ++j) ord[j] = (int)j;
+            std::sort(ord.begin(), ord.end(), [&](int x, int y) {
+              const int64_t cx = hi[x] - lo[x], cy = hi[y] - lo[y];
+              return cx != cy ? cx > cy : x < y;
+            });
+            for (int q = 0; q < nslpb; ++q) {
+              const int64_t sl = (int64_t)b * nslpb + q;
+              hh[sl] = (int)(hi[ord[32 * q]] - lo[ord[32 * q]]);
+              for (int l = 0; l < 32 && 32 * q + l < d; ++l) pp[sl * 32 + l] = ord[32 * q + l];
+            }
+          }
+        });
+      for (auto& x : th) x.join();
+    }
+    for (int64_t sl = 0; sl < nsl; ++sl) bb[sl + 1] = bb[sl] + 32 * (int64_t)hh[sl];
+    const int64_t ne = bb[nsl];
+    if (ne < ((int64_t)1 << 31)) {
+      std::vector<double> sv((size_t)std::max<int64_t>(ne, 1), 0.0);
+      std::vector<unsigned short> si((size_t)std::max<int64_t>(ne, 1), 0);
+      par([&](int t, int64_t, int64_t) {
+        for (int64_t sl = nsl * t / T; sl < nsl * (t + 1) / T; ++sl) {
+          const int b = (int)(sl / nslpb);
+          for (int l = 0; l < 32; ++l) {
+            const int j = pp[sl * 32 + l];
+            if (j < 0) continue;
+            const int64_t lo = bnd[(size_t)b * d + j], hi = bnd[(size_t)(b + 1) * d + j];
+            for (int64_t e = 0; e < hi - lo; ++e) {
+              sv[bb[sl] + 32 * e + l] = cval[lo + e];
+              si[bb[sl] + 32 * e + l] = (unsigned short)(cidx[lo + e] - (int64_t)b * SB_S);
+            }
+          }
+        }
+      });
+      // SB_CHUNKS chunks of consecutive slices with equal shares of entries
+      // (+ 32 per slice for its fixed cost)
+      std::vector<int> ch(SB_CHUNKS + 1, (int)nsl);
+      {
+        const double tot = (double)ne + 32.0 * (double)nsl;
+        int c = 1;
+        ch[0] = 0;
+        double acc = 0.0;
+        for (int64_t sl = 0; sl < nsl && c < SB_CHUNKS; ++sl) {
+          acc += 32.0 * hh[sl] + 32.0;
+          while (c < SB_CHUNKS && acc >= tot * c / SB_CHUNKS) ch[c++] = (int)(sl + 1);
+        }
+        for (; c < SB_CHUNKS; ++c) ch[c] = (int)nsl;
+      }
+      CK(dmalloc((void**)&ctx->sb_val, sv.size() * sizeof(double), ctx->st));
+      CK(dmalloc((void**)&ctx->sb_idx, si.size() * sizeof(unsigned short), ctx->st));
+      CK(dmalloc((void**)&ctx->sb_base, bb.size() * sizeof(int64_t), ctx->st));
+      CK(dmalloc((void**)&ctx->sb_h, hh.size() * sizeof(int), ctx->st));
+      CK(dmalloc((void**)&ctx->sb_perm, pp.size() * sizeof(int), ctx->st));
+      CK(dmalloc((void**)&ctx->sb_chunk, ch.size() * sizeof(int), ctx->st));
+      CK(cudaMemcpy(ctx->sb_val, sv.data(), sv.size() * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ctx->sb_idx, si.data(), si.size() * sizeof(unsigned short), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ctx->sb_base, bb.data(), bb.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ctx->sb_h, hh.data(), hh.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ctx->sb_perm, pp.data(), pp.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ctx->sb_chunk, ch.data(), ch.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CK(ctx->sb_part.ensure((size_t)nb * d * 2));
+      ctx->sb_nb = nb;
+      ctx->sb_nslpb = nslpb;
+      ctx->sb_entries = ne;
+    }
+    hmark("sample-blocked sliced ELL");
+  }
+  CK(ctx->tbuf.ensure((size_t)2 * n + 2));
   ctx->n = n;
   ctx->d = d;
   ctx->ldz = (d + 1) / 2 * 2;

@@ -124,6 +124,164 @@ __global__ void __launch_bounds__(SP_THREADS) sp_zmv_kernel(Op op, SpView A, con
   }
 }
 
+// ---------------------------------------------------------------------------
+// Z~ t on a sample-blocked sliced ELL (built at upload, gdwd.cu).  The CSR
+// gather kernel above is bound by the L1TEX pipe: every nonzero is its own
+// 8-byte gather of t from L2.  Here the samples are cut into blocks of
+// SB_S = 12288 (t's block, R values per sample, fits shared memory); within a
+// block the features are sorted by entry count and cut into 32-wide slices
+// stored column-major (entry e of lane l at base + 32 e + l: coalesced value
+// and 16-bit block-local index loads), so each lane sums one feature's
+// entries of the block in sample order, gathering t from shared memory.
+// Every (block, feature) partial is written (zero when empty); a second
+// kernel sums them over the blocks in block order and runs the epilogue --
+// per feature the entries are still summed in sample order, blocks in order.
+// CTAs take equal shares of the entries (chunks of consecutive slices, at
+// most a block boundary or two inside a chunk: t is restaged there).
+// ---------------------------------------------------------------------------
+constexpr int SB_S = 12288;       // samples per block
+constexpr int SB_THREADS = 512;
+constexpr int SB_CHUNKS = 2 * 148;  // chunk boundaries: 2 per SM (R = 1), pairs for R = 2
+constexpr int SB_U = 8;           // entries per lane in flight
+
+struct SbView {
+  const double* val;
+  const unsigned short* idx;
+  const int64_t* base;  // per slice: first entry
+  const int* h;         // per slice: entries per lane
+  const int* perm;      // per slice and lane: feature (-1: pad lane)
+  const int* chunk;     // SB_CHUNKS + 1 slice boundaries
+  int nslpb;            // slices per block (ceil(d / 32))
+  int nb;               // blocks
+  int64_t n, d;
+};
+
+// threads per CTA: R = 1 stages 96 KB of t (2 CTAs of 512 per SM), R = 2
+// stages 192 KB (one CTA of 1024 per SM): 32 warps per SM either way
+template <int R>
+__host__ __device__ constexpr int sb_threads() { return R == 1 ? SB_THREADS : 2 * SB_THREADS; }
+
+template <class Op>
+__global__ void __launch_bounds__(sb_threads<Op::R>()) sp_zmv_sb_kernel(Op op, SbView A, const double* tbuf,
+                                                                       double* part) {
+  constexpr int R = Op::R;
+  constexpr int NT = sb_threads<R>();
+  if (op.skip()) return;
+  extern __shared__ __align__(16) double tsm[];  // [SB_S][R]
+  constexpr int PER = R == 1 ? 1 : 2;           // chunks per CTA (grid SB_CHUNKS / PER)
+  const int s0 = A.chunk[blockIdx.x * PER], s1 = A.chunk[blockIdx.x * PER + PER];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = NT >> 5;
+  for (int s = s0; s < s1;) {
+    const int b = s / A.nslpb;
+    const int se = s1 < (b + 1) * A.nslpb ? s1 : (b + 1) * A.nslpb;
+    const int64_t i0 = (int64_t)b * SB_S;
+    const int cnt = (int)(A.n - i0 < SB_S ? A.n - i0 : SB_S);
+    __syncthreads();  // the previous block's gathers are done
+    {
+      const double2* src = reinterpret_cast<const double2*>(tbuf + i0 * R);
+      double2* dst = reinterpret_cast<double2*>(tsm);
+      for (int k = threadIdx.x; k < (cnt * R + 1) / 2; k += NT) dst[k] = __ldcg(src + k);
+    }
+    __syncthreads();
+    for (int ss = s + warp; ss < se; ss += nw) {
+      const int h = A.h[ss];
+      const int64_t base = A.base[ss] + lane;
+      const int j = A.perm[(int64_t)ss * 32 + lane];
+      double acc[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = 0.0;
+      int e = 0;
+      for (; e + SB_U <= h; e += SB_U) {
+        double v[SB_U];
+        int ix[SB_U];
+#pragma unroll
+        for (int u = 0; u < SB_U; ++u) {
+          v[u] = __ldcs(A.val + base + 32 * (int64_t)(e + u));
+          ix[u] = __ldcs(A.idx + base + 32 * (int64_t)(e + u));
+        }
+#pragma unroll
+        for (int u = 0; u < SB_U; ++u)
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] += v[u] * tsm[ix[u] * R + r];
+      }
+      for (; e < h; ++e) {
+        const double v = __ldcs(A.val + base + 32 * (int64_t)e);
+        const int ix = __ldcs(A.idx + base + 32 * (int64_t)e);
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] += v * tsm[ix * R + r];
+      }
+      if (j >= 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) part[((int64_t)b * A.d + j) * R + r] = acc[r];
+      }
+    }
+    s = se;
+  }
+}
+
+// v_j = sum of the per-block partials; per-feature epilogue, then the
+// finaliser (the prep kernel's n-partials and the d-partials) -- the tail of
+// sp_zmv_kernel.  A CTA covers 32 features: warp w sums blocks w, w + 8, ...
+// in order, then warp 0 adds the 8 warp sums in warp order (fixed tree).
+template <class Op>
+__global__ void __launch_bounds__(SP_THREADS) sp_zmv_sb_reduce_kernel(Op op, const double* part, int nb, int64_t d,
+                                                                    int nprep, Scratch s) {
+  constexpr int R = Op::R, NN = Op::NN, ND = Op::ND;
+  constexpr int NW = SP_THREADS / 32;
+  if (op.skip()) return;
+  __shared__ double pw[NW][R][32];
+  __shared__ double red2[NW * (NN > ND ? NN : ND)];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  double v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = 0.0;
+  if (j < d)
+#pragma unroll 4
+    for (int b = warp; b < nb; b += NW) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] += __ldcg(part + ((int64_t)b * d + j) * R + r);
+    }
+#pragma unroll
+  for (int r = 0; r < R; ++r) pw[warp][r][lane] = v[r];
+  __syncthreads();
+  double dacc[ND];
+#pragma unroll
+  for (int k = 0; k < ND; ++k) dacc[k] = 0.0;
+  if (warp == 0 && j < d) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double a = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) a += pw[w][r][lane];
+      v[r] = a;
+    }
+    if (s.bundle) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) s.bundle[(int64_t)r * d + j] = v[r];
+    } else {
+      op.epi(j, v, dacc);
+    }
+  }
+  block_sum<ND>(dacc, red2);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < ND; ++k) s.tpart[(int64_t)blockIdx.x * ND + k] = dacc[k];
+  }
+  if (!last_arrival(&s.tickets[0], gridDim.x)) return;
+  double nsum[NN], dsum[ND];
+  block_sum_partials<NN>(s.npart, nprep, nsum, red2);
+  block_sum_partials<ND>(s.tpart, gridDim.x, dsum, red2);
+  if (threadIdx.x == 0) {
+    if (s.bundle) {
+#pragma unroll
+      for (int k = 0; k < NN; ++k) s.bundle[(int64_t)R * d + k] = nsum[k];
+    } else {
+      op.fin(nsum, dsum);
+    }
+  }
+}
+
 // dot_i = sum_j Z[j,i] w_j (CSC columns = samples).  A warp takes 32
 // consecutive samples: in 32/G rounds each group of G lanes reduces one
 // sample's dot, which is parked in the lane with that sample's index; then
@@ -221,14 +379,18 @@ struct FbView {
   int nb, fb, parts, S, Q;
 };
 
+#ifndef FB_THREADS_V
+#define FB_THREADS_V 256
+#endif
+constexpr int FB_THREADS = FB_THREADS_V;  // two CTAs per SM (measured: one CTA of 512 over 24K-feature blocks: the same 99 us)
 template <class Op, int H, int U>
-__global__ void __launch_bounds__(SP_THREADS) sp_ztmv_fb_kernel(Op op, FbView A, Scratch s) {
+__global__ void __launch_bounds__(FB_THREADS) sp_ztmv_fb_kernel(Op op, FbView A, Scratch s) {
   constexpr int NN = Op::NN;
   if (op.skip()) return;
   extern __shared__ double fbsm[];
   double* wsm = fbsm;          // [fb] staged w block
   double* dot = fbsm + A.fb;   // [S] running dots of the part's samples
-  __shared__ double red[(SP_THREADS / 32) * NN];
+  __shared__ double red[(FB_THREADS / 32) * NN];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int p = blockIdx.x;
   const int64_t s0 = (int64_t)p * A.S;
@@ -237,12 +399,12 @@ __global__ void __launch_bounds__(SP_THREADS) sp_ztmv_fb_kernel(Op op, FbView A,
     const int64_t j0 = (int64_t)f * A.fb;
     const int jn = (int)min((int64_t)A.fb, A.d - j0);
     __syncthreads();  // the previous block's gathers are done
-    for (int j = threadIdx.x; j < jn; j += SP_THREADS) wsm[j] = op.wval(j0 + j);
+    for (int j = threadIdx.x; j < jn; j += FB_THREADS) wsm[j] = op.wval(j0 + j);
     __syncthreads();
     const int64_t pf = (int64_t)p * A.nb + f;
     const int* sb = A.sbase + pf * (A.Q + 1);
     // H slices per warp at a time (H*U rows in flight per lane)
-    for (int q0 = H * warp; q0 < A.Q; q0 += H * (SP_THREADS / 32)) {
+    for (int q0 = H * warp; q0 < A.Q; q0 += H * (FB_THREADS / 32)) {
       int b[H], len[H], ls[H], c[H];
       double acc[H];
 #pragma unroll
@@ -285,7 +447,7 @@ __global__ void __launch_bounds__(SP_THREADS) sp_ztmv_fb_kernel(Op op, FbView A,
   double nacc[NN];
 #pragma unroll
   for (int k = 0; k < NN; ++k) nacc[k] = 0.0;
-  for (int ls = threadIdx.x; ls < ns; ls += SP_THREADS) op.row(s0 + ls, dot[ls], nacc);
+  for (int ls = threadIdx.x; ls < ns; ls += FB_THREADS) op.row(s0 + ls, dot[ls], nacc);
   if (!Op::HAS_FIN) return;
   block_sum<NN>(nacc, red);
   if (threadIdx.x == 0) {
