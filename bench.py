@@ -186,6 +186,11 @@ def kernel_bytes(tag: str, n: int, d: int, nnz: int | None = None) -> float | No
     if nnz is not None and tag.startswith("ztmv_"):
         nb = -(-d // 8192)
         return 10.0 * nnz + 4.0 * n * nb + 8.0 * (d + 6 * n)
+    if nnz is not None and tag.startswith("zmv_"):
+        # sample-blocked sliced ELL: 8-byte value + 16-bit index per entry,
+        # t staged per block, one partial per (block, feature) written
+        nb = -(-n // 12288)
+        return 10.0 * nnz + 8.0 * (2 * n + nb * d + 2 * d)
     if tag.startswith("zft_"):
         return x + 8.0 * (3 * d + 10 * n)  # X once, w in, 6 sample vectors in / 4 out, 2 d-products out
     if tag.startswith("zmv_"):
