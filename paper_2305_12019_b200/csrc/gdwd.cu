@@ -266,6 +266,14 @@ struct gdwd_ctx {
   bool use_sgs = true, stopped = false, gram = false, persistent = false;
   bool iter_gram = false;  // ITERATIVE with the d x d Gram operator (gdmat)
   bool ft = false;         // X-space loop with the fused tail pass (zft.cuh)
+  // persistent launch, configured once per solve (solve_begin); a launch made
+  // by gdwd_time_iterations is settled (stop flag read back) after its end event
+  const void* pk_kfn = nullptr;
+  size_t pk_smem = 0;
+  bool pk_pending = false, pk_defer = false;
+  int pk_kend = 0;
+  unsigned long long* pk_ts = nullptr;
+  size_t pk_tsn = 0;
   unsigned long long* ft_ts = nullptr;  // GDWD_FT_TIMING stamps (diagnostics)
   bool ps_graph = false;   // ITERATIVE body captured with device-resident PSQMR (WHILE nodes)
   cudaStream_t cap_st = nullptr;  // capture-to-graph stream for conditional bodies
@@ -899,6 +907,20 @@ static void pk_timing_report(unsigned long long* ts, size_t tsn, int version) {
   if (cudaMemcpy(h.data(), ts, tsn * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) return;
   cudaFree(ts);
   const int NP = 32;
+  if (version == 3) {  // launch prologue / epilogue: points 27 (entry), 28 (loop start), 29 (exit) in row 0
+    std::vector<double> pro, epi;
+    unsigned long long emin = ~0ull, emax = 0;
+    for (int b = 0; b < NUM_SMS; ++b) {
+      const unsigned long long* r = &h[(size_t)b * NP];
+      if (r[27] && r[28]) pro.push_back((r[28] - r[27]) / 1965.0);
+      if (r[27]) emin = std::min(emin, r[27]), emax = std::max(emax, r[27]);
+    }
+    if (!pro.empty()) {
+      std::sort(pro.begin(), pro.end());
+      fprintf(stderr, "[pk timing] launch prologue (entry -> loop) median %.2f us  slowest %.2f us\n",
+              pro[pro.size() / 2], pro.back());
+    }
+  }
   const char* names[NP] = {"top", "A arrive", "A release", "C arrive", "C release", "D arrive", "D release",
                            "E arrive", "E release", "H arrive", "H release", "H staged", "H rows", "H step3",
                            "C staged", "C rows", "C scalars", "C writeback", "C waited", "C loop",
@@ -2456,6 +2478,21 @@ static void end_session(gdwd_ctx* ctx) {
   ctx->in_solve = false;
 }
 
+// Finish a persistent launch: wait for it and read its stop flag back.
+static int pk_settle(gdwd_ctx* ctx) {
+  if (!ctx->pk_pending) return GDWD_OK;
+  ctx->pk_pending = false;
+  CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  if (ctx->pk_ts) {
+    pk_timing_report(ctx->pk_ts, ctx->pk_tsn, 3);  // (frees the buffer)
+    ctx->pk_ts = nullptr;
+  }
+  ctx->k_host = ctx->Sh->stopped ? ctx->Sh->iters_done : ctx->pk_kend;
+  ctx->stopped = ctx->Sh->stopped != 0;
+  return GDWD_OK;
+}
+
 extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const double* sched, int64_t sched_len) {
   if (!ctx || !cfg) return set_err(ctx, GDWD_ERR_VALUE, "null argument");
   if (!(ctx->has_dense || ctx->has_sparse) || !ctx->has_problem)
@@ -2467,6 +2504,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   if (cfg->mu <= 0 || cfg->ell < 1 || cfg->max_iter < 1)
     return set_err(ctx, GDWD_ERR_VALUE, "q, mu must be positive; ell, max_iter at least 1");
   CK(cudaSetDevice(ctx->device));
+  RC(pk_settle(ctx));
   end_session(ctx);
   const int64_t n = ctx->n, d = ctx->d, m = d + 1;
   const int64_t ng = ctx->n_global > 0 ? ctx->n_global : n;  // sharded: the global sample count
@@ -2644,6 +2682,37 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
     if (nb < 1 || n > (int64_t)PK_MAX_OWN * NUM_SMS) ctx->persistent = false;
     else CK(ctx->pk_part.ensure((size_t)2 * NUM_SMS * PK_NPART + 8));  // + barrier counter
   }
+  if (ctx->persistent) {
+    // own rows of K and GK resident in tensor memory when n <= 1024 (<= 7
+    // rows per CTA, 8 ceil(n/64) words per lane and row); K alone up to
+    // n = 2048, GK streamed from L2 in 8-chunk groups whose loads overlap
+    // the group's TMEM words (c2: 24.9 vs 27.0 us/iteration streaming both;
+    // a fused 16-load variant spilled in-flight registers and was slower).
+    int tmem = n <= 1024 ? 2 : (n <= 2048 ? 1 : 0);
+    if (getenv("GDWD_PK_TMEM")) {  // diagnostics: 0 L2 only, 1 K in TMEM (n <= 2048), 2 K and GK (n <= 1024)
+      const int want = atoi(getenv("GDWD_PK_TMEM"));
+      tmem = want >= 2 && n <= 1024 ? 2 : (want >= 1 && n <= 2048 ? 1 : 0);
+    }
+    const void* kfn = tmem == 2   ? (const void*)gram_smw_persistent3<2>
+                      : tmem == 1 ? (const void*)gram_smw_persistent3<1>
+                                  : (const void*)gram_smw_persistent3<0>;
+    const size_t sm = (size_t)(11 * ((n + 3) / 2 * 2)) * sizeof(double);
+    // the TMEM variants allocate all 512 columns per CTA while spinning on
+    // grid barriers: a second CTA on the same SM would block in tcgen05.alloc
+    // forever.  One CTA per SM holds today by register pressure; enforce it by
+    // padding the dynamic shared memory past half an SM if that ever changes.
+    size_t sm_launch = sm;
+    if (tmem) {
+      int nb_tm = 0;
+      CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb_tm, kfn, PK_THREADS, sm));
+      if (nb_tm > 1) sm_launch = std::max(sm, (size_t)120 * 1024);
+    }
+    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_launch));
+    ctx->pk_kfn = kfn;
+    ctx->pk_smem = sm_launch;
+    CK(cudaMemsetAsync(ctx->pk_part.p + (size_t)2 * NUM_SMS * PK_NPART, 0, sizeof(unsigned), ctx->st));
+  }
   // ITERATIVE: the whole body with device-resident PSQMR (graph WHILE nodes),
   // unsharded (an NCCL all-reduce inside a conditional body is not relied on)
   ctx->ps_graph = kind == GDWD_BACKEND_ITERATIVE && cfg->use_graph && !ctx->prof && !sharded(ctx) &&
@@ -2674,62 +2743,32 @@ extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb,
                                   int32_t* stopped_out) {
   if (!ctx || !ctx->in_solve) return set_err(ctx, GDWD_ERR_VALUE, "no solve in progress");
   CK(cudaSetDevice(ctx->device));
+  RC(pk_settle(ctx));
   const Dev& D = ctx->D;
   MatView Z = zview(ctx);
   int status = GDWD_OK;
   const int kend = std::min(ctx->max_iter, ctx->k_host + std::max(0, count));
   if (ctx->persistent && !cb && ctx->k_host < kend && !ctx->stopped) {
-    // one cooperative launch runs all requested iterations (persist.cuh)
-    unsigned long long* ts = nullptr;
-    const bool timing = getenv("GDWD_PK_TIMING") != nullptr;
-    const size_t tsn = (size_t)PK_TS_ITERS * NUM_SMS * 32;
-    if (timing) {
-      CK(cudaMalloc(&ts, tsn * sizeof(unsigned long long)));
-      CK(cudaMemset(ts, 0, tsn * sizeof(unsigned long long)));
+    // one cooperative launch runs all requested iterations (persist3.cuh)
+    if (getenv("GDWD_PK_TIMING")) {
+      ctx->pk_tsn = (size_t)PK_TS_ITERS * NUM_SMS * 32;
+      CK(cudaMalloc(&ctx->pk_ts, ctx->pk_tsn * sizeof(unsigned long long)));
+      CK(cudaMemset(ctx->pk_ts, 0, ctx->pk_tsn * sizeof(unsigned long long)));
     }
     const int diag = getenv("GDWD_PK_DIAG") ? atoi(getenv("GDWD_PK_DIAG")) : 0;
-    const size_t sm = (size_t)(11 * ((ctx->n + 3) / 2 * 2)) * sizeof(double);
     // 3 grid barriers per iteration (persist3.cuh)
-    unsigned* ctr = nullptr;
-    if (!(getenv("GDWD_PK_BAR") && atoi(getenv("GDWD_PK_BAR")) == 0)) {
+    unsigned* ctr = nullptr;  // zeroed at solve_begin; Scal.pk_bar carries its value between launches
+    if (!(getenv("GDWD_PK_BAR") && atoi(getenv("GDWD_PK_BAR")) == 0))
       ctr = reinterpret_cast<unsigned*>(ctx->pk_part.p + (size_t)2 * NUM_SMS * PK_NPART);
-      CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), ctx->st));
-    }
-    // own rows of K and GK resident in tensor memory when n <= 1024 (<= 7
-    // rows per CTA, 8 ceil(n/64) words per lane and row); K alone up to
-    // n = 2048, GK streamed from L2 in 8-chunk groups whose loads overlap
-    // the group's TMEM words (c2: 24.9 vs 27.0 us/iteration streaming both;
-    // a fused 16-load variant spilled in-flight registers and was slower).
-    int tmem = ctx->n <= 1024 ? 2 : (ctx->n <= 2048 ? 1 : 0);
-    if (getenv("GDWD_PK_TMEM")) {  // diagnostics: 0 L2 only, 1 K in TMEM (n <= 2048), 2 K and GK (n <= 1024)
-      const int want = atoi(getenv("GDWD_PK_TMEM"));
-      tmem = want >= 2 && ctx->n <= 1024 ? 2 : (want >= 1 && ctx->n <= 2048 ? 1 : 0);
-    }
     PK3Args pa{D, ctx->kmat.p, ctx->gkmat.p, D.kap, D.gam, ctx->ldm, ctx->pk_part.p, kend - ctx->k_host,
-               diag, ts, ctx->use_sgs ? 1 : 0, ctr};
+               diag, ctx->pk_ts, ctx->use_sgs ? 1 : 0, ctr};
     void* args[] = {&pa};
-    const void* kfn = tmem == 2   ? (const void*)gram_smw_persistent3<2>
-                      : tmem == 1 ? (const void*)gram_smw_persistent3<1>
-                                  : (const void*)gram_smw_persistent3<0>;
-    // the TMEM variants allocate all 512 columns per CTA while spinning on
-    // grid barriers: a second CTA on the same SM would block in tcgen05.alloc
-    // forever.  One CTA per SM holds today by register pressure; enforce it by
-    // padding the dynamic shared memory past half an SM if that ever changes.
-    size_t sm_launch = sm;
-    if (tmem) {
-      int nb_tm = 0;
-      CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb_tm, kfn, PK_THREADS, sm));
-      if (nb_tm > 1) sm_launch = std::max(sm, (size_t)120 * 1024);
-    }
-    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_launch));
     Launch L(ctx, "persistent_gram_smw2");
-    CK(cudaLaunchCooperativeKernel(kfn, dim3(NUM_SMS), dim3(PK_THREADS), args, sm_launch, ctx->st));
-    CK(cudaMemcpyAsync(ctx->Sh, ctx->S, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaStreamSynchronize(ctx->st));
-    if (ts) pk_timing_report(ts, tsn, 3);
-    ctx->k_host = ctx->Sh->stopped ? ctx->Sh->iters_done : kend;
-    ctx->stopped = ctx->Sh->stopped != 0;
+    CK(cudaLaunchCooperativeKernel(ctx->pk_kfn, dim3(NUM_SMS), dim3(PK_THREADS), args, ctx->pk_smem, ctx->st));
+    ctx->pk_pending = true;
+    ctx->pk_kend = kend;
+    ctx->k_host = kend;  // tentative until pk_settle reads the stop flag back
+    if (!ctx->pk_defer) RC(pk_settle(ctx));
   }
   // the callback of iteration k: complete its KKT record (dual objective,
   // gap, stop test), materialise w/u/rho, hand the row to the host
@@ -2849,6 +2888,7 @@ static void ft_timing_report(gdwd_ctx* ctx) {
 extern "C" int gdwd_solve_end(gdwd_ctx* ctx, gdwd_result* out) {
   if (!ctx || !ctx->in_solve || !out) return set_err(ctx, GDWD_ERR_VALUE, "no solve in progress");
   CK(cudaSetDevice(ctx->device));
+  RC(pk_settle(ctx));
   if (ctx->ft_ts) {
     cudaDeviceSynchronize();
     ft_timing_report(ctx);
@@ -3030,9 +3070,14 @@ extern "C" int gdwd_time_iterations(gdwd_ctx* ctx, int32_t count, double* ms, in
   CK(cudaEventCreate(&b));
   CK(cudaEventRecord(a, ctx->st));
   int32_t st = 0;
-  RC(gdwd_solve_iterate(ctx, count, nullptr, nullptr, iters_done, &st));
+  ctx->pk_defer = true;  // a persistent launch is read back after the end event
+  const int rc = gdwd_solve_iterate(ctx, count, nullptr, nullptr, iters_done, &st);
+  ctx->pk_defer = false;
+  RC(rc);
   CK(cudaEventRecord(b, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
+  RC(pk_settle(ctx));
+  if (iters_done) *iters_done = ctx->k_host;
   float f = 0.f;
   cudaEventElapsedTime(&f, a, b);
   cudaEventDestroy(a);

@@ -119,15 +119,39 @@ GDWD_DEV void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "
 GDWD_DEV void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // copy row `row` (length n, zero beyond n) into this warp's TMEM block at `addr`
-GDWD_DEV void tm_put_row(uint32_t addr, const double* row, int64_t n) {
+// Row into TMEM, 16 chunks' loads in flight per batch (one L2 round trip per
+// batch, not per chunk).  With x != nullptr it also returns row . x in
+// pk_row_dot<1>'s order (the same chunks, FMA chains and butterfly), so the
+// launch's K rho needs no second pass over the row.
+GDWD_DEV double tm_put_row(uint32_t addr, const double* row, int64_t n, const double* x = nullptr) {
   const int lane = threadIdx.x & 31;
   const int U = (int)((n + 63) / 64);
-  for (int u = 0; u < U; ++u) {
-    const int64_t j = 2 * lane + 64 * (int64_t)u;
-    const double2 z = j < n ? __ldg(reinterpret_cast<const double2*>(row + j)) : make_double2(0.0, 0.0);
-    tm_st4(addr + 4 * u, __double2loint(z.x), __double2hiint(z.x), __double2loint(z.y), __double2hiint(z.y));
+  constexpr int B = 16;
+  double a0 = 0.0, a1 = 0.0;
+  for (int u0 = 0; u0 < U; u0 += B) {
+    double2 z[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int64_t j = 2 * lane + 64 * (int64_t)(u0 + u);
+      z[u] = j < n ? __ldg(reinterpret_cast<const double2*>(row + j)) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      if (u0 + u < U)
+        tm_st4(addr + 4 * (u0 + u), __double2loint(z[u].x), __double2hiint(z[u].x), __double2loint(z[u].y),
+               __double2hiint(z[u].y));
+      if (x) {
+        const int64_t j = 2 * lane + 64 * (int64_t)(u0 + u);
+        const double2 xv = j < n ? *reinterpret_cast<const double2*>(x + j) : make_double2(0.0, 0.0);
+        a0 = __fma_rn(z[u].x, xv.x, a0);
+        a1 = __fma_rn(z[u].y, xv.y, a1);
+      }
+    }
   }
   tm_wait_st();
+  double v[1] = {a0 + a1};
+  if (x) warp_sum<1>(v);
+  return v[0];
 }
 
 // Row a from TMEM against NA staged vectors, row b against NB staged vectors
@@ -282,6 +306,7 @@ struct PK3Args {
 
 template <int TM>  // own rows in TMEM: 0 none, 1 K, 2 K and GK (host picks by n)
 __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A) {
+  const unsigned long long pk_entry = pk_now();
   cg::grid_group grid = cg::this_grid();
   const Dev& D = A.D;
   const int64_t n = D.n;
@@ -329,7 +354,9 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
   // Grid barrier: one release-add per CTA on a counter that only grows, then
   // an acquire poll for this barrier's target (bar.sync before and after
   // carries the ordering to and from the CTA's other threads); no fence.sc.
-  unsigned bar_target = 0;
+  // the counter only grows: this launch starts where the previous one of the
+  // solve left it (no reset between launches)
+  unsigned bar_target = A.ctr ? D.S->pk_bar : 0u;
   auto pk_bar = [&]() {
     if (!A.ctr) {
       grid.sync();
@@ -389,14 +416,16 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
     tmK = tm_base + ((uint32_t)(32 * (warp & 3)) << 16) + blk * (uint32_t)(warp >> 2);
     tmG = tmK + blk / 2;
     if (warp < nsweep) {
-      tm_put_row(tmK, A.K + (i0 + warp) * A.ld, n);
+      // K rho of the own rows with the TMEM load (see below)
+      const double kr = tm_put_row(tmK, A.K + (i0 + warp) * A.ld, n, srho);
+      if (lane == 0) o_krho[warp] = kr;
       if (TM == 2) tm_put_row(tmG, A.GK + (i0 + warp) * A.ld, n);
     }
   }
   // K rho of the own rows, swept once per launch (u, rho may have been
   // advanced outside this kernel); within the launch it follows rho's update
   // by linearity: K rho -= tau sigma mu (K w - K u), K u = s K g
-  for (int r = warp; r < nsweep; r += PK_WARPS) {
+  for (int r = TM ? nsweep : warp; r < nsweep; r += PK_WARPS) {
     const double* rows[1] = {A.K + (i0 + r) * A.ld};
     const double* xs[1] = {srho};
     double o[1];
@@ -411,6 +440,10 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
   }
   const int k_end = S.k + A.count;
   const int k_begin = S.k;
+  if (A.tstamp && threadIdx.x == 0) {
+    A.tstamp[(size_t)blockIdx.x * 32 + 27] = pk_entry;
+    A.tstamp[(size_t)blockIdx.x * 32 + 28] = pk_now();
+  }
 #define PK3_TS(pt)                                                                         \
   do {                                                                                     \
     if (A.tstamp && threadIdx.x == 0 && S.k - k_begin < PK_TS_ITERS)                       \
@@ -883,6 +916,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) gram_smw_persistent3(PK3Args A)
     G->sigma = S.sigma; G->sigma_next = S.sigma_next; G->sdual = S.sdual; G->gnorm = S.gnorm;
     G->wu2 = S.wu2; G->w2 = S.w2;
     for (int f = 0; f < 11; ++f) G->eta[f] = S.eta[f];
+    G->pk_bar = bar_target;
   }
 }
 #undef PK3_TS

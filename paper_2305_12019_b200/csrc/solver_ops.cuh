@@ -35,6 +35,7 @@ struct Scal {
   double pv[16];      // proximal: V^T v of the last projection
   double px_beta;     // proximal: beta of the current solve
   double ft_ys, ft_ya, ft_zal2;  // fused tail: y.(xi - r), y.alpha, ||Z~ alpha||^2 after Step 3
+  unsigned pk_bar, pk_pad;       // persistent kernel: grid-barrier counter value at the end of the last launch
 };
 
 constexpr int PX_MAXL = 16;  // ell - 1 <= 16 eigenvectors in the proximal operator
