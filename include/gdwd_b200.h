@@ -104,6 +104,14 @@ int gdwd_version(void);
  * Dense Z~: the CSC values array of a fully stored d x n matrix, i.e. the
  * row-major [n][d] sample matrix (SparseMatrixCSC, linalg/sparse.py:20-57). */
 int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n);
+/* Optional, before gdwd_upload_dense: the backend (GDWD_BACKEND_*) and mu the
+ * coming solve will use (SolverConfig, solver.py:101-124).  In the
+ * sample-space regimes (n <= d, n <= 2500) a page-locked upload then forms
+ * the n x n Gram (subsolvers.py:109), its Cholesky factor and explicit
+ * inverse (cholesky.py:46,60-61) block by block while the samples are still
+ * being copied; a solve with another mu refactors from the Gram.  Default:
+ * AUTO, mu = 1.  GDWD_BACKEND_ITERATIVE: Gram only. */
+int gdwd_upload_hint(gdwd_ctx* ctx, int32_t backend, double mu);
 /* Sparse Z~ in the reference's CSC layout (int64 colptr/rowidx). */
 int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx, const double* values,
                     int64_t d, int64_t n);
@@ -240,6 +248,9 @@ int gdwd_newton_sweep(int32_t device, int64_t n, const double* a, double sigma, 
 /* cholesky_factorize + explicit inverse (linalg/cholesky.py:25-66): S (m x m
  * SPD, row-major) -> S^{-1}.  GDWD_ERR_INDEFINITE on a non-positive pivot. */
 int gdwd_chol_inverse(int32_t device, const double* S, int64_t m, double* inv_out);
+/* the same inverse by the row-block (bordered) chain of the pipelined upload,
+ * `block` rows at a time */
+int gdwd_chol_inverse_bordered(int32_t device, const double* S, int64_t m, int32_t block, double* inv_out);
 /* Gram of a row-major [rows][cols] matrix X on the FP64 tensor cores:
  * sum_over_rows=1: X^T X (cols x cols, "Z Z^T" of subsolvers.py:76)
  * sum_over_rows=0: X X^T (rows x rows, "Z^T Z" of subsolvers.py:109)

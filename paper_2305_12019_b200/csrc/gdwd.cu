@@ -204,10 +204,17 @@ struct gdwd_ctx {
   double fro2 = -1.0;  // ||Z~||_F^2 (device reduction at upload)
   // overlapped dense upload (pinned source): row chunks on a copy stream,
   // the SMW Gram block-rows on a second stream as the chunks land
-  static constexpr int UP_NCH = 16;
-  cudaStream_t cst = nullptr, gst = nullptr;
-  cudaEvent_t up_ev[UP_NCH] = {}, gram_ev = nullptr, st_ev = nullptr;
-  int64_t up_r[UP_NCH + 1] = {};
+  static constexpr int UP_BLOCK = 128;  // samples per block (two Cholesky leaves)
+  static constexpr int UP_MAXB = 24;    // n <= 2500 -> at most 20 blocks
+  cudaStream_t cst = nullptr, gst = nullptr, fst = nullptr, sst = nullptr, ast = nullptr;
+  cudaEvent_t up_ev[UP_MAXB] = {}, gr_ev[UP_MAXB] = {}, gram_ev = nullptr, st_ev = nullptr, pf_ev = nullptr;
+  void* aux = nullptr;        // pooled stream / scalars / events (CtxAux)
+  void* up_aux = nullptr;     // pooled streams / events (UploadAux)
+  DevBuf pfw;                 // G | L^{-1} | scratch (n x ld each) of the bordered factorisation
+  int64_t pf_gen = -1;        // zs_gen whose G^{-1} (fac) was formed during the upload ...
+  double pf_mu2 = 0.0;        // ... for this mu^2
+  double hint_mu = 1.0;       // mu the next upload's speculative factor is built for
+  int hint_backend = GDWD_BACKEND_AUTO;
   bool up_pending = false;    // copies of the current Zs may be in flight
   int64_t zs_gen = 0;         // bumped whenever the dense Z~ (Zs) changes
   int64_t k_gen = -1;         // zs_gen whose Gram K = Z~ Z~^T (kmat) was formed at upload
@@ -996,6 +1003,98 @@ static void pk_timing_report(unsigned long long* ts, size_t tsn, int version) {
   }
 }
 
+// streams + events of the pipelined upload, pooled per device
+struct UploadAux {
+  int device = -1;
+  cudaStream_t s[5] = {};
+  cudaEvent_t e[2 * gdwd_ctx::UP_MAXB + 3] = {};
+};
+static std::mutex g_aux_mu;
+static std::vector<UploadAux*> g_aux_free;
+static UploadAux* upload_aux_acquire(int device) {
+  {
+    std::lock_guard<std::mutex> g(g_aux_mu);
+    for (size_t i = 0; i < g_aux_free.size(); ++i)
+      if (g_aux_free[i]->device == device) {
+        UploadAux* a = g_aux_free[i];
+        g_aux_free.erase(g_aux_free.begin() + i);
+        return a;
+      }
+  }
+  UploadAux* a = new UploadAux;
+  a->device = device;
+  int lo = 0, hi = 0;
+  bool ok = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&a->s[0], cudaStreamNonBlocking) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&a->s[1], cudaStreamNonBlocking) == cudaSuccess;
+  // the dependent chain is latency-bound: its CTAs go ahead of the Gram's
+  for (int i = 2; i < 5; ++i) ok = ok && cudaStreamCreateWithPriority(&a->s[i], cudaStreamNonBlocking, hi) == cudaSuccess;
+  for (auto& e : a->e) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    delete a;
+    return nullptr;
+  }
+  return a;
+}
+static void upload_aux_release(UploadAux* a) {
+  if (!a) return;
+  for (cudaStream_t x : a->s) cudaStreamSynchronize(x);
+  std::lock_guard<std::mutex> g(g_aux_mu);
+  g_aux_free.push_back(a);
+}
+
+// Per-context device/host scalars, streams and events, pooled per device:
+// contexts are created inside timed end-to-end calls, and cudaMalloc /
+// cudaMallocHost / stream and event creation cost ~0.4 ms per context.
+struct CtxAux {
+  int device = -1;
+  cudaStream_t st = nullptr, cap_st = nullptr;
+  Scal* S = nullptr;
+  Scal* Sh = nullptr;
+  int* dinfo = nullptr;
+  int* poll_flag = nullptr;
+  cudaEvent_t poll_ev[2] = {}, ev[3] = {};
+};
+static std::mutex g_ctxaux_mu;
+static std::vector<CtxAux*> g_ctxaux_free;
+static CtxAux* ctx_aux_acquire(int device) {
+  {
+    std::lock_guard<std::mutex> g(g_ctxaux_mu);
+    for (size_t i = 0; i < g_ctxaux_free.size(); ++i)
+      if (g_ctxaux_free[i]->device == device) {
+        CtxAux* a = g_ctxaux_free[i];
+        g_ctxaux_free.erase(g_ctxaux_free.begin() + i);
+        return a;
+      }
+  }
+  CtxAux* a = new CtxAux;
+  a->device = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&a->st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->cap_st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&a->S, sizeof(Scal));
+  if (e == cudaSuccess) e = cudaMallocHost(&a->Sh, sizeof(Scal));
+  if (e == cudaSuccess) e = cudaMalloc(&a->dinfo, sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost(&a->poll_flag, 2 * sizeof(int));
+  for (auto& x : a->poll_ev)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  for (auto& x : a->ev)
+    if (e == cudaSuccess) e = cudaEventCreate(&x);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "gdwd_ctx_create: %s\n", cudaGetErrorString(e));
+    delete a;  // partial resources leak; the process is unusable anyway
+    return nullptr;
+  }
+  return a;
+}
+static void ctx_aux_release(CtxAux* a) {
+  if (!a) return;
+  cudaStreamSynchronize(a->st);
+  cudaStreamSynchronize(a->cap_st);
+  std::lock_guard<std::mutex> g(g_ctxaux_mu);
+  g_ctxaux_free.push_back(a);
+}
+
 extern "C" {
 
 int gdwd_version(void) { return 1; }
@@ -1013,21 +1112,29 @@ int gdwd_ctx_create(int32_t device, gdwd_ctx** out) {
   gdwd_ctx* ctx = new gdwd_ctx();
   ctx->device = device;
   cudaError_t e = cudaSetDevice(device);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->cap_st, cudaStreamNonBlocking);
+  CtxAux* ax = e == cudaSuccess ? ctx_aux_acquire(device) : nullptr;
+  if (!ax) {
+    if (e != cudaSuccess) fprintf(stderr, "gdwd_ctx_create: %s\n", cudaGetErrorString(e));
+    delete ctx;
+    return GDWD_ERR_CUDA;
+  }
+  ctx->aux = ax;
+  ctx->st = ax->st;
+  ctx->cap_st = ax->cap_st;
+  ctx->S = ax->S;
+  ctx->Sh = ax->Sh;
+  ctx->dinfo = ax->dinfo;
+  ctx->poll_flag = ax->poll_flag;
+  ctx->poll_ev[0] = ax->poll_ev[0];
+  ctx->poll_ev[1] = ax->poll_ev[1];
+  ctx->ev_begin = ax->ev[0];
+  ctx->ev_loop = ax->ev[1];
+  ctx->ev_end = ax->ev[2];
   if (e == cudaSuccess) {
     keep_pool_reserved(device);
     for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat, &ctx->gram_ws, &ctx->sb_part})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat, &ctx->gram_ws, &ctx->sb_part, &ctx->pfw})
       b->st = ctx->st;
-  }
-  if (e == cudaSuccess) e = cudaMalloc(&ctx->S, sizeof(Scal));
-  if (e == cudaSuccess) e = cudaMallocHost(&ctx->Sh, sizeof(Scal));
-  if (e == cudaSuccess) e = cudaMalloc(&ctx->dinfo, sizeof(int));
-  if (e != cudaSuccess) {
-    fprintf(stderr, "gdwd_ctx_create: %s\n", cudaGetErrorString(e));
-    delete ctx;
-    return GDWD_ERR_CUDA;
   }
   *out = ctx;
   return GDWD_OK;
@@ -1037,27 +1144,19 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
-  if (ctx->cap_st) cudaStreamDestroy(ctx->cap_st);
   if (ctx->cst) {
     cudaStreamSynchronize(ctx->cst);
     cudaStreamSynchronize(ctx->gst);
-    for (cudaEvent_t e : ctx->up_ev) cudaEventDestroy(e);
-    cudaEventDestroy(ctx->gram_ev);
-    cudaEventDestroy(ctx->st_ev);
-    cudaStreamDestroy(ctx->cst);
-    cudaStreamDestroy(ctx->gst);
+    upload_aux_release((UploadAux*)ctx->up_aux);  // synchronises its streams
     dfree(ctx->fro2_d, ctx->st);
   }
   dfree(ctx->Zs, ctx->st);
   free_sparse(ctx);
   for (DevBuf* b : {&ctx->y, &ctx->e, &ctx->wl, &ctx->part, &ctx->npart, &ctx->tpart, &ctx->nvec, &ctx->mvec,
-                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat, &ctx->gram_ws, &ctx->sb_part})
+                    &ctx->tabs, &ctx->histb, &ctx->fac, &ctx->facw, &ctx->colsq, &ctx->tbuf, &ctx->kmat, &ctx->pk_part, &ctx->gkmat, &ctx->bundle, &ctx->pxbuf, &ctx->gdmat, &ctx->gram_ws, &ctx->sb_part, &ctx->pfw})
     b->release();
   end_session(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
-  for (cudaEvent_t e : {ctx->ev_begin, ctx->ev_loop, ctx->ev_end, ctx->poll_ev[0], ctx->poll_ev[1]})
-    if (e) cudaEventDestroy(e);
-  if (ctx->poll_flag) cudaFreeHost(ctx->poll_flag);
   if (ctx->bundle_h) cudaFreeHost(ctx->bundle_h);
   if (ctx->comm && nccl::api().ok) nccl::api().CommDestroy(ctx->comm);
   for (int b = 0; b < 2; ++b) {
@@ -1065,11 +1164,192 @@ void gdwd_ctx_destroy(gdwd_ctx* ctx) {
     if (ctx->pin_ev[b]) cudaEventDestroy(ctx->pin_ev[b]);
   }
   dfree(ctx->tickets, ctx->st);
-  if (ctx->S) cudaFree(ctx->S);
-  if (ctx->Sh) cudaFreeHost(ctx->Sh);
-  if (ctx->dinfo) cudaFree(ctx->dinfo);
-  if (ctx->st) cudaStreamDestroy(ctx->st);
+  ctx_aux_release((CtxAux*)ctx->aux);  // synchronises st (the frees above are ordered on it)
   delete ctx;
+}
+
+static int select_kind(int64_t n, int64_t d);
+
+
+// Page-locked dense upload in the sample-space regimes, pipelined with the
+// one-time factorisation (subsolvers.py:109-113, cholesky.py:46,60-61): block
+// b of samples is copied (contiguous rows) on cst; gst then forms its rows of
+// K = Z~^T Z~ (DMMA, split-K partials summed in slice order) and of
+// G = K/mu^2 + I; fst advances the bordered Cholesky factor -- the block's
+// rows of L^{-1} from the rows before -- with the half that does not need the
+// diagonal block on sst, and ast adds the block's term of
+// G^{-1} = L^{-T} L^{-1}.  Only the last block's share runs after the last
+// byte has landed.  mu comes from the upload hint (default 1); a solve with
+// another mu, or outside the sample-space regimes, refactors from K.
+static int upload_dense_pipelined(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n, int64_t ld) {
+  const auto t_pre0 = std::chrono::steady_clock::now();
+  if (!ctx->cst) {
+    // streams and events come from a process-wide pool (contexts are created
+    // inside timed end-to-end calls; creating 5 streams + 51 events is ~0.25 ms)
+    UploadAux* ax = upload_aux_acquire(ctx->device);
+    if (!ax) return set_err(ctx, GDWD_ERR_CUDA, "upload streams");
+    ctx->up_aux = ax;
+    ctx->cst = ax->s[0]; ctx->gst = ax->s[1]; ctx->fst = ax->s[2]; ctx->sst = ax->s[3]; ctx->ast = ax->s[4];
+    for (int i = 0; i < gdwd_ctx::UP_MAXB; ++i) {
+      ctx->up_ev[i] = ax->e[i];
+      ctx->gr_ev[i] = ax->e[gdwd_ctx::UP_MAXB + i];
+    }
+    ctx->gram_ev = ax->e[2 * gdwd_ctx::UP_MAXB];
+    ctx->st_ev = ax->e[2 * gdwd_ctx::UP_MAXB + 1];
+    ctx->pf_ev = ax->e[2 * gdwd_ctx::UP_MAXB + 2];
+    ctx->fro2_h = pinned_slot();
+    CK(dmalloc((void**)&ctx->fro2_d, sizeof(double), ctx->st));
+  }
+  // factor only where the solve will run in sample space (gdwd_solve_begin:
+  // SMW2 with n <= d, DIRECT with 2n <= d)
+  int hk = ctx->hint_backend == GDWD_BACKEND_AUTO ? select_kind(n, d) : ctx->hint_backend;
+  const bool factor = (hk == GDWD_BACKEND_SMW2 || (hk == GDWD_BACKEND_DIRECT && 2 * n <= d)) &&
+                      getenv("GDWD_UPLOAD_FACTOR") == nullptr;
+  const double mu2 = ctx->hint_mu * ctx->hint_mu;
+  const int64_t ldk = (n + 1) / 2 * 2;
+  int64_t mb = gdwd_ctx::UP_BLOCK;
+  if (const char* ev = getenv("GDWD_UP_BLOCK")) mb = std::max(16, atoi(ev));
+  // the work a block triggers grows with the rows before it, and what runs
+  // after the last byte is the last block's share: the last `fine` rows go in
+  // half-size blocks
+  int64_t fine = 2 * mb;
+  if (const char* ev = getenv("GDWD_UP_FINE")) fine = std::max(0, atoi(ev));
+  while ((n + mb - 1) / mb + fine / mb > gdwd_ctx::UP_MAXB) mb += 64;
+  int64_t rb[gdwd_ctx::UP_MAXB + 1];
+  int nblk = 0;
+  rb[0] = 0;
+  while (rb[nblk] < n) {
+    const int64_t left = n - rb[nblk];
+    const int64_t step = (left <= fine && mb >= 32) ? mb / 2 : mb;
+    rb[nblk + 1] = std::min<int64_t>(n, rb[nblk] + step);
+    ++nblk;
+  }
+  const auto t_pre1 = std::chrono::steady_clock::now();
+  CK(ctx->kmat.ensure((size_t)n * ldk));
+  CK(ctx->fac.ensure((size_t)n * ldk));
+  const int64_t bws = bordered_workspace(n, mb);
+  CK(ctx->pfw.ensure((size_t)3 * n * ldk + (size_t)bws));
+  CK(ctx->gram_ws.ensure((size_t)std::max(gram_rowblock_workspace(n, d, mb),
+                                          gram_rowblock_workspace(n, d, std::max<int64_t>(mb / 2, 1)))));
+  double* G = ctx->pfw.p;
+  double* Wi = G + (size_t)n * ldk;
+  double* T = Wi + (size_t)n * ldk;
+  // zero: K's pad column (the persistent kernel's paired loads read it),
+  // L^{-1}'s upper triangle, the accumulated G^{-1}
+  CK(cudaMemsetAsync(ctx->kmat.p, 0, (size_t)n * ldk * sizeof(double), ctx->st));
+  if (factor) {
+    CK(cudaMemsetAsync(Wi, 0, (size_t)n * ldk * sizeof(double), ctx->st));
+    CK(cudaMemsetAsync(ctx->fac.p, 0, (size_t)n * ldk * sizeof(double), ctx->st));
+    CK(cudaMemsetAsync(ctx->dinfo, 0, sizeof(int), ctx->st));
+  }
+  CK(cudaEventRecord(ctx->st_ev, ctx->st));  // allocation / pad memsets first
+  for (cudaStream_t x : {ctx->cst, ctx->gst, ctx->fst, ctx->ast}) CK(cudaStreamWaitEvent(x, ctx->st_ev, 0));
+  const size_t row_b = (size_t)d * sizeof(double);
+  const bool tmark = getenv("GDWD_SETUP_TIMING") != nullptr;
+  // GDWD_SETUP_TIMING: device timeline (ms after the first copy starts) of
+  // each block's copy / Gram rows / factor rows / G^{-1} term
+  std::vector<cudaEvent_t> tl[4];
+  cudaEvent_t tl0 = nullptr;
+  auto tev = [&](int lane, int, cudaStream_t x) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, x);
+    tl[lane].push_back(e);
+  };
+  if (tmark) {
+    cudaEventCreate(&tl0);
+    cudaEventRecord(tl0, ctx->cst);
+  }
+  const auto t_h0 = std::chrono::steady_clock::now();
+  // every copy is queued before any compute launch, so the copy engine never
+  // waits for the host
+  for (int b = 0; b < nblk; ++b) {
+    const int64_t r0 = rb[b], r1 = rb[b + 1];
+    if (ld == d)
+      CK(cudaMemcpyAsync(ctx->Zs + r0 * ld, samples + r0 * d, (size_t)(r1 - r0) * row_b, cudaMemcpyHostToDevice,
+                         ctx->cst));
+    else
+      CK(cudaMemcpy2DAsync(ctx->Zs + r0 * ld, ld * sizeof(double), samples + r0 * d, row_b, row_b, r1 - r0,
+                           cudaMemcpyHostToDevice, ctx->cst));
+    CK(cudaEventRecord(ctx->up_ev[b], ctx->cst));
+    if (tmark) tev(0, b, ctx->cst);
+  }
+  const auto t_h1 = std::chrono::steady_clock::now();
+  for (int b = 0; b < nblk; ++b) {
+    const int64_t r0 = rb[b], r1 = rb[b + 1];
+    CK(cudaStreamWaitEvent(ctx->gst, ctx->up_ev[b], 0));
+    CK(gram_rowblock(ctx->Zs, ld, d, r0, r1, ctx->kmat.p, ldk, G, ldk, mu2, ctx->gram_ws.p, ctx->gst));
+    if (tmark) tev(1, b, ctx->gst);
+    if (factor) {
+      CK(cudaEventRecord(ctx->gr_ev[b], ctx->gst));
+      CK(cudaStreamWaitEvent(ctx->fst, ctx->gr_ev[b], 0));
+      CK(bordered_chol_step(G, Wi, T, ctx->fac.p, ldk, r0, r1, ctx->dinfo, ctx->fst, ctx->sst, ctx->ast,
+                            T + (size_t)n * ldk, bws));
+      if (tmark) tev(2, b, ctx->fst);
+      if (tmark) tev(3, b, ctx->ast);
+    }
+  }
+  const auto t_h2 = std::chrono::steady_clock::now();
+  ctx->up_pending = true;
+  ctx->n = n;
+  ctx->d = d;
+  ctx->ldz = ld;
+  ctx->has_dense = true;
+  ctx->has_problem = false;
+  ctx->data_gen++;
+  ctx->zs_gen++;
+  ctx->k_gen = ctx->zs_gen;
+  RC(ensure_scratch(ctx, n, d));  // may synchronise st: before st starts waiting for the copies
+  CK(cudaStreamWaitEvent(ctx->st, ctx->up_ev[nblk - 1], 0));
+  run_vm(ctx, OpSumSq{ctx->Zs, d, ld, ctx->fro2_d}, n * d, "vmap_fro2", false);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(ctx->fro2_h, ctx->fro2_d, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+  ctx->fro2_pending = true;
+  // everything later on st sees the whole K (and G^{-1})
+  CK(cudaEventRecord(ctx->gram_ev, ctx->gst));
+  CK(cudaStreamWaitEvent(ctx->st, ctx->gram_ev, 0));
+  if (factor) {
+    CK(mirror_lower(ctx->fac.p, ldk, n, ctx->ast));
+    CK(cudaEventRecord(ctx->pf_ev, ctx->ast));
+    CK(cudaStreamWaitEvent(ctx->st, ctx->pf_ev, 0));
+    ctx->pf_gen = ctx->zs_gen;
+    ctx->pf_mu2 = mu2;
+  }
+  // the host buffer is only borrowed for the call: wait for the copies (the
+  // Gram rows, the factor chain and the norm may still be running)
+  const auto t_h3 = std::chrono::steady_clock::now();
+  finish_upload(ctx);
+  if (tmark) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t_h4 = std::chrono::steady_clock::now();
+    for (cudaStream_t x : {ctx->gst, ctx->fst, ctx->ast}) cudaStreamSynchronize(x);
+    const auto t_h5 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[upload timing] streams/events %.3f, buffers %.3f ms\n", ms(t_pre0, t_pre1), ms(t_pre1, t_h0));
+    fprintf(stderr, "[upload timing] queue copies %.3f, queue compute %.3f, rest %.3f, wait copies %.3f, "
+            "compute tail after the last byte %.3f ms (%d blocks of %lld)\n", ms(t_h0, t_h1), ms(t_h1, t_h2),
+            ms(t_h2, t_h3), ms(t_h3, t_h4), ms(t_h4, t_h5), nblk, (long long)mb);
+    const char* names[4] = {"copy", "gram", "chain", "ginv"};
+    for (int l = 0; l < 4; ++l) {
+      fprintf(stderr, "[upload timeline] %-5s", names[l]);
+      for (cudaEvent_t e : tl[l]) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, tl0, e);
+        fprintf(stderr, " %.2f", t);
+        cudaEventDestroy(e);
+      }
+      fprintf(stderr, "\n");
+    }
+    cudaEventDestroy(tl0);
+  }
+  return GDWD_OK;
+}
+
+int gdwd_upload_hint(gdwd_ctx* ctx, int32_t backend, double mu) {
+  if (!ctx || !(mu > 0.0) || backend < GDWD_BACKEND_AUTO || backend > GDWD_BACKEND_ITERATIVE)
+    return set_err(ctx, GDWD_ERR_VALUE, "bad upload hint");
+  ctx->hint_backend = backend;
+  ctx->hint_mu = mu;
+  return GDWD_OK;
 }
 
 int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n) {
@@ -1082,79 +1362,17 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
   CK(dmalloc((void**)&ctx->Zs, (size_t)n * ld * sizeof(double), ctx->st));
   if (ld != d) CK(cudaMemsetAsync(ctx->Zs, 0, (size_t)n * ld * sizeof(double), ctx->st));
   // Sample-space regimes (n <= 2500, n <= d: SMW2, DIRECT with 2n <= d) with
-  // a page-locked source: the matrix is copied in UP_NCH feature-column
-  // chunks on a copy stream while the Gram consumes each chunk as it lands
-  // (second stream); ctx->st waits for the last copy and the Gram, so every
-  // other consumer sees the whole matrix.  ||Z~||_F^2 is reduced on st and
-  // read lazily.
+  // a page-locked source: the matrix is copied in blocks of samples
+  // (contiguous rows) on a copy stream; as each block lands, a second stream
+  // forms its rows of the n x n Gram K = Z~^T Z~ and of G = K/mu^2 + I, and a
+  // third advances the bordered Cholesky factor and L^{-1} by that block, so
+  // K, G^{-1} are ready shortly after the last byte (upload_dense_pipelined).
   cudaPointerAttributes pa{};
   const bool pinned = cudaPointerGetAttributes(&pa, samples) == cudaSuccess && pa.type == cudaMemoryTypeHost;
   cudaGetLastError();
   finish_upload(ctx);
-  if (pinned && n <= 2500 && n <= d && d >= 4 * gdwd_ctx::UP_NCH && !sharded(ctx) && !getenv("GDWD_UPLOAD")) {
-    if (!ctx->cst) {
-      CK(cudaStreamCreateWithFlags(&ctx->cst, cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&ctx->gst, cudaStreamNonBlocking));
-      for (auto& e : ctx->up_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&ctx->gram_ev, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&ctx->st_ev, cudaEventDisableTiming));
-      ctx->fro2_h = pinned_slot();
-      CK(dmalloc((void**)&ctx->fro2_d, sizeof(double), ctx->st));
-    }
-    CK(cudaEventRecord(ctx->st_ev, ctx->st));  // allocation / pad memset first
-    CK(cudaStreamWaitEvent(ctx->cst, ctx->st_ev, 0));
-    const size_t row_b = (size_t)d * sizeof(double);
-    // In the sample-space regimes (n <= 2500, n <= d: SMW2, DIRECT with 2n <=
-    // d) the n x n Gram K = Z~ Z~^T is formed here on a second stream as the
-    // chunks land: the chunks are feature columns, so each adds its own
-    // K_c = Z~[:, c] Z~[:, c]^T (DMMA SYRK) to K in chunk order.
-    const bool gram = true;
-    const int64_t ldk = (n + 1) / 2 * 2;
-    const int64_t cw = (d + gdwd_ctx::UP_NCH - 1) / gdwd_ctx::UP_NCH;
-    for (int c = 0; c <= gdwd_ctx::UP_NCH; ++c) ctx->up_r[c] = std::min<int64_t>(d, cw * c);
-    if (gram) {
-      CK(ctx->kmat.ensure((size_t)n * ldk));
-      CK(cudaMemsetAsync(ctx->kmat.p, 0, (size_t)n * ldk * sizeof(double), ctx->st));
-      CK(ctx->gram_ws.ensure((size_t)gram_workspace_doubles(n, cw)));
-      CK(cudaEventRecord(ctx->st_ev, ctx->st));
-      CK(cudaStreamWaitEvent(ctx->gst, ctx->st_ev, 0));
-    }
-    for (int c = 0; c < gdwd_ctx::UP_NCH; ++c) {
-      const int64_t c0 = ctx->up_r[c], c1 = ctx->up_r[c + 1];
-      if (c1 > c0)
-        CK(cudaMemcpy2DAsync(ctx->Zs + c0, ld * sizeof(double), samples + c0, row_b, (c1 - c0) * sizeof(double), n,
-                             cudaMemcpyHostToDevice, ctx->cst));
-      CK(cudaEventRecord(ctx->up_ev[c], ctx->cst));
-      if (gram && c1 > c0) {
-        CK(cudaStreamWaitEvent(ctx->gst, ctx->up_ev[c], 0));
-        CK(gram_syrk(ctx->Zs + c0, n, c1 - c0, ld, false, 1.0, 0.0, ctx->kmat.p, ldk, ctx->gram_ws.p, ctx->gst,
-                     c > 0));
-      }
-    }
-    CK(cudaStreamWaitEvent(ctx->st, ctx->up_ev[gdwd_ctx::UP_NCH - 1], 0));
-    if (gram) {
-      CK(cudaEventRecord(ctx->gram_ev, ctx->gst));
-      CK(cudaStreamWaitEvent(ctx->st, ctx->gram_ev, 0));
-    }
-    ctx->up_pending = true;
-    ctx->n = n;
-    ctx->d = d;
-    ctx->ldz = ld;
-    ctx->has_dense = true;
-    ctx->has_problem = false;
-    ctx->data_gen++;
-    ctx->zs_gen++;
-    ctx->k_gen = gram ? ctx->zs_gen : -1;
-    RC(ensure_scratch(ctx, n, d));
-    run_vm(ctx, OpSumSq{ctx->Zs, d, ld, ctx->fro2_d}, n * d, "vmap_fro2", false);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(ctx->fro2_h, ctx->fro2_d, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
-    ctx->fro2_pending = true;
-    // the host buffer is only borrowed for the call: wait for the copies
-    // (the Gram block-rows and the norm may still be running)
-    finish_upload(ctx);
-    return GDWD_OK;
-  }
+  if (pinned && n <= 2500 && n <= d && d >= 64 && !sharded(ctx) && !getenv("GDWD_UPLOAD"))
+    return upload_dense_pipelined(ctx, samples, d, n, ld);
   RC(upload_rows(ctx, samples, d, n, ld));
   ctx->zs_gen++;
   ctx->n = n;
@@ -1820,12 +2038,17 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
     T.mark("densify");
     const int64_t m = (kind == GDWD_BACKEND_DIRECT) ? d + 1 : n;
     const int64_t ld = (m + 1) / 2 * 2;
-    CK(ctx->fac.ensure((size_t)m * ld));
-    CK(cudaMemsetAsync(ctx->fac.p, 0, (size_t)m * ld * sizeof(double), ctx->st));
+    // G^{-1} already formed block by block during the upload (same data, same mu)
+    const bool pf = kind == GDWD_BACKEND_SMW2 && ctx->pf_gen == ctx->zs_gen && ctx->pf_mu2 == mu2 &&
+                    ctx->k_gen == ctx->zs_gen;
+    if (!pf) {
+      CK(ctx->fac.ensure((size_t)m * ld));
+      CK(cudaMemsetAsync(ctx->fac.p, 0, (size_t)m * ld * sizeof(double), ctx->st));
+    }
     const int64_t K = (kind == GDWD_BACKEND_DIRECT) ? n : d;
     const int64_t M = (kind == GDWD_BACKEND_DIRECT) ? d : n;
     size_t ws = std::max<size_t>((size_t)gram_workspace_doubles(M, K), (size_t)2 * m * ld);
-    CK(ctx->facw.ensure(ws));
+    if (!pf) CK(ctx->facw.ensure(ws));
     if (kind == GDWD_BACKEND_DIRECT) {
       if (sharded(ctx)) {
         // local Z_p Z_p^T, summed over the shards once (8 MB at d=1000), then + mu^2 I
@@ -1849,13 +2072,18 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
         CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, false, 1.0, 0.0, ctx->kmat.p, ld, ctx->facw.p, ctx->st));
       }
       T.mark("gram K = Z^T Z");
-      g_from_k_kernel<<<vm_grid(m * m), 256, 0, ctx->st>>>(ctx->kmat.p, ctx->fac.p, m, ld, mu2);
-      CK(cudaGetLastError());
-      T.mark("G = K/mu^2 + I");
+      if (!pf) {
+        g_from_k_kernel<<<vm_grid(m * m), 256, 0, ctx->st>>>(ctx->kmat.p, ctx->fac.p, m, ld, mu2);
+        CK(cudaGetLastError());
+        T.mark("G = K/mu^2 + I");
+      }
     }
-    CK(cudaMemsetAsync(ctx->dinfo, 0, sizeof(int), ctx->st));
-    CK(chol_inverse(ctx->fac.p, ctx->facw.p, ctx->facw.p + (size_t)m * ld, ld, m, ctx->dinfo, ctx->st));
-    T.mark("cholesky inverse");
+    if (!pf) {
+      CK(cudaMemsetAsync(ctx->dinfo, 0, sizeof(int), ctx->st));
+      CK(chol_inverse(ctx->fac.p, ctx->facw.p, ctx->facw.p + (size_t)m * ld, ld, m, ctx->dinfo, ctx->st));
+      T.mark("cholesky inverse");
+    }
+    ctx->pf_gen = -1;  // fac now belongs to this factorisation (a later refactor overwrites it)
     int info = 0;
     CK(cudaMemcpyAsync(&info, ctx->dinfo, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
@@ -3207,6 +3435,45 @@ extern "C" int gdwd_chol_inverse(int32_t device, const double* Sm, int64_t m, do
   CK(cudaMemcpy(&h, info, sizeof(int), cudaMemcpyDeviceToHost));
   if (h) return GDWD_ERR_INDEFINITE;
   CK(cudaMemcpy2D(inv_out, m * 8, A, ld * 8, m * 8, m, cudaMemcpyDeviceToHost));
+  return GDWD_OK;
+}
+
+// The same inverse by the bordered (row-block) chain the pipelined upload
+// runs: blocks of `block` rows, three streams as in upload_dense_pipelined.
+extern "C" int gdwd_chol_inverse_bordered(int32_t device, const double* Sm, int64_t m, int32_t block,
+                                          double* inv_out) {
+  gdwd_ctx* ctx = nullptr;
+  if (m < 1 || block < 1 || !Sm || !inv_out) return GDWD_ERR_VALUE;
+  if (cudaSetDevice(device) != cudaSuccess) return GDWD_ERR_CUDA;
+  Tmp t;
+  const int64_t ld = (m + 1) / 2 * 2;
+  double* A = t.alloc<double>((size_t)m * ld);
+  const int64_t bws = bordered_workspace(m, block);
+  double* W = t.alloc<double>((size_t)3 * m * ld + (size_t)bws);
+  int* info = t.alloc<int>(1);
+  if (!A || !W || !info) return GDWD_ERR_CUDA;
+  double* Wi = W;
+  double* T = W + (size_t)m * ld;
+  double* Ginv = W + (size_t)2 * m * ld;
+  CK(cudaMemcpy2D(A, ld * 8, Sm, m * 8, m * 8, m, cudaMemcpyHostToDevice));
+  CK(cudaMemset(info, 0, sizeof(int)));
+  CK(cudaMemset(W, 0, (size_t)3 * m * ld * 8));
+  cudaStream_t s3[3];
+  for (auto& x : s3) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+  cudaError_t e = cudaSuccess;
+  for (int64_t r0 = 0; r0 < m && e == cudaSuccess; r0 += block)
+    e = bordered_chol_step(A, Wi, T, Ginv, ld, r0, std::min<int64_t>(m, r0 + block), info, s3[0], s3[1], s3[2],
+                           W + (size_t)3 * m * ld, bws);
+  if (e == cudaSuccess) e = mirror_lower(Ginv, ld, m, s3[2]);
+  for (auto& x : s3) {
+    cudaStreamSynchronize(x);
+    cudaStreamDestroy(x);
+  }
+  CK(e);
+  int h = 0;
+  CK(cudaMemcpy(&h, info, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h) return GDWD_ERR_INDEFINITE;
+  CK(cudaMemcpy2D(inv_out, m * 8, Ginv, ld * 8, m * 8, m, cudaMemcpyDeviceToHost));
   return GDWD_OK;
 }
 

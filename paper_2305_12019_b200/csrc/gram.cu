@@ -397,19 +397,89 @@ cudaError_t gemm_f64(const double* a, int64_t sam, int64_t sak, const double* b,
   return cudaGetLastError();
 }
 
+namespace {
+// C = beta C + alpha sum_z W[z] (slice order), tiles above the diagonal
+// untouched when only the lower ones were computed
+__global__ void splitk_finish_kernel(const double* W, int64_t wslice, int nslice, int64_t M, int64_t N, double alpha,
+                                     double beta, double* C, int64_t ldc, int lower) {
+  const int64_t tot = M * N;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / N, j = idx % N;
+    if (lower && j / BN > i / BM) continue;
+    double s = 0.0;
+    for (int z = 0; z < nslice; ++z) s += W[z * wslice + idx];
+    double* cp = C + i * ldc + j;
+    *cp = (beta == 0.0) ? alpha * s : beta * *cp + alpha * s;
+  }
+}
+}  // namespace
+
+// gemm_f64 for few output tiles and a long K (the bordered chain's products):
+// K is split over grid.z so that the GPU fills, partials go to W (capacity
+// wcap doubles) and are summed in slice order.  Falls back to one slice.
+cudaError_t gemm_f64_splitk(const double* a, int64_t sam, int64_t sak, const double* b, int64_t sbn, int64_t sbk,
+                            int64_t M, int64_t N, int64_t K, double alpha, double beta, double* C, int64_t ldc,
+                            cudaStream_t st, int tri, double* W, int64_t wcap) {
+  const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
+  const int64_t tiles = (tri & GEMM_C_LOWER) ? tm * (tm + 1) / 2 : tm * tn;
+  int64_t ns = (148 * 2 + tiles - 1) / tiles;
+  const int64_t kmax = (K + 63) / 64;  // >= 64 of K per slice
+  if (ns > kmax) ns = kmax;
+  if (ns > 32) ns = 32;
+  if (W == nullptr || ns * M * N > wcap) ns = wcap / (M * N);
+  if (ns <= 1 || W == nullptr) return gemm_f64(a, sam, sak, b, sbn, sbk, M, N, K, alpha, beta, C, ldc, st, tri);
+  int64_t kslice = (K + ns - 1) / ns;
+  kslice = (kslice + BK - 1) / BK * BK;
+  ns = (K + kslice - 1) / kslice;
+  dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)ns);
+  Opnd A{a, sam, sak}, B{b, sbn, sbk};
+  const bool ak = (sak == 1), bk = (sbk == 1);
+  if (ak && bk)
+    gemm_dmma_kernel<true, true><<<grid, GT, 0, st>>>(A, B, M, N, K, kslice, W, N, M * N, false, 1.0, 0.0, nullptr, 0, tri);
+  else if (ak)
+    gemm_dmma_kernel<true, false><<<grid, GT, 0, st>>>(A, B, M, N, K, kslice, W, N, M * N, false, 1.0, 0.0, nullptr, 0, tri);
+  else if (bk)
+    gemm_dmma_kernel<false, true><<<grid, GT, 0, st>>>(A, B, M, N, K, kslice, W, N, M * N, false, 1.0, 0.0, nullptr, 0, tri);
+  else
+    gemm_dmma_kernel<false, false><<<grid, GT, 0, st>>>(A, B, M, N, K, kslice, W, N, M * N, false, 1.0, 0.0, nullptr, 0,
+                                                        tri);
+  splitk_finish_kernel<<<grid_for(M * N), 256, 0, st>>>(W, M * N, (int)ns, M, N, alpha, beta, C, ldc,
+                                                        (tri & GEMM_C_LOWER) != 0);
+  return cudaGetLastError();
+}
+
 int64_t gram_workspace_doubles(int64_t M, int64_t K) {
   int nslice = gram_slices(M, K);
   return (int64_t)nslice * M * M;
 }
 
+// Split-K factor for `tiles` output tiles: the kernel is resident at 2 CTAs
+// per SM (120 registers x 256 threads), i.e. 296 at once; pick the slice
+// count whose CTA total fills whole waves best (>= kmin of K per slice, at
+// least ~2 waves when K allows so the tail wave is a small share), smallest
+// such count on ties.
+static int pick_slices(int64_t tiles, int64_t K, int64_t kmin, int smax) {
+  const int64_t slots = 2 * 148;
+  int64_t kmax = (K + kmin - 1) / kmin;
+  if (kmax > smax) kmax = smax;
+  if (kmax < 1) kmax = 1;
+  int best = 1;
+  double best_eff = -1.0;
+  for (int64_t s = 1; s <= kmax; ++s) {
+    const int64_t ctas = tiles * s, waves = (ctas + slots - 1) / slots;
+    double eff = (double)ctas / (double)(waves * slots);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = (int)s;
+    }
+  }
+  return best;
+}
+
 int gram_slices(int64_t M, int64_t K) {
   const int64_t tiles = ((M + BM - 1) / BM) * ((M + BM - 1) / BM + 1) / 2;
-  int64_t s = (148 * 3 + tiles - 1) / tiles;  // aim for >= 3 CTAs per SM
-  int64_t kmax = (K + 255) / 256;             // keep >= 256 K per slice
-  if (s > kmax) s = kmax;
-  if (s > 64) s = 64;
-  if (s < 1) s = 1;
-  return (int)s;
+  return pick_slices(tiles, K, 512, 16);
 }
 
 // Symmetric Gram of the rows/columns of a row-major [R x L] matrix Zs:
@@ -531,6 +601,147 @@ cudaError_t chol_inverse(double* A, double* Li, double* T, int64_t ld, int64_t m
   // tiles on the DMMA SYRK path, mirrored (T is the workspace)
   if (gram_slices(m, m) == 1) return gram_syrk(Li, m, m, ld, true, 1.0, 0.0, A, ld, T, st);
   return gemm_f64(Li, 1, ld, Li, 1, ld, m, m, m, 1.0, 0.0, A, ld, st, GEMM_A_KGE_M | GEMM_B_KGE_N);
+}
+
+// ---------------------------------------------------------------------------
+// Row-block (bordered) forms: the n x n sample-space Gram, its Cholesky
+// factor and the explicit inverse advance one block of samples at a time, so
+// they run while the remaining samples are still being copied to the device
+// (gdwd.cu: upload_dense_pipelined).  Same quantities as gram_syrk +
+// chol_inverse (subsolvers.py:109, cholesky.py:46,60-61), other association.
+// ---------------------------------------------------------------------------
+namespace {
+
+int rowblock_slices(int64_t mb, int64_t r1, int64_t K) {
+  const int64_t tiles = ((mb + BM - 1) / BM) * ((r1 + BN - 1) / BN);
+  return pick_slices(tiles, K, 256, 64);
+}
+
+// Sum the split-K partials of block rows r0..r1 in slice order; the diagonal
+// block takes (min, max) so K stays exactly symmetric.  Writes K's rows and
+// their mirror, and G = K / mu2 + I on the rows (columns < r1).
+__global__ void rowblock_finish_kernel(const double* W, int64_t wslice, int nslice, int64_t r0, int64_t r1,
+                                       double* K, int64_t ldk, double* G, int64_t ldg, double mu2) {
+  const int64_t mb = r1 - r0, tot = mb * r1;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / r1, j = idx % r1;
+    int64_t a = i, b = j;
+    if (j >= r0 && j - r0 < i) { a = j - r0; b = r0 + i; }
+    double s = 0.0;
+    for (int z = 0; z < nslice; ++z) s += W[z * wslice + a * r1 + b];
+    K[(r0 + i) * ldk + j] = s;
+    if (j < r0) K[j * ldk + r0 + i] = s;
+    const double g = (mu2 == 1.0) ? s : s / mu2;
+    G[(r0 + i) * ldg + j] = (j == r0 + i) ? g + 1.0 : g;
+  }
+}
+
+__global__ void mirror_lower_kernel(double* A, int64_t ld, int64_t m) {
+  const int64_t tot = m * m;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / m, j = idx % m;
+    if (j > i) A[i * ld + j] = A[j * ld + i];
+  }
+}
+
+}  // namespace
+
+int64_t gram_rowblock_workspace(int64_t n, int64_t d, int64_t mb) {
+  int64_t best = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += mb) {
+    const int64_t r1 = r0 + mb < n ? r0 + mb : n;
+    const int64_t need = (int64_t)rowblock_slices(r1 - r0, r1, d) * (r1 - r0) * r1;
+    if (need > best) best = need;
+  }
+  return best;
+}
+
+// K[r0:r1, 0:r1] = Zs[r0:r1] Zs[0:r1]^T over the d feature columns (row-major
+// samples, ldz), mirrored into K[0:r0, r0:r1]; G rows = K / mu2 + I.
+cudaError_t gram_rowblock(const double* Zs, int64_t ldz, int64_t d, int64_t r0, int64_t r1, double* K, int64_t ldk,
+                          double* G, int64_t ldg, double mu2, double* W, cudaStream_t st) {
+  const int64_t mb = r1 - r0;
+  const int ns = rowblock_slices(mb, r1, d);
+  int64_t kslice = (d + ns - 1) / ns;
+  kslice = (kslice + BK - 1) / BK * BK;
+  dim3 grid((unsigned)((r1 + BN - 1) / BN), (unsigned)((mb + BM - 1) / BM), (unsigned)ns);
+  Opnd A{Zs + r0 * ldz, ldz, 1}, B{Zs, ldz, 1};
+  gemm_dmma_kernel<true, true><<<grid, GT, 0, st>>>(A, B, mb, r1, d, kslice, W, r1, mb * r1, false, 1.0, 0.0, nullptr,
+                                                    0);
+  rowblock_finish_kernel<<<grid_for(mb * r1), 256, 0, st>>>(W, mb * r1, ns, r0, r1, K, ldk, G, ldg, mu2);
+  return cudaGetLastError();
+}
+
+// One bordered step: rows r0..r1 of L^{-1} (into Wi) from the block's rows of
+// G and the r0 rows of L^{-1} already there, then Ginv's lower triangle
+// += Wi[r0:r1, 0:r1]^T Wi[r0:r1, 0:r1].
+//   G rows: consumed (scratch afterwards); T rows r0..r1: scratch.
+//   chain carries the dependent sequence, side the half of the inverse row
+//   that does not need the diagonal factor, acc the rank-mb update.
+cudaError_t bordered_chol_step(double* G, double* Wi, double* T, double* Ginv, int64_t ld, int64_t r0, int64_t r1,
+                               int* info, cudaStream_t chain, cudaStream_t side, cudaStream_t acc, double* ws,
+                               int64_t wcap) {
+  // split-K workspaces: one for the chain's products, one for the side stream's
+  double* ws_chain = ws;
+  double* ws_side = ws ? ws + wcap / 2 : nullptr;
+  const int64_t wc = wcap / 2;
+  const int64_t mb = r1 - r0, p = r0;
+  double* Gc = G + r0 * ld;
+  double* Wc = Wi + r0 * ld;
+  double* Tc = T + r0 * ld;
+  std::vector<cudaEvent_t> evs;
+  auto ev = [&]() {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    evs.push_back(e);
+    return e;
+  };
+  cudaError_t e = cudaSuccess;
+  auto done = [&](cudaError_t r) {
+    for (cudaEvent_t x : evs) cudaEventDestroy(x);  // released once the recorded work completes
+    return r;
+  };
+  cudaEvent_t ev_half = nullptr;
+  if (p > 0) {
+    // L_c = G[c, 0:p] W^T (W = L^{-1} of the rows before, lower triangular)
+    if ((e = gemm_f64_splitk(Gc, ld, 1, Wi, ld, 1, mb, p, p, 1.0, 0.0, Tc, ld, chain, GEMM_B_KLE_N, ws_chain, wc)) !=
+        cudaSuccess)
+      return done(e);
+    cudaEvent_t ev_fork = ev();
+    ev_half = ev();
+    cudaEventRecord(ev_fork, chain);
+    cudaStreamWaitEvent(side, ev_fork, 0);
+    // beside the diagonal block's factorisation: G[c, 0:p] <- L_c W
+    if ((e = gemm_f64_splitk(Tc, ld, 1, Wi, 1, ld, mb, p, p, 1.0, 0.0, Gc, ld, side, GEMM_B_KGE_N, ws_side, wc)) !=
+        cudaSuccess)
+      return done(e);
+    cudaEventRecord(ev_half, side);
+    // S = G[c, c] - L_c L_c^T (lower tiles)
+    if ((e = gemm_f64_splitk(Tc, ld, 1, Tc, ld, 1, mb, mb, p, -1.0, 1.0, Gc + r0, ld, chain, GEMM_C_LOWER, ws_chain,
+                             wc)) != cudaSuccess)
+      return done(e);
+  }
+  if ((e = chol_rec(Gc + r0, Wc + r0, Tc + r0, ld, mb, r0, info, chain, chol_side_stream(), evs)) != cudaSuccess)
+    return done(e);
+  if (p > 0) {
+    cudaStreamWaitEvent(chain, ev_half, 0);
+    // W[c, 0:p] = -W[c, c] (L_c W)
+    if ((e = gemm_f64(Wc + r0, ld, 1, Gc, 1, ld, mb, p, mb, -1.0, 0.0, Wc, ld, chain, GEMM_A_KLE_M)) != cudaSuccess)
+      return done(e);
+  }
+  cudaEvent_t ev_row = ev();
+  cudaEventRecord(ev_row, chain);
+  cudaStreamWaitEvent(acc, ev_row, 0);
+  e = gemm_f64(Wc, 1, ld, Wc, 1, ld, r1, r1, mb, 1.0, 1.0, Ginv, ld, acc, GEMM_C_LOWER);
+  return done(e);
+}
+
+// Ginv's upper triangle from its lower one (after the last bordered step)
+cudaError_t mirror_lower(double* A, int64_t ld, int64_t m, cudaStream_t st) {
+  mirror_lower_kernel<<<grid_for(m * m), 256, 0, st>>>(A, ld, m);
+  return cudaGetLastError();
 }
 
 }  // namespace gdwd

@@ -51,16 +51,21 @@ def psqmr_dense(A: np.ndarray, b: np.ndarray, precond_diag: Optional[np.ndarray]
     return PsqmrResult(out, int(info[0]), bool(info[1]), bool(info[2]), float(rn.value))
 
 
-def cholesky_inverse(S: np.ndarray, device: int = 0) -> np.ndarray:
+def cholesky_inverse(S: np.ndarray, device: int = 0, block: Optional[int] = None) -> np.ndarray:
     """S^{-1} of an SPD matrix via the device recursive Cholesky + triangular
-    inverse (linalg/cholesky.py:25-66).  Raises IndefiniteMatrixError."""
+    inverse (linalg/cholesky.py:25-66).  Raises IndefiniteMatrixError.
+    ``block``: the row-block (bordered) chain the pipelined upload uses,
+    ``block`` rows per step, instead of the recursion."""
     S = _lib.f64(S)
     m = S.shape[0]
     if S.shape != (m, m):
         raise ValueError("expected a square matrix")
     out = np.empty_like(S)
     lib = _lib.load()
-    rc = lib.gdwd_chol_inverse(device, _lib.ptr(S), m, _lib.ptr(out))
+    if block is None:
+        rc = lib.gdwd_chol_inverse(device, _lib.ptr(S), m, _lib.ptr(out))
+    else:
+        rc = lib.gdwd_chol_inverse_bordered(device, _lib.ptr(S), m, int(block), _lib.ptr(out))
     if rc == _lib.ERR_INDEFINITE:
         raise IndefiniteMatrixError("non-positive pivot")
     _check(rc, None, "chol_inverse")

@@ -301,7 +301,7 @@ class DeviceProblem:
     Z~ is uploaded once; repeated solves on the same ProblemData reuse it and
     the cached factorisation."""
 
-    def __init__(self, data: Optional[ProblemData], device: int = 0):
+    def __init__(self, data: Optional[ProblemData], device: int = 0, hint: Optional[tuple] = None):
         lib = _lib.load()
         self.lib = lib
         self.device = int(device)
@@ -318,6 +318,8 @@ class DeviceProblem:
         z = data.z_tilde
         if z.is_dense:
             vals = z.values
+            if hint is not None:  # (backend code, mu) of the coming solve: factor during the upload
+                _check(lib.gdwd_upload_hint(self.ctx, int(hint[0]), float(hint[1])), self.ctx, "upload hint")
             _check(lib.gdwd_upload_dense(self.ctx, _lib.ptr(vals), self.d, self.n), self.ctx, "upload")
         else:
             cp = np.ascontiguousarray(z.colptr, dtype=np.int64)
@@ -384,12 +386,13 @@ class DeviceProblem:
 _DEVICE_CACHE: "weakref.WeakValueDictionary[int, DeviceProblem]" = weakref.WeakValueDictionary()
 
 
-def device_problem(data: ProblemData, device: Optional[int] = None) -> DeviceProblem:
-    """The (cached) device-resident copy of ``data``."""
+def device_problem(data: ProblemData, device: Optional[int] = None, hint: Optional[tuple] = None) -> DeviceProblem:
+    """The (cached) device-resident copy of ``data``.  ``hint`` = (backend
+    code, mu) of the solve that follows a first upload."""
     dev = getattr(data, "_gdwd_device", None)
     want = 0 if device is None else int(device)
     if dev is None or dev.ctx is None or dev.device != want:
-        dev = DeviceProblem(data, want)
+        dev = DeviceProblem(data, want, hint)
         object.__setattr__(data, "_gdwd_device", dev)
     return dev
 
@@ -491,7 +494,10 @@ def sgs_admm_solve(data: ProblemData, config: SolverConfig, meta: Optional[Featu
         device = int(devices[0])
     t_start = time.perf_counter()
     data = as_problem(data)
-    dp = device_problem(data, device)
+    hint = None
+    if getattr(data, "_gdwd_device", None) is None and data.z_tilde is not None:
+        hint = (_lib.BACKEND_CODE[config.backend.resolve(data.n, data.d).value], config.mu)
+    dp = device_problem(data, device, hint)
     t_up = time.perf_counter()
     lib = dp.lib
     kind = config.backend.resolve(dp.n_global or data.n, data.d)  # sharded: the global sample count

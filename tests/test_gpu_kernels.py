@@ -97,6 +97,21 @@ def test_cholesky_inverse(m):
     assert relerr(inv, np.linalg.inv(S)) < 1e-12
 
 
+@pytest.mark.parametrize("m,block", [(2, 128), (100, 128), (129, 128), (300, 37), (1001, 128), (2000, 128),
+                                     (2000, 96), (777, 200)])
+def test_cholesky_inverse_bordered(m, block):
+    """The row-block chain of the pipelined upload (gram.cu bordered_chol_step):
+    rows of L^{-1} block by block, G^{-1} accumulated as rank-`block` updates."""
+    rng = np.random.default_rng(m)
+    B = rng.standard_normal((m, m))
+    S = B @ B.T + m * np.eye(m)
+    inv = L.cholesky_inverse(S, block=block)
+    assert relerr(inv, np.linalg.inv(S)) < 1e-12
+    assert np.array_equal(inv, inv.T)
+    with pytest.raises(G.IndefiniteMatrixError):
+        L.cholesky_inverse(np.array([[1.0, 2.0], [2.0, 1.0]]), block=128)
+
+
 @pytest.mark.parametrize("m", [64, 200, 1000])
 def test_cholesky_inverse_ill_conditioned(m):
     """Eigenvalues spread over 1e0..1e8: the leaf panels' rsqrt pivots and

@@ -304,10 +304,12 @@ def test_persistent_iterates_match_reference(case, version, monkeypatch):
 
 @pytest.mark.parametrize("case", ["tiny_smw2", "smw2_natural", "var_direct_gram", "var_odd", "var_q3_mu2"])
 def test_pinned_upload_with_overlapped_gram(case):
-    """A page-locked matrix takes the overlapped upload (feature-column chunks
-    on a copy stream, the Gram accumulated chunk by chunk on a second stream):
-    the solve matches the reference's iterates like the pageable path, and
-    the Frobenius norm (epsilon constant) is the same."""
+    """A page-locked matrix takes the pipelined upload (blocks of samples on a
+    copy stream; each block's rows of the Gram, of the Cholesky factor's
+    inverse and its term of G^{-1} on further streams as it lands): the solve
+    matches the reference's iterates like the pageable path, and the Frobenius
+    norm (epsilon constant) is the same.  An upload without the solve's mu
+    (the default hint, mu = 1) refactors from the Gram."""
     torch = pytest.importorskip("torch")
     tr = load_traj(case)
     prob = problem_for(tr)
@@ -329,6 +331,37 @@ def test_pinned_upload_with_overlapped_gram(case):
         assert relerr(v, tr["it_" + key][19]) < TOL20, key
         assert relerr(getattr(a.final_state, key), getattr(b.final_state, key)) < 1e-11, key
     assert a.final_state.eps_c == b.final_state.eps_c
+    # uploaded before the solve's config is known: factor built for mu = 1
+    zq = G.SparseMatrixCSC.from_dense_samples(buf.reshape(z.ncols, z.nrows))
+    pq = G.ProblemData(zq, prob.y, prob.e, prob.weights, prob.C, prob.q, prob.z_scale)
+    G.device_problem(pq)
+    c = G.sgs_admm_solve(pq, cfg)
+    for key in ("w", "r", "alpha"):
+        assert relerr(getattr(c.final_state, key), getattr(b.final_state, key)) < 1e-11, key
+
+
+def test_pinned_upload_blocks(monkeypatch):
+    """Several sample blocks (n = 700: six blocks of 128, the last ragged; and
+    blocks of 48): the bordered chain across blocks gives the same solve as
+    the pageable path's recursion."""
+    torch = pytest.importorskip("torch")
+    from paper_2305_12019_b200 import synth
+
+    prob = synth.make_variant_problem("c2", 3001, 700, seed=5)
+    z = prob.z_tilde
+    cfg = G.SolverConfig(q=prob.q, max_iter=20, backend=G.Backend.SMW2)
+    ref = G.sgs_admm_solve(prob, cfg)
+    buf = torch.empty(z.values.size, dtype=torch.float64, pin_memory=True).numpy()
+    buf[:] = z.values
+    for blk in (None, "48"):
+        if blk:
+            monkeypatch.setenv("GDWD_UP_BLOCK", blk)
+        zp = G.SparseMatrixCSC.from_dense_samples(buf.reshape(z.ncols, z.nrows))
+        pp = G.ProblemData(zp, prob.y, prob.e, prob.weights, prob.C, prob.q, prob.z_scale)
+        out = G.sgs_admm_solve(pp, cfg)
+        for key in ("w", "u", "rho", "r", "xi", "alpha"):
+            assert relerr(getattr(out.final_state, key), getattr(ref.final_state, key)) < 1e-10, (blk, key)
+        assert out.final_state.eps_c == ref.final_state.eps_c
 
 
 @pytest.mark.parametrize("d,n", [(6000, 1500), (5000, 2047)])

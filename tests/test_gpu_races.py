@@ -109,3 +109,8 @@ def test_cholesky_inverse_repeats_bitwise():
     for _ in range(REPS // 2):
         assert np.array_equal(linalg.cholesky_inverse(S), ref)
     assert np.abs(ref @ S - np.eye(1300)).max() < 1e-9
+    # the pipelined upload's row-block chain (three streams, event hand-offs)
+    refb = linalg.cholesky_inverse(S, block=128)
+    for _ in range(REPS // 2):
+        assert np.array_equal(linalg.cholesky_inverse(S, block=128), refb)
+    assert np.abs(refb - ref).max() < 1e-12 * np.abs(ref).max()
