@@ -448,26 +448,41 @@ def measure_e2e(G, synth, cfg_syn, args, device, dist, K, n, d, nnz):
     G.sgs_admm_solve(prob_w, G.SolverConfig(q=prob_w.q, max_iter=min(K, 20)), device=device)
     G.solver.device_problem(prob_w, device).close()
     del prob_w
-    prob2 = pinned_problem(G, synth.make_problem(cfg_syn, args.seed))  # fresh host data: nothing resident
-    dist.barrier()
-    t1 = time.perf_counter()
-    out = G.sgs_admm_solve(prob2, G.SolverConfig(q=prob2.q, max_iter=K), device=device)
-    e2e_s = dist.max(time.perf_counter() - t1)
+    # three timed calls, each on fresh host data with a new device context
+    # (nothing resident, no cached factor); the median call is reported
+    runs = []
+    reps = 3 if 8.0 * n * d < 4e9 else 1
+    for _ in range(reps):
+        prob2 = pinned_problem(G, synth.make_problem(cfg_syn, args.seed))
+        dist.barrier()
+        t1 = time.perf_counter()
+        out = G.sgs_admm_solve(prob2, G.SolverConfig(q=prob2.q, max_iter=K), device=device)
+        runs.append((dist.max(time.perf_counter() - t1), out))
+        G.solver.device_problem(prob2, device).close()
+        del prob2
+    e2e_s, out = sorted(runs, key=lambda r: r[0])[len(runs) // 2]
     h2d = (8.0 * n * d if nnz is None else 16.0 * nnz + 8.0 * (n + 1)) + 8.0 * 3 * n
     d2h = 8.0 * (4 * n + 3 * d + 1 + 16 * out.iterations)
-    G.solver.device_problem(prob2, device).close()
     return {"value": round(dist.world * out.iterations / e2e_s, 3), "unit": UNIT,
             "h2d_bytes_per_step": round(h2d / out.iterations), "d2h_bytes_per_step": round(d2h / out.iterations),
             "seconds": round(e2e_s, 4), "iterations": out.iterations,
+            "runs_s": [round(r[0], 4) for r in runs],
             "breakdown": {k: round(v, 5) for k, v in (out.timings or {}).items()},
             "note": "sgs_admm_solve from host numpy buffers (X in pinned host memory): X upload, factorisation, "
-                    "iterations, state download"}
+                    "iterations, state download; median of %d calls, each on fresh host data and a new context. "
+                    "Sample-space regimes: the Gram, its Cholesky factor and inverse advance block by block "
+                    "during the copy (DESIGN.md section 6)" % len(runs)}
 
 
 def time_to_kkt(G, prob, args, device):
     """One solve on a FRESH device copy (no cached factorisation): setup (Gram
     + factor) + iterations until max(eta_P, eta_D) < 1e-5, device time; and
     the same through the public API from host buffers (upload included)."""
+    # warm process first (memory-pool growth for the Gram's split-K workspace is a
+    # one-time driver cost): a short solve on its own fresh copy, then released
+    warm = G.ProblemData(prob.z_tilde, prob.y, prob.e, prob.weights, prob.C, prob.q, prob.z_scale)
+    G.sgs_admm_solve(warm, G.SolverConfig(q=prob.q, max_iter=3), device=device)
+    G.solver.device_problem(warm, device).close()
     fresh = G.ProblemData(prob.z_tilde, prob.y, prob.e, prob.weights, prob.C, prob.q, prob.z_scale)
     t0 = time.perf_counter()
     out = G.sgs_admm_solve(fresh, G.SolverConfig(q=prob.q, max_iter=args.kkt_iters), device=device)

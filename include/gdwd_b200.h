@@ -260,6 +260,11 @@ int gdwd_chol_inverse_bordered(int32_t device, const double* S, int64_t m, int32
 int gdwd_time_gram(gdwd_ctx* ctx, int32_t reps, double* ms);
 int gdwd_gram(int32_t device, const double* X, int64_t rows, int64_t cols, int32_t sum_over_rows, double div,
               double shift, double* out);
+/* the n x n Gram K = Z~^T Z~ (subsolvers.py:109) and G^{-1} = (K/mu^2 + I)^{-1}
+ * (cholesky.py:46,60-61) that a page-locked gdwd_upload_dense formed during
+ * the copy; row-major n x n outputs (nullable); *have: bit 0 = K is
+ * available, bit 1 = G^{-1} is. */
+int gdwd_get_upload_factor(gdwd_ctx* ctx, double* K_out, double* Ginv_out, int32_t* have);
 /* psqmr (linalg/psqmr.py:27-95) with a dense symmetric operator A (m x m,
  * row-major) and diagonal preconditioner M (nullable = identity); x0 nullable.
  * info[4] = {iterations, converged, breakdown, 0}; *resnorm = final |res|. */

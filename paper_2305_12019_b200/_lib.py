@@ -30,7 +30,7 @@ SYMBOLS = [
     "gdwd_get_profile", "gdwd_reset_counters", "gdwd_frobenius_sq", "gdwd_comm_unique_id",
     "gdwd_comm_init_nccl", "gdwd_comm_init_host", "gdwd_generate_dense", "gdwd_scale_dense",
     "gdwd_download_dense", "gdwd_set_lanczos_start", "gdwd_allreduce_host", "gdwd_time_gram",
-    "gdwd_upload_hint", "gdwd_chol_inverse_bordered",
+    "gdwd_upload_hint", "gdwd_chol_inverse_bordered", "gdwd_get_upload_factor",
 ]
 
 
@@ -120,6 +120,7 @@ def _declare(lib):
         "gdwd_chol_inverse": (C.c_int, [C.c_int32, _P, _I64, _P]),
         "gdwd_chol_inverse_bordered": (C.c_int, [C.c_int32, _P, _I64, C.c_int32, _P]),
         "gdwd_upload_hint": (C.c_int, [vp, C.c_int32, C.c_double]),
+        "gdwd_get_upload_factor": (C.c_int, [vp, _P, _P, C.POINTER(C.c_int32)]),
         "gdwd_gram": (C.c_int, [C.c_int32, _P, _I64, _I64, C.c_int32, C.c_double, C.c_double, _P]),
         "gdwd_psqmr_dense": (C.c_int, [C.c_int32, _P, _I64, _P, _P, C.c_double, C.c_int32, _P, _P,
                                        C.POINTER(C.c_int32), _P]),

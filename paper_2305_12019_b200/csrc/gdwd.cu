@@ -677,7 +677,8 @@ static int ensure_scratch(gdwd_ctx* ctx, int64_t rows, int64_t cols) {
   if (nt > ctx->ntickets) {
     dfree(ctx->tickets, ctx->st);
     CK(dmalloc((void**)&ctx->tickets, nt * sizeof(unsigned), ctx->st));
-    CK(cudaMemset(ctx->tickets, 0, nt * sizeof(unsigned)));
+    // ordered on st (non-blocking: the legacy stream does not synchronise with it)
+    CK(cudaMemsetAsync(ctx->tickets, 0, nt * sizeof(unsigned), ctx->st));
     ctx->ntickets = nt;
   }
   CK(ctx->bundle.ensure(std::max<size_t>((size_t)2 * cols + 32, ctx->bundle.n)));
@@ -1209,10 +1210,9 @@ static int upload_dense_pipelined(gdwd_ctx* ctx, const double* samples, int64_t 
   const int64_t ldk = (n + 1) / 2 * 2;
   int64_t mb = gdwd_ctx::UP_BLOCK;
   if (const char* ev = getenv("GDWD_UP_BLOCK")) mb = std::max(16, atoi(ev));
-  // the work a block triggers grows with the rows before it, and what runs
-  // after the last byte is the last block's share: the last `fine` rows go in
-  // half-size blocks
-  int64_t fine = 2 * mb;
+  // GDWD_UP_FINE: the last `fine` rows in half-size blocks (measured: the
+  // smaller launches lose more than the shorter last block gains; default 0)
+  int64_t fine = 0;
   if (const char* ev = getenv("GDWD_UP_FINE")) fine = std::max(0, atoi(ev));
   while ((n + mb - 1) / mb + fine / mb > gdwd_ctx::UP_MAXB) mb += 64;
   int64_t rb[gdwd_ctx::UP_MAXB + 1];
@@ -1687,6 +1687,9 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
     }
     hmark("sample-blocked sliced ELL");
   }
+  // the synchronous copies above are staged through the legacy stream, which
+  // the (non-blocking) solve stream does not wait for: let them land
+  CK(cudaStreamSynchronize(cudaStreamLegacy));
   CK(ctx->tbuf.ensure((size_t)2 * n + 2));
   ctx->n = n;
   ctx->d = d;
@@ -1752,6 +1755,7 @@ int gdwd_scale_dense(gdwd_ctx* ctx, const double* y, double z_scale) {
   DevBuf yd;
   CK(yd.ensure(ctx->n));
   CK(cudaMemcpy(yd.p, y, ctx->n * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaStreamSynchronize(cudaStreamLegacy));  // st is non-blocking: the staged copy must have landed
   scale_rows_kernel<<<NUM_SMS * 16, 256, 0, ctx->st>>>(ctx->Zs, ctx->ldz, ctx->d, ctx->n, yd.p, z_scale);
   ctx->zs_gen++;
   CK(cudaGetLastError());
@@ -2555,6 +2559,7 @@ static int build_prox(gdwd_ctx* ctx) {
   double* cb = px + (size_t)PX_MAXL * d;
   CK(cudaMemcpy(cb, cinv.data(), PX_MAXL * sizeof(double), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(cb + PX_MAXL, cfwd.data(), PX_MAXL * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaStreamSynchronize(cudaStreamLegacy));  // st is non-blocking: the staged copies must have landed
   double* vb = cb + 2 * PX_MAXL;
   D.pxV = px;
   D.px_cinv = cb;
@@ -2833,7 +2838,9 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
   CK(cudaEventRecord(ctx->ev_begin, ctx->st));
   RC(ensure_scratch(ctx, n, d));
   MatView Z = zview(ctx);
-  run_zmv(ctx, OpPlainZ{ctx->y.p, nullptr, const_cast<double*>(D.zy), nullptr}, Z, "zmv_zy");
+  // Z~ y: the border of A in feature space; the Gram-space iteration carries
+  // it as the coefficient vector y itself (no pass over X)
+  if (!gram) run_zmv(ctx, OpPlainZ{ctx->y.p, nullptr, const_cast<double*>(D.zy), nullptr}, Z, "zmv_zy");
   CK(cudaGetLastError());
   // ITERATIVE on dense data: the d x d Gram as PSQMR's operator when it is
   // much smaller than X (d <= n/4, n the global count) and fits in memory
@@ -3435,6 +3442,26 @@ extern "C" int gdwd_chol_inverse(int32_t device, const double* Sm, int64_t m, do
   CK(cudaMemcpy(&h, info, sizeof(int), cudaMemcpyDeviceToHost));
   if (h) return GDWD_ERR_INDEFINITE;
   CK(cudaMemcpy2D(inv_out, m * 8, A, ld * 8, m * 8, m, cudaMemcpyDeviceToHost));
+  return GDWD_OK;
+}
+
+// Test seam: the n x n Gram K = Z~^T Z~ and (when the upload also factored)
+// G^{-1} = (K/mu^2 + I)^{-1} that a page-locked upload in the sample-space
+// regimes formed block by block.  *have: bit 0 = K, bit 1 = G^{-1}.
+extern "C" int gdwd_get_upload_factor(gdwd_ctx* ctx, double* K_out, double* Ginv_out, int32_t* have) {
+  if (!ctx || !have) return set_err(ctx, GDWD_ERR_VALUE, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  *have = 0;
+  const int64_t n = ctx->n, ldk = (n + 1) / 2 * 2;
+  CK(cudaStreamSynchronize(ctx->st));
+  if (ctx->has_dense && ctx->k_gen == ctx->zs_gen && ctx->kmat.p) {
+    *have |= 1;
+    if (K_out) CK(cudaMemcpy2D(K_out, n * 8, ctx->kmat.p, ldk * 8, n * 8, n, cudaMemcpyDeviceToHost));
+  }
+  if (ctx->has_dense && ctx->pf_gen == ctx->zs_gen && ctx->fac.p) {
+    *have |= 2;
+    if (Ginv_out) CK(cudaMemcpy2D(Ginv_out, n * 8, ctx->fac.p, ldk * 8, n * 8, n, cudaMemcpyDeviceToHost));
+  }
   return GDWD_OK;
 }
 

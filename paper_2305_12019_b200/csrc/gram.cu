@@ -183,6 +183,146 @@ __global__ void syrk_finish_kernel(const double* W, int64_t ldw, int64_t wslice,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Gram-shaped products (both operands with the same fast axis, 16-byte
+// aligned rows): 64 x 128 CTA tile, 4 warps side by side, each warp
+// 64 x 32 = 8 x 4 DMMA tiles (32 DMMAs per 12 fragment loads), operands
+// brought global -> shared by 16-byte cp.async in a 3-stage ring (no register
+// staging).  Two CTAs per SM (192 registers x 128 threads, 90 KB of shared
+// memory each): one CTA's barrier / fragment-load bubble at a K step is
+// covered by the other's DMMAs.  K tails and rows beyond M / N are
+// zero-filled by the copy's source size.
+// ---------------------------------------------------------------------------
+constexpr int TMA = 64, TNB = 128, TK = 16, TSTAGES = 3, TT = 128;
+constexpr int T_KSTRIDE = TK + 4;    // k-fast tiles [r][k]: fragment reads conflict-free
+constexpr int T_RSTRIDE_A = TMA + 8;  // r-fast tiles [k][r]
+constexpr int T_RSTRIDE_B = TNB + 8;
+constexpr int T_TILE_A = (TMA * T_KSTRIDE > TK * T_RSTRIDE_A) ? TMA * T_KSTRIDE : TK * T_RSTRIDE_A;
+constexpr int T_TILE_B = (TNB * T_KSTRIDE > TK * T_RSTRIDE_B) ? TNB * T_KSTRIDE : TK * T_RSTRIDE_B;
+constexpr int T_STAGE = T_TILE_A + T_TILE_B;
+constexpr size_t T_SMEM = (size_t)TSTAGES * T_STAGE * sizeof(double);
+
+GDWD_DEV void cp_async16(double* smem, const double* g, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(g), "r"(src_bytes) : "memory");
+}
+
+// one ROWS x 16 operand tile in chunks of two doubles
+template <bool KF, int ROWS>
+GDWD_DEV void tile_load(double* sm, const Opnd& op, int64_t R, int64_t r0, int64_t k0, int64_t ke) {
+  constexpr int RSTRIDE = ROWS + 8;
+#pragma unroll
+  for (int e = 0; e < ROWS * 8 / TT; ++e) {
+    const int c = threadIdx.x + e * TT;
+    if (KF) {
+      const int rr = c >> 3, kc = (c & 7) * 2;
+      const int64_t r = r0 + rr, k = k0 + kc;
+      const int v = (r < R && k < ke) ? (ke - k >= 2 ? 2 : 1) : 0;
+      cp_async16(sm + rr * T_KSTRIDE + kc, op.p + (v ? r * op.sr + k : 0), v * 8);
+    } else {
+      const int kk = c / (ROWS / 2), rc = (c % (ROWS / 2)) * 2;
+      const int64_t r = r0 + rc, k = k0 + kk;
+      const int v = (k < ke && r < R) ? (R - r >= 2 ? 2 : 1) : 0;
+      cp_async16(sm + kk * RSTRIDE + rc, op.p + (v ? k * op.sk + r : 0), v * 8);
+    }
+  }
+}
+
+template <bool KF>
+__global__ void __launch_bounds__(TT, 2) gram_tile_kernel(Opnd A, Opnd B, int64_t M, int64_t N, int64_t K,
+                                                          int64_t kslice, double* W, int64_t ldw, int64_t wslice,
+                                                          bool upper_only, double alpha, double beta, double* C,
+                                                          int64_t ldc) {
+  const int bm = blockIdx.y, bn = blockIdx.x;
+  const int64_t m0 = (int64_t)bm * TMA, n0 = (int64_t)bn * TNB;
+  if (upper_only && n0 + TNB <= m0) return;  // every entry below the diagonal
+  extern __shared__ __align__(16) double tsm[];
+  const int64_t kb = (int64_t)blockIdx.z * kslice;
+  const int64_t ke = (kb + kslice < K) ? kb + kslice : K;
+  const int nk = kb < ke ? (int)((ke - kb + TK - 1) / TK) : 0;
+  const int lane = threadIdx.x & 31, wn = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < TSTAGES - 1; ++s) {
+    if (s < nk) {
+      tile_load<KF, TMA>(tsm + (size_t)s * T_STAGE, A, M, m0, kb + (int64_t)s * TK, ke);
+      tile_load<KF, TNB>(tsm + (size_t)s * T_STAGE + T_TILE_A, B, N, n0, kb + (int64_t)s * TK, ke);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int it = 0; it < nk; ++it) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(TSTAGES - 2) : "memory");
+    __syncthreads();  // stage `it` landed for everyone; stage it-1 is free again
+    {
+      const int nx = it + TSTAGES - 1;
+      if (nx < nk) {
+        double* st = tsm + (size_t)(nx % TSTAGES) * T_STAGE;
+        tile_load<KF, TMA>(st, A, M, m0, kb + (int64_t)nx * TK, ke);
+        tile_load<KF, TNB>(st + T_TILE_A, B, N, n0, kb + (int64_t)nx * TK, ke);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    const double* as = tsm + (size_t)(it % TSTAGES) * T_STAGE;
+    const double* bs = as + T_TILE_A;
+#pragma unroll
+    for (int kk = 0; kk < TK; kk += 4) {
+      double af[8], bf[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        af[i] = KF ? as[(i * 8 + g) * T_KSTRIDE + kk + t4] : as[(kk + t4) * T_RSTRIDE_A + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        bf[j] = KF ? bs[(wn * 32 + j * 8 + g) * T_KSTRIDE + kk + t4] : bs[(kk + t4) * T_RSTRIDE_B + wn * 32 + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t m = m0 + i * 8 + g;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t nn = n0 + wn * 32 + j * 8 + t4 * 2 + h;
+        if (nn >= N) continue;
+        if (W) {
+          W[(int64_t)blockIdx.z * wslice + m * ldw + nn] = acc[i][j][h];
+        } else {
+          double* cp = C + m * ldc + nn;
+          *cp = (beta == 0.0) ? alpha * acc[i][j][h] : beta * *cp + alpha * acc[i][j][h];
+        }
+      }
+    }
+  }
+}
+
+// the tiled kernel needs 16-byte aligned rows along the fast axis
+static bool tile_ok(const double* p, int64_t ld) { return ((uintptr_t)p & 15) == 0 && (ld & 1) == 0; }
+
+template <bool KF>
+static cudaError_t launch_tile(Opnd A, Opnd B, int64_t M, int64_t N, int64_t K, int64_t kslice, int ns, double* W,
+                               int64_t ldw, int64_t wslice, bool upper_only, cudaStream_t st) {
+  static unsigned long long attr = 0;
+  if (once_per_device(attr))
+    cudaFuncSetAttribute(gram_tile_kernel<KF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T_SMEM);
+  dim3 grid((unsigned)((N + TNB - 1) / TNB), (unsigned)((M + TMA - 1) / TMA), (unsigned)ns);
+  gram_tile_kernel<KF><<<grid, TT, T_SMEM, st>>>(A, B, M, N, K, kslice, W, ldw, wslice, upper_only, 1.0, 0.0, nullptr,
+                                                 0);
+  return cudaGetLastError();
+}
+
 // Dense factor + inverse of one diagonal block (m <= LEAF_MAX) in shared
 // memory: A = L L^T (L lower), Linv = L^{-1}.  Upper parts are written as
 // zeros.  Factor: 8-column panels; inverse: forward substitution, 8 columns
@@ -459,8 +599,7 @@ int64_t gram_workspace_doubles(int64_t M, int64_t K) {
 // count whose CTA total fills whole waves best (>= kmin of K per slice, at
 // least ~2 waves when K allows so the tail wave is a small share), smallest
 // such count on ties.
-static int pick_slices(int64_t tiles, int64_t K, int64_t kmin, int smax) {
-  const int64_t slots = 2 * 148;
+static int pick_slices(int64_t tiles, int64_t K, int64_t kmin, int smax, int64_t slots = 2 * 148) {
   int64_t kmax = (K + kmin - 1) / kmin;
   if (kmax > smax) kmax = smax;
   if (kmax < 1) kmax = 1;
@@ -477,9 +616,10 @@ static int pick_slices(int64_t tiles, int64_t K, int64_t kmin, int smax) {
   return best;
 }
 
-int gram_slices(int64_t M, int64_t K) {
-  const int64_t tiles = ((M + BM - 1) / BM) * ((M + BM - 1) / BM + 1) / 2;
-  return pick_slices(tiles, K, 512, 16);
+int gram_slices(int64_t M, int64_t K) {  // 64 x 128 tiles on or above the diagonal, two CTAs per SM
+  int64_t tiles = 0;
+  for (int64_t m0 = 0; m0 < M; m0 += TMA) tiles += (M + TNB - 1) / TNB - m0 / TNB;
+  return pick_slices(tiles, K, 512, 32, 2 * 148);
 }
 
 // Symmetric Gram of the rows/columns of a row-major [R x L] matrix Zs:
@@ -493,6 +633,14 @@ cudaError_t gram_syrk(const double* Zs, int64_t R, int64_t Lc, int64_t ldz, bool
   const int ns = gram_slices(M, K);
   int64_t kslice = (K + ns - 1) / ns;
   kslice = (kslice + BK - 1) / BK * BK;
+  if (tile_ok(Zs, ldz)) {
+    cudaError_t e = sum_over_rows
+                        ? launch_tile<false>(Opnd{Zs, 1, ldz}, Opnd{Zs, 1, ldz}, M, M, K, kslice, ns, W, M, M * M, true, st)
+                        : launch_tile<true>(Opnd{Zs, ldz, 1}, Opnd{Zs, ldz, 1}, M, M, K, kslice, ns, W, M, M * M, true, st);
+    if (e != cudaSuccess) return e;
+    syrk_finish_kernel<<<grid_for(M * M), 256, 0, st>>>(W, M, M * M, ns, M, div, shift, C, ldc, accumulate);
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)((M + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)ns);
   if (sum_over_rows) {
     // A(m,k) = Zs[k][m]: m stride 1, k stride ldz (r fastest)
@@ -613,8 +761,8 @@ cudaError_t chol_inverse(double* A, double* Li, double* T, int64_t ld, int64_t m
 namespace {
 
 int rowblock_slices(int64_t mb, int64_t r1, int64_t K) {
-  const int64_t tiles = ((mb + BM - 1) / BM) * ((r1 + BN - 1) / BN);
-  return pick_slices(tiles, K, 256, 64);
+  const int64_t tiles = ((mb + TMA - 1) / TMA) * ((r1 + TNB - 1) / TNB);
+  return pick_slices(tiles, K, 256, 64, 2 * 148);
 }
 
 // Sum the split-K partials of block rows r0..r1 in slice order; the diagonal
@@ -666,10 +814,15 @@ cudaError_t gram_rowblock(const double* Zs, int64_t ldz, int64_t d, int64_t r0, 
   const int ns = rowblock_slices(mb, r1, d);
   int64_t kslice = (d + ns - 1) / ns;
   kslice = (kslice + BK - 1) / BK * BK;
-  dim3 grid((unsigned)((r1 + BN - 1) / BN), (unsigned)((mb + BM - 1) / BM), (unsigned)ns);
   Opnd A{Zs + r0 * ldz, ldz, 1}, B{Zs, ldz, 1};
-  gemm_dmma_kernel<true, true><<<grid, GT, 0, st>>>(A, B, mb, r1, d, kslice, W, r1, mb * r1, false, 1.0, 0.0, nullptr,
-                                                    0);
+  if (tile_ok(Zs, ldz)) {
+    cudaError_t e = launch_tile<true>(A, B, mb, r1, d, kslice, ns, W, r1, mb * r1, false, st);
+    if (e != cudaSuccess) return e;
+  } else {
+    dim3 grid((unsigned)((r1 + BN - 1) / BN), (unsigned)((mb + BM - 1) / BM), (unsigned)ns);
+    gemm_dmma_kernel<true, true><<<grid, GT, 0, st>>>(A, B, mb, r1, d, kslice, W, r1, mb * r1, false, 1.0, 0.0,
+                                                      nullptr, 0);
+  }
   rowblock_finish_kernel<<<grid_for(mb * r1), 256, 0, st>>>(W, mb * r1, ns, r0, r1, K, ldk, G, ldg, mu2);
   return cudaGetLastError();
 }

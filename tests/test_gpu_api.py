@@ -195,3 +195,45 @@ def test_reference_problem_data_is_accepted_as_is():
         assert a.train_error_pct == b.train_error_pct
         kk = G.kkt_residuals(b.final_state, rp)
         assert np.isfinite(kk.eta_p)
+
+
+@pytest.mark.parametrize("n,d,mu", [(200, 6000, 1.0), (16, 90, 1.0), (700, 3001, 2.0), (333, 777, 0.7), (1000, 2000, 1.0)])
+def test_upload_time_gram_and_inverse(n, d, mu):
+    """A page-locked upload in the sample-space regimes forms K = Z~^T Z~
+    (subsolvers.py:109) and G^{-1} = (K/mu^2 + I)^{-1} (cholesky.py:46,60-61)
+    block by block while the samples are copied (gdwd_upload_hint +
+    gdwd_upload_dense): both match numpy; K is exactly symmetric."""
+    torch = pytest.importorskip("torch")
+    import ctypes as C
+
+    from paper_2305_12019_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((n, d)) * (3.0 / np.sqrt(d))
+    buf = torch.empty(n * d, dtype=torch.float64, pin_memory=True).numpy()
+    buf[:] = X.ravel()
+    h = C.c_void_p()
+    assert lib.gdwd_ctx_create(0, C.byref(h)) == 0
+    try:
+        assert lib.gdwd_upload_hint(h, _lib.BACKEND_CODE["smw2"], mu) == 0
+        assert lib.gdwd_upload_dense(h, _lib.ptr(buf), d, n) == 0
+        K, Gi, have = np.empty((n, n)), np.empty((n, n)), C.c_int32()
+        assert lib.gdwd_get_upload_factor(h, _lib.ptr(K), _lib.ptr(Gi), C.byref(have)) == 0
+        assert have.value == 3
+        Kr = X @ X.T
+        assert np.abs(K - Kr).max() <= 1e-13 * np.abs(Kr).max()
+        assert np.array_equal(K, K.T)
+        Gr = np.linalg.inv(Kr / mu ** 2 + np.eye(n))
+        assert np.abs(Gi - Gr).max() <= 1e-12 * np.abs(Gr).max()
+        assert np.array_equal(Gi, Gi.T)
+        fro2 = C.c_double()
+        assert lib.gdwd_frobenius_sq(h, C.byref(fro2)) == 0
+        assert abs(fro2.value - (X * X).sum()) <= 1e-12 * (X * X).sum()
+        # an ITERATIVE hint: the Gram only
+        assert lib.gdwd_upload_hint(h, _lib.BACKEND_CODE["iterative"], mu) == 0
+        assert lib.gdwd_upload_dense(h, _lib.ptr(buf), d, n) == 0
+        assert lib.gdwd_get_upload_factor(h, None, None, C.byref(have)) == 0
+        assert have.value == 1
+    finally:
+        lib.gdwd_ctx_destroy(h)
