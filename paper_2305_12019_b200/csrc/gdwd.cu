@@ -1055,8 +1055,10 @@ struct CtxAux {
   Scal* Sh = nullptr;
   int* dinfo = nullptr;
   int* poll_flag = nullptr;
+  double* stage = nullptr;  // pinned, CTX_STAGE_DOUBLES: result download staging
   cudaEvent_t poll_ev[2] = {}, ev[3] = {};
 };
+constexpr size_t CTX_STAGE_DOUBLES = (size_t)1 << 17;  // 1 MB
 static std::mutex g_ctxaux_mu;
 static std::vector<CtxAux*> g_ctxaux_free;
 static CtxAux* ctx_aux_acquire(int device) {
@@ -1077,6 +1079,7 @@ static CtxAux* ctx_aux_acquire(int device) {
   if (e == cudaSuccess) e = cudaMallocHost(&a->Sh, sizeof(Scal));
   if (e == cudaSuccess) e = cudaMalloc(&a->dinfo, sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&a->poll_flag, 2 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost(&a->stage, CTX_STAGE_DOUBLES * sizeof(double));
   for (auto& x : a->poll_ev)
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
   for (auto& x : a->ev)
@@ -3329,6 +3332,28 @@ extern "C" int gdwd_get_state(gdwd_ctx* ctx, double* r, double* xi, double* alph
   const int64_t n = ctx->n, d = ctx->d;
   struct P { double* h; const double* dp; int64_t len; } items[] = {
       {r, D.r, n}, {xi, D.xi, n}, {alpha, D.al, n}, {ztw, D.ztw, n}, {w, D.wd, d}, {u, D.ud, d}, {rho, D.rhod, d}, {beta, D.wd + d, 1}};
+  // through the context's page-locked staging block when everything fits:
+  // the copies run back to back without a staged (synchronous) transfer each
+  double* stage = ctx->aux ? ((CtxAux*)ctx->aux)->stage : nullptr;
+  size_t tot = 0;
+  for (auto& it : items)
+    if (it.h) tot += (size_t)it.len;
+  if (stage && tot <= CTX_STAGE_DOUBLES) {
+    size_t off = 0;
+    for (auto& it : items)
+      if (it.h) {
+        CK(cudaMemcpyAsync(stage + off, it.dp, it.len * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+        off += (size_t)it.len;
+      }
+    CK(cudaStreamSynchronize(ctx->st));
+    off = 0;
+    for (auto& it : items)
+      if (it.h) {
+        memcpy(it.h, stage + off, it.len * sizeof(double));
+        off += (size_t)it.len;
+      }
+    return GDWD_OK;
+  }
   for (auto& it : items)
     if (it.h) CK(cudaMemcpyAsync(it.h, it.dp, it.len * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
@@ -3339,7 +3364,14 @@ extern "C" int gdwd_get_history(gdwd_ctx* ctx, double* hist, int64_t max_rows, i
   if (!ctx || !hist || !rows) return set_err(ctx, GDWD_ERR_VALUE, "null argument");
   int64_t nr = std::min(max_rows, ctx->hist_rows);
   if (nr > 0) {
-    CK(cudaMemcpy(hist, ctx->histb.p, nr * HIST_W * sizeof(double), cudaMemcpyDeviceToHost));
+    double* stage = ctx->aux ? ((CtxAux*)ctx->aux)->stage : nullptr;
+    if (stage && (size_t)nr * HIST_W <= CTX_STAGE_DOUBLES) {
+      CK(cudaMemcpyAsync(stage, ctx->histb.p, nr * HIST_W * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+      CK(cudaStreamSynchronize(ctx->st));
+      memcpy(hist, stage, nr * HIST_W * sizeof(double));
+    } else {
+      CK(cudaMemcpy(hist, ctx->histb.p, nr * HIST_W * sizeof(double), cudaMemcpyDeviceToHost));
+    }
     // host-driven PSQMR counts its steps on the host; the device-resident
     // one records them in the history itself (OpPsEnd)
     if (!ctx->hist_ps_dev)

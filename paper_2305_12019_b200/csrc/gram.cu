@@ -173,13 +173,14 @@ __global__ void syrk_finish_kernel(const double* W, int64_t ldw, int64_t wslice,
   const int64_t tot = M * M;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = idx / M, j = idx % M;
-    int64_t a = i < j ? i : j, b = i < j ? j : i;
+    const int64_t i = idx / M, j = idx % M;
+    if (j < i) continue;  // each upper entry is summed once and stored to both halves
     double s = 0.0;
-    for (int z = 0; z < nslice; ++z) s += W[z * wslice + a * ldw + b];
+    for (int z = 0; z < nslice; ++z) s += W[z * wslice + i * ldw + j];
     double v = (div == 1.0) ? s : s / div;
     if (i == j) v += shift;
     C[i * ldc + j] = accumulate ? C[i * ldc + j] + v : v;
+    if (i != j) C[j * ldc + i] = accumulate ? C[j * ldc + i] + v : v;
   }
 }
 
