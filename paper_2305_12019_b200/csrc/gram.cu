@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <vector>
 
@@ -763,7 +764,25 @@ namespace {
 
 int rowblock_slices(int64_t mb, int64_t r1, int64_t K) {
   const int64_t tiles = ((mb + TMA - 1) / TMA) * ((r1 + TNB - 1) / TNB);
-  return pick_slices(tiles, K, 256, 64, 2 * 148);
+  // Default: whole waves of many short slices (c2's last block: 37 slices of
+  // 544, four exact waves), so Gram CTAs retire every ~70 us and the factor
+  // chain's launches (which cannot co-reside with two of them: registers)
+  // find a slot quickly.  Measured alternatives at c2, end to end: >= 1024 of
+  // K per slice (Gram kernel faster, chain starved) 8.15-8.24 ms; one partial
+  // wave of GDWD_RB_CTAS = 288 / 264 / 232 / 200 CTAs (some SMs left with one
+  // Gram CTA for the chain) 8.06-8.10 / 8.10-8.24 / 8.15-8.18 / 8.33-8.38 ms;
+  // this default 8.02-8.08 ms.
+  static const int64_t cap = [] {
+    const char* e = getenv("GDWD_RB_CTAS");
+    return (int64_t)(e ? atoi(e) : 0);
+  }();
+  if (cap <= 0) return pick_slices(tiles, K, 256, 64, 2 * 148);  // whole waves of short slices
+  int64_t s = cap / tiles;
+  const int64_t kmax = (K + 255) / 256;
+  if (s > kmax) s = kmax;
+  if (s > 64) s = 64;
+  if (s < 1) s = 1;
+  return (int)s;
 }
 
 // Sum the split-K partials of block rows r0..r1 in slice order; the diagonal
