@@ -15,7 +15,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <memory>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -1009,7 +1011,10 @@ struct UploadAux {
   int device = -1;
   cudaStream_t s[5] = {};
   cudaEvent_t e[2 * gdwd_ctx::UP_MAXB + 3] = {};
+  double* pin = nullptr;  // page-locked staging ring for pageable sources (kept with the pooled object)
+  size_t pin_bytes = 0;
 };
+constexpr int UP_NSLOT = 3;  // staging slots (blocks in flight between the host copy and the DMA)
 static std::mutex g_aux_mu;
 static std::vector<UploadAux*> g_aux_free;
 static UploadAux* upload_aux_acquire(int device) {
@@ -1185,7 +1190,8 @@ static int select_kind(int64_t n, int64_t d);
 // G^{-1} = L^{-T} L^{-1}.  Only the last block's share runs after the last
 // byte has landed.  mu comes from the upload hint (default 1); a solve with
 // another mu, or outside the sample-space regimes, refactors from K.
-static int upload_dense_pipelined(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n, int64_t ld) {
+static int upload_dense_pipelined(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n, int64_t ld,
+                                  bool pinned) {
   const auto t_pre0 = std::chrono::steady_clock::now();
   if (!ctx->cst) {
     // streams and events come from a process-wide pool (contexts are created
@@ -1264,22 +1270,70 @@ static int upload_dense_pipelined(gdwd_ctx* ctx, const double* samples, int64_t 
     cudaEventRecord(tl0, ctx->cst);
   }
   const auto t_h0 = std::chrono::steady_clock::now();
-  // every copy is queued before any compute launch, so the copy engine never
-  // waits for the host
-  for (int b = 0; b < nblk; ++b) {
+  auto queue_copy = [&](int b, const double* src) -> int {
     const int64_t r0 = rb[b], r1 = rb[b + 1];
     if (ld == d)
-      CK(cudaMemcpyAsync(ctx->Zs + r0 * ld, samples + r0 * d, (size_t)(r1 - r0) * row_b, cudaMemcpyHostToDevice,
-                         ctx->cst));
+      CK(cudaMemcpyAsync(ctx->Zs + r0 * ld, src, (size_t)(r1 - r0) * row_b, cudaMemcpyHostToDevice, ctx->cst));
     else
-      CK(cudaMemcpy2DAsync(ctx->Zs + r0 * ld, ld * sizeof(double), samples + r0 * d, row_b, row_b, r1 - r0,
+      CK(cudaMemcpy2DAsync(ctx->Zs + r0 * ld, ld * sizeof(double), src, row_b, row_b, r1 - r0,
                            cudaMemcpyHostToDevice, ctx->cst));
     CK(cudaEventRecord(ctx->up_ev[b], ctx->cst));
     if (tmark) tev(0, b, ctx->cst);
+    return GDWD_OK;
+  };
+  // Pageable source: host threads copy block b into a page-locked ring
+  // (UP_NSLOT slots) while the DMA engine drains the blocks before it; the
+  // DMA of a block is queued as soon as every thread has delivered its share.
+  UploadAux* ax = (UploadAux*)ctx->up_aux;
+  const size_t slot_b = (size_t)mb * row_b;
+  std::vector<std::thread> workers;
+  std::atomic<int> allowed{UP_NSLOT};  // blocks [0, allowed) may be staged (their slot is free)
+  std::unique_ptr<std::atomic<int>[]> staged(new std::atomic<int>[gdwd_ctx::UP_MAXB]);
+  unsigned nthr = 1;
+  struct Joiner {  // error returns must not leave running threads behind
+    std::vector<std::thread>& w;
+    std::atomic<int>& allowed;
+    ~Joiner() {
+      allowed.store(1 << 30, std::memory_order_release);
+      for (auto& t : w)
+        if (t.joinable()) t.join();
+    }
+  } joiner{workers, allowed};
+  if (!pinned) {
+    if (ax->pin_bytes < UP_NSLOT * slot_b) {
+      if (ax->pin) cudaFreeHost(ax->pin);
+      ax->pin = nullptr;
+      ax->pin_bytes = 0;
+      CK(cudaMallocHost(&ax->pin, UP_NSLOT * slot_b));
+      ax->pin_bytes = UP_NSLOT * slot_b;
+    }
+    for (int b = 0; b < gdwd_ctx::UP_MAXB; ++b) staged[b].store(0, std::memory_order_relaxed);
+    nthr = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const char* src0 = (const char*)samples;
+    char* ring = (char*)ax->pin;
+    const int64_t* rbp = rb;
+    for (unsigned t = 0; t < nthr; ++t)
+      workers.emplace_back([=, &allowed, &staged] {
+        for (int b = 0; b < nblk; ++b) {
+          while (allowed.load(std::memory_order_acquire) <= b) std::this_thread::yield();
+          const size_t bytes = (size_t)(rbp[b + 1] - rbp[b]) * row_b;
+          const size_t lo = bytes * t / nthr / 64 * 64, hi = t + 1 == nthr ? bytes : bytes * (t + 1) / nthr / 64 * 64;
+          memcpy(ring + (size_t)(b % UP_NSLOT) * slot_b + lo, src0 + (size_t)rbp[b] * row_b + lo, hi - lo);
+          staged[b].fetch_add(1, std::memory_order_release);
+        }
+      });
+  } else {
+    // page-locked source: every copy is queued before any compute launch, so
+    // the copy engine never waits for the host
+    for (int b = 0; b < nblk; ++b) RC(queue_copy(b, samples + rb[b] * d));
   }
   const auto t_h1 = std::chrono::steady_clock::now();
   for (int b = 0; b < nblk; ++b) {
     const int64_t r0 = rb[b], r1 = rb[b + 1];
+    if (!pinned) {
+      while (staged[b].load(std::memory_order_acquire) < (int)nthr) std::this_thread::yield();
+      RC(queue_copy(b, ax->pin + (size_t)(b % UP_NSLOT) * (slot_b / sizeof(double))));
+    }
     CK(cudaStreamWaitEvent(ctx->gst, ctx->up_ev[b], 0));
     CK(gram_rowblock(ctx->Zs, ld, d, r0, r1, ctx->kmat.p, ldk, G, ldk, mu2, ctx->gram_ws.p, ctx->gst));
     if (tmark) tev(1, b, ctx->gst);
@@ -1290,6 +1344,10 @@ static int upload_dense_pipelined(gdwd_ctx* ctx, const double* samples, int64_t 
                             T + (size_t)n * ldk, bws));
       if (tmark) tev(2, b, ctx->fst);
       if (tmark) tev(3, b, ctx->ast);
+    }
+    if (!pinned && b + 1 >= UP_NSLOT) {  // block b + 1 reuses the slot of block b + 1 - UP_NSLOT
+      CK(cudaEventSynchronize(ctx->up_ev[b + 1 - UP_NSLOT]));
+      allowed.store(b + 2, std::memory_order_release);
     }
   }
   const auto t_h2 = std::chrono::steady_clock::now();
@@ -1374,8 +1432,9 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
   const bool pinned = cudaPointerGetAttributes(&pa, samples) == cudaSuccess && pa.type == cudaMemoryTypeHost;
   cudaGetLastError();
   finish_upload(ctx);
-  if (pinned && n <= 2500 && n <= d && d >= 64 && !sharded(ctx) && !getenv("GDWD_UPLOAD"))
-    return upload_dense_pipelined(ctx, samples, d, n, ld);
+  if (n <= 2500 && n <= d && d >= 64 && !sharded(ctx) && !getenv("GDWD_UPLOAD") &&
+      (pinned || (size_t)n * d >= ((size_t)1 << 20)))  // pageable: worth the staging threads from ~8 MB
+    return upload_dense_pipelined(ctx, samples, d, n, ld, pinned);
   RC(upload_rows(ctx, samples, d, n, ld));
   ctx->zs_gen++;
   ctx->n = n;
@@ -3517,6 +3576,7 @@ extern "C" int gdwd_chol_inverse_bordered(int32_t device, const double* Sm, int6
   CK(cudaMemcpy2D(A, ld * 8, Sm, m * 8, m * 8, m, cudaMemcpyHostToDevice));
   CK(cudaMemset(info, 0, sizeof(int)));
   CK(cudaMemset(W, 0, (size_t)3 * m * ld * 8));
+  CK(cudaStreamSynchronize(cudaStreamLegacy));  // the streams below are non-blocking: inputs must have landed
   cudaStream_t s3[3];
   for (auto& x : s3) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
   cudaError_t e = cudaSuccess;
