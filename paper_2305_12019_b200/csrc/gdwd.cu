@@ -65,7 +65,7 @@ static Api& api() {
   const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
   void* h = nullptr;
   for (const char* nm : names)
-    if (nm && (h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (nm && (h = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;  // local: a later `import torch` must bind its own NCCL
   if (!h) return a;
   a.GetUniqueId = (Result(*)(UniqueId*))dlsym(h, "ncclGetUniqueId");
   a.CommInitRank = (Result(*)(Comm*, int, UniqueId, int))dlsym(h, "ncclCommInitRank");
@@ -1405,6 +1405,73 @@ static int upload_dense_pipelined(gdwd_ctx* ctx, const double* samples, int64_t 
   return GDWD_OK;
 }
 
+// Pageable [n][d] source outside the sample-space regimes: the same staging
+// as upload_dense_pipelined without the factorisation -- host threads copy
+// blocks of rows into the pooled page-locked ring while the DMA engine
+// drains the blocks before them (a pageable cudaMemcpy2D runs at ~11 GB/s on
+// these hosts, the staged copy at the host threads' ~35 GB/s).
+static int upload_rows_staged(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n, int64_t ld) {
+  UploadAux* ax = upload_aux_acquire(ctx->device);
+  if (!ax) return set_err(ctx, GDWD_ERR_CUDA, "upload streams");
+  struct Release {
+    UploadAux* a;
+    ~Release() { upload_aux_release(a); }  // synchronises its streams
+  } rel{ax};
+  const size_t row_b = (size_t)d * sizeof(double);
+  const int64_t mb = std::max<int64_t>(1, (int64_t)(((size_t)16 << 20) / row_b));
+  const size_t slot_b = (size_t)mb * row_b;
+  const int nblk = (int)((n + mb - 1) / mb);
+  if (ax->pin_bytes < UP_NSLOT * slot_b) {
+    if (ax->pin) cudaFreeHost(ax->pin);
+    ax->pin = nullptr;
+    ax->pin_bytes = 0;
+    CK(cudaMallocHost(&ax->pin, UP_NSLOT * slot_b));
+    ax->pin_bytes = UP_NSLOT * slot_b;
+  }
+  cudaStream_t cst = ax->s[0];
+  CK(cudaStreamSynchronize(ctx->st));  // Zs is allocated (and its pad zeroed) on st
+  std::vector<std::thread> workers;
+  std::atomic<int> allowed{UP_NSLOT};
+  std::unique_ptr<std::atomic<int>[]> staged(new std::atomic<int>[nblk]);
+  for (int b = 0; b < nblk; ++b) staged[b].store(0, std::memory_order_relaxed);
+  struct Joiner {
+    std::vector<std::thread>& w;
+    std::atomic<int>& allowed;
+    ~Joiner() {
+      allowed.store(1 << 30, std::memory_order_release);
+      for (auto& t : w)
+        if (t.joinable()) t.join();
+    }
+  } joiner{workers, allowed};
+  const unsigned nthr = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const char* src0 = (const char*)samples;
+  char* ring = (char*)ax->pin;
+  for (unsigned t = 0; t < nthr; ++t)
+    workers.emplace_back([=, &allowed, &staged] {
+      for (int b = 0; b < nblk; ++b) {
+        while (allowed.load(std::memory_order_acquire) <= b) std::this_thread::yield();
+        const int64_t r0 = (int64_t)b * mb, r1 = std::min<int64_t>(n, r0 + mb);
+        const size_t bytes = (size_t)(r1 - r0) * row_b;
+        const size_t lo = bytes * t / nthr / 64 * 64, hi = t + 1 == nthr ? bytes : bytes * (t + 1) / nthr / 64 * 64;
+        memcpy(ring + (size_t)(b % UP_NSLOT) * slot_b + lo, src0 + (size_t)r0 * row_b + lo, hi - lo);
+        staged[b].fetch_add(1, std::memory_order_release);
+      }
+    });
+  for (int b = 0; b < nblk; ++b) {
+    const int64_t r0 = (int64_t)b * mb, r1 = std::min<int64_t>(n, r0 + mb);
+    while (staged[b].load(std::memory_order_acquire) < (int)nthr) std::this_thread::yield();
+    CK(cudaMemcpy2DAsync(ctx->Zs + r0 * ld, ld * sizeof(double), ring + (size_t)(b % UP_NSLOT) * slot_b, row_b, row_b,
+                         r1 - r0, cudaMemcpyHostToDevice, cst));
+    CK(cudaEventRecord(ax->e[b % UP_NSLOT], cst));
+    if (b + 1 >= UP_NSLOT) {  // block b + 1 reuses the slot of block b + 1 - UP_NSLOT
+      CK(cudaEventSynchronize(ax->e[(b + 1 - UP_NSLOT) % UP_NSLOT]));
+      allowed.store(b + 2, std::memory_order_release);
+    }
+  }
+  CK(cudaStreamSynchronize(cst));
+  return GDWD_OK;
+}
+
 int gdwd_upload_hint(gdwd_ctx* ctx, int32_t backend, double mu) {
   if (!ctx || !(mu > 0.0) || backend < GDWD_BACKEND_AUTO || backend > GDWD_BACKEND_ITERATIVE)
     return set_err(ctx, GDWD_ERR_VALUE, "bad upload hint");
@@ -1435,7 +1502,10 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
   if (n <= 2500 && n <= d && d >= 64 && !sharded(ctx) && !getenv("GDWD_UPLOAD") &&
       (pinned || (size_t)n * d >= ((size_t)1 << 20)))  // pageable: worth the staging threads from ~8 MB
     return upload_dense_pipelined(ctx, samples, d, n, ld, pinned);
-  RC(upload_rows(ctx, samples, d, n, ld));
+  if (!pinned && !getenv("GDWD_UPLOAD") && (size_t)n * d >= ((size_t)1 << 20))
+    RC(upload_rows_staged(ctx, samples, d, n, ld));
+  else
+    RC(upload_rows(ctx, samples, d, n, ld));
   ctx->zs_gen++;
   ctx->n = n;
   ctx->d = d;
@@ -1830,6 +1900,7 @@ int gdwd_scale_dense(gdwd_ctx* ctx, const double* y, double z_scale) {
 int gdwd_download_dense(gdwd_ctx* ctx, double* samples) {
   if (!ctx || !ctx->has_dense || !samples) return set_err(ctx, GDWD_ERR_VALUE, "no dense data");
   CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->st));
   CK(cudaMemcpy2D(samples, ctx->d * sizeof(double), ctx->Zs, ctx->ldz * sizeof(double), ctx->d * sizeof(double),
                   ctx->n, cudaMemcpyDeviceToHost));
   return GDWD_OK;
@@ -3260,7 +3331,8 @@ static int comm_finish_init(gdwd_ctx* ctx, int32_t nranks, int32_t rank, int64_t
   DevBuf tmp;
   CK(tmp.ensure(2));
   double hv[2] = {get_fro2(ctx), (double)ctx->n};
-  CK(cudaMemcpy(tmp.p, hv, sizeof(hv), cudaMemcpyHostToDevice));
+  // on st (non-blocking): a legacy-stream copy is not ordered before the all-reduce's reads
+  CK(cudaMemcpyAsync(tmp.p, hv, sizeof(hv), cudaMemcpyHostToDevice, ctx->st));
   allreduce(ctx, tmp.p, 2);
   CK(cudaMemcpyAsync(hv, tmp.p, sizeof(hv), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));

@@ -100,6 +100,10 @@ class NcclCommunicator:
     def __init__(self, nranks: int, rank: int, broadcast_id: Callable[[Optional[bytes]], bytes]):
         """``broadcast_id(id_or_None)``: rank 0 passes its id, every rank gets it back."""
         pin_nccl_determinism()
+        try:  # torch's bundled libnccl.so.2 first: the library's dlopen then binds the same one
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         lib = _lib.load()
         uid = None
         if rank == 0:
