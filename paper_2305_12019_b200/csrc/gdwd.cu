@@ -8,6 +8,7 @@
 // ITERATIVE body is host-driven because PSQMR's step count is data
 // dependent (one 4-byte flag read per PSQMR step).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges cost nothing unless a tool is attached
 #include <dlfcn.h>
 #include <math.h>
 #include <stdint.h>
@@ -213,6 +214,7 @@ struct gdwd_ctx {
   void* aux = nullptr;        // pooled stream / scalars / events (CtxAux)
   void* up_aux = nullptr;     // pooled streams / events (UploadAux)
   DevBuf pfw;                 // G | L^{-1} | scratch (n x ld each) of the bordered factorisation
+  int64_t dg_gen = -1;        // zs_gen whose d x d Gram Z~ Z~^T (in fac, DIRECT layout) was summed during the upload
   int64_t pf_gen = -1;        // zs_gen whose G^{-1} (fac) was formed during the upload ...
   double pf_mu2 = 0.0;        // ... for this mu^2
   double hint_mu = 1.0;       // mu the next upload's speculative factor is built for
@@ -362,6 +364,7 @@ struct Launch {  // counts launches; with profiling on, brackets the launch with
   const char* tag;
   cudaEvent_t a = nullptr;
   Launch(gdwd_ctx* c_, const char* t) : c(c_), tag(t) {
+    nvtxRangePushA(t);  // host-side launch range, named like the profile tags
     c->launches++;
     if (c->prof) {
       a = c->take_event();
@@ -379,7 +382,13 @@ struct Launch {  // counts launches; with profiling on, brackets the launch with
       cudaEventRecord(b, c->st);
       c->prof_pending.push_back({tag, a, b});
     }
+    nvtxRangePop();
   }
+};
+// NVTX range over a host-side phase (upload, setup, iteration loop, download)
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
 };
 
 static int sp_grid(int64_t work_threads, int cap) {
@@ -1192,6 +1201,7 @@ static int select_kind(int64_t n, int64_t d);
 // another mu, or outside the sample-space regimes, refactors from K.
 static int upload_dense_pipelined(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n, int64_t ld,
                                   bool pinned) {
+  Range nvtx_range("upload_dense_pipelined (copy + Gram + factor)");
   const auto t_pre0 = std::chrono::steady_clock::now();
   if (!ctx->cst) {
     // streams and events come from a process-wide pool (contexts are created
@@ -1410,7 +1420,13 @@ static int upload_dense_pipelined(gdwd_ctx* ctx, const double* samples, int64_t 
 // blocks of rows into the pooled page-locked ring while the DMA engine
 // drains the blocks before them (a pageable cudaMemcpy2D runs at ~11 GB/s on
 // these hosts, the staged copy at the host threads' ~35 GB/s).
-static int upload_rows_staged(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n, int64_t ld) {
+// `pinned`: the source is page-locked (no staging, block-wise DMA).  `dgram`:
+// the DIRECT regime's d x d Gram Z~ Z~^T (subsolvers.py:76) is summed block by
+// block on a second stream as the rows land (into fac, the (d+1) x (d+1)
+// layout build_factor completes), so only the last block's share is left
+// after the copy.
+static int upload_rows_staged(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n, int64_t ld, bool pinned,
+                              bool dgram) {
   UploadAux* ax = upload_aux_acquire(ctx->device);
   if (!ax) return set_err(ctx, GDWD_ERR_CUDA, "upload streams");
   struct Release {
@@ -1421,14 +1437,20 @@ static int upload_rows_staged(gdwd_ctx* ctx, const double* samples, int64_t d, i
   const int64_t mb = std::max<int64_t>(1, (int64_t)(((size_t)16 << 20) / row_b));
   const size_t slot_b = (size_t)mb * row_b;
   const int nblk = (int)((n + mb - 1) / mb);
-  if (ax->pin_bytes < UP_NSLOT * slot_b) {
+  if (!pinned && ax->pin_bytes < UP_NSLOT * slot_b) {
     if (ax->pin) cudaFreeHost(ax->pin);
     ax->pin = nullptr;
     ax->pin_bytes = 0;
     CK(cudaMallocHost(&ax->pin, UP_NSLOT * slot_b));
     ax->pin_bytes = UP_NSLOT * slot_b;
   }
-  cudaStream_t cst = ax->s[0];
+  cudaStream_t cst = ax->s[0], gst = ax->s[1];
+  const int64_t ldm = (d + 2) / 2 * 2;  // DIRECT: m = d + 1 rows of stride ((m + 1) / 2) * 2
+  if (dgram) {
+    CK(ctx->fac.ensure((size_t)(d + 1) * ldm));
+    CK(ctx->facw.ensure(std::max<size_t>((size_t)gram_workspace_doubles(d, mb), (size_t)2 * (d + 1) * ldm)));
+    CK(cudaMemsetAsync(ctx->fac.p, 0, (size_t)(d + 1) * ldm * sizeof(double), ctx->st));
+  }
   CK(cudaStreamSynchronize(ctx->st));  // Zs is allocated (and its pad zeroed) on st
   std::vector<std::thread> workers;
   std::atomic<int> allowed{UP_NSLOT};
@@ -1446,29 +1468,44 @@ static int upload_rows_staged(gdwd_ctx* ctx, const double* samples, int64_t d, i
   const unsigned nthr = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
   const char* src0 = (const char*)samples;
   char* ring = (char*)ax->pin;
-  for (unsigned t = 0; t < nthr; ++t)
-    workers.emplace_back([=, &allowed, &staged] {
-      for (int b = 0; b < nblk; ++b) {
-        while (allowed.load(std::memory_order_acquire) <= b) std::this_thread::yield();
-        const int64_t r0 = (int64_t)b * mb, r1 = std::min<int64_t>(n, r0 + mb);
-        const size_t bytes = (size_t)(r1 - r0) * row_b;
-        const size_t lo = bytes * t / nthr / 64 * 64, hi = t + 1 == nthr ? bytes : bytes * (t + 1) / nthr / 64 * 64;
-        memcpy(ring + (size_t)(b % UP_NSLOT) * slot_b + lo, src0 + (size_t)r0 * row_b + lo, hi - lo);
-        staged[b].fetch_add(1, std::memory_order_release);
-      }
-    });
+  if (!pinned)
+    for (unsigned t = 0; t < nthr; ++t)
+      workers.emplace_back([=, &allowed, &staged] {
+        for (int b = 0; b < nblk; ++b) {
+          while (allowed.load(std::memory_order_acquire) <= b) std::this_thread::yield();
+          const int64_t r0 = (int64_t)b * mb, r1 = std::min<int64_t>(n, r0 + mb);
+          const size_t bytes = (size_t)(r1 - r0) * row_b;
+          const size_t lo = bytes * t / nthr / 64 * 64, hi = t + 1 == nthr ? bytes : bytes * (t + 1) / nthr / 64 * 64;
+          memcpy(ring + (size_t)(b % UP_NSLOT) * slot_b + lo, src0 + (size_t)r0 * row_b + lo, hi - lo);
+          staged[b].fetch_add(1, std::memory_order_release);
+        }
+      });
   for (int b = 0; b < nblk; ++b) {
     const int64_t r0 = (int64_t)b * mb, r1 = std::min<int64_t>(n, r0 + mb);
-    while (staged[b].load(std::memory_order_acquire) < (int)nthr) std::this_thread::yield();
-    CK(cudaMemcpy2DAsync(ctx->Zs + r0 * ld, ld * sizeof(double), ring + (size_t)(b % UP_NSLOT) * slot_b, row_b, row_b,
-                         r1 - r0, cudaMemcpyHostToDevice, cst));
+    const char* from = src0 + (size_t)r0 * row_b;
+    if (!pinned) {
+      while (staged[b].load(std::memory_order_acquire) < (int)nthr) std::this_thread::yield();
+      from = ring + (size_t)(b % UP_NSLOT) * slot_b;
+    }
+    CK(cudaMemcpy2DAsync(ctx->Zs + r0 * ld, ld * sizeof(double), from, row_b, row_b, r1 - r0, cudaMemcpyHostToDevice,
+                         cst));
     CK(cudaEventRecord(ax->e[b % UP_NSLOT], cst));
-    if (b + 1 >= UP_NSLOT) {  // block b + 1 reuses the slot of block b + 1 - UP_NSLOT
+    if (dgram) {  // + Z~[:, block] Z~[:, block]^T, blocks in order (fixed summation order)
+      CK(cudaStreamWaitEvent(gst, ax->e[b % UP_NSLOT], 0));
+      CK(gram_syrk(ctx->Zs + r0 * ld, r1 - r0, d, ld, true, 1.0, 0.0, ctx->fac.p, ldm, ctx->facw.p, gst, b > 0));
+    }
+    if (!pinned && b + 1 >= UP_NSLOT) {  // block b + 1 reuses the slot of block b + 1 - UP_NSLOT
       CK(cudaEventSynchronize(ax->e[(b + 1 - UP_NSLOT) % UP_NSLOT]));
       allowed.store(b + 2, std::memory_order_release);
     }
   }
   CK(cudaStreamSynchronize(cst));
+  if (dgram) {
+    // the Gram's tail may still be running: later work on st waits for it
+    CK(cudaEventRecord(ax->e[UP_NSLOT], gst));
+    CK(cudaStreamWaitEvent(ctx->st, ax->e[UP_NSLOT], 0));
+    ctx->dg_gen = ctx->zs_gen + 1;  // the caller bumps zs_gen for this upload
+  }
   return GDWD_OK;
 }
 
@@ -1481,6 +1518,7 @@ int gdwd_upload_hint(gdwd_ctx* ctx, int32_t backend, double mu) {
 }
 
 int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n) {
+  Range nvtx_range("gdwd_upload_dense");
   if (!ctx || !samples || d < 1 || n < 1) return set_err(ctx, GDWD_ERR_VALUE, "bad dense upload arguments");
   CK(cudaSetDevice(ctx->device));
   free_sparse(ctx);
@@ -1502,8 +1540,12 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
   if (n <= 2500 && n <= d && d >= 64 && !sharded(ctx) && !getenv("GDWD_UPLOAD") &&
       (pinned || (size_t)n * d >= ((size_t)1 << 20)))  // pageable: worth the staging threads from ~8 MB
     return upload_dense_pipelined(ctx, samples, d, n, ld, pinned);
-  if (!pinned && !getenv("GDWD_UPLOAD") && (size_t)n * d >= ((size_t)1 << 20))
-    RC(upload_rows_staged(ctx, samples, d, n, ld));
+  // DIRECT's own regime (and not the sample-space form of it): sum the d x d Gram during the copy
+  const int hk = ctx->hint_backend == GDWD_BACKEND_AUTO ? select_kind(n, d) : ctx->hint_backend;
+  const bool dgram = hk == GDWD_BACKEND_DIRECT && 2 * n > d && d <= 8192 && n >= 4 * d && !sharded(ctx) &&
+                     getenv("GDWD_UPLOAD_FACTOR") == nullptr;
+  if (!getenv("GDWD_UPLOAD") && (size_t)n * d >= ((size_t)1 << 20) && (!pinned || dgram))
+    RC(upload_rows_staged(ctx, samples, d, n, ld, pinned, dgram));
   else
     RC(upload_rows(ctx, samples, d, n, ld));
   ctx->zs_gen++;
@@ -1519,6 +1561,7 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
 
 int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx, const double* values, int64_t d,
                     int64_t n) {
+  Range nvtx_range("gdwd_upload_csc");
   if (!ctx || !colptr || d < 1 || n < 1) return set_err(ctx, GDWD_ERR_VALUE, "bad CSC upload arguments");
   const int64_t nnz = colptr[n];
   if (colptr[0] != 0 || nnz < 0) return set_err(ctx, GDWD_ERR_VALUE, "colptr endpoints do not match stored entries");
@@ -2163,6 +2206,7 @@ struct SetupTimer {
 };
 
 static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
+  Range nvtx_range("build_factor");
   if (ctx->fac_gen == ctx->data_gen && ctx->fac_kind == kind && ctx->fac_mu2 == mu2 &&
       ctx->fac_iter_gram == (int)ctx->iter_gram)
     return GDWD_OK;
@@ -2178,7 +2222,9 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
     // G^{-1} already formed block by block during the upload (same data, same mu)
     const bool pf = kind == GDWD_BACKEND_SMW2 && ctx->pf_gen == ctx->zs_gen && ctx->pf_mu2 == mu2 &&
                     ctx->k_gen == ctx->zs_gen;
-    if (!pf) {
+    // DIRECT: Z~ Z~^T already summed block by block during the upload (in fac)
+    const bool dg = kind == GDWD_BACKEND_DIRECT && !sharded(ctx) && ctx->dg_gen == ctx->zs_gen;
+    if (!pf && !dg) {
       CK(ctx->fac.ensure((size_t)m * ld));
       CK(cudaMemsetAsync(ctx->fac.p, 0, (size_t)m * ld * sizeof(double), ctx->st));
     }
@@ -2192,9 +2238,12 @@ static int build_factor(gdwd_ctx* ctx, int kind, double mu2) {
         CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, true, 1.0, 0.0, ctx->fac.p, ld, ctx->facw.p, ctx->st));
         allreduce(ctx, ctx->fac.p, (int64_t)m * ld);
         add_diag_kernel<<<(unsigned)((d + 255) / 256), 256, 0, ctx->st>>>(ctx->fac.p, ld, d, mu2);
+      } else if (dg) {
+        add_diag_kernel<<<(unsigned)((d + 255) / 256), 256, 0, ctx->st>>>(ctx->fac.p, ld, d, mu2);
       } else {
         CK(gram_syrk(ctx->Zs, n, d, ctx->ldz, true, 1.0, mu2, ctx->fac.p, ld, ctx->facw.p, ctx->st));
       }
+      ctx->dg_gen = -1;  // fac is overwritten by the inverse below
       assemble_direct_kernel<<<(unsigned)((d + 256) / 256), 256, 0, ctx->st>>>(ctx->fac.p, ld, d, D.zy, ctx->yty);
     } else {
       // keep K = Z^T Z for the Gram-space iteration; G = K/mu^2 + I
@@ -2860,6 +2909,7 @@ static int pk_settle(gdwd_ctx* ctx) {
 }
 
 extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const double* sched, int64_t sched_len) {
+  Range nvtx_range("gdwd_solve_begin (setup)");
   if (!ctx || !cfg) return set_err(ctx, GDWD_ERR_VALUE, "null argument");
   if (!(ctx->has_dense || ctx->has_sparse) || !ctx->has_problem)
     return set_err(ctx, GDWD_ERR_VALUE, "no problem uploaded");
@@ -3109,6 +3159,7 @@ extern "C" int gdwd_solve_begin(gdwd_ctx* ctx, const gdwd_config* cfg, const dou
 // Run up to `count` more iterations (fewer if the stopping rule fires).
 extern "C" int gdwd_solve_iterate(gdwd_ctx* ctx, int32_t count, gdwd_iter_cb cb, void* user, int32_t* iters_done,
                                   int32_t* stopped_out) {
+  Range nvtx_range("gdwd_solve_iterate (loop)");
   if (!ctx || !ctx->in_solve) return set_err(ctx, GDWD_ERR_VALUE, "no solve in progress");
   CK(cudaSetDevice(ctx->device));
   RC(pk_settle(ctx));
@@ -3254,6 +3305,7 @@ static void ft_timing_report(gdwd_ctx* ctx) {
 }
 
 extern "C" int gdwd_solve_end(gdwd_ctx* ctx, gdwd_result* out) {
+  Range nvtx_range("gdwd_solve_end");
   if (!ctx || !ctx->in_solve || !out) return set_err(ctx, GDWD_ERR_VALUE, "no solve in progress");
   CK(cudaSetDevice(ctx->device));
   RC(pk_settle(ctx));
@@ -3457,6 +3509,7 @@ extern "C" int gdwd_time_iterations(gdwd_ctx* ctx, int32_t count, double* ms, in
 
 extern "C" int gdwd_get_state(gdwd_ctx* ctx, double* r, double* xi, double* alpha, double* w, double* u,
                               double* rho, double* ztw, double* beta) {
+  Range nvtx_range("gdwd_get_state (download)");
   if (!ctx || !ctx->nvec.p) return set_err(ctx, GDWD_ERR_VALUE, "no solve state");
   CK(cudaSetDevice(ctx->device));
   const Dev& D = ctx->D;
