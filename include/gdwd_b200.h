@@ -104,6 +104,14 @@ int gdwd_version(void);
  * Dense Z~: the CSC values array of a fully stored d x n matrix, i.e. the
  * row-major [n][d] sample matrix (SparseMatrixCSC, linalg/sparse.py:20-57). */
 int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n);
+/* gdwd_upload_dense overlaps the copy with the one-time factorisation where
+ * the regime allows (unsharded contexts): a pageable source is staged by host
+ * threads through a pooled page-locked ring while earlier blocks are in
+ * flight; in the sample-space regimes the Gram, its Cholesky factor and
+ * inverse advance block by block under the copy (see gdwd_upload_hint); in
+ * DIRECT's own regime (n >= 4d) the d x d Gram Z~ Z~^T (subsolvers.py:76) is
+ * summed block by block.  Results match the plain path to rounding (other
+ * summation order; deterministic run to run). */
 /* Optional, before gdwd_upload_dense: the backend (GDWD_BACKEND_*) and mu the
  * coming solve will use (SolverConfig, solver.py:101-124).  In the
  * sample-space regimes (n <= d, n <= 2500) a page-locked upload then forms
