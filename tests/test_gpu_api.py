@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import paper_2305_12019_b200 as G
-from conftest import load_traj, problem_for
+from conftest import load_traj, problem_for, relerr
 
 pytestmark = pytest.mark.gpu
 
@@ -237,3 +237,66 @@ def test_upload_time_gram_and_inverse(n, d, mu):
         assert have.value == 1
     finally:
         lib.gdwd_ctx_destroy(h)
+
+
+@pytest.mark.parametrize("d,n", [(1001, 9000), (300, 4001)])
+def test_staged_pageable_upload_round_trip(d, n, monkeypatch):
+    """A pageable [n][d] source of >= 8 MB outside the sample-space regimes is
+    staged by host threads through the page-locked ring, several blocks deep
+    (odd d: padded rows, 2-D copies): the device copy is the source, bit for
+    bit, the products match numpy and the norm equals the plain path's."""
+    rng = np.random.default_rng(d + n)
+    S = rng.standard_normal((n, d))
+    z = G.SparseMatrixCSC.from_dense_samples(S)
+    ones = np.ones(n)
+    dp = G.DeviceProblem(G.ProblemData(z, ones, ones, ones, 1.0, 1.0, 1.0))
+    try:
+        back = np.empty_like(S)
+        from paper_2305_12019_b200 import _lib
+
+        assert dp.lib.gdwd_download_dense(dp.ctx, _lib.ptr(back)) == 0
+        assert np.array_equal(back, S)
+        t, w = rng.standard_normal(n), rng.standard_normal(d)
+        assert relerr(dp.matvec(t), S.T @ t) < 1e-13
+        assert relerr(dp.rmatvec(w), S @ w) < 1e-13
+        eps = dp.eps_c()
+    finally:
+        dp.close()
+    monkeypatch.setenv("GDWD_UPLOAD", "pageable")  # the plain pageable copy
+    dp = G.DeviceProblem(G.ProblemData(z, ones, ones, ones, 1.0, 1.0, 1.0))
+    try:
+        assert dp.eps_c() == eps
+    finally:
+        dp.close()
+
+
+@pytest.mark.parametrize("pin", [False, True])
+def test_direct_gram_summed_during_upload(pin, monkeypatch):
+    """DIRECT's own regime (n >= 4 d): the d x d Gram Z~ Z~^T is summed block
+    by block while the rows are copied (page-locked: block-wise DMA; pageable:
+    staged).  The solve equals the one that forms the Gram afterwards."""
+    from paper_2305_12019_b200 import synth
+
+    prob = synth.make_variant_problem("c3", 300, 40000, seed=4)
+    z = prob.z_tilde
+    cfg = G.SolverConfig(q=prob.q, max_iter=20, backend=G.Backend.DIRECT)
+
+    def solve():
+        vals = z.values
+        if pin:
+            torch = pytest.importorskip("torch")
+            vals = torch.empty(z.values.size, dtype=torch.float64, pin_memory=True).numpy()
+            vals[:] = z.values
+        zp = G.SparseMatrixCSC.from_dense_samples(vals.reshape(z.ncols, z.nrows))
+        pp = G.ProblemData(zp, prob.y, prob.e, prob.weights, prob.C, prob.q, prob.z_scale)
+        out = G.sgs_admm_solve(pp, cfg)
+        G.solver.device_problem(pp).close()
+        return out
+
+    a = solve()
+    monkeypatch.setenv("GDWD_UPLOAD_FACTOR", "0")
+    b = solve()
+    assert a.iterations == b.iterations == 20 and a.double_count == b.double_count
+    assert a.setup_ms < b.setup_ms  # no Gram left in the setup
+    for key in ("w", "u", "rho", "r", "xi", "alpha"):
+        assert relerr(getattr(a.final_state, key), getattr(b.final_state, key)) < 1e-10, key
