@@ -18,7 +18,7 @@
 // across tiles instead of meeting at block barriers:
 //
 //   producer warp  issues a stage's copies once every consumer released it
-//   dot warps (4)  each owns a quarter of the slice's columns: reads a w pair
+//   dot warps (6)  each owns a sixth of the slice's columns: reads a w pair
 //                  once per tile and applies it to every row (double2 smem
 //                  reads, FMA chains), one shuffle tree per row; partials
 //                  published to every rank (DSMEM + remote arrive)
@@ -26,7 +26,7 @@
 //                  dots (fixed order), runs the per-sample epilogue (inputs
 //                  staged FT_PFD tiles ahead by cp.async), writes t (R
 //                  values per row) for the axpy
-//   axpy warps(10) own column pairs of the slice; accumulate x * t over rows
+//   axpy warps (8) own column pairs of the slice; accumulate x * t over rows
 //                  in registers (row order)
 //
 // Measured (B200, scratch harness): the pass streams at the HBM rate without
@@ -44,8 +44,15 @@
 namespace gdwd {
 
 constexpr int FT_THREADS = 512;
-constexpr int FT_NDW = 4;                 // dot warps 0..3
-constexpr int FT_AW0 = 4, FT_NAW = 10;    // axpy warps 4..13
+// 6 dot + 8 axpy warps: at d = 1000 (c3) eight axpy warps still hold two
+// column pairs per thread, and the dot warps -- the longer chain per tile --
+// each get 84 instead of 125 pairs: 388 -> 368 us per pass (4 + 10: 388,
+// 5 + 9: 410, 7 + 7: four-row tiles, slower)
+#ifndef FT_NDW_V
+#define FT_NDW_V 6
+#endif
+constexpr int FT_NDW = FT_NDW_V;                    // dot warps 0..NDW-1
+constexpr int FT_AW0 = FT_NDW, FT_NAW = 14 - FT_NDW;  // axpy warps NDW..13
 constexpr int FT_NA = FT_NAW * 32;        // axpy threads
 constexpr int FT_PW = 14, FT_SW = 15;     // producer warp, sample warp
 constexpr int FT_TRMAX = 8;               // rows per stage
