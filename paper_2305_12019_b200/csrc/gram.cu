@@ -10,10 +10,18 @@
 //                      one GEMV with the explicit inverse (solver kernels).
 //
 // tcgen05 has no f64 kind; the FP64 tensor path on sm_100a is the legacy
-// warp-level mma.sync m8n8k4 (SASS: DMMA.8x8x4).  Tiles: CTA 64x64, BK=16,
-// 8 warps as 2(m) x 4(n), each warp 32x16 = 4x2 DMMA tiles; register-staged
-// double buffering of the next K-slab; split-K over grid.z writes
-// deterministic per-slice partials that a fixed-order reduction sums.
+// warp-level mma.sync m8n8k4 (SASS: DMMA.8x8x4).  Two kernels:
+//   gram_tile_kernel  the Gram-shaped products (both operands with the same
+//                     fast axis): 64x128 CTA tile, 4 warps of 64x32, 16-byte
+//                     cp.async into a 3-stage ring, two CTAs per SM
+//   gemm_dmma_kernel  general strides and triangular-operand skips (the
+//                     Cholesky recursion and chain): CTA 64x64, BK=16, 8
+//                     warps as 2(m) x 4(n), each warp 32x16 = 4x2 DMMA tiles,
+//                     register-staged double buffering of the next K-slab
+// Split-K over grid.z writes deterministic per-slice partials that a
+// fixed-order reduction sums.  The row-block (bordered) forms at the end of
+// the file advance the Gram, the Cholesky factor and the inverse one block
+// of samples at a time, under the host-to-device copy (gdwd.cu).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
