@@ -336,6 +336,9 @@ struct OpCopy {  // dst = src
 struct OpZtNewton {
   static constexpr int NN = 1;
   static constexpr bool HAS_FIN = true;
+  // <= 85 registers (3 CTAs per SM instead of 2 at the 100 the Newton epilogue
+  // asks for): c3's pass 328 -> 268 us (6.0 TB/s); 4 CTAs (64 registers) the same
+  static constexpr int ZT_MINB = 3;
   Dev D;
   GDWD_DEV bool skip() const { return D.S->stopped; }
   GDWD_DEV double wval(int64_t j) const { return D.xb[j]; }

@@ -224,8 +224,24 @@ struct ZtGeom {
   int cw;  // chunk width (even)
 };
 
+// An Op with a heavy per-sample epilogue (the Newton prox) declares
+// ZT_MINB: the minimum CTAs per SM the kernel is compiled for, so that the
+// epilogue's registers (run once per CTA) do not cut the streaming loop's
+// occupancy -- the rows' loads in flight are what the pass lives on.
+#ifndef ZT_MINB_OVERRIDE
+#define ZT_MINB_OVERRIDE 0
+#endif
+template <class Op, class = void>
+struct ZtMinB {
+  static constexpr int v = 1;
+};
 template <class Op>
-__global__ void __launch_bounds__(ZT_THREADS) ztmv_kernel(Op op, MatView X, ZtGeom g, Scratch s) {
+struct ZtMinB<Op, decltype((void)Op::ZT_MINB)> {
+  static constexpr int v = ZT_MINB_OVERRIDE ? ZT_MINB_OVERRIDE : Op::ZT_MINB;
+};
+
+template <class Op>
+__global__ void __launch_bounds__(ZT_THREADS, ZtMinB<Op>::v) ztmv_kernel(Op op, MatView X, ZtGeom g, Scratch s) {
   constexpr int NN = Op::NN;
   if (op.skip()) return;
   extern __shared__ double zsm[];
