@@ -93,10 +93,10 @@ constexpr int FB_COLS = FB_COLS_V;
 constexpr int FB_PARTS = FB_PARTS_PER_SM * NUM_SMS;
 constexpr size_t FB_SMEM_MAX = 100 * 1024;
 #ifndef FB_H
-#define FB_H 2
+#define FB_H 1
 #endif
 #ifndef FB_U
-#define FB_U 8
+#define FB_U 4
 #endif
 
 // Device memory comes from the device's default stream-ordered pool, whose

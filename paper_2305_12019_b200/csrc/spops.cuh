@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(sb_threads<Op::R>()) sp_zmv_sb_kernel(Op op, S
 #pragma unroll
           for (int r = 0; r < R; ++r) acc[r] += v[u] * tsm[ix[u] * R + r];
       }
+      // (a predicated whole-batch tail instead of this loop measured slower: 80.6 vs 74.5 us at c4)
       for (; e < h; ++e) {
         const double v = __ldcs(A.val + base + 32 * (int64_t)e);
         const int ix = __ldcs(A.idx + base + 32 * (int64_t)e);
@@ -379,12 +380,20 @@ struct FbView {
   int nb, fb, parts, S, Q;
 };
 
+// 512 threads, two CTAs per SM (<= 64 registers), one slice per warp and
+// four of its rows in flight (FB_H = 1, FB_U = 4 in gdwd.cu): c4 77.8 us per
+// pass.  Measured alternatives: 256 threads with H = 2, U = 8 (round 1) 98.7;
+// 512 threads with H = 2, U = 8 / 4 91.2 / 80.4, H = 1, U = 8 / 2 82.8 / 81.6;
+// 448-1024 threads with H = 1, U = 4 76.3-80.8 (a plateau).
 #ifndef FB_THREADS_V
-#define FB_THREADS_V 256
+#define FB_THREADS_V 512
 #endif
-constexpr int FB_THREADS = FB_THREADS_V;  // two CTAs per SM (measured: one CTA of 512 over 24K-feature blocks: the same 99 us)
+constexpr int FB_THREADS = FB_THREADS_V;
 template <class Op, int H, int U>
-__global__ void __launch_bounds__(FB_THREADS) sp_ztmv_fb_kernel(Op op, FbView A, Scratch s) {
+#ifndef FB_MINB
+#define FB_MINB 2
+#endif
+__global__ void __launch_bounds__(FB_THREADS, FB_MINB) sp_ztmv_fb_kernel(Op op, FbView A, Scratch s) {
   constexpr int NN = Op::NN;
   if (op.skip()) return;
   extern __shared__ double fbsm[];
