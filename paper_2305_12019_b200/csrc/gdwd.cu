@@ -448,7 +448,7 @@ static void run_zmv(gdwd_ctx* ctx, const Op& op, MatView X, const char* tag = "z
             op, A, ctx->tbuf.p, ctx->sb_part.p);
       }
       Launch L(ctx, "sp_zmv_sb_reduce");
-      sp_zmv_sb_reduce_kernel<Op><<<(unsigned)((ctx->d + 31) / 32), SP_THREADS, 0, ctx->st>>>(op, ctx->sb_part.p,
+      sp_zmv_sb_reduce_kernel<Op><<<(unsigned)((ctx->d + 32 * SBR_F - 1) / (32 * SBR_F)), SP_THREADS, 0, ctx->st>>>(op, ctx->sb_part.p,
                                                                                           ctx->sb_nb, ctx->d, g1, sc);
     } else {
       Launch L(ctx, tag);

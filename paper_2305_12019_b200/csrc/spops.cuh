@@ -222,46 +222,63 @@ __global__ void __launch_bounds__(sb_threads<Op::R>()) sp_zmv_sb_kernel(Op op, S
 
 // v_j = sum of the per-block partials; per-feature epilogue, then the
 // finaliser (the prep kernel's n-partials and the d-partials) -- the tail of
-// sp_zmv_kernel.  A CTA covers 32 features: warp w sums blocks w, w + 8, ...
-// in order, then warp 0 adds the 8 warp sums in warp order (fixed tree).
+// sp_zmv_kernel.  Per feature: warp w sums blocks w, w + 8, ... in order,
+// then the 8 warp sums are added in warp order (fixed tree).
+// SBR_F features per lane (a CTA covers 32 SBR_F features): one wave of CTAs
+// at c4 (782 for d = 50000) instead of two waves of 1563 latency-bound ones.
+constexpr int SBR_F = 2;
 template <class Op>
 __global__ void __launch_bounds__(SP_THREADS) sp_zmv_sb_reduce_kernel(Op op, const double* part, int nb, int64_t d,
                                                                     int nprep, Scratch s) {
   constexpr int R = Op::R, NN = Op::NN, ND = Op::ND;
   constexpr int NW = SP_THREADS / 32;
   if (op.skip()) return;
-  __shared__ double pw[NW][R][32];
+  __shared__ double pw[NW][SBR_F][R][32];
   __shared__ double red2[NW * (NN > ND ? NN : ND)];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
-  double v[R];
+  const int64_t j0 = (int64_t)blockIdx.x * (32 * SBR_F) + lane;
+  double v[SBR_F][R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = 0.0;
-  if (j < d)
-#pragma unroll 4
-    for (int b = warp; b < nb; b += NW) {
+  for (int f = 0; f < SBR_F; ++f)
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[r] += __ldcg(part + ((int64_t)b * d + j) * R + r);
+    for (int r = 0; r < R; ++r) v[f][r] = 0.0;
+#pragma unroll 2
+  for (int b = warp; b < nb; b += NW) {
+#pragma unroll
+    for (int f = 0; f < SBR_F; ++f) {
+      const int64_t j = j0 + 32 * f;
+      if (j < d) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[f][r] += __ldcg(part + ((int64_t)b * d + j) * R + r);
+      }
     }
+  }
 #pragma unroll
-  for (int r = 0; r < R; ++r) pw[warp][r][lane] = v[r];
+  for (int f = 0; f < SBR_F; ++f)
+#pragma unroll
+    for (int r = 0; r < R; ++r) pw[warp][f][r][lane] = v[f][r];
   __syncthreads();
   double dacc[ND];
 #pragma unroll
   for (int k = 0; k < ND; ++k) dacc[k] = 0.0;
-  if (warp == 0 && j < d) {
+  if (warp < SBR_F) {  // warp f finishes the CTA's f-th group of 32 features
+    const int f = warp;
+    const int64_t j = j0 + 32 * f;
+    if (j < d) {
+      double vv[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      double a = 0.0;
+      for (int r = 0; r < R; ++r) {
+        double a = 0.0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) a += pw[w][r][lane];
-      v[r] = a;
-    }
-    if (s.bundle) {
+        for (int w = 0; w < NW; ++w) a += pw[w][f][r][lane];
+        vv[r] = a;
+      }
+      if (s.bundle) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) s.bundle[(int64_t)r * d + j] = v[r];
-    } else {
-      op.epi(j, v, dacc);
+        for (int r = 0; r < R; ++r) s.bundle[(int64_t)r * d + j] = vv[r];
+      } else {
+        op.epi(j, vv, dacc);
+      }
     }
   }
   block_sum<ND>(dacc, red2);
