@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(SP_THREADS) sp_zmv_kernel(Op op, SpView A, con
 constexpr int SB_S = 12288;       // samples per block
 constexpr int SB_THREADS = 512;
 constexpr int SB_CHUNKS = 2 * 148;  // chunk boundaries: 2 per SM (R = 1), pairs for R = 2
-constexpr int SB_U = 8;           // entries per lane in flight
+#ifndef SB_U_V
+#define SB_U_V 8
+#endif
+constexpr int SB_U = SB_U_V;      // entries per lane in flight
 
 struct SbView {
   const double* val;
