@@ -118,7 +118,8 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
  * the n x n Gram (subsolvers.py:109), its Cholesky factor and explicit
  * inverse (cholesky.py:46,60-61) block by block while the samples are still
  * being copied; a solve with another mu refactors from the Gram.  Default:
- * AUTO, mu = 1.  GDWD_BACKEND_ITERATIVE: Gram only. */
+ * AUTO, mu = 1.  GDWD_BACKEND_ITERATIVE (also passed for the shards of a
+ * multi-GPU solve): plain copy, nothing is formed during the upload. */
 int gdwd_upload_hint(gdwd_ctx* ctx, int32_t backend, double mu);
 /* Sparse Z~ in the reference's CSC layout (int64 colptr/rowidx). */
 int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx, const double* values,

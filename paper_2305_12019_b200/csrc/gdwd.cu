@@ -1537,11 +1537,13 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
   const bool pinned = cudaPointerGetAttributes(&pa, samples) == cudaSuccess && pa.type == cudaMemoryTypeHost;
   cudaGetLastError();
   finish_upload(ctx);
-  if (n <= 2500 && n <= d && d >= 64 && !sharded(ctx) && !getenv("GDWD_UPLOAD") &&
+  const int hk = ctx->hint_backend == GDWD_BACKEND_AUTO ? select_kind(n, d) : ctx->hint_backend;
+  // (an ITERATIVE hint -- also what a shard of a multi-GPU solve passes -- means
+  // no Gram is needed at all: plain copy)
+  if (n <= 2500 && n <= d && d >= 64 && !sharded(ctx) && !getenv("GDWD_UPLOAD") && hk != GDWD_BACKEND_ITERATIVE &&
       (pinned || (size_t)n * d >= ((size_t)1 << 20)))  // pageable: worth the staging threads from ~8 MB
     return upload_dense_pipelined(ctx, samples, d, n, ld, pinned);
   // DIRECT's own regime (and not the sample-space form of it): sum the d x d Gram during the copy
-  const int hk = ctx->hint_backend == GDWD_BACKEND_AUTO ? select_kind(n, d) : ctx->hint_backend;
   const bool dgram = hk == GDWD_BACKEND_DIRECT && 2 * n > d && d <= 8192 && n >= 4 * d && !sharded(ctx) &&
                      getenv("GDWD_UPLOAD_FACTOR") == nullptr;
   if (!getenv("GDWD_UPLOAD") && (size_t)n * d >= ((size_t)1 << 20) && (!pinned || dgram))

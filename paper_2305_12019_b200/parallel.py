@@ -136,7 +136,9 @@ class NcclCommunicator:
 def attach(local: ProblemData, comm, n_global: int, device: Optional[int] = None) -> DeviceProblem:
     """Upload the local shard (if not yet resident) and join the communicator;
     later ``sgs_admm_solve(local, ...)`` calls run sharded."""
-    dp = device_problem(local, device)
+    # hint ITERATIVE: a shard needs nothing factored during its upload (the
+    # Grams a sharded solve uses are summed over the shards at setup)
+    dp = device_problem(local, device, (_lib.BACKEND_CODE["iterative"], 1.0))
     comm.attach(dp, n_global)
     return dp
 

@@ -230,11 +230,14 @@ def test_upload_time_gram_and_inverse(n, d, mu):
         fro2 = C.c_double()
         assert lib.gdwd_frobenius_sq(h, C.byref(fro2)) == 0
         assert abs(fro2.value - (X * X).sum()) <= 1e-12 * (X * X).sum()
-        # an ITERATIVE hint: the Gram only
+        # an ITERATIVE hint (also what the shards of a multi-GPU solve pass): plain copy
         assert lib.gdwd_upload_hint(h, _lib.BACKEND_CODE["iterative"], mu) == 0
         assert lib.gdwd_upload_dense(h, _lib.ptr(buf), d, n) == 0
         assert lib.gdwd_get_upload_factor(h, None, None, C.byref(have)) == 0
-        assert have.value == 1
+        assert have.value == 0
+        back = np.empty_like(X)
+        assert lib.gdwd_download_dense(h, _lib.ptr(back)) == 0
+        assert np.array_equal(back, X)
     finally:
         lib.gdwd_ctx_destroy(h)
 
