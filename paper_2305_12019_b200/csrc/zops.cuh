@@ -55,8 +55,13 @@ struct op_sq : std::false_type {};
 template <class Op>
 struct op_sq<Op, std::void_t<decltype(Op::SQ)>> : std::integral_constant<bool, Op::SQ> {};
 
+// (forcing >= 5 CTAs per SM spills the 8-row load batch: c3's Z~ [dr, z~tw] pass
+// 291 -> 337 us; the kernel's natural 64 registers, 4 CTAs per SM, stand)
+#ifndef ZMV_MINB
+#define ZMV_MINB 1
+#endif
 template <class Op>
-__global__ void __launch_bounds__(ZMV_THREADS) zmv_kernel(Op op, MatView X, ZmvGeom g, Scratch s) {
+__global__ void __launch_bounds__(ZMV_THREADS, ZMV_MINB) zmv_kernel(Op op, MatView X, ZmvGeom g, Scratch s) {
   constexpr int R = Op::R, NN = Op::NN, ND = Op::ND;
   if (op.skip()) return;
   __shared__ double ts[R][ZMV_STAGE];
