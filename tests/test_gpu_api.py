@@ -197,8 +197,9 @@ def test_reference_problem_data_is_accepted_as_is():
         assert np.isfinite(kk.eta_p)
 
 
+@pytest.mark.parametrize("pin", [True, False])
 @pytest.mark.parametrize("n,d,mu", [(200, 6000, 1.0), (16, 90, 1.0), (700, 3001, 2.0), (333, 777, 0.7), (1000, 2000, 1.0)])
-def test_upload_time_gram_and_inverse(n, d, mu):
+def test_upload_time_gram_and_inverse(n, d, mu, pin):
     """A page-locked upload in the sample-space regimes forms K = Z~^T Z~
     (subsolvers.py:109) and G^{-1} = (K/mu^2 + I)^{-1} (cholesky.py:46,60-61)
     block by block while the samples are copied (gdwd_upload_hint +
@@ -211,7 +212,8 @@ def test_upload_time_gram_and_inverse(n, d, mu):
     lib = _lib.load()
     rng = np.random.default_rng(n)
     X = rng.standard_normal((n, d)) * (3.0 / np.sqrt(d))
-    buf = torch.empty(n * d, dtype=torch.float64, pin_memory=True).numpy()
+    # page-locked source: block-wise DMA; pageable (from 8 MB): staged by host threads
+    buf = torch.empty(n * d, dtype=torch.float64, pin_memory=True).numpy() if pin else np.empty(n * d)
     buf[:] = X.ravel()
     h = C.c_void_p()
     assert lib.gdwd_ctx_create(0, C.byref(h)) == 0
@@ -220,6 +222,9 @@ def test_upload_time_gram_and_inverse(n, d, mu):
         assert lib.gdwd_upload_dense(h, _lib.ptr(buf), d, n) == 0
         K, Gi, have = np.empty((n, n)), np.empty((n, n)), C.c_int32()
         assert lib.gdwd_get_upload_factor(h, _lib.ptr(K), _lib.ptr(Gi), C.byref(have)) == 0
+        if not pin and n * d < (1 << 20):
+            assert have.value == 0  # small pageable sources take the plain copy
+            return
         assert have.value == 3
         Kr = X @ X.T
         assert np.abs(K - Kr).max() <= 1e-13 * np.abs(Kr).max()
