@@ -1024,6 +1024,7 @@ struct UploadAux {
   size_t pin_bytes = 0;
 };
 constexpr int UP_NSLOT = 3;  // staging slots (blocks in flight between the host copy and the DMA)
+constexpr int UP_NO_STAGING = -1;  // internal: the page-locked ring could not be allocated
 static std::mutex g_aux_mu;
 static std::vector<UploadAux*> g_aux_free;
 static UploadAux* upload_aux_acquire(int device) {
@@ -1314,7 +1315,11 @@ static int upload_dense_pipelined(gdwd_ctx* ctx, const double* samples, int64_t 
       if (ax->pin) cudaFreeHost(ax->pin);
       ax->pin = nullptr;
       ax->pin_bytes = 0;
-      CK(cudaMallocHost(&ax->pin, UP_NSLOT * slot_b));
+      if (cudaMallocHost(&ax->pin, UP_NSLOT * slot_b) != cudaSuccess) {
+        cudaGetLastError();
+        ax->pin = nullptr;
+        return UP_NO_STAGING;  // nothing queued yet: the caller takes the plain copy
+      }
       ax->pin_bytes = UP_NSLOT * slot_b;
     }
     for (int b = 0; b < gdwd_ctx::UP_MAXB; ++b) staged[b].store(0, std::memory_order_relaxed);
@@ -1441,7 +1446,11 @@ static int upload_rows_staged(gdwd_ctx* ctx, const double* samples, int64_t d, i
     if (ax->pin) cudaFreeHost(ax->pin);
     ax->pin = nullptr;
     ax->pin_bytes = 0;
-    CK(cudaMallocHost(&ax->pin, UP_NSLOT * slot_b));
+    if (cudaMallocHost(&ax->pin, UP_NSLOT * slot_b) != cudaSuccess) {
+      cudaGetLastError();
+      ax->pin = nullptr;
+      return UP_NO_STAGING;  // no page-locked memory to be had: the caller takes the plain copy
+    }
     ax->pin_bytes = UP_NSLOT * slot_b;
   }
   cudaStream_t cst = ax->s[0], gst = ax->s[1];
@@ -1541,15 +1550,18 @@ int gdwd_upload_dense(gdwd_ctx* ctx, const double* samples, int64_t d, int64_t n
   // (an ITERATIVE hint -- also what a shard of a multi-GPU solve passes -- means
   // no Gram is needed at all: plain copy)
   if (n <= 2500 && n <= d && d >= 64 && !sharded(ctx) && !getenv("GDWD_UPLOAD") && hk != GDWD_BACKEND_ITERATIVE &&
-      (pinned || (size_t)n * d >= ((size_t)1 << 20)))  // pageable: worth the staging threads from ~8 MB
-    return upload_dense_pipelined(ctx, samples, d, n, ld, pinned);
+      (pinned || (size_t)n * d >= ((size_t)1 << 20))) {  // pageable: worth the staging threads from ~8 MB
+    const int rc = upload_dense_pipelined(ctx, samples, d, n, ld, pinned);
+    if (rc != UP_NO_STAGING) return rc;
+  }
   // DIRECT's own regime (and not the sample-space form of it): sum the d x d Gram during the copy
   const bool dgram = hk == GDWD_BACKEND_DIRECT && 2 * n > d && d <= 8192 && n >= 4 * d && !sharded(ctx) &&
                      getenv("GDWD_UPLOAD_FACTOR") == nullptr;
+  int rc = UP_NO_STAGING;
   if (!getenv("GDWD_UPLOAD") && (size_t)n * d >= ((size_t)1 << 20) && (!pinned || dgram))
-    RC(upload_rows_staged(ctx, samples, d, n, ld, pinned, dgram));
-  else
-    RC(upload_rows(ctx, samples, d, n, ld));
+    rc = upload_rows_staged(ctx, samples, d, n, ld, pinned, dgram);
+  if (rc == UP_NO_STAGING) rc = upload_rows(ctx, samples, d, n, ld);
+  RC(rc);
   ctx->zs_gen++;
   ctx->n = n;
   ctx->d = d;
