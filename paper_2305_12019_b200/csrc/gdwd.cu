@@ -1060,6 +1060,21 @@ static void upload_aux_release(UploadAux* a) {
   g_aux_free.push_back(a);
 }
 
+// Host scratch array without the single-threaded zero fill of std::vector:
+// the worker threads' first touch places (and faults in) the pages in
+// parallel.  Every element is written before it is read.
+template <class T>
+struct RawBuf {
+  std::unique_ptr<T[]> p;
+  size_t n = 0;
+  explicit RawBuf(size_t cnt) : p(new T[std::max<size_t>(cnt, 1)]), n(cnt) {}
+  T* data() { return p.get(); }
+  const T* data() const { return p.get(); }
+  T& operator[](size_t i) { return p[i]; }
+  const T& operator[](size_t i) const { return p[i]; }
+  size_t size() const { return n; }
+};
+
 // Per-context device/host scalars, streams and events, pooled per device:
 // contexts are created inside timed end-to-end calls, and cudaMalloc /
 // cudaMallocHost / stream and event creation cost ~0.4 ms per context.
@@ -1518,6 +1533,76 @@ static int upload_rows_staged(gdwd_ctx* ctx, const double* samples, int64_t d, i
   return GDWD_OK;
 }
 
+// Large pageable host array -> device through the pooled page-locked ring
+// (host threads fill a slot while the DMA engine drains the ones before it);
+// small ones by the plain synchronous copy.  Returns when the data has landed.
+static int h2d_staged(gdwd_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  const size_t slot_b = (size_t)16 << 20;
+  UploadAux* ax = bytes >= 2 * slot_b && !getenv("GDWD_UPLOAD") ? upload_aux_acquire(ctx->device) : nullptr;
+  if (ax && ax->pin_bytes < UP_NSLOT * slot_b) {
+    if (ax->pin) cudaFreeHost(ax->pin);
+    ax->pin = nullptr;
+    ax->pin_bytes = 0;
+    if (cudaMallocHost(&ax->pin, UP_NSLOT * slot_b) == cudaSuccess) {
+      ax->pin_bytes = UP_NSLOT * slot_b;
+    } else {
+      cudaGetLastError();
+      ax->pin = nullptr;
+      upload_aux_release(ax);
+      ax = nullptr;
+    }
+  }
+  if (!ax) {
+    CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    CK(cudaStreamSynchronize(cudaStreamLegacy));  // staged by the driver: let it land
+    return GDWD_OK;
+  }
+  struct Release {
+    UploadAux* a;
+    ~Release() { upload_aux_release(a); }
+  } rel{ax};
+  const int nblk = (int)((bytes + slot_b - 1) / slot_b);
+  cudaStream_t cst = ax->s[0];
+  std::vector<std::thread> workers;
+  std::atomic<int> allowed{UP_NSLOT};
+  std::unique_ptr<std::atomic<int>[]> staged(new std::atomic<int>[nblk]);
+  for (int b = 0; b < nblk; ++b) staged[b].store(0, std::memory_order_relaxed);
+  struct Joiner {
+    std::vector<std::thread>& w;
+    std::atomic<int>& allowed;
+    ~Joiner() {
+      allowed.store(1 << 30, std::memory_order_release);
+      for (auto& t : w)
+        if (t.joinable()) t.join();
+    }
+  } joiner{workers, allowed};
+  const unsigned nthr = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const char* src0 = (const char*)src;
+  char* ring = (char*)ax->pin;
+  for (unsigned t = 0; t < nthr; ++t)
+    workers.emplace_back([=, &allowed, &staged] {
+      for (int b = 0; b < nblk; ++b) {
+        while (allowed.load(std::memory_order_acquire) <= b) std::this_thread::yield();
+        const size_t off = (size_t)b * slot_b, len = std::min(slot_b, bytes - off);
+        const size_t lo = len * t / nthr / 64 * 64, hi = t + 1 == nthr ? len : len * (t + 1) / nthr / 64 * 64;
+        memcpy(ring + (size_t)(b % UP_NSLOT) * slot_b + lo, src0 + off + lo, hi - lo);
+        staged[b].fetch_add(1, std::memory_order_release);
+      }
+    });
+  for (int b = 0; b < nblk; ++b) {
+    const size_t off = (size_t)b * slot_b, len = std::min(slot_b, bytes - off);
+    while (staged[b].load(std::memory_order_acquire) < (int)nthr) std::this_thread::yield();
+    CK(cudaMemcpyAsync((char*)dst + off, ring + (size_t)(b % UP_NSLOT) * slot_b, len, cudaMemcpyHostToDevice, cst));
+    CK(cudaEventRecord(ax->e[b % UP_NSLOT], cst));
+    if (b + 1 >= UP_NSLOT) {
+      CK(cudaEventSynchronize(ax->e[(b + 1 - UP_NSLOT) % UP_NSLOT]));
+      allowed.store(b + 2, std::memory_order_release);
+    }
+  }
+  CK(cudaStreamSynchronize(cst));
+  return GDWD_OK;
+}
+
 int gdwd_upload_hint(gdwd_ctx* ctx, int32_t backend, double mu) {
   if (!ctx || !(mu > 0.0) || backend < GDWD_BACKEND_AUTO || backend > GDWD_BACKEND_ITERATIVE)
     return set_err(ctx, GDWD_ERR_VALUE, "bad upload hint");
@@ -1611,7 +1696,7 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
   });
   const int64_t first_ptr = *std::min_element(bad_ptr.begin(), bad_ptr.end());
   std::vector<std::vector<int64_t>> hist(T);
-  std::vector<int> ci32((size_t)nnz);
+  RawBuf<int> ci32((size_t)nnz);
   par([&](int t, int64_t i0, int64_t i1) {
     hist[t].assign(d, 0);
     int64_t* h = hist[t].data();
@@ -1639,8 +1724,8 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
     }
     rp[j + 1] = o;
   }
-  std::vector<int> cidx((size_t)nnz);
-  std::vector<double> cval((size_t)nnz);
+  RawBuf<int> cidx((size_t)nnz);
+  RawBuf<double> cval((size_t)nnz);
   par([&](int t, int64_t i0, int64_t i1) {
     int64_t* fillp = hist[t].data();
     for (int64_t i = i0; i < i1; ++i)
@@ -1667,10 +1752,10 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
   CK(cudaMemcpy(ctx->csc_ptr, colptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->csr_ptr, rp.data(), (d + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
   if (nnz > 0) {
-    CK(cudaMemcpy(ctx->csc_idx, ci32.data(), nnz * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->csr_idx, cidx.data(), nnz * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->csc_val, values, nnz * sizeof(double), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->csr_val, cval.data(), nnz * sizeof(double), cudaMemcpyHostToDevice));
+    RC(h2d_staged(ctx, ctx->csc_idx, ci32.data(), nnz * sizeof(int)));
+    RC(h2d_staged(ctx, ctx->csr_idx, cidx.data(), nnz * sizeof(int)));
+    RC(h2d_staged(ctx, ctx->csc_val, values, nnz * sizeof(double)));
+    RC(h2d_staged(ctx, ctx->csr_val, cval.data(), nnz * sizeof(double)));
   }
   // feature-blocked CSC: parts of S samples (one CTA each, 2 per SM) x
   // feature blocks of FB_COLS; within (part, block) the samples in order,
@@ -1827,8 +1912,13 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
     for (int64_t sl = 0; sl < nsl; ++sl) bb[sl + 1] = bb[sl] + 32 * (int64_t)hh[sl];
     const int64_t ne = bb[nsl];
     if (ne < ((int64_t)1 << 31)) {
-      std::vector<double> sv((size_t)std::max<int64_t>(ne, 1), 0.0);
-      std::vector<unsigned short> si((size_t)std::max<int64_t>(ne, 1), 0);
+      RawBuf<double> sv((size_t)std::max<int64_t>(ne, 1));
+      RawBuf<unsigned short> si((size_t)std::max<int64_t>(ne, 1));
+      par([&](int t, int64_t, int64_t) {  // pad entries must read as zero: cleared in parallel
+        const size_t tot = sv.size(), lo = tot * t / T, hi = tot * (t + 1) / T;
+        memset(sv.data() + lo, 0, (hi - lo) * sizeof(double));
+        memset(si.data() + lo, 0, (hi - lo) * sizeof(unsigned short));
+      });
       par([&](int t, int64_t, int64_t) {
         for (int64_t sl = nsl * t / T; sl < nsl * (t + 1) / T; ++sl) {
           const int b = (int)(sl / nslpb);
@@ -1863,8 +1953,8 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
       CK(dmalloc((void**)&ctx->sb_h, hh.size() * sizeof(int), ctx->st));
       CK(dmalloc((void**)&ctx->sb_perm, pp.size() * sizeof(int), ctx->st));
       CK(dmalloc((void**)&ctx->sb_chunk, ch.size() * sizeof(int), ctx->st));
-      CK(cudaMemcpy(ctx->sb_val, sv.data(), sv.size() * sizeof(double), cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(ctx->sb_idx, si.data(), si.size() * sizeof(unsigned short), cudaMemcpyHostToDevice));
+      RC(h2d_staged(ctx, ctx->sb_val, sv.data(), sv.size() * sizeof(double)));
+      RC(h2d_staged(ctx, ctx->sb_idx, si.data(), si.size() * sizeof(unsigned short)));
       CK(cudaMemcpy(ctx->sb_base, bb.data(), bb.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(ctx->sb_h, hh.data(), hh.size() * sizeof(int), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(ctx->sb_perm, pp.data(), pp.size() * sizeof(int), cudaMemcpyHostToDevice));
