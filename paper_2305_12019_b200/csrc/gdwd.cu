@@ -1849,12 +1849,23 @@ int gdwd_upload_csc(gdwd_ctx* ctx, const int64_t* colptr, const int64_t* rowidx,
       CK(cudaMemcpy(ctx->fb_ptr, sbase.data(), sbase.size() * sizeof(int), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(ctx->fb_perm, perm.data(), perm.size() * sizeof(unsigned short), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(ctx->fb_cnt, cnt.data(), cnt.size() * sizeof(unsigned short), cudaMemcpyHostToDevice));
-      for (int p = 0; p < parts; ++p)
-        if (!pval[p].empty()) {
-          CK(cudaMemcpy(ctx->fb_idx + poff[p], pidx[p].data(), pidx[p].size() * sizeof(unsigned short),
-                        cudaMemcpyHostToDevice));
-          CK(cudaMemcpy(ctx->fb_val + poff[p], pval[p].data(), pval[p].size() * sizeof(double), cudaMemcpyHostToDevice));
+      {
+        // the parts' arrays gathered by all threads, then one staged copy each
+        // (592 separate pageable copies ran at ~11 GB/s)
+        RawBuf<double> allv(ne);
+        RawBuf<unsigned short> alli(ne);
+        par([&](int t, int64_t, int64_t) {
+          for (int p = t; p < parts; p += T)
+            if (!pval[p].empty()) {
+              memcpy(allv.data() + poff[p], pval[p].data(), pval[p].size() * sizeof(double));
+              memcpy(alli.data() + poff[p], pidx[p].data(), pidx[p].size() * sizeof(unsigned short));
+            }
+        });
+        if (poff[parts] > 0) {
+          RC(h2d_staged(ctx, ctx->fb_val, allv.data(), poff[parts] * sizeof(double)));
+          RC(h2d_staged(ctx, ctx->fb_idx, alli.data(), poff[parts] * sizeof(unsigned short)));
         }
+      }
       ctx->fb_nb = nb;
       ctx->fb_parts = parts;
       ctx->fb_S = S;
