@@ -733,7 +733,8 @@ def main():
     ap.add_argument("--kkt-iters", type=int, default=-1,
                     help="iterations of the time-to-KKT solve (default: the reference's max_iter, 2000, for the "
                          "Gram-space configs c1/c2; 100 elsewhere)")
-    ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--cpu-steps", type=int, default=24,
+                    help="iterations of the CPU oracle leg (c2: ~0.5 s each on 16 cores, i.e. ~12 s)")
     ap.add_argument("--x-space", action="store_true", help="SMW2 iterations as passes over X (no Gram-space)")
     ap.add_argument("--no-persistent", action="store_true", help="Gram-space SMW2 as a CUDA graph of kernels")
     ap.add_argument("--devices", default=None, help="single-process N > 1: device ids (default 0..N-1)")
